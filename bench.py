@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py — FDiRW step throughput on B200 (BASELINE.json metric: voxel-updates/s and
+HBM GB/s fraction of the FDiRW step at 192³ on 1/2/4/8 GPUs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl fdirw|reference]
+  N>1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step = one FDiRW macro step (a5 superposition + a6 halo exchange when N>1) over the
+whole grid, with the kernels built once beforehand by fdirw_build_kernels (a1-a4,
+"preconditioned" P; timed separately under "kgen").  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import fdirw_inputs as fi  # noqa: E402
+
+METRIC = "voxel-updates/s (FDiRW step)"
+UNIT = "voxel-updates/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def _hbm_peak():
+    p = _peaks()
+    if p and p.get("hbm_gbs"):
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg: fi.Config, mask: np.ndarray, steps: int = 20):
+    """The CPU fp64 oracle as it stands, on a bounded sample of the same workload: kernels of
+    the sources in a 12×12×8 box at the particle surface (oracle kgen, OpenMP over all host
+    cores), then `steps` oracle superposition steps over that box (scatter, 1 thread),
+    counting one voxel-update per source/target of the box."""
+    import oracle
+
+    oracle.build()
+    pb = oracle.Problem(mask=mask, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt, R=cfg.R,
+                        n_fd=cfg.n_fd)
+    nz, ny, nx = mask.shape
+    cx, cy, cz = nx // 2, ny // 2, nz // 2
+    x0 = min(nx - 12, cx + int(0.45 * nx) // 2 if nx >= 64 else 0)
+    box = (max(0, x0), max(0, x0) + min(12, nx), max(0, cy - 6), max(0, cy - 6) + min(12, ny),
+           max(0, cz - 4), max(0, cz - 4) + min(8, nz))
+    n_src = (box[1] - box[0]) * (box[3] - box[2]) * (box[5] - box[4])
+    t = time.perf_counter()
+    W = oracle.build_kernels(pb, box)
+    t_kgen = time.perf_counter() - t
+    C = fi.initial_c(mask, "paper").astype(np.float64)
+    t = time.perf_counter()
+    for _ in range(steps):
+        oracle.step_scatter(pb, W, box, C, box)
+    t_step = (time.perf_counter() - t) / steps
+    cores = os.cpu_count()
+    return {"value": n_src / t_step, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "oracle fp64 scatter step over a %dx%dx%d box (%d voxel-updates/step, mean of %d steps, "
+                      "1 thread); its kernels from oracle kgen on %d cores: %.3f s for %d sources "
+                      "(%.3g window cell-updates/s)" % (box[1] - box[0], box[3] - box[2], box[5] - box[4], n_src,
+                                                        steps, cores, t_kgen, n_src,
+                                                        n_src * cfg.K * oracle.derive(pb).n_fd / t_kgen),
+            "kgen_sources_per_s": n_src / t_kgen, "kgen_cores": cores}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (this tier's reference arm) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = fi.config(args.config, weights=args.weights)
+    mask = cfg.mask()
+    import oracle
+
+    oracle.build()
+    pb = oracle.Problem(mask=mask, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt, R=cfg.R,
+                        n_fd=cfg.n_fd)
+    nz, ny, nx = mask.shape
+    cy, cz = ny // 2, nz // 2
+    x0 = min(nx - 8, nx // 2 + int(0.45 * nx) // 2) if nx >= 64 else 0
+    box = (x0, x0 + min(8, nx), max(0, cy - 4), max(0, cy - 4) + min(8, ny), max(0, cz - 4), max(0, cz - 4) + min(8, nz))
+    n_src = (box[1] - box[0]) * (box[3] - box[2]) * (box[5] - box[4])
+    t = time.perf_counter()
+    W = oracle.build_kernels(pb, box)
+    t_kgen = time.perf_counter() - t
+    C = fi.initial_c(mask, "paper").astype(np.float64)
+    for _ in range(args.warmup):
+        oracle.step_scatter(pb, W, box, C, box)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        C_box = oracle.step_scatter(pb, W, box, C, box)
+    dt = (time.perf_counter() - t) / args.steps
+    v = n_src / dt
+    sample = ("oracle fp64 scatter step over an %dx%dx%d box of %s (%d voxel-updates per step, 1 thread); "
+              "kernels from oracle kgen (%d cores, %.2f s, untimed)" % (box[1] - box[0], box[3] - box[2],
+                                                                        box[5] - box[4], args.config, n_src,
+                                                                        os.cpu_count(), t_kgen))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload_name(cfg), "sample": "%d voxels" % n_src},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def _workload_name(cfg):
+    return "%s: %s grid, R=%d (K=%d), %s weights, n_fd=%s" % (
+        cfg.name, "x".join(map(str, cfg.shape[::-1])), cfg.R, cfg.K,
+        cfg.weights, cfg.n_fd or "derived")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--weights", default=None)
+    ap.add_argument("--impl", default="fdirw", choices=["fdirw", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_11376_b200 as fd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit("--gpus %d but WORLD_SIZE %d (launch N>1 with torch.distributed.run)" % (args.gpus, world))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = fi.config(args.config, weights=args.weights)
+    mask = cfg.mask()
+    nz, ny, nx = cfg.shape
+    z0, z1 = fd.slabs(nz, world)[rank]
+    nccl_id = None
+    if world > 1:
+        obj = [fd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    params = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt,
+                       radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    ctx = fd.build_kernels(params, mask, rank=rank, world=world, z_begin=z0, z_end=z1, device=local,
+                           nccl_id=nccl_id, stream=stream)
+    t_kgen = time.perf_counter() - t
+    info = ctx.info
+
+    c_host = torch.from_numpy(np.ascontiguousarray(fi.initial_c(mask, "paper")[z0:z1])).pin_memory()
+    c = c_host.to("cuda", non_blocking=True)
+    m0 = fd.mass(ctx, c)
+    fd.run(ctx, c, args.warmup)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        fd.run(ctx, c, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    m1 = fd.mass(ctx, c)
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        km = torch.tensor([t_kgen], device="cuda")
+        dist.all_reduce(km, op=dist.ReduceOp.MAX)
+        t_kgen = float(km.item())
+
+    # e2e through the public API with host buffers: H2D(c) → fdirw_step → D2H(c_out), every step
+    out_dev = torch.empty_like(c)
+    out_host = torch.empty_like(c_host).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        c.copy_(c_host, non_blocking=True)
+        fd.step(ctx, c, out_dev, stream)
+        out_host.copy_(out_dev, non_blocking=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        c.copy_(c_host, non_blocking=True)
+        fd.step(ctx, c, out_dev, stream)
+        out_host.copy_(out_dev, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_ms = float(tt.item())
+
+    N = nx * ny * nz
+    ms_step = t_ms / args.steps
+    value = N * args.steps / (t_ms * 1e-3)
+    e2e_value = N * args.e2e_steps / (e_ms * 1e-3)
+    bpv = info["bytes_per_voxel_update"]
+    per_launch_bytes = bpv * info["voxels"]
+    peak, peak_src = _hbm_peak()
+    launches_per_step = 1 if world == 1 else (3 if info["n_tiles"] > 0 else 1)
+    # one superpose launch per step at N=1 (+1 pack, +1 unpack per fdirw_run); the launch
+    # duration is the timed region / K to within the two ~10 µs state kernels.
+    achieved = per_launch_bytes / (ms_step * 1e-3) / 1e9
+    n_src_planes = min(nz, z1 + cfg.R) - max(0, z0 - cfg.R)
+    kgen_cells = nx * ny * n_src_planes * cfg.K * info["n_fd"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": {"fp32": "f32", "fp16": "f16", "bf16": "bf16"}[cfg.weights] + "-weights/f32-accum",
+        "data": "synthetic",
+        "config": {"workload": _workload_name(cfg), "voxels": N, "parallelism": "z-slab x%d" % world,
+                   "l2": "inputs larger than L2 (%.1f GB of weights streamed per step)" %
+                         (info["weight_bytes"] * world / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "superpose_kernel",
+                     "peak_source": peak_src, "bytes_per_voxel_update": bpv,
+                     "note": "algorithmic bytes (K-1)*b_w+12 per voxel-update x voxels / step time (per rank)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(c.numel() * 4 * world),
+                "d2h_bytes_per_step": int(c.numel() * 4 * world), "api": "fdirw_step with pinned host copies"},
+        "gpu_launches": (args.steps * launches_per_step + 2) * world,
+        "kgen": {"seconds": t_kgen, "window_cell_updates": kgen_cells * world,
+                 "cell_updates_per_s": kgen_cells * world / t_kgen, "n_fd": info["n_fd"]},
+        "mass_rel_err": abs(m1 - m0) / abs(m0) if m0 else None,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, mask)
+    fd.destroy(ctx)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

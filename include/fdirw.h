@@ -1,0 +1,175 @@
+/*
+ * fdirw.h — C ABI of the B200-native FDiRW hot path (arXiv 2408.11376).
+ *
+ * FDiRW (Finite Difference informed Random Walker) advances a strongly
+ * inhomogeneous diffusion field over a LARGE step Δt by superposition of
+ * pre-computed transition kernels (§3.1 Eq.8):
+ *
+ *     C_new(x) = Σ_s W_s(x − s) · C_old(s)                                 (a5)
+ *
+ * where W_s, the mass fraction moving from source voxel s to x over Δt
+ * ("p_ij is the mass proportion moving from node j to node i"), is
+ * obtained by an explicit finite-difference run from a single point source
+ * (P:109), here inside the source's own (2R+1)^3 window (a3).  The library
+ * builds all W_s on the GPU (fdirw_build_kernels), stores them in fp32, fp16
+ * or bf16 (§3.3 mixed precision; accumulation always fp32), and
+ * applies the step (fdirw_step / fdirw_run).  With world > 1 every rank owns a
+ * z-slab of targets and exchanges R-plane halos of C over NCCL each step.
+ *
+ * Conventions
+ *   - Grid [nz][ny][nx], x fastest.  All concentration buffers passed to the
+ *     library are DEVICE pointers to dense fp32 arrays of the caller's slab
+ *     [z_end − z_begin][ny][nx] (the whole grid when world == 1).
+ *   - phase_host is a HOST pointer to the WHOLE grid's uint8 mask
+ *     (1 = fast phase / liquid, 0 = slow phase / solid), read only
+ *     during fdirw_build_kernels and copied.
+ *   - Diffusivities are EFFECTIVE ones, D·A/RT (Eqs.1-3).
+ *   - Window: cube of Chebyshev radius R around each source, K = (2R+1)^3.
+ *     Window edges and domain edges carry no flux (closed domain; DESIGN.md
+ *     readings A1-A3, A21).  Face diffusivity across phases: harmonic mean (A4).
+ *   - Streams: `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ *     Every call that takes a stream only ENQUEUES work on it and returns;
+ *     errors of enqueued kernels surface at the next call or synchronisation.
+ *   - Errors: every entry point returns an fdirw_status; the thread-local
+ *     message of the last failure is fdirw_last_error().  No C++ exception
+ *     crosses the ABI.  After FDIRW_E_CUDA / FDIRW_E_NCCL the context is
+ *     unusable and must be destroyed.
+ *   - Ownership: the caller owns phase_host and every concentration buffer;
+ *     the context owns the weights, the diagonal, the padded ping-pong state,
+ *     the halo buffers, the NCCL communicator and the CUDA graph, all freed by
+ *     fdirw_destroy.
+ */
+#ifndef FDIRW_H
+#define FDIRW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fdirw_ctx fdirw_ctx; /* opaque */
+
+typedef enum {
+    FDIRW_OK = 0,
+    FDIRW_E_INVALID = 1,  /* bad argument: dims < 1, R < 1 or R > 8, D_fast <= 0, D_slow < 0, dt <= 0,
+                             dh <= 0, NULL pointer, bad slab split, bad weight format           */
+    FDIRW_E_UNSTABLE = 2, /* explicit FD unstable: λ_max = Δt_fd·D_max/Δh² > 1/6 (given n_fd)  */
+    FDIRW_E_OOM = 3,      /* device allocation failed; message names the bytes required          */
+    FDIRW_E_CUDA = 4,     /* CUDA runtime error (message has the CUDA error string)              */
+    FDIRW_E_NCCL = 5,     /* NCCL error, or NCCL library not loadable when world > 1              */
+    FDIRW_E_ALIAS = 6,    /* c_in == c_out in fdirw_step                                          */
+    FDIRW_E_STATE = 7     /* call not valid in this context state (e.g. debug upload on world>1) */
+} fdirw_status;
+
+typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weight_t;
+
+/* fdirw_params.flags */
+#define FDIRW_F_NO_MASS_FIX 1u /* diagonal = RNE_fmt(W_s(0)) instead of the fp32 mass fix-up (A10) */
+
+/* The paper's problem statement (Table 1) + north_star's window radius / precision. */
+typedef struct {
+    int32_t nx, ny, nz;     /* global grid, each >= 1                                          */
+    double dh;              /* voxel edge Δh > 0                                               */
+    double D_fast, D_slow;  /* effective diffusivities, D_fast > 0, D_slow >= 0 (0 = impermeable) */
+    double dt;              /* macro step Δt > 0                                               */
+    int32_t radius;         /* window half-width R, 1 <= R <= 8                                */
+    int32_t n_fd;           /* FD substeps per Δt; 0 = derive n_fd = ceil(x(1−1e-9)),
+                               x = D_max·Δt/(0.1·Δh²) (λ* = 0.1 from Table 1, reading A5)     */
+    int32_t weights;        /* fdirw_weight_t: storage format of W (accumulation is fp32)     */
+    uint32_t flags;         /* FDIRW_F_*                                                       */
+} fdirw_params;
+
+/* Slab decomposition (world > 1): rank r owns target planes [z_begin, z_end).
+ * Slabs must tile [0, nz) in rank order and be at least R planes thick.
+ * nccl_id: 128 bytes produced by fdirw_nccl_unique_id on rank 0 and broadcast
+ * by the caller (e.g. torch.distributed).  world == 1 needs no id.  */
+typedef struct {
+    int32_t rank, world;
+    int32_t z_begin, z_end;
+    int32_t device;         /* CUDA device ordinal the context lives on                      */
+    const void* nccl_id;    /* NULL when world == 1                                          */
+} fdirw_dist;
+
+typedef struct {
+    int32_t n_fd;           /* FD substeps per macro step                                      */
+    int32_t K;              /* (2R+1)^3                                                        */
+    int32_t z_begin, z_end; /* this context's target slab                                      */
+    double dt_fd;           /* Δt / n_fd                                                        */
+    double lambda_fast, lambda_fs, lambda_slow; /* face numbers Δt_fd·D/Δh² (fast-fast, cross, slow-slow) */
+    uint64_t weight_bytes;  /* device bytes of the stored weights incl. fp32 diagonal + padding */
+    uint64_t state_bytes;   /* device bytes of the padded ping-pong concentration state         */
+    uint64_t bytes_per_voxel_update; /* algorithmic: (K−1)·b_w + 4 (diag) + 4 (C read) + 4 (C write) */
+    uint64_t voxels;        /* targets in this slab: nx·ny·(z_end − z_begin)                   */
+    int32_t tile_chunks;    /* 8-voxel x-chunks per superposition tile (CTA)                   */
+    int32_t n_tiles;        /* tiles in this slab                                              */
+} fdirw_info;
+
+/* Writes a fresh 128-byte ncclUniqueId to out128 (host).  Call on rank 0 only.
+ * FDIRW_E_NCCL if libnccl.so.2 cannot be loaded. */
+fdirw_status fdirw_nccl_unique_id(void* out128);
+
+/* a1-a4: validate params, derive n_fd and the face numbers (host, fp64), plan
+ * device memory for the slab, copy the mask planes [z_begin−2R, z_end+2R)
+ * to the device, and generate every kernel W_s whose window reaches the slab
+ * (sources [z_begin−R, z_end+R) ∩ [0,nz)) with the batched-window FD kernel,
+ * then renormalise (fp64), quantise (RNE), fix the fp32 diagonal and write the
+ * gather layout.  Enqueued on cuda_stream; the call synchronises that stream
+ * before returning so the context is ready.  dist == NULL means world = 1 on
+ * the current device.  On success *out owns all device memory.  */
+fdirw_status fdirw_build_kernels(const fdirw_params* params, const uint8_t* phase_host,
+                                 const fdirw_dist* dist, void* cuda_stream, fdirw_ctx** out);
+
+/* a5/a6: one FDiRW step C_out = W ⊛ C_in on this rank's slab (halo exchange with
+ * the z-neighbours when world > 1; every rank must call it).  c_in and c_out are
+ * device fp32 [z_end−z_begin][ny][nx]; c_in is not modified; c_in == c_out →
+ * FDIRW_E_ALIAS.  Asynchronous on cuda_stream. */
+fdirw_status fdirw_step(fdirw_ctx* ctx, const float* c_in_dev, float* c_out_dev, void* cuda_stream);
+
+/* a7: n_steps FDiRW steps in place on c_dev (device fp32 slab), ping-ponging
+ * inside the context's padded state and replayed from a CUDA graph.  n_steps
+ * >= 0.  Asynchronous on cuda_stream. */
+fdirw_status fdirw_run(fdirw_ctx* ctx, float* c_dev, int32_t n_steps, void* cuda_stream);
+
+/* a7 diagnostics: Σ c over the WHOLE grid in fp64 (each rank sums its slab on
+ * the device; an NCCL all-reduce combines ranks).  Synchronises cuda_stream and
+ * writes the result to *out_host. */
+fdirw_status fdirw_mass(fdirw_ctx* ctx, const float* c_dev, double* out_host, void* cuda_stream);
+
+/* Fills *info (host).  Never fails on a valid ctx. */
+fdirw_status fdirw_query(const fdirw_ctx* ctx, fdirw_info* info);
+
+/* Frees everything the context owns (synchronises its device first).  NULL is a no-op. */
+void fdirw_destroy(fdirw_ctx* ctx);
+
+/* Thread-local message of the last non-OK status on this thread ("" if none). */
+const char* fdirw_last_error(void);
+
+/* ---- test support ------------------------------------------------------------
+ * Replace the weights of a world == 1 context by caller-supplied per-source
+ * kernels (host fp64, [nz][ny][nx][K], slot o = ((oz+R)·L+(oy+R))·L+(ox+R),
+ * centre slot = the fp32 diagonal).  Off-centre values are converted to the
+ * context's storage format with RNE; out-of-domain slots are ignored.  Used
+ * to test the superposition in isolation against oracle weights.
+ * Synchronous.  FDIRW_E_STATE when world > 1. */
+fdirw_status fdirw_debug_upload_weights(fdirw_ctx* ctx, const double* kernels_host);
+
+/* Read back the stored kernels of the sources in the box [x0,x1)×[y0,y1)×[z0,z1)
+ * (global coordinates; box = int32[6] = x0,x1,y0,y1,z0,z1) as host fp64
+ * [bz][by][bx][K], decoded from the gather layout (centre slot = diagonal).
+ * Slots whose target lies outside this context's slab or the domain read 0.
+ * Synchronous. */
+fdirw_status fdirw_export_kernels(const fdirw_ctx* ctx, const int32_t* box, double* kernels_host);
+
+/* Single-process "virtual ranks": n contexts built on ONE device with
+ * dist = {r, n, slab_r, device, NULL} and flag-free params, stepped together
+ * with the halo planes moved by cudaMemcpyAsync instead of NCCL.  Exercises
+ * the slab, halo and interior/boundary logic of the multi-GPU path on one GPU.
+ * c_in[r], c_out[r] are the ranks' slab buffers. */
+fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, const float* const* c_in,
+                                float* const* c_out, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDIRW_H */

@@ -1,0 +1,240 @@
+"""paper_2408_11376_b200 — B200-native FDiRW hot path (arXiv 2408.11376).
+
+Thin ctypes binding of ``include/fdirw.h`` (libfdirw.so, built in-tree for
+sm_100a).  Argument marshalling only: every step of the method runs in the
+library's CUDA kernels.  torch supplies device memory (tensors), streams and
+the torch.distributed bootstrap of the NCCL id; nothing else.
+
+There is no CPU fallback: importing this package raises if libfdirw.so is
+missing, and every call raises ``FdirwError`` on a non-OK status.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libfdirw.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        "libfdirw.so not found at %s — build it with `python -m paper_2408_11376_b200.build` "
+        "(or __graft_entry__.build()); there is no fallback path" % _LIB_PATH)
+
+_lib = ctypes.CDLL(_LIB_PATH)
+
+FDIRW_OK, E_INVALID, E_UNSTABLE, E_OOM, E_CUDA, E_NCCL, E_ALIAS, E_STATE = range(8)
+STATUS_NAMES = ["OK", "E_INVALID", "E_UNSTABLE", "E_OOM", "E_CUDA", "E_NCCL", "E_ALIAS", "E_STATE"]
+WEIGHTS = {"fp32": 0, "fp16": 1, "bf16": 2}
+F_NO_MASS_FIX = 1
+
+EXPORTS = ["fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
+           "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
+           "fdirw_export_kernels", "fdirw_step_virtual"]
+
+
+class fdirw_params(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("dh", ctypes.c_double), ("D_fast", ctypes.c_double), ("D_slow", ctypes.c_double),
+                ("dt", ctypes.c_double), ("radius", ctypes.c_int32), ("n_fd", ctypes.c_int32),
+                ("weights", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+
+
+class fdirw_dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("z_begin", ctypes.c_int32),
+                ("z_end", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+
+
+class fdirw_info(ctypes.Structure):
+    _fields_ = [("n_fd", ctypes.c_int32), ("K", ctypes.c_int32), ("z_begin", ctypes.c_int32),
+                ("z_end", ctypes.c_int32), ("dt_fd", ctypes.c_double), ("lambda_fast", ctypes.c_double),
+                ("lambda_fs", ctypes.c_double), ("lambda_slow", ctypes.c_double),
+                ("weight_bytes", ctypes.c_uint64), ("state_bytes", ctypes.c_uint64),
+                ("bytes_per_voxel_update", ctypes.c_uint64), ("voxels", ctypes.c_uint64),
+                ("tile_chunks", ctypes.c_int32), ("n_tiles", ctypes.c_int32)]
+
+
+_vp = ctypes.c_void_p
+_st = ctypes.c_int
+_lib.fdirw_nccl_unique_id.argtypes = [_vp]
+_lib.fdirw_nccl_unique_id.restype = _st
+_lib.fdirw_build_kernels.argtypes = [ctypes.POINTER(fdirw_params), _vp, ctypes.POINTER(fdirw_dist), _vp,
+                                     ctypes.POINTER(_vp)]
+_lib.fdirw_build_kernels.restype = _st
+_lib.fdirw_step.argtypes = [_vp, _vp, _vp, _vp]
+_lib.fdirw_step.restype = _st
+_lib.fdirw_run.argtypes = [_vp, _vp, ctypes.c_int32, _vp]
+_lib.fdirw_run.restype = _st
+_lib.fdirw_mass.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_double), _vp]
+_lib.fdirw_mass.restype = _st
+_lib.fdirw_query.argtypes = [_vp, ctypes.POINTER(fdirw_info)]
+_lib.fdirw_query.restype = _st
+_lib.fdirw_destroy.argtypes = [_vp]
+_lib.fdirw_destroy.restype = None
+_lib.fdirw_last_error.argtypes = []
+_lib.fdirw_last_error.restype = ctypes.c_char_p
+_lib.fdirw_debug_upload_weights.argtypes = [_vp, _vp]
+_lib.fdirw_debug_upload_weights.restype = _st
+_lib.fdirw_export_kernels.argtypes = [_vp, _vp, _vp]
+_lib.fdirw_export_kernels.restype = _st
+_lib.fdirw_step_virtual.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32, ctypes.POINTER(_vp),
+                                    ctypes.POINTER(_vp), _vp]
+_lib.fdirw_step_virtual.restype = _st
+
+
+class FdirwError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__("%s: %s" % (STATUS_NAMES[status] if 0 <= status < 8 else status, msg))
+
+
+def last_error() -> str:
+    return _lib.fdirw_last_error().decode()
+
+
+def _check(rc: int):
+    if rc != FDIRW_OK:
+        raise FdirwError(rc, last_error())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dptr(t):
+    """Device pointer of a contiguous fp32 CUDA tensor."""
+    if not (t.is_cuda and t.is_contiguous() and str(t.dtype) == "torch.float32"):
+        raise ValueError("expected a contiguous float32 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class Params:
+    nx: int
+    ny: int
+    nz: int
+    dh: float
+    D_fast: float
+    D_slow: float
+    dt: float
+    radius: int
+    n_fd: int = 0
+    weights: str = "bf16"
+    flags: int = 0
+
+    def c(self) -> fdirw_params:
+        return fdirw_params(self.nx, self.ny, self.nz, self.dh, self.D_fast, self.D_slow, self.dt, self.radius,
+                            self.n_fd, WEIGHTS[self.weights], self.flags)
+
+
+class Context:
+    """Owns an fdirw_ctx*; call destroy() (or use as a context manager)."""
+
+    def __init__(self, handle: int, params: Params):
+        self.handle = ctypes.c_void_p(handle)
+        self.params = params
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        destroy(self)
+
+    @property
+    def info(self):
+        return query(self)
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.fdirw_nccl_unique_id(buf))
+    return buf.raw
+
+
+def build_kernels(params: Params, phase: np.ndarray, rank: int = 0, world: int = 1, z_begin: int | None = None,
+                  z_end: int | None = None, device: int | None = None, nccl_id: bytes | None = None,
+                  stream=None) -> Context:
+    """fdirw_build_kernels: phase = WHOLE-grid uint8 mask [nz][ny][nx] (host), 1 = fast."""
+    phase = np.ascontiguousarray(phase, dtype=np.uint8)
+    if phase.shape != (params.nz, params.ny, params.nx):
+        raise ValueError("phase shape %s != (nz, ny, nx)" % (phase.shape,))
+    p = params.c()
+    dist = None
+    idbuf = None
+    if world > 1 or z_begin is not None or device is not None:
+        if device is None:
+            import torch
+
+            device = torch.cuda.current_device()
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(nccl_id, 128)
+        dist = fdirw_dist(rank, world, 0 if z_begin is None else z_begin, params.nz if z_end is None else z_end,
+                          device, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None)
+    h = ctypes.c_void_p()
+    _check(_lib.fdirw_build_kernels(ctypes.byref(p), phase.ctypes.data_as(ctypes.c_void_p),
+                                    ctypes.byref(dist) if dist is not None else None, _stream(stream),
+                                    ctypes.byref(h)))
+    return Context(h.value, params)
+
+
+def step(ctx: Context, c_in, c_out, stream=None):
+    _check(_lib.fdirw_step(ctx.handle, _dptr(c_in), _dptr(c_out), _stream(stream)))
+
+
+def run(ctx: Context, c, n_steps: int, stream=None):
+    _check(_lib.fdirw_run(ctx.handle, _dptr(c), int(n_steps), _stream(stream)))
+
+
+def mass(ctx: Context, c, stream=None) -> float:
+    out = ctypes.c_double()
+    _check(_lib.fdirw_mass(ctx.handle, _dptr(c), ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+def query(ctx: Context) -> dict:
+    info = fdirw_info()
+    _check(_lib.fdirw_query(ctx.handle, ctypes.byref(info)))
+    return {f: getattr(info, f) for f, _ in fdirw_info._fields_}
+
+
+def destroy(ctx: Context):
+    if ctx.handle and ctx.handle.value:
+        _lib.fdirw_destroy(ctx.handle)
+        ctx.handle = ctypes.c_void_p()
+
+
+def debug_upload_weights(ctx: Context, kernels: np.ndarray):
+    k = np.ascontiguousarray(kernels, dtype=np.float64)
+    _check(_lib.fdirw_debug_upload_weights(ctx.handle, k.ctypes.data_as(ctypes.c_void_p)))
+
+
+def export_kernels(ctx: Context, box) -> np.ndarray:
+    """Stored kernels of the sources in box = (x0,x1,y0,y1,z0,z1) → fp64 [bz][by][bx][K]."""
+    b = np.array(box, np.int32)
+    K = (2 * ctx.params.radius + 1) ** 3
+    out = np.zeros((b[5] - b[4], b[3] - b[2], b[1] - b[0], K), np.float64)
+    _check(_lib.fdirw_export_kernels(ctx.handle, b.ctypes.data_as(ctypes.c_void_p),
+                                     out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def step_virtual(ctxs, c_in, c_out, stream=None):
+    n = len(ctxs)
+    H = (_vp * n)(*[c.handle.value for c in ctxs])
+    I = (_vp * n)(*[_dptr(t).value for t in c_in])
+    O = (_vp * n)(*[_dptr(t).value for t in c_out])
+    _check(_lib.fdirw_step_virtual(H, n, I, O, _stream(stream)))
+
+
+def slabs(nz: int, world: int):
+    """Equal z-slabs [r·nz/P, (r+1)·nz/P)."""
+    return [(r * nz // world, (r + 1) * nz // world) for r in range(world)]

@@ -1,0 +1,540 @@
+// fdirw_api.cu — the C ABI of include/fdirw.h: validation, parameter derivation (a1),
+// memory plan, kernel generation driver (a2-a4), step / run loop with CUDA graphs
+// (a5-a7), NCCL slab exchange (a6) and test-support entry points.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fdirw_internal.h"
+#include "layout.cuh"
+
+using namespace fdirw;
+
+struct fdirw_ctx {
+    fdirw_params p;
+    Derived d;
+    Geometry g;
+    int rank = 0, world = 1, device = 0;
+    bool is_virtual = false;
+    int fmt = 0, b_w = 4;
+    void* Wt = nullptr;
+    float* diag = nullptr;
+    float* cpad[2] = {nullptr, nullptr};
+    double* mass_partial = nullptr;
+    double* mass_out = nullptr;
+    int mass_blocks = 0;
+    cudaStream_t comm_stream = nullptr, capture_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_comm = nullptr;
+    cudaGraphExec_t graph2 = nullptr;
+    Nccl* nccl = nullptr;
+    void* comm = nullptr;
+};
+
+static thread_local std::string g_err;
+
+static fdirw_status fail(fdirw_status s, const std::string& msg)
+{
+    g_err = msg;
+    return s;
+}
+
+#define CUDA_TRY(call)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(FDIRW_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+namespace fdirw {
+
+Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1)
+{
+    Geometry g{};
+    g.nx = nx; g.ny = ny; g.nz = nz; g.R = R;
+    g.L = 2 * R + 1;
+    g.K = g.L * g.L * g.L;
+    g.z0 = z0; g.z1 = z1; g.nzl = z1 - z0;
+    g.nxq = (nx + kChunk - 1) / kChunk;
+    g.cpp = ny * g.nxq;
+    int tile = ((g.cpp + 31) / 32) * 32;
+    g.tile = tile > 256 ? 256 : tile;
+    g.tpp = (g.cpp + g.tile - 1) / g.tile;
+    g.n_tiles = g.nzl * g.tpp;
+    g.nxp = g.nxq * kChunk + 2 * kPadX;
+    g.nyp = ny + 2 * R;
+    g.nzp = g.nzl + 2 * R;
+    g.plane_elems = (size_t)g.nyp * g.nxp;
+    g.state_elems = (size_t)g.nzp * g.plane_elems;
+    g.w_elems = (size_t)g.n_tiles * (g.K - 1) * g.tile * kChunk;
+    g.diag_elems = (size_t)g.n_tiles * g.tile * kChunk;
+    g.mz0 = z0 - 2 * R < 0 ? 0 : z0 - 2 * R;
+    g.mz1 = z1 + 2 * R > nz ? nz : z1 + 2 * R;
+    g.sz0 = z0 - R < 0 ? 0 : z0 - R;
+    g.sz1 = z1 + R > nz ? nz : z1 + R;
+    return g;
+}
+
+}  // namespace fdirw
+
+// a1: n_fd = ceil(x·(1 − 1e-9)), x = D_max·Δt/(λ*·Δh²), λ* = 0.1 (Table 1, P:84-91;
+// reading A5); face numbers λ = Δt_fd·D/Δh² with the harmonic mean across phases (A4).
+static fdirw_status derive(const fdirw_params& p, Derived* d)
+{
+    const double dmax = p.D_fast > p.D_slow ? p.D_fast : p.D_slow;
+    long n = p.n_fd;
+    if (n == 0) {
+        const double x = dmax * p.dt / (0.1 * p.dh * p.dh);
+        const double c = std::ceil(x * (1.0 - 1e-9));
+        if (!(c < 2.0e9)) return fail(FDIRW_E_INVALID, "derived n_fd too large (" + std::to_string(c) + ")");
+        n = c < 1.0 ? 1 : (long)c;
+    }
+    d->n_fd = (int)n;
+    d->dt_fd = p.dt / (double)n;
+    const double s = d->dt_fd / (p.dh * p.dh);
+    const double hm = (p.D_fast + p.D_slow) == 0.0 ? 0.0 : 2.0 * p.D_fast * p.D_slow / (p.D_fast + p.D_slow);
+    d->lam_ff = s * p.D_fast;
+    d->lam_ss = s * p.D_slow;
+    d->lam_fs = s * hm;
+    if (d->lam_ff > 1.0 / 6.0 || d->lam_ss > 1.0 / 6.0) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "explicit FD unstable: lambda_max = %.6g > 1/6 (n_fd = %d)",
+                 d->lam_ff > d->lam_ss ? d->lam_ff : d->lam_ss, d->n_fd);
+        return fail(FDIRW_E_UNSTABLE, buf);
+    }
+    return FDIRW_OK;
+}
+
+static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const fdirw_dist* dist,
+                             fdirw_ctx** out)
+{
+    if (!p || !phase || !out) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (p->nx < 1 || p->ny < 1 || p->nz < 1) return fail(FDIRW_E_INVALID, "grid dims must be >= 1");
+    if (p->radius < 1 || p->radius > kMaxR) return fail(FDIRW_E_INVALID, "radius must be in [1, 8]");
+    if (!(p->dh > 0) || !(p->dt > 0)) return fail(FDIRW_E_INVALID, "dh and dt must be > 0");
+    if (!(p->D_fast > 0) || !(p->D_slow >= 0)) return fail(FDIRW_E_INVALID, "need D_fast > 0, D_slow >= 0");
+    if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
+    if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
+    if (p->flags & ~FDIRW_F_NO_MASS_FIX) return fail(FDIRW_E_INVALID, "unknown flags");
+    if ((long long)p->nx * p->ny * p->nz > (1LL << 40)) return fail(FDIRW_E_INVALID, "grid too large");
+    if (dist) {
+        if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+            return fail(FDIRW_E_INVALID, "bad rank/world");
+        if (dist->z_begin < 0 || dist->z_end > p->nz || dist->z_begin >= dist->z_end)
+            return fail(FDIRW_E_INVALID, "bad slab [z_begin, z_end)");
+        if (dist->world == 1 && (dist->z_begin != 0 || dist->z_end != p->nz))
+            return fail(FDIRW_E_INVALID, "world == 1 must own [0, nz)");
+        if (dist->world > 1) {
+            if (dist->z_end - dist->z_begin < p->radius)
+                return fail(FDIRW_E_INVALID, "slab thinner than the window radius R");
+            if (dist->rank == 0 && dist->z_begin != 0) return fail(FDIRW_E_INVALID, "rank 0 must start at z = 0");
+            if (dist->rank == dist->world - 1 && dist->z_end != p->nz)
+                return fail(FDIRW_E_INVALID, "last rank must end at z = nz");
+        }
+    }
+    return FDIRW_OK;
+}
+
+static void free_ctx(fdirw_ctx* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    if (c->graph2) cudaGraphExecDestroy(c->graph2);
+    if (c->comm) nccl_comm_destroy(c->nccl, c->comm);
+    cudaFree(c->Wt);
+    cudaFree(c->diag);
+    cudaFree(c->cpad[0]);
+    cudaFree(c->cpad[1]);
+    cudaFree(c->mass_partial);
+    cudaFree(c->mass_out);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+    delete c;
+}
+
+static fdirw_status alloc(void** ptr, size_t bytes, const char* what)
+{
+    cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 16);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        char buf[200];
+        snprintf(buf, sizeof buf, "out of device memory allocating %s: %zu bytes required, %zu free", what, bytes, fr);
+        return fail(FDIRW_E_OOM, buf);
+    }
+    if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_nccl_unique_id(void* out128)
+{
+    if (!out128) return fail(FDIRW_E_INVALID, "NULL argument");
+    std::string err;
+    Nccl* n = nccl_load(&err);
+    if (!n) return fail(FDIRW_E_NCCL, err);
+    if (nccl_unique_id(n, out128, &err)) return fail(FDIRW_E_NCCL, err);
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const uint8_t* phase_host,
+                                            const fdirw_dist* dist, void* cuda_stream, fdirw_ctx** out)
+{
+    fdirw_status st = validate(params, phase_host, dist, out);
+    if (st != FDIRW_OK) return st;
+    *out = nullptr;
+    Derived d;
+    if ((st = derive(*params, &d)) != FDIRW_OK) return st;
+
+    fdirw_ctx* c = new fdirw_ctx();
+    c->p = *params;
+    c->d = d;
+    c->fmt = params->weights;
+    c->b_w = c->fmt == FDIRW_W_FP32 ? 4 : 2;
+    int z0 = 0, z1 = params->nz;
+    if (dist) {
+        c->rank = dist->rank;
+        c->world = dist->world;
+        c->device = dist->device;
+        z0 = dist->z_begin;
+        z1 = dist->z_end;
+        c->is_virtual = dist->world > 1 && dist->nccl_id == nullptr;
+        if (cudaSetDevice(c->device) != cudaSuccess) {
+            delete c;
+            return fail(FDIRW_E_INVALID, "cudaSetDevice failed for dist->device");
+        }
+    } else {
+        cudaGetDevice(&c->device);
+    }
+    c->g = make_geometry(params->nx, params->ny, params->nz, params->radius, z0, z1);
+    const Geometry& g = c->g;
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+
+    auto bail = [&](fdirw_status e) {
+        std::string keep = g_err;
+        free_ctx(c);
+        g_err = keep;
+        return e;
+    };
+#define BAIL_CUDA(call)                                                                               \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess) {                                                                      \
+            g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                               \
+            return bail(FDIRW_E_CUDA);                                                                \
+        }                                                                                             \
+    } while (0)
+
+    // a2: mask planes [mz0, mz1) → device (the face number is a function of the two phases only)
+    uint8_t* mask_d = nullptr;
+    const size_t plane = (size_t)g.nx * g.ny;
+    const size_t mbytes = (size_t)(g.mz1 - g.mz0) * plane;
+    if ((st = alloc((void**)&mask_d, mbytes, "mask")) != FDIRW_OK) return bail(st);
+    if ((st = alloc(&c->Wt, g.w_elems * c->b_w, "weights")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
+    if ((st = alloc((void**)&c->diag, g.diag_elems * 4, "diagonal")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
+    for (int i = 0; i < 2; ++i)
+        if ((st = alloc((void**)&c->cpad[i], g.state_elems * 4, "state")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
+    c->mass_blocks = 148 * 4;
+    if ((st = alloc((void**)&c->mass_partial, c->mass_blocks * 8, "mass")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
+    if ((st = alloc((void**)&c->mass_out, 8, "mass")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
+
+    BAIL_CUDA(cudaMemcpyAsync(mask_d, phase_host + (size_t)g.mz0 * plane, mbytes, cudaMemcpyHostToDevice, s));
+    BAIL_CUDA(cudaMemsetAsync(c->Wt, 0, g.w_elems * c->b_w, s));
+    BAIL_CUDA(cudaMemsetAsync(c->diag, 0, g.diag_elems * 4, s));
+    BAIL_CUDA(cudaMemsetAsync(c->cpad[0], 0, g.state_elems * 4, s));
+    BAIL_CUDA(cudaMemsetAsync(c->cpad[1], 0, g.state_elems * 4, s));
+
+    // a3 + a4
+    KgenArgs ka{};
+    ka.mask = mask_d;
+    ka.mz0 = g.mz0;
+    ka.nx = g.nx; ka.ny = g.ny; ka.nz = g.nz;
+    ka.sz0 = g.sz0; ka.sz1 = g.sz1;
+    ka.z0 = g.z0; ka.z1 = g.z1;
+    ka.lam_ff = (float)d.lam_ff; ka.lam_fs = (float)d.lam_fs; ka.lam_ss = (float)d.lam_ss;
+    ka.n_fd = d.n_fd;
+    ka.fmt = c->fmt;
+    ka.mass_fix = (params->flags & FDIRW_F_NO_MASS_FIX) ? 0 : 1;
+    ka.Wt = c->Wt;
+    ka.diag = c->diag;
+    ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;
+    BAIL_CUDA(launch_kgen(ka, g.R, s));
+    BAIL_CUDA(cudaStreamSynchronize(s));
+    cudaFree(mask_d);
+
+    BAIL_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    BAIL_CUDA(cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking));
+    BAIL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    BAIL_CUDA(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+
+    if (c->world > 1 && !c->is_virtual) {
+        std::string err;
+        c->nccl = nccl_load(&err);
+        if (!c->nccl) { g_err = err; return bail(FDIRW_E_NCCL); }
+        c->comm = nccl_comm_init(c->nccl, c->world, c->rank, dist->nccl_id, &err);
+        if (!c->comm) { g_err = err; return bail(FDIRW_E_NCCL); }
+    }
+#undef BAIL_CUDA
+    *out = c;
+    return FDIRW_OK;
+}
+
+// Superpose tiles [t0, t1) of `src` (padded) into `out` with strides (ps, rs).
+static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps, long rs, int t0, int t1,
+                             cudaStream_t s)
+{
+    const Geometry& g = c->g;
+    SuperArgs a{};
+    a.cpad = src;
+    a.Wt = c->Wt;
+    a.diag = c->diag;
+    a.out = out;
+    a.out_ps = ps;
+    a.out_rs = rs;
+    a.nx = g.nx; a.ny = g.ny; a.nxq = g.nxq; a.tile = g.tile; a.tpp = g.tpp; a.K = g.K;
+    a.nxp = g.nxp; a.nyp = g.nyp;
+    a.t_begin = t0;
+    a.t_end = t1;
+    return launch_superpose(a, g.R, c->fmt, s);
+}
+
+// Interior tiles are those whose targets read no halo plane: z_local ∈ [R, nzl − R).
+static void split_tiles(const Geometry& g, int* int0, int* int1)
+{
+    if (g.nzl <= 2 * g.R) { *int0 = *int1 = 0; return; }
+    *int0 = g.R * g.tpp;
+    *int1 = (g.nzl - g.R) * g.tpp;
+}
+
+// One step src (padded, slab planes filled) → out; exchanges the halo planes of src first.
+static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, long rs, cudaStream_t s)
+{
+    const Geometry& g = c->g;
+    if (c->world == 1) {
+        CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
+        return FDIRW_OK;
+    }
+    int i0, i1;
+    split_tiles(g, &i0, &i1);
+    CUDA_TRY(cudaEventRecord(c->ev_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+    std::string err;
+    if (nccl_halo(c->nccl, c->comm, src, g, c->rank, c->world, c->comm_stream, &err)) return fail(FDIRW_E_NCCL, err);
+    CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
+    CUDA_TRY(superpose(c, src, out, ps, rs, i0, i1, s));  // interior overlaps the exchange
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
+    if (i1 > i0) {
+        CUDA_TRY(superpose(c, src, out, ps, rs, 0, i0, s));
+        CUDA_TRY(superpose(c, src, out, ps, rs, i1, g.n_tiles, s));
+    } else {
+        CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
+    }
+    return FDIRW_OK;
+}
+
+static float* pad_interior(fdirw_ctx* c, int i)
+{
+    const Geometry& g = c->g;
+    return c->cpad[i] + (size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX;
+}
+
+extern "C" fdirw_status fdirw_step(fdirw_ctx* c, const float* c_in, float* c_out, void* cuda_stream)
+{
+    if (!c || !c_in || !c_out) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (c->is_virtual) return fail(FDIRW_E_STATE, "virtual-rank context: use fdirw_step_virtual");
+    if (c_in == c_out) return fail(FDIRW_E_ALIAS, "c_in == c_out");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const Geometry& g = c->g;
+    CUDA_TRY(launch_pack(c_in, c->cpad[0], g, s));
+    return enqueue_step(c, c->cpad[0], c_out, (long)g.nx * g.ny, g.nx, s);
+}
+
+extern "C" fdirw_status fdirw_run(fdirw_ctx* c, float* c_dev, int32_t n_steps, void* cuda_stream)
+{
+    if (!c || !c_dev) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (n_steps < 0) return fail(FDIRW_E_INVALID, "n_steps must be >= 0");
+    if (c->is_virtual) return fail(FDIRW_E_STATE, "virtual-rank context: use fdirw_step_virtual");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const Geometry& g = c->g;
+    if (n_steps == 0) return FDIRW_OK;
+    CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s));
+    const long ps = (long)g.plane_elems, rs = g.nxp;
+    if (n_steps >= 2 && !c->graph2) {
+        // capture step(0→1); step(1→0) once; replay it n/2 times
+        cudaStream_t cs = c->capture_stream;
+        CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        fdirw_status st = enqueue_step(c, c->cpad[0], pad_interior(c, 1), ps, rs, cs);
+        if (st == FDIRW_OK) st = enqueue_step(c, c->cpad[1], pad_interior(c, 0), ps, rs, cs);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        if (st != FDIRW_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+        if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        e = cudaGraphInstantiate(&c->graph2, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) { c->graph2 = nullptr; return fail(FDIRW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)); }
+    }
+    for (int i = 0; i < n_steps / 2; ++i) CUDA_TRY(cudaGraphLaunch(c->graph2, s));
+    int fin = 0;
+    if (n_steps & 1) {
+        fdirw_status st = enqueue_step(c, c->cpad[0], pad_interior(c, 1), ps, rs, s);
+        if (st != FDIRW_OK) return st;
+        fin = 1;
+    }
+    CUDA_TRY(launch_unpack(c->cpad[fin], c_dev, g, s));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_mass(fdirw_ctx* c, const float* c_dev, double* out_host, void* cuda_stream)
+{
+    if (!c || !c_dev || !out_host) return fail(FDIRW_E_INVALID, "NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const size_t n = (size_t)c->g.nx * c->g.ny * c->g.nzl;
+    CUDA_TRY(launch_mass(c_dev, n, c->mass_partial, c->mass_blocks, c->mass_out, s));
+    if (c->world > 1 && !c->is_virtual) {
+        std::string err;
+        if (nccl_allreduce_sum_f64(c->nccl, c->comm, c->mass_out, s, &err)) return fail(FDIRW_E_NCCL, err);
+    }
+    CUDA_TRY(cudaMemcpyAsync(out_host, c->mass_out, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
+{
+    if (!c || !info) return fail(FDIRW_E_INVALID, "NULL argument");
+    const Geometry& g = c->g;
+    info->n_fd = c->d.n_fd;
+    info->K = g.K;
+    info->z_begin = g.z0;
+    info->z_end = g.z1;
+    info->dt_fd = c->d.dt_fd;
+    info->lambda_fast = c->d.lam_ff;
+    info->lambda_fs = c->d.lam_fs;
+    info->lambda_slow = c->d.lam_ss;
+    info->weight_bytes = (uint64_t)g.w_elems * c->b_w + (uint64_t)g.diag_elems * 4;
+    info->state_bytes = (uint64_t)g.state_elems * 4 * 2;
+    info->bytes_per_voxel_update = (uint64_t)(g.K - 1) * c->b_w + 12;
+    info->voxels = (uint64_t)g.nx * g.ny * g.nzl;
+    info->tile_chunks = g.tile;
+    info->n_tiles = g.n_tiles;
+    return FDIRW_OK;
+}
+
+extern "C" void fdirw_destroy(fdirw_ctx* c) { free_ctx(c); }
+
+extern "C" const char* fdirw_last_error(void) { return g_err.c_str(); }
+
+extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k)
+{
+    if (!c || !k) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (c->world != 1) return fail(FDIRW_E_STATE, "debug upload needs world == 1");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const Geometry& g = c->g;
+    const int R = g.R, L = g.L, K = g.K;
+    std::vector<unsigned char> wt(g.w_elems * c->b_w, 0);
+    std::vector<float> dg(g.diag_elems, 0.f);
+    for (int sz = 0; sz < g.nz; ++sz)
+        for (int sy = 0; sy < g.ny; ++sy)
+            for (int sx = 0; sx < g.nx; ++sx) {
+                const double* ks = k + (((size_t)sz * g.ny + sy) * g.nx + sx) * K;
+                for (int o = 0; o < K; ++o) {
+                    const int ox = o % L - R, oy = (o / L) % L - R, oz = o / (L * L) - R;
+                    const int x = sx + ox, y = sy + oy, z = sz + oz;
+                    if (x < 0 || x >= g.nx || y < 0 || y >= g.ny || z < 0 || z >= g.nz) continue;
+                    const int q = y * g.nxq + (x >> 3);
+                    const size_t tile = (size_t)z * g.tpp + q / g.tile;
+                    const int e = q % g.tile, j = x & 7;
+                    if (o == K / 2) {
+                        dg[(tile * g.tile + e) * 8 + j] = (float)ks[o];
+                        continue;
+                    }
+                    const size_t idx = ((tile * (size_t)(K - 1) + slot_of(ox, oy, oz, R)) * g.tile + e) * 8 + j;
+                    const float f = (float)ks[o];
+                    if (c->fmt == FDIRW_W_FP32) {
+                        memcpy(&wt[idx * 4], &f, 4);
+                    } else if (c->fmt == FDIRW_W_FP16) {
+                        const __half h = __float2half_rn(f);
+                        memcpy(&wt[idx * 2], &h, 2);
+                    } else {
+                        const __nv_bfloat16 h = __float2bfloat16_rn(f);
+                        memcpy(&wt[idx * 2], &h, 2);
+                    }
+                }
+            }
+    CUDA_TRY(cudaMemcpy(c->Wt, wt.data(), wt.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->diag, dg.data(), dg.size() * 4, cudaMemcpyHostToDevice));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_export_kernels(const fdirw_ctx* c, const int32_t* box, double* out)
+{
+    if (!c || !box || !out) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (box[1] < box[0] || box[3] < box[2] || box[5] < box[4]) return fail(FDIRW_E_INVALID, "bad box");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const size_t n = (size_t)(box[1] - box[0]) * (box[3] - box[2]) * (box[5] - box[4]) * c->g.K;
+    if (n == 0) return FDIRW_OK;
+    double* d = nullptr;
+    fdirw_status st = alloc((void**)&d, n * 8, "export buffer");
+    if (st != FDIRW_OK) return st;
+    cudaError_t e = launch_export(c->Wt, c->diag, c->g, c->fmt, box, d, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("export: ") + cudaGetErrorString(e));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, const float* const* c_in,
+                                           float* const* c_out, void* cuda_stream)
+{
+    if (!ctxs || !c_in || !c_out || n < 1) return fail(FDIRW_E_INVALID, "NULL argument");
+    for (int r = 0; r < n; ++r) {
+        if (!ctxs[r] || !c_in[r] || !c_out[r]) return fail(FDIRW_E_INVALID, "NULL argument");
+        if (ctxs[r]->world != n || ctxs[r]->rank != r) return fail(FDIRW_E_INVALID, "contexts must be ranks 0..n-1");
+        if (n > 1 && !ctxs[r]->is_virtual) return fail(FDIRW_E_STATE, "not a virtual-rank context");
+        if (ctxs[r]->device != ctxs[0]->device) return fail(FDIRW_E_INVALID, "virtual ranks share one device");
+        if (c_in[r] == c_out[r]) return fail(FDIRW_E_ALIAS, "c_in == c_out");
+    }
+    CUDA_TRY(cudaSetDevice(ctxs[0]->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    for (int r = 0; r < n; ++r) CUDA_TRY(launch_pack(c_in[r], ctxs[r]->cpad[0], ctxs[r]->g, s));
+    // halo planes by device copies: the same planes NCCL would move (comm.cpp)
+    for (int r = 0; r < n; ++r) {
+        const Geometry& g = ctxs[r]->g;
+        const size_t bytes = (size_t)g.R * g.plane_elems * 4;
+        if (r > 0) {
+            const Geometry& gl = ctxs[r - 1]->g;
+            CUDA_TRY(cudaMemcpyAsync(ctxs[r]->cpad[0], ctxs[r - 1]->cpad[0] + (size_t)gl.nzl * gl.plane_elems, bytes,
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+        if (r < n - 1) {
+            CUDA_TRY(cudaMemcpyAsync(ctxs[r]->cpad[0] + (size_t)(g.nzl + g.R) * g.plane_elems,
+                                     ctxs[r + 1]->cpad[0] + (size_t)g.R * g.plane_elems, bytes,
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+    }
+    for (int r = 0; r < n; ++r) {
+        fdirw_ctx* c = ctxs[r];
+        const Geometry& g = c->g;
+        int i0, i1;
+        split_tiles(g, &i0, &i1);
+        const long ps = (long)g.nx * g.ny, rs = g.nx;
+        if (i1 > i0) {
+            CUDA_TRY(superpose(c, c->cpad[0], c_out[r], ps, rs, i0, i1, s));
+            CUDA_TRY(superpose(c, c->cpad[0], c_out[r], ps, rs, 0, i0, s));
+            CUDA_TRY(superpose(c, c->cpad[0], c_out[r], ps, rs, i1, g.n_tiles, s));
+        } else {
+            CUDA_TRY(superpose(c, c->cpad[0], c_out[r], ps, rs, 0, g.n_tiles, s));
+        }
+    }
+    return FDIRW_OK;
+}

@@ -1,0 +1,84 @@
+// fdirw_internal.h — internal types shared by the FDiRW CUDA sources (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/fdirw.h"
+
+namespace fdirw {
+
+constexpr int kChunk = 8;     // targets per superposition thread (8 consecutive x)
+constexpr int kPadX = 8;      // x padding of the padded state (≥ R_max so [x−8, x+16) is in range)
+constexpr int kMaxR = 8;
+
+// Target-slab geometry and the gather layout of the weights.
+//   chunk q (within a plane) = y·nxq + x/8; tile tp = q / tile; element e = q % tile; j = x % 8
+//   tile index t = (z − z0)·tpp + tp
+//   Wt[t][slot][e][j] (slot = window offset o minus the centre), diag[t][e][j] fp32
+//   padded state: [nzl + 2R][ny + 2R][nxp], nxp = 8·nxq + 16, x offset kPadX
+struct Geometry {
+    int nx, ny, nz, R, L, K;
+    int z0, z1, nzl;
+    int nxq, cpp, tile, tpp, n_tiles;
+    int nxp, nyp, nzp;
+    size_t plane_elems, state_elems;
+    size_t w_elems, diag_elems;  // element counts of Wt and diag
+    int mz0, mz1;                // device mask planes [mz0, mz1)
+    int sz0, sz1;                // source planes whose windows reach the slab
+};
+
+Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1);
+
+struct Derived {
+    int n_fd;
+    double dt_fd, lam_ff, lam_fs, lam_ss;
+};
+
+// ---- kernels (kgen.cu / superpose.cu) --------------------------------------------
+struct KgenArgs {
+    const uint8_t* mask;  // device planes [mz0, mz1) × ny × nx
+    int mz0;
+    int nx, ny, nz;
+    int sz0, sz1;         // source planes
+    int z0, z1;           // target slab
+    float lam_ff, lam_fs, lam_ss;
+    int n_fd;
+    int fmt, mass_fix;
+    void* Wt;
+    float* diag;
+    int nxq, tile, tpp, K;
+};
+cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s);
+
+struct SuperArgs {
+    const float* cpad;   // padded state, pointer to padded plane 0
+    const void* Wt;
+    const float* diag;
+    float* out;          // output element (z=0 of slab, y=0, x=0)
+    long out_ps, out_rs; // output plane / row strides (elements)
+    int nx, ny, nxq, tile, tpp, K;
+    int nxp, nyp;        // padded row length, rows per padded plane
+    int t_begin, t_end;  // tile range
+};
+cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
+
+cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStream_t s);
+cudaError_t launch_unpack(const float* cpad, float* c, const Geometry& g, cudaStream_t s);
+cudaError_t launch_mass(const float* c, size_t n, double* partial, int nblk, double* out, cudaStream_t s);
+cudaError_t launch_export(const void* Wt, const float* diag, const Geometry& g, int fmt, const int32_t* box,
+                          double* out, cudaStream_t s);
+
+// ---- NCCL (comm.cpp): dlopen'ed, no link-time dependency ------------------------
+struct Nccl;
+Nccl* nccl_load(std::string* err);
+int nccl_unique_id(Nccl*, void* out128, std::string* err);
+void* nccl_comm_init(Nccl*, int world, int rank, const void* id128, std::string* err);
+int nccl_halo(Nccl*, void* comm, float* cpad, const Geometry& g, int rank, int world, cudaStream_t s,
+              std::string* err);
+int nccl_allreduce_sum_f64(Nccl*, void* comm, double* buf, cudaStream_t s, std::string* err);
+void nccl_comm_destroy(Nccl*, void* comm);
+
+}  // namespace fdirw

@@ -1,0 +1,246 @@
+// kgen.cu — a3/a4: batched-window explicit FD kernel generation + quantising epilogue.
+//
+// For every source s (§3.1: column j of p "obtained directly by solving the
+// governing diffusion equation with an initial single point source ... using the
+// explicit Finite Difference Method"), run n_fd Jacobi substeps of the 7-point
+// variable-coefficient stencil inside the source's (2R+1)^3 window (north_star;
+// readings A1-A4, A21 in DESIGN.md):
+//     c⁰ = δ_s,  c^{k+1}_i = c^k_i + Σ_{j∈nb(i)∩Ω_s} λ_ij (c^k_j − c^k_i)
+// with λ_ij = Δt_fd·H(D_i, D_j)/Δh² (harmonic mean H), no flux across window or
+// domain edges.  Then (a4): renormalise by the fp64 sum, round every off-centre
+// weight to fp32 then to the storage format (RNE, §3.3), set the fp32
+// diagonal d_s = 1 − Σ_{o≠0} W̃_s(o) (fp64 sum; reading A10) and scatter the
+// weights into the gather layout Wt[tile(x)][slot(o)][e(x)][j(x)], x = s + o.
+//
+// Mapping: one CTA per window at a time (persistent grid, sources x-fastest so
+// the CTAs in flight write neighbouring targets and L2 merges the 2-byte writes).
+// Thread t < L² owns the z-column (ox, oy) = (t % L − R, t / L − R) of the window
+// in registers: the ±z neighbours are register reads; the ±x/±y neighbours come
+// from a double-buffered shared-memory copy of the window (one barrier per
+// substep).  The 6 face numbers of every owned cell live in registers.
+// Bound: shared-memory bandwidth (4 LDS + 1 STS per cell-update).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "fdirw_internal.h"
+#include "layout.cuh"
+
+namespace fdirw {
+
+template <int R>
+struct KgenShape {
+    static constexpr int L = 2 * R + 1;
+    static constexpr int LL = L * L;
+    static constexpr int LLL = L * L * L;
+    static constexpr int NT = ((LL + 31) / 32) * 32;
+    static constexpr int NW = NT / 32;
+    static constexpr size_t smem_floats = 2 * (size_t)L * LL;             // double-buffered window
+    static constexpr size_t smem_bytes = smem_floats * 4 + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
+};
+
+__device__ __forceinline__ double warp_sum_f64(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block reduction (fixed shuffle tree + fixed warp order).
+template <int NW>
+__device__ __forceinline__ double block_sum_f64(double v, double* red)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum_f64(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double w = lane < NW ? red[lane] : 0.0;
+        w = warp_sum_f64(w);
+        if (lane == 0) red[NW] = w;
+    }
+    __syncthreads();
+    const double r = red[NW];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ float face_lambda(unsigned p, unsigned q, float ff, float fs, float ss)
+{
+    // p, q ∈ {0 slow, 1 fast, 2 outside the domain}
+    if (p > 1u || q > 1u) return 0.f;
+    return (p & q) ? ff : ((p | q) ? fs : ss);
+}
+
+template <int R>
+__global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a)
+{
+    using S = KgenShape<R>;
+    constexpr int L = S::L, LL = S::LL, LLL = S::LLL, NT = S::NT;
+    constexpr int KC = LLL / 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* buf = reinterpret_cast<float*>(smem_raw);
+    unsigned char* ph = smem_raw + S::smem_floats * 4;
+    double* red = reinterpret_cast<double*>(smem_raw + S::smem_floats * 4 + ((LLL + 15) / 16) * 16);
+
+    const int t = threadIdx.x;
+    const bool col = t < LL;
+    const int cx = t % L, cy = t / L;
+    const int oxm = (col && cx > 0) ? -1 : 0, oxp = (col && cx < L - 1) ? 1 : 0;
+    const int oym = (col && cy > 0) ? -L : 0, oyp = (col && cy < L - 1) ? L : 0;
+    const int nx = a.nx, ny = a.ny, nz = a.nz;
+    const long nsrc = (long)nx * ny * (a.sz1 - a.sz0);
+
+    for (long src = blockIdx.x; src < nsrc; src += gridDim.x) {
+        const int sx = (int)(src % nx);
+        const int sy = (int)((src / nx) % ny);
+        const int sz = a.sz0 + (int)(src / ((long)nx * ny));
+
+        // window phases → smem (2 = outside the domain)
+        for (int i = t; i < LLL; i += NT) {
+            const int gx = sx + i % L - R, gy = sy + (i / L) % L - R, gz = sz + i / LL - R;
+            const bool in = gx >= 0 && gx < nx && gy >= 0 && gy < ny && gz >= 0 && gz < nz;
+            ph[i] = in ? a.mask[((size_t)(gz - a.mz0) * ny + gy) * nx + gx] : (unsigned char)2;
+        }
+        __syncthreads();
+
+        float c[L], lxm[L], lxp[L], lym[L], lyp[L], lzp[L];
+#pragma unroll
+        for (int z = 0; z < L; ++z) {
+            const int i = z * LL + t;
+            const unsigned p = col ? ph[i] : 2u;
+            lxm[z] = col ? face_lambda(p, ph[i + oxm], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+            lxp[z] = col ? face_lambda(p, ph[i + oxp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+            lym[z] = col ? face_lambda(p, ph[i + oym], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+            lyp[z] = col ? face_lambda(p, ph[i + oyp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+            lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+            if (oxm == 0) lxm[z] = 0.f;  // no neighbour inside the window: no flux
+            if (oxp == 0) lxp[z] = 0.f;
+            if (oym == 0) lym[z] = 0.f;
+            if (oyp == 0) lyp[z] = 0.f;
+            c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
+        }
+
+        // n_fd Jacobi substeps; faces summed −x,+x,−y,+y,−z,+z
+        for (int k = 0; k < a.n_fd; ++k) {
+            float* b = buf + (k & 1) * (L * LL);
+            if (col) {
+#pragma unroll
+                for (int z = 0; z < L; ++z) b[z * LL + t] = c[z];
+            }
+            __syncthreads();
+            if (col) {
+                float prev = 0.f;
+#pragma unroll
+                for (int z = 0; z < L; ++z) {
+                    const float* bz = b + z * LL + t;
+                    const float cz = c[z];
+                    float acc = cz;
+                    acc = fmaf(lxm[z], bz[oxm] - cz, acc);
+                    acc = fmaf(lxp[z], bz[oxp] - cz, acc);
+                    acc = fmaf(lym[z], bz[oym] - cz, acc);
+                    acc = fmaf(lyp[z], bz[oyp] - cz, acc);
+                    if (z > 0) acc = fmaf(lzp[z - 1], prev - cz, acc);
+                    if (z < L - 1) acc = fmaf(lzp[z], c[z + 1] - cz, acc);
+                    prev = cz;
+                    c[z] = acc;
+                }
+            }
+        }
+
+        // ---- epilogue (a4) ----
+        double s = 0.0;
+        if (col) {
+#pragma unroll
+            for (int z = 0; z < L; ++z) s += (double)c[z];
+        }
+        const double S_ = block_sum_f64<S::NW>(s, red);
+        const double inv = 1.0 / S_;
+        double qsum = 0.0;
+        float centre_q = 0.f;
+        if (col) {
+            const int ox = cx - R, oy = cy - R;
+            const int gx = sx + ox, gy = sy + oy;
+#pragma unroll
+            for (int z = 0; z < L; ++z) {
+                const int o = z * LL + t;
+                const int oz = z - R, gz = sz + oz;
+                const bool active = ph[o] <= 1;
+                const float wf = (float)((double)c[z] * inv);
+                float qd;
+                unsigned short bits = 0;
+                if (a.fmt == 1) {
+                    const __half h = __float2half_rn(wf);
+                    bits = __half_as_ushort(h);
+                    qd = __half2float(h);
+                } else if (a.fmt == 2) {
+                    const __nv_bfloat16 h = __float2bfloat16_rn(wf);
+                    bits = __bfloat16_as_ushort(h);
+                    qd = __bfloat162float(h);
+                } else {
+                    qd = wf;
+                }
+                if (o == KC) {
+                    centre_q = qd;
+                    continue;
+                }
+                if (!active) continue;
+                qsum += (double)qd;
+                if (gz < a.z0 || gz >= a.z1) continue;
+                const int zl = gz - a.z0;
+                const int q = gy * a.nxq + (gx >> 3);
+                const size_t tile = (size_t)zl * a.tpp + q / a.tile;
+                const int e = q % a.tile, j = gx & 7;
+                const size_t idx = ((tile * (size_t)(a.K - 1) + slot_of(ox, oy, oz, R)) * a.tile + e) * 8 + j;
+                if (a.fmt == 0) reinterpret_cast<float*>(a.Wt)[idx] = wf;
+                else reinterpret_cast<unsigned short*>(a.Wt)[idx] = bits;
+            }
+        }
+        const double off = block_sum_f64<S::NW>(qsum, red);
+        if (t == R * L + R && sz >= a.z0 && sz < a.z1) {
+            const float d = a.mass_fix ? (float)(1.0 - off) : centre_q;
+            const int zl = sz - a.z0;
+            const int q = sy * a.nxq + (sx >> 3);
+            const size_t tile = (size_t)zl * a.tpp + q / a.tile;
+            a.diag[(tile * a.tile + q % a.tile) * 8 + (sx & 7)] = d;
+        }
+        // (the block_sum barriers separate this source's smem use from the next one's)
+    }
+}
+
+template <int R>
+static cudaError_t launch_kgen_r(const KgenArgs& a, cudaStream_t s)
+{
+    using S = KgenShape<R>;
+    const long nsrc = (long)a.nx * a.ny * (a.sz1 - a.sz0);
+    if (nsrc <= 0) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kgen_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)S::smem_bytes);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_kernel<R>, S::NT, S::smem_bytes);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    long grid = (long)sms * per_sm;
+    if (grid > nsrc) grid = nsrc;
+    kgen_kernel<R><<<(unsigned)grid, S::NT, S::smem_bytes, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s)
+{
+    switch (R) {
+        case 1: return launch_kgen_r<1>(a, s);
+        case 2: return launch_kgen_r<2>(a, s);
+        case 3: return launch_kgen_r<3>(a, s);
+        case 4: return launch_kgen_r<4>(a, s);
+        case 5: return launch_kgen_r<5>(a, s);
+        case 6: return launch_kgen_r<6>(a, s);
+        case 7: return launch_kgen_r<7>(a, s);
+        case 8: return launch_kgen_r<8>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace fdirw

@@ -1,0 +1,316 @@
+// superpose.cu — a5: the FDiRW superposition step in gather form, plus the small
+// state kernels (pack/unpack of the padded state, fp64 mass reduction, kernel export).
+//
+//   C_new(x) = d_x·C_old(x) + Σ_{o≠0} Wt[o][x]·C_old(x − o)
+//
+// = P:101 Eq.8 / P:131 Eq.14 with the per-source kernels W_s(o) = p_{s+o,s}
+// read in gather order (closed domain: no p_BC term, reading A3).
+// Weights are fp32/fp16/bf16 (§3.3; reading A9: reduced-precision
+// storage, fp32 products and accumulation).
+//
+// B200 mapping: HBM-bound weight streaming.
+//  * one thread = 8 consecutive x targets of one row; one CTA = one tile of
+//    `tile` such chunks; the tile's weights for one slot are `tile`·8 contiguous
+//    values, so a warp reads 512 B (bf16) per slot with 128-bit loads, and the
+//    whole tile streams one contiguous (K−1)·tile·8·b_w region;
+//  * weights: ld.global.nc.L1::no_allocate + L2 evict_first policy (read once);
+//  * C_old: the padded state (zero halo of R planes/rows, 8 columns), read with
+//    128-bit L1-cached loads: per (oz, oy) row a thread loads the aligned
+//    24-float segment [x−8, x+16) once and reuses it for all 2R+1 x-offsets
+//    × 8 targets (register blocking: 6 loads per 8·(2R+1) FMAs);
+//  * bf16 → fp32 is a shift/mask, fp16 → fp32 a cvt; accumulation fp32 FMA in a
+//    fixed order (diag, centre row, rows (oz, oy) ascending), so the result is
+//    bitwise independent of the slab decomposition.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "fdirw_internal.h"
+#include "layout.cuh"
+
+namespace fdirw {
+
+__device__ __forceinline__ uint64_t evict_first_policy()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const void* ptr, uint64_t pol)
+{
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ float4 ld_c(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+template <typename WT>
+struct WLoad;
+
+template <>
+struct WLoad<float> {
+    static __device__ __forceinline__ void load(const float* p, uint64_t pol, float w[8])
+    {
+        const uint4 a = ld_stream(p, pol), b = ld_stream(p + 4, pol);
+        w[0] = __uint_as_float(a.x); w[1] = __uint_as_float(a.y); w[2] = __uint_as_float(a.z); w[3] = __uint_as_float(a.w);
+        w[4] = __uint_as_float(b.x); w[5] = __uint_as_float(b.y); w[6] = __uint_as_float(b.z); w[7] = __uint_as_float(b.w);
+    }
+};
+
+template <>
+struct WLoad<__nv_bfloat16> {
+    static __device__ __forceinline__ void load(const __nv_bfloat16* p, uint64_t pol, float w[8])
+    {
+        const uint4 a = ld_stream(p, pol);
+        const unsigned u[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            w[2 * i] = __uint_as_float(u[i] << 16);
+            w[2 * i + 1] = __uint_as_float(u[i] & 0xffff0000u);
+        }
+    }
+};
+
+template <>
+struct WLoad<__half> {
+    static __device__ __forceinline__ void load(const __half* p, uint64_t pol, float w[8])
+    {
+        const uint4 a = ld_stream(p, pol);
+        const unsigned u[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u[i]));
+            w[2 * i] = f.x;
+            w[2 * i + 1] = f.y;
+        }
+    }
+};
+
+// One (oz, oy) row: 2R+1 x-offsets (all of them, or all but the centre).
+template <int R, typename WT, bool CENTRE_ROW>
+__device__ __forceinline__ void do_row(const float* srow, const WT* wp, size_t wstride, uint64_t pol, float acc[8])
+{
+    float seg[24];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const float4 v = ld_c(srow + 4 * i);
+        seg[4 * i] = v.x; seg[4 * i + 1] = v.y; seg[4 * i + 2] = v.z; seg[4 * i + 3] = v.w;
+    }
+    float w[2 * R + 1][8];
+#pragma unroll
+    for (int ox = -R; ox <= R; ++ox) {
+        if (CENTRE_ROW && ox == 0) continue;
+        const int k = CENTRE_ROW ? (ox < 0 ? ox + R : ox + R - 1) : ox + R;
+        WLoad<WT>::load(wp + (size_t)k * wstride, pol, w[ox + R]);
+    }
+#pragma unroll
+    for (int ox = -R; ox <= R; ++ox) {
+        if (CENTRE_ROW && ox == 0) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(w[ox + R][j], seg[j - ox + 8], acc[j]);
+    }
+}
+
+template <int R, typename WT>
+__global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
+{
+    constexpr int L = 2 * R + 1, K = L * L * L;
+    const int tile = a.t_begin + blockIdx.x;
+    const int zl = tile / a.tpp, tp = tile % a.tpp;
+    const int e = threadIdx.x;
+    const int q = tp * a.tile + e;
+    if (q >= a.ny * a.nxq) return;  // dummy chunk at the end of the plane
+    const int y = q / a.nxq, x = (q % a.nxq) * 8;
+    const long nxp = a.nxp, plane = (long)a.nyp * nxp;
+    const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;  // C_old(z, y, x)
+    const size_t wstride = (size_t)a.tile * 8;
+    const WT* wt = reinterpret_cast<const WT*>(a.Wt) + ((size_t)tile * (K - 1) * a.tile + e) * 8;
+    const float* dp = a.diag + ((size_t)tile * a.tile + e) * 8;
+    const uint64_t pol = evict_first_policy();
+
+    float acc[8];
+    {
+        const float4 d0 = __ldg(reinterpret_cast<const float4*>(dp));
+        const float4 d1 = __ldg(reinterpret_cast<const float4*>(dp + 4));
+        const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
+        acc[0] = d0.x * v0.x; acc[1] = d0.y * v0.y; acc[2] = d0.z * v0.z; acc[3] = d0.w * v0.w;
+        acc[4] = d1.x * v1.x; acc[5] = d1.y * v1.y; acc[6] = d1.z * v1.z; acc[7] = d1.w * v1.w;
+    }
+    // centre row (oz = oy = 0): slots [0, L−1)
+    do_row<R, WT, true>(c0 - 8, wt, wstride, pol, acc);
+    // remaining rows, ascending (oz, oy); source row of target row (z, y) is (z − oz, y − oy)
+    const WT* wr = wt + (size_t)(L - 1) * wstride;
+#pragma unroll 1
+    for (int r = 0; r < L * L; ++r) {
+        if (r == R * L + R) continue;
+        const int oz = r / L - R, oy = r % L - R;
+        const float* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
+        do_row<R, WT, false>(srow, wr, wstride, pol, acc);
+        wr += (size_t)L * wstride;
+    }
+
+    float* out = a.out + (long)zl * a.out_ps + (long)y * a.out_rs + x;
+    if (x + 8 <= a.nx && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (x + j < a.nx) out[j] = acc[j];
+    }
+}
+
+template <int R>
+static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t s)
+{
+    const int nblk = a.t_end - a.t_begin;
+    if (nblk <= 0) return cudaSuccess;
+    if (fmt == 0) superpose_kernel<R, float><<<nblk, a.tile, 0, s>>>(a);
+    else if (fmt == 1) superpose_kernel<R, __half><<<nblk, a.tile, 0, s>>>(a);
+    else superpose_kernel<R, __nv_bfloat16><<<nblk, a.tile, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s)
+{
+    switch (R) {
+        case 1: return launch_superpose_r<1>(a, fmt, s);
+        case 2: return launch_superpose_r<2>(a, fmt, s);
+        case 3: return launch_superpose_r<3>(a, fmt, s);
+        case 4: return launch_superpose_r<4>(a, fmt, s);
+        case 5: return launch_superpose_r<5>(a, fmt, s);
+        case 6: return launch_superpose_r<6>(a, fmt, s);
+        case 7: return launch_superpose_r<7>(a, fmt, s);
+        case 8: return launch_superpose_r<8>(a, fmt, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// ---- state kernels ------------------------------------------------------------------
+__global__ void pack_kernel(const float* __restrict__ c, float* __restrict__ cpad, int nx, int ny, long n,
+                            int R, int nxp, int nyp)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx);
+        const long r = i / nx;
+        const int y = (int)(r % ny);
+        const long z = r / ny;
+        cpad[((z + R) * nyp + (y + R)) * (long)nxp + kPadX + x] = c[i];
+    }
+}
+
+__global__ void unpack_kernel(const float* __restrict__ cpad, float* __restrict__ c, int nx, int ny, long n,
+                              int R, int nxp, int nyp)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx);
+        const long r = i / nx;
+        const int y = (int)(r % ny);
+        const long z = r / ny;
+        c[i] = cpad[((z + R) * nyp + (y + R)) * (long)nxp + kPadX + x];
+    }
+}
+
+static unsigned grid_for(long n, int threads)
+{
+    long b = (n + threads - 1) / threads;
+    if (b > 148L * 16) b = 148L * 16;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStream_t s)
+{
+    const long n = (long)g.nx * g.ny * g.nzl;
+    if (n == 0) return cudaSuccess;
+    pack_kernel<<<grid_for(n, 256), 256, 0, s>>>(c, cpad, g.nx, g.ny, n, g.R, g.nxp, g.nyp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const float* cpad, float* c, const Geometry& g, cudaStream_t s)
+{
+    const long n = (long)g.nx * g.ny * g.nzl;
+    if (n == 0) return cudaSuccess;
+    unpack_kernel<<<grid_for(n, 256), 256, 0, s>>>(cpad, c, g.nx, g.ny, n, g.R, g.nxp, g.nyp);
+    return cudaGetLastError();
+}
+
+// fp64 sum, two passes with a fixed order (deterministic).
+__global__ void mass_partial_kernel(const float* __restrict__ c, size_t n, double* __restrict__ partial)
+{
+    __shared__ double red[32];
+    double v = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        v += (double)c[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) partial[blockIdx.x] = v;
+    }
+}
+
+__global__ void mass_final_kernel(const double* __restrict__ partial, int n, double* __restrict__ out)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double v = 0.0;
+        for (int i = 0; i < n; ++i) v += partial[i];
+        *out = v;
+    }
+}
+
+cudaError_t launch_mass(const float* c, size_t n, double* partial, int nblk, double* out, cudaStream_t s)
+{
+    mass_partial_kernel<<<nblk, 256, 0, s>>>(c, n, partial);
+    mass_final_kernel<<<1, 32, 0, s>>>(partial, nblk, out);
+    return cudaGetLastError();
+}
+
+// Decode the stored kernels of the sources in `box` back to per-source fp64 arrays.
+__global__ void export_kernel(const void* __restrict__ Wt, const float* __restrict__ diag, Geometry g, int fmt,
+                              int bx0, int bx, int by0, int by, int bz0, int bz, double* __restrict__ out)
+{
+    const long total = (long)bx * by * bz * g.K;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const int o = (int)(i % g.K);
+        const long n = i / g.K;
+        const int sx = bx0 + (int)(n % bx), sy = by0 + (int)((n / bx) % by), sz = bz0 + (int)(n / ((long)bx * by));
+        const int ox = o % g.L - g.R, oy = (o / g.L) % g.L - g.R, oz = o / (g.L * g.L) - g.R;
+        const int x = sx + ox, y = sy + oy, z = sz + oz;
+        double v = 0.0;
+        if (x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= g.z0 && z < g.z1 && sx >= 0 && sx < g.nx &&
+            sy >= 0 && sy < g.ny && sz >= 0 && sz < g.nz) {
+            const int q = y * g.nxq + (x >> 3);
+            const size_t tile = (size_t)(z - g.z0) * g.tpp + q / g.tile;
+            const int e = q % g.tile, j = x & 7;
+            if (o == g.K / 2) {
+                v = diag[(tile * g.tile + e) * 8 + j];
+            } else {
+                const size_t idx = ((tile * (size_t)(g.K - 1) + slot_of(ox, oy, oz, g.R)) * g.tile + e) * 8 + j;
+                if (fmt == 0) v = reinterpret_cast<const float*>(Wt)[idx];
+                else if (fmt == 1) v = __half2float(reinterpret_cast<const __half*>(Wt)[idx]);
+                else v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(Wt)[idx]);
+            }
+        }
+        out[i] = v;
+    }
+}
+
+cudaError_t launch_export(const void* Wt, const float* diag, const Geometry& g, int fmt, const int32_t* box,
+                          double* out, cudaStream_t s)
+{
+    const int bx = box[1] - box[0], by = box[3] - box[2], bz = box[5] - box[4];
+    const long total = (long)bx * by * bz * g.K;
+    if (total <= 0) return cudaSuccess;
+    export_kernel<<<grid_for(total, 256), 256, 0, s>>>(Wt, diag, g, fmt, box[0], bx, box[2], by, box[4], bz, out);
+    return cudaGetLastError();
+}
+
+}  // namespace fdirw

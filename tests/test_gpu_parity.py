@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU fp64 oracle on the
+same seeded inputs.  Tolerances from north_star: fp32 relL2 ≤ 1e-5,
+fp16/bf16 relL2 ≤ 5e-3, total mass ≤ 1e-6 relative; the superposition alone on the
+oracle's own quantised weights ≤ 1e-6 (only fp32 accumulation order differs)."""
+import numpy as np
+import pytest
+
+import fdirw_inputs as fi
+from _util import lib_params, oracle_problem, rel_l2, small_cfg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2408_11376_b200 import build as b
+
+    b.build()
+    import paper_2408_11376_b200 as fd
+
+    return fd
+
+
+def _gpu_steps(fd, cfg, mask, c0, steps, weights=None, flags=0, use_run=True):
+    import torch
+
+    ctx = fd.build_kernels(lib_params(cfg, weights, flags), mask)
+    try:
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        m0 = fd.mass(ctx, c)
+        if use_run:
+            fd.run(ctx, c, steps)
+        else:
+            out = torch.empty_like(c)
+            for _ in range(steps):
+                fd.step(ctx, c, out)
+                c, out = out, c
+        m1 = fd.mass(ctx, c)
+        torch.cuda.synchronize()
+        return c.cpu().numpy().astype(np.float64), m0, m1, ctx.info
+    finally:
+        fd.destroy(ctx)
+
+
+# ------------------------------------------------------------------ cfg1 (16³, R2)
+@pytest.mark.parametrize("n_fd", [2, 1000])
+def test_cfg1_fp32_10_steps(fd, oracle_lib, n_fd):
+    """BASELINE configs[0]: 16³ two-phase porous grid, D ratio 1e3, R2, fp32, 10 steps,
+    exact (n_fd = 2 ≤ R) and truncated (n_fd = 1000) regimes."""
+    cfg = fi.config("cfg1", n_fd=n_fd, weights="fp32")
+    mask = cfg.mask()
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=1)
+    ref = oracle_lib.step_full(pb, c0.astype(np.float64), steps=10)
+    got, m0, m1, info = _gpu_steps(fd, cfg, mask, c0, 10)
+    assert info["n_fd"] == n_fd
+    assert rel_l2(got, ref) <= 1e-5
+    assert abs(m1 - m0) / abs(m0) <= 1e-6
+    assert abs(got.sum() - c0.astype(np.float64).sum()) / c0.sum() <= 1e-6
+    if n_fd == 2:  # P1 on the GPU: == 20 whole-grid FD substeps
+        fdref = oracle_lib.fd_whole_grid(pb, c0.astype(np.float64), 20)
+        assert rel_l2(got, fdref) <= 1e-5
+
+
+@pytest.mark.parametrize("fmt", ["fp32", "fp16", "bf16"])
+def test_kgen_matches_oracle_kernels(fd, oracle_lib, fmt):
+    """a3/a4 in isolation: the stored kernels (export) vs the oracle's quantised kernels (O5)."""
+    cfg = fi.config("cfg1", n_fd=1000, weights=fmt)
+    mask = cfg.mask()
+    pb = oracle_problem(cfg, mask)
+    Wo = oracle_lib.quantize(pb, oracle_lib.build_kernels(pb), fmt)
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        Wg = fd.export_kernels(ctx, (0, 16, 0, 16, 0, 16))
+    finally:
+        fd.destroy(ctx)
+    ulp = {"fp32": 2e-6, "fp16": 2.0 ** -10, "bf16": 2.0 ** -7}[fmt]
+    # off-centre: equal up to one storage ulp (the GPU's fp32 FD may round differently)
+    c = pb.K // 2
+    off = np.ones(pb.K, bool)
+    off[c] = False
+    err = np.abs(Wg[..., off] - Wo[..., off])
+    assert np.all(err <= ulp * np.maximum(np.abs(Wo[..., off]), 1e-30) + 1e-7)
+    np.testing.assert_allclose(Wg.sum(-1), 1.0, atol=3e-7)  # mass fix-up: every column sums to 1
+    assert np.all(Wg >= 0)
+
+
+@pytest.mark.parametrize("fmt", ["fp32", "fp16", "bf16"])
+def test_superposition_on_oracle_weights(fd, oracle_lib, fmt):
+    """a5 in isolation: upload the oracle's O5 weights, one GPU step vs the oracle's fp64 scatter."""
+    import torch
+
+    cfg = small_cfg((13, 17, 21), 3, 40, D_slow=1e-3, weights=fmt)  # ragged: nx % 8 != 0
+    mask = fi.random_two_phase(cfg.shape, 0.6, seed=5)
+    pb = oracle_problem(cfg, mask)
+    Wq = oracle_lib.quantize(pb, oracle_lib.build_kernels(pb), fmt)
+    c0 = fi.initial_c(mask, "random", seed=5)
+    ref = oracle_lib.step_scatter(pb, Wq, (0, 21, 0, 17, 0, 13), c0.astype(np.float64), (0, 21, 0, 17, 0, 13))
+    ctx = fd.build_kernels(lib_params(cfg, fmt), mask)
+    try:
+        fd.debug_upload_weights(ctx, Wq)
+        cin = torch.from_numpy(c0).cuda()
+        out = torch.empty_like(cin)
+        fd.step(ctx, cin, out)
+        got = out.cpu().numpy()
+    finally:
+        fd.destroy(ctx)
+    assert rel_l2(got, ref) <= 1e-6
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("shape,R,n_fd,fmt", [
+    ((7, 9, 13), 3, 50, "fp32"),      # ragged, several tiles per plane
+    ((1, 1, 37), 4, 9, "fp32"),       # 1-D grid
+    ((5, 3, 4), 1, 1, "fp32"),        # tiny, R = 1, one substep
+    ((6, 5, 9), 2, 300, "bf16"),
+    ((4, 12, 19), 5, 60, "fp16"),     # window larger than the domain in z
+    ((3, 3, 3), 8, 30, "bf16"),       # R = 8 > every dimension (P2 regime)
+])
+def test_edge_shapes(fd, oracle_lib, shape, R, n_fd, fmt):
+    cfg = small_cfg(shape, R, n_fd, D_slow=2e-3, weights=fmt)
+    mask = fi.random_two_phase(shape, 0.55, seed=R + n_fd)
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=3)
+    ref = oracle_lib.step_full(pb, c0.astype(np.float64), steps=3)
+    got, m0, m1, _ = _gpu_steps(fd, cfg, mask, c0, 3)
+    tol = 1e-5 if fmt == "fp32" else 5e-3
+    assert rel_l2(got, ref) <= tol
+    assert abs(m1 - m0) / m0 <= 1e-6
+
+
+def test_impermeable_and_no_mass_fix(fd, oracle_lib):
+    """D_slow = 0 (reading A23) and FDIRW_F_NO_MASS_FIX reproduce the oracle's variants."""
+    cfg = small_cfg((8, 8, 8), 2, 30, D_slow=0.0, weights="bf16")
+    mask = fi.random_two_phase(cfg.shape, 0.5, seed=2)
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=2)
+    ref = oracle_lib.step_full(pb, c0.astype(np.float64), steps=2)
+    got, m0, m1, _ = _gpu_steps(fd, cfg, mask, c0, 2)
+    assert rel_l2(got, ref) <= 5e-3
+    np.testing.assert_allclose(got[mask == 0], c0[mask == 0], rtol=1e-6)  # slow voxels keep their mass
+    refq = oracle_lib.step_full(pb, c0.astype(np.float64), steps=1, fmt="bf16", mass_fix=False)
+    got2, _, _, _ = _gpu_steps(fd, cfg, mask, c0, 1, flags=1)
+    assert rel_l2(got2, refq) <= 1e-4
+
+
+def test_step_equals_run(fd):
+    """fdirw_run (CUDA graph, padded ping-pong) is bitwise fdirw_step repeated."""
+    cfg = small_cfg((12, 10, 11), 2, 20, weights="bf16")
+    mask = fi.random_two_phase(cfg.shape, 0.6, seed=1)
+    c0 = fi.initial_c(mask, "random", seed=1)
+    a, _, _, _ = _gpu_steps(fd, cfg, mask, c0, 5, use_run=True)
+    b, _, _, _ = _gpu_steps(fd, cfg, mask, c0, 5, use_run=False)
+    np.testing.assert_array_equal(a, b)
+
+
+# ------------------------------------------------------------------ cfg2 (64³, R4), sampled boxes
+@pytest.mark.parametrize("fmt", ["fp32", "bf16"])
+def test_cfg2_boxes(fd, oracle_lib, fmt):
+    """BASELINE configs[1]: 64³ porous waste-form block, D ratio 1e5, R4, n_fd = 1000;
+    one full-grid GPU step compared on target boxes (corner, ragged interior, far corner)."""
+    import torch
+
+    cfg = fi.config("cfg2", weights=fmt)
+    mask = cfg.mask()
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "paper")
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        c = torch.from_numpy(c0).cuda()
+        m0 = fd.mass(ctx, c)
+        fd.run(ctx, c, 1)
+        m1 = fd.mass(ctx, c)
+        got = c.cpu().numpy()
+    finally:
+        fd.destroy(ctx)
+    assert abs(m1 - m0) / m0 <= 1e-6
+    tol = 1e-5 if fmt == "fp32" else 5e-3
+    for tb in [(0, 9, 0, 8, 0, 7), (27, 38, 30, 37, 20, 29), (57, 64, 58, 64, 60, 64)]:
+        ref = oracle_lib.step_box(pb, c0.astype(np.float64), tb)
+        assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= tol, tb
+
+
+# ------------------------------------------------------------------ cfg3 (192³, R5) — bench launch config
+def test_cfg3_bench_config_sampled(fd, oracle_lib):
+    """BASELINE configs[2] at full size in bench.py's launch configuration (fdirw_run):
+    192³ R50 particle, Table 1 SI parameters (n_fd = 1000), R5, bf16 weights.  Sampled
+    target boxes vs the oracle; total mass over the whole grid."""
+    import torch
+
+    cfg = fi.config("cfg3")
+    mask = cfg.mask()
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "paper")
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        assert ctx.info["n_fd"] == 1000
+        c = torch.from_numpy(c0).cuda()
+        m0 = fd.mass(ctx, c)
+        fd.run(ctx, c, 1)
+        m1 = fd.mass(ctx, c)
+        got = c.cpu().numpy()
+    finally:
+        fd.destroy(ctx)
+    assert abs(m1 - m0) / m0 <= 1e-6
+    # a box on the particle surface (r ≈ 50 from the centre) and a ragged one at a domain corner
+    for tb in [(140, 146, 92, 98, 92, 97), (0, 5, 185, 192, 0, 3)]:
+        ref = oracle_lib.step_box(pb, c0.astype(np.float64), tb)
+        assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= 5e-3, tb
+
+
+# ------------------------------------------------------------------ slabs (virtual ranks)
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_virtual_ranks_bitwise(fd, world):
+    """P13: the slab decomposition with R-plane halos reproduces the 1-GPU result bitwise
+    (thin slabs: thickness ≥ R, interior/boundary split exercised)."""
+    import torch
+
+    cfg = small_cfg((4 * 3, 11, 13), 3, 25, weights="bf16")
+    mask = fi.random_two_phase(cfg.shape, 0.6, seed=world)
+    c0 = fi.initial_c(mask, "random", seed=world)
+    one, _, _, _ = _gpu_steps(fd, cfg, mask, c0, 1, use_run=False)
+    nz = cfg.shape[0]
+    sl = fd.slabs(nz, world)
+    ctxs = [fd.build_kernels(lib_params(cfg), mask, rank=r, world=world, z_begin=a, z_end=b, device=0)
+            for r, (a, b) in enumerate(sl)]
+    try:
+        cin = [torch.from_numpy(c0[a:b].copy()).cuda() for a, b in sl]
+        cout = [torch.empty_like(t) for t in cin]
+        fd.step_virtual(ctxs, cin, cout)
+        got = np.concatenate([t.cpu().numpy() for t in cout], axis=0)
+    finally:
+        for c in ctxs:
+            fd.destroy(c)
+    np.testing.assert_array_equal(got, one.astype(np.float32))
+
+
+def test_errors(fd):
+    import torch
+
+    cfg = small_cfg((4, 4, 4), 1, 2)
+    mask = np.ones(cfg.shape, np.uint8)
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        c = torch.zeros(cfg.shape, device="cuda")
+        with pytest.raises(fd.FdirwError) as e:
+            fd.step(ctx, c, c)
+        assert e.value.status == fd.E_ALIAS
+    finally:
+        fd.destroy(ctx)

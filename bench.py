@@ -171,6 +171,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _ncu_traffic(cfg, bytes_per_launch):
+    """dram read+write bytes per launch of the superposition kernel from the newest committed
+    `ncu --set full` capture of this config (profiles/r*_superpose_<cfg>_ncu.json), else None."""
+    import glob
+
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_superpose_%s_ncu.json" % cfg.name))):
+        try:
+            js = json.load(open(f))
+            for rec in js.get("launches", []):
+                if "superpose" in rec.get("kernel", "") and rec.get("traffic_bytes"):
+                    best = (rec["traffic_bytes"], os.path.relpath(f, ROOT))
+        except Exception:
+            pass
+    return best
+
+
 def _workload_name(cfg):
     return "%s: %s grid, R=%d (K=%d), %s weights, n_fd=%s" % (
         cfg.name, "x".join(map(str, cfg.shape[::-1])), cfg.R, cfg.K,
@@ -307,11 +324,18 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(c.numel() * 4 * world),
                 "d2h_bytes_per_step": int(c.numel() * 4 * world), "api": "fdirw_step with pinned host copies"},
         "gpu_launches": (args.steps * launches_per_step + 2) * world,
+        "paper_run": {"steps": 1000, "physical_time_s": 1000 * cfg.dt if cfg.dh != 1.0 else None,
+                      "seconds_incl_kgen": t_kgen + 1000 * ms_step * 1e-3,
+                      "note": "t = 0.5 s of Fig.7 (1000 macro steps) incl. the one-time kernel build"},
         "kgen": {"seconds": t_kgen, "window_cell_updates": kgen_cells * world,
                  "cell_updates_per_s": kgen_cells * world / t_kgen, "n_fd": info["n_fd"]},
         "mass_rel_err": abs(m1 - m0) / abs(m0) if m0 else None,
         "clocks": clk.summary(),
     }
+    tr = _ncu_traffic(cfg, per_launch_bytes) if world == 1 else None
+    if tr:
+        line["roofline"]["traffic"] = tr[0]
+        line["roofline"]["traffic_source"] = tr[1] + " (ncu --set full, one launch)"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, mask)
     fd.destroy(ctx)

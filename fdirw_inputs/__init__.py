@@ -154,6 +154,10 @@ class Config:
     n_fd: int = 0
     geometry: dict = field(default_factory=dict)
 
+    @property
+    def K(self) -> int:
+        return (2 * self.R + 1) ** 3
+
     def mask(self) -> np.ndarray:
         g = dict(self.geometry)
         kind = g.pop("kind")

@@ -105,6 +105,28 @@ typedef struct {
     int32_t n_tiles;        /* tiles in this slab                                              */
 } fdirw_info;
 
+/* Host-only decomposition plan of one rank (no CUDA call; usable without a GPU).
+ * Offsets index the padded fp32 state [padded_z][padded_y][padded_x] whose voxel
+ * (x, y, z) sits at ((z − z_begin + R)·padded_y + (y + R))·padded_x + pad_x0 + x.
+ * The halo exchange of a6 moves halo_elems contiguous elements per message:
+ * [send_lo, +halo_elems) → peer_lo's [recv_hi, …), [send_hi, …) → peer_hi's [recv_lo, …). */
+typedef struct {
+    int32_t z_begin, z_end;             /* target slab                                          */
+    int32_t src_z_begin, src_z_end;     /* source planes whose windows reach the slab (kgen)    */
+    int32_t mask_z_begin, mask_z_end;   /* mask planes copied to the device                     */
+    int32_t tile_chunks, tiles_per_plane, n_tiles;
+    int32_t interior_tile_begin, interior_tile_end; /* tiles that read no halo plane            */
+    int32_t peer_lo, peer_hi;           /* neighbour ranks, −1 if none                          */
+    int32_t n_fd;
+    int64_t padded_x, padded_y, padded_z, pad_x0;
+    int64_t halo_elems;
+    int64_t send_lo, recv_lo, send_hi, recv_hi; /* element offsets, −1 if no peer            */
+    uint64_t weight_bytes, state_bytes; /* device bytes the context will allocate            */
+} fdirw_plan;
+
+/* Validates exactly like fdirw_build_kernels and fills *plan.  Host only. */
+fdirw_status fdirw_make_plan(const fdirw_params* params, const fdirw_dist* dist, fdirw_plan* plan);
+
 /* Writes a fresh 128-byte ncclUniqueId to out128 (host).  Call on rank 0 only.
  * FDIRW_E_NCCL if libnccl.so.2 cannot be loaded. */
 fdirw_status fdirw_nccl_unique_id(void* out128);

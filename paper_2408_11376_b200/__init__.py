@@ -31,7 +31,7 @@ STATUS_NAMES = ["OK", "E_INVALID", "E_UNSTABLE", "E_OOM", "E_CUDA", "E_NCCL", "E
 WEIGHTS = {"fp32": 0, "fp16": 1, "bf16": 2}
 F_NO_MASS_FIX = 1
 
-EXPORTS = ["fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
+EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
            "fdirw_export_kernels", "fdirw_step_virtual"]
 
@@ -57,8 +57,19 @@ class fdirw_info(ctypes.Structure):
                 ("tile_chunks", ctypes.c_int32), ("n_tiles", ctypes.c_int32)]
 
 
+class fdirw_plan(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "z_begin", "z_end", "src_z_begin", "src_z_end", "mask_z_begin", "mask_z_end", "tile_chunks",
+        "tiles_per_plane", "n_tiles", "interior_tile_begin", "interior_tile_end", "peer_lo", "peer_hi", "n_fd")] + \
+        [(n, ctypes.c_int64) for n in ("padded_x", "padded_y", "padded_z", "pad_x0", "halo_elems", "send_lo",
+                                       "recv_lo", "send_hi", "recv_hi")] + \
+        [("weight_bytes", ctypes.c_uint64), ("state_bytes", ctypes.c_uint64)]
+
+
 _vp = ctypes.c_void_p
 _st = ctypes.c_int
+_lib.fdirw_make_plan.argtypes = [ctypes.POINTER(fdirw_params), ctypes.POINTER(fdirw_dist), ctypes.POINTER(fdirw_plan)]
+_lib.fdirw_make_plan.restype = _st
 _lib.fdirw_nccl_unique_id.argtypes = [_vp]
 _lib.fdirw_nccl_unique_id.restype = _st
 _lib.fdirw_build_kernels.argtypes = [ctypes.POINTER(fdirw_params), _vp, ctypes.POINTER(fdirw_dist), _vp,
@@ -152,6 +163,16 @@ class Context:
     @property
     def info(self):
         return query(self)
+
+
+def make_plan(params: Params, rank: int = 0, world: int = 1, z_begin: int | None = None,
+              z_end: int | None = None) -> dict:
+    """fdirw_make_plan: the host-side slab / halo / tile plan of one rank (no GPU needed)."""
+    p = params.c()
+    d = fdirw_dist(rank, world, 0 if z_begin is None else z_begin, params.nz if z_end is None else z_end, 0, None)
+    pl = fdirw_plan()
+    _check(_lib.fdirw_make_plan(ctypes.byref(p), ctypes.byref(d), ctypes.byref(pl)))
+    return {f: getattr(pl, f) for f, _ in fdirw_plan._fields_}
 
 
 def nccl_unique_id() -> bytes:

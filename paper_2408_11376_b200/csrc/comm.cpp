@@ -2,9 +2,8 @@
 //
 // libnccl.so.2 is dlopen'ed (the copy PyTorch already loaded when present), so
 // single-GPU use has no NCCL dependency.  Halo = R whole z-planes of the padded
-// state, contiguous because x is fastest: no packing.
-//   send padded planes [R, 2R)          → rank−1   recv padded [0, R)           ← rank−1
-//   send padded planes [nzl, nzl+R)     → rank+1   recv padded [nzl+R, nzl+2R)  ← rank+1
+// state, contiguous because x is fastest: no packing; the offsets
+// come from make_halo_plan (fdirw_api.cu), the same plan fdirw_make_plan reports.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -92,23 +91,17 @@ void* nccl_comm_init(Nccl* n, int world, int rank, const void* id128, std::strin
     return comm;
 }
 
-int nccl_halo(Nccl* n, void* comm, float* cpad, const Geometry& g, int rank, int world, cudaStream_t s,
-              std::string* err)
+int nccl_halo(Nccl* n, void* comm, float* cpad, const HaloPlan& h, cudaStream_t s, std::string* err)
 {
     ncclComm_t c = static_cast<ncclComm_t>(comm);
-    const size_t cnt = (size_t)g.R * g.plane_elems;
-    float* lo_send = cpad + (size_t)g.R * g.plane_elems;
-    float* lo_recv = cpad;
-    float* hi_send = cpad + (size_t)g.nzl * g.plane_elems;
-    float* hi_recv = cpad + (size_t)(g.nzl + g.R) * g.plane_elems;
     if (check(n, n->GroupStart(), "ncclGroupStart", err)) return 1;
-    if (rank > 0) {
-        if (check(n, n->Send(lo_send, cnt, ncclFloat32, rank - 1, c, s), "ncclSend", err)) return 1;
-        if (check(n, n->Recv(lo_recv, cnt, ncclFloat32, rank - 1, c, s), "ncclRecv", err)) return 1;
+    if (h.peer_lo >= 0) {
+        if (check(n, n->Send(cpad + h.send_lo, h.count, ncclFloat32, h.peer_lo, c, s), "ncclSend", err)) return 1;
+        if (check(n, n->Recv(cpad + h.recv_lo, h.count, ncclFloat32, h.peer_lo, c, s), "ncclRecv", err)) return 1;
     }
-    if (rank < world - 1) {
-        if (check(n, n->Send(hi_send, cnt, ncclFloat32, rank + 1, c, s), "ncclSend", err)) return 1;
-        if (check(n, n->Recv(hi_recv, cnt, ncclFloat32, rank + 1, c, s), "ncclRecv", err)) return 1;
+    if (h.peer_hi >= 0) {
+        if (check(n, n->Send(cpad + h.send_hi, h.count, ncclFloat32, h.peer_hi, c, s), "ncclSend", err)) return 1;
+        if (check(n, n->Recv(cpad + h.recv_hi, h.count, ncclFloat32, h.peer_hi, c, s), "ncclRecv", err)) return 1;
     }
     return check(n, n->GroupEnd(), "ncclGroupEnd", err);
 }

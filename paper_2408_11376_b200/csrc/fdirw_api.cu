@@ -79,6 +79,19 @@ Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1)
     return g;
 }
 
+HaloPlan make_halo_plan(const Geometry& g, int rank, int world)
+{
+    HaloPlan h{};
+    h.count = (long)g.R * (long)g.plane_elems;
+    h.peer_lo = rank > 0 ? rank - 1 : -1;
+    h.peer_hi = rank < world - 1 ? rank + 1 : -1;
+    h.send_lo = h.peer_lo >= 0 ? (long)g.R * (long)g.plane_elems : -1;
+    h.recv_lo = h.peer_lo >= 0 ? 0 : -1;
+    h.send_hi = h.peer_hi >= 0 ? (long)g.nzl * (long)g.plane_elems : -1;
+    h.recv_hi = h.peer_hi >= 0 ? (long)(g.nzl + g.R) * (long)g.plane_elems : -1;
+    return h;
+}
+
 }  // namespace fdirw
 
 // a1: n_fd = ceil(x·(1 − 1e-9)), x = D_max·Δt/(λ*·Δh²), λ* = 0.1 (Table 1, P:84-91;
@@ -326,7 +339,8 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     CUDA_TRY(cudaEventRecord(c->ev_fork, s));
     CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
     std::string err;
-    if (nccl_halo(c->nccl, c->comm, src, g, c->rank, c->world, c->comm_stream, &err)) return fail(FDIRW_E_NCCL, err);
+    if (nccl_halo(c->nccl, c->comm, src, make_halo_plan(g, c->rank, c->world), c->comm_stream, &err))
+        return fail(FDIRW_E_NCCL, err);
     CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
     CUDA_TRY(superpose(c, src, out, ps, rs, i0, i1, s));  // interior overlaps the exchange
     CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
@@ -432,6 +446,39 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
 
 extern "C" void fdirw_destroy(fdirw_ctx* c) { free_ctx(c); }
 
+extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist* dist, fdirw_plan* pl)
+{
+    static const uint8_t dummy = 0;
+    fdirw_ctx* unused = nullptr;
+    fdirw_status st = validate(p, &dummy, dist, &unused);
+    if (st != FDIRW_OK) return st;
+    if (!pl) return fail(FDIRW_E_INVALID, "NULL argument");
+    Derived d;
+    if ((st = derive(*p, &d)) != FDIRW_OK) return st;
+    const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
+    const Geometry g = make_geometry(p->nx, p->ny, p->nz, p->radius, dist ? dist->z_begin : 0,
+                                     dist ? dist->z_end : p->nz);
+    const HaloPlan h = make_halo_plan(g, rank, world);
+    int i0, i1;
+    split_tiles(g, &i0, &i1);
+    const int b_w = p->weights == FDIRW_W_FP32 ? 4 : 2;
+    pl->z_begin = g.z0; pl->z_end = g.z1;
+    pl->src_z_begin = g.sz0; pl->src_z_end = g.sz1;
+    pl->mask_z_begin = g.mz0; pl->mask_z_end = g.mz1;
+    pl->tile_chunks = g.tile; pl->tiles_per_plane = g.tpp; pl->n_tiles = g.n_tiles;
+    pl->interior_tile_begin = world > 1 ? i0 : 0;
+    pl->interior_tile_end = world > 1 ? i1 : g.n_tiles;
+    pl->peer_lo = h.peer_lo; pl->peer_hi = h.peer_hi;
+    pl->padded_x = g.nxp; pl->padded_y = g.nyp; pl->padded_z = g.nzp;
+    pl->pad_x0 = kPadX;
+    pl->halo_elems = h.count;
+    pl->send_lo = h.send_lo; pl->recv_lo = h.recv_lo; pl->send_hi = h.send_hi; pl->recv_hi = h.recv_hi;
+    pl->weight_bytes = (uint64_t)g.w_elems * b_w + (uint64_t)g.diag_elems * 4;
+    pl->state_bytes = (uint64_t)g.state_elems * 8;
+    pl->n_fd = d.n_fd;
+    return FDIRW_OK;
+}
+
 extern "C" const char* fdirw_last_error(void) { return g_err.c_str(); }
 
 extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k)
@@ -507,18 +554,18 @@ extern "C" fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, co
     CUDA_TRY(cudaSetDevice(ctxs[0]->device));
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     for (int r = 0; r < n; ++r) CUDA_TRY(launch_pack(c_in[r], ctxs[r]->cpad[0], ctxs[r]->g, s));
-    // halo planes by device copies: the same planes NCCL would move (comm.cpp)
+    // halo planes by device copies: the planes NCCL would move (same HaloPlan as comm.cpp)
     for (int r = 0; r < n; ++r) {
-        const Geometry& g = ctxs[r]->g;
-        const size_t bytes = (size_t)g.R * g.plane_elems * 4;
-        if (r > 0) {
-            const Geometry& gl = ctxs[r - 1]->g;
-            CUDA_TRY(cudaMemcpyAsync(ctxs[r]->cpad[0], ctxs[r - 1]->cpad[0] + (size_t)gl.nzl * gl.plane_elems, bytes,
+        const HaloPlan h = make_halo_plan(ctxs[r]->g, r, n);
+        const size_t bytes = (size_t)h.count * 4;
+        if (h.peer_lo >= 0) {
+            const HaloPlan hl = make_halo_plan(ctxs[h.peer_lo]->g, h.peer_lo, n);
+            CUDA_TRY(cudaMemcpyAsync(ctxs[r]->cpad[0] + h.recv_lo, ctxs[h.peer_lo]->cpad[0] + hl.send_hi, bytes,
                                      cudaMemcpyDeviceToDevice, s));
         }
-        if (r < n - 1) {
-            CUDA_TRY(cudaMemcpyAsync(ctxs[r]->cpad[0] + (size_t)(g.nzl + g.R) * g.plane_elems,
-                                     ctxs[r + 1]->cpad[0] + (size_t)g.R * g.plane_elems, bytes,
+        if (h.peer_hi >= 0) {
+            const HaloPlan hh = make_halo_plan(ctxs[h.peer_hi]->g, h.peer_hi, n);
+            CUDA_TRY(cudaMemcpyAsync(ctxs[r]->cpad[0] + h.recv_hi, ctxs[h.peer_hi]->cpad[0] + hh.send_lo, bytes,
                                      cudaMemcpyDeviceToDevice, s));
         }
     }

@@ -32,6 +32,16 @@ struct Geometry {
 
 Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1);
 
+// a6: which padded planes move where (element offsets into the padded state; −1 = no peer).
+//   send padded planes [R, 2R)        → rank−1    recv padded [0, R)          ← rank−1
+//   send padded planes [nzl, nzl+R)   → rank+1    recv padded [nzl+R, nzl+2R) ← rank+1
+struct HaloPlan {
+    long count;  // fp32 elements per message (R whole padded planes, contiguous)
+    int peer_lo, peer_hi;
+    long send_lo, recv_lo, send_hi, recv_hi;
+};
+HaloPlan make_halo_plan(const Geometry& g, int rank, int world);
+
 struct Derived {
     int n_fd;
     double dt_fd, lam_ff, lam_fs, lam_ss;
@@ -76,8 +86,7 @@ struct Nccl;
 Nccl* nccl_load(std::string* err);
 int nccl_unique_id(Nccl*, void* out128, std::string* err);
 void* nccl_comm_init(Nccl*, int world, int rank, const void* id128, std::string* err);
-int nccl_halo(Nccl*, void* comm, float* cpad, const Geometry& g, int rank, int world, cudaStream_t s,
-              std::string* err);
+int nccl_halo(Nccl*, void* comm, float* cpad, const HaloPlan& h, cudaStream_t s, std::string* err);
 int nccl_allreduce_sum_f64(Nccl*, void* comm, double* buf, cudaStream_t s, std::string* err);
 void nccl_comm_destroy(Nccl*, void* comm);
 

@@ -66,6 +66,8 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weig
 
 /* fdirw_params.flags */
 #define FDIRW_F_NO_MASS_FIX 1u /* diagonal = RNE_fmt(W_s(0)) instead of the fp32 mass fix-up (A10) */
+#define FDIRW_F_NO_DEDUP 2u    /* run kgen on every source window instead of once per distinct window
+                                  (results are bitwise identical either way)          */
 
 /* The paper's problem statement (Table 1) + north_star's window radius / precision. */
 typedef struct {
@@ -103,6 +105,8 @@ typedef struct {
     uint64_t voxels;        /* targets in this slab: nx·ny·(z_end − z_begin)                   */
     int32_t tile_chunks;    /* 8-voxel x-chunks per superposition tile (CTA)                   */
     int32_t n_tiles;        /* tiles in this slab                                              */
+    uint64_t kgen_sources;  /* sources whose kernels the slab needs (planes [z_begin−R, z_end+R))  */
+    uint64_t kgen_windows;  /* windows actually run through the FD (distinct windows with dedup)   */
 } fdirw_info;
 
 /* Host-only decomposition plan of one rank (no CUDA call; usable without a GPU).

@@ -30,6 +30,7 @@ FDIRW_OK, E_INVALID, E_UNSTABLE, E_OOM, E_CUDA, E_NCCL, E_ALIAS, E_STATE = range
 STATUS_NAMES = ["OK", "E_INVALID", "E_UNSTABLE", "E_OOM", "E_CUDA", "E_NCCL", "E_ALIAS", "E_STATE"]
 WEIGHTS = {"fp32": 0, "fp16": 1, "bf16": 2}
 F_NO_MASS_FIX = 1
+F_NO_DEDUP = 2
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
@@ -54,7 +55,8 @@ class fdirw_info(ctypes.Structure):
                 ("lambda_fs", ctypes.c_double), ("lambda_slow", ctypes.c_double),
                 ("weight_bytes", ctypes.c_uint64), ("state_bytes", ctypes.c_uint64),
                 ("bytes_per_voxel_update", ctypes.c_uint64), ("voxels", ctypes.c_uint64),
-                ("tile_chunks", ctypes.c_int32), ("n_tiles", ctypes.c_int32)]
+                ("tile_chunks", ctypes.c_int32), ("n_tiles", ctypes.c_int32),
+                ("kgen_sources", ctypes.c_uint64), ("kgen_windows", ctypes.c_uint64)]
 
 
 class fdirw_plan(ctypes.Structure):

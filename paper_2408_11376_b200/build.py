@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfdirw.so")
-SOURCES = ["fdirw_api.cu", "kgen.cu", "superpose.cu", "comm.cpp"]
+SOURCES = ["fdirw_api.cu", "kgen.cu", "superpose.cu", "dedup.cu", "comm.cpp"]
 HEADERS = ["fdirw_internal.h", "layout.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if src.endswith(".cu") and verbose:
             cmd += ["-Xptxas", "-v"]
         if src.endswith(".cpp"):
-            cmd = [NVCC, *FLAGS, "-x", "c++", "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, *ARCH, *FLAGS, "-x", "c++", "-c", os.path.join(CSRC, src), "-o", obj]
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = LIB + ".tmp%d" % os.getpid()

@@ -1,0 +1,265 @@
+// dedup.cu — kgen work reduction by window de-duplication (a3), bit-exact.
+//
+// A source's kernel W_s depends only on its window: the phases of the (2R+1)³ cells
+// around s and which of them lie outside the domain (the column is the FD
+// solution from a point source in that local geometry).  Two sources with identical
+// windows therefore have bitwise identical kernels from the same FD code.  In the
+// paper's geometries most windows are homogeneous liquid (or liquid clipped by the
+// same domain face), e.g. 7.08 M sources but 0.75 M distinct windows at 192³ R5.
+//
+//   1. hash_kernel      two 64-bit polynomial hashes of every source window
+//   2. cub radix sort   (h1, source) pairs; stable, so a class's representative is
+//                       its smallest source index (deterministic)
+//   3. classify         run heads → class ids (inclusive scan − 1); class map in the padded layout
+//                       of the state (−1 outside the domain); every non-head member is
+//                       VERIFIED byte-for-byte against its representative's window —
+//                       any mismatch (a hash collision) makes the caller fall back to
+//                       the direct path, so results never depend on the hash
+//   4. kgen_kernel      on the representatives only, class-major output
+//   5. expand_kernel    writes the gather layout Wt / diag from the class kernels,
+//                       coalesced 16/32-byte stores (replaces the memset + scatter)
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "fdirw_internal.h"
+#include "layout.cuh"
+
+namespace fdirw {
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ unsigned window_code(const DedupArgs& a, int gx, int gy, int gz)
+{
+    if (gx < 0 || gx >= a.nx || gy < 0 || gy >= a.ny || gz < 0 || gz >= a.nz) return 2u;
+    return a.mask[((size_t)(gz - a.mz0) * a.ny + gy) * a.nx + gx];
+}
+
+__global__ void hash_kernel(const DedupArgs a, uint64_t* __restrict__ keys, int* __restrict__ vals,
+                            uint64_t* __restrict__ h2out)
+{
+    const long n = (long)a.nx * a.ny * (a.sz1 - a.sz0);
+    const int L = 2 * a.R + 1;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int sx = (int)(i % a.nx), sy = (int)((i / a.nx) % a.ny), sz = a.sz0 + (int)(i / ((long)a.nx * a.ny));
+        uint64_t h1 = 0x243F6A8885A308D3ull, h2 = 0x13198A2E03707344ull;
+        int k = 0;
+        for (int oz = -a.R; oz <= a.R; ++oz)
+            for (int oy = -a.R; oy <= a.R; ++oy)
+                for (int ox = -a.R; ox <= a.R; ++ox, ++k) {
+                    const uint64_t c = window_code(a, sx + ox, sy + oy, sz + oz) + 1u;
+                    h1 += c * (splitmix64(2 * k) | 1ull);
+                    h2 += c * (splitmix64(2 * k + 1) | 1ull);
+                }
+        (void)L;
+        keys[i] = h1;
+        vals[i] = (int)i;
+        h2out[i] = h2;
+    }
+}
+
+__global__ void heads_kernel(const uint64_t* __restrict__ k, long n, int* __restrict__ head)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        head[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+
+// class ids, representatives, class map (padded layout), and exact verification
+__global__ void classify_kernel(const DedupArgs a, const uint64_t* __restrict__ h2, const int* __restrict__ vals,
+                                const int* __restrict__ head, const int* __restrict__ cid, long n,
+                                int* __restrict__ rep, int* __restrict__ class_pad, int* __restrict__ mismatch)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int s = vals[i];
+        const int c = cid[i] - 1;  // inclusive scan of the run heads
+        if (head[i]) rep[c] = s;
+        const int sx = s % a.nx, sy = (s / a.nx) % a.ny, sz = a.sz0 + s / (a.nx * a.ny);
+        // padded state layout covers planes [z0 − R, z1 + R) — exactly the source planes
+        class_pad[((long)(sz - a.z0 + a.R) * a.nyp + (sy + a.R)) * a.nxp + kPadX + sx] = c;
+    }
+}
+
+__global__ void verify_kernel(const DedupArgs a, const uint64_t* __restrict__ h2, const int* __restrict__ vals,
+                              const int* __restrict__ head, const int* __restrict__ cid, const int* __restrict__ rep,
+                              long n, int* __restrict__ mismatch)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        if (head[i]) continue;
+        const int s = vals[i], r = rep[cid[i] - 1];
+        if (h2[s] != h2[r]) { atomicOr(mismatch, 1); continue; }
+        const int sx = s % a.nx, sy = (s / a.nx) % a.ny, sz = a.sz0 + s / (a.nx * a.ny);
+        const int rx = r % a.nx, ry = (r / a.nx) % a.ny, rz = a.sz0 + r / (a.nx * a.ny);
+        bool same = true;
+        for (int oz = -a.R; oz <= a.R && same; ++oz)
+            for (int oy = -a.R; oy <= a.R && same; ++oy)
+                for (int ox = -a.R; ox <= a.R; ++ox)
+                    if (window_code(a, sx + ox, sy + oy, sz + oz) != window_code(a, rx + ox, ry + oy, rz + oz)) {
+                        same = false;
+                        break;
+                    }
+        if (!same) atomicOr(mismatch, 1);
+    }
+}
+
+// Gather layout from class kernels: thread = 8-target chunk, loop over slots in the
+// superposition's order; per (oz, oy) row the 24 class ids of source row
+// (z − oz, y − oy, x−8 … x+15) are loaded once from the padded class map.
+template <int R, typename WT>
+__global__ void __launch_bounds__(256) expand_kernel(const ExpandArgs a)
+{
+    constexpr int L = 2 * R + 1, LL = L * L, K = L * L * L;
+    const int tile = blockIdx.x;
+    const int zl = tile / a.tpp, tp = tile % a.tpp;
+    const int e = threadIdx.x;
+    const int q = tp * a.tile + e;
+    const size_t wstride = (size_t)a.tile * 8;
+    WT* wt = reinterpret_cast<WT*>(a.Wt) + ((size_t)tile * (K - 1) * a.tile + e) * 8;
+    const WT* cw = reinterpret_cast<const WT*>(a.class_w);
+    const bool real = q < a.ny * a.nxq;
+    const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;
+    const long nxp = a.nxp, plane = (long)a.nyp * nxp;
+    const int* c0 = a.class_pad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
+    {
+        float d[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = (real && x + j < a.nx) ? c0[j] : -1;
+            d[j] = c >= 0 ? a.class_diag[c] : 0.f;
+        }
+        float4* dp = reinterpret_cast<float4*>(a.diag + ((size_t)tile * a.tile + e) * 8);
+        dp[0] = make_float4(d[0], d[1], d[2], d[3]);
+        dp[1] = make_float4(d[4], d[5], d[6], d[7]);
+    }
+    for (int r = -1; r < LL; ++r) {  // r = −1: the centre row first (slot order of layout.cuh)
+        if (r == R * L + R) continue;
+        const int oz = r < 0 ? 0 : r / L - R, oy = r < 0 ? 0 : r % L - R;
+        int seg[24];
+        const int* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
+#pragma unroll
+        for (int i = 0; i < 24; ++i) seg[i] = real ? srow[i] : -1;
+#pragma unroll
+        for (int ox = -R; ox <= R; ++ox) {
+            if (r < 0 && ox == 0) continue;
+            const int o = (oz + R) * LL + (oy + R) * L + (ox + R);
+            WT v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = seg[j - ox + 8];
+                v[j] = c >= 0 ? cw[(size_t)c * K + o] : WT(0.f);
+            }
+            WT* dst = wt + (size_t)slot_of(ox, oy, oz, R) * wstride;
+            if (sizeof(WT) == 2) {
+                *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+            } else {
+                reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(v)[0];
+                reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(v)[1];
+            }
+        }
+    }
+}
+
+static unsigned grid_n(long n)
+{
+    long b = (n + 255) / 256;
+    if (b > 148L * 32) b = 148L * 32;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+#define DCK(call)                              \
+    do {                                       \
+        cudaError_t e_ = (call);               \
+        if (e_ != cudaSuccess) return e_;      \
+    } while (0)
+
+cudaError_t dedup_classify(const DedupArgs& a, DedupResult* res, cudaStream_t s)
+{
+    const long n = (long)a.nx * a.ny * (a.sz1 - a.sz0);
+    res->n_src = n;
+    uint64_t *keys = nullptr, *keys2 = nullptr, *h2 = nullptr;
+    int *vals = nullptr, *vals2 = nullptr, *head = nullptr, *cid = nullptr, *mism = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0, scan_bytes = 0;
+    cudaError_t e = cudaSuccess;
+    auto cleanup = [&]() {
+        cudaFree(keys); cudaFree(keys2); cudaFree(h2); cudaFree(vals); cudaFree(vals2);
+        cudaFree(head); cudaFree(cid); cudaFree(mism); cudaFree(tmp);
+    };
+#define TRY(call)                       \
+    do {                                \
+        e = (call);                     \
+        if (e != cudaSuccess) {         \
+            cleanup();                  \
+            return e;                   \
+        }                               \
+    } while (0)
+    TRY(cudaMalloc(&keys, n * 8));
+    TRY(cudaMalloc(&keys2, n * 8));
+    TRY(cudaMalloc(&h2, n * 8));
+    TRY(cudaMalloc(&vals, n * 4));
+    TRY(cudaMalloc(&vals2, n * 4));
+    TRY(cudaMalloc(&head, n * 4));
+    TRY(cudaMalloc(&cid, n * 4));
+    TRY(cudaMalloc(&mism, 4));
+    TRY(cudaMemsetAsync(mism, 0, 4, s));
+    hash_kernel<<<grid_n(n), 256, 0, s>>>(a, keys, vals, h2);
+    TRY(cudaGetLastError());
+    TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, 64, s));
+    TRY(cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, head, cid, (int)n, s));
+    if (scan_bytes > tmp_bytes) tmp_bytes = scan_bytes;
+    TRY(cudaMalloc(&tmp, tmp_bytes));
+    TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, 64, s));
+    heads_kernel<<<grid_n(n), 256, 0, s>>>(keys2, n, head);
+    TRY(cudaGetLastError());
+    TRY(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, head, cid, (int)n, s));  // class id + 1
+    int last = 0;
+    TRY(cudaMemcpyAsync(&last, cid + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    const long n_class = last;
+    res->n_class = n_class;
+    TRY(cudaMalloc(&res->rep, n_class * 4));
+    classify_kernel<<<grid_n(n), 256, 0, s>>>(a, h2, vals2, head, cid, n, res->rep, a.class_pad, mism);
+    TRY(cudaGetLastError());
+    verify_kernel<<<grid_n(n), 256, 0, s>>>(a, h2, vals2, head, cid, res->rep, n, mism);
+    TRY(cudaGetLastError());
+    int mm = 0;
+    TRY(cudaMemcpyAsync(&mm, mism, 4, cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    res->collision = mm != 0;
+    cleanup();
+    return cudaSuccess;
+#undef TRY
+}
+
+template <int R>
+static cudaError_t launch_expand_r(const ExpandArgs& a, int fmt, cudaStream_t s)
+{
+    if (a.n_tiles <= 0) return cudaSuccess;
+    if (fmt == 0) expand_kernel<R, float><<<a.n_tiles, a.tile, 0, s>>>(a);
+    else if (fmt == 1) expand_kernel<R, __half><<<a.n_tiles, a.tile, 0, s>>>(a);
+    else expand_kernel<R, __nv_bfloat16><<<a.n_tiles, a.tile, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s)
+{
+    switch (R) {
+        case 1: return launch_expand_r<1>(a, fmt, s);
+        case 2: return launch_expand_r<2>(a, fmt, s);
+        case 3: return launch_expand_r<3>(a, fmt, s);
+        case 4: return launch_expand_r<4>(a, fmt, s);
+        case 5: return launch_expand_r<5>(a, fmt, s);
+        case 6: return launch_expand_r<6>(a, fmt, s);
+        case 7: return launch_expand_r<7>(a, fmt, s);
+        case 8: return launch_expand_r<8>(a, fmt, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace fdirw

@@ -33,6 +33,7 @@ struct fdirw_ctx {
     cudaGraphExec_t graph2 = nullptr;
     Nccl* nccl = nullptr;
     void* comm = nullptr;
+    uint64_t kgen_sources = 0, kgen_windows = 0;
 };
 
 static thread_local std::string g_err;
@@ -132,7 +133,7 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (!(p->D_fast > 0) || !(p->D_slow >= 0)) return fail(FDIRW_E_INVALID, "need D_fast > 0, D_slow >= 0");
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
-    if (p->flags & ~FDIRW_F_NO_MASS_FIX) return fail(FDIRW_E_INVALID, "unknown flags");
+    if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP)) return fail(FDIRW_E_INVALID, "unknown flags");
     if ((long long)p->nx * p->ny * p->nz > (1LL << 40)) return fail(FDIRW_E_INVALID, "grid too large");
     if (dist) {
         if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
@@ -259,8 +260,6 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     if ((st = alloc((void**)&c->mass_out, 8, "mass")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
 
     BAIL_CUDA(cudaMemcpyAsync(mask_d, phase_host + (size_t)g.mz0 * plane, mbytes, cudaMemcpyHostToDevice, s));
-    BAIL_CUDA(cudaMemsetAsync(c->Wt, 0, g.w_elems * c->b_w, s));
-    BAIL_CUDA(cudaMemsetAsync(c->diag, 0, g.diag_elems * 4, s));
     BAIL_CUDA(cudaMemsetAsync(c->cpad[0], 0, g.state_elems * 4, s));
     BAIL_CUDA(cudaMemsetAsync(c->cpad[1], 0, g.state_elems * 4, s));
 
@@ -278,7 +277,48 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     ka.Wt = c->Wt;
     ka.diag = c->diag;
     ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;
-    BAIL_CUDA(launch_kgen(ka, g.R, s));
+    c->kgen_sources = (uint64_t)g.nx * g.ny * (g.sz1 - g.sz0);
+    c->kgen_windows = c->kgen_sources;
+    bool dedup = !(params->flags & FDIRW_F_NO_DEDUP);
+    if (dedup) {
+        // identical windows ⇒ identical kernels: compute each distinct window once (dedup.cu)
+        int* class_pad = nullptr;
+        void* class_w = nullptr;
+        float* class_diag = nullptr;
+        DedupResult dr;
+        auto dfree = [&]() { cudaFree(class_pad); cudaFree(class_w); cudaFree(class_diag); cudaFree(dr.rep); };
+        if ((st = alloc((void**)&class_pad, g.state_elems * 4, "class map")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
+        cudaError_t e = cudaMemsetAsync(class_pad, 0xff, g.state_elems * 4, s);
+        DedupArgs da{mask_d, g.mz0, g.nx, g.ny, g.nz, g.R, g.sz0, g.sz1, g.z0, g.nxp, g.nyp, class_pad};
+        if (e == cudaSuccess) e = dedup_classify(da, &dr, s);
+        if (e != cudaSuccess) { dfree(); cudaFree(mask_d); g_err = std::string("dedup: ") + cudaGetErrorString(e); return bail(FDIRW_E_CUDA); }
+        if (dr.collision) {
+            dedup = false;  // hash collision detected by the exact check: take the direct path
+        } else {
+            if ((st = alloc(&class_w, (size_t)dr.n_class * g.K * c->b_w, "class kernels")) != FDIRW_OK ||
+                (st = alloc((void**)&class_diag, (size_t)dr.n_class * 4, "class diagonal")) != FDIRW_OK) {
+                dfree(); cudaFree(mask_d); return bail(st);
+            }
+            ka.src_list = dr.rep;
+            ka.n_list = dr.n_class;
+            ka.class_w = class_w;
+            ka.class_diag = class_diag;
+            e = launch_kgen(ka, g.R, s);
+            ExpandArgs ea{class_pad, class_w, class_diag, c->Wt, c->diag, g.nx, g.ny, g.nxq, g.tile, g.tpp,
+                          g.n_tiles, g.nxp, g.nyp};
+            if (e == cudaSuccess) e = launch_expand(ea, g.R, c->fmt, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) { dfree(); cudaFree(mask_d); g_err = std::string("kgen: ") + cudaGetErrorString(e); return bail(FDIRW_E_CUDA); }
+            c->kgen_windows = (uint64_t)dr.n_class;
+        }
+        dfree();
+    }
+    if (!dedup) {
+        ka.src_list = nullptr; ka.n_list = 0; ka.class_w = nullptr; ka.class_diag = nullptr;
+        BAIL_CUDA(cudaMemsetAsync(c->Wt, 0, g.w_elems * c->b_w, s));
+        BAIL_CUDA(cudaMemsetAsync(c->diag, 0, g.diag_elems * 4, s));
+        BAIL_CUDA(launch_kgen(ka, g.R, s));
+    }
     BAIL_CUDA(cudaStreamSynchronize(s));
     cudaFree(mask_d);
 
@@ -441,6 +481,8 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->voxels = (uint64_t)g.nx * g.ny * g.nzl;
     info->tile_chunks = g.tile;
     info->n_tiles = g.n_tiles;
+    info->kgen_sources = c->kgen_sources;
+    info->kgen_windows = c->kgen_windows;
     return FDIRW_OK;
 }
 

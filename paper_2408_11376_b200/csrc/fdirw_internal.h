@@ -60,8 +60,39 @@ struct KgenArgs {
     void* Wt;
     float* diag;
     int nxq, tile, tpp, K;
+    // class mode (dedup.cu): process src_list[0..n_list) (linear source indices within
+    // planes [sz0, sz1)) and write class-major class_w[i][K] (storage format) + class_diag[i]
+    const int* src_list;
+    long n_list;
+    void* class_w;
+    float* class_diag;
 };
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s);
+
+// ---- window de-duplication (dedup.cu) -------------------------------------------
+struct DedupArgs {
+    const uint8_t* mask;
+    int mz0, nx, ny, nz, R;
+    int sz0, sz1, z0;
+    int nxp, nyp;
+    int* class_pad;  // padded-state layout, pre-filled with −1
+};
+struct DedupResult {
+    long n_src = 0, n_class = 0;
+    int* rep = nullptr;  // device [n_class]: representative source (linear index in [sz0, sz1))
+    bool collision = false;
+};
+cudaError_t dedup_classify(const DedupArgs& a, DedupResult* res, cudaStream_t s);
+
+struct ExpandArgs {
+    const int* class_pad;
+    const void* class_w;
+    const float* class_diag;
+    void* Wt;
+    float* diag;
+    int nx, ny, nxq, tile, tpp, n_tiles, nxp, nyp;
+};
+cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s);
 
 struct SuperArgs {
     const float* cpad;   // padded state, pointer to padded plane 0

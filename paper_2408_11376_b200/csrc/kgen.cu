@@ -88,9 +88,10 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
     const int oxm = (col && cx > 0) ? -1 : 0, oxp = (col && cx < L - 1) ? 1 : 0;
     const int oym = (col && cy > 0) ? -L : 0, oyp = (col && cy < L - 1) ? L : 0;
     const int nx = a.nx, ny = a.ny, nz = a.nz;
-    const long nsrc = (long)nx * ny * (a.sz1 - a.sz0);
+    const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
-    for (long src = blockIdx.x; src < nsrc; src += gridDim.x) {
+    for (long it = blockIdx.x; it < nsrc; it += gridDim.x) {
+        const long src = a.src_list ? (long)a.src_list[it] : it;
         const int sx = (int)(src % nx);
         const int sy = (int)((src / nx) % ny);
         const int sz = a.sz0 + (int)(src / ((long)nx * ny));
@@ -179,13 +180,19 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
                 } else {
                     qd = wf;
                 }
+                if (a.class_w) {  // class-major store (dedup path): every slot written
+                    const size_t ci = (size_t)it * LLL + o;
+                    const bool keep = active && o != KC;
+                    if (a.fmt == 0) reinterpret_cast<float*>(a.class_w)[ci] = keep ? wf : 0.f;
+                    else reinterpret_cast<unsigned short*>(a.class_w)[ci] = keep ? bits : (unsigned short)0;
+                }
                 if (o == KC) {
                     centre_q = qd;
                     continue;
                 }
                 if (!active) continue;
                 qsum += (double)qd;
-                if (gz < a.z0 || gz >= a.z1) continue;
+                if (a.class_w || gz < a.z0 || gz >= a.z1) continue;
                 const int zl = gz - a.z0;
                 const int q = gy * a.nxq + (gx >> 3);
                 const size_t tile = (size_t)zl * a.tpp + q / a.tile;
@@ -196,7 +203,9 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
             }
         }
         const double off = block_sum_f64<S::NW>(qsum, red);
-        if (t == R * L + R && sz >= a.z0 && sz < a.z1) {
+        if (t == R * L + R && a.class_w) {
+            a.class_diag[it] = a.mass_fix ? (float)(1.0 - off) : centre_q;
+        } else if (t == R * L + R && sz >= a.z0 && sz < a.z1) {
             const float d = a.mass_fix ? (float)(1.0 - off) : centre_q;
             const int zl = sz - a.z0;
             const int q = sy * a.nxq + (sx >> 3);
@@ -211,7 +220,7 @@ template <int R>
 static cudaError_t launch_kgen_r(const KgenArgs& a, cudaStream_t s)
 {
     using S = KgenShape<R>;
-    const long nsrc = (long)a.nx * a.ny * (a.sz1 - a.sz0);
+    const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
     if (nsrc <= 0) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kgen_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)S::smem_bytes);

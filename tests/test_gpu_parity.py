@@ -251,3 +251,57 @@ def test_errors(fd):
         assert e.value.status == fd.E_ALIAS
     finally:
         fd.destroy(ctx)
+
+
+# ------------------------------------------------------------------ window de-duplication
+@pytest.mark.parametrize("fmt,R,n_fd", [("bf16", 3, 100), ("fp32", 2, 1000), ("fp16", 4, 40)])
+def test_dedup_bitwise(fd, fmt, R, n_fd):
+    """kgen once per distinct window (default) == kgen on every source (FDIRW_F_NO_DEDUP),
+    bitwise: stored kernels and stepped fields; on a particle geometry with many duplicates."""
+    import torch
+
+    shape = (30, 28, 33)
+    mask = fi.porous_particle(shape, 9, pore_r=(1.0, 2.0), porosity=0.3, seed=4)
+    cfg = small_cfg(shape, R, n_fd, D_slow=1e-3, weights=fmt)
+    c0 = fi.initial_c(mask, "random", seed=4)
+    outs, infos, kerns = [], [], []
+    for flags in (0, fd.F_NO_DEDUP):
+        ctx = fd.build_kernels(lib_params(cfg, flags=flags), mask)
+        try:
+            infos.append(ctx.info)
+            kerns.append(fd.export_kernels(ctx, (0, 33, 0, 28, 0, 30)))
+            c = torch.from_numpy(c0).cuda()
+            fd.run(ctx, c, 3)
+            outs.append(c.cpu().numpy())
+        finally:
+            fd.destroy(ctx)
+    assert infos[0]["kgen_windows"] < 0.6 * infos[0]["kgen_sources"]  # 6204 / 9181 / 13148 of 27720
+    assert infos[1]["kgen_windows"] == infos[1]["kgen_sources"] == 30 * 28 * 33
+    np.testing.assert_array_equal(kerns[0], kerns[1])
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_cfg5_r8_sampled(fd, oracle_lib):
+    """BASELINE configs[4]: cfg3 geometry, D ratio 1e8, R8 (K = 4913), bf16; one step,
+    a sampled box at the particle surface vs the oracle; whole-grid mass."""
+    import torch
+
+    cfg = fi.config("cfg5")
+    mask = cfg.mask()
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "paper")
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        info = ctx.info
+        assert info["K"] == 4913 and info["n_fd"] == 1000
+        c = torch.from_numpy(c0).cuda()
+        m0 = fd.mass(ctx, c)
+        fd.run(ctx, c, 1)
+        m1 = fd.mass(ctx, c)
+        got = c.cpu().numpy()
+    finally:
+        fd.destroy(ctx)
+    assert abs(m1 - m0) / m0 <= 1e-6
+    tb = (143, 147, 93, 97, 94, 97)
+    ref = oracle_lib.step_box(pb, c0.astype(np.float64), tb)
+    assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= 5e-3

@@ -124,6 +124,17 @@ def tiled_particles(n_tile: int = 192, tiles=(2, 2, 2), r_p: float = 50, porosit
     return out
 
 
+def near_field(mask: np.ndarray, r_p: float, margin: float = 5.0, center=None) -> np.ndarray:
+    """Near-field liquid: liquid voxels whose centre lies within r_p + margin·Δh of
+    the particle centre (Euclidean, boundary inclusive).  uint8 region."""
+    nz, ny, nx = mask.shape
+    c0 = center if center is not None else ((nx - 1) / 2.0, (ny - 1) / 2.0, (nz - 1) / 2.0)
+    z, y, x = np.ogrid[0:nz, 0:ny, 0:nx]
+    r = r_p + margin
+    inside = (x - c0[0]) ** 2 + (y - c0[1]) ** 2 + (z - c0[2]) ** 2 <= r * r
+    return ((mask == 1) & inside).astype(np.uint8)
+
+
 def random_two_phase(shape, p_fast: float = 0.6, seed: int = 0) -> np.ndarray:
     """i.i.d. Bernoulli phases — a stress input for small parity cases (not a paper shape)."""
     rng = np.random.Generator(np.random.PCG64(seed))

@@ -195,6 +195,49 @@ fdirw_status fdirw_export_kernels(const fdirw_ctx* ctx, const int32_t* box, doub
 fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, const float* const* c_in,
                                 float* const* c_out, void* cuda_stream);
 
+/* ---- NEXT row N1: coarse-mesh FDiRW (§3.1, Eqs.10-15) ------------------
+ * The paper's own step on a coarse mesh, for the fast phase only (§3 "FDiRW solver
+ * for fast diffusion in near-field liquid"), closed domain (no P_BC, reading A3):
+ *   region   Ω_L = voxels with region_host[v] != 0 (e.g. near-field liquid)
+ *   groups   Ω_L ∩ b×b×b blocks anchored at the origin, empty blocks dropped,
+ *            numbered in block order (N = N_L/125 ⇔ b = 5)
+ *   P        dense N×N; column J = group means (Eq.13) of an explicit FD run over Ω_L
+ *            (faces leaving Ω_L carry no flux, face number λ = Δt_fd·D_fast/Δh²) from
+ *            the group-uniform source 1 on group J, n_fd substeps; stored in
+ *            params->weights format, off-diagonal RNE, fp32 diagonal fixed so that
+ *            Σ_I N_I P̃_IJ = N_J (column mass; coarse analogue of reading A10)
+ *   step     C_I = Σ_{i∈I} c_i / N_I in fp32 (Eq.13, "mapping ... in FP32");
+ *            C'_I = Σ_J P̃_IJ C_J, fp32 accumulation (Eq.14);  c'_i = C'_I (Eq.15);
+ *            voxels outside Ω_L are copied unchanged.
+ * params: nx, ny, nz, dh, D_fast, dt, n_fd, weights as for the fine path (D_slow,
+ * radius and flags are ignored).  Single GPU.  Buffers are device fp32 [nz][ny][nx].
+ */
+typedef struct fdirw_coarse fdirw_coarse; /* opaque */
+
+typedef struct {
+    int32_t n_fd;
+    int32_t block;          /* b                                                       */
+    int64_t n_groups;       /* N (coarse nodes)                                        */
+    int64_t n_region;       /* N_L (fine voxels in Ω_L)                                */
+    uint64_t p_bytes;       /* stored P incl. fp32 diagonal                           */
+    uint64_t flops_per_step;/* the paper's model N(N+1) + 2·N_L                */
+} fdirw_coarse_info;
+
+/* Builds groups, P (batched whole-region FD on the GPU), quantises.  Synchronous. */
+fdirw_status fdirw_coarse_build(const fdirw_params* params, const uint8_t* region_host, int32_t block,
+                                void* cuda_stream, fdirw_coarse** out);
+/* One coarse step c_out = remap(P̃ · map(c_in)) (c_in != c_out).  Asynchronous. */
+fdirw_status fdirw_coarse_step(fdirw_coarse* ctx, const float* c_in_dev, float* c_out_dev, void* cuda_stream);
+/* n_steps coarse steps in place on c_dev (each step map → GEMV → remap of the Ω_L
+ * voxels, replayed from a CUDA graph; bitwise equal to n fdirw_coarse_step calls).
+ * Asynchronous. */
+fdirw_status fdirw_coarse_run(fdirw_coarse* ctx, float* c_dev, int32_t n_steps, void* cuda_stream);
+fdirw_status fdirw_coarse_query(const fdirw_coarse* ctx, fdirw_coarse_info* info);
+/* Host copies: P_host [N][N] fp64 decoded (diagonal = fp32 fix-up) if non-NULL;
+ * group_of_host [nz][ny][nx] int32 (−1 outside Ω_L) if non-NULL.  Synchronous. */
+fdirw_status fdirw_coarse_export(const fdirw_coarse* ctx, double* P_host, int32_t* group_of_host);
+void fdirw_coarse_destroy(fdirw_coarse* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ _LIB_PATH = os.path.join(_HERE, "libfdirw.so")
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
-        "libfdirw.so not found at %s — build it with `python -m paper_2408_11376_b200.build` "
+        "libfdirw.so not found at %s — build it with `python paper_2408_11376_b200/build.py` "
         "(or __graft_entry__.build()); there is no fallback path" % _LIB_PATH)
 
 _lib = ctypes.CDLL(_LIB_PATH)
@@ -34,7 +34,8 @@ F_NO_DEDUP = 2
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
-           "fdirw_export_kernels", "fdirw_step_virtual"]
+           "fdirw_export_kernels", "fdirw_step_virtual", "fdirw_coarse_build", "fdirw_coarse_step",
+           "fdirw_coarse_run", "fdirw_coarse_query", "fdirw_coarse_export", "fdirw_coarse_destroy"]
 
 
 class fdirw_params(ctypes.Structure):
@@ -68,6 +69,11 @@ class fdirw_plan(ctypes.Structure):
         [("weight_bytes", ctypes.c_uint64), ("state_bytes", ctypes.c_uint64)]
 
 
+class fdirw_coarse_info(ctypes.Structure):
+    _fields_ = [("n_fd", ctypes.c_int32), ("block", ctypes.c_int32), ("n_groups", ctypes.c_int64),
+                ("n_region", ctypes.c_int64), ("p_bytes", ctypes.c_uint64), ("flops_per_step", ctypes.c_uint64)]
+
+
 _vp = ctypes.c_void_p
 _st = ctypes.c_int
 _lib.fdirw_make_plan.argtypes = [ctypes.POINTER(fdirw_params), ctypes.POINTER(fdirw_dist), ctypes.POINTER(fdirw_plan)]
@@ -96,6 +102,18 @@ _lib.fdirw_export_kernels.restype = _st
 _lib.fdirw_step_virtual.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32, ctypes.POINTER(_vp),
                                     ctypes.POINTER(_vp), _vp]
 _lib.fdirw_step_virtual.restype = _st
+_lib.fdirw_coarse_build.argtypes = [ctypes.POINTER(fdirw_params), _vp, ctypes.c_int32, _vp, ctypes.POINTER(_vp)]
+_lib.fdirw_coarse_build.restype = _st
+_lib.fdirw_coarse_step.argtypes = [_vp, _vp, _vp, _vp]
+_lib.fdirw_coarse_step.restype = _st
+_lib.fdirw_coarse_run.argtypes = [_vp, _vp, ctypes.c_int32, _vp]
+_lib.fdirw_coarse_run.restype = _st
+_lib.fdirw_coarse_query.argtypes = [_vp, ctypes.POINTER(fdirw_coarse_info)]
+_lib.fdirw_coarse_query.restype = _st
+_lib.fdirw_coarse_export.argtypes = [_vp, _vp, _vp]
+_lib.fdirw_coarse_export.restype = _st
+_lib.fdirw_coarse_destroy.argtypes = [_vp]
+_lib.fdirw_coarse_destroy.restype = None
 
 
 class FdirwError(RuntimeError):
@@ -261,3 +279,64 @@ def step_virtual(ctxs, c_in, c_out, stream=None):
 def slabs(nz: int, world: int):
     """Equal z-slabs [r·nz/P, (r+1)·nz/P)."""
     return [(r * nz // world, (r + 1) * nz // world) for r in range(world)]
+
+
+# ---- NEXT row N1: coarse-mesh FDiRW (P:109-133 Eqs.10-15) ------------------------------
+class Coarse:
+    """Owns an fdirw_coarse*."""
+
+    def __init__(self, handle: int, params: Params, shape):
+        self.handle = ctypes.c_void_p(handle)
+        self.params = params
+        self.shape = shape
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        coarse_destroy(self)
+
+    @property
+    def info(self):
+        return coarse_query(self)
+
+
+def coarse_build(params: Params, region: np.ndarray, block: int = 5, stream=None) -> Coarse:
+    """fdirw_coarse_build: region = uint8 [nz][ny][nx] (host), nonzero = Ω_L."""
+    region = np.ascontiguousarray(region, dtype=np.uint8)
+    if region.shape != (params.nz, params.ny, params.nx):
+        raise ValueError("region shape %s != (nz, ny, nx)" % (region.shape,))
+    p = params.c()
+    h = ctypes.c_void_p()
+    _check(_lib.fdirw_coarse_build(ctypes.byref(p), region.ctypes.data_as(ctypes.c_void_p), int(block),
+                                   _stream(stream), ctypes.byref(h)))
+    return Coarse(h.value, params, region.shape)
+
+
+def coarse_step(ctx: Coarse, c_in, c_out, stream=None):
+    _check(_lib.fdirw_coarse_step(ctx.handle, _dptr(c_in), _dptr(c_out), _stream(stream)))
+
+
+def coarse_run(ctx: Coarse, c, n_steps: int, stream=None):
+    _check(_lib.fdirw_coarse_run(ctx.handle, _dptr(c), int(n_steps), _stream(stream)))
+
+
+def coarse_query(ctx: Coarse) -> dict:
+    info = fdirw_coarse_info()
+    _check(_lib.fdirw_coarse_query(ctx.handle, ctypes.byref(info)))
+    return {f: getattr(info, f) for f, _ in fdirw_coarse_info._fields_}
+
+
+def coarse_export(ctx: Coarse):
+    """(P decoded fp64 [N][N] with the fp32 diagonal, group_of int32 [nz][ny][nx])."""
+    N = coarse_query(ctx)["n_groups"]
+    P = np.zeros((N, N), np.float64)
+    g = np.zeros(ctx.shape, np.int32)
+    _check(_lib.fdirw_coarse_export(ctx.handle, P.ctypes.data_as(ctypes.c_void_p), g.ctypes.data_as(ctypes.c_void_p)))
+    return P, g
+
+
+def coarse_destroy(ctx: Coarse):
+    if ctx.handle and ctx.handle.value:
+        _lib.fdirw_coarse_destroy(ctx.handle)
+        ctx.handle = ctypes.c_void_p()

@@ -1,0 +1,530 @@
+// coarse.cu — NEXT row N1: coarse-mesh FDiRW (§3.1, Eqs.10-15) on B200.
+//
+// Build (one-time, "preconditioned" P):
+//   groups      Ω_L ∩ b³ blocks (P:113 N = N_L/125 ⇔ b = 5): used-block flags → scan → ids;
+//               group CSR (stable radix sort of (group, voxel)) for the mapping step
+//   columns     explicit FD over Ω_L from the group-uniform sources 1_J,
+//               all columns of a chunk at once: X[row][j] with j fastest, so the 7-point
+//               stencil reads whole neighbour rows (coalesced 16-byte loads, neighbour
+//               table read once per row, rows of 3 z-planes of the region stay in L2)
+//   P           group means of the FD result (Eq.11/13), fp64, then RNE to the storage
+//               format with an fp32 diagonal fixing Σ_I N_I P̃_IJ = N_J
+// Step (the paper's three kernels, §3.2 / Fig.2, fused into a CUDA graph for run):
+//   map_kernel     one warp per group, fp32 sum over its voxels ("mapping ... FP32")
+//   gemv_kernel    one warp per row I of P̃ (row-major, L2-resident: N² b_w bytes), 128-bit
+//                  loads, fp32 FMA + fixed shuffle tree ("accumulation ... FP32")
+//   remap_kernel   c'_i = C'_{I(i)} for every Ω_L voxel (Eq.15)
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "fdirw_internal.h"
+
+using namespace fdirw;
+
+struct fdirw_coarse {
+    fdirw_params p;
+    int n_fd = 0, b = 5, fmt = 0, b_w = 4, device = 0;
+    double lam = 0;
+    long nvox = 0, NL = 0, N = 0;
+    int* group_of = nullptr;  // [nvox]
+    int* rows = nullptr;      // [NL] voxel of each region row (voxel order)
+    int* grp_ptr = nullptr;   // [N+1]
+    int* grp_vox = nullptr;   // [NL] voxels sorted by group
+    int* sizes = nullptr;     // [N]
+    void* P = nullptr;        // [N][N] storage format, diagonal slot 0
+    float* Pdiag = nullptr;   // [N]
+    float* C = nullptr;       // [N]
+    float* C2 = nullptr;      // [N]
+    cudaStream_t cap = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    float* graph_c = nullptr;
+};
+
+namespace fdirw {
+const char* coarse_set_error(const std::string& m);
+}
+
+static fdirw_status cfail(fdirw_status s, const std::string& m)
+{
+    coarse_set_error(m);
+    return s;
+}
+
+#define CK(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess) return cfail(FDIRW_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+static unsigned gridn(long n, int t = 256)
+{
+    long b = (n + t - 1) / t;
+    if (b > 148L * 32) b = 148L * 32;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+#define GRID_STRIDE(i, n) for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (n); i += (long)gridDim.x * blockDim.x)
+
+__global__ void k_mark_blocks(const uint8_t* reg, long nvox, int nx, int ny, int b, int bx, int by, int* used)
+{
+    GRID_STRIDE(v, nvox)
+    {
+        if (!reg[v]) continue;
+        const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((long)nx * ny));
+        used[((z / b) * by + (y / b)) * bx + (x / b)] = 1;
+    }
+}
+
+__global__ void k_group_of(const uint8_t* reg, long nvox, int nx, int ny, int b, int bx, int by, const int* bid,
+                           int* group_of, int* sizes, int* row_flag)
+{
+    GRID_STRIDE(v, nvox)
+    {
+        int g = -1;
+        if (reg[v]) {
+            const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((long)nx * ny));
+            g = bid[((z / b) * by + (y / b)) * bx + (x / b)];
+            atomicAdd(&sizes[g], 1);
+        }
+        group_of[v] = g;
+        row_flag[v] = g >= 0 ? 1 : 0;
+    }
+}
+
+__global__ void k_rows(const int* row_flag, const int* row_pos, long nvox, int* rows, int* row_of, const int* group_of,
+                       int* row_group)
+{
+    GRID_STRIDE(v, nvox)
+    {
+        if (row_flag[v]) {
+            const int r = row_pos[v];
+            rows[r] = (int)v;
+            row_group[r] = group_of[v];
+            row_of[v] = r;
+        } else {
+            row_of[v] = -1;
+        }
+    }
+}
+
+// neighbour rows in the order −x, +x, −y, +y, −z, +z (−1: no flux)
+__global__ void k_neighbours(const int* rows, long NL, const int* row_of, int nx, int ny, int nz, int* nb)
+{
+    GRID_STRIDE(r, NL)
+    {
+        const int v = rows[r];
+        const int x = v % nx, y = (v / nx) % ny, z = v / (nx * ny);
+        const long pl = (long)nx * ny;
+        nb[r * 6 + 0] = x > 0 ? row_of[v - 1] : -1;
+        nb[r * 6 + 1] = x < nx - 1 ? row_of[v + 1] : -1;
+        nb[r * 6 + 2] = y > 0 ? row_of[v - nx] : -1;
+        nb[r * 6 + 3] = y < ny - 1 ? row_of[v + nx] : -1;
+        nb[r * 6 + 4] = z > 0 ? row_of[v - pl] : -1;
+        nb[r * 6 + 5] = z < nz - 1 ? row_of[v + pl] : -1;
+    }
+}
+
+__global__ void k_init_cols(const int* row_group, long NL, int CB, int J0, float* X)
+{
+    GRID_STRIDE(i, NL * (long)CB)
+    {
+        const long r = i / CB;
+        const int j = (int)(i % CB);
+        X[i] = row_group[r] == J0 + j ? 1.f : 0.f;
+    }
+}
+
+// One FD substep for CB columns at once: one warp per row, lanes over float4 column quads.
+__global__ void __launch_bounds__(256) k_fd_cols(const float* __restrict__ X, float* __restrict__ Y,
+                                                 const int* __restrict__ nb, long NL, int CB, float lam)
+{
+    const int lane = threadIdx.x & 31;
+    const long warps = (long)gridDim.x * (blockDim.x >> 5);
+    const int q4 = CB >> 2;
+    for (long r = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < NL; r += warps) {
+        int n[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) n[f] = __ldg(nb + r * 6 + f);
+        const float4* xr = reinterpret_cast<const float4*>(X + r * (long)CB);
+        float4* yr = reinterpret_cast<float4*>(Y + r * (long)CB);
+        for (int q = lane; q < q4; q += 32) {
+            const float4 c = xr[q];
+            float4 a = c;
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                if (n[f] < 0) continue;
+                const float4 m = reinterpret_cast<const float4*>(X + (long)n[f] * CB)[q];
+                a.x = fmaf(lam, m.x - c.x, a.x);
+                a.y = fmaf(lam, m.y - c.y, a.y);
+                a.z = fmaf(lam, m.z - c.z, a.z);
+                a.w = fmaf(lam, m.w - c.w, a.w);
+            }
+            yr[q] = a;
+        }
+    }
+}
+
+// P64[I][J0 + j] = Σ_{v∈I} X[row(v)][j] / N_I (fp64, CSR order)
+__global__ void k_map_cols(const float* X, const int* grp_ptr, const int* grp_vox, const int* row_of, long N, int CB,
+                           int J0, int Jn, double* P64)
+{
+    GRID_STRIDE(i, N * (long)Jn)
+    {
+        const long I = i / Jn;
+        const int j = (int)(i % Jn);
+        double s = 0.0;
+        for (int k = grp_ptr[I]; k < grp_ptr[I + 1]; ++k) s += (double)X[(long)row_of[grp_vox[k]] * CB + j];
+        P64[I * N + J0 + j] = s / (double)(grp_ptr[I + 1] - grp_ptr[I]);
+    }
+}
+
+template <typename WT>
+__device__ __forceinline__ WT enc(float f);
+template <>
+__device__ __forceinline__ float enc<float>(float f) { return f; }
+template <>
+__device__ __forceinline__ __half enc<__half>(float f) { return __float2half_rn(f); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 enc<__nv_bfloat16>(float f) { return __float2bfloat16_rn(f); }
+__device__ __forceinline__ float dec(float v) { return v; }
+__device__ __forceinline__ float dec(__half v) { return __half2float(v); }
+__device__ __forceinline__ float dec(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// one block per column J: quantise off-diagonal entries, fp64 column mass, fp32 diagonal
+template <typename WT>
+__global__ void k_quantize(const double* P64, const int* sizes, long N, WT* P, float* Pdiag)
+{
+    __shared__ double red[32];
+    const long J = blockIdx.x;
+    double s = 0.0;
+    for (long I = threadIdx.x; I < N; I += blockDim.x) {
+        WT q = enc<WT>((float)P64[I * N + J]);
+        if (I == J) q = enc<WT>(0.f);
+        P[I * N + J] = q;
+        s += (double)sizes[I] * (double)dec(q);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        const double nj = (double)sizes[J];
+        Pdiag[J] = (float)((nj - t) / nj);
+    }
+}
+
+// ---- step kernels -------------------------------------------------------------------
+__global__ void k_map(const float* __restrict__ c, const int* __restrict__ grp_ptr, const int* __restrict__ grp_vox,
+                      long N, float* __restrict__ C)
+{
+    const int lane = threadIdx.x & 31;
+    const long warps = (long)gridDim.x * (blockDim.x >> 5);
+    for (long I = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); I < N; I += warps) {
+        const int a = grp_ptr[I], b = grp_ptr[I + 1];
+        float s = 0.f;
+        for (int k = a + lane; k < b; k += 32) s += c[grp_vox[k]];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) C[I] = s / (float)(b - a);
+    }
+}
+
+template <typename WT>
+__global__ void __launch_bounds__(256) k_gemv(const WT* __restrict__ P, const float* __restrict__ Pdiag,
+                                              const float* __restrict__ C, long N, float* __restrict__ Cout)
+{
+    const int lane = threadIdx.x & 31;
+    const long warps = (long)gridDim.x * (blockDim.x >> 5);
+    constexpr int V = 16 / sizeof(WT);  // elements per 128-bit load
+    for (long I = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); I < N; I += warps) {
+        const WT* row = P + I * N;
+        float acc = 0.f;
+        const bool vec = (N % V) == 0;
+        if (vec) {
+            for (long j0 = (long)lane * V; j0 < N; j0 += 32L * V) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + j0));
+                const WT* w = reinterpret_cast<const WT*>(&u);
+#pragma unroll
+                for (int k = 0; k < V; ++k) acc = fmaf(dec(w[k]), __ldg(C + j0 + k), acc);
+            }
+        } else {
+            for (long j = lane; j < N; j += 32) acc = fmaf(dec(row[j]), __ldg(C + j), acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) Cout[I] = fmaf(Pdiag[I], C[I], acc);
+    }
+}
+
+__global__ void k_remap(const int* __restrict__ rows, long NL, const int* __restrict__ group_of,
+                        const float* __restrict__ C, float* __restrict__ c)
+{
+    GRID_STRIDE(r, NL)
+    {
+        const int v = rows[r];
+        c[v] = C[group_of[v]];
+    }
+}
+
+static void coarse_free(fdirw_coarse* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->cap) cudaStreamDestroy(c->cap);
+    cudaFree(c->group_of); cudaFree(c->rows); cudaFree(c->grp_ptr); cudaFree(c->grp_vox); cudaFree(c->sizes);
+    cudaFree(c->P); cudaFree(c->Pdiag); cudaFree(c->C); cudaFree(c->C2);
+    delete c;
+}
+
+extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t* region_host, int32_t block,
+                                           void* cuda_stream, fdirw_coarse** out)
+{
+    if (!p || !region_host || !out) return cfail(FDIRW_E_INVALID, "NULL argument");
+    *out = nullptr;
+    if (p->nx < 1 || p->ny < 1 || p->nz < 1 || block < 1) return cfail(FDIRW_E_INVALID, "dims and block must be >= 1");
+    if (!(p->dh > 0) || !(p->dt > 0) || !(p->D_fast > 0) || p->n_fd < 0)
+        return cfail(FDIRW_E_INVALID, "need dh, dt, D_fast > 0 and n_fd >= 0");
+    if (p->weights < 0 || p->weights > 2) return cfail(FDIRW_E_INVALID, "bad weight format");
+    // a1 for the fast phase (reading A5)
+    long n = p->n_fd;
+    if (n == 0) {
+        const double x = p->D_fast * p->dt / (0.1 * p->dh * p->dh);
+        const double cc = std::ceil(x * (1.0 - 1e-9));
+        if (!(cc < 2.0e9)) return cfail(FDIRW_E_INVALID, "derived n_fd too large");
+        n = cc < 1.0 ? 1 : (long)cc;
+    }
+    const double lam = (p->dt / (double)n) * p->D_fast / (p->dh * p->dh);
+    if (lam > 1.0 / 6.0) return cfail(FDIRW_E_UNSTABLE, "explicit FD unstable: lambda > 1/6");
+
+    fdirw_coarse* c = new fdirw_coarse();
+    c->p = *p;
+    c->n_fd = (int)n;
+    c->lam = lam;
+    c->b = block;
+    c->fmt = p->weights;
+    c->b_w = c->fmt == FDIRW_W_FP32 ? 4 : 2;
+    cudaGetDevice(&c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const int nx = p->nx, ny = p->ny, nz = p->nz, b = block;
+    const long nvox = (long)nx * ny * nz;
+    c->nvox = nvox;
+    const int bx = (nx + b - 1) / b, by = (ny + b - 1) / b, bz = (nz + b - 1) / b;
+    const long nblk = (long)bx * by * bz;
+
+    uint8_t* reg = nullptr;
+    int *used = nullptr, *bid = nullptr, *row_flag = nullptr, *row_pos = nullptr, *row_of = nullptr;
+    int *row_group = nullptr, *row_group2 = nullptr, *nb = nullptr, *tmp_rows = nullptr;
+    float *X = nullptr, *Y = nullptr;
+    double* P64 = nullptr;
+    void* tmp = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(reg); cudaFree(used); cudaFree(bid); cudaFree(row_flag); cudaFree(row_pos); cudaFree(row_of);
+        cudaFree(row_group); cudaFree(row_group2); cudaFree(nb); cudaFree(tmp_rows); cudaFree(X); cudaFree(Y);
+        cudaFree(P64); cudaFree(tmp);
+    };
+    cudaError_t e = cudaSuccess;
+#define T(call)                                                                     \
+    do {                                                                            \
+        e = (call);                                                                 \
+        if (e != cudaSuccess) {                                                     \
+            std::string m_ = std::string(#call) + ": " + cudaGetErrorString(e);     \
+            cleanup();                                                              \
+            coarse_free(c);                                                         \
+            return cfail(e == cudaErrorMemoryAllocation ? FDIRW_E_OOM : FDIRW_E_CUDA, m_); \
+        }                                                                           \
+    } while (0)
+    T(cudaMalloc(&reg, nvox));
+    T(cudaMemcpyAsync(reg, region_host, nvox, cudaMemcpyHostToDevice, s));
+    T(cudaMalloc(&used, (nblk + 1) * 4));
+    T(cudaMalloc(&bid, (nblk + 1) * 4));
+    T(cudaMemsetAsync(used, 0, (nblk + 1) * 4, s));
+    k_mark_blocks<<<gridn(nvox), 256, 0, s>>>(reg, nvox, nx, ny, b, bx, by, used);
+    T(cudaGetLastError());
+    size_t tb = 0, tb2 = 0;
+    T(cub::DeviceScan::ExclusiveSum(nullptr, tb, used, bid, (int)(nblk + 1), s));
+    T(cub::DeviceScan::ExclusiveSum(nullptr, tb2, used, bid, (int)nvox, s));
+    if (tb2 > tb) tb = tb2;
+    T(cudaMalloc(&tmp, tb));
+    T(cub::DeviceScan::ExclusiveSum(tmp, tb, used, bid, (int)(nblk + 1), s));
+    int N = 0;
+    T(cudaMemcpyAsync(&N, bid + nblk, 4, cudaMemcpyDeviceToHost, s));
+    T(cudaStreamSynchronize(s));
+    if (N == 0) {
+        cleanup();
+        coarse_free(c);
+        return cfail(FDIRW_E_INVALID, "empty region");
+    }
+    c->N = N;
+    T(cudaMalloc(&c->group_of, nvox * 4));
+    T(cudaMalloc(&c->sizes, (long)N * 4));
+    T(cudaMemsetAsync(c->sizes, 0, (long)N * 4, s));
+    T(cudaMalloc(&row_flag, nvox * 4));
+    T(cudaMalloc(&row_pos, nvox * 4));
+    k_group_of<<<gridn(nvox), 256, 0, s>>>(reg, nvox, nx, ny, b, bx, by, bid, c->group_of, c->sizes, row_flag);
+    T(cudaGetLastError());
+    T(cub::DeviceScan::ExclusiveSum(tmp, tb, row_flag, row_pos, (int)nvox, s));
+    int last[2];
+    T(cudaMemcpyAsync(&last[0], row_pos + nvox - 1, 4, cudaMemcpyDeviceToHost, s));
+    T(cudaMemcpyAsync(&last[1], row_flag + nvox - 1, 4, cudaMemcpyDeviceToHost, s));
+    T(cudaStreamSynchronize(s));
+    const long NL = (long)last[0] + last[1];
+    c->NL = NL;
+    T(cudaMalloc(&c->rows, NL * 4));
+    T(cudaMalloc(&row_of, nvox * 4));
+    T(cudaMalloc(&row_group, NL * 4));
+    T(cudaMalloc(&row_group2, NL * 4));
+    T(cudaMalloc(&tmp_rows, NL * 4));
+    k_rows<<<gridn(nvox), 256, 0, s>>>(row_flag, row_pos, nvox, c->rows, row_of, c->group_of, row_group);
+    T(cudaGetLastError());
+    // group CSR: stable sort of (group, voxel) over the region rows
+    T(cudaMalloc(&c->grp_vox, NL * 4));
+    T(cudaMalloc(&c->grp_ptr, ((long)N + 1) * 4));
+    size_t ts = 0;
+    T(cub::DeviceRadixSort::SortPairs(nullptr, ts, row_group, row_group2, c->rows, c->grp_vox, (int)NL, 0, 32, s));
+    if (ts > tb) {
+        cudaFree(tmp);
+        tmp = nullptr;
+        T(cudaMalloc(&tmp, ts));
+        tb = ts;
+    }
+    T(cub::DeviceRadixSort::SortPairs(tmp, tb, row_group, row_group2, c->rows, c->grp_vox, (int)NL, 0, 32, s));
+    T(cudaMemsetAsync(c->grp_ptr, 0, 4, s));
+    T(cub::DeviceScan::InclusiveSum(tmp, tb, c->sizes, c->grp_ptr + 1, N, s));
+    T(cudaMalloc(&nb, NL * 6 * 4));
+    k_neighbours<<<gridn(NL), 256, 0, s>>>(c->rows, NL, row_of, nx, ny, nz, nb);
+    T(cudaGetLastError());
+
+    // P columns: batched FD over Ω_L from group-uniform sources, CB columns per pass
+    const long budget = 4L << 30;  // bytes for the two FD buffers
+    long CB = budget / (2L * 4 * NL);
+    CB = CB < 4 ? 4 : (CB / 4) * 4;
+    const long Npad = ((long)N + 3) / 4 * 4;
+    if (CB > Npad) CB = Npad;
+    T(cudaMalloc(&X, NL * CB * 4));
+    T(cudaMalloc(&Y, NL * CB * 4));
+    T(cudaMalloc(&P64, (long)N * N * 8));
+    for (long J0 = 0; J0 < N; J0 += CB) {
+        const int Jn = (int)((N - J0) < CB ? (N - J0) : CB);
+        k_init_cols<<<gridn(NL * CB), 256, 0, s>>>(row_group, NL, (int)CB, (int)J0, X);
+        T(cudaGetLastError());
+        float *a = X, *bb = Y;
+        for (int k = 0; k < c->n_fd; ++k) {
+            k_fd_cols<<<gridn(NL * 32), 256, 0, s>>>(a, bb, nb, NL, (int)CB, (float)lam);
+            float* t = a; a = bb; bb = t;
+        }
+        T(cudaGetLastError());
+        k_map_cols<<<gridn((long)N * Jn), 256, 0, s>>>(a, c->grp_ptr, c->grp_vox, row_of, N, (int)CB, (int)J0, Jn, P64);
+        T(cudaGetLastError());
+    }
+    T(cudaMalloc(&c->P, (long)N * N * c->b_w));
+    T(cudaMalloc(&c->Pdiag, (long)N * 4));
+    if (c->fmt == 0) k_quantize<float><<<N, 256, 0, s>>>(P64, c->sizes, N, (float*)c->P, c->Pdiag);
+    else if (c->fmt == 1) k_quantize<__half><<<N, 256, 0, s>>>(P64, c->sizes, N, (__half*)c->P, c->Pdiag);
+    else k_quantize<__nv_bfloat16><<<N, 256, 0, s>>>(P64, c->sizes, N, (__nv_bfloat16*)c->P, c->Pdiag);
+    T(cudaGetLastError());
+    T(cudaMalloc(&c->C, Npad * 4));
+    T(cudaMalloc(&c->C2, Npad * 4));
+    T(cudaStreamSynchronize(s));
+    T(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+#undef T
+    cleanup();
+    *out = c;
+    return FDIRW_OK;
+}
+
+static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
+{
+    const long N = c->N;
+    k_map<<<gridn(N * 32), 256, 0, s>>>(cbuf, c->grp_ptr, c->grp_vox, N, c->C);
+    if (c->fmt == 0) k_gemv<float><<<gridn(N * 32), 256, 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->C2);
+    else if (c->fmt == 1) k_gemv<__half><<<gridn(N * 32), 256, 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->C2);
+    else k_gemv<__nv_bfloat16><<<gridn(N * 32), 256, 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->C2);
+    k_remap<<<gridn(c->NL), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf);
+    return cudaGetLastError();
+}
+
+extern "C" fdirw_status fdirw_coarse_step(fdirw_coarse* c, const float* cin, float* cout, void* cuda_stream)
+{
+    if (!c || !cin || !cout) return cfail(FDIRW_E_INVALID, "NULL argument");
+    if (cin == cout) return cfail(FDIRW_E_ALIAS, "c_in == c_out");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    CK(cudaMemcpyAsync(cout, cin, c->nvox * 4, cudaMemcpyDeviceToDevice, s));
+    CK(coarse_enqueue(c, cout, s));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_coarse_run(fdirw_coarse* c, float* cbuf, int32_t n, void* cuda_stream)
+{
+    if (!c || !cbuf) return cfail(FDIRW_E_INVALID, "NULL argument");
+    if (n < 0) return cfail(FDIRW_E_INVALID, "n_steps must be >= 0");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    if (n == 0) return FDIRW_OK;
+    if (!c->graph || c->graph_c != cbuf) {
+        if (c->graph) cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+        CK(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = coarse_enqueue(c, cbuf, c->cap);
+        cudaGraph_t g = nullptr;
+        cudaError_t e2 = cudaStreamEndCapture(c->cap, &g);
+        if (e != cudaSuccess || e2 != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            return cfail(FDIRW_E_CUDA, std::string("coarse graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+        }
+        e = cudaGraphInstantiate(&c->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) { c->graph = nullptr; return cfail(FDIRW_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)); }
+        c->graph_c = cbuf;
+    }
+    for (int i = 0; i < n; ++i) CK(cudaGraphLaunch(c->graph, s));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_coarse_query(const fdirw_coarse* c, fdirw_coarse_info* info)
+{
+    if (!c || !info) return cfail(FDIRW_E_INVALID, "NULL argument");
+    info->n_fd = c->n_fd;
+    info->block = c->b;
+    info->n_groups = c->N;
+    info->n_region = c->NL;
+    info->p_bytes = (uint64_t)c->N * c->N * c->b_w + (uint64_t)c->N * 4;
+    info->flops_per_step = (uint64_t)c->N * (c->N + 1) + 2ull * c->NL;
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_coarse_export(const fdirw_coarse* c, double* P_host, int32_t* group_of_host)
+{
+    if (!c) return cfail(FDIRW_E_INVALID, "NULL argument");
+    CK(cudaSetDevice(c->device));
+    const long N = c->N;
+    if (P_host) {
+        std::vector<unsigned char> raw((size_t)N * N * c->b_w);
+        std::vector<float> dg(N);
+        CK(cudaMemcpy(raw.data(), c->P, raw.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dg.data(), c->Pdiag, N * 4, cudaMemcpyDeviceToHost));
+        for (long i = 0; i < N * N; ++i) {
+            double v;
+            if (c->fmt == 0) { float f; memcpy(&f, &raw[i * 4], 4); v = f; }
+            else if (c->fmt == 1) { __half h; memcpy(&h, &raw[i * 2], 2); v = __half2float(h); }
+            else { __nv_bfloat16 h; memcpy(&h, &raw[i * 2], 2); v = __bfloat162float(h); }
+            P_host[i] = v;
+        }
+        for (long I = 0; I < N; ++I) P_host[I * N + I] = dg[I];
+    }
+    if (group_of_host) CK(cudaMemcpy(group_of_host, c->group_of, c->nvox * 4, cudaMemcpyDeviceToHost));
+    return FDIRW_OK;
+}
+
+extern "C" void fdirw_coarse_destroy(fdirw_coarse* c) { coarse_free(c); }

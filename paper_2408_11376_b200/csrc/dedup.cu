@@ -7,7 +7,8 @@
 // paper's geometries most windows are homogeneous liquid (or liquid clipped by the
 // same domain face), e.g. 7.08 M sources but 0.75 M distinct windows at 192³ R5.
 //
-//   1. hash_kernel      two 64-bit polynomial hashes of every source window
+//   1. rowword_kernel   2-bit codes of every window row packed in one 64-bit word (L ≤ 17);
+//      hash_kernel      two 64-bit hashes of every source window's L² row words
 //   2. cub radix sort   (h1, source) pairs; stable, so a class's representative is
 //                       its smallest source index (deterministic)
 //   3. classify         run heads → class ids (inclusive scan − 1); class map in the padded layout
@@ -42,23 +43,43 @@ __device__ __forceinline__ unsigned window_code(const DedupArgs& a, int gx, int 
     return a.mask[((size_t)(gz - a.mz0) * a.ny + gy) * a.nx + gx];
 }
 
-__global__ void hash_kernel(const DedupArgs a, uint64_t* __restrict__ keys, int* __restrict__ vals,
+// Row words: rw(x, y, z) packs the L codes of (x−R … x+R, y, z), 2 bits each (L ≤ 17),
+// for y ∈ [−R, ny+R), z ∈ [sz0−R, sz1+R).  A window is then its L² row words.
+struct RowWords {
+    const uint64_t* w;
+    int nx, nyr, R, zr0;  // nyr = ny + 2R; plane zr0 = sz0 − R
+    __device__ __forceinline__ uint64_t at(int x, int y, int z) const
+    {
+        return w[((long)(z - zr0) * nyr + (y + R)) * nx + x];
+    }
+};
+
+__global__ void rowword_kernel(const DedupArgs a, uint64_t* __restrict__ rw, int nzr)
+{
+    const int nyr = a.ny + 2 * a.R;
+    const long n = (long)a.nx * nyr * nzr;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % a.nx), y = (int)((i / a.nx) % nyr) - a.R, z = (int)(i / ((long)a.nx * nyr)) + a.sz0 - a.R;
+        uint64_t v = 0;
+        for (int k = 0; k <= 2 * a.R; ++k) v |= (uint64_t)window_code(a, x - a.R + k, y, z) << (2 * k);
+        rw[i] = v;
+    }
+}
+
+__global__ void hash_kernel(const DedupArgs a, RowWords rw, uint64_t* __restrict__ keys, int* __restrict__ vals,
                             uint64_t* __restrict__ h2out)
 {
     const long n = (long)a.nx * a.ny * (a.sz1 - a.sz0);
-    const int L = 2 * a.R + 1;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         const int sx = (int)(i % a.nx), sy = (int)((i / a.nx) % a.ny), sz = a.sz0 + (int)(i / ((long)a.nx * a.ny));
         uint64_t h1 = 0x243F6A8885A308D3ull, h2 = 0x13198A2E03707344ull;
         int k = 0;
         for (int oz = -a.R; oz <= a.R; ++oz)
-            for (int oy = -a.R; oy <= a.R; ++oy)
-                for (int ox = -a.R; ox <= a.R; ++ox, ++k) {
-                    const uint64_t c = window_code(a, sx + ox, sy + oy, sz + oz) + 1u;
-                    h1 += c * (splitmix64(2 * k) | 1ull);
-                    h2 += c * (splitmix64(2 * k + 1) | 1ull);
-                }
-        (void)L;
+            for (int oy = -a.R; oy <= a.R; ++oy, ++k) {
+                const uint64_t c = rw.at(sx, sy + oy, sz + oz) + 1u;
+                h1 += c * (splitmix64(2 * k) | 1ull);
+                h2 += splitmix64(c ^ splitmix64(2 * k + 1));
+            }
         keys[i] = h1;
         vals[i] = (int)i;
         h2out[i] = h2;
@@ -86,9 +107,9 @@ __global__ void classify_kernel(const DedupArgs a, const uint64_t* __restrict__ 
     }
 }
 
-__global__ void verify_kernel(const DedupArgs a, const uint64_t* __restrict__ h2, const int* __restrict__ vals,
-                              const int* __restrict__ head, const int* __restrict__ cid, const int* __restrict__ rep,
-                              long n, int* __restrict__ mismatch)
+__global__ void verify_kernel(const DedupArgs a, RowWords rw, const uint64_t* __restrict__ h2,
+                              const int* __restrict__ vals, const int* __restrict__ head, const int* __restrict__ cid,
+                              const int* __restrict__ rep, long n, int* __restrict__ mismatch)
 {
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         if (head[i]) continue;
@@ -98,12 +119,11 @@ __global__ void verify_kernel(const DedupArgs a, const uint64_t* __restrict__ h2
         const int rx = r % a.nx, ry = (r / a.nx) % a.ny, rz = a.sz0 + r / (a.nx * a.ny);
         bool same = true;
         for (int oz = -a.R; oz <= a.R && same; ++oz)
-            for (int oy = -a.R; oy <= a.R && same; ++oy)
-                for (int ox = -a.R; ox <= a.R; ++ox)
-                    if (window_code(a, sx + ox, sy + oy, sz + oz) != window_code(a, rx + ox, ry + oy, rz + oz)) {
-                        same = false;
-                        break;
-                    }
+            for (int oy = -a.R; oy <= a.R; ++oy)
+                if (rw.at(sx, sy + oy, sz + oz) != rw.at(rx, ry + oy, rz + oz)) {  // exact: all L codes of the row
+                    same = false;
+                    break;
+                }
         if (!same) atomicOr(mismatch, 1);
     }
 }
@@ -182,14 +202,14 @@ cudaError_t dedup_classify(const DedupArgs& a, DedupResult* res, cudaStream_t s)
 {
     const long n = (long)a.nx * a.ny * (a.sz1 - a.sz0);
     res->n_src = n;
-    uint64_t *keys = nullptr, *keys2 = nullptr, *h2 = nullptr;
+    uint64_t *keys = nullptr, *keys2 = nullptr, *h2 = nullptr, *rwb = nullptr;
     int *vals = nullptr, *vals2 = nullptr, *head = nullptr, *cid = nullptr, *mism = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0, scan_bytes = 0;
     cudaError_t e = cudaSuccess;
     auto cleanup = [&]() {
         cudaFree(keys); cudaFree(keys2); cudaFree(h2); cudaFree(vals); cudaFree(vals2);
-        cudaFree(head); cudaFree(cid); cudaFree(mism); cudaFree(tmp);
+        cudaFree(head); cudaFree(cid); cudaFree(mism); cudaFree(tmp); cudaFree(rwb);
     };
 #define TRY(call)                       \
     do {                                \
@@ -208,7 +228,13 @@ cudaError_t dedup_classify(const DedupArgs& a, DedupResult* res, cudaStream_t s)
     TRY(cudaMalloc(&cid, n * 4));
     TRY(cudaMalloc(&mism, 4));
     TRY(cudaMemsetAsync(mism, 0, 4, s));
-    hash_kernel<<<grid_n(n), 256, 0, s>>>(a, keys, vals, h2);
+    const int nzr = a.sz1 - a.sz0 + 2 * a.R;
+    const long nrw = (long)a.nx * (a.ny + 2 * a.R) * nzr;
+    TRY(cudaMalloc(&rwb, nrw * 8));
+    rowword_kernel<<<grid_n(nrw), 256, 0, s>>>(a, rwb, nzr);
+    TRY(cudaGetLastError());
+    const RowWords rw{rwb, a.nx, a.ny + 2 * a.R, a.R, a.sz0 - a.R};
+    hash_kernel<<<grid_n(n), 256, 0, s>>>(a, rw, keys, vals, h2);
     TRY(cudaGetLastError());
     TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, 64, s));
     TRY(cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, head, cid, (int)n, s));
@@ -226,7 +252,7 @@ cudaError_t dedup_classify(const DedupArgs& a, DedupResult* res, cudaStream_t s)
     TRY(cudaMalloc(&res->rep, n_class * 4));
     classify_kernel<<<grid_n(n), 256, 0, s>>>(a, h2, vals2, head, cid, n, res->rep, a.class_pad, mism);
     TRY(cudaGetLastError());
-    verify_kernel<<<grid_n(n), 256, 0, s>>>(a, h2, vals2, head, cid, res->rep, n, mism);
+    verify_kernel<<<grid_n(n), 256, 0, s>>>(a, rw, h2, vals2, head, cid, res->rep, n, mism);
     TRY(cudaGetLastError());
     int mm = 0;
     TRY(cudaMemcpyAsync(&mm, mism, 4, cudaMemcpyDeviceToHost, s));

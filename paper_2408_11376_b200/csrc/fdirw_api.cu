@@ -44,6 +44,14 @@ static fdirw_status fail(fdirw_status s, const std::string& msg)
     return s;
 }
 
+namespace fdirw {
+const char* coarse_set_error(const std::string& m)  // coarse.cu shares the thread-local message
+{
+    g_err = m;
+    return g_err.c_str();
+}
+}  // namespace fdirw
+
 #define CUDA_TRY(call)                                                                              \
     do {                                                                                            \
         cudaError_t e_ = (call);                                                                    \

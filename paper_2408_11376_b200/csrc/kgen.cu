@@ -34,7 +34,8 @@ struct KgenShape {
     static constexpr int LLL = L * L * L;
     static constexpr int NT = ((LL + 31) / 32) * 32;
     static constexpr int NW = NT / 32;
-    static constexpr size_t smem_floats = 2 * (size_t)L * LL;             // double-buffered window
+    static constexpr int Lp = (L + 3) / 4 * 4;                             // column padded to float4s
+    static constexpr size_t smem_floats = 2 * (size_t)NT * Lp;             // double-buffered, column-major
     static constexpr size_t smem_bytes = smem_floats * 4 + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
 };
 
@@ -61,6 +62,31 @@ __device__ __forceinline__ double block_sum_f64(double v, double* red)
     __syncthreads();
     const double r = red[NW];
     __syncthreads();
+    return r;
+}
+
+// Packed fp32x2 arithmetic (sm_100a FADD2/FFMA2): two cells per instruction, each
+// lane an ordinary IEEE fp32 add / fma — bitwise identical to the scalar form.
+__device__ __forceinline__ unsigned long long pk2(float a, float b)
+{
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long v, float& a, float& b)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b)
+{
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c)
+{
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
 
@@ -104,47 +130,75 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
         }
         __syncthreads();
 
-        float c[L], lxm[L], lxp[L], lym[L], lyp[L], lzp[L];
+        constexpr int Lp = S::Lp, NQ = Lp / 4;
+        float c[Lp], lzp[L];
+        unsigned long long lxm2[Lp / 2], lxp2[Lp / 2], lym2[Lp / 2], lyp2[Lp / 2];  // (z, z+1) pairs
 #pragma unroll
-        for (int z = 0; z < L; ++z) {
-            const int i = z * LL + t;
-            const unsigned p = col ? ph[i] : 2u;
-            lxm[z] = col ? face_lambda(p, ph[i + oxm], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-            lxp[z] = col ? face_lambda(p, ph[i + oxp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-            lym[z] = col ? face_lambda(p, ph[i + oym], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-            lyp[z] = col ? face_lambda(p, ph[i + oyp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-            lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-            if (oxm == 0) lxm[z] = 0.f;  // no neighbour inside the window: no flux
-            if (oxp == 0) lxp[z] = 0.f;
-            if (oym == 0) lym[z] = 0.f;
-            if (oyp == 0) lyp[z] = 0.f;
-            c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
+        for (int h = 0; h < Lp / 2; ++h) {
+            float v[4][2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int z = 2 * h + u;
+                const int i = z * LL + t;
+                const bool ok = col && z < L;
+                const unsigned p = ok ? ph[i] : 2u;
+                v[0][u] = (ok && oxm) ? face_lambda(p, ph[i + oxm], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                v[1][u] = (ok && oxp) ? face_lambda(p, ph[i + oxp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                v[2][u] = (ok && oym) ? face_lambda(p, ph[i + oym], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                v[3][u] = (ok && oyp) ? face_lambda(p, ph[i + oyp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                if (z < L)
+                    lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
+            }
+            lxm2[h] = pk2(v[0][0], v[0][1]);
+            lxp2[h] = pk2(v[1][0], v[1][1]);
+            lym2[h] = pk2(v[2][0], v[2][1]);
+            lyp2[h] = pk2(v[3][0], v[3][1]);
         }
 
-        // n_fd Jacobi substeps; faces summed −x,+x,−y,+y,−z,+z
+        // n_fd Jacobi substeps; faces summed −x,+x,−y,+y,−z,+z.  The window lives in
+        // smem column-major (thread t's column at t·Lp, float4-aligned): a thread
+        // reads each lateral neighbour column with Lp/4 128-bit loads (conflict-free
+        // for Lp ∈ {4, 8, 12, 20}), adds the four lateral fluxes two cells at a time
+        // (FADD2/FFMA2), then the two z fluxes from its own registers.
         for (int k = 0; k < a.n_fd; ++k) {
-            float* b = buf + (k & 1) * (L * LL);
+            float* b = buf + (k & 1) * (NT * Lp);
             if (col) {
 #pragma unroll
-                for (int z = 0; z < L; ++z) b[z * LL + t] = c[z];
+                for (int q = 0; q < NQ; ++q)
+                    *reinterpret_cast<float4*>(b + t * Lp + 4 * q) =
+                        make_float4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
             }
             __syncthreads();
             if (col) {
-                float prev = 0.f;
+                float nw[Lp];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const float4 xm = *reinterpret_cast<const float4*>(b + (t + oxm) * Lp + 4 * q);
+                    const float4 xp = *reinterpret_cast<const float4*>(b + (t + oxp) * Lp + 4 * q);
+                    const float4 ym = *reinterpret_cast<const float4*>(b + (t + oym) * Lp + 4 * q);
+                    const float4 yp = *reinterpret_cast<const float4*>(b + (t + oyp) * Lp + 4 * q);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int h = 2 * q + hh;
+                        const unsigned long long cc = pk2(c[2 * h], c[2 * h + 1]);
+                        unsigned long long acc = cc;
+                        acc = fma2(lxm2[h], sub2(hh ? pk2(xm.z, xm.w) : pk2(xm.x, xm.y), cc), acc);
+                        acc = fma2(lxp2[h], sub2(hh ? pk2(xp.z, xp.w) : pk2(xp.x, xp.y), cc), acc);
+                        acc = fma2(lym2[h], sub2(hh ? pk2(ym.z, ym.w) : pk2(ym.x, ym.y), cc), acc);
+                        acc = fma2(lyp2[h], sub2(hh ? pk2(yp.z, yp.w) : pk2(yp.x, yp.y), cc), acc);
+                        upk2(acc, nw[2 * h], nw[2 * h + 1]);
+                    }
+                }
 #pragma unroll
                 for (int z = 0; z < L; ++z) {
-                    const float* bz = b + z * LL + t;
-                    const float cz = c[z];
-                    float acc = cz;
-                    acc = fmaf(lxm[z], bz[oxm] - cz, acc);
-                    acc = fmaf(lxp[z], bz[oxp] - cz, acc);
-                    acc = fmaf(lym[z], bz[oym] - cz, acc);
-                    acc = fmaf(lyp[z], bz[oyp] - cz, acc);
-                    if (z > 0) acc = fmaf(lzp[z - 1], prev - cz, acc);
-                    if (z < L - 1) acc = fmaf(lzp[z], c[z + 1] - cz, acc);
-                    prev = cz;
-                    c[z] = acc;
+                    float acc = nw[z];
+                    if (z > 0) acc = fmaf(lzp[z - 1], c[z - 1] - c[z], acc);
+                    if (z < L - 1) acc = fmaf(lzp[z], c[z + 1] - c[z], acc);
+                    nw[z] = acc;
                 }
+#pragma unroll
+                for (int z = 0; z < L; ++z) c[z] = nw[z];
             }
         }
 

@@ -13,9 +13,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def fd():
-    from paper_2408_11376_b200 import build as b
+    import __graft_entry__
 
-    b.build()
+    __graft_entry__.build()
     import paper_2408_11376_b200 as fd
 
     return fd

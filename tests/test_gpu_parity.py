@@ -16,9 +16,9 @@ def fd():
     import torch
 
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
-    from paper_2408_11376_b200 import build as b
+    import __graft_entry__
 
-    b.build()
+    __graft_entry__.build()
     import paper_2408_11376_b200 as fd
 
     return fd
@@ -305,3 +305,46 @@ def test_cfg5_r8_sampled(fd, oracle_lib):
     tb = (143, 147, 93, 97, 94, 97)
     ref = oracle_lib.step_box(pb, c0.astype(np.float64), tb)
     assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= 5e-3
+
+
+# ------------------------------------------------------------------ NEXT row N1: coarse-mesh FDiRW
+@pytest.mark.parametrize("fmt,b", [("fp32", 3), ("bf16", 4), ("fp16", 5)])
+def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b):
+    """N1 (Eqs.10-15): GPU-built P vs the oracle's P (FD from group-uniform
+    sources, group means), and coarse steps vs the oracle's map → P·C → remap."""
+    import torch
+    from oracle import coarse as oc
+
+    shape = (22, 21, 23)
+    mask = fi.porous_particle(shape, 6, pore_r=(1.0, 2.0), porosity=0.3, seed=7)
+    region = fi.near_field(mask, 6, margin=3)
+    cfg = small_cfg(shape, 1, 200, weights=fmt)
+    pb = oracle_problem(cfg, mask)
+    P, g, sizes = oc.build_P(pb, region, b=b)
+    c0 = fi.initial_c(mask, "random", seed=7).astype(np.float64)
+    ref = c0
+    for _ in range(3):
+        ref = oc.step(P, g, sizes, ref)
+    ctx = fd.coarse_build(lib_params(cfg, fmt), region, block=b)
+    try:
+        info = ctx.info
+        assert info["n_groups"] == len(sizes) and info["n_region"] == int(region.sum())
+        assert info["flops_per_step"] == oc.flop_count(len(sizes), int(region.sum()))
+        Pg, gg = fd.coarse_export(ctx)
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        out = torch.empty_like(c)
+        fd.coarse_step(ctx, c, out)
+        fd.coarse_run(ctx, out, 2)
+        got = out.cpu().numpy()
+    finally:
+        fd.coarse_destroy(ctx)
+    np.testing.assert_array_equal(gg, g)
+    tolP = {"fp32": 2e-6, "fp16": 2e-3, "bf16": 8e-3}[fmt]
+    off = ~np.eye(len(sizes), dtype=bool)
+    assert np.abs(Pg[off] - P[off]).max() <= tolP * max(P.max(), 1e-30)
+    np.testing.assert_allclose(sizes @ Pg, sizes, rtol=3e-7)        # column mass fix-up
+    tol = 1e-5 if fmt == "fp32" else 5e-3
+    assert rel_l2(got[region == 1], ref[region == 1]) <= tol
+    np.testing.assert_array_equal(got[region == 0], c0.astype(np.float32)[region == 0])
+    m0 = c0.astype(np.float32)[region == 1].astype(np.float64).sum()
+    assert abs(got[region == 1].astype(np.float64).sum() - m0) / m0 <= 1e-6

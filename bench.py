@@ -194,6 +194,53 @@ def _workload_name(cfg):
         cfg.weights, cfg.n_fd or "derived")
 
 
+def run_coarse(args):
+    """NEXT row N1: the paper's coarse-mesh FDiRW step on the near-field liquid
+    of the config's particle (r_p + 5Δh), b = 5, 1 GPU.  Metric: fine Ω_L
+    voxels updated per second (N_L per step)."""
+    import torch
+
+    import paper_2408_11376_b200 as fd
+
+    cfg = fi.config(args.config, weights=args.weights)
+    mask = cfg.mask()
+    r_p = cfg.geometry.get("r_p", 50)
+    region = fi.near_field(mask, r_p)
+    nz, ny, nx = cfg.shape
+    params = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt,
+                       radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    ctx = fd.coarse_build(params, region, block=args.block)
+    t_build = time.perf_counter() - t
+    info = ctx.info
+    c = torch.from_numpy(fi.initial_c(mask, "paper")).cuda()
+    fd.coarse_run(ctx, c, args.warmup)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        fd.coarse_run(ctx, c, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    NL, N = info["n_region"], info["n_groups"]
+    line = {"metric": "voxel-updates/s (coarse-mesh FDiRW step, NEXT row N1)", "value": NL / (ms * 1e-3),
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": {"fp32": "f32", "fp16": "f16", "bf16": "bf16"}[cfg.weights] + "-P/f32-accum",
+            "data": "synthetic",
+            "config": {"workload": "N1 coarse mesh on the %s near-field liquid (r_p+5), b=%d" % (cfg.name, args.block),
+                       "N_L": NL, "N": N, "P_bytes": info["p_bytes"], "n_fd": info["n_fd"]},
+            "paper_context": {"R50_N_L": 329404, "R50_N": 2515, "V100_fdirw_s_per_1000_steps": 0.7,
+                              "source": "P:181 Fig.7e, P:262-263 Table 3"},
+            "flops_per_step": info["flops_per_step"],
+            "build_seconds": t_build, "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+    fd.coarse_destroy(ctx)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -204,10 +251,15 @@ def main():
     ap.add_argument("--impl", default="fdirw", choices=["fdirw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--mode", default="fine", choices=["fine", "coarse"],
+                    help="fine: the north_star windowed step (default); coarse: NEXT row N1")
+    ap.add_argument("--block", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "coarse":
+        return run_coarse(args)
 
     import torch
     import torch.distributed as dist

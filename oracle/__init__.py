@@ -60,8 +60,8 @@ def lib():
         L.oracle_kernel.argtypes = [P, D, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
         L.oracle_build_kernels.argtypes = [P, D, vp, vp, vp]
         L.oracle_step_scatter.argtypes = [P, vp, vp, vp, vp, vp]
-        L.oracle_quantize.argtypes = [P, vp, ctypes.c_long, ctypes.c_int, ctypes.c_int, vp]
-        L.oracle_fd_whole_grid.argtypes = [P, D, vp, vp, ctypes.c_int, vp]
+        L.oracle_quantize.argtypes = [P, vp, ctypes.c_long, ctypes.c_int, ctypes.c_int, vp, vp]
+        L.oracle_fd_whole_grid.argtypes = [P, D, vp, vp, ctypes.c_int, ctypes.c_double, vp]
         L.oracle_f32_to_f16.argtypes = [ctypes.c_float]
         L.oracle_f32_to_f16.restype = ctypes.c_uint16
         L.oracle_f32_to_bf16.argtypes = [ctypes.c_float]
@@ -165,12 +165,32 @@ def build_kernels(pb: Problem, box=None) -> np.ndarray:
     return W
 
 
-def quantize(pb: Problem, W: np.ndarray, fmt: str, mass_fix: bool = True) -> np.ndarray:
-    """O5: the stored operator (decoded to fp64), diagonal in the centre slot."""
+def quantize(pb: Problem, W: np.ndarray, fmt: str, mass_fix: bool = True, box=None) -> np.ndarray:
+    """O5: the stored operator (decoded to fp64), diagonal in the centre slot.  With a far
+    field (mask 2, N2) the kernels of windows that touch it keep their own mass M = ΣW;
+    `box` = the source box of W (default: whole grid) locates those windows."""
     W = np.ascontiguousarray(W, np.float64)
     Wq = np.empty_like(W)
-    lib().oracle_quantize(ctypes.byref(pb._params()), _ptr(W), W.size // pb.K, FMT[fmt], int(mass_fix), _ptr(Wq))
+    ow = None
+    if (pb.mask == 2).any():
+        ow = np.ascontiguousarray(open_windows(pb, box).ravel().astype(np.uint8))
+    lib().oracle_quantize(ctypes.byref(pb._params()), _ptr(W), W.size // pb.K, FMT[fmt], int(mass_fix), _ptr(Wq),
+                          _ptr(ow) if ow is not None else None)
     return Wq
+
+
+def open_windows(pb: Problem, box=None) -> np.ndarray:
+    """bool [bz][by][bx]: does the source's window contain a far-field cell (mask 2)?"""
+    nz, ny, nx = pb.shape
+    box = clip_box(pb, box or (0, nx, 0, ny, 0, nz))
+    R = pb.R
+    far = np.pad(pb.mask == 2, R)
+    out = np.zeros((box[5] - box[4], box[3] - box[2], box[1] - box[0]), bool)
+    for oz in range(2 * R + 1):
+        for oy in range(2 * R + 1):
+            for ox in range(2 * R + 1):
+                out |= far[box[4] + oz:box[5] + oz, box[2] + oy:box[3] + oy, box[0] + ox:box[1] + ox]
+    return out
 
 
 def step_scatter(pb: Problem, W: np.ndarray, sbox, C_old: np.ndarray, tbox) -> np.ndarray:
@@ -196,7 +216,7 @@ def step_box(pb: Problem, C_old: np.ndarray, tbox, fmt: str | None = None, mass_
     if W is None:
         W = build_kernels(pb, sbox)
     if fmt is not None:
-        W = quantize(pb, W, fmt, mass_fix)
+        W = quantize(pb, W, fmt, mass_fix, box=sbox)
     return step_scatter(pb, W, sbox, C_old, tbox)
 
 
@@ -213,12 +233,14 @@ def step_full(pb: Problem, C_old: np.ndarray, steps: int = 1, fmt: str | None = 
     return C
 
 
-def fd_whole_grid(pb: Problem, C0: np.ndarray, nsub: int) -> np.ndarray:
-    """O6: nsub whole-grid explicit FD substeps (closed domain)."""
+def fd_whole_grid(pb: Problem, C0: np.ndarray, nsub: int, c_far: float = 0.0) -> np.ndarray:
+    """O6: nsub whole-grid explicit FD substeps (closed domain; far-field cells, mask 2,
+    held at c_far)."""
     p, d = _pd(pb)
     C0 = np.ascontiguousarray(C0, np.float64)
     out = np.empty_like(C0)
-    lib().oracle_fd_whole_grid(ctypes.byref(p), ctypes.byref(d), _ptr(pb.mask), _ptr(C0), int(nsub), _ptr(out))
+    lib().oracle_fd_whole_grid(ctypes.byref(p), ctypes.byref(d), _ptr(pb.mask), _ptr(C0), int(nsub), float(c_far),
+                               _ptr(out))
     return out
 
 

@@ -79,8 +79,12 @@ int oracle_derive(const oracle_params* p, oracle_derived* d)
     return OR_OK;
 }
 
+/* phase codes: 0 slow, 1 fast, 2 far-field liquid reservoir (NEXT row N2: a fast-phase
+ * Dirichlet cell) — for the face number it counts as fast. */
 static double face_lambda(const oracle_derived* d, int pi, int pj)
 {
+    pi = pi != 0;
+    pj = pj != 0;
     if (pi && pj) return d->lam_ff;
     if (!pi && !pj) return d->lam_ss;
     return d->lam_fs;
@@ -98,6 +102,10 @@ static double face_lambda(const oracle_derived* d, int pi, int pj)
  * window AND in the domain; faces leaving either carry no flux (A2, A3, A21).
  * Jacobi: every flux uses the previous iterate.  Output W[o] = c^{n_fd}(s+o),
  * 0 for window cells outside the domain.
+ * N2 (open domain): window cells with mask 2 are the far-field reservoir held at 0
+ * (absorbing Dirichlet: the kernel is the response to c(t0) with
+ * c_far = 0; the c_far part is p_BC): their value stays 0 and faces into them
+ * carry flux λ(p_i, fast)·(0 − c_i).  A source on a far-field cell has W = 0.
  * ------------------------------------------------------------------------- */
 void oracle_kernel(const oracle_params* p, const oracle_derived* d, const uint8_t* mask,
                    int sx, int sy, int sz, double* W)
@@ -106,6 +114,7 @@ void oracle_kernel(const oracle_params* p, const oracle_derived* d, const uint8_
     double* cur = (double*)calloc((size_t)K, sizeof(double));
     double* nxt = (double*)calloc((size_t)K, sizeof(double));
     uint8_t* act = (uint8_t*)calloc((size_t)K, 1);
+    uint8_t* res = (uint8_t*)calloc((size_t)K, 1); /* far-field reservoir cell */
     uint8_t* ph = (uint8_t*)calloc((size_t)K, 1);
     double* lam = (double*)calloc((size_t)K * 6, sizeof(double)); /* per cell, per face */
     int* nbr = (int*)malloc((size_t)K * 6 * sizeof(int));
@@ -117,8 +126,9 @@ void oracle_kernel(const oracle_params* p, const oracle_derived* d, const uint8_
                 int i = ((oz + R) * L + (oy + R)) * L + (ox + R);
                 int x = sx + ox, y = sy + oy, z = sz + oz;
                 int in = x >= 0 && x < p->nx && y >= 0 && y < p->ny && z >= 0 && z < p->nz;
-                act[i] = (uint8_t)in;
                 ph[i] = in ? mask[((size_t)z * p->ny + y) * p->nx + x] : 0;
+                res[i] = (uint8_t)(in && ph[i] == 2);
+                act[i] = (uint8_t)(in && ph[i] != 2);
             }
     for (int oz = -R; oz <= R; ++oz)
         for (int oy = -R; oy <= R; ++oy)
@@ -129,7 +139,7 @@ void oracle_kernel(const oracle_params* p, const oracle_derived* d, const uint8_
                     int j = -1;
                     if (qx >= -R && qx <= R && qy >= -R && qy <= R && qz >= -R && qz <= R)
                         j = ((qz + R) * L + (qy + R)) * L + (qx + R);
-                    if (j >= 0 && act[i] && act[j]) {
+                    if (j >= 0 && act[i] && (act[j] || res[j])) {
                         nbr[i * 6 + f] = j;
                         lam[i * 6 + f] = face_lambda(d, ph[i], ph[j]);
                     } else {
@@ -138,7 +148,7 @@ void oracle_kernel(const oracle_params* p, const oracle_derived* d, const uint8_
                     }
                 }
             }
-    cur[(R * L + R) * L + R] = 1.0;
+    if (act[(R * L + R) * L + R]) cur[(R * L + R) * L + R] = 1.0;
     for (int k = 0; k < d->n_fd; ++k) {
         for (int i = 0; i < K; ++i) {
             if (!act[i]) { nxt[i] = 0.0; continue; }
@@ -152,7 +162,7 @@ void oracle_kernel(const oracle_params* p, const oracle_derived* d, const uint8_
         double* t = cur; cur = nxt; nxt = t;
     }
     memcpy(W, cur, (size_t)K * sizeof(double));
-    free(cur); free(nxt); free(act); free(ph); free(lam); free(nbr);
+    free(cur); free(nxt); free(act); free(res); free(ph); free(lam); free(nbr);
 }
 
 /* Kernels of every source in the box [x0,x1)×[y0,y1)×[z0,z1) (clipped to the
@@ -217,7 +227,9 @@ void oracle_step_scatter(const oracle_params* p, const double* W, const int32_t*
  * role Eq.7 plays in the paper).  IEEE 754 round-to-nearest-even (ref 26,
  * P:151; A11).
  *   for o ≠ centre:  Wq[o] = RNE_fmt( RNE_fp32( W[o] ) )
- *   diag            = RNE_fp32( 1 − Σ_{o≠centre, ascending o} Wq[o] )   (fp64 sum)
+ *   diag            = RNE_fp32( M − Σ_{o≠centre, ascending o} Wq[o] )   (fp64 sum)
+ *   M = 1 for a closed window (Σ_o W = 1, reading A2); with a far field (N2) the
+ *   kernel keeps M = Σ_o W (ascending o) and the rest went to the reservoir
  *   (mass_fix = 0:  diag = RNE_fmt(RNE_fp32(W[centre])))
  * Wq[centre] ← diag, so oracle_step_scatter applies the stored operator.
  * fmt: 0 fp32, 1 fp16 (binary16), 2 bf16.
@@ -283,35 +295,43 @@ double oracle_round_fmt(double w, int fmt)
     return (double)f;
 }
 
-void oracle_quantize(const oracle_params* p, const double* W, long nsrc, int fmt, int mass_fix, double* Wq)
+void oracle_quantize(const oracle_params* p, const double* W, long nsrc, int fmt, int mass_fix, double* Wq,
+                     const uint8_t* open_window)
 {
     const int L = 2 * p->R + 1, K = L * L * L, c = K / 2;
     for (long n = 0; n < nsrc; ++n) {
         const double* w = W + (size_t)n * K;
         double* q = Wq + (size_t)n * K;
-        double sum = 0.0;
+        double M = 1.0, sum = 0.0;
+        if (open_window && open_window[n]) {
+            M = 0.0;
+            for (int o = 0; o < K; ++o) M += w[o];
+        }
         for (int o = 0; o < K; ++o) {
             if (o == c) continue;
             q[o] = oracle_round_fmt(w[o], fmt);
             sum += q[o];
         }
-        q[c] = mass_fix ? (double)(float)(1.0 - sum) : oracle_round_fmt(w[c], fmt);
+        q[c] = mass_fix ? (double)(float)(M - sum) : oracle_round_fmt(w[c], fmt);
     }
 }
 
 /* ---------------------------------------------------------------------------
  * O6. Whole-grid explicit FD (the paper's fine-mesh FD solver, §4.1,
  * as a brute-force reference): the same 7-point Jacobi update as
- * oracle_kernel, on the whole closed domain, for nsub substeps.
+ * oracle_kernel, on the whole closed domain, for nsub substeps.  Far-field
+ * cells (mask 2, N2) are held at c_far (Dirichlet, P:76 / SPEC S:190).
  * ------------------------------------------------------------------------- */
 void oracle_fd_whole_grid(const oracle_params* p, const oracle_derived* d, const uint8_t* mask,
-                          const double* C0, int nsub, double* Cout)
+                          const double* C0, int nsub, double c_far, double* Cout)
 {
     const int nx = p->nx, ny = p->ny, nz = p->nz;
     const size_t N = (size_t)nx * ny * nz;
     double* cur = (double*)malloc(N * sizeof(double));
     double* nxt = (double*)malloc(N * sizeof(double));
     memcpy(cur, C0, N * sizeof(double));
+    for (size_t i = 0; i < N; ++i)
+        if (mask[i] == 2) cur[i] = c_far;
     static const int DX[6] = {-1, 1, 0, 0, 0, 0}, DY[6] = {0, 0, -1, 1, 0, 0}, DZ[6] = {0, 0, 0, 0, -1, 1};
     for (int k = 0; k < nsub; ++k) {
 #pragma omp parallel for
@@ -319,6 +339,7 @@ void oracle_fd_whole_grid(const oracle_params* p, const oracle_derived* d, const
             for (int y = 0; y < ny; ++y)
                 for (int x = 0; x < nx; ++x) {
                     size_t i = ((size_t)z * ny + y) * nx + x;
+                    if (mask[i] == 2) { nxt[i] = c_far; continue; }
                     double acc = cur[i];
                     for (int f = 0; f < 6; ++f) {
                         int qx = x + DX[f], qy = y + DY[f], qz = z + DZ[f];

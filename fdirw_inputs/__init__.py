@@ -135,6 +135,15 @@ def near_field(mask: np.ndarray, r_p: float, margin: float = 5.0, center=None) -
     return ((mask == 1) & inside).astype(np.uint8)
 
 
+def with_far_field(mask: np.ndarray, r_p: float, margin: float = 5.0, center=None) -> np.ndarray:
+    """NEXT row N2 layout: liquid beyond r_p + margin·Δh of the particle centre becomes
+    the far-field reservoir (label 2); the near field (solid + liquid within) keeps 0/1."""
+    nf = near_field(mask, r_p, margin, center)
+    out = mask.copy()
+    out[(mask == 1) & (nf == 0)] = 2
+    return out
+
+
 def random_two_phase(shape, p_fast: float = 0.6, seed: int = 0) -> np.ndarray:
     """i.i.d. Bernoulli phases — a stress input for small parity cases (not a paper shape)."""
     rng = np.random.Generator(np.random.PCG64(seed))
@@ -164,6 +173,8 @@ class Config:
     weights: str
     n_fd: int = 0
     geometry: dict = field(default_factory=dict)
+    v_far: float = 0.0    # N2: far-field reservoir volume in voxels (0 = closed domain)
+    c_far0: float = 0.0   # N2: initial far-field concentration
 
     @property
     def K(self) -> int:
@@ -172,8 +183,10 @@ class Config:
     def mask(self) -> np.ndarray:
         g = dict(self.geometry)
         kind = g.pop("kind")
+        far_margin = g.pop("far_margin", None)
         if kind == "particle":
-            return porous_particle(self.shape, **g)
+            m = porous_particle(self.shape, **g)
+            return with_far_field(m, g["r_p"], far_margin) if far_margin is not None else m
         if kind == "block":
             return porous_block(self.shape, **g)
         if kind == "tiled":
@@ -211,9 +224,15 @@ def config(name: str, n_fd: int | None = None, weights: str | None = None) -> Co
         c = Config("cfg5", (192, 192, 192), 8, dh=TABLE1["dh"], D_fast=D_FAST_SI, D_slow=D_FAST_SI * 1e-8,
                    dt=TABLE1["dt"], weights="bf16",
                    geometry=dict(kind="particle", r_p=50, pore_r=(2.0, 4.0), porosity=0.3, seed=3))
+    elif name == "cfg3o":  # NEXT row N2: the paper's open R50 model — near field r_p+5Δh inside a
+        # grid that just encloses it, far-field reservoir V_L^far = 1.80e-10 mL (Table 1) = 1.8e8 Δh³
+        c = Config("cfg3o", (120, 120, 120), 5, dh=TABLE1["dh"], D_fast=D_FAST_SI, D_slow=D_SLOW_SI,
+                   dt=TABLE1["dt"], weights="bf16",
+                   geometry=dict(kind="particle", r_p=50, pore_r=(2.0, 4.0), porosity=0.3, seed=3, far_margin=5.0),
+                   v_far=1.80e-16 / TABLE1["dh"] ** 3, c_far0=TABLE1["c_L0"])
     else:
         raise ValueError(name)
-    if n_fd is not None and name in ("cfg3", "cfg4", "cfg5"):
+    if n_fd is not None and name in ("cfg3", "cfg4", "cfg5", "cfg3o"):
         c.n_fd = n_fd
     if weights is not None:
         c.weights = weights

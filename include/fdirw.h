@@ -80,6 +80,13 @@ typedef struct {
                                x = D_max·Δt/(0.1·Δh²) (λ* = 0.1 from Table 1, reading A5)     */
     int32_t weights;        /* fdirw_weight_t: storage format of W (accumulation is fp32)     */
     uint32_t flags;         /* FDIRW_F_*                                                       */
+    double v_far;           /* NEXT row N2: far-field reservoir volume in voxels (V_L^far/Δh³,
+                               P:93 Table 1); 0 = closed domain.  With v_far > 0 the mask may
+                               hold 2 = far-field liquid: those voxels are not sources/targets
+                               (their concentration is the scalar c_far), window FD
+                               holds them at 0 (absorbing), each target gets p_BC(x)·c_far
+                               with p_BC(x) = 1 − Σ_s W̃_s(x−s) (reading A26), and every step
+                               ends with Eq.7: c_far = (M0 − Σ c)/v_far (see fdirw_far_init). */
 } fdirw_params;
 
 /* Slab decomposition (world > 1): rank r owns target planes [z_begin, z_end).
@@ -164,6 +171,17 @@ fdirw_status fdirw_mass(fdirw_ctx* ctx, const float* c_dev, double* out_host, vo
 
 /* Fills *info (host).  Never fails on a valid ctx. */
 fdirw_status fdirw_query(const fdirw_ctx* ctx, fdirw_info* info);
+
+/* N2 (v_far > 0 only): set the reservoir c_far(t0) and the conserved total
+ * M0 = Σ c_dev + c_far0·v_far (Σc_{S+L}(t0) of Eq.7, fp64; all ranks must call it;
+ * far-field voxels of c_dev are ignored).  *M0_out (may be NULL) receives M0.
+ * Synchronises cuda_stream.  FDIRW_E_STATE on a closed-domain context. */
+fdirw_status fdirw_far_init(fdirw_ctx* ctx, const float* c_dev, double c_far0, double* M0_out, void* cuda_stream);
+/* N2 on virtual ranks (see fdirw_step_virtual): the same initialisation for all n contexts. */
+fdirw_status fdirw_far_init_virtual(fdirw_ctx* const* ctxs, int32_t n, const float* const* c_dev, double c_far0,
+                                    double* M0_out, void* cuda_stream);
+/* N2: current c_far (after the last enqueued step).  Synchronises cuda_stream. */
+fdirw_status fdirw_far_get(fdirw_ctx* ctx, double* c_far_out, void* cuda_stream);
 
 /* Frees everything the context owns (synchronises its device first).  NULL is a no-op. */
 void fdirw_destroy(fdirw_ctx* ctx);

@@ -35,14 +35,15 @@ F_NO_DEDUP = 2
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
            "fdirw_export_kernels", "fdirw_step_virtual", "fdirw_coarse_build", "fdirw_coarse_step",
-           "fdirw_coarse_run", "fdirw_coarse_query", "fdirw_coarse_export", "fdirw_coarse_destroy"]
+           "fdirw_coarse_run", "fdirw_coarse_query", "fdirw_coarse_export", "fdirw_coarse_destroy",
+           "fdirw_far_init", "fdirw_far_init_virtual", "fdirw_far_get"]
 
 
 class fdirw_params(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
                 ("dh", ctypes.c_double), ("D_fast", ctypes.c_double), ("D_slow", ctypes.c_double),
                 ("dt", ctypes.c_double), ("radius", ctypes.c_int32), ("n_fd", ctypes.c_int32),
-                ("weights", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+                ("weights", ctypes.c_int32), ("flags", ctypes.c_uint32), ("v_far", ctypes.c_double)]
 
 
 class fdirw_dist(ctypes.Structure):
@@ -114,6 +115,13 @@ _lib.fdirw_coarse_export.argtypes = [_vp, _vp, _vp]
 _lib.fdirw_coarse_export.restype = _st
 _lib.fdirw_coarse_destroy.argtypes = [_vp]
 _lib.fdirw_coarse_destroy.restype = None
+_lib.fdirw_far_init.argtypes = [_vp, _vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double), _vp]
+_lib.fdirw_far_init.restype = _st
+_lib.fdirw_far_init_virtual.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32, ctypes.POINTER(_vp), ctypes.c_double,
+                                        ctypes.POINTER(ctypes.c_double), _vp]
+_lib.fdirw_far_init_virtual.restype = _st
+_lib.fdirw_far_get.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), _vp]
+_lib.fdirw_far_get.restype = _st
 
 
 class FdirwError(RuntimeError):
@@ -161,10 +169,11 @@ class Params:
     n_fd: int = 0
     weights: str = "bf16"
     flags: int = 0
+    v_far: float = 0.0  # N2: far-field reservoir volume (voxels); 0 = closed domain
 
     def c(self) -> fdirw_params:
         return fdirw_params(self.nx, self.ny, self.nz, self.dh, self.D_fast, self.D_slow, self.dt, self.radius,
-                            self.n_fd, WEIGHTS[self.weights], self.flags)
+                            self.n_fd, WEIGHTS[self.weights], self.flags, self.v_far)
 
 
 class Context:
@@ -340,3 +349,26 @@ def coarse_destroy(ctx: Coarse):
     if ctx.handle and ctx.handle.value:
         _lib.fdirw_coarse_destroy(ctx.handle)
         ctx.handle = ctypes.c_void_p()
+
+
+# ---- NEXT row N2: far-field reservoir (Eq.7) ---------------------------------------
+def far_init(ctx: Context, c, c_far0: float, stream=None) -> float:
+    """fdirw_far_init: sets c_far(t0) and returns M0 = Σ c + c_far0·v_far (Eq.7's Σc_{S+L}(t0))."""
+    m0 = ctypes.c_double()
+    _check(_lib.fdirw_far_init(ctx.handle, _dptr(c), float(c_far0), ctypes.byref(m0), _stream(stream)))
+    return m0.value
+
+
+def far_init_virtual(ctxs, cs, c_far0: float, stream=None) -> float:
+    n = len(ctxs)
+    H = (_vp * n)(*[c.handle.value for c in ctxs])
+    C = (_vp * n)(*[_dptr(t).value for t in cs])
+    m0 = ctypes.c_double()
+    _check(_lib.fdirw_far_init_virtual(H, n, C, float(c_far0), ctypes.byref(m0), _stream(stream)))
+    return m0.value
+
+
+def far_get(ctx: Context, stream=None) -> float:
+    v = ctypes.c_double()
+    _check(_lib.fdirw_far_get(ctx.handle, ctypes.byref(v), _stream(stream)))
+    return v.value

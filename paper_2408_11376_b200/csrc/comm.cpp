@@ -26,6 +26,7 @@ struct Nccl {
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -59,6 +60,7 @@ Nccl* nccl_load(std::string* err)
     LOAD(GroupStart, "ncclGroupStart");
     LOAD(GroupEnd, "ncclGroupEnd");
     LOAD(AllReduce, "ncclAllReduce");
+    LOAD(AllGather, "ncclAllGather");
     LOAD(GetErrorString, "ncclGetErrorString");
 #undef LOAD
     g_nccl = n;
@@ -110,6 +112,14 @@ int nccl_allreduce_sum_f64(Nccl* n, void* comm, double* buf, cudaStream_t s, std
 {
     return check(n, n->AllReduce(buf, buf, 1, ncclFloat64, ncclSum, static_cast<ncclComm_t>(comm), s),
                  "ncclAllReduce", err);
+}
+
+// N2: every rank's [n_tiles, tile sums...] block, so each rank sums them in global tile order
+int nccl_allgather_f64(Nccl* n, void* comm, const double* send, long count, double* recv, cudaStream_t s,
+                       std::string* err)
+{
+    return check(n, n->AllGather(send, recv, (size_t)count, ncclFloat64, static_cast<ncclComm_t>(comm), s),
+                 "ncclAllGather", err);
 }
 
 void nccl_comm_destroy(Nccl* n, void* comm)

@@ -40,7 +40,8 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x)
 __device__ __forceinline__ unsigned window_code(const DedupArgs& a, int gx, int gy, int gz)
 {
     if (gx < 0 || gx >= a.nx || gy < 0 || gy >= a.ny || gz < 0 || gz >= a.nz) return 2u;
-    return a.mask[((size_t)(gz - a.mz0) * a.ny + gy) * a.nx + gx];
+    const unsigned v = a.mask[((size_t)(gz - a.mz0) * a.ny + gy) * a.nx + gx];
+    return v == 2u ? 3u : v;  // kgen's codes: 0 slow, 1 fast, 2 outside, 3 far field (N2)
 }
 
 // Row words: rw(x, y, z) packs the L codes of (x−R … x+R, y, z), 2 bits each (L ≤ 17),
@@ -102,8 +103,10 @@ __global__ void classify_kernel(const DedupArgs a, const uint64_t* __restrict__ 
         const int c = cid[i] - 1;  // inclusive scan of the run heads
         if (head[i]) rep[c] = s;
         const int sx = s % a.nx, sy = (s / a.nx) % a.ny, sz = a.sz0 + s / (a.nx * a.ny);
-        // padded state layout covers planes [z0 − R, z1 + R) — exactly the source planes
-        class_pad[((long)(sz - a.z0 + a.R) * a.nyp + (sy + a.R)) * a.nxp + kPadX + sx] = c;
+        // padded state layout covers planes [z0 − R, z1 + R) — exactly the source planes;
+        // far-field voxels (N2) are not sources: class −1 → zero weights and diagonal
+        class_pad[((long)(sz - a.z0 + a.R) * a.nyp + (sy + a.R)) * a.nxp + kPadX + sx] =
+            window_code(a, sx, sy, sz) == 3u ? -1 : c;
     }
 }
 

@@ -34,7 +34,19 @@ struct fdirw_ctx {
     Nccl* nccl = nullptr;
     void* comm = nullptr;
     uint64_t kgen_sources = 0, kgen_windows = 0;
+    // N2 far field
+    bool far = false;
+    double v_far = 0.0;
+    uint8_t* farmask = nullptr;   // slab planes [z0, z1): 1 = far-field voxel
+    float* pbc = nullptr;         // p_BC in the diag layout
+    double* tile_buf = nullptr;   // [tile_stride]: n_tiles, then per-tile Σ C_new
+    double* gathered = nullptr;   // [world · tile_stride] (NCCL all-gather target)
+    double* far_state = nullptr;  // {c_far, M0}
+    long tile_stride = 0;
 };
+
+static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s);
+static cudaError_t virtual_gather(fdirw_ctx* const* ctxs, int n, cudaStream_t s, int mode, double c_far0);
 
 static thread_local std::string g_err;
 
@@ -132,7 +144,7 @@ static fdirw_status derive(const fdirw_params& p, Derived* d)
 }
 
 static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const fdirw_dist* dist,
-                             fdirw_ctx** out)
+                             fdirw_ctx** out, bool scan_phase = true)
 {
     if (!p || !phase || !out) return fail(FDIRW_E_INVALID, "NULL argument");
     if (p->nx < 1 || p->ny < 1 || p->nz < 1) return fail(FDIRW_E_INVALID, "grid dims must be >= 1");
@@ -142,6 +154,14 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
     if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP)) return fail(FDIRW_E_INVALID, "unknown flags");
+    if (!(p->v_far >= 0)) return fail(FDIRW_E_INVALID, "v_far must be >= 0");
+    if (scan_phase) {
+        const size_t n = (size_t)p->nx * p->ny * p->nz;
+        uint8_t mx = 0;
+        for (size_t i = 0; i < n; ++i) mx = phase[i] > mx ? phase[i] : mx;
+        if (mx > 2) return fail(FDIRW_E_INVALID, "phase values must be 0 (slow), 1 (fast) or 2 (far field)");
+        if (mx == 2 && !(p->v_far > 0)) return fail(FDIRW_E_INVALID, "far-field voxels (2) need v_far > 0");
+    }
     if ((long long)p->nx * p->ny * p->nz > (1LL << 40)) return fail(FDIRW_E_INVALID, "grid too large");
     if (dist) {
         if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
@@ -174,6 +194,11 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->cpad[1]);
     cudaFree(c->mass_partial);
     cudaFree(c->mass_out);
+    cudaFree(c->farmask);
+    cudaFree(c->pbc);
+    cudaFree(c->tile_buf);
+    cudaFree(c->gathered);
+    cudaFree(c->far_state);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -328,6 +353,32 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         BAIL_CUDA(launch_kgen(ka, g.R, s));
     }
     BAIL_CUDA(cudaStreamSynchronize(s));
+
+    c->v_far = params->v_far;
+    c->far = params->v_far > 0;
+    if (c->far) {  // N2: far-field mask of the slab, p_BC, Eq.7 reduction buffers
+        const size_t ns = (size_t)g.nx * g.ny * g.nzl;
+        std::vector<uint8_t> fm(ns);
+        for (size_t i = 0; i < ns; ++i) fm[i] = phase_host[(size_t)g.z0 * plane + i] == 2 ? 1 : 0;
+        c->tile_stride = 1 + (long)g.nz * g.tpp;
+        if ((st = alloc((void**)&c->farmask, ns, "far mask")) != FDIRW_OK ||
+            (st = alloc((void**)&c->pbc, g.diag_elems * 4, "p_BC")) != FDIRW_OK ||
+            (st = alloc((void**)&c->tile_buf, c->tile_stride * 8, "tile sums")) != FDIRW_OK ||
+            (st = alloc((void**)&c->gathered, (size_t)c->world * c->tile_stride * 8, "gathered sums")) != FDIRW_OK ||
+            (st = alloc((void**)&c->far_state, 16, "far state")) != FDIRW_OK) {
+            cudaFree(mask_d);
+            return bail(st);
+        }
+        const double nt = (double)g.n_tiles;
+        BAIL_CUDA(cudaMemcpy(c->farmask, fm.data(), ns, cudaMemcpyHostToDevice));
+        BAIL_CUDA(cudaMemset(c->tile_buf, 0, c->tile_stride * 8));
+        BAIL_CUDA(cudaMemcpy(c->tile_buf, &nt, 8, cudaMemcpyHostToDevice));
+        BAIL_CUDA(cudaMemset(c->far_state, 0, 16));
+        if ((st = build_pbc(c, mask_d, s)) != FDIRW_OK) {
+            cudaFree(mask_d);
+            return bail(st);
+        }
+    }
     cudaFree(mask_d);
 
     BAIL_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
@@ -347,9 +398,10 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     return FDIRW_OK;
 }
 
-// Superpose tiles [t0, t1) of `src` (padded) into `out` with strides (ps, rs).
+// Superpose tiles [t0, t1) of `src` (padded) into `out` with strides (ps, rs).  With a far
+// field (N2) and far_terms: + p_BC·c_far and the per-tile Σ C_new for Eq.7.
 static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps, long rs, int t0, int t1,
-                             cudaStream_t s)
+                             cudaStream_t s, bool far_terms = true)
 {
     const Geometry& g = c->g;
     SuperArgs a{};
@@ -363,7 +415,46 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
     a.nxp = g.nxp; a.nyp = g.nyp;
     a.t_begin = t0;
     a.t_end = t1;
+    if (c->far && far_terms) {
+        a.pbc = c->pbc;
+        a.far_state = c->far_state;
+        a.tile_sum = c->tile_buf + 1;
+    }
     return launch_superpose(a, g.R, c->fmt, s);
+}
+
+// N2: p_BC(x) = 1 − Σ_s W̃_s(x−s) (reading A26) = 1 − (stored operator applied to the
+// indicator of the non-far voxels); computed once after kgen with the superposition itself.
+static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s)
+{
+    const Geometry& g = c->g;
+    float* rowsum = nullptr;
+    const size_t n = (size_t)g.nx * g.ny * g.nzl;
+    fdirw_status st = alloc((void**)&rowsum, n * 4, "p_BC scratch");
+    if (st != FDIRW_OK) return st;
+    cudaError_t e = launch_ones(mask_d, g.mz0, g, c->cpad[1], s);
+    if (e == cudaSuccess) e = superpose(c, c->cpad[1], rowsum, (long)g.nx * g.ny, g.nx, 0, g.n_tiles, s, false);
+    if (e == cudaSuccess) e = launch_pbc(rowsum, c->farmask, g, c->pbc, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->cpad[1], 0, g.state_elems * 4, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(rowsum);
+    if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("p_BC: ") + cudaGetErrorString(e));
+    return FDIRW_OK;
+}
+
+// N2: Eq.7 after a step (or M0 at init, mode 1): tile sums of every rank in global tile order.
+static fdirw_status far_reduce(fdirw_ctx* c, cudaStream_t s, int mode, double c_far0)
+{
+    if (c->world == 1 || c->is_virtual) {
+        if (c->is_virtual) return FDIRW_OK;  // fdirw_step_virtual gathers across the contexts
+        CUDA_TRY(launch_far_reduce(c->tile_buf, 1, c->tile_stride, c->far_state, c->v_far, c_far0, mode, s));
+        return FDIRW_OK;
+    }
+    std::string err;
+    if (nccl_allgather_f64(c->nccl, c->comm, c->tile_buf, c->tile_stride, c->gathered, s, &err))
+        return fail(FDIRW_E_NCCL, err);
+    CUDA_TRY(launch_far_reduce(c->gathered, c->world, c->tile_stride, c->far_state, c->v_far, c_far0, mode, s));
+    return FDIRW_OK;
 }
 
 // Interior tiles are those whose targets read no halo plane: z_local ∈ [R, nzl − R).
@@ -380,7 +471,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     const Geometry& g = c->g;
     if (c->world == 1) {
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
-        return FDIRW_OK;
+        return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
     }
     int i0, i1;
     split_tiles(g, &i0, &i1);
@@ -398,7 +489,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     } else {
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
     }
-    return FDIRW_OK;
+    return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
 }
 
 static float* pad_interior(fdirw_ctx* c, int i)
@@ -415,7 +506,7 @@ extern "C" fdirw_status fdirw_step(fdirw_ctx* c, const float* c_in, float* c_out
     CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const Geometry& g = c->g;
-    CUDA_TRY(launch_pack(c_in, c->cpad[0], g, s));
+    CUDA_TRY(launch_pack(c_in, c->cpad[0], g, s, c->farmask));
     return enqueue_step(c, c->cpad[0], c_out, (long)g.nx * g.ny, g.nx, s);
 }
 
@@ -428,7 +519,7 @@ extern "C" fdirw_status fdirw_run(fdirw_ctx* c, float* c_dev, int32_t n_steps, v
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const Geometry& g = c->g;
     if (n_steps == 0) return FDIRW_OK;
-    CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s));
+    CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s, c->farmask));
     const long ps = (long)g.plane_elems, rs = g.nxp;
     if (n_steps >= 2 && !c->graph2) {
         // capture step(0→1); step(1→0) once; replay it n/2 times
@@ -500,7 +591,7 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
 {
     static const uint8_t dummy = 0;
     fdirw_ctx* unused = nullptr;
-    fdirw_status st = validate(p, &dummy, dist, &unused);
+    fdirw_status st = validate(p, &dummy, dist, &unused, false);
     if (st != FDIRW_OK) return st;
     if (!pl) return fail(FDIRW_E_INVALID, "NULL argument");
     Derived d;
@@ -603,7 +694,7 @@ extern "C" fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, co
     }
     CUDA_TRY(cudaSetDevice(ctxs[0]->device));
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
-    for (int r = 0; r < n; ++r) CUDA_TRY(launch_pack(c_in[r], ctxs[r]->cpad[0], ctxs[r]->g, s));
+    for (int r = 0; r < n; ++r) CUDA_TRY(launch_pack(c_in[r], ctxs[r]->cpad[0], ctxs[r]->g, s, ctxs[r]->farmask));
     // halo planes by device copies: the planes NCCL would move (same HaloPlan as comm.cpp)
     for (int r = 0; r < n; ++r) {
         const HaloPlan h = make_halo_plan(ctxs[r]->g, r, n);
@@ -633,5 +724,71 @@ extern "C" fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, co
             CUDA_TRY(superpose(c, c->cpad[0], c_out[r], ps, rs, 0, g.n_tiles, s));
         }
     }
+    if (ctxs[0]->far) CUDA_TRY(virtual_gather(ctxs, n, s, 0, 0.0));
+    return FDIRW_OK;
+}
+
+// N2 on virtual ranks: every context gathers all ranks' tile sums (the NCCL all-gather's
+// bytes) and runs the same Eq.7 reduction.
+static cudaError_t virtual_gather(fdirw_ctx* const* ctxs, int n, cudaStream_t s, int mode, double c_far0)
+{
+    for (int r = 0; r < n; ++r) {
+        for (int q = 0; q < n; ++q) {
+            cudaError_t e = cudaMemcpyAsync(ctxs[r]->gathered + (long)q * ctxs[r]->tile_stride, ctxs[q]->tile_buf,
+                                            ctxs[q]->tile_stride * 8, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = launch_far_reduce(ctxs[r]->gathered, n, ctxs[r]->tile_stride, ctxs[r]->far_state,
+                                          ctxs[r]->v_far, c_far0, mode, s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+extern "C" fdirw_status fdirw_far_init(fdirw_ctx* c, const float* c_dev, double c_far0, double* M0_out,
+                                       void* cuda_stream)
+{
+    if (!c || !c_dev) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (!c->far) return fail(FDIRW_E_STATE, "closed-domain context (v_far = 0)");
+    if (c->is_virtual) return fail(FDIRW_E_STATE, "virtual-rank context: use fdirw_far_init_virtual");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    CUDA_TRY(launch_tile_mass(c_dev, c->farmask, c->g, c->tile_buf + 1, s));
+    fdirw_status st = far_reduce(c, s, 1, c_far0);
+    if (st != FDIRW_OK) return st;
+    double fs[2];
+    CUDA_TRY(cudaMemcpyAsync(fs, c->far_state, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (M0_out) *M0_out = fs[1];
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_far_init_virtual(fdirw_ctx* const* ctxs, int32_t n, const float* const* c_dev,
+                                               double c_far0, double* M0_out, void* cuda_stream)
+{
+    if (!ctxs || !c_dev || n < 1) return fail(FDIRW_E_INVALID, "NULL argument");
+    for (int r = 0; r < n; ++r)
+        if (!ctxs[r] || !ctxs[r]->far || ctxs[r]->world != n || ctxs[r]->rank != r)
+            return fail(FDIRW_E_STATE, "need far-field contexts of ranks 0..n-1");
+    CUDA_TRY(cudaSetDevice(ctxs[0]->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    for (int r = 0; r < n; ++r)
+        CUDA_TRY(launch_tile_mass(c_dev[r], ctxs[r]->farmask, ctxs[r]->g, ctxs[r]->tile_buf + 1, s));
+    CUDA_TRY(virtual_gather(ctxs, n, s, 1, c_far0));
+    double fs[2];
+    CUDA_TRY(cudaMemcpyAsync(fs, ctxs[0]->far_state, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (M0_out) *M0_out = fs[1];
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_far_get(fdirw_ctx* c, double* c_far_out, void* cuda_stream)
+{
+    if (!c || !c_far_out) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (!c->far) return fail(FDIRW_E_STATE, "closed-domain context (v_far = 0)");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    CUDA_TRY(cudaMemcpyAsync(c_far_out, c->far_state, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return FDIRW_OK;
 }

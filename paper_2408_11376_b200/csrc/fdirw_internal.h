@@ -103,10 +103,29 @@ struct SuperArgs {
     int nx, ny, nxq, tile, tpp, K;
     int nxp, nyp;        // padded row length, rows per padded plane
     int t_begin, t_end;  // tile range
+    // N2 (far field): + pbc·far_state[0] per target, per-tile Σ C_new into tile_sum[tile]
+    const float* pbc = nullptr;
+    const double* far_state = nullptr;  // {c_far, M0}
+    double* tile_sum = nullptr;
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
 
-cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStream_t s);
+// ---- N2 far field (superpose.cu) ----------------------------------------------------
+// per-tile Σ c over a dense slab field (far voxels skipped), same order as superpose's sums
+cudaError_t launch_tile_mass(const float* c, const uint8_t* farmask, const Geometry& g, double* tile_sum,
+                             cudaStream_t s);
+// padded field = 1 on in-domain non-far voxels of planes [z0−R, z1+R) (mask planes from mz0)
+cudaError_t launch_ones(const uint8_t* mask, int mz0, const Geometry& g, float* cpad, cudaStream_t s);
+// pbc[tile layout] = 1 − rowsum for real non-far targets, else 0
+cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s);
+// gathered = world blocks of (1 + stride−1) doubles: [count, tile sums...]; sum in global tile
+// order (deterministic for any decomposition).  mode 0: c_far = (M0 − Σ)/v_far;
+// mode 1 (init): M0 = Σ + c_far0·v_far, c_far = c_far0
+cudaError_t launch_far_reduce(const double* gathered, int world, long stride, double* far_state, double v_far,
+                              double c_far0, int mode, cudaStream_t s);
+
+cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStream_t s,
+                        const uint8_t* farmask = nullptr);
 cudaError_t launch_unpack(const float* cpad, float* c, const Geometry& g, cudaStream_t s);
 cudaError_t launch_mass(const float* c, size_t n, double* partial, int nblk, double* out, cudaStream_t s);
 cudaError_t launch_export(const void* Wt, const float* diag, const Geometry& g, int fmt, const int32_t* box,
@@ -119,6 +138,8 @@ int nccl_unique_id(Nccl*, void* out128, std::string* err);
 void* nccl_comm_init(Nccl*, int world, int rank, const void* id128, std::string* err);
 int nccl_halo(Nccl*, void* comm, float* cpad, const HaloPlan& h, cudaStream_t s, std::string* err);
 int nccl_allreduce_sum_f64(Nccl*, void* comm, double* buf, cudaStream_t s, std::string* err);
+int nccl_allgather_f64(Nccl*, void* comm, const double* send, long count, double* recv, cudaStream_t s,
+                       std::string* err);
 void nccl_comm_destroy(Nccl*, void* comm);
 
 }  // namespace fdirw

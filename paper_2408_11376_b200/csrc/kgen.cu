@@ -92,8 +92,11 @@ __device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigne
 
 __device__ __forceinline__ float face_lambda(unsigned p, unsigned q, float ff, float fs, float ss)
 {
-    // p, q ∈ {0 slow, 1 fast, 2 outside the domain}
-    if (p > 1u || q > 1u) return 0.f;
+    // p, q ∈ {0 slow, 1 fast, 2 outside the domain, 3 far-field reservoir (N2)}.  A far
+    // cell is a fast-phase Dirichlet cell held at 0: faces into it carry flux, its own
+    // value never changes (p = 3 → no update).
+    if (p > 1u || q == 2u) return 0.f;
+    if (q == 3u) q = 1u;
     return (p & q) ? ff : ((p | q) ? fs : ss);
 }
 
@@ -122,16 +125,22 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
         const int sy = (int)((src / nx) % ny);
         const int sz = a.sz0 + (int)(src / ((long)nx * ny));
 
-        // window phases → smem (2 = outside the domain)
+        // window phases → smem (2 = outside the domain, 3 = far field)
+        __syncthreads();  // the previous source's readers of ph are done
+        int far_here = 0;
         for (int i = t; i < LLL; i += NT) {
             const int gx = sx + i % L - R, gy = sy + (i / L) % L - R, gz = sz + i / LL - R;
             const bool in = gx >= 0 && gx < nx && gy >= 0 && gy < ny && gz >= 0 && gz < nz;
-            ph[i] = in ? a.mask[((size_t)(gz - a.mz0) * ny + gy) * nx + gx] : (unsigned char)2;
+            unsigned char v = in ? a.mask[((size_t)(gz - a.mz0) * ny + gy) * nx + gx] : (unsigned char)2;
+            if (in && v == 2) v = 3;
+            far_here |= v == 3;
+            ph[i] = v;
         }
-        __syncthreads();
+        const bool open = __syncthreads_or(far_here) != 0;  // window touches the reservoir
+        if (ph[KC] == 3) continue;  // far-field voxels are not sources (their value is c_far)
 
         constexpr int Lp = S::Lp, NQ = Lp / 4;
-        float c[Lp], lzp[L];
+        float c[Lp], lzp[L], lzm[L];  // own +z / −z face numbers (asymmetric next to the reservoir)
         unsigned long long lxm2[Lp / 2], lxp2[Lp / 2], lym2[Lp / 2], lyp2[Lp / 2];  // (z, z+1) pairs
 #pragma unroll
         for (int h = 0; h < Lp / 2; ++h) {
@@ -146,8 +155,10 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
                 v[1][u] = (ok && oxp) ? face_lambda(p, ph[i + oxp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
                 v[2][u] = (ok && oym) ? face_lambda(p, ph[i + oym], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
                 v[3][u] = (ok && oyp) ? face_lambda(p, ph[i + oyp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-                if (z < L)
+                if (z < L) {
                     lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                    lzm[z] = (col && z > 0) ? face_lambda(p, ph[i - LL], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                }
                 c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
             }
             lxm2[h] = pk2(v[0][0], v[0][1]);
@@ -193,7 +204,7 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
 #pragma unroll
                 for (int z = 0; z < L; ++z) {
                     float acc = nw[z];
-                    if (z > 0) acc = fmaf(lzp[z - 1], c[z - 1] - c[z], acc);
+                    if (z > 0) acc = fmaf(lzm[z], c[z - 1] - c[z], acc);
                     if (z < L - 1) acc = fmaf(lzp[z], c[z + 1] - c[z], acc);
                     nw[z] = acc;
                 }
@@ -209,7 +220,10 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
             for (int z = 0; z < L; ++z) s += (double)c[z];
         }
         const double S_ = block_sum_f64<S::NW>(s, red);
-        const double inv = 1.0 / S_;
+        // closed window: renormalise to mass 1 (fp32 FD drift); open window (N2): the kernel
+        // keeps its own mass M = S, the rest went to the reservoir
+        const double inv = open ? 1.0 : 1.0 / S_;
+        const double M = open ? S_ : 1.0;
         double qsum = 0.0;
         float centre_q = 0.f;
         if (col) {
@@ -258,9 +272,9 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
         }
         const double off = block_sum_f64<S::NW>(qsum, red);
         if (t == R * L + R && a.class_w) {
-            a.class_diag[it] = a.mass_fix ? (float)(1.0 - off) : centre_q;
+            a.class_diag[it] = a.mass_fix ? (float)(M - off) : centre_q;
         } else if (t == R * L + R && sz >= a.z0 && sz < a.z1) {
-            const float d = a.mass_fix ? (float)(1.0 - off) : centre_q;
+            const float d = a.mass_fix ? (float)(M - off) : centre_q;
             const int zl = sz - a.z0;
             const int q = sy * a.nxq + (sx >> 3);
             const size_t tile = (size_t)zl * a.tpp + q / a.tile;

@@ -137,6 +137,20 @@ __device__ __forceinline__ void do_row(const float* srow, const WT* wp, size_t w
     }
 }
 
+// Deterministic fp64 sum over the CTA (≤ 256 threads): shuffle tree, then warps in order.
+__device__ __forceinline__ double tile_block_sum(double s)
+{
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    return t;  // valid in thread 0
+}
+
 template <int R, typename WT>
 __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
 {
@@ -145,8 +159,9 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
     const int zl = tile / a.tpp, tp = tile % a.tpp;
     const int e = threadIdx.x;
     const int q = tp * a.tile + e;
-    if (q >= a.ny * a.nxq) return;  // dummy chunk at the end of the plane
-    const int y = q / a.nxq, x = (q % a.nxq) * 8;
+    const bool real = q < a.ny * a.nxq;  // false: dummy chunk at the end of the plane
+    if (!real && a.tile_sum == nullptr) return;
+    const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;  // dummies: harmless reads
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;  // C_old(z, y, x)
     const size_t wstride = (size_t)a.tile * 8;
@@ -180,14 +195,34 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(hi[j], lo[j]);
-    float* out = a.out + (long)zl * a.out_ps + (long)y * a.out_rs + x;
-    if (x + 8 <= a.nx && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-        reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-    } else {
+    if (a.pbc) {  // N2: + p_BC(x)·c_far(t)  (Eq.8 boundary term; 0 on far-field targets)
+        const float cf = (float)a.far_state[0];
+        const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.pbc + ((size_t)tile * a.tile + e) * 8));
+        const float4 b1 = __ldg(reinterpret_cast<const float4*>(a.pbc + ((size_t)tile * a.tile + e) * 8 + 4));
+        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (x + j < a.nx) out[j] = acc[j];
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(b[j], cf, acc[j]);
+    }
+    if (real) {
+        float* out = a.out + (long)zl * a.out_ps + (long)y * a.out_rs + x;
+        if (x + 8 <= a.nx && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (x + j < a.nx) out[j] = acc[j];
+        }
+    }
+    if (a.tile_sum) {  // N2: this tile's Σ C_new (fp64, fixed order) for Eq.7
+        double s = 0.0;
+        if (real) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (x + j < a.nx) s += (double)acc[j];
+        }
+        s = tile_block_sum(s);
+        if (threadIdx.x == 0) a.tile_sum[tile] = s;
     }
 }
 
@@ -219,15 +254,129 @@ cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s)
 
 // ---- state kernels ------------------------------------------------------------------
 __global__ void pack_kernel(const float* __restrict__ c, float* __restrict__ cpad, int nx, int ny, long n,
-                            int R, int nxp, int nyp)
+                            int R, int nxp, int nyp, const uint8_t* __restrict__ farmask)
 {
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         const int x = (int)(i % nx);
         const long r = i / nx;
         const int y = (int)(r % ny);
         const long z = r / ny;
-        cpad[((z + R) * nyp + (y + R)) * (long)nxp + kPadX + x] = c[i];
+        // N2: far-field voxels carry no fine value (theirs is the scalar c_far)
+        cpad[((z + R) * nyp + (y + R)) * (long)nxp + kPadX + x] = (farmask && farmask[i]) ? 0.f : c[i];
     }
+}
+
+// ---- N2 far field --------------------------------------------------------------------
+static unsigned grid_for(long n, int threads);
+__global__ void tile_mass_kernel(const float* __restrict__ c, const uint8_t* __restrict__ farmask, int nx, int ny,
+                                 int nxq, int tile, int tpp, double* __restrict__ tile_sum)
+{
+    const int t = blockIdx.x, zl = t / tpp, tp = t % tpp;
+    const int q = tp * tile + threadIdx.x;
+    double s = 0.0;
+    if (q < ny * nxq) {
+        const int y = q / nxq, x = (q % nxq) * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (x + j >= nx) continue;
+            const long i = ((long)zl * ny + y) * nx + x + j;
+            s += (farmask && farmask[i]) ? 0.0 : (double)c[i];
+        }
+    }
+    s = tile_block_sum(s);
+    if (threadIdx.x == 0) tile_sum[t] = s;
+}
+
+cudaError_t launch_tile_mass(const float* c, const uint8_t* farmask, const Geometry& g, double* tile_sum,
+                             cudaStream_t s)
+{
+    if (g.n_tiles <= 0) return cudaSuccess;
+    tile_mass_kernel<<<g.n_tiles, g.tile, 0, s>>>(c, farmask, g.nx, g.ny, g.nxq, g.tile, g.tpp, tile_sum);
+    return cudaGetLastError();
+}
+
+__global__ void ones_kernel(const uint8_t* __restrict__ mask, int mz0, int nx, int ny, int nz, int z0, int R,
+                            int nzl, int nxp, int nyp, float* __restrict__ cpad)
+{
+    const long n = (long)nx * ny * (nzl + 2 * R);
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx), y = (int)((i / nx) % ny);
+        const int pz = (int)(i / ((long)nx * ny));  // padded plane
+        const int z = z0 - R + pz;
+        float v = 0.f;
+        if (z >= 0 && z < nz) v = mask[((long)(z - mz0) * ny + y) * nx + x] == 2 ? 0.f : 1.f;
+        cpad[((long)pz * nyp + (y + R)) * nxp + kPadX + x] = v;
+    }
+}
+
+cudaError_t launch_ones(const uint8_t* mask, int mz0, const Geometry& g, float* cpad, cudaStream_t s)
+{
+    const long n = (long)g.nx * g.ny * (g.nzl + 2 * g.R);
+    ones_kernel<<<grid_for(n, 256), 256, 0, s>>>(mask, mz0, g.nx, g.ny, g.nz, g.z0, g.R, g.nzl, g.nxp, g.nyp, cpad);
+    return cudaGetLastError();
+}
+
+__global__ void pbc_kernel(const float* __restrict__ rowsum, const uint8_t* __restrict__ farmask, int nx, int ny,
+                           int nxq, int tile, int tpp, long n_elems, float* __restrict__ pbc)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n_elems; i += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(i & 7);
+        const long te = i >> 3;
+        const int e = (int)(te % tile);
+        const long t = te / tile;
+        const int zl = (int)(t / tpp), tp = (int)(t % tpp);
+        const int q = tp * tile + e;
+        float v = 0.f;
+        if (q < ny * nxq) {
+            const int y = q / nxq, x = (q % nxq) * 8 + j;
+            if (x < nx) {
+                const long k = ((long)zl * ny + y) * nx + x;
+                v = farmask[k] ? 0.f : 1.f - rowsum[k];  // reading A26: p_BC = 1 − Σ_s W̃_s(x−s)
+            }
+        }
+        pbc[i] = v;
+    }
+}
+
+cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s)
+{
+    pbc_kernel<<<grid_for((long)g.diag_elems, 256), 256, 0, s>>>(rowsum, farmask, g.nx, g.ny, g.nxq, g.tile, g.tpp,
+                                                                (long)g.diag_elems, pbc);
+    return cudaGetLastError();
+}
+
+// One warp: lane l sums the tile partials whose GLOBAL tile index ≡ l (mod 32) in increasing
+// order, then a fixed shuffle tree — the same sequence for every slab decomposition.
+__global__ void far_reduce_kernel(const double* __restrict__ gathered, int world, long stride,
+                                  double* __restrict__ far_state, double v_far, double c_far0, int mode)
+{
+    const int lane = threadIdx.x;
+    double s = 0.0;
+    long g0 = 0;
+    for (int r = 0; r < world; ++r) {
+        const double* blk = gathered + (long)r * stride;
+        const long n = (long)blk[0];
+        long t = ((lane - g0) % 32 + 32) % 32;
+        for (; t < n; t += 32) s += blk[1 + t];
+        g0 += n;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        if (mode == 0) {
+            far_state[0] = (far_state[1] - s) / v_far;  // Eq.7
+        } else {
+            far_state[1] = s + c_far0 * v_far;          // M0 = Σc_{S+L}(t0)
+            far_state[0] = c_far0;
+        }
+    }
+}
+
+cudaError_t launch_far_reduce(const double* gathered, int world, long stride, double* far_state, double v_far,
+                              double c_far0, int mode, cudaStream_t s)
+{
+    far_reduce_kernel<<<1, 32, 0, s>>>(gathered, world, stride, far_state, v_far, c_far0, mode);
+    return cudaGetLastError();
 }
 
 __global__ void unpack_kernel(const float* __restrict__ cpad, float* __restrict__ c, int nx, int ny, long n,
@@ -250,11 +399,11 @@ static unsigned grid_for(long n, int threads)
     return (unsigned)b;
 }
 
-cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStream_t s)
+cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStream_t s, const uint8_t* farmask)
 {
     const long n = (long)g.nx * g.ny * g.nzl;
     if (n == 0) return cudaSuccess;
-    pack_kernel<<<grid_for(n, 256), 256, 0, s>>>(c, cpad, g.nx, g.ny, n, g.R, g.nxp, g.nyp);
+    pack_kernel<<<grid_for(n, 256), 256, 0, s>>>(c, cpad, g.nx, g.ny, n, g.R, g.nxp, g.nyp, farmask);
     return cudaGetLastError();
 }
 

@@ -11,12 +11,13 @@ def oracle_problem(cfg: fi.Config, mask=None, n_fd=None):
                           D_slow=cfg.D_slow, dt=cfg.dt, R=cfg.R, n_fd=cfg.n_fd if n_fd is None else n_fd)
 
 
-def lib_params(cfg: fi.Config, weights=None, flags=0):
+def lib_params(cfg: fi.Config, weights=None, flags=0, v_far=None):
     import paper_2408_11376_b200 as fd
 
     nz, ny, nx = cfg.shape
     return fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt,
-                     radius=cfg.R, n_fd=cfg.n_fd, weights=weights or cfg.weights, flags=flags)
+                     radius=cfg.R, n_fd=cfg.n_fd, weights=weights or cfg.weights, flags=flags,
+                     v_far=cfg.v_far if v_far is None else v_far)
 
 
 def small_cfg(shape, R, n_fd, D_slow=1e-3, weights="fp32", mask=None, seed=0, kind="random"):

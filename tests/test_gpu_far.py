@@ -1,0 +1,158 @@
+"""GPU parity of NEXT row N2 — open domain with a far-field reservoir (Eq.7,
+P:101-107 Eq.8) — against oracle/farfield.py, through the C-ABI."""
+import numpy as np
+import pytest
+
+import fdirw_inputs as fi
+from _util import lib_params, oracle_problem, rel_l2, small_cfg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2408_11376_b200 as fd
+
+    return fd
+
+
+def _open_mask(shape, seed):
+    m = fi.porous_particle(shape, min(shape) / 2 - 4, pore_r=(1.0, 2.0), porosity=0.3, seed=seed)
+    return fi.with_far_field(m, min(shape) / 2 - 4, margin=2.0)
+
+
+def _gpu_far(fd, cfg, mask, c0, c_far0, steps, v_far, flags=0):
+    import torch
+
+    ctx = fd.build_kernels(lib_params(cfg, flags=flags, v_far=v_far), mask)
+    try:
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        M0 = fd.far_init(ctx, c, c_far0)
+        fd.run(ctx, c, steps)
+        cf = fd.far_get(ctx)
+        return c.cpu().numpy().astype(np.float64), cf, M0, ctx.info
+    finally:
+        fd.destroy(ctx)
+
+
+@pytest.mark.parametrize("n_fd,R", [(2, 2), (4, 4)])
+def test_far_exact_regime_vs_dirichlet_fd(fd, oracle_lib, n_fd, R):
+    """n_fd ≤ R: one GPU step == n_fd whole-grid FD substeps with the reservoir held at c_far
+    (oracle O6), and c_far(t+Δt) == Eq.7 on the GPU's own field."""
+    shape = (13, 14, 15)
+    mask = _open_mask(shape, 2)
+    assert (mask == 2).sum() > 100
+    cfg = small_cfg(shape, R, n_fd, D_slow=1e-2, weights="fp32")
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=2).astype(np.float64) * (mask != 2)
+    got, cf, M0, _ = _gpu_far(fd, cfg, mask, c0, 0.3, 1, v_far=500.0)
+    ref = oracle_lib.fd_whole_grid(pb, c0, n_fd, c_far=0.3) * (mask != 2)
+    assert rel_l2(got, ref) <= 1e-5
+    assert np.all(got[mask == 2] == 0)
+    assert M0 == pytest.approx(c0.astype(np.float32).astype(np.float64).sum() + 0.3 * 500.0, rel=1e-12)
+    assert cf == pytest.approx((M0 - got.sum()) / 500.0, rel=1e-9)
+
+
+@pytest.mark.parametrize("fmt", ["fp32", "bf16"])
+def test_far_truncated_vs_oracle(fd, oracle_lib, fmt):
+    """Truncated regime (n_fd = 300 > R), 3 steps with the reservoir: field, c_far and the
+    conserved total (Eq.7) vs oracle.farfield.run_full (quantised the same way)."""
+    from oracle import farfield as ff
+
+    shape = (14, 13, 15)
+    mask = _open_mask(shape, 4)
+    cfg = small_cfg(shape, 3, 300, D_slow=1e-3, weights=fmt)
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=4).astype(np.float64)
+    V = 2000.0
+    refC, refcf, refM0 = ff.run_full(pb, c0, 0.5, V, 3)
+    got, cf, M0, _ = _gpu_far(fd, cfg, mask, c0, 0.5, 3, v_far=V)
+    tol = 1e-5 if fmt == "fp32" else 5e-3
+    nf = mask != 2
+    assert rel_l2(got[nf], refC[nf]) <= tol
+    assert abs(cf - refcf) / refcf <= (1e-6 if fmt == "fp32" else 1e-4)
+    assert (got.sum() + cf * V - M0) / M0 == pytest.approx(0.0, abs=1e-9)   # Eq.7 closes the balance
+
+
+def test_far_uniform_stationary(fd):
+    """c ≡ c_far ≡ κ stays κ (p_BC = 1 − row sum)."""
+    import torch
+
+    shape = (12, 12, 12)
+    mask = _open_mask(shape, 6)
+    cfg = small_cfg(shape, 2, 100, weights="bf16")
+    c0 = np.where(mask != 2, 0.8, 0.0)
+    got, cf, M0, _ = _gpu_far(fd, cfg, mask, c0, 0.8, 4, v_far=1e4)
+    np.testing.assert_allclose(got[mask != 2], 0.8, rtol=2e-6)
+    assert cf == pytest.approx(0.8, rel=1e-6)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_far_virtual_ranks_bitwise(fd, world):
+    """Slabs + Eq.7 with tile sums gathered in global order: bitwise equal to world = 1."""
+    import torch
+
+    shape = (12, 11, 13)
+    mask = _open_mask(shape, 8)
+    cfg = small_cfg(shape, 3, 60, weights="bf16")
+    c0 = fi.initial_c(mask, "random", seed=8)
+    V = 777.0
+    ctx = fd.build_kernels(lib_params(cfg, v_far=V), mask)
+    try:
+        cin = torch.from_numpy(c0).cuda()
+        out = torch.empty_like(cin)
+        fd.far_init(ctx, cin, 0.4)
+        fd.step(ctx, cin, out)
+        fd.step(ctx, out, cin)
+        one, cf1 = cin.cpu().numpy(), fd.far_get(ctx)
+    finally:
+        fd.destroy(ctx)
+    sl = fd.slabs(shape[0], world)
+    ctxs = [fd.build_kernels(lib_params(cfg, v_far=V), mask, rank=r, world=world, z_begin=a, z_end=b, device=0)
+            for r, (a, b) in enumerate(sl)]
+    try:
+        cin = [torch.from_numpy(c0[a:b].copy()).cuda() for a, b in sl]
+        cout = [torch.empty_like(t) for t in cin]
+        fd.far_init_virtual(ctxs, cin, 0.4)
+        fd.step_virtual(ctxs, cin, cout)
+        fd.step_virtual(ctxs, cout, cin)
+        got = np.concatenate([t.cpu().numpy() for t in cin], axis=0)
+        cfs = [fd.far_get(c) for c in ctxs]
+    finally:
+        for c in ctxs:
+            fd.destroy(c)
+    np.testing.assert_array_equal(got, one)
+    assert all(x == cf1 for x in cfs)
+
+
+def test_cfg3o_open_r50_sampled(fd, oracle_lib):
+    """The paper's open R50 model (near field r_p + 5Δh in a 120³ grid, V_far from Table 1),
+    Table 1 SI parameters, R5, bf16: sampled boxes (particle surface; near-field edge next to
+    the reservoir) vs oracle.farfield.step_box_far; Eq.7 balance."""
+    import torch
+    from oracle import farfield as ff
+
+    cfg = fi.config("cfg3o")
+    mask = cfg.mask()
+    assert set(np.unique(mask)) == {0, 1, 2}
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "paper") * (mask != 2)
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        c = torch.from_numpy(c0).cuda()
+        M0 = fd.far_init(ctx, c, cfg.c_far0)
+        fd.run(ctx, c, 1)
+        cf = fd.far_get(ctx)
+        got = c.cpu().numpy()
+    finally:
+        fd.destroy(ctx)
+    assert (got.astype(np.float64).sum() + cf * cfg.v_far - M0) / M0 == pytest.approx(0.0, abs=1e-9)
+    for tb in [(107, 112, 57, 62, 58, 62), (112, 117, 58, 63, 57, 61)]:
+        ref = ff.step_box_far(pb, c0.astype(np.float64), cfg.c_far0, tb, fmt=None)
+        assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= 5e-3, tb

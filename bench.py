@@ -254,6 +254,8 @@ def main():
     ap.add_argument("--mode", default="fine", choices=["fine", "coarse"],
                     help="fine: the north_star windowed step (default); coarse: NEXT row N1")
     ap.add_argument("--block", type=int, default=5)
+    ap.add_argument("--storage", default="dense", choices=["dense", "dedup"],
+                    help="dense: north_star gather layout (default); dedup: NEXT row N4 uniform-chunk kernels")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -285,7 +287,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     params = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt,
-                       radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights)
+                       radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights, v_far=cfg.v_far,
+                       flags=fd.F_DEDUP_STORAGE if args.storage == "dedup" else 0)
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
     t = time.perf_counter()
@@ -294,8 +297,12 @@ def main():
     t_kgen = time.perf_counter() - t
     info = ctx.info
 
-    c_host = torch.from_numpy(np.ascontiguousarray(fi.initial_c(mask, "paper")[z0:z1])).pin_memory()
+    c0 = fi.initial_c(mask, "paper") * (mask != 2)  # far-field voxels carry the scalar c_far (N2)
+    c_host = torch.from_numpy(np.ascontiguousarray(c0[z0:z1])).pin_memory()
     c = c_host.to("cuda", non_blocking=True)
+    far = cfg.v_far > 0
+    if far:
+        total0 = fd.far_init(ctx, c, cfg.c_far0, stream)  # Eq.7's Σc_{S+L}(t0)
     m0 = fd.mass(ctx, c)
     fd.run(ctx, c, args.warmup)
     torch.cuda.synchronize()
@@ -315,6 +322,7 @@ def main():
         barrier()
     t_ms = ev0.elapsed_time(ev1)
     m1 = fd.mass(ctx, c)
+    cf1 = fd.far_get(ctx, stream) if far else None
     if world > 1:
         tt = torch.tensor([t_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -347,12 +355,19 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_ms = float(tt.item())
 
-    N = nx * ny * nz
+    # voxel-updates: every target whose C the step computes (far-field voxels, N2, hold the
+    # scalar c_far instead and are not counted)
+    N = int((mask != 2).sum())
+    n_slab = int((mask[z0:z1] != 2).sum())
     ms_step = t_ms / args.steps
     value = N * args.steps / (t_ms * 1e-3)
     e2e_value = N * args.e2e_steps / (e_ms * 1e-3)
     bpv = info["bytes_per_voxel_update"]
-    per_launch_bytes = bpv * info["voxels"]
+    dedup_storage = bool(params.flags & fd.F_DEDUP_STORAGE)
+    f_u = info["uniform_chunks"] / max(info["chunks"], 1)
+    if dedup_storage:  # N4 byte model: uniform chunks' weights come from an L2-resident table
+        bpv = int(round((1.0 - f_u) * (info["K"] - 1) * (2 if cfg.weights != "fp32" else 4))) + 12
+    per_launch_bytes = bpv * n_slab
     peak, peak_src = _hbm_peak()
     launches_per_step = 1 if world == 1 else (3 if info["n_tiles"] > 0 else 1)
     # one superpose launch per step at N=1 (+1 pack, +1 unpack per fdirw_run); the launch
@@ -372,7 +387,10 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "superpose_kernel",
                      "peak_source": peak_src, "bytes_per_voxel_update": bpv,
-                     "note": "algorithmic bytes (K-1)*b_w+12 per voxel-update x voxels / step time (per rank)"},
+                     "note": ("N4 byte model: (1-f_uniform)*(K-1)*b_w+12 per voxel-update, f_uniform=%.4f"
+                              % f_u if dedup_storage else
+                              "algorithmic bytes (K-1)*b_w+12 per voxel-update x voxels / step time (per rank)")},
+        "storage": "dedup (NEXT row N4)" if dedup_storage else "dense",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(c.numel() * 4 * world),
                 "d2h_bytes_per_step": int(c.numel() * 4 * world), "api": "fdirw_step with pinned host copies"},
         "gpu_launches": (args.steps * launches_per_step + 2) * world,
@@ -381,10 +399,11 @@ def main():
                       "note": "t = 0.5 s of Fig.7 (1000 macro steps) incl. the one-time kernel build"},
         "kgen": {"seconds": t_kgen, "window_cell_updates": kgen_cells * world,
                  "cell_updates_per_s": kgen_cells * world / t_kgen, "n_fd": info["n_fd"]},
-        "mass_rel_err": abs(m1 - m0) / abs(m0) if m0 else None,
+        "mass_rel_err": (abs(m1 + cf1 * cfg.v_far - total0) / total0 if far
+                         else (abs(m1 - m0) / abs(m0) if m0 else None)),
         "clocks": clk.summary(),
     }
-    tr = _ncu_traffic(cfg, per_launch_bytes) if world == 1 else None
+    tr = _ncu_traffic(cfg, per_launch_bytes) if (world == 1 and not dedup_storage) else None
     if tr:
         line["roofline"]["traffic"] = tr[0]
         line["roofline"]["traffic_source"] = tr[1] + " (ncu --set full, one launch)"

@@ -68,6 +68,10 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weig
 #define FDIRW_F_NO_MASS_FIX 1u /* diagonal = RNE_fmt(W_s(0)) instead of the fp32 mass fix-up (A10) */
 #define FDIRW_F_NO_DEDUP 2u    /* run kgen on every source window instead of once per distinct window
                                   (results are bitwise identical either way)          */
+#define FDIRW_F_DEDUP_STORAGE 4u /* NEXT row N4: 8-target chunks whose every source shares one window
+                                  class read that class's kernel from a small L2-resident table
+                                  instead of streaming their gather weights (bitwise identical
+                                  results; fewer HBM bytes)                        */
 
 /* The paper's problem statement (Table 1) + north_star's window radius / precision. */
 typedef struct {
@@ -114,6 +118,9 @@ typedef struct {
     int32_t n_tiles;        /* tiles in this slab                                              */
     uint64_t kgen_sources;  /* sources whose kernels the slab needs (planes [z_begin−R, z_end+R))  */
     uint64_t kgen_windows;  /* windows actually run through the FD (distinct windows with dedup)   */
+    uint64_t chunks;        /* 8-target x-chunks of the slab                                        */
+    uint64_t uniform_chunks;/* N4: chunks whose weights come from a shared class kernel (else 0)   */
+    int32_t uniform_classes;/* N4: distinct class kernels those chunks use                          */
 } fdirw_info;
 
 /* Host-only decomposition plan of one rank (no CUDA call; usable without a GPU).

@@ -31,6 +31,7 @@ STATUS_NAMES = ["OK", "E_INVALID", "E_UNSTABLE", "E_OOM", "E_CUDA", "E_NCCL", "E
 WEIGHTS = {"fp32": 0, "fp16": 1, "bf16": 2}
 F_NO_MASS_FIX = 1
 F_NO_DEDUP = 2
+F_DEDUP_STORAGE = 4  # NEXT row N4: uniform chunks read shared class kernels (fewer HBM bytes)
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
@@ -58,7 +59,8 @@ class fdirw_info(ctypes.Structure):
                 ("weight_bytes", ctypes.c_uint64), ("state_bytes", ctypes.c_uint64),
                 ("bytes_per_voxel_update", ctypes.c_uint64), ("voxels", ctypes.c_uint64),
                 ("tile_chunks", ctypes.c_int32), ("n_tiles", ctypes.c_int32),
-                ("kgen_sources", ctypes.c_uint64), ("kgen_windows", ctypes.c_uint64)]
+                ("kgen_sources", ctypes.c_uint64), ("kgen_windows", ctypes.c_uint64),
+                ("chunks", ctypes.c_uint64), ("uniform_chunks", ctypes.c_uint64), ("uniform_classes", ctypes.c_int32)]
 
 
 class fdirw_plan(ctypes.Structure):

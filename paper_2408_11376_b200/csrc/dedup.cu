@@ -24,6 +24,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <vector>
+
 #include "fdirw_internal.h"
 #include "layout.cuh"
 
@@ -186,6 +188,130 @@ __global__ void __launch_bounds__(256) expand_kernel(const ExpandArgs a)
             }
         }
     }
+}
+
+// N4: a chunk (8 consecutive targets of a row) is uniform when every source that reaches it
+// ((x0−R … x0+7+R) × (y±R) × (z±R)) has the same window class — then all its gather weights
+// are that class's kernel.  cls_out[tile·tile_sz + e] = class, or −1.
+__global__ void chunk_class_kernel(const int* __restrict__ class_pad, int nx, int ny, int nxq, int tile_sz, int tpp,
+                                   int n_tiles, int nxp, int nyp, int R, int* __restrict__ cls_out,
+                                   int* __restrict__ used)
+{
+    const long n = (long)n_tiles * tile_sz;
+    const long plane = (long)nyp * nxp;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int e = (int)(i % tile_sz);
+        const long t = i / tile_sz;
+        const int zl = (int)(t / tpp), tp = (int)(t % tpp);
+        const int q = tp * tile_sz + e;
+        int k = -1;
+        if (q < ny * nxq) {
+            const int y = q / nxq, x = (q % nxq) * 8;
+            if (x + 8 <= nx) {
+                const int* c0 = class_pad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
+                k = c0[0];
+                for (int oz = -R; oz <= R && k >= 0; ++oz)
+                    for (int oy = -R; oy <= R && k >= 0; ++oy) {
+                        const int* row = c0 + (long)oz * plane + (long)oy * nxp;
+                        for (int j = -R; j < 8 + R; ++j)
+                            if (row[j] != k) { k = -1; break; }
+                    }
+            }
+        }
+        cls_out[i] = k;
+        if (k >= 0) used[k] = 1;
+    }
+}
+
+// uk8[u][slot][j] = class_w[k(u)][o(slot)] for j = 0..7 (the 8 targets share it)
+template <typename WT>
+__global__ void uk8_kernel(const WT* __restrict__ class_w, const int* __restrict__ used, const int* __restrict__ uid,
+                           long n_class, int R, WT* __restrict__ uk8)
+{
+    const int L = 2 * R + 1, K = L * L * L;
+    const long n = n_class * (long)(K - 1);
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long k = i / (K - 1);
+        if (!used[k]) continue;
+        const int s = (int)(i % (K - 1));
+        // slot → offset (inverse of slot_of): centre row first, then rows ascending
+        int ox, oy, oz;
+        if (s < L - 1) {
+            oz = 0; oy = 0; ox = s < R ? s - R : s - R + 1;
+        } else {
+            const int r0 = (s - (L - 1)) / L;
+            const int r = r0 >= R * L + R ? r0 + 1 : r0;
+            oz = r / L - R; oy = r % L - R; ox = (s - (L - 1)) % L - R;
+        }
+        const WT v = class_w[k * K + (oz + R) * L * L + (oy + R) * L + (ox + R)];
+        WT* d = uk8 + ((long)uid[k] * (K - 1) + s) * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = v;
+    }
+}
+
+__global__ void chunk_uid_kernel(int* __restrict__ cls, long n, const int* __restrict__ uid)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        if (cls[i] >= 0) cls[i] = uid[cls[i]];
+}
+
+static unsigned grid_n(long n);
+
+cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, int** chunk_u, void** uk8,
+                          long* n_uniform, int* n_u, cudaStream_t s)
+{
+    const long nch = (long)a.n_tiles * a.tile;
+    int *used = nullptr, *uid = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    cudaError_t e = cudaMalloc(chunk_u, nch * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&used, (n_class + 1) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&uid, (n_class + 1) * 4);
+    if (e == cudaSuccess) e = cudaMemsetAsync(used, 0, (n_class + 1) * 4, s);
+    if (e == cudaSuccess) {
+        chunk_class_kernel<<<grid_n(nch), 256, 0, s>>>(a.class_pad, a.nx, a.ny, a.nxq, a.tile, a.tpp, a.n_tiles,
+                                                       a.nxp, a.nyp, R, *chunk_u, used);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tb, used, uid, (int)(n_class + 1), s);
+    if (e == cudaSuccess) e = cudaMalloc(&tmp, tb);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tb, used, uid, (int)(n_class + 1), s);
+    int nu = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&nu, uid + n_class, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    const int bw = fmt == 0 ? 4 : 2;
+    const int K = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
+    if (e == cudaSuccess) e = cudaMalloc(uk8, ((long)(nu > 0 ? nu : 1) * (K - 1) * 8) * bw);
+    if (e == cudaSuccess && nu > 0) {
+        const long n = n_class * (long)(K - 1);
+        if (fmt == 0)
+            uk8_kernel<float><<<grid_n(n), 256, 0, s>>>((const float*)a.class_w, used, uid, n_class, R, (float*)*uk8);
+        else if (fmt == 1)
+            uk8_kernel<__half><<<grid_n(n), 256, 0, s>>>((const __half*)a.class_w, used, uid, n_class, R, (__half*)*uk8);
+        else
+            uk8_kernel<__nv_bfloat16><<<grid_n(n), 256, 0, s>>>((const __nv_bfloat16*)a.class_w, used, uid, n_class,
+                                                                 R, (__nv_bfloat16*)*uk8);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) {
+            chunk_uid_kernel<<<grid_n(nch), 256, 0, s>>>(*chunk_u, nch, uid);
+            e = cudaGetLastError();
+        }
+    }
+    if (e == cudaSuccess) {
+        // count uniform chunks (for the byte model)
+        std::vector<int> h(nch);
+        e = cudaMemcpyAsync(h.data(), *chunk_u, nch * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        long cnt = 0;
+        for (long i = 0; i < nch; ++i) cnt += h[i] >= 0;
+        *n_uniform = cnt;
+        *n_u = nu;
+    }
+    cudaFree(used);
+    cudaFree(uid);
+    cudaFree(tmp);
+    return e;
 }
 
 static unsigned grid_n(long n)

@@ -34,6 +34,11 @@ struct fdirw_ctx {
     Nccl* nccl = nullptr;
     void* comm = nullptr;
     uint64_t kgen_sources = 0, kgen_windows = 0;
+    // N4 uniform-chunk weight dedup (FDIRW_F_DEDUP_STORAGE)
+    int* chunk_u = nullptr;
+    void* uk8 = nullptr;
+    long n_uniform = 0;
+    int n_uclasses = 0;
     // N2 far field
     bool far = false;
     double v_far = 0.0;
@@ -153,7 +158,10 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (!(p->D_fast > 0) || !(p->D_slow >= 0)) return fail(FDIRW_E_INVALID, "need D_fast > 0, D_slow >= 0");
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
-    if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP)) return fail(FDIRW_E_INVALID, "unknown flags");
+    if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE))
+        return fail(FDIRW_E_INVALID, "unknown flags");
+    if ((p->flags & FDIRW_F_NO_DEDUP) && (p->flags & FDIRW_F_DEDUP_STORAGE))
+        return fail(FDIRW_E_INVALID, "FDIRW_F_DEDUP_STORAGE needs the window de-duplication");
     if (!(p->v_far >= 0)) return fail(FDIRW_E_INVALID, "v_far must be >= 0");
     if (scan_phase) {
         const size_t n = (size_t)p->nx * p->ny * p->nz;
@@ -199,6 +207,8 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->tile_buf);
     cudaFree(c->gathered);
     cudaFree(c->far_state);
+    cudaFree(c->chunk_u);
+    cudaFree(c->uk8);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -341,6 +351,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                           g.n_tiles, g.nxp, g.nyp};
             if (e == cudaSuccess) e = launch_expand(ea, g.R, c->fmt, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e == cudaSuccess && (params->flags & FDIRW_F_DEDUP_STORAGE))
+                e = build_uniform(ea, g.R, c->fmt, dr.n_class, &c->chunk_u, &c->uk8, &c->n_uniform, &c->n_uclasses, s);
             if (e != cudaSuccess) { dfree(); cudaFree(mask_d); g_err = std::string("kgen: ") + cudaGetErrorString(e); return bail(FDIRW_E_CUDA); }
             c->kgen_windows = (uint64_t)dr.n_class;
         }
@@ -415,6 +427,8 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
     a.nxp = g.nxp; a.nyp = g.nyp;
     a.t_begin = t0;
     a.t_end = t1;
+    a.chunk_u = c->chunk_u;  // N4 (null unless FDIRW_F_DEDUP_STORAGE)
+    a.uk8 = c->uk8;
     if (c->far && far_terms) {
         a.pbc = c->pbc;
         a.far_state = c->far_state;
@@ -582,6 +596,9 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->n_tiles = g.n_tiles;
     info->kgen_sources = c->kgen_sources;
     info->kgen_windows = c->kgen_windows;
+    info->chunks = (uint64_t)g.nzl * g.ny * g.nxq;
+    info->uniform_chunks = (uint64_t)c->n_uniform;
+    info->uniform_classes = c->n_uclasses;
     return FDIRW_OK;
 }
 

@@ -93,6 +93,9 @@ struct ExpandArgs {
     int nx, ny, nxq, tile, tpp, n_tiles, nxp, nyp;
 };
 cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s);
+// N4: per-chunk uniform class table (see superpose.cu); *chunk_u / *uk8 are cudaMalloc'ed
+cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, int** chunk_u, void** uk8,
+                          long* n_uniform, int* n_u, cudaStream_t s);
 
 struct SuperArgs {
     const float* cpad;   // padded state, pointer to padded plane 0
@@ -107,6 +110,10 @@ struct SuperArgs {
     const float* pbc = nullptr;
     const double* far_state = nullptr;  // {c_far, M0}
     double* tile_sum = nullptr;
+    // N4 (uniform-chunk weight dedup): per chunk the uniform class u (−1: use Wt), and the
+    // replicated class kernels uk8[u][slot][8]
+    const int* chunk_u = nullptr;
+    const void* uk8 = nullptr;
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
 

@@ -164,32 +164,46 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
     const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;  // dummies: harmless reads
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;  // C_old(z, y, x)
-    const size_t wstride = (size_t)a.tile * 8;
+    size_t wstride = (size_t)a.tile * 8;
     const WT* wt = reinterpret_cast<const WT*>(a.Wt) + ((size_t)tile * (K - 1) * a.tile + e) * 8;
+    uint64_t pol = evict_first_policy();
+    if (a.chunk_u) {
+        // N4 (uniform chunks): every source of these 8 targets has the same window class u,
+        // so its weights are class u's kernel, read from the small replicated table uk8
+        // (L1/L2-resident, broadcast across the warp) instead of streaming from HBM.
+        // Same instructions, different address: no divergence between the two kinds.
+        const int u = a.chunk_u[(size_t)tile * a.tile + e];
+        if (u >= 0) {
+            wt = reinterpret_cast<const WT*>(a.uk8) + (size_t)u * (K - 1) * 8;
+            wstride = 8;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        }
+    }
     const float* dp = a.diag + ((size_t)tile * a.tile + e) * 8;
-    const uint64_t pol = evict_first_policy();
 
     float hi[8], lo[8];
-    {
-        const float4 d0 = __ldg(reinterpret_cast<const float4*>(dp));
-        const float4 d1 = __ldg(reinterpret_cast<const float4*>(dp + 4));
-        const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
-        hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
-        hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) lo[j] = 0.f;
-    }
-    // centre row (oz = oy = 0): slots [0, L−1)
-    do_row<R, WT, true>(c0 - 8, wt, wstride, pol, hi, lo);
-    // remaining rows, ascending (oz, oy); source row of target row (z, y) is (z − oz, y − oy)
-    const WT* wr = wt + (size_t)(L - 1) * wstride;
+    for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.f;
+    if (real) {
+        {
+            const float4 d0 = __ldg(reinterpret_cast<const float4*>(dp));
+            const float4 d1 = __ldg(reinterpret_cast<const float4*>(dp + 4));
+            const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
+            hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
+            hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
+        }
+        // centre row (oz = oy = 0): slots [0, L−1)
+        do_row<R, WT, true>(c0 - 8, wt, wstride, pol, hi, lo);
+        // remaining rows, ascending (oz, oy); source row of target row (z, y) is (z − oz, y − oy)
+        const WT* wr = wt + (size_t)(L - 1) * wstride;
 #pragma unroll 1
-    for (int r = 0; r < L * L; ++r) {
-        if (r == R * L + R) continue;
-        const int oz = r / L - R, oy = r % L - R;
-        const float* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
-        do_row<R, WT, false>(srow, wr, wstride, pol, hi, lo);
-        wr += (size_t)L * wstride;
+        for (int r = 0; r < L * L; ++r) {
+            if (r == R * L + R) continue;
+            const int oz = r / L - R, oy = r % L - R;
+            const float* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
+            do_row<R, WT, false>(srow, wr, wstride, pol, hi, lo);
+            wr += (size_t)L * wstride;
+        }
     }
 
     float acc[8];

@@ -348,3 +348,33 @@ def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b):
     np.testing.assert_array_equal(got[region == 0], c0.astype(np.float32)[region == 0])
     m0 = c0.astype(np.float32)[region == 1].astype(np.float64).sum()
     assert abs(got[region == 1].astype(np.float64).sum() - m0) / m0 <= 1e-6
+
+
+# ------------------------------------------------------------------ NEXT row N4: uniform-chunk dedup
+@pytest.mark.parametrize("cfgname,steps", [("small", 3), ("cfg3", 2)])
+def test_dedup_storage_bitwise(fd, cfgname, steps):
+    """FDIRW_F_DEDUP_STORAGE (uniform chunks read their shared class kernel) gives bitwise the
+    dense path's field, on a particle geometry and on the full cfg3 workload."""
+    import torch
+
+    if cfgname == "small":
+        shape = (40, 37, 48)
+        mask = fi.porous_particle(shape, 8, pore_r=(1.0, 2.0), porosity=0.3, seed=9)
+        cfg = small_cfg(shape, 3, 200, weights="bf16")
+    else:
+        cfg = fi.config("cfg3")
+        mask = cfg.mask()
+    c0 = fi.initial_c(mask, "random", seed=9)
+    outs, infos = [], []
+    for flags in (0, fd.F_DEDUP_STORAGE):
+        ctx = fd.build_kernels(lib_params(cfg, flags=flags), mask)
+        try:
+            infos.append(ctx.info)
+            c = torch.from_numpy(c0).cuda()
+            fd.run(ctx, c, steps)
+            outs.append(c.cpu().numpy())
+        finally:
+            fd.destroy(ctx)
+    assert infos[0]["uniform_chunks"] == 0
+    assert infos[1]["uniform_chunks"] > 0.2 * infos[1]["chunks"]
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -24,12 +24,17 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "fdirw_internal.h"
 #include "layout.cuh"
 
 namespace fdirw {
+
+__device__ __forceinline__ float dec_w(float v) { return v; }
+__device__ __forceinline__ float dec_w(__half v) { return __half2float(v); }
+__device__ __forceinline__ float dec_w(__nv_bfloat16 v) { return __bfloat162float(v); }
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x)
 {
@@ -223,10 +228,11 @@ __global__ void chunk_class_kernel(const int* __restrict__ class_pad, int nx, in
     }
 }
 
-// uk8[u][slot][j] = class_w[k(u)][o(slot)] for j = 0..7 (the 8 targets share it)
+// ukf[u][slot] = class_w[k(u)][o(slot)] decoded to fp32; udiag[u] = class_diag[k(u)]
 template <typename WT>
-__global__ void uk8_kernel(const WT* __restrict__ class_w, const int* __restrict__ used, const int* __restrict__ uid,
-                           long n_class, int R, WT* __restrict__ uk8)
+__global__ void ukf_kernel(const WT* __restrict__ class_w, const float* __restrict__ class_diag,
+                           const int* __restrict__ used, const int* __restrict__ uid, long n_class, int R,
+                           float* __restrict__ ukf, float* __restrict__ udiag)
 {
     const int L = 2 * R + 1, K = L * L * L;
     const long n = n_class * (long)(K - 1);
@@ -243,10 +249,8 @@ __global__ void uk8_kernel(const WT* __restrict__ class_w, const int* __restrict
             const int r = r0 >= R * L + R ? r0 + 1 : r0;
             oz = r / L - R; oy = r % L - R; ox = (s - (L - 1)) % L - R;
         }
-        const WT v = class_w[k * K + (oz + R) * L * L + (oy + R) * L + (ox + R)];
-        WT* d = uk8 + ((long)uid[k] * (K - 1) + s) * 8;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] = v;
+        ukf[(long)uid[k] * (K - 1) + s] = dec_w(class_w[k * K + (oz + R) * L * L + (oy + R) * L + (ox + R)]);
+        if (s == 0) udiag[uid[k]] = class_diag[k];
     }
 }
 
@@ -258,20 +262,19 @@ __global__ void chunk_uid_kernel(int* __restrict__ cls, long n, const int* __res
 
 static unsigned grid_n(long n);
 
-cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, int** chunk_u, void** uk8,
-                          long* n_uniform, int* n_u, cudaStream_t s)
+cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, UniformTables* t, cudaStream_t s)
 {
     const long nch = (long)a.n_tiles * a.tile;
     int *used = nullptr, *uid = nullptr;
     void* tmp = nullptr;
     size_t tb = 0;
-    cudaError_t e = cudaMalloc(chunk_u, nch * 4);
+    cudaError_t e = cudaMalloc(&t->chunk_u, nch * 4);
     if (e == cudaSuccess) e = cudaMalloc(&used, (n_class + 1) * 4);
     if (e == cudaSuccess) e = cudaMalloc(&uid, (n_class + 1) * 4);
     if (e == cudaSuccess) e = cudaMemsetAsync(used, 0, (n_class + 1) * 4, s);
     if (e == cudaSuccess) {
         chunk_class_kernel<<<grid_n(nch), 256, 0, s>>>(a.class_pad, a.nx, a.ny, a.nxq, a.tile, a.tpp, a.n_tiles,
-                                                       a.nxp, a.nyp, R, *chunk_u, used);
+                                                       a.nxp, a.nyp, R, t->chunk_u, used);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tb, used, uid, (int)(n_class + 1), s);
@@ -280,33 +283,55 @@ cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, int
     int nu = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&nu, uid + n_class, 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    const int bw = fmt == 0 ? 4 : 2;
     const int K = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
-    if (e == cudaSuccess) e = cudaMalloc(uk8, ((long)(nu > 0 ? nu : 1) * (K - 1) * 8) * bw);
+    const long nu1 = nu > 0 ? nu : 1;
+    if (e == cudaSuccess) e = cudaMalloc(&t->ukf, nu1 * (K - 1) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&t->udiag, nu1 * 4);
     if (e == cudaSuccess && nu > 0) {
         const long n = n_class * (long)(K - 1);
         if (fmt == 0)
-            uk8_kernel<float><<<grid_n(n), 256, 0, s>>>((const float*)a.class_w, used, uid, n_class, R, (float*)*uk8);
+            ukf_kernel<float><<<grid_n(n), 256, 0, s>>>((const float*)a.class_w, a.class_diag, used, uid, n_class, R,
+                                                        t->ukf, t->udiag);
         else if (fmt == 1)
-            uk8_kernel<__half><<<grid_n(n), 256, 0, s>>>((const __half*)a.class_w, used, uid, n_class, R, (__half*)*uk8);
+            ukf_kernel<__half><<<grid_n(n), 256, 0, s>>>((const __half*)a.class_w, a.class_diag, used, uid, n_class,
+                                                         R, t->ukf, t->udiag);
         else
-            uk8_kernel<__nv_bfloat16><<<grid_n(n), 256, 0, s>>>((const __nv_bfloat16*)a.class_w, used, uid, n_class,
-                                                                 R, (__nv_bfloat16*)*uk8);
+            ukf_kernel<__nv_bfloat16><<<grid_n(n), 256, 0, s>>>((const __nv_bfloat16*)a.class_w, a.class_diag, used,
+                                                                uid, n_class, R, t->ukf, t->udiag);
         e = cudaGetLastError();
         if (e == cudaSuccess) {
-            chunk_uid_kernel<<<grid_n(nch), 256, 0, s>>>(*chunk_u, nch, uid);
+            chunk_uid_kernel<<<grid_n(nch), 256, 0, s>>>(t->chunk_u, nch, uid);
             e = cudaGetLastError();
         }
     }
     if (e == cudaSuccess) {
-        // count uniform chunks (for the byte model)
+        // chunk lists per class and CTA blocks of ≤ 256 chunks of one class (host side: nu is small)
         std::vector<int> h(nch);
-        e = cudaMemcpyAsync(h.data(), *chunk_u, nch * 4, cudaMemcpyDeviceToHost, s);
+        e = cudaMemcpyAsync(h.data(), t->chunk_u, nch * 4, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        std::vector<std::vector<int>> per(nu > 0 ? nu : 0);
         long cnt = 0;
-        for (long i = 0; i < nch; ++i) cnt += h[i] >= 0;
-        *n_uniform = cnt;
-        *n_u = nu;
+        for (long i = 0; i < nch; ++i)
+            if (h[i] >= 0) { per[h[i]].push_back((int)i); ++cnt; }
+        std::vector<int> list;
+        std::vector<int4> blocks;
+        list.reserve(cnt);
+        for (int u = 0; u < nu; ++u) {
+            for (size_t b0 = 0; b0 < per[u].size(); b0 += 256) {
+                const int c = (int)std::min<size_t>(256, per[u].size() - b0);
+                blocks.push_back(make_int4((int)list.size(), c, u, 0));
+                list.insert(list.end(), per[u].begin() + b0, per[u].begin() + b0 + c);
+            }
+        }
+        t->n_uniform = cnt;
+        t->n_u = nu;
+        t->n_blocks = (int)blocks.size();
+        if (e == cudaSuccess) e = cudaMalloc(&t->list, std::max<size_t>(list.size(), 1) * 4);
+        if (e == cudaSuccess) e = cudaMalloc(&t->blocks, std::max<size_t>(blocks.size(), 1) * sizeof(int4));
+        if (e == cudaSuccess && !list.empty())
+            e = cudaMemcpy(t->list, list.data(), list.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && !blocks.empty())
+            e = cudaMemcpy(t->blocks, blocks.data(), blocks.size() * sizeof(int4), cudaMemcpyHostToDevice);
     }
     cudaFree(used);
     cudaFree(uid);

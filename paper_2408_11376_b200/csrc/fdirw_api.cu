@@ -35,10 +35,7 @@ struct fdirw_ctx {
     void* comm = nullptr;
     uint64_t kgen_sources = 0, kgen_windows = 0;
     // N4 uniform-chunk weight dedup (FDIRW_F_DEDUP_STORAGE)
-    int* chunk_u = nullptr;
-    void* uk8 = nullptr;
-    long n_uniform = 0;
-    int n_uclasses = 0;
+    UniformTables ut;
     // N2 far field
     bool far = false;
     double v_far = 0.0;
@@ -163,6 +160,8 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if ((p->flags & FDIRW_F_NO_DEDUP) && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_DEDUP_STORAGE needs the window de-duplication");
     if (!(p->v_far >= 0)) return fail(FDIRW_E_INVALID, "v_far must be >= 0");
+    if (p->v_far > 0 && (p->flags & FDIRW_F_DEDUP_STORAGE))
+        return fail(FDIRW_E_INVALID, "FDIRW_F_DEDUP_STORAGE is not combined with a far field (v_far > 0)");
     if (scan_phase) {
         const size_t n = (size_t)p->nx * p->ny * p->nz;
         uint8_t mx = 0;
@@ -207,8 +206,11 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->tile_buf);
     cudaFree(c->gathered);
     cudaFree(c->far_state);
-    cudaFree(c->chunk_u);
-    cudaFree(c->uk8);
+    cudaFree(c->ut.chunk_u);
+    cudaFree(c->ut.ukf);
+    cudaFree(c->ut.udiag);
+    cudaFree(c->ut.list);
+    cudaFree(c->ut.blocks);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -352,7 +354,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             if (e == cudaSuccess) e = launch_expand(ea, g.R, c->fmt, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e == cudaSuccess && (params->flags & FDIRW_F_DEDUP_STORAGE))
-                e = build_uniform(ea, g.R, c->fmt, dr.n_class, &c->chunk_u, &c->uk8, &c->n_uniform, &c->n_uclasses, s);
+                e = build_uniform(ea, g.R, c->fmt, dr.n_class, &c->ut, s);
             if (e != cudaSuccess) { dfree(); cudaFree(mask_d); g_err = std::string("kgen: ") + cudaGetErrorString(e); return bail(FDIRW_E_CUDA); }
             c->kgen_windows = (uint64_t)dr.n_class;
         }
@@ -427,14 +429,32 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
     a.nxp = g.nxp; a.nyp = g.nyp;
     a.t_begin = t0;
     a.t_end = t1;
-    a.chunk_u = c->chunk_u;  // N4 (null unless FDIRW_F_DEDUP_STORAGE)
-    a.uk8 = c->uk8;
+    a.chunk_u = c->ut.chunk_u;  // N4 (null unless FDIRW_F_DEDUP_STORAGE): skip uniform chunks
     if (c->far && far_terms) {
         a.pbc = c->pbc;
         a.far_state = c->far_state;
         a.tile_sum = c->tile_buf + 1;
     }
     return launch_superpose(a, g.R, c->fmt, s);
+}
+
+// N4: the uniform chunks (one CTA per ≤ 256 chunks of one class, class kernel in smem).
+static cudaError_t superpose_uniform(fdirw_ctx* c, const float* src, float* out, long ps, long rs, cudaStream_t s)
+{
+    if (!c->ut.chunk_u || c->ut.n_blocks == 0) return cudaSuccess;
+    const Geometry& g = c->g;
+    UniArgs u{};
+    u.cpad = src;
+    u.out = out;
+    u.out_ps = ps;
+    u.out_rs = rs;
+    u.nx = g.nx; u.ny = g.ny; u.nxq = g.nxq; u.tile = g.tile; u.tpp = g.tpp; u.nxp = g.nxp; u.nyp = g.nyp;
+    u.list = c->ut.list;
+    u.blocks = c->ut.blocks;
+    u.n_blocks = c->ut.n_blocks;
+    u.ukf = c->ut.ukf;
+    u.udiag = c->ut.udiag;
+    return launch_superpose_uniform(u, g.R, s);
 }
 
 // N2: p_BC(x) = 1 − Σ_s W̃_s(x−s) (reading A26) = 1 − (stored operator applied to the
@@ -485,6 +505,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     const Geometry& g = c->g;
     if (c->world == 1) {
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
+        CUDA_TRY(superpose_uniform(c, src, out, ps, rs, s));
         return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
     }
     int i0, i1;
@@ -503,6 +524,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     } else {
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
     }
+    CUDA_TRY(superpose_uniform(c, src, out, ps, rs, s));  // N4 (no-op unless enabled), after the halo
     return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
 }
 
@@ -597,8 +619,8 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->kgen_sources = c->kgen_sources;
     info->kgen_windows = c->kgen_windows;
     info->chunks = (uint64_t)g.nzl * g.ny * g.nxq;
-    info->uniform_chunks = (uint64_t)c->n_uniform;
-    info->uniform_classes = c->n_uclasses;
+    info->uniform_chunks = (uint64_t)c->ut.n_uniform;
+    info->uniform_classes = c->ut.n_u;
     return FDIRW_OK;
 }
 

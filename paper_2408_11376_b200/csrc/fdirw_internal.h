@@ -93,9 +93,9 @@ struct ExpandArgs {
     int nx, ny, nxq, tile, tpp, n_tiles, nxp, nyp;
 };
 cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s);
-// N4: per-chunk uniform class table (see superpose.cu); *chunk_u / *uk8 are cudaMalloc'ed
-cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, int** chunk_u, void** uk8,
-                          long* n_uniform, int* n_u, cudaStream_t s);
+// N4: per-chunk uniform class tables (see superpose.cu); arrays are cudaMalloc'ed
+struct UniformTables;
+cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, UniformTables* t, cudaStream_t s);
 
 struct SuperArgs {
     const float* cpad;   // padded state, pointer to padded plane 0
@@ -116,6 +116,30 @@ struct SuperArgs {
     const void* uk8 = nullptr;
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
+
+// N4: uniform chunks, one CTA per block of ≤ 256 chunks of one class (superpose.cu)
+struct UniArgs {
+    const float* cpad;
+    float* out;
+    long out_ps, out_rs;
+    int nx, ny, nxq, tile, tpp, nxp, nyp;
+    const int* list;      // uniform chunk ids (tile·tile_sz + e), grouped by class
+    const int4* blocks;   // {start in list, count ≤ 256, class u, 0}
+    int n_blocks;
+    const float* ukf;     // [u][K−1] class kernels in slot order, decoded to fp32
+    const float* udiag;   // [u] fp32 diagonal
+};
+cudaError_t launch_superpose_uniform(const UniArgs& a, int R, cudaStream_t s);
+
+struct UniformTables {
+    int* chunk_u = nullptr;   // [n_tiles·tile] class u or −1
+    float* ukf = nullptr;
+    float* udiag = nullptr;
+    int* list = nullptr;
+    int4* blocks = nullptr;
+    int n_blocks = 0, n_u = 0;
+    long n_uniform = 0;
+};
 
 // ---- N2 far field (superpose.cu) ----------------------------------------------------
 // per-tile Σ c over a dense slab field (far voxels skipped), same order as superpose's sums

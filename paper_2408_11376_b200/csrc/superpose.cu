@@ -137,6 +137,111 @@ __device__ __forceinline__ void do_row(const float* srow, const WT* wp, size_t w
     }
 }
 
+// N4: one (oz, oy) row with the weights of a uniform chunk — the class kernel's value for
+// this slot, shared by all 8 targets, read from shared memory.  The same fmaf sequence and
+// (hi, lo) update as do_row, so the result is bitwise the dense path's.
+template <int R, bool CENTRE_ROW>
+__device__ __forceinline__ void do_row_u(const float* srow, const float* ws, float hi[8], float lo[8])
+{
+    float seg[24];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const float4 v = ld_c(srow + 4 * i);
+        seg[4 * i] = v.x; seg[4 * i + 1] = v.y; seg[4 * i + 2] = v.z; seg[4 * i + 3] = v.w;
+    }
+    float p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = 0.f;
+#pragma unroll
+    for (int ox = -R; ox <= R; ++ox) {
+        if (CENTRE_ROW && ox == 0) continue;
+        const int k = CENTRE_ROW ? (ox < 0 ? ox + R : ox + R - 1) : ox + R;
+        const float w = ws[k];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) p[j] = fmaf(w, seg[j - ox + 8], p[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float s, e;
+        two_sum(hi[j], p[j], s, e);
+        hi[j] = s;
+        lo[j] = __fadd_rn(lo[j], e);
+    }
+}
+
+// N4: a CTA = up to 256 uniform chunks of ONE class u; the class kernel (slot order, fp32
+// values decoded from the storage format) is staged once in shared memory.  No weight bytes
+// come from HBM: the chunk's cost is FMAs + L1-resident C reads.
+template <int R>
+__global__ void __launch_bounds__(256) superpose_uniform_kernel(const UniArgs a)
+{
+    constexpr int L = 2 * R + 1, K = L * L * L;
+    __shared__ float ws[K - 1];
+    const int4 b = a.blocks[blockIdx.x];  // {start, count, u, -}
+    for (int i = threadIdx.x; i < K - 1; i += blockDim.x) ws[i] = a.ukf[(size_t)b.z * (K - 1) + i];
+    __syncthreads();
+    if ((int)threadIdx.x >= b.y) return;
+    const int chunk = a.list[b.x + threadIdx.x];
+    const int tile = chunk / a.tile, e = chunk % a.tile;
+    const int zl = tile / a.tpp, tp = tile % a.tpp;
+    const int q = tp * a.tile + e;
+    const int y = q / a.nxq, x = (q % a.nxq) * 8;
+    const long nxp = a.nxp, plane = (long)a.nyp * nxp;
+    const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
+    const float d = a.udiag[b.z];
+    float hi[8], lo[8];
+    {
+        const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
+        hi[0] = d * v0.x; hi[1] = d * v0.y; hi[2] = d * v0.z; hi[3] = d * v0.w;
+        hi[4] = d * v1.x; hi[5] = d * v1.y; hi[6] = d * v1.z; hi[7] = d * v1.w;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) lo[j] = 0.f;
+    }
+    do_row_u<R, true>(c0 - 8, ws, hi, lo);
+    const float* wr = ws + (L - 1);
+#pragma unroll 1
+    for (int r = 0; r < L * L; ++r) {
+        if (r == R * L + R) continue;
+        const int oz = r / L - R, oy = r % L - R;
+        do_row_u<R, false>(c0 - (long)oz * plane - (long)oy * nxp - 8, wr, hi, lo);
+        wr += L;
+    }
+    float* out = a.out + (long)zl * a.out_ps + (long)y * a.out_rs + x;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(hi[j], lo[j]);
+    if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) out[j] = acc[j];
+    }
+}
+
+template <int R>
+static cudaError_t launch_uniform_r(const UniArgs& a, cudaStream_t s)
+{
+    if (a.n_blocks <= 0) return cudaSuccess;
+    superpose_uniform_kernel<R><<<a.n_blocks, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_superpose_uniform(const UniArgs& a, int R, cudaStream_t s)
+{
+    switch (R) {
+        case 1: return launch_uniform_r<1>(a, s);
+        case 2: return launch_uniform_r<2>(a, s);
+        case 3: return launch_uniform_r<3>(a, s);
+        case 4: return launch_uniform_r<4>(a, s);
+        case 5: return launch_uniform_r<5>(a, s);
+        case 6: return launch_uniform_r<6>(a, s);
+        case 7: return launch_uniform_r<7>(a, s);
+        case 8: return launch_uniform_r<8>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 // Deterministic fp64 sum over the CTA (≤ 256 threads): shuffle tree, then warps in order.
 __device__ __forceinline__ double tile_block_sum(double s)
 {
@@ -159,7 +264,9 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
     const int zl = tile / a.tpp, tp = tile % a.tpp;
     const int e = threadIdx.x;
     const int q = tp * a.tile + e;
-    const bool real = q < a.ny * a.nxq;  // false: dummy chunk at the end of the plane
+    bool real = q < a.ny * a.nxq;  // false: dummy chunk at the end of the plane
+    // N4: uniform chunks are computed by superpose_uniform_kernel (no HBM weight stream)
+    if (real && a.chunk_u && a.chunk_u[(size_t)tile * a.tile + e] >= 0) real = false;
     if (!real && a.tile_sum == nullptr) return;
     const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;  // dummies: harmless reads
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
@@ -167,18 +274,6 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
     size_t wstride = (size_t)a.tile * 8;
     const WT* wt = reinterpret_cast<const WT*>(a.Wt) + ((size_t)tile * (K - 1) * a.tile + e) * 8;
     uint64_t pol = evict_first_policy();
-    if (a.chunk_u) {
-        // N4 (uniform chunks): every source of these 8 targets has the same window class u,
-        // so its weights are class u's kernel, read from the small replicated table uk8
-        // (L1/L2-resident, broadcast across the warp) instead of streaming from HBM.
-        // Same instructions, different address: no divergence between the two kinds.
-        const int u = a.chunk_u[(size_t)tile * a.tile + e];
-        if (u >= 0) {
-            wt = reinterpret_cast<const WT*>(a.uk8) + (size_t)u * (K - 1) * 8;
-            wstride = 8;
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        }
-    }
     const float* dp = a.diag + ((size_t)tile * a.tile + e) * 8;
 
     float hi[8], lo[8];

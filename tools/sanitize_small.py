@@ -1,0 +1,62 @@
+#!/usr/bin/env python
+"""Small end-to-end exercise of every CUDA entry point, for compute-sanitizer
+(memcheck / racecheck / initcheck):  compute-sanitizer --tool memcheck python tools/sanitize_small.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import fdirw_inputs as fi  # noqa: E402
+import paper_2408_11376_b200 as fd  # noqa: E402
+
+
+def params(shape, R, n_fd, fmt="bf16", flags=0, v_far=0.0):
+    nz, ny, nx = shape
+    return fd.Params(nx=nx, ny=ny, nz=nz, dh=1.0, D_fast=1.0, D_slow=1e-3, dt=0.1 * n_fd, radius=R, n_fd=0,
+                     weights=fmt, flags=flags, v_far=v_far)
+
+
+def main():
+    shape = (12, 11, 21)
+    mask = fi.porous_particle(shape, 4, pore_r=(1.0, 1.5), n_pores=3, seed=1)
+    c0 = torch.from_numpy(fi.initial_c(mask, "random", seed=1)).cuda()
+    for fmt, flags in (("bf16", 0), ("fp32", fd.F_NO_DEDUP), ("fp16", fd.F_DEDUP_STORAGE)):
+        with fd.build_kernels(params(shape, 3, 30, fmt, flags), mask) as ctx:
+            out = torch.empty_like(c0)
+            fd.step(ctx, c0, out)
+            c = c0.clone()
+            fd.run(ctx, c, 3)
+            fd.mass(ctx, c)
+            fd.export_kernels(ctx, (0, 5, 0, 4, 0, 3))
+    # far field (N2)
+    fmask = fi.with_far_field(fi.porous_particle(shape, 4, pore_r=(1.0, 1.5), n_pores=3, seed=1), 4, 2.0)
+    with fd.build_kernels(params(shape, 2, 20, v_far=100.0), fmask) as ctx:
+        c = c0.clone()
+        fd.far_init(ctx, c, 0.5)
+        fd.run(ctx, c, 2)
+        fd.far_get(ctx)
+    # virtual ranks
+    sl = fd.slabs(shape[0], 3)
+    ctxs = [fd.build_kernels(params(shape, 3, 20, v_far=100.0), fmask, rank=r, world=3, z_begin=a, z_end=b, device=0)
+            for r, (a, b) in enumerate(sl)]
+    cin = [c0[a:b].contiguous() for a, b in sl]
+    cout = [torch.empty_like(t) for t in cin]
+    fd.far_init_virtual(ctxs, cin, 0.5)
+    fd.step_virtual(ctxs, cin, cout)
+    for x in ctxs:
+        fd.destroy(x)
+    # coarse mesh (N1)
+    region = fi.near_field(mask, 4, margin=2)
+    with fd.coarse_build(params(shape, 1, 30), region, block=3) as cc:
+        out = torch.empty_like(c0)
+        fd.coarse_step(cc, c0, out)
+        fd.coarse_run(cc, out, 2)
+        fd.coarse_export(cc)
+    torch.cuda.synchronize()
+    print("sanitize_small: ok")
+
+
+if __name__ == "__main__":
+    main()

@@ -162,7 +162,9 @@ def run(mask: np.ndarray, c0: np.ndarray, c_far0: float, ab: Absorb, steps: int,
     """The integrated loop; returns (c, c_far, kinetics list of (Q_S, Q_L, c_far, c̄_S))."""
     pb = liquid_problem(mask, ab)
     W = build_kernels(pb)
-    Wq = quantize(pb, W, "fp16") if mode in ("mixed", "fp16") else (quantize(pb, W, "fp32") if mode == "fp32" else W)
+    # the paper stores P plainly in the mode's format (P:157): no diagonal fix-up here
+    Wq = (quantize(pb, W, "fp16", mass_fix=False) if mode in ("mixed", "fp16")
+          else (quantize(pb, W, "fp32", mass_fix=False) if mode == "fp32" else W))
     pbc = farfield.p_bc_full(pb, Wq)
     c = np.asarray(c0, np.float64) * (mask != 2)
     M0 = float(c.sum()) + c_far0 * ab.V_far

@@ -190,6 +190,36 @@ fdirw_status fdirw_far_init_virtual(fdirw_ctx* const* ctxs, int32_t n, const flo
 /* N2: current c_far (after the last enqueued step).  Synchronises cuda_stream. */
 fdirw_status fdirw_far_get(fdirw_ctx* ctx, double* c_far_out, void* cuda_stream);
 
+/* ---- NEXT row N3: integrated absorption loop (Eqs.1-7, Fig.4) -------------
+ * Table 1 quantities for components (2)-(3) of P:42. */
+typedef struct {
+    double D_S;     /* effective solid diffusivity D_S·A_S/RT (slow FD, solid–solid faces)   */
+    double k;       /* pseudo-second-order rate constant [1/s] (Eq.4)                       */
+    double c_S_eq;  /* solid equilibrium concentration (Eq.6), > 0                          */
+    double c_L_eq;  /* liquid equilibrium concentration (Eq.5), > 0                         */
+} fdirw_absorb_params;
+
+/* n_steps macro steps of the integrated loop on c_dev (world == 1; build the context with
+ * D_slow = 0 so the liquid FDiRW treats the solid as impermeable):
+ *   (1) FDiRW liquid step (+ p_BC·c_far, Eq.8, when v_far > 0)
+ *   (2) solid FD, n_s = ceil(D_S·Δt/(0.1·Δh²)) substeps
+ *   (3) PSO interface reaction per solid|liquid face (Eqs.4-6, Jacobi); a liquid voxel
+ *       never gives more than c − c_L_eq (reading A29)
+ *   (4) Eq.7 c_far update; (5) kinetics
+ * kinetics_host (may be NULL): [n_steps][4] = {Q_S, Q_L, c_far, c̄_S = Q_S/(N_S·c_S_eq)}.
+ * Synchronises cuda_stream. */
+fdirw_status fdirw_absorb_run(fdirw_ctx* ctx, const fdirw_absorb_params* params, float* c_dev, int32_t n_steps,
+                              double* kinetics_host, void* cuda_stream);
+
+/* §3.3 precision modes of the superposition (Figs.8-10), world == 1, dense layout:
+ *   0 default: stored weights, fp32 FMA products, compensated fp32 sum (the product path)
+ *   1 "FP32":  FP32 weights, fp32 products, plain fp32 running sum
+ *   2 "mixed": FP16 weights, C converted to fp16, fp16 products, fp32 sum
+ *   3 "FP16":  as 2 with an fp16 running sum
+ * Modes 1-3 are study kernels (one thread per target), used through fdirw_run /
+ * fdirw_absorb_run.  FDIRW_E_STATE if the weight format does not match. */
+fdirw_status fdirw_set_precision_mode(fdirw_ctx* ctx, int32_t mode);
+
 /* Frees everything the context owns (synchronises its device first).  NULL is a no-op. */
 void fdirw_destroy(fdirw_ctx* ctx);
 

@@ -37,7 +37,8 @@ EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fd
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
            "fdirw_export_kernels", "fdirw_step_virtual", "fdirw_coarse_build", "fdirw_coarse_step",
            "fdirw_coarse_run", "fdirw_coarse_query", "fdirw_coarse_export", "fdirw_coarse_destroy",
-           "fdirw_far_init", "fdirw_far_init_virtual", "fdirw_far_get"]
+           "fdirw_far_init", "fdirw_far_init_virtual", "fdirw_far_get", "fdirw_absorb_run",
+           "fdirw_set_precision_mode"]
 
 
 class fdirw_params(ctypes.Structure):
@@ -124,6 +125,18 @@ _lib.fdirw_far_init_virtual.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32, cty
 _lib.fdirw_far_init_virtual.restype = _st
 _lib.fdirw_far_get.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), _vp]
 _lib.fdirw_far_get.restype = _st
+
+
+class fdirw_absorb_params(ctypes.Structure):
+    _fields_ = [("D_S", ctypes.c_double), ("k", ctypes.c_double), ("c_S_eq", ctypes.c_double),
+                ("c_L_eq", ctypes.c_double)]
+
+
+_lib.fdirw_absorb_run.argtypes = [_vp, ctypes.POINTER(fdirw_absorb_params), _vp, ctypes.c_int32, _vp, _vp]
+_lib.fdirw_absorb_run.restype = _st
+_lib.fdirw_set_precision_mode.argtypes = [_vp, ctypes.c_int32]
+_lib.fdirw_set_precision_mode.restype = _st
+PRECISION_MODES = {"default": 0, "fp32": 1, "mixed": 2, "fp16": 3}
 
 
 class FdirwError(RuntimeError):
@@ -374,3 +387,19 @@ def far_get(ctx: Context, stream=None) -> float:
     v = ctypes.c_double()
     _check(_lib.fdirw_far_get(ctx.handle, ctypes.byref(v), _stream(stream)))
     return v.value
+
+
+# ---- NEXT row N3: integrated absorption loop + §3.3 precision modes ------------------------
+def absorb_run(ctx: Context, c, n_steps: int, D_S: float, k: float, c_S_eq: float, c_L_eq: float,
+               stream=None) -> np.ndarray:
+    """fdirw_absorb_run → kinetics [n_steps][4] = (Q_S, Q_L, c_far, c̄_S)."""
+    ap = fdirw_absorb_params(D_S, k, c_S_eq, c_L_eq)
+    kin = np.zeros((max(int(n_steps), 1), 4), np.float64)
+    _check(_lib.fdirw_absorb_run(ctx.handle, ctypes.byref(ap), _dptr(c), int(n_steps),
+                                 kin.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
+    return kin[:n_steps]
+
+
+def set_precision_mode(ctx: Context, mode):
+    """'default' | 'fp32' | 'mixed' | 'fp16' (or 0..3), see include/fdirw.h."""
+    _check(_lib.fdirw_set_precision_mode(ctx.handle, PRECISION_MODES.get(mode, mode)))

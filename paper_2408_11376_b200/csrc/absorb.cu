@@ -1,0 +1,252 @@
+// absorb.cu — NEXT row N3: the integrated absorption loop (P:42 components, Eqs.1-7,
+// P:165-171 Fig.4) and the §3.3 precision modes of the superposition (Figs.8-10).
+//
+// Per macro step (operator split, reading A29; world == 1):
+//   (1) FDiRW liquid step (the context's kernels, solid impermeable: D_slow = 0) — superpose.cu
+//   (2) slow solid FD: n_s Jacobi passes, solid–solid faces, λ_S = D_S·A_S/RT·Δt_s/Δh²
+//   (3) PSO interface reaction (Eqs.4-6), per solid|liquid face pair, pre-step values; a
+//       liquid voxel gives at most c − c_L^eq (all its transfers scaled by one factor α)
+//   (4) Eq.7 c_far from the conserved total (tile sums in global order, as in N2)
+//   (5) kinetics Q_S, Q_L (fp64 deterministic sums)
+// The state is the padded layout of the fine path (zero halo); phases come from a padded
+// uint8 map (255 = outside the domain).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "fdirw_internal.h"
+#include "layout.cuh"
+
+namespace fdirw {
+
+__device__ __forceinline__ long pidx(int x, int y, int z, int R, int nxp, int nyp)
+{
+    return ((long)(z + R) * nyp + (y + R)) * nxp + kPadX + x;
+}
+
+// phase map in the padded layout: 0 solid, 1 near liquid, 2 far, 255 outside
+__global__ void phase_pad_kernel(const uint8_t* __restrict__ mask, int nx, int ny, int nz, int R, int nxp, int nyp,
+                                 uint8_t* __restrict__ pp)
+{
+    const long n = (long)nx * ny * nz;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+        pp[pidx(x, y, z, R, nxp, nyp)] = mask[i];
+    }
+}
+
+// (2) one Jacobi pass of the solid FD: faces −x,+x,−y,+y,−z,+z between solid voxels only
+__global__ void solid_fd_kernel(const float* __restrict__ cin, float* __restrict__ cout,
+                                const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R, int nxp, int nyp,
+                                float lam)
+{
+    const long n = (long)nx * ny * nz;
+    const long dxy[3] = {1, nxp, (long)nxp * nyp};
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+        const long p = pidx(x, y, z, R, nxp, nyp);
+        const float c = cin[p];
+        float acc = c;
+        if (pp[p] == 0) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const long q = p + (f & 1 ? dxy[f >> 1] : -dxy[f >> 1]);
+                if (pp[q] == 0) acc = fmaf(lam, cin[q] - c, acc);
+            }
+        }
+        cout[p] = acc;
+    }
+}
+
+__device__ __forceinline__ float fL(float c, float eq) { return c <= eq ? 0.f : (c - eq) / eq; }
+__device__ __forceinline__ float fS(float c, float eq) { return fmaxf((eq - c) / eq, 0.f); }
+
+// (3a) per liquid voxel: requested total Q_l and the clamp factor α_l
+__global__ void react_alpha_kernel(const float* __restrict__ c, const uint8_t* __restrict__ pp, int nx, int ny,
+                                   int nz, int R, int nxp, int nyp, float kdt, float cSeq, float cLeq,
+                                   float* __restrict__ alpha)
+{
+    const long n = (long)nx * ny * nz;
+    const long dxy[3] = {1, nxp, (long)nxp * nyp};
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+        const long p = pidx(x, y, z, R, nxp, nyp);
+        float a = 1.f;
+        if (pp[p] == 1) {
+            const float fl = fL(c[p], cLeq);
+            float Q = 0.f;
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const long q = p + (f & 1 ? dxy[f >> 1] : -dxy[f >> 1]);
+                if (pp[q] == 0) Q += kdt * fS(c[q], cSeq) * fl;
+            }
+            const float avail = fmaxf(c[p] - cLeq, 0.f);
+            if (Q > avail) a = Q > 0.f ? avail / Q : 0.f;
+        }
+        alpha[p] = a;
+    }
+}
+
+// (3b) apply: solid gains Σ α_l q_sl, liquid loses α_l Σ q_sl (the same q expression both sides)
+__global__ void react_apply_kernel(const float* __restrict__ c, const float* __restrict__ alpha,
+                                   const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R, int nxp, int nyp,
+                                   float kdt, float cSeq, float cLeq, float* __restrict__ out)
+{
+    const long n = (long)nx * ny * nz;
+    const long dxy[3] = {1, nxp, (long)nxp * nyp};
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+        const long p = pidx(x, y, z, R, nxp, nyp);
+        float v = c[p];
+        const uint8_t ph = pp[p];
+        if (ph == 0) {
+            const float fs = fS(c[p], cSeq);
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const long q = p + (f & 1 ? dxy[f >> 1] : -dxy[f >> 1]);
+                if (pp[q] == 1) v += alpha[q] * (kdt * fs * fL(c[q], cLeq));
+            }
+        } else if (ph == 1) {
+            const float fl = fL(c[p], cLeq);
+            float Q = 0.f;
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const long q = p + (f & 1 ? dxy[f >> 1] : -dxy[f >> 1]);
+                if (pp[q] == 0) Q += kdt * fS(c[q], cSeq) * fl;
+            }
+            v -= alpha[p] * Q;
+        }
+        out[p] = v;
+    }
+}
+
+// (5) kinetics: Q_S, Q_L partial sums per block (fp64), then a fixed-order final sum
+__global__ void kin_partial_kernel(const float* __restrict__ c, const uint8_t* __restrict__ pp, int nx, int ny,
+                                   int nz, int R, int nxp, int nyp, double* __restrict__ part)
+{
+    __shared__ double rs[8], rl[8];
+    const long n = (long)nx * ny * nz;
+    double s = 0.0, l = 0.0;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+        const long p = pidx(x, y, z, R, nxp, nyp);
+        if (pp[p] == 0) s += (double)c[p];
+        else if (pp[p] == 1) l += (double)c[p];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+    }
+    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = s; rl[threadIdx.x >> 5] = l; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ts = 0.0, tl = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { ts += rs[w]; tl += rl[w]; }
+        part[2 * blockIdx.x] = ts;
+        part[2 * blockIdx.x + 1] = tl;
+    }
+}
+
+__global__ void kin_final_kernel(const double* __restrict__ part, int nblk, double* __restrict__ far_state,
+                                 double v_far, double n_solid, double cSeq, int far, double* __restrict__ rec)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s = 0.0, l = 0.0;
+    for (int b = 0; b < nblk; ++b) { s += part[2 * b]; l += part[2 * b + 1]; }
+    if (far) far_state[0] = (far_state[1] - s - l) / v_far;  // (4) Eq.7 after the whole step
+    rec[0] = s;
+    rec[1] = l;
+    rec[2] = far ? far_state[0] : 0.0;
+    rec[3] = n_solid > 0 ? s / (n_solid * cSeq) : 0.0;     // c̄_S (Fig.10)
+}
+
+static unsigned gridn(long n)
+{
+    long b = (n + 255) / 256;
+    if (b > 148L * 16) b = 148L * 16;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_phase_pad(const uint8_t* mask, const Geometry& g, uint8_t* pp, cudaStream_t s)
+{
+    cudaError_t e = cudaMemsetAsync(pp, 255, g.state_elems, s);
+    if (e != cudaSuccess) return e;
+    phase_pad_kernel<<<gridn((long)g.nx * g.ny * g.nz), 256, 0, s>>>(mask, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, pp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uint8_t* pp, const Geometry& g,
+                               const AbsorbArgs& ab, double* part, double* far_state, double v_far, int far,
+                               double* rec, cudaStream_t s, float** result)
+{
+    const long n = (long)g.nx * g.ny * g.nz;
+    // (2) solid FD, n_s passes
+    for (int k = 0; k < ab.n_s; ++k) {
+        solid_fd_kernel<<<gridn(n), 256, 0, s>>>(cur, other, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.lam_s);
+        float* t = cur; cur = other; other = t;
+    }
+    // (3) interface reaction
+    react_alpha_kernel<<<gridn(n), 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt, ab.cSeq,
+                                                ab.cLeq, alpha);
+    react_apply_kernel<<<gridn(n), 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt,
+                                                ab.cSeq, ab.cLeq, other);
+    float* t = cur; cur = other; other = t;
+    // (4)+(5)
+    const int nblk = 148 * 4;
+    kin_partial_kernel<<<nblk, 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, part);
+    kin_final_kernel<<<1, 32, 0, s>>>(part, nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec);
+    *result = cur;
+    return cudaGetLastError();
+}
+
+// ---- §3.3 precision modes of the superposition (study) ---------------
+// one thread per target; sources visited in ascending order (descending offset o)
+template <int MODE, typename WT>
+__global__ void superpose_study_kernel(const StudyArgs a)
+{
+    const int R = a.R, L = 2 * R + 1, K = L * L * L;
+    const long n = (long)a.nx * a.ny * a.nzl;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % a.nx), y = (int)((i / a.nx) % a.ny), zl = (int)(i / ((long)a.nx * a.ny));
+        const int q = y * a.nxq + (x >> 3);
+        const size_t tile = (size_t)zl * a.tpp + q / a.tile;
+        const int e = q % a.tile, j = x & 7;
+        const long p = pidx(x, y, zl, R, a.nxp, a.nyp);
+        const WT* wt = reinterpret_cast<const WT*>(a.Wt);
+        float acc32 = 0.f;
+        __half acc16 = __float2half_rn(0.f);
+        for (int o = K - 1; o >= 0; --o) {
+            const int ox = o % L - R, oy = (o / L) % L - R, oz = o / (L * L) - R;
+            const float cs = a.cpad[p - ((long)oz * a.nyp + oy) * a.nxp - ox];
+            float w;
+            if (o == K / 2) w = a.diag[(tile * a.tile + e) * 8 + j];
+            else {
+                const size_t idx = ((tile * (size_t)(K - 1) + slot_of(ox, oy, oz, R)) * a.tile + e) * 8 + j;
+                if (sizeof(WT) == 4) w = reinterpret_cast<const float*>(wt)[idx];
+                else w = __half2float(reinterpret_cast<const __half*>(wt)[idx]);
+            }
+            if (MODE == 1) {                 // fp32 weights, fp32 products, plain fp32 sum
+                acc32 = __fadd_rn(acc32, __fmul_rn(w, cs));
+            } else {                         // C → fp16, fp16 product
+                const __half pr = __hmul(__float2half_rn(w), __float2half_rn(cs));
+                if (MODE == 2) acc32 = __fadd_rn(acc32, __half2float(pr));   // fp32 accumulation
+                else acc16 = __hadd(acc16, pr);                               // FP16 everything
+            }
+        }
+        float v = MODE == 3 ? __half2float(acc16) : acc32;
+        if (a.pbc) v = fmaf(a.pbc[(tile * a.tile + e) * 8 + j], (float)a.far_state[0], v);
+        a.out[p] = v;
+    }
+}
+
+cudaError_t launch_superpose_study(const StudyArgs& a, int mode, cudaStream_t s)
+{
+    const unsigned grid = gridn((long)a.nx * a.ny * a.nzl);
+    if (mode == 1) superpose_study_kernel<1, float><<<grid, 256, 0, s>>>(a);
+    else if (mode == 2) superpose_study_kernel<2, __half><<<grid, 256, 0, s>>>(a);
+    else if (mode == 3) superpose_study_kernel<3, __half><<<grid, 256, 0, s>>>(a);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+}  // namespace fdirw

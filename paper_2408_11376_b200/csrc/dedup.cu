@@ -146,13 +146,24 @@ __global__ void __launch_bounds__(256) expand_kernel(const ExpandArgs a)
 {
     constexpr int L = 2 * R + 1, LL = L * L, K = L * L * L;
     const int tile = blockIdx.x;
-    const int zl = tile / a.tpp, tp = tile % a.tpp;
     const int e = threadIdx.x;
-    const int q = tp * a.tile + e;
+    int zl, q;
+    bool real;
+    if (a.list) {  // N4: compacted non-uniform chunks
+        const long idx = (long)tile * a.tile + e;
+        real = idx < a.n_list;
+        const int chunk = real ? a.list[idx] : 0;
+        const int ot = chunk / a.tile;
+        zl = ot / a.tpp;
+        q = (ot % a.tpp) * a.tile + chunk % a.tile;
+    } else {
+        zl = tile / a.tpp;
+        q = (tile % a.tpp) * a.tile + e;
+        real = q < a.ny * a.nxq;
+    }
     const size_t wstride = (size_t)a.tile * 8;
     WT* wt = reinterpret_cast<WT*>(a.Wt) + ((size_t)tile * (K - 1) * a.tile + e) * 8;
     const WT* cw = reinterpret_cast<const WT*>(a.class_w);
-    const bool real = q < a.ny * a.nxq;
     const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const int* c0 = a.class_pad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
@@ -326,6 +337,19 @@ cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, Uni
         t->n_uniform = cnt;
         t->n_u = nu;
         t->n_blocks = (int)blocks.size();
+        // the real non-uniform chunks, in chunk order, compacted into tiles of a.tile
+        std::vector<int> dense;
+        dense.reserve(nch - cnt);
+        for (long i = 0; i < nch; ++i) {
+            const long tt = i / a.tile;
+            const int q = (int)(tt % a.tpp) * a.tile + (int)(i % a.tile);
+            if (h[i] < 0 && q < a.ny * a.nxq) dense.push_back((int)i);
+        }
+        t->n_dense = (long)dense.size();
+        t->nd_tiles = (int)((t->n_dense + a.tile - 1) / a.tile);
+        if (e == cudaSuccess) e = cudaMalloc(&t->dense_list, std::max<size_t>(dense.size(), 1) * 4);
+        if (e == cudaSuccess && !dense.empty())
+            e = cudaMemcpy(t->dense_list, dense.data(), dense.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMalloc(&t->list, std::max<size_t>(list.size(), 1) * 4);
         if (e == cudaSuccess) e = cudaMalloc(&t->blocks, std::max<size_t>(blocks.size(), 1) * sizeof(int4));
         if (e == cudaSuccess && !list.empty())

@@ -45,6 +45,14 @@ struct fdirw_ctx {
     double* gathered = nullptr;   // [world · tile_stride] (NCCL all-gather target)
     double* far_state = nullptr;  // {c_far, M0}
     long tile_stride = 0;
+    // N3 integrated loop / precision modes (world == 1)
+    int prec_mode = 0;            // 0 = default kernel; 1/2/3 = §3.3 study modes (absorb.cu)
+    uint8_t* phase_pp = nullptr;  // padded phase map (255 outside)
+    float* alpha = nullptr;       // padded scratch for the reaction clamp
+    double* kin_part = nullptr;
+    double* kin_rec = nullptr;
+    int kin_cap = 0;
+    double n_solid = 0;
 };
 
 static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s);
@@ -160,6 +168,8 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if ((p->flags & FDIRW_F_NO_DEDUP) && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_DEDUP_STORAGE needs the window de-duplication");
     if (!(p->v_far >= 0)) return fail(FDIRW_E_INVALID, "v_far must be >= 0");
+    if (dist && dist->world > 1 && (p->flags & FDIRW_F_DEDUP_STORAGE))
+        return fail(FDIRW_E_INVALID, "FDIRW_F_DEDUP_STORAGE needs world == 1");
     if (p->v_far > 0 && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_DEDUP_STORAGE is not combined with a far field (v_far > 0)");
     if (scan_phase) {
@@ -206,7 +216,12 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->tile_buf);
     cudaFree(c->gathered);
     cudaFree(c->far_state);
+    cudaFree(c->phase_pp);
+    cudaFree(c->alpha);
+    cudaFree(c->kin_part);
+    cudaFree(c->kin_rec);
     cudaFree(c->ut.chunk_u);
+    cudaFree(c->ut.dense_list);
     cudaFree(c->ut.ukf);
     cudaFree(c->ut.udiag);
     cudaFree(c->ut.list);
@@ -296,8 +311,6 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     const size_t plane = (size_t)g.nx * g.ny;
     const size_t mbytes = (size_t)(g.mz1 - g.mz0) * plane;
     if ((st = alloc((void**)&mask_d, mbytes, "mask")) != FDIRW_OK) return bail(st);
-    if ((st = alloc(&c->Wt, g.w_elems * c->b_w, "weights")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
-    if ((st = alloc((void**)&c->diag, g.diag_elems * 4, "diagonal")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
     for (int i = 0; i < 2; ++i)
         if ((st = alloc((void**)&c->cpad[i], g.state_elems * 4, "state")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
     c->mass_blocks = 148 * 4;
@@ -319,8 +332,6 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     ka.n_fd = d.n_fd;
     ka.fmt = c->fmt;
     ka.mass_fix = (params->flags & FDIRW_F_NO_MASS_FIX) ? 0 : 1;
-    ka.Wt = c->Wt;
-    ka.diag = c->diag;
     ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;
     c->kgen_sources = (uint64_t)g.nx * g.ny * (g.sz1 - g.sz0);
     c->kgen_windows = c->kgen_sources;
@@ -349,12 +360,28 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             ka.class_w = class_w;
             ka.class_diag = class_diag;
             e = launch_kgen(ka, g.R, s);
-            ExpandArgs ea{class_pad, class_w, class_diag, c->Wt, c->diag, g.nx, g.ny, g.nxq, g.tile, g.tpp,
+            ExpandArgs ea{class_pad, class_w, class_diag, nullptr, nullptr, g.nx, g.ny, g.nxq, g.tile, g.tpp,
                           g.n_tiles, g.nxp, g.nyp};
-            if (e == cudaSuccess) e = launch_expand(ea, g.R, c->fmt, s);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-            if (e == cudaSuccess && (params->flags & FDIRW_F_DEDUP_STORAGE))
+            size_t w_elems = g.w_elems, d_elems = g.diag_elems;
+            if (e == cudaSuccess && (params->flags & FDIRW_F_DEDUP_STORAGE)) {
+                // N4: uniform chunks get no gather weights; the others are compacted into tiles
                 e = build_uniform(ea, g.R, c->fmt, dr.n_class, &c->ut, s);
+                ea.list = c->ut.dense_list;
+                ea.n_list = c->ut.n_dense;
+                ea.n_tiles = c->ut.nd_tiles;
+                w_elems = (size_t)c->ut.nd_tiles * (g.K - 1) * g.tile * kChunk;
+                d_elems = (size_t)c->ut.nd_tiles * g.tile * kChunk;
+            }
+            if (e == cudaSuccess) {
+                if ((st = alloc(&c->Wt, (w_elems ? w_elems : 1) * c->b_w, "weights")) != FDIRW_OK ||
+                    (st = alloc((void**)&c->diag, (d_elems ? d_elems : 1) * 4, "diagonal")) != FDIRW_OK) {
+                    dfree(); cudaFree(mask_d); return bail(st);
+                }
+                ea.Wt = c->Wt;
+                ea.diag = c->diag;
+                e = launch_expand(ea, g.R, c->fmt, s);
+            }
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) { dfree(); cudaFree(mask_d); g_err = std::string("kgen: ") + cudaGetErrorString(e); return bail(FDIRW_E_CUDA); }
             c->kgen_windows = (uint64_t)dr.n_class;
         }
@@ -362,6 +389,13 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     }
     if (!dedup) {
         ka.src_list = nullptr; ka.n_list = 0; ka.class_w = nullptr; ka.class_diag = nullptr;
+        if ((st = alloc(&c->Wt, g.w_elems * c->b_w, "weights")) != FDIRW_OK ||
+            (st = alloc((void**)&c->diag, g.diag_elems * 4, "diagonal")) != FDIRW_OK) {
+            cudaFree(mask_d);
+            return bail(st);
+        }
+        ka.Wt = c->Wt;
+        ka.diag = c->diag;
         BAIL_CUDA(cudaMemsetAsync(c->Wt, 0, g.w_elems * c->b_w, s));
         BAIL_CUDA(cudaMemsetAsync(c->diag, 0, g.diag_elems * 4, s));
         BAIL_CUDA(launch_kgen(ka, g.R, s));
@@ -392,6 +426,15 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             cudaFree(mask_d);
             return bail(st);
         }
+    }
+    if (c->world == 1) {  // N3: padded phase map for the integrated loop (mask_d holds the whole grid)
+        for (size_t i = 0; i < plane * g.nz; ++i) c->n_solid += phase_host[i] == 0;
+        if ((st = alloc((void**)&c->phase_pp, g.state_elems, "phase map")) != FDIRW_OK) {
+            cudaFree(mask_d);
+            return bail(st);
+        }
+        BAIL_CUDA(launch_phase_pad(mask_d, g, c->phase_pp, s));
+        BAIL_CUDA(cudaStreamSynchronize(s));
     }
     cudaFree(mask_d);
 
@@ -429,7 +472,8 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
     a.nxp = g.nxp; a.nyp = g.nyp;
     a.t_begin = t0;
     a.t_end = t1;
-    a.chunk_u = c->ut.chunk_u;  // N4 (null unless FDIRW_F_DEDUP_STORAGE): skip uniform chunks
+    a.list = c->ut.dense_list;  // N4 (null unless FDIRW_F_DEDUP_STORAGE): compacted non-uniform chunks
+    a.n_list = c->ut.n_dense;
     if (c->far && far_terms) {
         a.pbc = c->pbc;
         a.far_state = c->far_state;
@@ -503,9 +547,28 @@ static void split_tiles(const Geometry& g, int* int0, int* int1)
 static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, long rs, cudaStream_t s)
 {
     const Geometry& g = c->g;
+    if (c->world == 1 && c->prec_mode != 0) {  // N3 §3.3 study modes: padded output only
+        StudyArgs a{src, out - ((size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX), c->Wt, c->diag,
+                    g.nx, g.ny, g.nzl, g.nxq, g.tile, g.tpp, g.nxp, g.nyp, g.R, c->pbc, c->far_state};
+        if (ps != (long)g.plane_elems) return fail(FDIRW_E_STATE, "precision study modes run through fdirw_run");
+        CUDA_TRY(launch_superpose_study(a, c->prec_mode, s));
+        if (c->far) {  // study kernel has no tile sums: Eq.7 from a separate pass
+            CUDA_TRY(launch_tile_mass_padded(out, c->farmask, g, c->tile_buf + 1, s));
+            return far_reduce(c, s, 0, 0.0);
+        }
+        return FDIRW_OK;
+    }
     if (c->world == 1) {
+        if (c->ut.chunk_u) {  // N4: dense (HBM-bound) and uniform (FMA-bound) chunks run concurrently
+            CUDA_TRY(cudaEventRecord(c->ev_fork, s));
+            CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+            CUDA_TRY(superpose_uniform(c, src, out, ps, rs, c->comm_stream));
+            CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
+            CUDA_TRY(superpose(c, src, out, ps, rs, 0, c->ut.nd_tiles, s));
+            CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
+            return FDIRW_OK;
+        }
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
-        CUDA_TRY(superpose_uniform(c, src, out, ps, rs, s));
         return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
     }
     int i0, i1;
@@ -524,7 +587,6 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     } else {
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
     }
-    CUDA_TRY(superpose_uniform(c, src, out, ps, rs, s));  // N4 (no-op unless enabled), after the halo
     return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
 }
 
@@ -610,7 +672,8 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->lambda_fast = c->d.lam_ff;
     info->lambda_fs = c->d.lam_fs;
     info->lambda_slow = c->d.lam_ss;
-    info->weight_bytes = (uint64_t)g.w_elems * c->b_w + (uint64_t)g.diag_elems * 4;
+    const uint64_t wt_tiles = c->ut.chunk_u ? (uint64_t)c->ut.nd_tiles : (uint64_t)g.n_tiles;  // N4 compacts
+    info->weight_bytes = wt_tiles * (g.K - 1) * g.tile * kChunk * c->b_w + wt_tiles * g.tile * kChunk * 4;
     info->state_bytes = (uint64_t)g.state_elems * 4 * 2;
     info->bytes_per_voxel_update = (uint64_t)(g.K - 1) * c->b_w + 12;
     info->voxels = (uint64_t)g.nx * g.ny * g.nzl;
@@ -665,6 +728,7 @@ extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k
 {
     if (!c || !k) return fail(FDIRW_E_INVALID, "NULL argument");
     if (c->world != 1) return fail(FDIRW_E_STATE, "debug upload needs world == 1");
+    if (c->ut.chunk_u) return fail(FDIRW_E_STATE, "debug upload needs the dense layout");
     CUDA_TRY(cudaSetDevice(c->device));
     const Geometry& g = c->g;
     const int R = g.R, L = g.L, K = g.K;
@@ -707,6 +771,7 @@ extern "C" fdirw_status fdirw_export_kernels(const fdirw_ctx* c, const int32_t* 
 {
     if (!c || !box || !out) return fail(FDIRW_E_INVALID, "NULL argument");
     if (box[1] < box[0] || box[3] < box[2] || box[5] < box[4]) return fail(FDIRW_E_INVALID, "bad box");
+    if (c->ut.chunk_u) return fail(FDIRW_E_STATE, "export needs the dense layout (FDIRW_F_DEDUP_STORAGE compacts it)");
     CUDA_TRY(cudaSetDevice(c->device));
     const size_t n = (size_t)(box[1] - box[0]) * (box[3] - box[2]) * (box[5] - box[4]) * c->g.K;
     if (n == 0) return FDIRW_OK;
@@ -818,6 +883,73 @@ extern "C" fdirw_status fdirw_far_init_virtual(fdirw_ctx* const* ctxs, int32_t n
     CUDA_TRY(cudaMemcpyAsync(fs, ctxs[0]->far_state, 16, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (M0_out) *M0_out = fs[1];
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_set_precision_mode(fdirw_ctx* c, int32_t mode)
+{
+    if (!c) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (mode < 0 || mode > 3) return fail(FDIRW_E_INVALID, "precision mode must be 0..3");
+    if (mode != 0 && c->world != 1) return fail(FDIRW_E_STATE, "precision study modes need world == 1");
+    if (mode != 0 && c->ut.chunk_u) return fail(FDIRW_E_STATE, "precision study modes need the dense layout");
+    if (mode == 1 && c->fmt != FDIRW_W_FP32) return fail(FDIRW_E_STATE, "mode 1 (fp32) needs FP32 weights");
+    if ((mode == 2 || mode == 3) && c->fmt != FDIRW_W_FP16)
+        return fail(FDIRW_E_STATE, "modes 2/3 (paper mixed / fp16) need FP16 weights");
+    if (c->graph2) {  // the captured step depends on the mode
+        cudaGraphExecDestroy(c->graph2);
+        c->graph2 = nullptr;
+    }
+    c->prec_mode = mode;
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params* ap, float* c_dev, int32_t n,
+                                         double* kinetics_host, void* cuda_stream)
+{
+    if (!c || !ap || !c_dev) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (n < 0) return fail(FDIRW_E_INVALID, "n_steps must be >= 0");
+    if (c->world != 1 || !c->phase_pp) return fail(FDIRW_E_STATE, "the integrated loop needs world == 1");
+    if (!(ap->D_S >= 0) || !(ap->k >= 0) || !(ap->c_S_eq > 0) || !(ap->c_L_eq > 0))
+        return fail(FDIRW_E_INVALID, "need D_S >= 0, k >= 0, c_S_eq > 0, c_L_eq > 0");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const Geometry& g = c->g;
+    AbsorbArgs ab{};
+    const double dt = c->p.dt, dh = c->p.dh;
+    if (ap->D_S > 0) {  // component (3): λ_S ≤ λ* = 0.1 (reading A5 applied to the solid)
+        const double x = ap->D_S * dt / (0.1 * dh * dh);
+        const double nn = std::ceil(x * (1.0 - 1e-9));
+        ab.n_s = nn < 1.0 ? 1 : (int)nn;
+        ab.lam_s = (float)(ap->D_S * (dt / ab.n_s) / (dh * dh));
+    }
+    ab.kdt = (float)(ap->k * dt);
+    ab.cSeq = (float)ap->c_S_eq;
+    ab.cLeq = (float)ap->c_L_eq;
+    ab.n_solid = c->n_solid;
+    fdirw_status st;
+    if (!c->alpha && (st = alloc((void**)&c->alpha, g.state_elems * 4, "reaction scratch")) != FDIRW_OK) return st;
+    if (!c->kin_part && (st = alloc((void**)&c->kin_part, 2 * 148 * 4 * 8, "kinetics")) != FDIRW_OK) return st;
+    if (n > c->kin_cap) {
+        cudaFree(c->kin_rec);
+        c->kin_rec = nullptr;
+        if ((st = alloc((void**)&c->kin_rec, (size_t)n * 4 * 8, "kinetics record")) != FDIRW_OK) return st;
+        c->kin_cap = n;
+    }
+    if (n == 0) return FDIRW_OK;
+    CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s, c->farmask));
+    const size_t ioff = (size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX;
+    float* in = c->cpad[0];
+    for (int i = 0; i < n; ++i) {
+        float* out = in == c->cpad[0] ? c->cpad[1] : c->cpad[0];
+        if ((st = enqueue_step(c, in, out + ioff, (long)g.plane_elems, g.nxp, s)) != FDIRW_OK) return st;  // (1)
+        float* res = nullptr;
+        CUDA_TRY(launch_absorb_tail(out, in, c->alpha, c->phase_pp, g, ab, c->kin_part, c->far_state, c->v_far,
+                                    c->far ? 1 : 0, c->kin_rec + 4 * (size_t)i, s, &res));  // (2)-(5)
+        in = res;
+    }
+    CUDA_TRY(launch_unpack(in, c_dev, g, s));
+    if (kinetics_host) CUDA_TRY(cudaMemcpyAsync(kinetics_host, c->kin_rec, (size_t)n * 32, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return FDIRW_OK;
 }
 

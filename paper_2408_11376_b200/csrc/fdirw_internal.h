@@ -91,6 +91,8 @@ struct ExpandArgs {
     void* Wt;
     float* diag;
     int nx, ny, nxq, tile, tpp, n_tiles, nxp, nyp;
+    const int* list = nullptr;  // N4: compacted chunk ids (null = tile/e is the chunk)
+    long n_list = 0;
 };
 cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s);
 // N4: per-chunk uniform class tables (see superpose.cu); arrays are cudaMalloc'ed
@@ -112,8 +114,8 @@ struct SuperArgs {
     double* tile_sum = nullptr;
     // N4 (uniform-chunk weight dedup): per chunk the uniform class u (−1: use Wt), and the
     // replicated class kernels uk8[u][slot][8]
-    const int* chunk_u = nullptr;
-    const void* uk8 = nullptr;
+    const int* list = nullptr;  // compacted chunk ids (orig tile·tile + e); tiles index the list
+    long n_list = 0;
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
 
@@ -139,10 +141,38 @@ struct UniformTables {
     int4* blocks = nullptr;
     int n_blocks = 0, n_u = 0;
     long n_uniform = 0;
+    int* dense_list = nullptr;  // real non-uniform chunks (chunk order), compacted into tiles
+    long n_dense = 0;
+    int nd_tiles = 0;
 };
+
+// ---- N3 integrated loop + precision modes (absorb.cu) --------------------------------
+struct AbsorbArgs {
+    int n_s;          // solid FD substeps per macro step
+    float lam_s;      // D_S·A_S/RT · (Δt/n_s) / Δh²
+    float kdt;        // k·Δt (Eq.4)
+    float cSeq, cLeq;
+    double n_solid;   // N_S (for c̄_S)
+};
+cudaError_t launch_phase_pad(const uint8_t* mask, const Geometry& g, uint8_t* pp, cudaStream_t s);
+cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uint8_t* pp, const Geometry& g,
+                               const AbsorbArgs& ab, double* part, double* far_state, double v_far, int far,
+                               double* rec, cudaStream_t s, float** result);
+struct StudyArgs {
+    const float* cpad;
+    float* out;           // padded layout
+    const void* Wt;
+    const float* diag;
+    int nx, ny, nzl, nxq, tile, tpp, nxp, nyp, R;
+    const float* pbc;
+    const double* far_state;
+};
+cudaError_t launch_superpose_study(const StudyArgs& a, int mode, cudaStream_t s);
 
 // ---- N2 far field (superpose.cu) ----------------------------------------------------
 // per-tile Σ c over a dense slab field (far voxels skipped), same order as superpose's sums
+cudaError_t launch_tile_mass_padded(const float* c_interior, const uint8_t* farmask, const Geometry& g,
+                                    double* tile_sum, cudaStream_t s);
 cudaError_t launch_tile_mass(const float* c, const uint8_t* farmask, const Geometry& g, double* tile_sum,
                              cudaStream_t s);
 // padded field = 1 on in-domain non-far voxels of planes [z0−R, z1+R) (mask planes from mz0)

@@ -260,13 +260,22 @@ template <int R, typename WT>
 __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
 {
     constexpr int L = 2 * R + 1, K = L * L * L;
-    const int tile = a.t_begin + blockIdx.x;
-    const int zl = tile / a.tpp, tp = tile % a.tpp;
+    const int tile = a.t_begin + blockIdx.x;  // weight tile (compact tile when a.list, N4)
     const int e = threadIdx.x;
-    const int q = tp * a.tile + e;
-    bool real = q < a.ny * a.nxq;  // false: dummy chunk at the end of the plane
-    // N4: uniform chunks are computed by superpose_uniform_kernel (no HBM weight stream)
-    if (real && a.chunk_u && a.chunk_u[(size_t)tile * a.tile + e] >= 0) real = false;
+    int zl, q;
+    bool real;
+    if (a.list) {  // N4: tiles hold only the non-uniform chunks, in chunk order
+        const long idx = (long)tile * a.tile + e;
+        real = idx < a.n_list;
+        const int chunk = real ? a.list[idx] : 0;
+        const int ot = chunk / a.tile;
+        zl = ot / a.tpp;
+        q = (ot % a.tpp) * a.tile + chunk % a.tile;
+    } else {
+        zl = tile / a.tpp;
+        q = (tile % a.tpp) * a.tile + e;
+        real = q < a.ny * a.nxq;  // false: dummy chunk at the end of the plane
+    }
     if (!real && a.tile_sum == nullptr) return;
     const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;  // dummies: harmless reads
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
@@ -377,8 +386,8 @@ __global__ void pack_kernel(const float* __restrict__ c, float* __restrict__ cpa
 
 // ---- N2 far field --------------------------------------------------------------------
 static unsigned grid_for(long n, int threads);
-__global__ void tile_mass_kernel(const float* __restrict__ c, const uint8_t* __restrict__ farmask, int nx, int ny,
-                                 int nxq, int tile, int tpp, double* __restrict__ tile_sum)
+__global__ void tile_mass_kernel(const float* __restrict__ c, long ps, long rs, const uint8_t* __restrict__ farmask,
+                                 int nx, int ny, int nxq, int tile, int tpp, double* __restrict__ tile_sum)
 {
     const int t = blockIdx.x, zl = t / tpp, tp = t % tpp;
     const int q = tp * tile + threadIdx.x;
@@ -388,8 +397,8 @@ __global__ void tile_mass_kernel(const float* __restrict__ c, const uint8_t* __r
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             if (x + j >= nx) continue;
-            const long i = ((long)zl * ny + y) * nx + x + j;
-            s += (farmask && farmask[i]) ? 0.0 : (double)c[i];
+            const long i = ((long)zl * ny + y) * nx + x + j;  // dense index of the far mask
+            s += (farmask && farmask[i]) ? 0.0 : (double)c[(long)zl * ps + (long)y * rs + x + j];
         }
     }
     s = tile_block_sum(s);
@@ -400,7 +409,17 @@ cudaError_t launch_tile_mass(const float* c, const uint8_t* farmask, const Geome
                              cudaStream_t s)
 {
     if (g.n_tiles <= 0) return cudaSuccess;
-    tile_mass_kernel<<<g.n_tiles, g.tile, 0, s>>>(c, farmask, g.nx, g.ny, g.nxq, g.tile, g.tpp, tile_sum);
+    tile_mass_kernel<<<g.n_tiles, g.tile, 0, s>>>(c, (long)g.nx * g.ny, g.nx, farmask, g.nx, g.ny, g.nxq, g.tile,
+                                                  g.tpp, tile_sum);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_mass_padded(const float* c_interior, const uint8_t* farmask, const Geometry& g,
+                                    double* tile_sum, cudaStream_t s)
+{
+    if (g.n_tiles <= 0) return cudaSuccess;
+    tile_mass_kernel<<<g.n_tiles, g.tile, 0, s>>>(c_interior, (long)g.plane_elems, g.nxp, farmask, g.nx, g.ny,
+                                                  g.nxq, g.tile, g.tpp, tile_sum);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,86 @@
+"""GPU parity of NEXT row N3 — the integrated absorption loop (Eqs.1-7) and the §3.3
+precision modes (Figs.8-10) — against oracle/integrated.py, through the C-ABI."""
+import numpy as np
+import pytest
+
+import fdirw_inputs as fi
+from _util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2408_11376_b200 as fd
+
+    return fd
+
+
+@pytest.fixture(scope="module")
+def desk(oracle_lib):
+    """The oracle's desk model: 20³, r_p = 6 particle, near field r_p + 3, Table 1 SI values."""
+    from oracle import integrated as ig
+
+    shape = (20, 20, 20)
+    m = fi.with_far_field(fi.porous_particle(shape, 6, pore_r=(1.0, 2.0), porosity=0.3, seed=3), 6, 3.0)
+    T = fi.TABLE1
+    c0 = np.where(m == 1, T["c_L0"], np.where(m == 0, T["c_S0"], 0.0))
+    ab = ig.Absorb(D_L=fi.D_FAST_SI, D_S=fi.D_SLOW_SI, dh=T["dh"], dt=T["dt"], k=0.05, c_S_eq=1.0, c_L_eq=1e-5,
+                   V_far=2e4, R=3)
+    runs = {mode: ig.run(m, c0, T["c_L0"], ab, 20, mode) for mode in ("fp64", "fp32", "mixed", "fp16")}
+    return m, c0, ab, runs
+
+
+def _gpu(fd, m, c0, ab, weights, mode, steps=20):
+    import torch
+
+    nz, ny, nx = m.shape
+    p = fd.Params(nx=nx, ny=ny, nz=nz, dh=ab.dh, D_fast=ab.D_L, D_slow=0.0, dt=ab.dt, radius=ab.R, weights=weights,
+                  v_far=ab.V_far, flags=fd.F_NO_MASS_FIX if mode != "default" else 0)
+    ctx = fd.build_kernels(p, m)
+    try:
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        M0 = fd.far_init(ctx, c, fi.TABLE1["c_L0"])
+        fd.set_precision_mode(ctx, mode)
+        kin = fd.absorb_run(ctx, c, steps, ab.D_S, ab.k, ab.c_S_eq, ab.c_L_eq)
+        return c.cpu().numpy().astype(np.float64), kin, M0
+    finally:
+        fd.destroy(ctx)
+
+
+def test_absorb_loop_vs_oracle(fd, desk):
+    """Default product path (fp32 weights): field, kinetics (Q_S, c̄_S, c_far) and the Eq.7
+    balance vs the oracle's fp64 loop."""
+    m, c0, ab, runs = desk
+    got, kin, M0 = _gpu(fd, m, c0, ab, "fp32", "default")
+    ref, refcf, refkin = runs["fp64"]
+    nf = m != 2
+    assert rel_l2(got[nf], ref[nf]) <= 1e-5
+    rk = np.array(refkin)
+    np.testing.assert_allclose(kin[:, 0], rk[:, 0], rtol=1e-5)           # Q_S(t)
+    np.testing.assert_allclose(kin[:, 3], rk[:, 3], rtol=1e-5)           # c̄_S(t)
+    np.testing.assert_allclose(kin[:, 2], rk[:, 2], rtol=1e-5)           # c_far(t)
+    assert np.all(np.diff(kin[:, 0]) >= -1e-9 * kin[0, 0])               # absorption only
+    tot = got[nf].sum() + kin[-1, 2] * ab.V_far
+    assert abs(tot - M0) / M0 <= 1e-6
+
+
+def test_precision_modes_vs_oracle(fd, desk):
+    """The paper's FP32 / mixed FP32-FP16 / FP16 modes on the GPU track the oracle's
+    emulation of the same modes, and keep the §4.2 ordering of the error in c̄_S vs FP64."""
+    m, c0, ab, runs = desk
+    ref = np.array([k[3] for k in runs["fp64"][2]])
+    re = {}
+    for mode, w in (("fp32", "fp32"), ("mixed", "fp16"), ("fp16", "fp16")):
+        _, kin, _ = _gpu(fd, m, c0, ab, w, mode)
+        emu = np.array([k[3] for k in runs[mode][2]])
+        re[mode] = np.max(np.abs(kin[:, 3] - ref) / ref)
+        tol = {"fp32": 1e-5, "mixed": 5e-4, "fp16": 5e-3}[mode]
+        assert np.max(np.abs(kin[:, 3] - emu) / emu) <= tol, mode
+    assert re["fp32"] < re["mixed"] < re["fp16"]

@@ -501,6 +501,37 @@ static cudaError_t superpose_uniform(fdirw_ctx* c, const float* src, float* out,
     return launch_superpose_uniform(u, g.R, s);
 }
 
+// N4: the compacted dense tiles and the uniform blocks in one mixed launch.
+static cudaError_t superpose_n4_mixed(fdirw_ctx* c, const float* src, float* out, long ps, long rs, cudaStream_t s)
+{
+    const Geometry& g = c->g;
+    SuperArgs a{};
+    a.cpad = src;
+    a.Wt = c->Wt;
+    a.diag = c->diag;
+    a.out = out;
+    a.out_ps = ps;
+    a.out_rs = rs;
+    a.nx = g.nx; a.ny = g.ny; a.nxq = g.nxq; a.tile = g.tile; a.tpp = g.tpp; a.K = g.K;
+    a.nxp = g.nxp; a.nyp = g.nyp;
+    a.t_begin = 0;
+    a.t_end = c->ut.nd_tiles;
+    a.list = c->ut.dense_list;
+    a.n_list = c->ut.n_dense;
+    UniArgs u{};
+    u.cpad = src;
+    u.out = out;
+    u.out_ps = ps;
+    u.out_rs = rs;
+    u.nx = g.nx; u.ny = g.ny; u.nxq = g.nxq; u.tile = g.tile; u.tpp = g.tpp; u.nxp = g.nxp; u.nyp = g.nyp;
+    u.list = c->ut.list;
+    u.blocks = c->ut.blocks;
+    u.n_blocks = c->ut.n_blocks;
+    u.ukf = c->ut.ukf;
+    u.udiag = c->ut.udiag;
+    return launch_superpose_mixed(a, u, g.R, c->fmt, s);
+}
+
 // N2: p_BC(x) = 1 − Σ_s W̃_s(x−s) (reading A26) = 1 − (stored operator applied to the
 // indicator of the non-far voxels); computed once after kgen with the superposition itself.
 static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s)
@@ -559,7 +590,11 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
         return FDIRW_OK;
     }
     if (c->world == 1) {
-        if (c->ut.chunk_u) {  // N4: dense (HBM-bound) and uniform (FMA-bound) chunks run concurrently
+        if (c->ut.chunk_u && g.tile == 256) {  // N4: one launch mixing dense and uniform blocks
+            CUDA_TRY(superpose_n4_mixed(c, src, out, ps, rs, s));
+            return FDIRW_OK;
+        }
+        if (c->ut.chunk_u) {  // N4 (small tiles): dense and uniform kernels on two streams
             CUDA_TRY(cudaEventRecord(c->ev_fork, s));
             CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
             CUDA_TRY(superpose_uniform(c, src, out, ps, rs, c->comm_stream));

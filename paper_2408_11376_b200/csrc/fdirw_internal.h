@@ -132,6 +132,7 @@ struct UniArgs {
     const float* udiag;   // [u] fp32 diagonal
 };
 cudaError_t launch_superpose_uniform(const UniArgs& a, int R, cudaStream_t s);
+cudaError_t launch_superpose_mixed(const SuperArgs& a, const UniArgs& u, int R, int fmt, cudaStream_t s);
 
 struct UniformTables {
     int* chunk_u = nullptr;   // [n_tiles·tile] class u or −1

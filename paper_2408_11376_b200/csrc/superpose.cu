@@ -173,11 +173,10 @@ __device__ __forceinline__ void do_row_u(const float* srow, const float* ws, flo
 // values decoded from the storage format) is staged once in shared memory.  No weight bytes
 // come from HBM: the chunk's cost is FMAs + L1-resident C reads.
 template <int R>
-__global__ void __launch_bounds__(256) superpose_uniform_kernel(const UniArgs a)
+__device__ __forceinline__ void uniform_body(const UniArgs& a, int blk, float* ws)
 {
     constexpr int L = 2 * R + 1, K = L * L * L;
-    __shared__ float ws[K - 1];
-    const int4 b = a.blocks[blockIdx.x];  // {start, count, u, -}
+    const int4 b = a.blocks[blk];  // {start, count, u, -}
     for (int i = threadIdx.x; i < K - 1; i += blockDim.x) ws[i] = a.ukf[(size_t)b.z * (K - 1) + i];
     __syncthreads();
     if ((int)threadIdx.x >= b.y) return;
@@ -220,6 +219,13 @@ __global__ void __launch_bounds__(256) superpose_uniform_kernel(const UniArgs a)
 }
 
 template <int R>
+__global__ void __launch_bounds__(256) superpose_uniform_kernel(const UniArgs a)
+{
+    __shared__ float ws[(2 * R + 1) * (2 * R + 1) * (2 * R + 1) - 1];
+    uniform_body<R>(a, blockIdx.x, ws);
+}
+
+template <int R>
 static cudaError_t launch_uniform_r(const UniArgs& a, cudaStream_t s)
 {
     if (a.n_blocks <= 0) return cudaSuccess;
@@ -257,10 +263,10 @@ __device__ __forceinline__ double tile_block_sum(double s)
 }
 
 template <int R, typename WT>
-__global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
+__device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
 {
     constexpr int L = 2 * R + 1, K = L * L * L;
-    const int tile = a.t_begin + blockIdx.x;  // weight tile (compact tile when a.list, N4)
+    const int tile = a.t_begin + blk;  // weight tile (compact tile when a.list, N4)
     const int e = threadIdx.x;
     int zl, q;
     bool real;
@@ -344,6 +350,25 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
     }
 }
 
+template <int R, typename WT>
+__global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
+{
+    dense_body<R, WT>(a, blockIdx.x);
+}
+
+// N4: ONE launch mixing the HBM-bound dense tiles and the FMA-bound uniform blocks, the U
+// uniform blocks spread evenly over the grid (block b is uniform iff ⌊(b+1)U/T⌋ > ⌊bU/T⌋),
+// so every SM streams weights and runs uniform FMAs at the same time.
+template <int R, typename WT>
+__global__ void __launch_bounds__(256) superpose_mixed_kernel(const SuperArgs a, const UniArgs u)
+{
+    __shared__ float ws[(2 * R + 1) * (2 * R + 1) * (2 * R + 1) - 1];
+    const long T = gridDim.x, U = u.n_blocks, b = blockIdx.x;
+    const long u0 = b * U / T, u1 = (b + 1) * U / T;
+    if (u1 > u0) uniform_body<R>(u, (int)u0, ws);
+    else dense_body<R, WT>(a, (int)(b - u0));
+}
+
 template <int R>
 static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t s)
 {
@@ -353,6 +378,33 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
     else if (fmt == 1) superpose_kernel<R, __half><<<nblk, a.tile, 0, s>>>(a);
     else superpose_kernel<R, __nv_bfloat16><<<nblk, a.tile, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_mixed_r(const SuperArgs& a, const UniArgs& u, int fmt, cudaStream_t s)
+{
+    const int nblk = (a.t_end - a.t_begin) + u.n_blocks;
+    if (nblk <= 0) return cudaSuccess;
+    if (a.tile != 256) return cudaErrorInvalidValue;  // uniform blocks are 256 chunks
+    if (fmt == 0) superpose_mixed_kernel<R, float><<<nblk, 256, 0, s>>>(a, u);
+    else if (fmt == 1) superpose_mixed_kernel<R, __half><<<nblk, 256, 0, s>>>(a, u);
+    else superpose_mixed_kernel<R, __nv_bfloat16><<<nblk, 256, 0, s>>>(a, u);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_superpose_mixed(const SuperArgs& a, const UniArgs& u, int R, int fmt, cudaStream_t s)
+{
+    switch (R) {
+        case 1: return launch_mixed_r<1>(a, u, fmt, s);
+        case 2: return launch_mixed_r<2>(a, u, fmt, s);
+        case 3: return launch_mixed_r<3>(a, u, fmt, s);
+        case 4: return launch_mixed_r<4>(a, u, fmt, s);
+        case 5: return launch_mixed_r<5>(a, u, fmt, s);
+        case 6: return launch_mixed_r<6>(a, u, fmt, s);
+        case 7: return launch_mixed_r<7>(a, u, fmt, s);
+        case 8: return launch_mixed_r<8>(a, u, fmt, s);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s)

@@ -194,6 +194,37 @@ def _workload_name(cfg):
         cfg.weights, cfg.n_fd or "derived")
 
 
+def _variant_n4(fd, torch, params, mask, c_host, args, stream, peak):
+    """NEXT row N4 measured in the same run: FDIRW_F_DEDUP_STORAGE (bitwise the same field)."""
+    import dataclasses
+
+    p = dataclasses.replace(params, flags=params.flags | fd.F_DEDUP_STORAGE)
+    ctx = fd.build_kernels(p, mask, stream=stream)
+    try:
+        info = ctx.info
+        c = c_host.to("cuda", non_blocking=True)
+        fd.run(ctx, c, args.warmup)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        fd.run(ctx, c, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / args.steps
+    finally:
+        fd.destroy(ctx)
+    N = int((mask != 2).sum())
+    f_u = info["uniform_chunks"] / max(info["chunks"], 1)
+    b_w = 4 if p.weights == "fp32" else 2
+    bpv = (1.0 - f_u) * (info["K"] - 1) * b_w + 12
+    ach = bpv * N / (ms * 1e-3) / 1e9
+    return {"value": N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "uniform_fraction": f_u,
+            "uniform_classes": info["uniform_classes"], "bytes_per_voxel_update": bpv,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak},
+            "weight_bytes": info["weight_bytes"],
+            "note": "uniform chunks read a shared class kernel (smem) instead of streaming; bitwise = dense"}
+
+
 def run_coarse(args):
     """NEXT row N1: the paper's coarse-mesh FDiRW step on the near-field liquid
     of the config's particle (r_p + 5Δh), b = 5, 1 GPU.  Metric: fine Ω_L
@@ -250,6 +281,7 @@ def main():
     ap.add_argument("--weights", default=None)
     ap.add_argument("--impl", default="fdirw", choices=["fdirw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the N4 variant measurement")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--mode", default="fine", choices=["fine", "coarse"],
                     help="fine: the north_star windowed step (default); coarse: NEXT row N1")
@@ -407,9 +439,11 @@ def main():
     if tr:
         line["roofline"]["traffic"] = tr[0]
         line["roofline"]["traffic_source"] = tr[1] + " (ncu --set full, one launch)"
+    fd.destroy(ctx)
+    if world == 1 and not dedup_storage and not far and not args.no_variants:
+        line["variants"] = {"N4_dedup_storage": _variant_n4(fd, torch, params, mask, c_host, args, stream, peak)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, mask)
-    fd.destroy(ctx)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -31,7 +31,7 @@ from . import Problem, fd_whole_grid, round_fmt
 
 def groups(region: np.ndarray, b: int = 5):
     """group_of[z, y, x] ∈ {−1, 0..N−1} and N_I (group sizes)."""
-    region = np.asarray(region).astype(bool)
+    region = np.asarray(region) == 1  # 2 = far-field reservoir (N2), not grouped
     nz, ny, nx = region.shape
     bz, by, bx = -(-nz // b), -(-ny // b), -(-nx // b)
     z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
@@ -61,7 +61,8 @@ def remap_coarse_to_fine(C: np.ndarray, g: np.ndarray, c: np.ndarray) -> np.ndar
 
 def region_problem(pb: Problem, region: np.ndarray) -> Problem:
     """FD over Ω_L only: Ω_L voxels are the fast phase, everything else impermeable
-    (D_slow = 0 ⇒ harmonic-mean faces into it vanish, reading A23)."""
+    (D_slow = 0 ⇒ harmonic-mean faces into it vanish, reading A23); region value 2 marks the
+    far-field reservoir, held at c_far by oracle.fd_whole_grid (N2)."""
     return Problem(mask=np.asarray(region, np.uint8), dh=pb.dh, D_fast=pb.D_fast, D_slow=0.0, dt=pb.dt, R=1,
                    n_fd=pb.n_fd if pb.n_fd else 0)
 
@@ -81,8 +82,20 @@ def build_P(pb: Problem, region: np.ndarray, b: int = 5, n_fd: int | None = None
     return P, g, sizes
 
 
+def build_PBC(pb: Problem, region: np.ndarray, b: int = 5, n_fd: int | None = None) -> np.ndarray:
+    """N2 on the coarse mesh: P_BC (Eq.10) = map of the FD over Ω_L from c = 0 with the far
+    field held at 1."""
+    import oracle
+
+    g, sizes = groups(region, b)
+    n = oracle.derive(pb).n_fd if n_fd is None else n_fd
+    return map_fine_to_coarse(fd_whole_grid(region_problem(pb, region), np.zeros(region.shape), n, c_far=1.0),
+                              g, sizes)
+
+
 def quantize_P(P: np.ndarray, sizes: np.ndarray, fmt: str) -> np.ndarray:
-    """Off-diagonal RNE_fmt(RNE_fp32(P_IJ)); fp32 diagonal with Σ_I N_I P̃_IJ = N_J."""
+    """Off-diagonal RNE_fmt(RNE_fp32(P_IJ)); fp32 diagonal keeping each column's mass
+    M_J = Σ_I N_I P_IJ (= N_J in a closed domain; less with a far field, N2)."""
     N = P.shape[0]
     Q = np.empty_like(P)
     for I in range(N):
@@ -90,8 +103,9 @@ def quantize_P(P: np.ndarray, sizes: np.ndarray, fmt: str) -> np.ndarray:
             Q[I, J] = round_fmt(P[I, J], fmt) if I != J else 0.0
     s = sizes.astype(np.float64)
     for J in range(N):
+        M = float(np.dot(s, P[:, J]))
         off = float(np.dot(s, Q[:, J]))  # Σ_{I≠J} N_I P̃_IJ (diagonal entry is 0 here)
-        Q[J, J] = float(np.float32((s[J] - off) / s[J]))
+        Q[J, J] = float(np.float32((M - off) / s[J]))
     return Q
 
 
@@ -99,6 +113,12 @@ def step(P: np.ndarray, g: np.ndarray, sizes: np.ndarray, c: np.ndarray) -> np.n
     """One coarse FDiRW step, Eqs.13-15."""
     C = map_fine_to_coarse(c, g, sizes)
     return remap_coarse_to_fine(P @ C, g, c)
+
+
+def step_far(P: np.ndarray, PBC: np.ndarray, g: np.ndarray, sizes: np.ndarray, c: np.ndarray, c_far: float):
+    """Eq.14 with the boundary term: C' = P·C + P_BC·c_far, then Eq.15."""
+    C = map_fine_to_coarse(c, g, sizes)
+    return remap_coarse_to_fine(P @ C + PBC * c_far, g, c)
 
 
 def flop_count(N: int, N_L: int) -> int:

@@ -130,3 +130,31 @@ def test_near_field_region():
     n_l = int(fi.near_field(mask, 50).sum())
     n_s = int((mask == 0).sum())
     assert abs(n_l - t3["N_L"]) / t3["N_L"] < 0.05 and abs(n_s - t3["N_S"]) / t3["N_S"] < 0.05
+
+
+def test_coarse_far_field(co, oracle_lib):
+    """N1 + N2 (Eq.10 with P_BC): the row-sum identity Σ_J P_IJ + P_BC_I = 1 (SPEC S:318,
+    S:330), a uniform field with c_far equal to it is stationary, and b = 1 reproduces the
+    held-Dirichlet fine FD exactly (linearity in (c, c_far))."""
+    mask = fi.porous_particle((14, 15, 13), 4, pore_r=(1, 1.5), n_pores=2, seed=3)
+    region = fi.with_far_field(mask, 4, 2.0)            # 1 near liquid, 2 far, 0 solid
+    region = np.where(region == 0, 0, region).astype(np.uint8)
+    pb = lat(mask, 40)
+    P, g, s = co.build_P(pb, region, b=3)
+    PBC = co.build_PBC(pb, region, b=3)
+    np.testing.assert_allclose(P.sum(1) + PBC, 1.0, atol=1e-12)
+    assert PBC.max() > 1e-3 and PBC.min() >= 0
+    c = np.where(region == 1, 0.6, 0.0)
+    np.testing.assert_allclose(co.step_far(P, PBC, g, s, c, 0.6)[region == 1], 0.6, rtol=1e-12)
+    Q = co.quantize_P(P, s, "bf16")
+    np.testing.assert_allclose(s @ Q, s @ P, rtol=2e-7)   # column masses kept (A10 generalised)
+    # b = 1: P·c + P_BC·c_far == fine FD with the far field held at c_far
+    reg = np.zeros((5, 4, 6), np.uint8)
+    reg[1:4, 1:3, 1:5] = 1
+    reg[0] = 2
+    P1, g1, s1 = co.build_P(lat(np.ones_like(reg), 25), reg, b=1)
+    B1 = co.build_PBC(lat(np.ones_like(reg), 25), reg, b=1)
+    c1 = np.where(reg == 1, np.random.default_rng(0).random(reg.shape), 0.0)
+    got = co.step_far(P1, B1, g1, s1, c1, 0.3)
+    ref = oracle_lib.fd_whole_grid(co.region_problem(lat(np.ones_like(reg), 25), reg), c1, 25, c_far=0.3)
+    np.testing.assert_allclose(got[reg == 1], ref[reg == 1], rtol=1e-12)

@@ -236,16 +236,18 @@ def run_coarse(args):
     cfg = fi.config(args.config, weights=args.weights)
     mask = cfg.mask()
     r_p = cfg.geometry.get("r_p", 50)
-    region = fi.near_field(mask, r_p)
+    far = cfg.v_far > 0  # N2: the config's mask already labels the far-field reservoir 2
+    region = mask.astype(np.uint8) if far else fi.near_field(mask, r_p)
     nz, ny, nx = cfg.shape
     params = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt,
-                       radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights)
+                       radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights, v_far=cfg.v_far)
     torch.cuda.synchronize()
     t = time.perf_counter()
     ctx = fd.coarse_build(params, region, block=args.block)
     t_build = time.perf_counter() - t
     info = ctx.info
     c = torch.from_numpy(fi.initial_c(mask, "paper")).cuda()
+    K0 = fd.coarse_far_init(ctx, c, cfg.c_far0) if far else None
     fd.coarse_run(ctx, c, args.warmup)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -257,17 +259,24 @@ def run_coarse(args):
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     NL, N = info["n_region"], info["n_groups"]
+    extra = {}
+    if far:  # Eq.7 balance over Ω_L + reservoir after all steps
+        cf = fd.coarse_far_get(ctx)
+        m = float(c.double()[torch.from_numpy(region == 1).cuda()].sum())
+        extra = {"c_far": cf, "mass_rel_err": abs(m + cf * cfg.v_far - K0) / K0}
     line = {"metric": "voxel-updates/s (coarse-mesh FDiRW step, NEXT row N1)", "value": NL / (ms * 1e-3),
             "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": {"fp32": "f32", "fp16": "f16", "bf16": "bf16"}[cfg.weights] + "-P/f32-accum",
             "data": "synthetic",
-            "config": {"workload": "N1 coarse mesh on the %s near-field liquid (r_p+5), b=%d" % (cfg.name, args.block),
+            "config": {"workload": "N1%s coarse mesh on the %s near-field liquid (r_p+5), b=%d"
+                                   % ("+N2 far field" if far else "", cfg.name, args.block),
                        "N_L": NL, "N": N, "P_bytes": info["p_bytes"], "n_fd": info["n_fd"]},
             "paper_context": {"R50_N_L": 329404, "R50_N": 2515, "V100_fdirw_s_per_1000_steps": 0.7,
                               "source": "P:181 Fig.7e, P:262-263 Table 3"},
             "flops_per_step": info["flops_per_step"],
-            "build_seconds": t_build, "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+            "build_seconds": t_build, "gpu_launches": (4 if far else 3) * args.steps, "clocks": clk.summary(),
+            **extra}
     fd.coarse_destroy(ctx)
     print(json.dumps(line), flush=True)
 

@@ -252,18 +252,26 @@ fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, const float* 
 
 /* ---- NEXT row N1: coarse-mesh FDiRW (§3.1, Eqs.10-15) ------------------
  * The paper's own step on a coarse mesh, for the fast phase only (§3 "FDiRW solver
- * for fast diffusion in near-field liquid"), closed domain (no P_BC, reading A3):
- *   region   Ω_L = voxels with region_host[v] != 0 (e.g. near-field liquid)
+ * for fast diffusion in near-field liquid"), with the far-field term of NEXT row N2
+ * when params->v_far > 0 (Eq.10 P_BC, Eq.7):
+ *   region   Ω_L = voxels with region_host[v] == 1 (e.g. near-field liquid);
+ *            region_host[v] == 2 marks far-field reservoir voxels (needs v_far > 0);
+ *            any other value is outside (no flux)
  *   groups   Ω_L ∩ b×b×b blocks anchored at the origin, empty blocks dropped,
  *            numbered in block order (N = N_L/125 ⇔ b = 5)
  *   P        dense N×N; column J = group means (Eq.13) of an explicit FD run over Ω_L
  *            (faces leaving Ω_L carry no flux, face number λ = Δt_fd·D_fast/Δh²) from
  *            the group-uniform source 1 on group J, n_fd substeps; stored in
  *            params->weights format, off-diagonal RNE, fp32 diagonal fixed so that
- *            Σ_I N_I P̃_IJ = N_J (column mass; coarse analogue of reading A10)
+ *            Σ_I N_I P̃_IJ = M_J = Σ_I N_I P_IJ (fp64 column mass; = N_J in a closed
+ *            domain; coarse analogue of reading A10).  Faces from Ω_L into far-field
+ *            voxels are Dirichlet (value 0 for the P columns).
+ *   P_BC     (v_far > 0) group means of the same FD from c = 0 with the far field held
+ *            at 1 (Eq.10), fp32 [N]
  *   step     C_I = Σ_{i∈I} c_i / N_I in fp32 (Eq.13, "mapping ... in FP32");
- *            C'_I = Σ_J P̃_IJ C_J, fp32 accumulation (Eq.14);  c'_i = C'_I (Eq.15);
- *            voxels outside Ω_L are copied unchanged.
+ *            C'_I = Σ_J P̃_IJ C_J (+ P_BC_I·c_far), fp32 accumulation (Eq.14);
+ *            c'_i = C'_I (Eq.15); voxels outside Ω_L are copied unchanged; then (v_far > 0)
+ *            Eq.7 on the device: c_far = (K0 − Σ_I N_I C'_I)/v_far, fp64.
  * params: nx, ny, nz, dh, D_fast, dt, n_fd, weights as for the fine path (D_slow,
  * radius and flags are ignored).  Single GPU.  Buffers are device fp32 [nz][ny][nx].
  */
@@ -291,6 +299,16 @@ fdirw_status fdirw_coarse_query(const fdirw_coarse* ctx, fdirw_coarse_info* info
 /* Host copies: P_host [N][N] fp64 decoded (diagonal = fp32 fix-up) if non-NULL;
  * group_of_host [nz][ny][nx] int32 (−1 outside Ω_L) if non-NULL.  Synchronous. */
 fdirw_status fdirw_coarse_export(const fdirw_coarse* ctx, double* P_host, int32_t* group_of_host);
+/* N2: starts the far-field bookkeeping (Eq.7) from the field c_dev and c_far(t0) = c_far0:
+ * K0 = Σ_I N_I C_I(t0) + c_far0·v_far (C = fp32 mapping of c_dev, summed in fp64) is
+ * written to *M_out if non-NULL.  Must be called before the first step of a far-field
+ * context (c_far is 0 otherwise).  FDIRW_E_STATE if v_far == 0.  Synchronous. */
+fdirw_status fdirw_coarse_far_init(fdirw_coarse* ctx, const float* c_dev, double c_far0, double* M_out,
+                                   void* cuda_stream);
+/* Current c_far (after the last enqueued step).  Synchronous on cuda_stream. */
+fdirw_status fdirw_coarse_far_get(fdirw_coarse* ctx, double* c_far_out, void* cuda_stream);
+/* P_BC as stored (fp32 decoded to fp64) into pbc_host [N].  FDIRW_E_STATE if v_far == 0. */
+fdirw_status fdirw_coarse_export_pbc(const fdirw_coarse* ctx, double* pbc_host);
 void fdirw_coarse_destroy(fdirw_coarse* ctx);
 
 #ifdef __cplusplus

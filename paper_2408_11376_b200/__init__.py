@@ -38,7 +38,8 @@ EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fd
            "fdirw_export_kernels", "fdirw_step_virtual", "fdirw_coarse_build", "fdirw_coarse_step",
            "fdirw_coarse_run", "fdirw_coarse_query", "fdirw_coarse_export", "fdirw_coarse_destroy",
            "fdirw_far_init", "fdirw_far_init_virtual", "fdirw_far_get", "fdirw_absorb_run",
-           "fdirw_set_precision_mode"]
+           "fdirw_set_precision_mode", "fdirw_coarse_far_init", "fdirw_coarse_far_get",
+           "fdirw_coarse_export_pbc"]
 
 
 class fdirw_params(ctypes.Structure):
@@ -116,6 +117,12 @@ _lib.fdirw_coarse_query.argtypes = [_vp, ctypes.POINTER(fdirw_coarse_info)]
 _lib.fdirw_coarse_query.restype = _st
 _lib.fdirw_coarse_export.argtypes = [_vp, _vp, _vp]
 _lib.fdirw_coarse_export.restype = _st
+_lib.fdirw_coarse_far_init.argtypes = [_vp, _vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double), _vp]
+_lib.fdirw_coarse_far_init.restype = _st
+_lib.fdirw_coarse_far_get.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), _vp]
+_lib.fdirw_coarse_far_get.restype = _st
+_lib.fdirw_coarse_export_pbc.argtypes = [_vp, _vp]
+_lib.fdirw_coarse_export_pbc.restype = _st
 _lib.fdirw_coarse_destroy.argtypes = [_vp]
 _lib.fdirw_coarse_destroy.restype = None
 _lib.fdirw_far_init.argtypes = [_vp, _vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double), _vp]
@@ -326,7 +333,7 @@ class Coarse:
 
 
 def coarse_build(params: Params, region: np.ndarray, block: int = 5, stream=None) -> Coarse:
-    """fdirw_coarse_build: region = uint8 [nz][ny][nx] (host), nonzero = Ω_L."""
+    """fdirw_coarse_build: region = uint8 [nz][ny][nx] (host), 1 = Ω_L, 2 = far field (v_far > 0)."""
     region = np.ascontiguousarray(region, dtype=np.uint8)
     if region.shape != (params.nz, params.ny, params.nx):
         raise ValueError("region shape %s != (nz, ny, nx)" % (region.shape,))
@@ -358,6 +365,26 @@ def coarse_export(ctx: Coarse):
     g = np.zeros(ctx.shape, np.int32)
     _check(_lib.fdirw_coarse_export(ctx.handle, P.ctypes.data_as(ctypes.c_void_p), g.ctypes.data_as(ctypes.c_void_p)))
     return P, g
+
+
+def coarse_export_pbc(ctx: Coarse):
+    """P_BC as stored (fp32 → fp64) [N] (N2 far-field contexts only)."""
+    pbc = np.zeros(coarse_query(ctx)["n_groups"], np.float64)
+    _check(_lib.fdirw_coarse_export_pbc(ctx.handle, pbc.ctypes.data_as(ctypes.c_void_p)))
+    return pbc
+
+
+def coarse_far_init(ctx: Coarse, c, c_far0: float, stream=None) -> float:
+    """fdirw_coarse_far_init → K0 = Σ_{Ω_L} c + c_far0·v_far (Eq.7 invariant)."""
+    m = ctypes.c_double(0.0)
+    _check(_lib.fdirw_coarse_far_init(ctx.handle, _dptr(c), float(c_far0), ctypes.byref(m), _stream(stream)))
+    return m.value
+
+
+def coarse_far_get(ctx: Coarse, stream=None) -> float:
+    v = ctypes.c_double(0.0)
+    _check(_lib.fdirw_coarse_far_get(ctx.handle, ctypes.byref(v), _stream(stream)))
+    return v.value
 
 
 def coarse_destroy(ctx: Coarse):

@@ -1,4 +1,5 @@
-// coarse.cu — NEXT row N1: coarse-mesh FDiRW (§3.1, Eqs.10-15) on B200.
+// coarse.cu — NEXT row N1: coarse-mesh FDiRW (§3.1, Eqs.10-15) on B200,
+// with the far-field boundary term of NEXT row N2 (P_BC, Eq.7) when v_far > 0.
 //
 // Build (one-time, "preconditioned" P):
 //   groups      Ω_L ∩ b³ blocks (P:113 N = N_L/125 ⇔ b = 5): used-block flags → scan → ids;
@@ -6,14 +7,19 @@
 //   columns     explicit FD over Ω_L from the group-uniform sources 1_J,
 //               all columns of a chunk at once: X[row][j] with j fastest, so the 7-point
 //               stencil reads whole neighbour rows (coalesced 16-byte loads, neighbour
-//               table read once per row, rows of 3 z-planes of the region stay in L2)
+//               table read once per row, rows of 3 z-planes of the region stay in L2).
+//               Faces into far-field voxels (region value 2) are Dirichlet: 0 for the P
+//               columns, 1 for the extra P_BC column
 //   P           group means of the FD result (Eq.11/13), fp64, then RNE to the storage
-//               format with an fp32 diagonal fixing Σ_I N_I P̃_IJ = N_J
-// Step (the paper's three kernels, §3.2 / Fig.2, fused into a CUDA graph for run):
+//               format with an fp32 diagonal keeping each column's mass Σ_I N_I P_IJ
+// Step (the paper's three kernels, §3.2 / Fig.2, captured in a CUDA graph for run):
 //   map_kernel     one warp per group, fp32 sum over its voxels ("mapping ... FP32")
 //   gemv_kernel    one warp per row I of P̃ (row-major, L2-resident: N² b_w bytes), 128-bit
-//                  loads, fp32 FMA + fixed shuffle tree ("accumulation ... FP32")
+//                  loads, fp32 FMA + fixed shuffle tree ("accumulation ... FP32"),
+//                  + P_BC_I·c_far (Eq.14)
 //   remap_kernel   c'_i = C'_{I(i)} for every Ω_L voxel (Eq.15)
+//   far_kernel     Eq.7: c_far = (K0 − Σ_I N_I C'_I)/V_far (voxels outside Ω_L are not
+//                  touched by the coarse step, so their mass is a constant folded into K0)
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_bf16.h>
@@ -21,6 +27,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -45,6 +52,11 @@ struct fdirw_coarse {
     cudaStream_t cap = nullptr;
     cudaGraphExec_t graph = nullptr;
     float* graph_c = nullptr;
+    // N2
+    bool far = false;
+    double v_far = 0;
+    float* Pbc = nullptr;        // [N] fp32
+    double* far_state = nullptr; // {c_far, K0}
 };
 
 namespace fdirw {
@@ -72,11 +84,12 @@ static unsigned gridn(long n, int t = 256)
 
 #define GRID_STRIDE(i, n) for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (n); i += (long)gridDim.x * blockDim.x)
 
+// region codes: 1 = Ω_L, 2 = far-field reservoir (N2), anything else = outside
 __global__ void k_mark_blocks(const uint8_t* reg, long nvox, int nx, int ny, int b, int bx, int by, int* used)
 {
     GRID_STRIDE(v, nvox)
     {
-        if (!reg[v]) continue;
+        if (reg[v] != 1) continue;
         const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((long)nx * ny));
         used[((z / b) * by + (y / b)) * bx + (x / b)] = 1;
     }
@@ -88,7 +101,7 @@ __global__ void k_group_of(const uint8_t* reg, long nvox, int nx, int ny, int b,
     GRID_STRIDE(v, nvox)
     {
         int g = -1;
-        if (reg[v]) {
+        if (reg[v] == 1) {
             const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((long)nx * ny));
             g = bid[((z / b) * by + (y / b)) * bx + (x / b)];
             atomicAdd(&sizes[g], 1);
@@ -114,20 +127,24 @@ __global__ void k_rows(const int* row_flag, const int* row_pos, long nvox, int* 
     }
 }
 
-// neighbour rows in the order −x, +x, −y, +y, −z, +z (−1: no flux)
-__global__ void k_neighbours(const int* rows, long NL, const int* row_of, int nx, int ny, int nz, int* nb)
+// neighbour rows in the order −x, +x, −y, +y, −z, +z: a row index, −2 = far-field (Dirichlet),
+// −1 = no flux
+__global__ void k_neighbours(const int* rows, long NL, const int* row_of, const uint8_t* reg, int nx, int ny, int nz,
+                             int* nb)
 {
     GRID_STRIDE(r, NL)
     {
         const int v = rows[r];
         const int x = v % nx, y = (v / nx) % ny, z = v / (nx * ny);
         const long pl = (long)nx * ny;
-        nb[r * 6 + 0] = x > 0 ? row_of[v - 1] : -1;
-        nb[r * 6 + 1] = x < nx - 1 ? row_of[v + 1] : -1;
-        nb[r * 6 + 2] = y > 0 ? row_of[v - nx] : -1;
-        nb[r * 6 + 3] = y < ny - 1 ? row_of[v + nx] : -1;
-        nb[r * 6 + 4] = z > 0 ? row_of[v - pl] : -1;
-        nb[r * 6 + 5] = z < nz - 1 ? row_of[v + pl] : -1;
+        const long q[6] = {x > 0 ? v - 1 : -1L, x < nx - 1 ? v + 1 : -1L, y > 0 ? v - nx : -1L,
+                           y < ny - 1 ? v + nx : -1L, z > 0 ? v - pl : -1L, z < nz - 1 ? v + pl : -1L};
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            int code = -1;
+            if (q[f] >= 0) code = row_of[q[f]] >= 0 ? row_of[q[f]] : (reg[q[f]] == 2 ? -2 : -1);
+            nb[r * 6 + f] = code;
+        }
     }
 }
 
@@ -137,13 +154,15 @@ __global__ void k_init_cols(const int* row_group, long NL, int CB, int J0, float
     {
         const long r = i / CB;
         const int j = (int)(i % CB);
-        X[i] = row_group[r] == J0 + j ? 1.f : 0.f;
+        X[i] = row_group[r] == J0 + j ? 1.f : 0.f;  // column N (P_BC) has no group: starts at 0
     }
 }
 
 // One FD substep for CB columns at once: one warp per row, lanes over float4 column quads.
+// A far-field face adds λ·(b_j − c) with b_j = 1 for the P_BC column (global index Nbc), else 0.
 __global__ void __launch_bounds__(256) k_fd_cols(const float* __restrict__ X, float* __restrict__ Y,
-                                                 const int* __restrict__ nb, long NL, int CB, float lam)
+                                                 const int* __restrict__ nb, long NL, int CB, float lam, int J0,
+                                                 int Nbc)
 {
     const int lane = threadIdx.x & 31;
     const long warps = (long)gridDim.x * (blockDim.x >> 5);
@@ -157,10 +176,13 @@ __global__ void __launch_bounds__(256) k_fd_cols(const float* __restrict__ X, fl
         for (int q = lane; q < q4; q += 32) {
             const float4 c = xr[q];
             float4 a = c;
+            const int j0 = J0 + 4 * q;
+            const float4 bv = make_float4(j0 == Nbc ? 1.f : 0.f, j0 + 1 == Nbc ? 1.f : 0.f, j0 + 2 == Nbc ? 1.f : 0.f,
+                                          j0 + 3 == Nbc ? 1.f : 0.f);
 #pragma unroll
             for (int f = 0; f < 6; ++f) {
-                if (n[f] < 0) continue;
-                const float4 m = reinterpret_cast<const float4*>(X + (long)n[f] * CB)[q];
+                if (n[f] == -1) continue;
+                const float4 m = n[f] >= 0 ? reinterpret_cast<const float4*>(X + (long)n[f] * CB)[q] : bv;
                 a.x = fmaf(lam, m.x - c.x, a.x);
                 a.y = fmaf(lam, m.y - c.y, a.y);
                 a.z = fmaf(lam, m.z - c.z, a.z);
@@ -171,9 +193,9 @@ __global__ void __launch_bounds__(256) k_fd_cols(const float* __restrict__ X, fl
     }
 }
 
-// P64[I][J0 + j] = Σ_{v∈I} X[row(v)][j] / N_I (fp64, CSR order)
-__global__ void k_map_cols(const float* X, const int* grp_ptr, const int* grp_vox, const int* row_of, long N, int CB,
-                           int J0, int Jn, double* P64)
+// P64[I][J0 + j] = Σ_{v∈I} X[row(v)][j] / N_I (fp64, CSR order); stride Ncol
+__global__ void k_map_cols(const float* X, const int* grp_ptr, const int* grp_vox, const int* row_of, long N,
+                           long Ncol, int CB, int J0, int Jn, double* P64)
 {
     GRID_STRIDE(i, N * (long)Jn)
     {
@@ -181,7 +203,7 @@ __global__ void k_map_cols(const float* X, const int* grp_ptr, const int* grp_vo
         const int j = (int)(i % Jn);
         double s = 0.0;
         for (int k = grp_ptr[I]; k < grp_ptr[I + 1]; ++k) s += (double)X[(long)row_of[grp_vox[k]] * CB + j];
-        P64[I * N + J0 + j] = s / (double)(grp_ptr[I + 1] - grp_ptr[I]);
+        P64[I * Ncol + J0 + j] = s / (double)(grp_ptr[I + 1] - grp_ptr[I]);
     }
 }
 
@@ -197,29 +219,39 @@ __device__ __forceinline__ float dec(float v) { return v; }
 __device__ __forceinline__ float dec(__half v) { return __half2float(v); }
 __device__ __forceinline__ float dec(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// one block per column J: quantise off-diagonal entries, fp64 column mass, fp32 diagonal
+// one block per column J: quantise off-diagonal entries; the fp32 diagonal keeps the column's
+// fp64 mass M_J = Σ_I N_I P_IJ (N_J when closed)
 template <typename WT>
-__global__ void k_quantize(const double* P64, const int* sizes, long N, WT* P, float* Pdiag)
+__global__ void k_quantize(const double* P64, long Ncol, const int* sizes, long N, WT* P, float* Pdiag)
 {
-    __shared__ double red[32];
+    __shared__ double red[32], redm[32];
     const long J = blockIdx.x;
-    double s = 0.0;
+    double s = 0.0, m = 0.0;
     for (long I = threadIdx.x; I < N; I += blockDim.x) {
-        WT q = enc<WT>((float)P64[I * N + J]);
+        const double pv = P64[I * Ncol + J];
+        WT q = enc<WT>((float)pv);
         if (I == J) q = enc<WT>(0.f);
         P[I * N + J] = q;
         s += (double)sizes[I] * (double)dec(q);
+        m += (double)sizes[I] * pv;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        m += __shfl_xor_sync(0xffffffffu, m, o);
+    }
+    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = s; redm[threadIdx.x >> 5] = m; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-        const double nj = (double)sizes[J];
-        Pdiag[J] = (float)((nj - t) / nj);
+        double t = 0.0, tm = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += red[w]; tm += redm[w]; }
+        Pdiag[J] = (float)((tm - t) / (double)sizes[J]);
     }
+}
+
+__global__ void k_pbc(const double* P64, long Ncol, long N, float* Pbc)
+{
+    GRID_STRIDE(I, N) Pbc[I] = (float)P64[I * Ncol + N];
 }
 
 // ---- step kernels -------------------------------------------------------------------
@@ -240,7 +272,8 @@ __global__ void k_map(const float* __restrict__ c, const int* __restrict__ grp_p
 
 template <typename WT>
 __global__ void __launch_bounds__(256) k_gemv(const WT* __restrict__ P, const float* __restrict__ Pdiag,
-                                              const float* __restrict__ C, long N, float* __restrict__ Cout)
+                                              const float* __restrict__ C, long N, float* __restrict__ Cout,
+                                              const float* __restrict__ Pbc, const double* __restrict__ far_state)
 {
     const int lane = threadIdx.x & 31;
     const long warps = (long)gridDim.x * (blockDim.x >> 5);
@@ -261,7 +294,11 @@ __global__ void __launch_bounds__(256) k_gemv(const WT* __restrict__ P, const fl
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) Cout[I] = fmaf(Pdiag[I], C[I], acc);
+        if (lane == 0) {
+            float v = fmaf(Pdiag[I], C[I], acc);
+            if (Pbc) v = fmaf(Pbc[I], (float)far_state[0], v);  // Eq.14 boundary term
+            Cout[I] = v;
+        }
     }
 }
 
@@ -275,6 +312,24 @@ __global__ void k_remap(const int* __restrict__ rows, long NL, const int* __rest
     }
 }
 
+// Eq.7 on the coarse mesh: one warp, lane-strided groups, fixed shuffle tree
+__global__ void k_far(const float* __restrict__ C, const int* __restrict__ sizes, long N, double* far_state,
+                      double v_far, int init, double c_far0)
+{
+    double s = 0.0;
+    for (long I = threadIdx.x; I < N; I += 32) s += (double)sizes[I] * (double)C[I];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+        if (init) {
+            far_state[1] = s + c_far0 * v_far;  // K0 = Σ_{Ω_L} c(t0) + c_far(t0)·V_far
+            far_state[0] = c_far0;
+        } else {
+            far_state[0] = (far_state[1] - s) / v_far;
+        }
+    }
+}
+
 static void coarse_free(fdirw_coarse* c)
 {
     if (!c) return;
@@ -283,7 +338,7 @@ static void coarse_free(fdirw_coarse* c)
     if (c->graph) cudaGraphExecDestroy(c->graph);
     if (c->cap) cudaStreamDestroy(c->cap);
     cudaFree(c->group_of); cudaFree(c->rows); cudaFree(c->grp_ptr); cudaFree(c->grp_vox); cudaFree(c->sizes);
-    cudaFree(c->P); cudaFree(c->Pdiag); cudaFree(c->C); cudaFree(c->C2);
+    cudaFree(c->P); cudaFree(c->Pdiag); cudaFree(c->C); cudaFree(c->C2); cudaFree(c->Pbc); cudaFree(c->far_state);
     delete c;
 }
 
@@ -296,6 +351,11 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
     if (!(p->dh > 0) || !(p->dt > 0) || !(p->D_fast > 0) || p->n_fd < 0)
         return cfail(FDIRW_E_INVALID, "need dh, dt, D_fast > 0 and n_fd >= 0");
     if (p->weights < 0 || p->weights > 2) return cfail(FDIRW_E_INVALID, "bad weight format");
+    if (!(p->v_far >= 0)) return cfail(FDIRW_E_INVALID, "v_far must be >= 0");
+    const long nvox = (long)p->nx * p->ny * p->nz;
+    bool has_far = false;
+    for (long i = 0; i < nvox && !has_far; ++i) has_far = region_host[i] == 2;
+    if (has_far && !(p->v_far > 0)) return cfail(FDIRW_E_INVALID, "far-field voxels (2) need v_far > 0");
     // a1 for the fast phase (reading A5)
     long n = p->n_fd;
     if (n == 0) {
@@ -314,24 +374,25 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
     c->b = block;
     c->fmt = p->weights;
     c->b_w = c->fmt == FDIRW_W_FP32 ? 4 : 2;
+    c->far = p->v_far > 0;
+    c->v_far = p->v_far;
     cudaGetDevice(&c->device);
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const int nx = p->nx, ny = p->ny, nz = p->nz, b = block;
-    const long nvox = (long)nx * ny * nz;
     c->nvox = nvox;
     const int bx = (nx + b - 1) / b, by = (ny + b - 1) / b, bz = (nz + b - 1) / b;
     const long nblk = (long)bx * by * bz;
 
     uint8_t* reg = nullptr;
     int *used = nullptr, *bid = nullptr, *row_flag = nullptr, *row_pos = nullptr, *row_of = nullptr;
-    int *row_group = nullptr, *row_group2 = nullptr, *nb = nullptr, *tmp_rows = nullptr;
+    int *row_group = nullptr, *row_group2 = nullptr, *nb = nullptr;
     float *X = nullptr, *Y = nullptr;
     double* P64 = nullptr;
     void* tmp = nullptr;
     auto cleanup = [&]() {
         cudaFree(reg); cudaFree(used); cudaFree(bid); cudaFree(row_flag); cudaFree(row_pos); cudaFree(row_of);
-        cudaFree(row_group); cudaFree(row_group2); cudaFree(nb); cudaFree(tmp_rows); cudaFree(X); cudaFree(Y);
-        cudaFree(P64); cudaFree(tmp);
+        cudaFree(row_group); cudaFree(row_group2); cudaFree(nb); cudaFree(X); cudaFree(Y); cudaFree(P64);
+        cudaFree(tmp);
     };
     cudaError_t e = cudaSuccess;
 #define T(call)                                                                     \
@@ -384,7 +445,6 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
     T(cudaMalloc(&row_of, nvox * 4));
     T(cudaMalloc(&row_group, NL * 4));
     T(cudaMalloc(&row_group2, NL * 4));
-    T(cudaMalloc(&tmp_rows, NL * 4));
     k_rows<<<gridn(nvox), 256, 0, s>>>(row_flag, row_pos, nvox, c->rows, row_of, c->group_of, row_group);
     T(cudaGetLastError());
     // group CSR: stable sort of (group, voxel) over the region rows
@@ -402,39 +462,50 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
     T(cudaMemsetAsync(c->grp_ptr, 0, 4, s));
     T(cub::DeviceScan::InclusiveSum(tmp, tb, c->sizes, c->grp_ptr + 1, N, s));
     T(cudaMalloc(&nb, NL * 6 * 4));
-    k_neighbours<<<gridn(NL), 256, 0, s>>>(c->rows, NL, row_of, nx, ny, nz, nb);
+    k_neighbours<<<gridn(NL), 256, 0, s>>>(c->rows, NL, row_of, reg, nx, ny, nz, nb);
     T(cudaGetLastError());
 
-    // P columns: batched FD over Ω_L from group-uniform sources, CB columns per pass
+    // P (and P_BC as column N) by batched FD over Ω_L, CB columns per pass
+    const long Ncol = (long)N + (c->far ? 1 : 0);
     const long budget = 4L << 30;  // bytes for the two FD buffers
     long CB = budget / (2L * 4 * NL);
     CB = CB < 4 ? 4 : (CB / 4) * 4;
-    const long Npad = ((long)N + 3) / 4 * 4;
+    const long Npad = (Ncol + 3) / 4 * 4;
     if (CB > Npad) CB = Npad;
     T(cudaMalloc(&X, NL * CB * 4));
     T(cudaMalloc(&Y, NL * CB * 4));
-    T(cudaMalloc(&P64, (long)N * N * 8));
-    for (long J0 = 0; J0 < N; J0 += CB) {
-        const int Jn = (int)((N - J0) < CB ? (N - J0) : CB);
+    T(cudaMalloc(&P64, (long)N * Ncol * 8));
+    const int Nbc = c->far ? N : -1;
+    for (long J0 = 0; J0 < Ncol; J0 += CB) {
+        const int Jn = (int)((Ncol - J0) < CB ? (Ncol - J0) : CB);
         k_init_cols<<<gridn(NL * CB), 256, 0, s>>>(row_group, NL, (int)CB, (int)J0, X);
         T(cudaGetLastError());
         float *a = X, *bb = Y;
         for (int k = 0; k < c->n_fd; ++k) {
-            k_fd_cols<<<gridn(NL * 32), 256, 0, s>>>(a, bb, nb, NL, (int)CB, (float)lam);
+            k_fd_cols<<<gridn(NL * 32), 256, 0, s>>>(a, bb, nb, NL, (int)CB, (float)lam, (int)J0, Nbc);
             float* t = a; a = bb; bb = t;
         }
         T(cudaGetLastError());
-        k_map_cols<<<gridn((long)N * Jn), 256, 0, s>>>(a, c->grp_ptr, c->grp_vox, row_of, N, (int)CB, (int)J0, Jn, P64);
+        k_map_cols<<<gridn((long)N * Jn), 256, 0, s>>>(a, c->grp_ptr, c->grp_vox, row_of, N, Ncol, (int)CB, (int)J0,
+                                                       Jn, P64);
         T(cudaGetLastError());
     }
     T(cudaMalloc(&c->P, (long)N * N * c->b_w));
     T(cudaMalloc(&c->Pdiag, (long)N * 4));
-    if (c->fmt == 0) k_quantize<float><<<N, 256, 0, s>>>(P64, c->sizes, N, (float*)c->P, c->Pdiag);
-    else if (c->fmt == 1) k_quantize<__half><<<N, 256, 0, s>>>(P64, c->sizes, N, (__half*)c->P, c->Pdiag);
-    else k_quantize<__nv_bfloat16><<<N, 256, 0, s>>>(P64, c->sizes, N, (__nv_bfloat16*)c->P, c->Pdiag);
+    if (c->fmt == 0) k_quantize<float><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, (float*)c->P, c->Pdiag);
+    else if (c->fmt == 1) k_quantize<__half><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, (__half*)c->P, c->Pdiag);
+    else k_quantize<__nv_bfloat16><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, (__nv_bfloat16*)c->P, c->Pdiag);
     T(cudaGetLastError());
-    T(cudaMalloc(&c->C, Npad * 4));
-    T(cudaMalloc(&c->C2, Npad * 4));
+    if (c->far) {
+        T(cudaMalloc(&c->Pbc, (long)N * 4));
+        T(cudaMalloc(&c->far_state, 16));
+        T(cudaMemsetAsync(c->far_state, 0, 16, s));
+        k_pbc<<<gridn(N), 256, 0, s>>>(P64, Ncol, N, c->Pbc);
+        T(cudaGetLastError());
+    }
+    const long Np4 = ((long)N + 3) / 4 * 4;
+    T(cudaMalloc(&c->C, Np4 * 4));
+    T(cudaMalloc(&c->C2, Np4 * 4));
     T(cudaStreamSynchronize(s));
     T(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
 #undef T
@@ -447,10 +518,16 @@ static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
 {
     const long N = c->N;
     k_map<<<gridn(N * 32), 256, 0, s>>>(cbuf, c->grp_ptr, c->grp_vox, N, c->C);
-    if (c->fmt == 0) k_gemv<float><<<gridn(N * 32), 256, 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->C2);
-    else if (c->fmt == 1) k_gemv<__half><<<gridn(N * 32), 256, 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->C2);
-    else k_gemv<__nv_bfloat16><<<gridn(N * 32), 256, 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->C2);
+    if (c->fmt == 0)
+        k_gemv<float><<<gridn(N * 32), 256, 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->C2, c->Pbc, c->far_state);
+    else if (c->fmt == 1)
+        k_gemv<__half><<<gridn(N * 32), 256, 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->C2, c->Pbc,
+                                                     c->far_state);
+    else
+        k_gemv<__nv_bfloat16><<<gridn(N * 32), 256, 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->C2,
+                                                             c->Pbc, c->far_state);
     k_remap<<<gridn(c->NL), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf);
+    if (c->far) k_far<<<1, 32, 0, s>>>(c->C2, c->sizes, N, c->far_state, c->v_far, 0, 0.0);
     return cudaGetLastError();
 }
 
@@ -492,6 +569,35 @@ extern "C" fdirw_status fdirw_coarse_run(fdirw_coarse* c, float* cbuf, int32_t n
     return FDIRW_OK;
 }
 
+extern "C" fdirw_status fdirw_coarse_far_init(fdirw_coarse* c, const float* c_dev, double c_far0, double* M_out,
+                                              void* cuda_stream)
+{
+    if (!c || !c_dev) return cfail(FDIRW_E_INVALID, "NULL argument");
+    if (!c->far) return cfail(FDIRW_E_STATE, "closed-domain coarse context (v_far = 0)");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    // Σ_{Ω_L} c(t0) as Σ_I N_I C_I of the mapped field (the coarse step's own conserved form)
+    k_map<<<gridn(c->N * 32), 256, 0, s>>>(c_dev, c->grp_ptr, c->grp_vox, c->N, c->C2);
+    k_far<<<1, 32, 0, s>>>(c->C2, c->sizes, c->N, c->far_state, c->v_far, 1, c_far0);
+    CK(cudaGetLastError());
+    double fs[2];
+    CK(cudaMemcpyAsync(fs, c->far_state, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (M_out) *M_out = fs[1];
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_coarse_far_get(fdirw_coarse* c, double* c_far_out, void* cuda_stream)
+{
+    if (!c || !c_far_out) return cfail(FDIRW_E_INVALID, "NULL argument");
+    if (!c->far) return cfail(FDIRW_E_STATE, "closed-domain coarse context (v_far = 0)");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    CK(cudaMemcpyAsync(c_far_out, c->far_state, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return FDIRW_OK;
+}
+
 extern "C" fdirw_status fdirw_coarse_query(const fdirw_coarse* c, fdirw_coarse_info* info)
 {
     if (!c || !info) return cfail(FDIRW_E_INVALID, "NULL argument");
@@ -499,7 +605,7 @@ extern "C" fdirw_status fdirw_coarse_query(const fdirw_coarse* c, fdirw_coarse_i
     info->block = c->b;
     info->n_groups = c->N;
     info->n_region = c->NL;
-    info->p_bytes = (uint64_t)c->N * c->N * c->b_w + (uint64_t)c->N * 4;
+    info->p_bytes = (uint64_t)c->N * c->N * c->b_w + (uint64_t)c->N * 4 * (c->far ? 2 : 1);
     info->flops_per_step = (uint64_t)c->N * (c->N + 1) + 2ull * c->NL;
     return FDIRW_OK;
 }
@@ -524,6 +630,17 @@ extern "C" fdirw_status fdirw_coarse_export(const fdirw_coarse* c, double* P_hos
         for (long I = 0; I < N; ++I) P_host[I * N + I] = dg[I];
     }
     if (group_of_host) CK(cudaMemcpy(group_of_host, c->group_of, c->nvox * 4, cudaMemcpyDeviceToHost));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_coarse_export_pbc(const fdirw_coarse* c, double* pbc_host)
+{
+    if (!c || !pbc_host) return cfail(FDIRW_E_INVALID, "NULL argument");
+    if (!c->far) return cfail(FDIRW_E_STATE, "closed-domain coarse context (v_far = 0)");
+    CK(cudaSetDevice(c->device));
+    std::vector<float> v(c->N);
+    CK(cudaMemcpy(v.data(), c->Pbc, c->N * 4, cudaMemcpyDeviceToHost));
+    for (long i = 0; i < c->N; ++i) pbc_host[i] = v[i];
     return FDIRW_OK;
 }
 

@@ -350,6 +350,58 @@ def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b):
     assert abs(got[region == 1].astype(np.float64).sum() - m0) / m0 <= 1e-6
 
 
+@pytest.mark.parametrize("fmt,b", [("fp32", 3), ("fp16", 5)])
+def test_coarse_far_vs_oracle(fd, oracle_lib, fmt, b):
+    """N1 + N2 (Eq.10 with P_BC, Eq.7): GPU P_BC vs the oracle's held-Dirichlet FD, coarse
+    steps with the boundary term and the device-side c_far update vs the oracle, and the
+    Eq.7 balance Σ_{Ω_L} c + c_far·V_far = K0."""
+    import torch
+    from oracle import coarse as oc
+
+    shape = (22, 21, 23)
+    mask = fi.porous_particle(shape, 6, pore_r=(1.0, 2.0), porosity=0.3, seed=7)
+    region = fi.with_far_field(mask, 6, 3.0)          # 1 near liquid, 2 far reservoir, 0 solid
+    cfg = small_cfg(shape, 1, 200, weights=fmt)
+    pb = oracle_problem(cfg, mask)
+    P, g, sizes = oc.build_P(pb, region, b=b)
+    PBC = oc.build_PBC(pb, region, b=b)
+    Q = oc.quantize_P(P, sizes, fmt)
+    v_far, cf0 = 4.0e4, 0.7
+    c0 = np.where(region == 1, fi.initial_c(mask, "random", seed=9), 0.0).astype(np.float32)
+    ref, cf = c0.astype(np.float64), cf0
+    K0 = ref[region == 1].sum() + cf0 * v_far
+    hist = []
+    for _ in range(4):
+        ref = oc.step_far(Q, PBC.astype(np.float32).astype(np.float64), g, sizes, ref, cf)
+        cf = (K0 - ref[region == 1].sum()) / v_far        # Eq.7
+        hist.append(cf)
+    ctx = fd.coarse_build(lib_params(cfg, fmt, v_far=v_far), region, block=b)
+    try:
+        Pg, gg = fd.coarse_export(ctx)
+        Bg = fd.coarse_export_pbc(ctx)
+        c = torch.from_numpy(c0).cuda()
+        out = torch.empty_like(c)
+        K0g = fd.coarse_far_init(ctx, c, cf0)
+        fd.coarse_step(ctx, c, out)
+        cf1 = fd.coarse_far_get(ctx)
+        fd.coarse_run(ctx, out, 3)
+        cf4 = fd.coarse_far_get(ctx)
+        got = out.cpu().numpy()
+    finally:
+        fd.coarse_destroy(ctx)
+    np.testing.assert_array_equal(gg, g)
+    assert np.abs(Bg - PBC).max() <= 2e-6 * PBC.max()                 # fp32 FD, as P (tolP)
+    assert PBC.max() > 1e-3
+    np.testing.assert_allclose(sizes @ Pg, sizes @ P, rtol=2e-6)    # column masses (absorbing; fp32 FD)
+    assert abs(K0g - K0) <= 1e-6 * K0
+    tol = 1e-5 if fmt == "fp32" else 5e-3
+    assert rel_l2(got[region == 1], ref[region == 1]) <= tol
+    assert abs(cf1 - hist[0]) <= 1e-6 * cf0 and abs(cf4 - hist[3]) <= 1e-6 * cf0
+    np.testing.assert_array_equal(got[region != 1], c0[region != 1])
+    bal = got[region == 1].astype(np.float64).sum() + cf4 * v_far
+    assert abs(bal - K0g) <= 1e-9 * K0g
+
+
 # ------------------------------------------------------------------ NEXT row N4: uniform-chunk dedup
 @pytest.mark.parametrize("cfgname,steps", [("small", 3), ("cfg3", 2)])
 def test_dedup_storage_bitwise(fd, cfgname, steps):

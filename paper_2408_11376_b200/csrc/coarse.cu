@@ -26,6 +26,7 @@
 #include <cuda_fp16.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -40,15 +41,19 @@ struct fdirw_coarse {
     int n_fd = 0, b = 5, fmt = 0, b_w = 4, device = 0;
     double lam = 0;
     long nvox = 0, NL = 0, N = 0;
+    long ldp = 0;             // row stride of P: N rounded up to 8 (16-byte rows, zero padding)
+    int bulk_m = 0;           // > 0: bulk-copy GEMV with GEMV_NW·bulk_m row stages per CTA
+    size_t bulk_smem = 0;
+    int n_sm = 148;
     int* group_of = nullptr;  // [nvox]
     int* rows = nullptr;      // [NL] voxel of each region row (voxel order)
     int* grp_ptr = nullptr;   // [N+1]
     int* grp_vox = nullptr;   // [NL] voxels sorted by group
     int* sizes = nullptr;     // [N]
-    void* P = nullptr;        // [N][N] storage format, diagonal slot 0
+    void* P = nullptr;        // [N][ldp] storage format, diagonal slot 0, zero padding
     float* Pdiag = nullptr;   // [N]
-    float* C = nullptr;       // [N]
-    float* C2 = nullptr;      // [N]
+    float* C = nullptr;       // [ldp], zero padding
+    float* C2 = nullptr;      // [ldp]
     cudaStream_t cap = nullptr;
     cudaGraphExec_t graph = nullptr;
     float* graph_c = nullptr;
@@ -222,7 +227,7 @@ __device__ __forceinline__ float dec(__nv_bfloat16 v) { return __bfloat162float(
 // one block per column J: quantise off-diagonal entries; the fp32 diagonal keeps the column's
 // fp64 mass M_J = Σ_I N_I P_IJ (N_J when closed)
 template <typename WT>
-__global__ void k_quantize(const double* P64, long Ncol, const int* sizes, long N, WT* P, float* Pdiag)
+__global__ void k_quantize(const double* P64, long Ncol, const int* sizes, long N, long ldp, WT* P, float* Pdiag)
 {
     __shared__ double red[32], redm[32];
     const long J = blockIdx.x;
@@ -231,7 +236,7 @@ __global__ void k_quantize(const double* P64, long Ncol, const int* sizes, long 
         const double pv = P64[I * Ncol + J];
         WT q = enc<WT>((float)pv);
         if (I == J) q = enc<WT>(0.f);
-        P[I * N + J] = q;
+        P[I * ldp + J] = q;
         s += (double)sizes[I] * (double)dec(q);
         m += (double)sizes[I] * pv;
     }
@@ -270,63 +275,265 @@ __global__ void k_map(const float* __restrict__ c, const int* __restrict__ grp_p
     }
 }
 
+// C (fp32, zero-padded to ldp) is read as float4 through L1; each lane keeps GU 16-byte loads
+// of its row in flight before the FMAs.  Rows of P̃ bypass L1 and carry an L2 evict_last hint:
+// P̃ is re-read every step and (N² b_w ≤ ~100 MB) can stay resident in the 126 MB L2.
+__device__ __forceinline__ uint4 ld_row(const uint4* p, uint64_t pol)
+{
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+template <typename WT>
+__device__ __forceinline__ float dot16(const uint4& u, const float (&cv)[16 / sizeof(WT)])
+{
+    constexpr int V = 16 / sizeof(WT);
+    const WT* w = reinterpret_cast<const WT*>(&u);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc = fmaf(dec(w[k]), cv[k], acc);
+    return acc;
+}
+
+// One warp per GEMV_RW consecutive rows: every C quad read from L1 serves GEMV_RW rows (the
+// single-row form was L1-throughput bound on the C reads, ncu 94% of peak).  Per row the lane
+// partition (q ≡ lane mod 32, increasing q) and the FMA order are fixed.
+constexpr int GEMV_RW = 4;
+
 template <typename WT>
 __global__ void __launch_bounds__(256) k_gemv(const WT* __restrict__ P, const float* __restrict__ Pdiag,
-                                              const float* __restrict__ C, long N, float* __restrict__ Cout,
-                                              const float* __restrict__ Pbc, const double* __restrict__ far_state)
+                                              const float* __restrict__ C, long N, long ldp,
+                                              float* __restrict__ Cout, const float* __restrict__ Pbc,
+                                              const double* __restrict__ far_state)
 {
+    constexpr int V = 16 / sizeof(WT);  // elements per 128-bit load
+    constexpr int GU = 4;
     const int lane = threadIdx.x & 31;
     const long warps = (long)gridDim.x * (blockDim.x >> 5);
-    constexpr int V = 16 / sizeof(WT);  // elements per 128-bit load
-    for (long I = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); I < N; I += warps) {
-        const WT* row = P + I * N;
-        float acc = 0.f;
-        const bool vec = (N % V) == 0;
-        if (vec) {
-            for (long j0 = (long)lane * V; j0 < N; j0 += 32L * V) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + j0));
-                const WT* w = reinterpret_cast<const WT*>(&u);
+    const int nv = (int)(ldp / V);
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    for (long I0 = (blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * GEMV_RW; I0 < N;
+         I0 += warps * GEMV_RW) {
+        const int nrow = (int)min((long)GEMV_RW, N - I0);
+        float acc[GEMV_RW];
 #pragma unroll
-                for (int k = 0; k < V; ++k) acc = fmaf(dec(w[k]), __ldg(C + j0 + k), acc);
+        for (int r = 0; r < GEMV_RW; ++r) acc[r] = 0.f;
+        for (int q0 = lane; q0 < nv; q0 += 32 * GU) {
+            uint4 u[GEMV_RW][GU];
+#pragma unroll
+            for (int r = 0; r < GEMV_RW; ++r)
+#pragma unroll
+                for (int k = 0; k < GU; ++k)
+                    u[r][k] = (r < nrow && q0 + 32 * k < nv)
+                                  ? ld_row(reinterpret_cast<const uint4*>(P + (I0 + r) * ldp) + q0 + 32 * k, pol)
+                                  : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int k = 0; k < GU; ++k) {
+                if (q0 + 32 * k < nv) {
+                    float cv[V];
+#pragma unroll
+                    for (int h = 0; h < V / 4; ++h) {
+                        const float4 c4 = __ldg(reinterpret_cast<const float4*>(C + (long)(q0 + 32 * k) * V) + h);
+                        cv[4 * h] = c4.x; cv[4 * h + 1] = c4.y; cv[4 * h + 2] = c4.z; cv[4 * h + 3] = c4.w;
+                    }
+#pragma unroll
+                    for (int r = 0; r < GEMV_RW; ++r) acc[r] += dot16<WT>(u[r][k], cv);
+                }
             }
-        } else {
-            for (long j = lane; j < N; j += 32) acc = fmaf(dec(row[j]), __ldg(C + j), acc);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-            float v = fmaf(Pdiag[I], C[I], acc);
-            if (Pbc) v = fmaf(Pbc[I], (float)far_state[0], v);  // Eq.14 boundary term
-            Cout[I] = v;
+        for (int r = 0; r < GEMV_RW; ++r) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+            if (lane == 0 && r < nrow) {
+                const long I = I0 + r;
+                float v = fmaf(Pdiag[I], C[I], acc[r]);
+                if (Pbc) v = fmaf(Pbc[I], (float)far_state[0], v);  // Eq.14 boundary term
+                Cout[I] = v;
+            }
         }
     }
 }
 
-__global__ void k_remap(const int* __restrict__ rows, long NL, const int* __restrict__ group_of,
-                        const float* __restrict__ C, float* __restrict__ c)
+// ---- bulk-copy GEMV (opt-in, FDIRW_COARSE_GEMV=1; measured slower than k_gemv) ----
+// Persistent: one CTA per SM owns a contiguous range of rows, cut into groups of GEMV_RB
+// consecutive rows.  A producer warp streams each group (one contiguous run of P̃) into a
+// ring of shared-memory stages with cp.async.bulk (TMA engine, no registers held per byte in
+// flight) signalled through mbarriers; GEMV_NW consumer warps each own bulk_m stages and take
+// groups g ≡ w (mod GEMV_NW) — a warp's stage is refilled only after that warp released it,
+// so every wait is on the next phase of its own barrier.  C is staged in shared memory once
+// per CTA and each C quad read serves GEMV_RB rows.  Per row, lane partition and FMA order
+// are those of k_gemv, so the two kernels give identical bits.
+constexpr int GEMV_NW = 4, GEMV_RB = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t a, int cnt)
 {
-    GRID_STRIDE(r, NL)
-    {
-        const int v = rows[r];
-        c[v] = C[group_of[v]];
-    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mbar), "l"(pol)
+        : "memory");
 }
 
-// Eq.7 on the coarse mesh: one warp, lane-strided groups, fixed shuffle tree
-__global__ void k_far(const float* __restrict__ C, const int* __restrict__ sizes, long N, double* far_state,
-                      double v_far, int init, double c_far0)
+template <typename WT>
+__global__ void __launch_bounds__((GEMV_NW + 1) * 32) k_gemv_bulk(const WT* __restrict__ P,
+                                                                  const float* __restrict__ Pdiag,
+                                                                  const float* __restrict__ C, long N, long ldp,
+                                                                  float* __restrict__ Cout, const float* __restrict__ Pbc,
+                                                                  const double* __restrict__ far_state, int m)
 {
-    double s = 0.0;
-    for (long I = threadIdx.x; I < N; I += 32) s += (double)sizes[I] * (double)C[I];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    constexpr int V = 16 / sizeof(WT);
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int S = GEMV_NW * m;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* empty = full + S;
+    float* Cs = reinterpret_cast<float*>(sm + ((16 * S + 127) / 128) * 128);
+    unsigned char* stage = reinterpret_cast<unsigned char*>(Cs) + ((ldp * 4 + 127) / 128) * 128;
+    const uint32_t rowB = (uint32_t)(ldp * sizeof(WT));
+    const long r0 = blockIdx.x * N / gridDim.x, r1 = (blockIdx.x + 1) * N / gridDim.x;
+    const int nr = (int)(r1 - r0), ng = (nr + GEMV_RB - 1) / GEMV_RB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(smem_u32(full + i), 1);
+            mbar_init(smem_u32(empty + i), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (long i = threadIdx.x; i < ldp / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(Cs)[i] = __ldg(reinterpret_cast<const float4*>(C) + i);
+    __syncthreads();
+    if (warp == GEMV_NW) {  // producer
+        if (lane == 0) {
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            for (int g = 0; g < ng; ++g) {
+                const int j = g / GEMV_NW, st = (g % GEMV_NW) * m + j % m, u = j / m;
+                const int rows = min(GEMV_RB, nr - g * GEMV_RB);
+                if (u > 0) mbar_wait(smem_u32(empty + st), (u - 1) & 1);
+                mbar_expect_tx(smem_u32(full + st), rows * rowB);
+                bulk_g2s(smem_u32(stage + (size_t)st * GEMV_RB * rowB), P + (r0 + (long)g * GEMV_RB) * ldp,
+                         rows * rowB, smem_u32(full + st), pol);
+            }
+        }
+        return;
+    }
+    const int nv = (int)(ldp / V);
+    for (int g = warp, j = 0; g < ng; g += GEMV_NW, ++j) {
+        const int st = warp * m + j % m, u = j / m;
+        const int rows = min(GEMV_RB, nr - g * GEMV_RB);
+        mbar_wait(smem_u32(full + st), u & 1);
+        const uint4* base = reinterpret_cast<const uint4*>(stage + (size_t)st * GEMV_RB * rowB);
+        float acc[GEMV_RB];
+#pragma unroll
+        for (int r = 0; r < GEMV_RB; ++r) acc[r] = 0.f;
+        for (int q = lane; q < nv; q += 32) {
+            float cv[V];
+#pragma unroll
+            for (int h = 0; h < V / 4; ++h) {
+                const float4 c4 = reinterpret_cast<const float4*>(Cs + (long)q * V)[h];
+                cv[4 * h] = c4.x; cv[4 * h + 1] = c4.y; cv[4 * h + 2] = c4.z; cv[4 * h + 3] = c4.w;
+            }
+#pragma unroll
+            for (int r = 0; r < GEMV_RB; ++r) {
+                if (r < rows) {
+                    const uint4 uu = base[(long)r * nv + q];
+                    const WT* w = reinterpret_cast<const WT*>(&uu);
+                    float d = 0.f;
+#pragma unroll
+                    for (int k = 0; k < V; ++k) d = fmaf(dec(w[k]), cv[k], d);
+                    acc[r] += d;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(empty + st));
+#pragma unroll
+        for (int r = 0; r < GEMV_RB; ++r) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+            if (lane == 0 && r < rows) {
+                const long I = r0 + (long)g * GEMV_RB + r;
+                float v = fmaf(Pdiag[I], Cs[I], acc[r]);
+                if (Pbc) v = fmaf(Pbc[I], (float)far_state[0], v);  // Eq.14 boundary term
+                Cout[I] = v;
+            }
+        }
+    }
+}
+
+// Eq.7 on the coarse mesh, one block of 256 threads: thread-strided fp64 partials, fixed
+// shared-memory tree (deterministic)
+__device__ void far_block(const float* __restrict__ C, const int* __restrict__ sizes, long N, double* far_state,
+                          double v_far, int init, double c_far0)
+{
+    __shared__ double red[256];
+    double s = 0.0;
+    for (long I = threadIdx.x; I < N; I += 256) s += (double)sizes[I] * (double)C[I];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s = red[0];
         if (init) {
             far_state[1] = s + c_far0 * v_far;  // K0 = Σ_{Ω_L} c(t0) + c_far(t0)·V_far
             far_state[0] = c_far0;
         } else {
             far_state[0] = (far_state[1] - s) / v_far;
         }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_far(const float* __restrict__ C, const int* __restrict__ sizes, long N,
+                                             double* far_state, double v_far, int init, double c_far0)
+{
+    far_block(C, sizes, N, far_state, v_far, init, c_far0);
+}
+
+// c'_i = C'_{I(i)} over the Ω_L rows; with a far field block 0 does Eq.7 instead (it
+// reads only C', so it runs beside the remap rather than as a fourth launch)
+__global__ void __launch_bounds__(256) k_remap(const int* __restrict__ rows, long NL, const int* __restrict__ group_of,
+                                               const float* __restrict__ C, float* __restrict__ c,
+                                               const int* __restrict__ sizes, long N, double* far_state, double v_far)
+{
+    const unsigned f = far_state ? 1 : 0;
+    if (f && blockIdx.x == 0) {  // first block: scheduled first, its serial reduction overlaps the remap
+        far_block(C, sizes, N, far_state, v_far, 0, 0.0);
+        return;
+    }
+    const unsigned nb = gridDim.x - f;
+    for (long r = (blockIdx.x - f) * (long)blockDim.x + threadIdx.x; r < NL; r += (long)nb * blockDim.x) {
+        const int v = rows[r];
+        c[v] = C[group_of[v]];
     }
 }
 
@@ -490,11 +697,13 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
                                                        Jn, P64);
         T(cudaGetLastError());
     }
-    T(cudaMalloc(&c->P, (long)N * N * c->b_w));
+    c->ldp = ((long)N + 7) / 8 * 8;
+    T(cudaMalloc(&c->P, (long)N * c->ldp * c->b_w));
+    T(cudaMemsetAsync(c->P, 0, (long)N * c->ldp * c->b_w, s));
     T(cudaMalloc(&c->Pdiag, (long)N * 4));
-    if (c->fmt == 0) k_quantize<float><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, (float*)c->P, c->Pdiag);
-    else if (c->fmt == 1) k_quantize<__half><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, (__half*)c->P, c->Pdiag);
-    else k_quantize<__nv_bfloat16><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, (__nv_bfloat16*)c->P, c->Pdiag);
+    if (c->fmt == 0) k_quantize<float><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, c->ldp, (float*)c->P, c->Pdiag);
+    else if (c->fmt == 1) k_quantize<__half><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, c->ldp, (__half*)c->P, c->Pdiag);
+    else k_quantize<__nv_bfloat16><<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N, c->ldp, (__nv_bfloat16*)c->P, c->Pdiag);
     T(cudaGetLastError());
     if (c->far) {
         T(cudaMalloc(&c->Pbc, (long)N * 4));
@@ -503,11 +712,32 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
         k_pbc<<<gridn(N), 256, 0, s>>>(P64, Ncol, N, c->Pbc);
         T(cudaGetLastError());
     }
-    const long Np4 = ((long)N + 3) / 4 * 4;
-    T(cudaMalloc(&c->C, Np4 * 4));
-    T(cudaMalloc(&c->C2, Np4 * 4));
+    T(cudaMalloc(&c->C, c->ldp * 4));
+    T(cudaMalloc(&c->C2, c->ldp * 4));
+    T(cudaMemsetAsync(c->C, 0, c->ldp * 4, s));
+    T(cudaMemsetAsync(c->C2, 0, c->ldp * 4, s));
     T(cudaStreamSynchronize(s));
     T(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    {  // bulk-copy GEMV: as many row-group stages per consumer warp (≤ 4) as shared memory allows
+        int dev_smem = 0;
+        T(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+        T(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, c->device));
+        const size_t rowB = (size_t)c->ldp * c->b_w, cB = ((size_t)c->ldp * 4 + 127) / 128 * 128;
+        const int fl = getenv("FDIRW_COARSE_GEMV") ? atoi(getenv("FDIRW_COARSE_GEMV")) : 0;  // 1 = bulk GEMV
+        for (int m = 4; m >= 1 && fl == 1; --m) {
+            const size_t need = ((16 * GEMV_NW * m + 127) / 128) * 128 + cB + (size_t)GEMV_NW * m * GEMV_RB * rowB;
+            if (need <= (size_t)dev_smem) {
+                c->bulk_m = m;
+                c->bulk_smem = need;
+                break;
+            }
+        }
+        if (c->bulk_m > 0) {
+            const void* f = c->fmt == 0 ? (const void*)k_gemv_bulk<float>
+                          : c->fmt == 1 ? (const void*)k_gemv_bulk<__half> : (const void*)k_gemv_bulk<__nv_bfloat16>;
+            T(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->bulk_smem));
+        }
+    }
 #undef T
     cleanup();
     *out = c;
@@ -518,16 +748,27 @@ static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
 {
     const long N = c->N;
     k_map<<<gridn(N * 32), 256, 0, s>>>(cbuf, c->grp_ptr, c->grp_vox, N, c->C);
-    if (c->fmt == 0)
-        k_gemv<float><<<gridn(N * 32), 256, 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->C2, c->Pbc, c->far_state);
+    if (c->bulk_m > 0) {
+        const dim3 g((unsigned)(N < c->n_sm ? N : c->n_sm)), bl((GEMV_NW + 1) * 32);
+        if (c->fmt == 0)
+            k_gemv_bulk<float><<<g, bl, c->bulk_smem, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
+                                                          c->Pbc, c->far_state, c->bulk_m);
+        else if (c->fmt == 1)
+            k_gemv_bulk<__half><<<g, bl, c->bulk_smem, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
+                                                           c->Pbc, c->far_state, c->bulk_m);
+        else
+            k_gemv_bulk<__nv_bfloat16><<<g, bl, c->bulk_smem, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N,
+                                                                  c->ldp, c->C2, c->Pbc, c->far_state, c->bulk_m);
+    } else if (c->fmt == 0)
+        k_gemv<float><<<gridn((N + GEMV_RW - 1) / GEMV_RW * 32), 256, 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc, c->far_state);
     else if (c->fmt == 1)
-        k_gemv<__half><<<gridn(N * 32), 256, 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->C2, c->Pbc,
-                                                     c->far_state);
+        k_gemv<__half><<<gridn((N + GEMV_RW - 1) / GEMV_RW * 32), 256, 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
+                                                     c->Pbc, c->far_state);
     else
-        k_gemv<__nv_bfloat16><<<gridn(N * 32), 256, 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->C2,
-                                                             c->Pbc, c->far_state);
-    k_remap<<<gridn(c->NL), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf);
-    if (c->far) k_far<<<1, 32, 0, s>>>(c->C2, c->sizes, N, c->far_state, c->v_far, 0, 0.0);
+        k_gemv<__nv_bfloat16><<<gridn((N + GEMV_RW - 1) / GEMV_RW * 32), 256, 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->ldp,
+                                                             c->C2, c->Pbc, c->far_state);
+    k_remap<<<gridn(c->NL) + (c->far ? 1 : 0), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf, c->sizes, N,
+                                                           c->far ? c->far_state : nullptr, c->v_far);
     return cudaGetLastError();
 }
 
@@ -578,7 +819,7 @@ extern "C" fdirw_status fdirw_coarse_far_init(fdirw_coarse* c, const float* c_de
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     // Σ_{Ω_L} c(t0) as Σ_I N_I C_I of the mapped field (the coarse step's own conserved form)
     k_map<<<gridn(c->N * 32), 256, 0, s>>>(c_dev, c->grp_ptr, c->grp_vox, c->N, c->C2);
-    k_far<<<1, 32, 0, s>>>(c->C2, c->sizes, c->N, c->far_state, c->v_far, 1, c_far0);
+    k_far<<<1, 256, 0, s>>>(c->C2, c->sizes, c->N, c->far_state, c->v_far, 1, c_far0);
     CK(cudaGetLastError());
     double fs[2];
     CK(cudaMemcpyAsync(fs, c->far_state, 16, cudaMemcpyDeviceToHost, s));
@@ -605,7 +846,7 @@ extern "C" fdirw_status fdirw_coarse_query(const fdirw_coarse* c, fdirw_coarse_i
     info->block = c->b;
     info->n_groups = c->N;
     info->n_region = c->NL;
-    info->p_bytes = (uint64_t)c->N * c->N * c->b_w + (uint64_t)c->N * 4 * (c->far ? 2 : 1);
+    info->p_bytes = (uint64_t)c->N * c->ldp * c->b_w + (uint64_t)c->N * 4 * (c->far ? 2 : 1);
     info->flops_per_step = (uint64_t)c->N * (c->N + 1) + 2ull * c->NL;
     return FDIRW_OK;
 }
@@ -616,17 +857,20 @@ extern "C" fdirw_status fdirw_coarse_export(const fdirw_coarse* c, double* P_hos
     CK(cudaSetDevice(c->device));
     const long N = c->N;
     if (P_host) {
-        std::vector<unsigned char> raw((size_t)N * N * c->b_w);
+        const long ld = c->ldp;
+        std::vector<unsigned char> raw((size_t)N * ld * c->b_w);
         std::vector<float> dg(N);
         CK(cudaMemcpy(raw.data(), c->P, raw.size(), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(dg.data(), c->Pdiag, N * 4, cudaMemcpyDeviceToHost));
-        for (long i = 0; i < N * N; ++i) {
-            double v;
-            if (c->fmt == 0) { float f; memcpy(&f, &raw[i * 4], 4); v = f; }
-            else if (c->fmt == 1) { __half h; memcpy(&h, &raw[i * 2], 2); v = __half2float(h); }
-            else { __nv_bfloat16 h; memcpy(&h, &raw[i * 2], 2); v = __bfloat162float(h); }
-            P_host[i] = v;
-        }
+        for (long I = 0; I < N; ++I)
+            for (long J = 0; J < N; ++J) {
+                const long i = I * ld + J;
+                double v;
+                if (c->fmt == 0) { float f; memcpy(&f, &raw[i * 4], 4); v = f; }
+                else if (c->fmt == 1) { __half h; memcpy(&h, &raw[i * 2], 2); v = __half2float(h); }
+                else { __nv_bfloat16 h; memcpy(&h, &raw[i * 2], 2); v = __bfloat162float(h); }
+                P_host[I * N + J] = v;
+            }
         for (long I = 0; I < N; ++I) P_host[I * N + I] = dg[I];
     }
     if (group_of_host) CK(cudaMemcpy(group_of_host, c->group_of, c->nvox * 4, cudaMemcpyDeviceToHost));

@@ -350,6 +350,31 @@ def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b):
     assert abs(got[region == 1].astype(np.float64).sum() - m0) / m0 <= 1e-6
 
 
+@pytest.mark.parametrize("fmt", ["fp32", "bf16"])
+def test_coarse_bulk_gemv_bitwise(fd, fmt, monkeypatch):
+    """The bulk-copy (cp.async.bulk + mbarrier ring) GEMV and the register GEMV
+    (FDIRW_COARSE_GEMV=0) give identical bits: same lane partition and FMA order per row."""
+    import torch
+
+    shape = (30, 29, 31)
+    mask = fi.porous_particle(shape, 9, pore_r=(1.0, 2.0), porosity=0.3, seed=4)
+    region = fi.near_field(mask, 9, margin=4)
+    cfg = small_cfg(shape, 1, 50, weights=fmt)
+    c0 = torch.from_numpy(fi.initial_c(mask, "random", seed=4)).cuda()
+    outs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("FDIRW_COARSE_GEMV", mode)
+        ctx = fd.coarse_build(lib_params(cfg, fmt), region, block=3)
+        try:
+            assert ctx.info["n_groups"] > 148  # several rows per CTA
+            c = c0.clone()
+            fd.coarse_run(ctx, c, 4)
+            outs.append(c.cpu().numpy())
+        finally:
+            fd.coarse_destroy(ctx)
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("fmt,b", [("fp32", 3), ("fp16", 5)])
 def test_coarse_far_vs_oracle(fd, oracle_lib, fmt, b):
     """N1 + N2 (Eq.10 with P_BC, Eq.7): GPU P_BC vs the oracle's held-Dirichlet FD, coarse

@@ -71,7 +71,15 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weig
 #define FDIRW_F_DEDUP_STORAGE 4u /* NEXT row N4: 8-target chunks whose every source shares one window
                                   class read that class's kernel from a small L2-resident table
                                   instead of streaming their gather weights (bitwise identical
-                                  results; fewer HBM bytes; DESIGN.md §13)                        */
+                                  results; fewer HBM bytes; DESIGN.md §14)                        */
+#define FDIRW_F_KGEN_FP64 8u   /* kgen substeps in fp64, in the oracle's operation order (no FMA), no
+                                  renormalisation: the off-centre weights equal the oracle's O5
+                                  weights bit for bit (reading A22; debugging — fp64 is slower)   */
+#define FDIRW_F_SYMMETRIC_RULE 16u /* exact regime only (n_fd <= R, else FDIRW_E_INVALID): P = Pᵀ,
+                                  so target x's gather weights are x's own kernel reflected,
+                                  W_x(−o); each rank generates only its own slab's kernels (no
+                                  halo sources).  Not combined with FDIRW_F_DEDUP_STORAGE
+                                  (reading A24)                                                   */
 
 /* The paper's problem statement (Table 1) + north_star's window radius / precision. */
 typedef struct {

@@ -32,6 +32,8 @@ WEIGHTS = {"fp32": 0, "fp16": 1, "bf16": 2}
 F_NO_MASS_FIX = 1
 F_NO_DEDUP = 2
 F_DEDUP_STORAGE = 4  # NEXT row N4: uniform chunks read shared class kernels (fewer HBM bytes)
+F_KGEN_FP64 = 8  # kgen in fp64, the oracle's operation order (reading A22, debugging)
+F_SYMMETRIC_RULE = 16  # exact regime only: gather weights = own kernel reflected (reading A24)
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",

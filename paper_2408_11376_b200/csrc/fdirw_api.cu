@@ -163,8 +163,11 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (!(p->D_fast > 0) || !(p->D_slow >= 0)) return fail(FDIRW_E_INVALID, "need D_fast > 0, D_slow >= 0");
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
-    if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE))
+    if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE | FDIRW_F_KGEN_FP64 |
+                     FDIRW_F_SYMMETRIC_RULE))
         return fail(FDIRW_E_INVALID, "unknown flags");
+    if ((p->flags & FDIRW_F_SYMMETRIC_RULE) && (p->flags & FDIRW_F_DEDUP_STORAGE))
+        return fail(FDIRW_E_INVALID, "FDIRW_F_SYMMETRIC_RULE is not combined with FDIRW_F_DEDUP_STORAGE");
     if ((p->flags & FDIRW_F_NO_DEDUP) && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_DEDUP_STORAGE needs the window de-duplication");
     if (!(p->v_far >= 0)) return fail(FDIRW_E_INVALID, "v_far must be >= 0");
@@ -266,6 +269,9 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     *out = nullptr;
     Derived d;
     if ((st = derive(*params, &d)) != FDIRW_OK) return st;
+    if ((params->flags & FDIRW_F_SYMMETRIC_RULE) && d.n_fd > params->radius)
+        return fail(FDIRW_E_INVALID, "FDIRW_F_SYMMETRIC_RULE needs the exact regime n_fd <= R (reading A24); n_fd = " +
+                                         std::to_string(d.n_fd));
 
     fdirw_ctx* c = new fdirw_ctx();
     c->p = *params;
@@ -329,13 +335,21 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     ka.sz0 = g.sz0; ka.sz1 = g.sz1;
     ka.z0 = g.z0; ka.z1 = g.z1;
     ka.lam_ff = (float)d.lam_ff; ka.lam_fs = (float)d.lam_fs; ka.lam_ss = (float)d.lam_ss;
+    ka.lam_d[0] = d.lam_ff; ka.lam_d[1] = d.lam_fs; ka.lam_d[2] = d.lam_ss;
+    ka.fp64 = (params->flags & FDIRW_F_KGEN_FP64) ? 1 : 0;
+    ka.symmetric = (params->flags & FDIRW_F_SYMMETRIC_RULE) ? 1 : 0;
+    if (ka.symmetric) {  // every rank generates its own targets' kernels only: no halo sources
+        ka.sz0 = g.z0;
+        ka.sz1 = g.z1;
+    }
     ka.n_fd = d.n_fd;
     ka.fmt = c->fmt;
     ka.mass_fix = (params->flags & FDIRW_F_NO_MASS_FIX) ? 0 : 1;
     ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;
-    c->kgen_sources = (uint64_t)g.nx * g.ny * (g.sz1 - g.sz0);
+    c->kgen_sources = (uint64_t)g.nx * g.ny * (ka.sz1 - ka.sz0);
     c->kgen_windows = c->kgen_sources;
-    bool dedup = !(params->flags & FDIRW_F_NO_DEDUP);
+    // (the symmetric rule writes through the direct path: the expand kernel scatters forward)
+    bool dedup = !(params->flags & (FDIRW_F_NO_DEDUP | FDIRW_F_SYMMETRIC_RULE));
     if (dedup) {
         // identical windows ⇒ identical kernels: compute each distinct window once (dedup.cu)
         int* class_pad = nullptr;

@@ -55,6 +55,9 @@ struct KgenArgs {
     int sz0, sz1;         // source planes
     int z0, z1;           // target slab
     float lam_ff, lam_fs, lam_ss;
+    double lam_d[3];      // {ff, fs, ss} in fp64 (FDIRW_F_KGEN_FP64)
+    int fp64;             // FDIRW_F_KGEN_FP64: fp64 substeps in the oracle's order (reading A22)
+    int symmetric;        // FDIRW_F_SYMMETRIC_RULE: write W_s(o) as target s's slot −o (reading A24)
     int n_fd;
     int fmt, mass_fix;
     void* Wt;

@@ -22,12 +22,14 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "fdirw_internal.h"
 #include "layout.cuh"
 
 namespace fdirw {
 
-template <int R>
+template <int R, bool F64 = false>
 struct KgenShape {
     static constexpr int L = 2 * R + 1;
     static constexpr int LL = L * L;
@@ -36,7 +38,8 @@ struct KgenShape {
     static constexpr int NW = NT / 32;
     static constexpr int Lp = (L + 3) / 4 * 4;                             // column padded to float4s
     static constexpr size_t smem_floats = 2 * (size_t)NT * Lp;             // double-buffered, column-major
-    static constexpr size_t smem_bytes = smem_floats * 4 + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
+    static constexpr size_t buf_bytes = smem_floats * (F64 ? 8 : 4);
+    static constexpr size_t smem_bytes = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
 };
 
 __device__ __forceinline__ double warp_sum_f64(double v)
@@ -100,16 +103,29 @@ __device__ __forceinline__ float face_lambda(unsigned p, unsigned q, float ff, f
     return (p & q) ? ff : ((p | q) ? fs : ss);
 }
 
-template <int R>
-__global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a)
+__device__ __forceinline__ double face_lambda_d(unsigned p, unsigned q, const double* lam)
 {
-    using S = KgenShape<R>;
+    if (p > 1u || q == 2u) return 0.0;
+    if (q == 3u) q = 1u;
+    return (p & q) ? lam[0] : ((p | q) ? lam[1] : lam[2]);
+}
+
+// F64 = true: FDIRW_F_KGEN_FP64 (reading A22, debugging).  The same window, thread mapping
+// and epilogue, but the substeps run in fp64 in the oracle's operation order
+// (acc = c; acc += λ_f·(c_f − c) for f = −x,+x,−y,+y,−z,+z, separate multiply and add, no
+// FMA) and the result is not renormalised (fp64 FD keeps Σ = 1 to rounding), so the
+// off-centre weights are the oracle's O2 kernels rounded exactly as O5 rounds them.
+template <int R, bool F64>
+__global__ void __launch_bounds__(KgenShape<R, F64>::NT) kgen_kernel(const KgenArgs a)
+{
+    using S = KgenShape<R, F64>;
+    using T = typename std::conditional<F64, double, float>::type;
     constexpr int L = S::L, LL = S::LL, LLL = S::LLL, NT = S::NT;
     constexpr int KC = LLL / 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* buf = reinterpret_cast<float*>(smem_raw);
-    unsigned char* ph = smem_raw + S::smem_floats * 4;
-    double* red = reinterpret_cast<double*>(smem_raw + S::smem_floats * 4 + ((LLL + 15) / 16) * 16);
+    T* buf = reinterpret_cast<T*>(smem_raw);
+    unsigned char* ph = smem_raw + S::buf_bytes;
+    double* red = reinterpret_cast<double*>(smem_raw + S::buf_bytes + ((LLL + 15) / 16) * 16);
 
     const int t = threadIdx.x;
     const bool col = t < LL;
@@ -140,7 +156,46 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
         if (ph[KC] == 3) continue;  // far-field voxels are not sources (their value is c_far)
 
         constexpr int Lp = S::Lp, NQ = Lp / 4;
-        float c[Lp], lzp[L], lzm[L];  // own +z / −z face numbers (asymmetric next to the reservoir)
+        T c[Lp];
+        if constexpr (F64) {
+#pragma unroll
+            for (int z = 0; z < Lp; ++z) c[z] = (col && t == R * L + R && z == R) ? 1.0 : 0.0;
+            for (int k = 0; k < a.n_fd; ++k) {
+                double* b = buf + (k & 1) * (NT * Lp);
+                if (col) {
+#pragma unroll
+                    for (int z = 0; z < Lp; ++z) b[t * Lp + z] = c[z];
+                }
+                __syncthreads();
+                if (col) {
+                    double nw[L];
+#pragma unroll
+                    for (int z = 0; z < L; ++z) {
+                        const int i = z * LL + t;
+                        const unsigned p = ph[i];
+                        double acc = c[z];
+                        const double cz = c[z];
+                        // −x, +x, −y, +y, −z, +z (the oracle's face order)
+                        if (oxm) acc = __dadd_rn(acc, __dmul_rn(face_lambda_d(p, ph[i + oxm], a.lam_d),
+                                                                __dsub_rn(b[(t + oxm) * Lp + z], cz)));
+                        if (oxp) acc = __dadd_rn(acc, __dmul_rn(face_lambda_d(p, ph[i + oxp], a.lam_d),
+                                                                __dsub_rn(b[(t + oxp) * Lp + z], cz)));
+                        if (oym) acc = __dadd_rn(acc, __dmul_rn(face_lambda_d(p, ph[i + oym], a.lam_d),
+                                                                __dsub_rn(b[(t + oym) * Lp + z], cz)));
+                        if (oyp) acc = __dadd_rn(acc, __dmul_rn(face_lambda_d(p, ph[i + oyp], a.lam_d),
+                                                                __dsub_rn(b[(t + oyp) * Lp + z], cz)));
+                        if (z > 0) acc = __dadd_rn(acc, __dmul_rn(face_lambda_d(p, ph[i - LL], a.lam_d),
+                                                                  __dsub_rn(c[z - 1], cz)));
+                        if (z < L - 1) acc = __dadd_rn(acc, __dmul_rn(face_lambda_d(p, ph[i + LL], a.lam_d),
+                                                                      __dsub_rn(c[z + 1], cz)));
+                        nw[z] = acc;
+                    }
+#pragma unroll
+                    for (int z = 0; z < L; ++z) c[z] = nw[z];
+                }
+            }
+        } else {
+        float lzp[L], lzm[L];  // own +z / −z face numbers (asymmetric next to the reservoir)
         unsigned long long lxm2[Lp / 2], lxp2[Lp / 2], lym2[Lp / 2], lyp2[Lp / 2];  // (z, z+1) pairs
 #pragma unroll
         for (int h = 0; h < Lp / 2; ++h) {
@@ -212,6 +267,7 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
                 for (int z = 0; z < L; ++z) c[z] = nw[z];
             }
         }
+        }  // fp32 substeps
 
         // ---- epilogue (a4) ----
         double s = 0.0;
@@ -222,17 +278,19 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
         const double S_ = block_sum_f64<S::NW>(s, red);
         // closed window: renormalise to mass 1 (fp32 FD drift); open window (N2): the kernel
         // keeps its own mass M = S, the rest went to the reservoir
-        const double inv = open ? 1.0 : 1.0 / S_;
+        const double inv = (open || F64) ? 1.0 : 1.0 / S_;
         const double M = open ? S_ : 1.0;
         double qsum = 0.0;
         float centre_q = 0.f;
         if (col) {
             const int ox = cx - R, oy = cy - R;
-            const int gx = sx + ox, gy = sy + oy;
+            // gather target and slot of this weight: x = s + o in slot o, or with the symmetric
+            // rule (reading A24, exact regime P = Pᵀ) the source's own target x = s in slot −o
+            const int gx = a.symmetric ? sx : sx + ox, gy = a.symmetric ? sy : sy + oy;
 #pragma unroll
             for (int z = 0; z < L; ++z) {
                 const int o = z * LL + t;
-                const int oz = z - R, gz = sz + oz;
+                const int oz = z - R, gz = a.symmetric ? sz : sz + oz;
                 const bool active = ph[o] <= 1;
                 const float wf = (float)((double)c[z] * inv);
                 float qd;
@@ -265,7 +323,8 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
                 const int q = gy * a.nxq + (gx >> 3);
                 const size_t tile = (size_t)zl * a.tpp + q / a.tile;
                 const int e = q % a.tile, j = gx & 7;
-                const size_t idx = ((tile * (size_t)(a.K - 1) + slot_of(ox, oy, oz, R)) * a.tile + e) * 8 + j;
+                const int sl = a.symmetric ? slot_of(-ox, -oy, -oz, R) : slot_of(ox, oy, oz, R);
+                const size_t idx = ((tile * (size_t)(a.K - 1) + sl) * a.tile + e) * 8 + j;
                 if (a.fmt == 0) reinterpret_cast<float*>(a.Wt)[idx] = wf;
                 else reinterpret_cast<unsigned short*>(a.Wt)[idx] = bits;
             }
@@ -284,38 +343,51 @@ __global__ void __launch_bounds__(KgenShape<R>::NT) kgen_kernel(const KgenArgs a
     }
 }
 
-template <int R>
+template <int R, bool F64>
 static cudaError_t launch_kgen_r(const KgenArgs& a, cudaStream_t s)
 {
-    using S = KgenShape<R>;
+    using S = KgenShape<R, F64>;
     const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
     if (nsrc <= 0) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kgen_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(kgen_kernel<R, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)S::smem_bytes);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_kernel<R>, S::NT, S::smem_bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_kernel<R, F64>, S::NT, S::smem_bytes);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     long grid = (long)sms * per_sm;
     if (grid > nsrc) grid = nsrc;
-    kgen_kernel<R><<<(unsigned)grid, S::NT, S::smem_bytes, s>>>(a);
+    kgen_kernel<R, F64><<<(unsigned)grid, S::NT, S::smem_bytes, s>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s)
 {
+    if (a.fp64) {
+        switch (R) {
+            case 1: return launch_kgen_r<1, true>(a, s);
+            case 2: return launch_kgen_r<2, true>(a, s);
+            case 3: return launch_kgen_r<3, true>(a, s);
+            case 4: return launch_kgen_r<4, true>(a, s);
+            case 5: return launch_kgen_r<5, true>(a, s);
+            case 6: return launch_kgen_r<6, true>(a, s);
+            case 7: return launch_kgen_r<7, true>(a, s);
+            case 8: return launch_kgen_r<8, true>(a, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (R) {
-        case 1: return launch_kgen_r<1>(a, s);
-        case 2: return launch_kgen_r<2>(a, s);
-        case 3: return launch_kgen_r<3>(a, s);
-        case 4: return launch_kgen_r<4>(a, s);
-        case 5: return launch_kgen_r<5>(a, s);
-        case 6: return launch_kgen_r<6>(a, s);
-        case 7: return launch_kgen_r<7>(a, s);
-        case 8: return launch_kgen_r<8>(a, s);
+        case 1: return launch_kgen_r<1, false>(a, s);
+        case 2: return launch_kgen_r<2, false>(a, s);
+        case 3: return launch_kgen_r<3, false>(a, s);
+        case 4: return launch_kgen_r<4, false>(a, s);
+        case 5: return launch_kgen_r<5, false>(a, s);
+        case 6: return launch_kgen_r<6, false>(a, s);
+        case 7: return launch_kgen_r<7, false>(a, s);
+        case 8: return launch_kgen_r<8, false>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }

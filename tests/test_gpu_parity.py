@@ -238,6 +238,67 @@ def test_virtual_ranks_bitwise(fd, world):
     np.testing.assert_array_equal(got, one.astype(np.float32))
 
 
+@pytest.mark.parametrize("fmt,far", [("fp32", False), ("bf16", False), ("fp16", True)])
+def test_kgen_fp64_flag_equals_oracle_bits(fd, oracle_lib, fmt, far):
+    """FDIRW_F_KGEN_FP64 (reading A22): fp64 substeps in the oracle's operation order and no
+    renormalisation ⇒ every stored off-centre weight equals the oracle's O5 weight bit for bit
+    (closed and open windows); the diagonal differs only by fp64 summation order."""
+    shape = (9, 10, 11)
+    mask = fi.random_two_phase(shape, 0.6, seed=11)
+    if far:
+        mask[:, :, :2][mask[:, :, :2] == 1] = 2
+    cfg = small_cfg(shape, 3, 60, D_slow=1e-2, weights=fmt)
+    pb = oracle_problem(cfg, mask)
+    Wo = oracle_lib.quantize(pb, oracle_lib.build_kernels(pb), fmt)  # open windows keep M = ΣW
+    for flags in (fd.F_KGEN_FP64, fd.F_KGEN_FP64 | fd.F_NO_DEDUP):
+        ctx = fd.build_kernels(lib_params(cfg, fmt, flags, v_far=1e3 if far else 0.0), mask)
+        try:
+            Wg = fd.export_kernels(ctx, (0, shape[2], 0, shape[1], 0, shape[0]))
+        finally:
+            fd.destroy(ctx)
+        src = (mask != 2).reshape(-1)
+        c = pb.K // 2
+        off = np.ones(pb.K, bool)
+        off[c] = False
+        Wg2, Wo2 = Wg.reshape(-1, pb.K)[src], Wo.reshape(-1, pb.K)[src]
+        np.testing.assert_array_equal(Wg2[:, off], Wo2[:, off])
+        np.testing.assert_allclose(Wg2[:, c], Wo2[:, c], rtol=2.4e-7, atol=1e-12)
+
+
+def test_symmetric_rule(fd, oracle_lib):
+    """FDIRW_F_SYMMETRIC_RULE (reading A24): in the exact regime (n_fd ≤ R) target x's gather
+    weights are its own kernel reflected.  Matches the oracle and the default build; the slab
+    decomposition (no halo sources) stays bitwise equal to one GPU; rejected when n_fd > R."""
+    import torch
+
+    cfg = small_cfg((12, 11, 13), 3, 3, D_slow=1e-2, weights="fp32")
+    mask = fi.random_two_phase(cfg.shape, 0.6, seed=8)
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=8)
+    ref = oracle_lib.step_full(pb, c0.astype(np.float64), steps=2)
+    sym, m0, m1, info = _gpu_steps(fd, cfg, mask, c0, 2, flags=fd.F_SYMMETRIC_RULE)
+    dflt, _, _, _ = _gpu_steps(fd, cfg, mask, c0, 2)
+    assert rel_l2(sym, ref) <= 1e-5 and rel_l2(sym, dflt) <= 1e-6
+    assert abs(m1 - m0) / m0 <= 1e-6
+    one, _, _, _ = _gpu_steps(fd, cfg, mask, c0, 1, use_run=False, flags=fd.F_SYMMETRIC_RULE)
+    sl = fd.slabs(cfg.shape[0], 3)
+    ctxs = [fd.build_kernels(lib_params(cfg, flags=fd.F_SYMMETRIC_RULE), mask, rank=r, world=3, z_begin=a,
+                             z_end=b, device=0) for r, (a, b) in enumerate(sl)]
+    try:
+        assert ctxs[1].info["kgen_sources"] == (sl[1][1] - sl[1][0]) * 11 * 13  # own slab only
+        cin = [torch.from_numpy(c0[a:b].copy()).cuda() for a, b in sl]
+        cout = [torch.empty_like(t) for t in cin]
+        fd.step_virtual(ctxs, cin, cout)
+        got = np.concatenate([t.cpu().numpy() for t in cout], axis=0)
+    finally:
+        for c in ctxs:
+            fd.destroy(c)
+    np.testing.assert_array_equal(got, one.astype(np.float32))
+    with pytest.raises(fd.FdirwError) as e:
+        fd.build_kernels(lib_params(small_cfg((6, 6, 6), 2, 3), flags=fd.F_SYMMETRIC_RULE), np.ones((6, 6, 6), np.uint8))
+    assert e.value.status == fd.E_INVALID
+
+
 def test_errors(fd):
     import torch
 

@@ -463,6 +463,16 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         if (!c->nccl) { g_err = err; return bail(FDIRW_E_NCCL); }
         c->comm = nccl_comm_init(c->nccl, c->world, c->rank, dist->nccl_id, &err);
         if (!c->comm) { g_err = err; return bail(FDIRW_E_NCCL); }
+        // NCCL connects peers lazily on first use; do that here, outside any stream capture
+        // (fdirw_run captures the halo exchange and the Eq.7 all-gather into a CUDA graph).
+        // The state buffers are still zero, so the exchange moves zeros.
+        if (nccl_halo(c->nccl, c->comm, c->cpad[0], make_halo_plan(g, c->rank, c->world), c->comm_stream, &err) ||
+            (c->far && nccl_allgather_f64(c->nccl, c->comm, c->tile_buf, c->tile_stride, c->gathered, c->comm_stream, &err)) ||
+            nccl_allreduce_sum_f64(c->nccl, c->comm, c->mass_out, c->comm_stream, &err)) {
+            g_err = err;
+            return bail(FDIRW_E_NCCL);
+        }
+        BAIL_CUDA(cudaStreamSynchronize(c->comm_stream));
     }
 #undef BAIL_CUDA
     *out = c;

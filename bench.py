@@ -308,6 +308,9 @@ def main():
     ap.add_argument("--mode", default="fine", choices=["fine", "coarse"],
                     help="fine: the north_star windowed step (default); coarse: NEXT row N1")
     ap.add_argument("--block", type=int, default=5)
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 halo: p2p = edge planes stored into the neighbours' memory by the superposition "
+                         "(default); nccl = grouped ncclSend/Recv overlapped with the interior tiles")
     ap.add_argument("--storage", default="dense", choices=["dense", "dedup"],
                     help="dense: north_star gather layout (default); dedup: NEXT row N4 uniform-chunk kernels")
     args = ap.parse_args()
@@ -325,11 +328,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: FDIRW_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 with a gloo process group
+    # (exercises the N>1 orchestration on a one-GPU box; P2P transport only — NCCL refuses
+    # two ranks on one device).  Never set by the driver.
+    one_dev = os.environ.get("FDIRW_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     if world != args.gpus:
         raise SystemExit("--gpus %d but WORLD_SIZE %d (launch N>1 with torch.distributed.run)" % (args.gpus, world))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = fi.config(args.config, weights=args.weights)
     mask = cfg.mask()
@@ -344,12 +356,42 @@ def main():
                        radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights, v_far=cfg.v_far,
                        flags=fd.F_DEDUP_STORAGE if args.storage == "dedup" else 0)
     stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            if one_dev:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
+
+    def allreduce(v, op=dist.ReduceOp.SUM):  # scalar fp64 across ranks
+        t_ = torch.tensor([v], dtype=torch.float64, device="cpu" if one_dev else "cuda")
+        dist.all_reduce(t_, op=op)
+        return float(t_.item())
+
+    transport = args.transport if (world > 1 and cfg.v_far == 0) else "nccl"  # P2P: closed domain only
+
+    def build(tr):
+        cx = fd.build_kernels(params, mask, rank=rank, world=world, z_begin=z0, z_end=z1, device=local,
+                              nccl_id=nccl_id if tr == "nccl" else None, stream=stream, transport=tr)
+        if tr == "p2p":  # all-gather the CUDA IPC blobs, open the neighbours' buffers
+            blobs = [None] * world
+            dist.all_gather_object(blobs, fd.p2p_export(cx))
+            fd.p2p_attach(cx, blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank < world - 1 else None)
+            barrier()
+        return cx
+
     torch.cuda.synchronize()
     t = time.perf_counter()
-    ctx = fd.build_kernels(params, mask, rank=rank, world=world, z_begin=z0, z_end=z1, device=local,
-                           nccl_id=nccl_id, stream=stream)
+    ctx = build(transport)
     t_kgen = time.perf_counter() - t
     info = ctx.info
+
+    def gmass(cc):  # with P2P fdirw_mass is slab-local
+        m = fd.mass(ctx, cc)
+        if transport == "p2p":
+            m = allreduce(m)
+        return m
 
     c0 = fi.initial_c(mask, "paper") * (mask != 2)  # far-field voxels carry the scalar c_far (N2)
     c_host = torch.from_numpy(np.ascontiguousarray(c0[z0:z1])).pin_memory()
@@ -357,13 +399,20 @@ def main():
     far = cfg.v_far > 0
     if far:
         total0 = fd.far_init(ctx, c, cfg.c_far0, stream)  # Eq.7's Σc_{S+L}(t0)
-    m0 = fd.mass(ctx, c)
+    m0 = gmass(c)
     fd.run(ctx, c, args.warmup)
     torch.cuda.synchronize()
+    p2p_note = None
+    if transport == "p2p":  # a wait that timed out (never expected) → rebuild on NCCL
+        if allreduce(1.0 if fd.p2p_check(ctx) else 0.0, dist.ReduceOp.MAX) > 0:
+            fd.destroy(ctx)
+            transport, p2p_note = "nccl", "P2P neighbour wait timed out during warm-up; fell back to NCCL"
+            ctx = build(transport)
+            c.copy_(c_host.to("cuda"))
+            m0 = gmass(c)
+            fd.run(ctx, c, args.warmup)
+            torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -375,15 +424,11 @@ def main():
         torch.cuda.synchronize()
         barrier()
     t_ms = ev0.elapsed_time(ev1)
-    m1 = fd.mass(ctx, c)
+    m1 = gmass(c)
     cf1 = fd.far_get(ctx, stream) if far else None
     if world > 1:
-        tt = torch.tensor([t_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-        km = torch.tensor([t_kgen], device="cuda")
-        dist.all_reduce(km, op=dist.ReduceOp.MAX)
-        t_kgen = float(km.item())
+        t_ms = allreduce(t_ms, dist.ReduceOp.MAX)
+        t_kgen = allreduce(t_kgen, dist.ReduceOp.MAX)
 
     # e2e through the public API with host buffers: every step copies its input from pinned
     # host memory (H2D), runs fdirw_step and copies its result back (D2H).  Pipelined the way a
@@ -426,9 +471,7 @@ def main():
     barrier()
     e_ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([e_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e_ms = float(tt.item())
+        e_ms = allreduce(e_ms, dist.ReduceOp.MAX)
 
     # voxel-updates: every target whose C the step computes (far-field voxels, N2, hold the
     # scalar c_far instead and are not counted)
@@ -444,7 +487,9 @@ def main():
         bpv = int(round((1.0 - f_u) * (info["K"] - 1) * (2 if cfg.weights != "fp32" else 4))) + 12
     per_launch_bytes = bpv * n_slab
     peak, peak_src = _hbm_peak()
-    launches_per_step = 1 if world == 1 else (3 if info["n_tiles"] > 0 else 1)
+    # N=1: one superpose launch; N>1: interior + 2 boundary superpose launches (+ wait and
+    # signal kernels with P2P; NCCL's own kernels are not counted)
+    launches_per_step = 1 if world == 1 else (5 if transport == "p2p" else 3)
     # one superpose launch per step at N=1 (+1 pack, +1 unpack per fdirw_run); the launch
     # duration is the timed region / K to within the two ~10 µs state kernels.
     achieved = per_launch_bytes / (ms_step * 1e-3) / 1e9
@@ -457,6 +502,7 @@ def main():
         "vs_baseline": None, "dtype": {"fp32": "f32", "fp16": "f16", "bf16": "bf16"}[cfg.weights] + "-weights/f32-accum",
         "data": "synthetic",
         "config": {"workload": _workload_name(cfg), "voxels": N, "parallelism": "z-slab x%d" % world,
+                   "transport": transport if world > 1 else None,
                    "l2": "inputs larger than L2 (%.1f GB of weights streamed per step)" %
                          (info["weight_bytes"] * world / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -478,6 +524,8 @@ def main():
                          else (abs(m1 - m0) / abs(m0) if m0 else None)),
         "clocks": clk.summary(),
     }
+    if p2p_note:
+        line["config"]["transport_note"] = p2p_note
     tr = _ncu_traffic(cfg, per_launch_bytes) if (world == 1 and not dedup_storage) else None
     if tr:
         line["roofline"]["traffic"] = tr[0]

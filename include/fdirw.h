@@ -103,13 +103,20 @@ typedef struct {
 
 /* Slab decomposition (world > 1): rank r owns target planes [z_begin, z_end).
  * Slabs must tile [0, nz) in rank order and be at least R planes thick.
- * nccl_id: 128 bytes produced by fdirw_nccl_unique_id on rank 0 and broadcast
- * by the caller (e.g. torch.distributed).  world == 1 needs no id.  */
+ * transport FDIRW_TRANSPORT_NCCL: nccl_id = 128 bytes produced by fdirw_nccl_unique_id on
+ *   rank 0 and broadcast by the caller (e.g. torch.distributed); NULL = virtual ranks in
+ *   one process (fdirw_step_virtual).  world == 1 needs no id.
+ * transport FDIRW_TRANSPORT_P2P: no NCCL; the halo planes travel as peer-memory stores
+ *   fused into the superposition (csrc/p2p.cu), after fdirw_p2p_attach /
+ *   fdirw_p2p_attach_local.  Closed domain only (v_far == 0).                        */
+#define FDIRW_TRANSPORT_NCCL 0
+#define FDIRW_TRANSPORT_P2P 1
 typedef struct {
     int32_t rank, world;
     int32_t z_begin, z_end;
     int32_t device;         /* CUDA device ordinal the context lives on                      */
-    const void* nccl_id;    /* NULL when world == 1                                          */
+    const void* nccl_id;    /* NULL when world == 1 (or P2P transport)                       */
+    int32_t transport;      /* FDIRW_TRANSPORT_NCCL (0) or FDIRW_TRANSPORT_P2P (1)           */
 } fdirw_dist;
 
 typedef struct {
@@ -318,6 +325,28 @@ fdirw_status fdirw_coarse_far_get(fdirw_coarse* ctx, double* c_far_out, void* cu
 /* P_BC as stored (fp32 decoded to fp64) into pbc_host [N].  FDIRW_E_STATE if v_far == 0. */
 fdirw_status fdirw_coarse_export_pbc(const fdirw_coarse* ctx, double* pbc_host);
 void fdirw_coarse_destroy(fdirw_coarse* ctx);
+
+/* ---- a6 over NVLink peer memory (FDIRW_TRANSPORT_P2P) -----------------------------------
+ * north_star (d)'s halo exchange without a separate collective: the CTAs computing a
+ * rank's first / last R output planes store them straight into the neighbours' halo
+ * planes through peer pointers; a 64-bit epoch flag per side orders the steps.
+ * Bitwise equal to world == 1 for any slab decomposition (tested).
+ *
+ * fdirw_p2p_export: FDIRW_P2P_BLOB_BYTES bytes describing this context (geometry + CUDA IPC
+ *   handles of its two state buffers and its flags); the caller all-gathers the blobs.
+ * fdirw_p2p_attach: opens the neighbours' blobs (lo_blob of rank−1 or NULL on rank 0,
+ *   hi_blob of rank+1 or NULL on the last rank); peer access is enabled lazily.
+ *   FDIRW_E_INVALID if a blob's geometry or rank does not fit.  Synchronous.
+ * fdirw_p2p_attach_local: the same for n contexts of ONE process (rank order), e.g. on
+ *   one GPU for testing; each context then runs on its own stream, concurrently.
+ * fdirw_p2p_check: *timed_out = 1 if a wait for a neighbour exceeded 20 s (the wait
+ *   kernel then gives up instead of hanging the GPU; results are invalid).  Synchronous.
+ * With P2P, fdirw_mass returns this slab's sum only (the caller reduces).             */
+#define FDIRW_P2P_BLOB_BYTES 256
+fdirw_status fdirw_p2p_export(fdirw_ctx* ctx, void* blob_out);
+fdirw_status fdirw_p2p_attach(fdirw_ctx* ctx, const void* lo_blob, const void* hi_blob);
+fdirw_status fdirw_p2p_attach_local(fdirw_ctx* const* ctxs, int32_t n);
+fdirw_status fdirw_p2p_check(fdirw_ctx* ctx, int32_t* timed_out, void* cuda_stream);
 
 #ifdef __cplusplus
 }

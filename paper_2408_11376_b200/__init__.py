@@ -41,7 +41,10 @@ EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fd
            "fdirw_coarse_run", "fdirw_coarse_query", "fdirw_coarse_export", "fdirw_coarse_destroy",
            "fdirw_far_init", "fdirw_far_init_virtual", "fdirw_far_get", "fdirw_absorb_run",
            "fdirw_set_precision_mode", "fdirw_coarse_far_init", "fdirw_coarse_far_get",
-           "fdirw_coarse_export_pbc"]
+           "fdirw_coarse_export_pbc", "fdirw_p2p_export", "fdirw_p2p_attach", "fdirw_p2p_attach_local",
+           "fdirw_p2p_check"]
+TRANSPORTS = {"nccl": 0, "p2p": 1}
+P2P_BLOB_BYTES = 256
 
 
 class fdirw_params(ctypes.Structure):
@@ -53,7 +56,8 @@ class fdirw_params(ctypes.Structure):
 
 class fdirw_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("z_begin", ctypes.c_int32),
-                ("z_end", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+                ("z_end", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("transport", ctypes.c_int32)]
 
 
 class fdirw_info(ctypes.Structure):
@@ -134,6 +138,14 @@ _lib.fdirw_far_init_virtual.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32, cty
 _lib.fdirw_far_init_virtual.restype = _st
 _lib.fdirw_far_get.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), _vp]
 _lib.fdirw_far_get.restype = _st
+_lib.fdirw_p2p_export.argtypes = [_vp, _vp]
+_lib.fdirw_p2p_export.restype = _st
+_lib.fdirw_p2p_attach.argtypes = [_vp, _vp, _vp]
+_lib.fdirw_p2p_attach.restype = _st
+_lib.fdirw_p2p_attach_local.argtypes = [ctypes.POINTER(_vp), ctypes.c_int32]
+_lib.fdirw_p2p_attach_local.restype = _st
+_lib.fdirw_p2p_check.argtypes = [_vp, ctypes.POINTER(ctypes.c_int32), _vp]
+_lib.fdirw_p2p_check.restype = _st
 
 
 class fdirw_absorb_params(ctypes.Structure):
@@ -236,8 +248,11 @@ def nccl_unique_id() -> bytes:
 
 def build_kernels(params: Params, phase: np.ndarray, rank: int = 0, world: int = 1, z_begin: int | None = None,
                   z_end: int | None = None, device: int | None = None, nccl_id: bytes | None = None,
-                  stream=None) -> Context:
-    """fdirw_build_kernels: phase = WHOLE-grid uint8 mask [nz][ny][nx] (host), 1 = fast."""
+                  stream=None, transport: str = "nccl") -> Context:
+    """fdirw_build_kernels: phase = WHOLE-grid uint8 mask [nz][ny][nx] (host), 1 = fast.
+    transport: "nccl" (halo via NCCL send/recv; nccl_id None + world > 1 = virtual ranks) or
+    "p2p" (halo planes stored into the neighbours' memory by the superposition; attach with
+    p2p_attach / p2p_attach_local before stepping)."""
     phase = np.ascontiguousarray(phase, dtype=np.uint8)
     if phase.shape != (params.nz, params.ny, params.nx):
         raise ValueError("phase shape %s != (nz, ny, nx)" % (phase.shape,))
@@ -252,12 +267,38 @@ def build_kernels(params: Params, phase: np.ndarray, rank: int = 0, world: int =
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(nccl_id, 128)
         dist = fdirw_dist(rank, world, 0 if z_begin is None else z_begin, params.nz if z_end is None else z_end,
-                          device, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None)
+                          device, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
+                          TRANSPORTS[transport])
     h = ctypes.c_void_p()
     _check(_lib.fdirw_build_kernels(ctypes.byref(p), phase.ctypes.data_as(ctypes.c_void_p),
                                     ctypes.byref(dist) if dist is not None else None, _stream(stream),
                                     ctypes.byref(h)))
     return Context(h.value, params)
+
+
+def p2p_export(ctx: Context) -> bytes:
+    """fdirw_p2p_export → the 256-byte blob (geometry + CUDA IPC handles) to all-gather."""
+    buf = ctypes.create_string_buffer(P2P_BLOB_BYTES)
+    _check(_lib.fdirw_p2p_export(ctx.handle, buf))
+    return buf.raw
+
+
+def p2p_attach(ctx: Context, lo_blob: bytes | None, hi_blob: bytes | None):
+    lo = ctypes.create_string_buffer(lo_blob, P2P_BLOB_BYTES) if lo_blob is not None else None
+    hi = ctypes.create_string_buffer(hi_blob, P2P_BLOB_BYTES) if hi_blob is not None else None
+    _check(_lib.fdirw_p2p_attach(ctx.handle, lo, hi))
+
+
+def p2p_attach_local(ctxs):
+    H = (_vp * len(ctxs))(*[c.handle.value for c in ctxs])
+    _check(_lib.fdirw_p2p_attach_local(H, len(ctxs)))
+
+
+def p2p_check(ctx: Context, stream=None) -> bool:
+    """True if a neighbour wait timed out (results invalid)."""
+    t = ctypes.c_int32(0)
+    _check(_lib.fdirw_p2p_check(ctx.handle, ctypes.byref(t), _stream(stream)))
+    return bool(t.value)
 
 
 def step(ctx: Context, c_in, c_out, stream=None):

@@ -53,6 +53,16 @@ struct fdirw_ctx {
     double* kin_rec = nullptr;
     int kin_cap = 0;
     double n_solid = 0;
+    // a6 over peer memory (FDIRW_TRANSPORT_P2P)
+    int transport = FDIRW_TRANSPORT_NCCL;
+    unsigned long long* p2p_flags = nullptr;   // [4]: from lo, from hi, own epoch, timed out
+    float* peer_lo[2] = {nullptr, nullptr};    // the neighbours' padded state buffers
+    float* peer_hi[2] = {nullptr, nullptr};
+    unsigned long long* peer_lo_flag = nullptr;  // lo neighbour's flags[1]
+    unsigned long long* peer_hi_flag = nullptr;  // hi neighbour's flags[0]
+    int nzl_lo = 0;
+    bool p2p_ready = false;
+    std::vector<void*> ipc_opened;
 };
 
 static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s);
@@ -186,6 +196,10 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (dist) {
         if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
             return fail(FDIRW_E_INVALID, "bad rank/world");
+        if (dist->transport != FDIRW_TRANSPORT_NCCL && dist->transport != FDIRW_TRANSPORT_P2P)
+            return fail(FDIRW_E_INVALID, "transport must be FDIRW_TRANSPORT_NCCL or FDIRW_TRANSPORT_P2P");
+        if (dist->transport == FDIRW_TRANSPORT_P2P && p->v_far > 0)
+            return fail(FDIRW_E_INVALID, "FDIRW_TRANSPORT_P2P supports the closed domain only (v_far == 0)");
         if (dist->z_begin < 0 || dist->z_end > p->nz || dist->z_begin >= dist->z_end)
             return fail(FDIRW_E_INVALID, "bad slab [z_begin, z_end)");
         if (dist->world == 1 && (dist->z_begin != 0 || dist->z_end != p->nz))
@@ -208,6 +222,8 @@ static void free_ctx(fdirw_ctx* c)
     cudaDeviceSynchronize();
     if (c->graph2) cudaGraphExecDestroy(c->graph2);
     if (c->comm) nccl_comm_destroy(c->nccl, c->comm);
+    for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    cudaFree(c->p2p_flags);
     cudaFree(c->Wt);
     cudaFree(c->diag);
     cudaFree(c->cpad[0]);
@@ -285,7 +301,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         c->device = dist->device;
         z0 = dist->z_begin;
         z1 = dist->z_end;
-        c->is_virtual = dist->world > 1 && dist->nccl_id == nullptr;
+        c->transport = dist->transport;
+        c->is_virtual = dist->world > 1 && dist->nccl_id == nullptr && dist->transport == FDIRW_TRANSPORT_NCCL;
         if (cudaSetDevice(c->device) != cudaSuccess) {
             delete c;
             return fail(FDIRW_E_INVALID, "cudaSetDevice failed for dist->device");
@@ -457,7 +474,10 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     BAIL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     BAIL_CUDA(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
 
-    if (c->world > 1 && !c->is_virtual) {
+    if (c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) {
+        if ((st = alloc((void**)&c->p2p_flags, 32, "p2p flags")) != FDIRW_OK) return bail(st);
+        BAIL_CUDA(cudaMemset(c->p2p_flags, 0, 32));
+    } else if (c->world > 1 && !c->is_virtual) {
         std::string err;
         c->nccl = nccl_load(&err);
         if (!c->nccl) { g_err = err; return bail(FDIRW_E_NCCL); }
@@ -482,7 +502,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
 // Superpose tiles [t0, t1) of `src` (padded) into `out` with strides (ps, rs).  With a far
 // field (N2) and far_terms: + p_BC·c_far and the per-tile Σ C_new for Eq.7.
 static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps, long rs, int t0, int t1,
-                             cudaStream_t s, bool far_terms = true)
+                             cudaStream_t s, bool far_terms = true, int push_parity = -1)
 {
     const Geometry& g = c->g;
     SuperArgs a{};
@@ -502,6 +522,13 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
         a.pbc = c->pbc;
         a.far_state = c->far_state;
         a.tile_sum = c->tile_buf + 1;
+    }
+    if (push_parity >= 0) {  // a6 over peer memory: boundary planes also into the neighbours' halos
+        const long pe = (long)g.plane_elems, row0 = (long)g.R * g.nxp + kPadX;
+        if (c->peer_lo[push_parity]) a.push_lo = c->peer_lo[push_parity] + (long)(c->nzl_lo + g.R) * pe + row0;
+        if (c->peer_hi[push_parity]) a.push_hi = c->peer_hi[push_parity] + row0;
+        a.nzl = g.nzl;
+        a.pR = g.R;
     }
     return launch_superpose(a, g.R, c->fmt, s);
 }
@@ -599,9 +626,26 @@ static void split_tiles(const Geometry& g, int* int0, int* int1)
 }
 
 // One step src (padded, slab planes filled) → out; exchanges the halo planes of src first.
-static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, long rs, cudaStream_t s)
+static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, long rs, cudaStream_t s,
+                                 int dst_parity = 1)
 {
     const Geometry& g = c->g;
+    if (c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) {
+        // interior tiles (no halo reads) → wait for the neighbours' previous step → boundary
+        // tiles, whose edge planes are stored into the neighbours' halos → signal
+        int i0, i1;
+        split_tiles(g, &i0, &i1);
+        CUDA_TRY(superpose(c, src, out, ps, rs, i0, i1, s));
+        CUDA_TRY(p2p_wait(c->p2p_flags, c->peer_lo_flag != nullptr, c->peer_hi_flag != nullptr, s));
+        if (i1 > i0) {
+            CUDA_TRY(superpose(c, src, out, ps, rs, 0, i0, s, true, dst_parity));
+            CUDA_TRY(superpose(c, src, out, ps, rs, i1, g.n_tiles, s, true, dst_parity));
+        } else {
+            CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity));
+        }
+        CUDA_TRY(p2p_signal(c->p2p_flags, c->peer_lo_flag, c->peer_hi_flag, s));
+        return FDIRW_OK;
+    }
     if (c->world == 1 && c->prec_mode != 0) {  // N3 §3.3 study modes: padded output only
         StudyArgs a{src, out - ((size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX), c->Wt, c->diag,
                     g.nx, g.ny, g.nzl, g.nxq, g.tile, g.tpp, g.nxp, g.nyp, g.R, c->pbc, c->far_state};
@@ -649,6 +693,19 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
 }
 
+// P2P run start (after the pack into cpad[0]): signal "packed", wait for the neighbours'
+// (so nobody still reads the halo of cpad[0]), push our edge planes into their halos, signal.
+static fdirw_status p2p_start(fdirw_ctx* c, cudaStream_t s)
+{
+    if (!c->p2p_ready) return fail(FDIRW_E_STATE, "P2P transport: call fdirw_p2p_attach first");
+    const bool lo = c->peer_lo_flag != nullptr, hi = c->peer_hi_flag != nullptr;
+    CUDA_TRY(p2p_signal(c->p2p_flags, c->peer_lo_flag, c->peer_hi_flag, s));
+    CUDA_TRY(p2p_wait(c->p2p_flags, lo, hi, s));
+    CUDA_TRY(p2p_push_planes(c->g, c->cpad[0], c->peer_lo[0], c->nzl_lo, c->peer_hi[0], s));
+    CUDA_TRY(p2p_signal(c->p2p_flags, c->peer_lo_flag, c->peer_hi_flag, s));
+    return FDIRW_OK;
+}
+
 static float* pad_interior(fdirw_ctx* c, int i)
 {
     const Geometry& g = c->g;
@@ -664,7 +721,35 @@ extern "C" fdirw_status fdirw_step(fdirw_ctx* c, const float* c_in, float* c_out
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const Geometry& g = c->g;
     CUDA_TRY(launch_pack(c_in, c->cpad[0], g, s, c->farmask));
-    return enqueue_step(c, c->cpad[0], c_out, (long)g.nx * g.ny, g.nx, s);
+    if (c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) {
+        fdirw_status st = p2p_start(c, s);
+        if (st != FDIRW_OK) return st;
+    }
+    return enqueue_step(c, c->cpad[0], c_out, (long)g.nx * g.ny, g.nx, s, 1);
+}
+
+// capture step(0→1); step(1→0) once; fdirw_run replays it n/2 times.  With P2P this is done
+// at attach time: instantiating a graph can wait for the device, which must not happen while
+// a neighbour's step spins on this context's flags.
+static fdirw_status capture_graph2(fdirw_ctx* c)
+{
+    const Geometry& g = c->g;
+    if (c->transport == FDIRW_TRANSPORT_P2P) CUDA_TRY(p2p_preload());
+    const long ps = (long)g.plane_elems, rs = g.nxp;
+    cudaStream_t cs = c->capture_stream;
+    CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    fdirw_status st = enqueue_step(c, c->cpad[0], pad_interior(c, 1), ps, rs, cs, 1);
+    if (st == FDIRW_OK) st = enqueue_step(c, c->cpad[1], pad_interior(c, 0), ps, rs, cs, 0);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    if (st != FDIRW_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+    if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&c->graph2, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) { c->graph2 = nullptr; return fail(FDIRW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)); }
+    CUDA_TRY(cudaGraphUpload(c->graph2, c->capture_stream));
+    CUDA_TRY(cudaStreamSynchronize(c->capture_stream));
+    return FDIRW_OK;
 }
 
 extern "C" fdirw_status fdirw_run(fdirw_ctx* c, float* c_dev, int32_t n_steps, void* cuda_stream)
@@ -677,25 +762,19 @@ extern "C" fdirw_status fdirw_run(fdirw_ctx* c, float* c_dev, int32_t n_steps, v
     const Geometry& g = c->g;
     if (n_steps == 0) return FDIRW_OK;
     CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s, c->farmask));
+    if (c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) {
+        fdirw_status st = p2p_start(c, s);
+        if (st != FDIRW_OK) return st;
+    }
     const long ps = (long)g.plane_elems, rs = g.nxp;
     if (n_steps >= 2 && !c->graph2) {
-        // capture step(0→1); step(1→0) once; replay it n/2 times
-        cudaStream_t cs = c->capture_stream;
-        CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        fdirw_status st = enqueue_step(c, c->cpad[0], pad_interior(c, 1), ps, rs, cs);
-        if (st == FDIRW_OK) st = enqueue_step(c, c->cpad[1], pad_interior(c, 0), ps, rs, cs);
-        cudaGraph_t graph = nullptr;
-        cudaError_t e = cudaStreamEndCapture(cs, &graph);
-        if (st != FDIRW_OK) { if (graph) cudaGraphDestroy(graph); return st; }
-        if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-        e = cudaGraphInstantiate(&c->graph2, graph, 0);
-        cudaGraphDestroy(graph);
-        if (e != cudaSuccess) { c->graph2 = nullptr; return fail(FDIRW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)); }
+        fdirw_status st = capture_graph2(c);
+        if (st != FDIRW_OK) return st;
     }
     for (int i = 0; i < n_steps / 2; ++i) CUDA_TRY(cudaGraphLaunch(c->graph2, s));
     int fin = 0;
     if (n_steps & 1) {
-        fdirw_status st = enqueue_step(c, c->cpad[0], pad_interior(c, 1), ps, rs, s);
+        fdirw_status st = enqueue_step(c, c->cpad[0], pad_interior(c, 1), ps, rs, s, 1);
         if (st != FDIRW_OK) return st;
         fin = 1;
     }
@@ -710,7 +789,7 @@ extern "C" fdirw_status fdirw_mass(fdirw_ctx* c, const float* c_dev, double* out
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const size_t n = (size_t)c->g.nx * c->g.ny * c->g.nzl;
     CUDA_TRY(launch_mass(c_dev, n, c->mass_partial, c->mass_blocks, c->mass_out, s));
-    if (c->world > 1 && !c->is_virtual) {
+    if (c->world > 1 && !c->is_virtual && c->transport == FDIRW_TRANSPORT_NCCL) {
         std::string err;
         if (nccl_allreduce_sum_f64(c->nccl, c->comm, c->mass_out, s, &err)) return fail(FDIRW_E_NCCL, err);
     }
@@ -1020,5 +1099,124 @@ extern "C" fdirw_status fdirw_far_get(fdirw_ctx* c, double* c_far_out, void* cud
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     CUDA_TRY(cudaMemcpyAsync(c_far_out, c->far_state, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    return FDIRW_OK;
+}
+
+// ---- a6 over peer memory: attach -----------------------------------------------------------
+namespace {
+struct P2PBlob {
+    uint32_t magic;
+    int32_t rank, world, nx, ny, R, nzl, device;
+    cudaIpcMemHandle_t cpad[2];
+    cudaIpcMemHandle_t flags;
+};
+static_assert(sizeof(P2PBlob) <= FDIRW_P2P_BLOB_BYTES, "blob");
+constexpr uint32_t kBlobMagic = 0xFD1B2B01u;
+}  // namespace
+
+extern "C" fdirw_status fdirw_p2p_export(fdirw_ctx* c, void* blob_out)
+{
+    if (!c || !blob_out) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (c->transport != FDIRW_TRANSPORT_P2P || c->world < 2) return fail(FDIRW_E_STATE, "not a P2P context with world > 1");
+    CUDA_TRY(cudaSetDevice(c->device));
+    P2PBlob b{};
+    b.magic = kBlobMagic;
+    b.rank = c->rank; b.world = c->world; b.nx = c->g.nx; b.ny = c->g.ny; b.R = c->g.R; b.nzl = c->g.nzl;
+    b.device = c->device;
+    CUDA_TRY(cudaIpcGetMemHandle(&b.cpad[0], c->cpad[0]));
+    CUDA_TRY(cudaIpcGetMemHandle(&b.cpad[1], c->cpad[1]));
+    CUDA_TRY(cudaIpcGetMemHandle(&b.flags, c->p2p_flags));
+    memset(blob_out, 0, FDIRW_P2P_BLOB_BYTES);
+    memcpy(blob_out, &b, sizeof b);
+    return FDIRW_OK;
+}
+
+static fdirw_status p2p_check_blob(const fdirw_ctx* c, const P2PBlob& b, int want_rank)
+{
+    if (b.magic != kBlobMagic) return fail(FDIRW_E_INVALID, "not an fdirw P2P blob");
+    if (b.rank != want_rank || b.world != c->world) return fail(FDIRW_E_INVALID, "P2P blob from the wrong rank/world");
+    if (b.nx != c->g.nx || b.ny != c->g.ny || b.R != c->g.R) return fail(FDIRW_E_INVALID, "P2P blob geometry mismatch");
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_p2p_attach(fdirw_ctx* c, const void* lo_blob, const void* hi_blob)
+{
+    if (!c) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (c->transport != FDIRW_TRANSPORT_P2P || c->world < 2) return fail(FDIRW_E_STATE, "not a P2P context with world > 1");
+    if ((c->rank > 0) != (lo_blob != nullptr) || (c->rank < c->world - 1) != (hi_blob != nullptr))
+        return fail(FDIRW_E_INVALID, "need lo_blob iff rank > 0 and hi_blob iff rank < world-1");
+    CUDA_TRY(cudaSetDevice(c->device));
+    for (int side = 0; side < 2; ++side) {
+        const void* blob = side == 0 ? lo_blob : hi_blob;
+        if (!blob) continue;
+        P2PBlob b;
+        memcpy(&b, blob, sizeof b);
+        fdirw_status st = p2p_check_blob(c, b, c->rank + (side == 0 ? -1 : 1));
+        if (st != FDIRW_OK) return st;
+        void* q[3];
+        const cudaIpcMemHandle_t hs[3] = {b.cpad[0], b.cpad[1], b.flags};
+        for (int i = 0; i < 3; ++i) {
+            CUDA_TRY(cudaIpcOpenMemHandle(&q[i], hs[i], cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(q[i]);
+        }
+        if (side == 0) {
+            c->peer_lo[0] = (float*)q[0];
+            c->peer_lo[1] = (float*)q[1];
+            c->peer_lo_flag = (unsigned long long*)q[2] + 1;  // we are its hi neighbour
+            c->nzl_lo = b.nzl;
+        } else {
+            c->peer_hi[0] = (float*)q[0];
+            c->peer_hi[1] = (float*)q[1];
+            c->peer_hi_flag = (unsigned long long*)q[2] + 0;  // we are its lo neighbour
+        }
+    }
+    c->p2p_ready = true;
+    return capture_graph2(c);
+}
+
+extern "C" fdirw_status fdirw_p2p_attach_local(fdirw_ctx* const* ctxs, int32_t n)
+{
+    if (!ctxs || n < 2) return fail(FDIRW_E_INVALID, "need >= 2 contexts");
+    for (int r = 0; r < n; ++r) {
+        fdirw_ctx* c = ctxs[r];
+        if (!c || c->transport != FDIRW_TRANSPORT_P2P || c->world != n || c->rank != r)
+            return fail(FDIRW_E_INVALID, "contexts must be P2P ranks 0..n-1 of one world, in order");
+        if (c->g.nx != ctxs[0]->g.nx || c->g.ny != ctxs[0]->g.ny || c->g.R != ctxs[0]->g.R)
+            return fail(FDIRW_E_INVALID, "geometry mismatch");
+    }
+    for (int r = 0; r < n; ++r) {
+        fdirw_ctx* c = ctxs[r];
+        if (r > 0) {
+            c->peer_lo[0] = ctxs[r - 1]->cpad[0];
+            c->peer_lo[1] = ctxs[r - 1]->cpad[1];
+            c->peer_lo_flag = ctxs[r - 1]->p2p_flags + 1;
+            c->nzl_lo = ctxs[r - 1]->g.nzl;
+        }
+        if (r < n - 1) {
+            c->peer_hi[0] = ctxs[r + 1]->cpad[0];
+            c->peer_hi[1] = ctxs[r + 1]->cpad[1];
+            c->peer_hi_flag = ctxs[r + 1]->p2p_flags + 0;
+        }
+        c->p2p_ready = true;
+    }
+    for (int r = 0; r < n; ++r) {
+        CUDA_TRY(cudaSetDevice(ctxs[r]->device));
+        fdirw_status st = capture_graph2(ctxs[r]);
+        if (st != FDIRW_OK) return st;
+    }
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_p2p_check(fdirw_ctx* c, int32_t* timed_out, void* cuda_stream)
+{
+    if (!c || !timed_out) return fail(FDIRW_E_INVALID, "NULL argument");
+    *timed_out = 0;
+    if (!c->p2p_flags) return FDIRW_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    unsigned long long f[4];
+    CUDA_TRY(cudaMemcpyAsync(f, c->p2p_flags, 32, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *timed_out = f[3] ? 1 : 0;
     return FDIRW_OK;
 }

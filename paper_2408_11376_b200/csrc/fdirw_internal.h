@@ -72,6 +72,14 @@ struct KgenArgs {
 };
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s);
 
+// ---- a6 over peer memory (p2p.cu) -------------------------------------------------
+cudaError_t p2p_preload();  // loads every kernel a P2P step launches (lazy loading can wait for the device)
+cudaError_t p2p_wait(unsigned long long* flags, bool has_lo, bool has_hi, cudaStream_t s);
+cudaError_t p2p_signal(unsigned long long* flags, unsigned long long* peer_lo_flag, unsigned long long* peer_hi_flag,
+                       cudaStream_t s);
+cudaError_t p2p_push_planes(const Geometry& g, const float* cpad, float* peer_lo, int nzl_lo, float* peer_hi,
+                            cudaStream_t s);
+
 // ---- window de-duplication (dedup.cu) -------------------------------------------
 struct DedupArgs {
     const uint8_t* mask;
@@ -119,6 +127,13 @@ struct SuperArgs {
     // replicated class kernels uk8[u][slot][8]
     const int* list = nullptr;  // compacted chunk ids (orig tile·tile + e); tiles index the list
     long n_list = 0;
+    // a6 over peer memory (FDIRW_TRANSPORT_P2P): targets in the first / last R slab planes are
+    // also stored into the lo / hi neighbour's padded state (their next-step halo planes).
+    // push_lo → the lo neighbour's padded plane (nzl_lo + R), row R, x offset kPadX;
+    // push_hi → the hi neighbour's padded plane 0, row R, x offset kPadX
+    float* push_lo = nullptr;
+    float* push_hi = nullptr;
+    int nzl = 0, pR = 0;
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
 

@@ -337,6 +337,26 @@ __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
             for (int j = 0; j < 8; ++j)
                 if (x + j < a.nx) out[j] = acc[j];
         }
+        // a6 over peer memory: the first / last R planes also go straight into the
+        // neighbours' halo planes (P2P stores over NVLink), fenced before the step's signal
+        float* pd[2] = {nullptr, nullptr};
+        if (a.push_lo && zl < a.pR) pd[0] = a.push_lo + (long)zl * plane + (long)y * nxp + x;
+        if (a.push_hi && zl >= a.nzl - a.pR) pd[1] = a.push_hi + (long)(zl - (a.nzl - a.pR)) * plane + (long)y * nxp + x;
+        if (pd[0] || pd[1]) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!pd[h]) continue;
+                if (x + 8 <= a.nx) {
+                    reinterpret_cast<float4*>(pd[h])[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                    reinterpret_cast<float4*>(pd[h])[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (x + j < a.nx) pd[h][j] = acc[j];
+                }
+            }
+            __threadfence_system();
+        }
     }
     if (a.tile_sum) {  // N2: this tile's Σ C_new (fp64, fixed order) for Eq.7
         double s = 0.0;
@@ -593,6 +613,17 @@ cudaError_t launch_unpack(const float* cpad, float* c, const Geometry& g, cudaSt
     if (n == 0) return cudaSuccess;
     unpack_kernel<<<grid_for(n, 256), 256, 0, s>>>(cpad, c, g.nx, g.ny, n, g.R, g.nxp, g.nyp);
     return cudaGetLastError();
+}
+
+// CUDA 12 loads kernels lazily at their first launch, and loading can wait for the device.
+// Steps whose kernels spin on a neighbour's flags (P2P transport, several contexts on one
+// device) must not trigger a load mid-run: load the step's kernels up front.
+cudaError_t preload_step_kernels()
+{
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, pack_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, unpack_kernel);
+    return e;
 }
 
 // fp64 sum, two passes with a fixed order (deterministic).

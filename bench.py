@@ -225,6 +225,25 @@ def _variant_n4(fd, torch, params, mask, c_host, args, stream, peak):
             "note": "uniform chunks read a shared class kernel (smem) instead of streaming; bitwise = dense"}
 
 
+def _kgen_line(t_kgen, cells_algo, info, cfg, world):
+    """kgen (one-time build, a3+a4).  Algorithmic work = every source's window (dedup counts
+    each source); the ALU roofline counts what was computed: distinct windows × K × n_fd
+    cell-updates, each 12 FP32 lane-ops (6 face differences + 6 FMAs), against
+    148 SMs × 128 FP32 lanes × max SM clock (MEASURED_PEAKS sm_max_mhz)."""
+    p = _peaks() or {}
+    mhz = float(p.get("sm_max_mhz", 1965.0))
+    peak_cells = 148 * 128 * mhz * 1e6 / 12
+    computed = info["kgen_windows"] * world * cfg.K * info["n_fd"]
+    ach = computed / t_kgen
+    return {"seconds": t_kgen, "window_cell_updates": cells_algo, "cell_updates_per_s": cells_algo / t_kgen,
+            "n_fd": info["n_fd"], "windows_computed": info["kgen_windows"] * world,
+            "sources": info["kgen_sources"] * world,
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak_cells, "unit": "cell-updates/s",
+                         "frac": ach / peak_cells,
+                         "note": "computed windows only; peak = 148*128 FP32 lanes * %.0f MHz / 12 lane-ops "
+                                 "per cell-update (time includes dedup + expand)" % mhz}}
+
+
 def _coarse_roofline(info, ms):
     """Whole coarse step against HBM: algorithmic bytes = stored P̃ (+diag, P_BC) once, plus the
     Ω_L field read by the map and written by the remap (8 B per Ω_L voxel).  P̃ fits in L2 and
@@ -372,18 +391,41 @@ def main():
     transport = args.transport if (world > 1 and cfg.v_far == 0) else "nccl"  # P2P: closed domain only
 
     def build(tr):
-        cx = fd.build_kernels(params, mask, rank=rank, world=world, z_begin=z0, z_end=z1, device=local,
-                              nccl_id=nccl_id if tr == "nccl" else None, stream=stream, transport=tr)
-        if tr == "p2p":  # all-gather the CUDA IPC blobs, open the neighbours' buffers
-            blobs = [None] * world
-            dist.all_gather_object(blobs, fd.p2p_export(cx))
-            fd.p2p_attach(cx, blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank < world - 1 else None)
+        if tr == "nccl":
+            return fd.build_kernels(params, mask, rank=rank, world=world, z_begin=z0, z_end=z1, device=local,
+                                    nccl_id=nccl_id, stream=stream, transport=tr)
+        # P2P: build, all-gather the CUDA IPC blobs, open the neighbours' buffers.  Every stage
+        # agrees across ranks before the next collective, so a failure anywhere falls back to
+        # NCCL on all ranks instead of leaving some of them blocked.
+        cx, blob, err = None, None, None
+        try:
+            cx = fd.build_kernels(params, mask, rank=rank, world=world, z_begin=z0, z_end=z1, device=local,
+                                  stream=stream, transport=tr)
+            blob = fd.p2p_export(cx)
+        except fd.FdirwError as e:
+            err = str(e)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        if all(b is not None for b in blobs):
+            try:
+                fd.p2p_attach(cx, blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank < world - 1 else None)
+            except fd.FdirwError as e:
+                err = str(e)
+        if allreduce(1.0 if err or any(b is None for b in blobs) else 0.0, dist.ReduceOp.MAX) > 0:
+            if cx is not None:
+                fd.destroy(cx)
             barrier()
+            return None
+        barrier()
         return cx
 
     torch.cuda.synchronize()
     t = time.perf_counter()
     ctx = build(transport)
+    p2p_note = None
+    if ctx is None:
+        transport, p2p_note = "nccl", "P2P setup failed on some rank; fell back to NCCL"
+        ctx = build(transport)
     t_kgen = time.perf_counter() - t
     info = ctx.info
 
@@ -402,7 +444,6 @@ def main():
     m0 = gmass(c)
     fd.run(ctx, c, args.warmup)
     torch.cuda.synchronize()
-    p2p_note = None
     if transport == "p2p":  # a wait that timed out (never expected) → rebuild on NCCL
         if allreduce(1.0 if fd.p2p_check(ctx) else 0.0, dist.ReduceOp.MAX) > 0:
             fd.destroy(ctx)
@@ -518,8 +559,7 @@ def main():
         "paper_run": {"steps": 1000, "physical_time_s": 1000 * cfg.dt if cfg.dh != 1.0 else None,
                       "seconds_incl_kgen": t_kgen + 1000 * ms_step * 1e-3,
                       "note": "t = 0.5 s of Fig.7 (1000 macro steps) incl. the one-time kernel build"},
-        "kgen": {"seconds": t_kgen, "window_cell_updates": kgen_cells * world,
-                 "cell_updates_per_s": kgen_cells * world / t_kgen, "n_fd": info["n_fd"]},
+        "kgen": _kgen_line(t_kgen, kgen_cells * world, info, cfg, world),
         "mass_rel_err": (abs(m1 + cf1 * cfg.v_far - total0) / total0 if far
                          else (abs(m1 - m0) / abs(m0) if m0 else None)),
         "clocks": clk.summary(),

@@ -234,6 +234,8 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
     mhz = float(p.get("sm_max_mhz", 1965.0))
     peak_cells = 148 * 128 * mhz * 1e6 / 12
     computed = info["kgen_windows"] * world * cfg.K * info["n_fd"]
+    L = 2 * cfg.R + 1
+    lp = (L + 3) // 4 * 4
     ach = computed / t_kgen
     return {"seconds": t_kgen, "window_cell_updates": cells_algo, "cell_updates_per_s": cells_algo / t_kgen,
             "n_fd": info["n_fd"], "windows_computed": info["kgen_windows"] * world,
@@ -241,7 +243,12 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
             "roofline": {"bound": "alu", "achieved": ach, "peak": peak_cells, "unit": "cell-updates/s",
                          "frac": ach / peak_cells,
                          "note": "computed windows only; peak = 148*128 FP32 lanes * %.0f MHz / 12 lane-ops "
-                                 "per cell-update (time includes dedup + expand)" % mhz}}
+                                 "per cell-update (time includes dedup + expand)" % mhz},
+            # the binding resource of kgen v2: shared memory (4 lateral neighbour reads + 1 write of
+            # 4 B per cell-update, z columns padded from L to Lp), 128 B/clk/SM
+            "smem": {"achieved_TBps": ach * 20.0 * lp / L / 1e12, "peak_TBps": 148 * 128 * mhz * 1e6 / 1e12,
+                     "frac": (ach * 20.0 * lp / L) / (148 * 128 * mhz * 1e6),
+                     "bytes_per_cell_update": 20.0 * lp / L}}
 
 
 def _coarse_roofline(info, ms):

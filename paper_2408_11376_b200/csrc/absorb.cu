@@ -209,9 +209,19 @@ __global__ void superpose_study_kernel(const StudyArgs a)
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         const int x = (int)(i % a.nx), y = (int)((i / a.nx) % a.ny), zl = (int)(i / ((long)a.nx * a.ny));
         const int q = y * a.nxq + (x >> 3);
-        const size_t tile = (size_t)zl * a.tpp + q / a.tile;
-        const int e = q % a.tile, j = x & 7;
+        size_t tile = (size_t)zl * a.tpp + q / a.tile;
+        int e = q % a.tile;
+        const int j = x & 7;
         const long p = pidx(x, y, zl, R, a.nxp, a.nyp);
+        if (a.chunk_pos) {  // N2 compaction: all-far chunks have no weights (their targets hold 0)
+            const int cp = a.chunk_pos[tile * a.tile + e];
+            if (cp < 0) {
+                a.out[p] = 0.f;
+                continue;
+            }
+            tile = cp / a.tile;
+            e = cp % a.tile;
+        }
         const WT* wt = reinterpret_cast<const WT*>(a.Wt);
         float acc32 = 0.f;
         __half acc16 = __float2half_rn(0.f);

@@ -45,6 +45,11 @@ struct fdirw_ctx {
     double* gathered = nullptr;   // [world · tile_stride] (NCCL all-gather target)
     double* far_state = nullptr;  // {c_far, M0}
     long tile_stride = 0;
+    // N2, world == 1: chunks whose 8 targets are all far-field voxels get no gather weights;
+    // Wt / diag / p_BC hold the other chunks compacted (ut.dense_list), chunk_pos maps a
+    // chunk (tile·tile + e) to its compact position or −1
+    bool compact = false;
+    int* chunk_pos = nullptr;
     // N3 integrated loop / precision modes (world == 1)
     int prec_mode = 0;            // 0 = default kernel; 1/2/3 = §3.3 study modes (absorb.cu)
     uint8_t* phase_pp = nullptr;  // padded phase map (255 outside)
@@ -235,6 +240,7 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->tile_buf);
     cudaFree(c->gathered);
     cudaFree(c->far_state);
+    cudaFree(c->chunk_pos);
     cudaFree(c->phase_pp);
     cudaFree(c->alpha);
     cudaFree(c->kin_part);
@@ -274,6 +280,37 @@ extern "C" fdirw_status fdirw_nccl_unique_id(void* out128)
     Nccl* n = nccl_load(&err);
     if (!n) return fail(FDIRW_E_NCCL, err);
     if (nccl_unique_id(n, out128, &err)) return fail(FDIRW_E_NCCL, err);
+    return FDIRW_OK;
+}
+
+// N2 (world == 1): list the chunks (tile·tile + e, ascending) holding at least one non-far
+// target; the rest carry no weights.  Fills c->ut.{dense_list, n_dense, nd_tiles}, chunk_pos.
+static fdirw_status far_compact(fdirw_ctx* c, const uint8_t* phase_host, cudaStream_t s)
+{
+    const Geometry& g = c->g;
+    const size_t nch = (size_t)g.n_tiles * g.tile;
+    std::vector<int> pos(nch, -1), list;
+    list.reserve(nch);
+    for (int zl = 0; zl < g.nzl; ++zl)
+        for (int q = 0; q < g.ny * g.nxq; ++q) {
+            const int y = q / g.nxq, x0 = (q % g.nxq) * 8;
+            const uint8_t* row = phase_host + ((size_t)(g.z0 + zl) * g.ny + y) * g.nx;
+            bool any = false;
+            for (int j = 0; j < 8 && x0 + j < g.nx; ++j) any |= row[x0 + j] != 2;
+            if (!any) continue;
+            const int ch = (zl * g.tpp + q / g.tile) * g.tile + q % g.tile;
+            pos[ch] = (int)list.size();
+            list.push_back(ch);
+        }
+    fdirw_status st;
+    if ((st = alloc((void**)&c->ut.dense_list, (list.size() + 1) * 4, "far compaction list")) != FDIRW_OK) return st;
+    if ((st = alloc((void**)&c->chunk_pos, nch * 4, "far compaction map")) != FDIRW_OK) return st;
+    if (!list.empty()) CUDA_TRY(cudaMemcpyAsync(c->ut.dense_list, list.data(), list.size() * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->chunk_pos, pos.data(), nch * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->ut.n_dense = (long)list.size();
+    c->ut.nd_tiles = (int)((list.size() + g.tile - 1) / g.tile);
+    c->compact = true;
     return FDIRW_OK;
 }
 
@@ -402,6 +439,14 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                 ea.n_tiles = c->ut.nd_tiles;
                 w_elems = (size_t)c->ut.nd_tiles * (g.K - 1) * g.tile * kChunk;
                 d_elems = (size_t)c->ut.nd_tiles * g.tile * kChunk;
+            } else if (e == cudaSuccess && params->v_far > 0 && c->world == 1) {
+                // N2: all-far chunks (no targets) get no gather weights either
+                if ((st = far_compact(c, phase_host, s)) != FDIRW_OK) { dfree(); cudaFree(mask_d); return bail(st); }
+                ea.list = c->ut.dense_list;
+                ea.n_list = c->ut.n_dense;
+                ea.n_tiles = c->ut.nd_tiles;
+                w_elems = (size_t)c->ut.nd_tiles * (g.K - 1) * g.tile * kChunk;
+                d_elems = (size_t)c->ut.nd_tiles * g.tile * kChunk;
             }
             if (e == cudaSuccess) {
                 if ((st = alloc(&c->Wt, (w_elems ? w_elems : 1) * c->b_w, "weights")) != FDIRW_OK ||
@@ -441,7 +486,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         for (size_t i = 0; i < ns; ++i) fm[i] = phase_host[(size_t)g.z0 * plane + i] == 2 ? 1 : 0;
         c->tile_stride = 1 + (long)g.nz * g.tpp;
         if ((st = alloc((void**)&c->farmask, ns, "far mask")) != FDIRW_OK ||
-            (st = alloc((void**)&c->pbc, g.diag_elems * 4, "p_BC")) != FDIRW_OK ||
+            (st = alloc((void**)&c->pbc, (c->compact ? (size_t)c->ut.nd_tiles * g.tile * kChunk + 8 : g.diag_elems) * 4,
+                        "p_BC")) != FDIRW_OK ||
             (st = alloc((void**)&c->tile_buf, c->tile_stride * 8, "tile sums")) != FDIRW_OK ||
             (st = alloc((void**)&c->gathered, (size_t)c->world * c->tile_stride * 8, "gathered sums")) != FDIRW_OK ||
             (st = alloc((void**)&c->far_state, 16, "far state")) != FDIRW_OK) {
@@ -521,7 +567,8 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
     if (c->far && far_terms) {
         a.pbc = c->pbc;
         a.far_state = c->far_state;
-        a.tile_sum = c->tile_buf + 1;
+        // compacted tiles are not the global tiles of Eq.7: the sums come from tile_mass then
+        a.tile_sum = c->compact ? nullptr : c->tile_buf + 1;
     }
     if (push_parity >= 0) {  // a6 over peer memory: boundary planes also into the neighbours' halos
         const long pe = (long)g.plane_elems, row0 = (long)g.R * g.nxp + kPadX;
@@ -593,8 +640,11 @@ static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t 
     fdirw_status st = alloc((void**)&rowsum, n * 4, "p_BC scratch");
     if (st != FDIRW_OK) return st;
     cudaError_t e = launch_ones(mask_d, g.mz0, g, c->cpad[1], s);
-    if (e == cudaSuccess) e = superpose(c, c->cpad[1], rowsum, (long)g.nx * g.ny, g.nx, 0, g.n_tiles, s, false);
-    if (e == cudaSuccess) e = launch_pbc(rowsum, c->farmask, g, c->pbc, s);
+    if (e == cudaSuccess)
+        e = superpose(c, c->cpad[1], rowsum, (long)g.nx * g.ny, g.nx, 0, c->compact ? c->ut.nd_tiles : g.n_tiles, s, false);
+    if (e == cudaSuccess)
+        e = launch_pbc(rowsum, c->farmask, g, c->pbc, s, c->compact ? c->ut.dense_list : nullptr, c->ut.n_dense,
+                       c->ut.nd_tiles);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->cpad[1], 0, g.state_elems * 4, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(rowsum);
@@ -648,7 +698,8 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     }
     if (c->world == 1 && c->prec_mode != 0) {  // N3 §3.3 study modes: padded output only
         StudyArgs a{src, out - ((size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX), c->Wt, c->diag,
-                    g.nx, g.ny, g.nzl, g.nxq, g.tile, g.tpp, g.nxp, g.nyp, g.R, c->pbc, c->far_state};
+                    g.nx, g.ny, g.nzl, g.nxq, g.tile, g.tpp, g.nxp, g.nyp, g.R, c->pbc, c->far_state,
+                    c->compact ? c->chunk_pos : nullptr};
         if (ps != (long)g.plane_elems) return fail(FDIRW_E_STATE, "precision study modes run through fdirw_run");
         CUDA_TRY(launch_superpose_study(a, c->prec_mode, s));
         if (c->far) {  // study kernel has no tile sums: Eq.7 from a separate pass
@@ -670,6 +721,12 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, c->ut.nd_tiles, s));
             CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
             return FDIRW_OK;
+        }
+        if (c->compact) {  // N2 compacted: superpose the listed chunks, Eq.7 sums per global tile
+            CUDA_TRY(superpose(c, src, out, ps, rs, 0, c->ut.nd_tiles, s));
+            if (ps == (long)g.plane_elems) CUDA_TRY(launch_tile_mass_padded(out, c->farmask, g, c->tile_buf + 1, s));
+            else CUDA_TRY(launch_tile_mass(out, c->farmask, g, c->tile_buf + 1, s));
+            return far_reduce(c, s, 0, 0.0);
         }
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
         return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
@@ -721,6 +778,8 @@ extern "C" fdirw_status fdirw_step(fdirw_ctx* c, const float* c_in, float* c_out
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const Geometry& g = c->g;
     CUDA_TRY(launch_pack(c_in, c->cpad[0], g, s, c->farmask));
+    if (c->compact)  // targets of all-far chunks are not computed; far voxels read 0 as on every path
+        CUDA_TRY(cudaMemsetAsync(c_out, 0, (size_t)g.nx * g.ny * g.nzl * 4, s));
     if (c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) {
         fdirw_status st = p2p_start(c, s);
         if (st != FDIRW_OK) return st;
@@ -810,7 +869,7 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->lambda_fast = c->d.lam_ff;
     info->lambda_fs = c->d.lam_fs;
     info->lambda_slow = c->d.lam_ss;
-    const uint64_t wt_tiles = c->ut.chunk_u ? (uint64_t)c->ut.nd_tiles : (uint64_t)g.n_tiles;  // N4 compacts
+    const uint64_t wt_tiles = (c->ut.chunk_u || c->compact) ? (uint64_t)c->ut.nd_tiles : (uint64_t)g.n_tiles;  // N4 / N2 compact
     info->weight_bytes = wt_tiles * (g.K - 1) * g.tile * kChunk * c->b_w + wt_tiles * g.tile * kChunk * 4;
     info->state_bytes = (uint64_t)g.state_elems * 4 * 2;
     info->bytes_per_voxel_update = (uint64_t)(g.K - 1) * c->b_w + 12;
@@ -866,7 +925,7 @@ extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k
 {
     if (!c || !k) return fail(FDIRW_E_INVALID, "NULL argument");
     if (c->world != 1) return fail(FDIRW_E_STATE, "debug upload needs world == 1");
-    if (c->ut.chunk_u) return fail(FDIRW_E_STATE, "debug upload needs the dense layout");
+    if (c->ut.chunk_u || c->compact) return fail(FDIRW_E_STATE, "debug upload needs the dense layout");
     CUDA_TRY(cudaSetDevice(c->device));
     const Geometry& g = c->g;
     const int R = g.R, L = g.L, K = g.K;
@@ -916,7 +975,7 @@ extern "C" fdirw_status fdirw_export_kernels(const fdirw_ctx* c, const int32_t* 
     double* d = nullptr;
     fdirw_status st = alloc((void**)&d, n * 8, "export buffer");
     if (st != FDIRW_OK) return st;
-    cudaError_t e = launch_export(c->Wt, c->diag, c->g, c->fmt, box, d, nullptr);
+    cudaError_t e = launch_export(c->Wt, c->diag, c->g, c->fmt, box, d, nullptr, c->compact ? c->chunk_pos : nullptr);
     if (e == cudaSuccess) e = cudaMemcpy(out, d, n * 8, cudaMemcpyDeviceToHost);
     cudaFree(d);
     if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("export: ") + cudaGetErrorString(e));

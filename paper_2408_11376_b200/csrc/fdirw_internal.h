@@ -185,6 +185,7 @@ struct StudyArgs {
     int nx, ny, nzl, nxq, tile, tpp, nxp, nyp, R;
     const float* pbc;
     const double* far_state;
+    const int* chunk_pos;  // N2 compaction: chunk → compact position or −1 (null: full layout)
 };
 cudaError_t launch_superpose_study(const StudyArgs& a, int mode, cudaStream_t s);
 
@@ -197,7 +198,8 @@ cudaError_t launch_tile_mass(const float* c, const uint8_t* farmask, const Geome
 // padded field = 1 on in-domain non-far voxels of planes [z0−R, z1+R) (mask planes from mz0)
 cudaError_t launch_ones(const uint8_t* mask, int mz0, const Geometry& g, float* cpad, cudaStream_t s);
 // pbc[tile layout] = 1 − rowsum for real non-far targets, else 0
-cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s);
+cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s,
+                       const int* list = nullptr, long n_list = 0, int n_list_tiles = 0);
 // gathered = world blocks of (1 + stride−1) doubles: [count, tile sums...]; sum in global tile
 // order (deterministic for any decomposition).  mode 0: c_far = (M0 − Σ)/v_far;
 // mode 1 (init): M0 = Σ + c_far0·v_far, c_far = c_far0
@@ -209,7 +211,7 @@ cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStre
 cudaError_t launch_unpack(const float* cpad, float* c, const Geometry& g, cudaStream_t s);
 cudaError_t launch_mass(const float* c, size_t n, double* partial, int nblk, double* out, cudaStream_t s);
 cudaError_t launch_export(const void* Wt, const float* diag, const Geometry& g, int fmt, const int32_t* box,
-                          double* out, cudaStream_t s);
+                          double* out, cudaStream_t s, const int* chunk_pos = nullptr);
 
 // ---- NCCL (comm.cpp): dlopen'ed, no link-time dependency ------------------------
 struct Nccl;

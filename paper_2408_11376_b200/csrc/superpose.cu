@@ -517,17 +517,23 @@ cudaError_t launch_ones(const uint8_t* mask, int mz0, const Geometry& g, float* 
 }
 
 __global__ void pbc_kernel(const float* __restrict__ rowsum, const uint8_t* __restrict__ farmask, int nx, int ny,
-                           int nxq, int tile, int tpp, long n_elems, float* __restrict__ pbc)
+                           int nxq, int tile, int tpp, long n_elems, float* __restrict__ pbc,
+                           const int* __restrict__ list, long n_list)
 {
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n_elems; i += (long)gridDim.x * blockDim.x) {
         const int j = (int)(i & 7);
-        const long te = i >> 3;
+        long te = i >> 3;
+        bool ok = true;
+        if (list) {  // N2 compaction: element te of the compact layout is chunk list[te]
+            ok = te < n_list;
+            te = ok ? list[te] : 0;
+        }
         const int e = (int)(te % tile);
         const long t = te / tile;
         const int zl = (int)(t / tpp), tp = (int)(t % tpp);
         const int q = tp * tile + e;
         float v = 0.f;
-        if (q < ny * nxq) {
+        if (ok && q < ny * nxq) {
             const int y = q / nxq, x = (q % nxq) * 8 + j;
             if (x < nx) {
                 const long k = ((long)zl * ny + y) * nx + x;
@@ -538,10 +544,13 @@ __global__ void pbc_kernel(const float* __restrict__ rowsum, const uint8_t* __re
     }
 }
 
-cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s)
+cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s,
+                       const int* list, long n_list, int n_list_tiles)
 {
-    pbc_kernel<<<grid_for((long)g.diag_elems, 256), 256, 0, s>>>(rowsum, farmask, g.nx, g.ny, g.nxq, g.tile, g.tpp,
-                                                                (long)g.diag_elems, pbc);
+    const long n = list ? (long)n_list_tiles * g.tile * kChunk : (long)g.diag_elems;
+    if (n <= 0) return cudaSuccess;
+    pbc_kernel<<<grid_for(n, 256), 256, 0, s>>>(rowsum, farmask, g.nx, g.ny, g.nxq, g.tile, g.tpp, n, pbc, list,
+                                                n_list);
     return cudaGetLastError();
 }
 
@@ -663,7 +672,8 @@ cudaError_t launch_mass(const float* c, size_t n, double* partial, int nblk, dou
 
 // Decode the stored kernels of the sources in `box` back to per-source fp64 arrays.
 __global__ void export_kernel(const void* __restrict__ Wt, const float* __restrict__ diag, Geometry g, int fmt,
-                              int bx0, int bx, int by0, int by, int bz0, int bz, double* __restrict__ out)
+                              int bx0, int bx, int by0, int by, int bz0, int bz, double* __restrict__ out,
+                              const int* __restrict__ chunk_pos)
 {
     const long total = (long)bx * by * bz * g.K;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -676,9 +686,17 @@ __global__ void export_kernel(const void* __restrict__ Wt, const float* __restri
         if (x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= g.z0 && z < g.z1 && sx >= 0 && sx < g.nx &&
             sy >= 0 && sy < g.ny && sz >= 0 && sz < g.nz) {
             const int q = y * g.nxq + (x >> 3);
-            const size_t tile = (size_t)(z - g.z0) * g.tpp + q / g.tile;
-            const int e = q % g.tile, j = x & 7;
-            if (o == g.K / 2) {
+            size_t tile = (size_t)(z - g.z0) * g.tpp + q / g.tile;
+            int e = q % g.tile;
+            const int j = x & 7;
+            const int cp = chunk_pos ? chunk_pos[tile * g.tile + e] : 0;  // N2 compaction
+            if (chunk_pos && cp >= 0) {
+                tile = cp / g.tile;
+                e = cp % g.tile;
+            }
+            if (chunk_pos && cp < 0) {
+                v = 0.0;  // an all-far chunk: no weights stored (they are 0)
+            } else if (o == g.K / 2) {
                 v = diag[(tile * g.tile + e) * 8 + j];
             } else {
                 const size_t idx = ((tile * (size_t)(g.K - 1) + slot_of(ox, oy, oz, g.R)) * g.tile + e) * 8 + j;
@@ -692,12 +710,13 @@ __global__ void export_kernel(const void* __restrict__ Wt, const float* __restri
 }
 
 cudaError_t launch_export(const void* Wt, const float* diag, const Geometry& g, int fmt, const int32_t* box,
-                          double* out, cudaStream_t s)
+                          double* out, cudaStream_t s, const int* chunk_pos)
 {
     const int bx = box[1] - box[0], by = box[3] - box[2], bz = box[5] - box[4];
     const long total = (long)bx * by * bz * g.K;
     if (total <= 0) return cudaSuccess;
-    export_kernel<<<grid_for(total, 256), 256, 0, s>>>(Wt, diag, g, fmt, box[0], bx, box[2], by, box[4], bz, out);
+    export_kernel<<<grid_for(total, 256), 256, 0, s>>>(Wt, diag, g, fmt, box[0], bx, box[2], by, box[4], bz, out,
+                                                       chunk_pos);
     return cudaGetLastError();
 }
 

@@ -24,6 +24,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "fdirw_internal.h"
 #include "layout.cuh"
 
@@ -89,6 +91,35 @@ struct WLoad<__half> {
     }
 };
 
+// Raw 128-bit words of one weight slot (8 targets): 2 for fp32, 1 for fp16/bf16.
+template <typename WT>
+struct RawW {
+    static constexpr int N = sizeof(WT) == 4 ? 2 : 1;
+};
+
+__device__ __forceinline__ void decode_w(const uint4 (&r)[2], float w[8])
+{
+    w[0] = __uint_as_float(r[0].x); w[1] = __uint_as_float(r[0].y); w[2] = __uint_as_float(r[0].z);
+    w[3] = __uint_as_float(r[0].w); w[4] = __uint_as_float(r[1].x); w[5] = __uint_as_float(r[1].y);
+    w[6] = __uint_as_float(r[1].z); w[7] = __uint_as_float(r[1].w);
+}
+template <typename WT>
+__device__ __forceinline__ void decode_w(const uint4 (&r)[1], float w[8])
+{
+    const unsigned u[4] = {r[0].x, r[0].y, r[0].z, r[0].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if constexpr (std::is_same<WT, __nv_bfloat16>::value) {
+            w[2 * i] = __uint_as_float(u[i] << 16);
+            w[2 * i + 1] = __uint_as_float(u[i] & 0xffff0000u);
+        } else {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u[i]));
+            w[2 * i] = f.x;
+            w[2 * i + 1] = f.y;
+        }
+    }
+}
+
 // Error-free addition (Knuth TwoSum): s + e == a + b exactly.
 __device__ __forceinline__ void two_sum(float a, float b, float& s, float& e)
 {
@@ -127,6 +158,52 @@ __device__ __forceinline__ void do_row(const float* srow, const WT* wp, size_t w
         if (CENTRE_ROW && ox == 0) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) p[j] = fmaf(w[ox + R][j], seg[j - ox + 8], p[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float s, e;
+        two_sum(hi[j], p[j], s, e);
+        hi[j] = s;
+        lo[j] = __fadd_rn(lo[j], e);
+    }
+}
+
+// Prefetching form (small grids): the raw weight words of a row are loaded into
+// registers one row ahead, so each thread keeps two rows of weight loads in flight.  The
+// arithmetic (seg, FMA chain in ox order from 0, TwoSum into (hi, lo)) is do_row's exactly.
+template <int R, typename WT, int NS>
+__device__ __forceinline__ void load_row_raw(const WT* wp, size_t wstride, uint64_t pol,
+                                             uint4 (&raw)[2 * R + 1][RawW<WT>::N])
+{
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        raw[k][0] = ld_stream(wp + (size_t)k * wstride, pol);
+        if constexpr (RawW<WT>::N == 2) raw[k][1] = ld_stream(wp + (size_t)k * wstride + 4, pol);
+    }
+}
+
+template <int R, typename WT, bool CENTRE_ROW>
+__device__ __forceinline__ void fma_row_raw(const float* srow, const uint4 (&raw)[2 * R + 1][RawW<WT>::N],
+                                            float hi[8], float lo[8])
+{
+    float seg[24];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const float4 v = ld_c(srow + 4 * i);
+        seg[4 * i] = v.x; seg[4 * i + 1] = v.y; seg[4 * i + 2] = v.z; seg[4 * i + 3] = v.w;
+    }
+    float p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = 0.f;
+#pragma unroll
+    for (int ox = -R; ox <= R; ++ox) {
+        if (CENTRE_ROW && ox == 0) continue;
+        const int k = CENTRE_ROW ? (ox < 0 ? ox + R : ox + R - 1) : ox + R;
+        float w[8];
+        if constexpr (RawW<WT>::N == 2) decode_w(raw[k], w);
+        else decode_w<WT>(raw[k], w);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) p[j] = fmaf(w[j], seg[j - ox + 8], p[j]);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -262,7 +339,7 @@ __device__ __forceinline__ double tile_block_sum(double s)
     return t;  // valid in thread 0
 }
 
-template <int R, typename WT>
+template <int R, typename WT, bool PF = false>
 __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
 {
     constexpr int L = 2 * R + 1, K = L * L * L;
@@ -302,6 +379,27 @@ __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
             hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
             hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
         }
+        if constexpr (PF) {
+            // same rows in the same order, each row's weights loaded while the previous row
+            // computes (ping-pong register buffers; L² − 1 is even)
+            uint4 ra[L][RawW<WT>::N], rb[L][RawW<WT>::N];
+            const WT* wr = wt + (size_t)(L - 1) * wstride;
+            load_row_raw<R, WT, L - 1>(wt, wstride, pol, ra);
+            load_row_raw<R, WT, L>(wr, wstride, pol, rb);
+            fma_row_raw<R, WT, true>(c0 - 8, ra, hi, lo);
+            constexpr int NR = L * L - 1, RC = R * L + R;
+#pragma unroll 1
+            for (int i = 0; i < NR; i += 2) {
+                const int r0 = i < RC ? i : i + 1, r1 = i + 1 < RC ? i + 1 : i + 2;
+                if (i + 1 < NR) load_row_raw<R, WT, L>(wr + (size_t)L * wstride, wstride, pol, ra);
+                fma_row_raw<R, WT, false>(c0 - (long)(r0 / L - R) * plane - (long)(r0 % L - R) * nxp - 8, rb, hi, lo);
+                wr += (size_t)L * wstride;
+                if (i + 1 >= NR) break;
+                if (i + 2 < NR) load_row_raw<R, WT, L>(wr + (size_t)L * wstride, wstride, pol, rb);
+                fma_row_raw<R, WT, false>(c0 - (long)(r1 / L - R) * plane - (long)(r1 % L - R) * nxp - 8, ra, hi, lo);
+                wr += (size_t)L * wstride;
+            }
+        } else {
         // centre row (oz = oy = 0): slots [0, L−1)
         do_row<R, WT, true>(c0 - 8, wt, wstride, pol, hi, lo);
         // remaining rows, ascending (oz, oy); source row of target row (z, y) is (z − oz, y − oy)
@@ -313,6 +411,7 @@ __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
             const float* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
             do_row<R, WT, false>(srow, wr, wstride, pol, hi, lo);
             wr += (size_t)L * wstride;
+        }
         }
     }
 
@@ -370,10 +469,10 @@ __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
     }
 }
 
-template <int R, typename WT>
+template <int R, typename WT, bool PF>
 __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
 {
-    dense_body<R, WT>(a, blockIdx.x);
+    dense_body<R, WT, PF>(a, blockIdx.x);
 }
 
 // N4: ONE launch mixing the HBM-bound dense tiles and the FMA-bound uniform blocks, the U
@@ -389,14 +488,34 @@ __global__ void __launch_bounds__(256) superpose_mixed_kernel(const SuperArgs a,
     else dense_body<R, WT>(a, (int)(b - u0));
 }
 
+// prefetch buffers are 2·L·(1 or 2) 128-bit words: only where they fit the registers
+template <int R, typename WT>
+struct PfOK {
+    static constexpr bool v = (2 * R + 1) * RawW<WT>::N <= 18;
+};
+template <int R>
+constexpr bool kPrefetchOK(int fmt)
+{
+    return fmt == 0 ? PfOK<R, float>::v : PfOK<R, __half>::v;
+}
+
 template <int R>
 static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t s)
 {
     const int nblk = a.t_end - a.t_begin;
     if (nblk <= 0) return cudaSuccess;
-    if (fmt == 0) superpose_kernel<R, float><<<nblk, a.tile, 0, s>>>(a);
-    else if (fmt == 1) superpose_kernel<R, __half><<<nblk, a.tile, 0, s>>>(a);
-    else superpose_kernel<R, __nv_bfloat16><<<nblk, a.tile, 0, s>>>(a);
+    // a launch of fewer than two CTAs per SM cannot keep enough weight loads in flight
+    // through occupancy: those threads prefetch one row ahead instead (identical bits)
+    const bool pf = nblk < 2 * 148 && kPrefetchOK<R>(fmt);
+    if (pf) {
+        if (fmt == 0) superpose_kernel<R, float, PfOK<R, float>::v><<<nblk, a.tile, 0, s>>>(a);
+        else if (fmt == 1) superpose_kernel<R, __half, PfOK<R, __half>::v><<<nblk, a.tile, 0, s>>>(a);
+        else superpose_kernel<R, __nv_bfloat16, PfOK<R, __nv_bfloat16>::v><<<nblk, a.tile, 0, s>>>(a);
+    } else {
+        if (fmt == 0) superpose_kernel<R, float, false><<<nblk, a.tile, 0, s>>>(a);
+        else if (fmt == 1) superpose_kernel<R, __half, false><<<nblk, a.tile, 0, s>>>(a);
+        else superpose_kernel<R, __nv_bfloat16, false><<<nblk, a.tile, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 

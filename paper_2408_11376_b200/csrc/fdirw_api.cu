@@ -548,7 +548,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
 // Superpose tiles [t0, t1) of `src` (padded) into `out` with strides (ps, rs).  With a far
 // field (N2) and far_terms: + p_BC·c_far and the per-tile Σ C_new for Eq.7.
 static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps, long rs, int t0, int t1,
-                             cudaStream_t s, bool far_terms = true, int push_parity = -1)
+                             cudaStream_t s, bool far_terms = true, int push_parity = -1, int gap0 = 0, int gap1 = 0)
 {
     const Geometry& g = c->g;
     SuperArgs a{};
@@ -562,6 +562,10 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
     a.nxp = g.nxp; a.nyp = g.nyp;
     a.t_begin = t0;
     a.t_end = t1;
+    if (gap1 > gap0) {  // tiles [t0, gap0) ∪ [gap1, t1) in one launch
+        a.gap_at = gap0;
+        a.gap_len = gap1 - gap0;
+    }
     a.list = c->ut.dense_list;  // N4 (null unless FDIRW_F_DEDUP_STORAGE): compacted non-uniform chunks
     a.n_list = c->ut.n_dense;
     if (c->far && far_terms) {
@@ -687,12 +691,10 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
         split_tiles(g, &i0, &i1);
         CUDA_TRY(superpose(c, src, out, ps, rs, i0, i1, s));
         CUDA_TRY(p2p_wait(c->p2p_flags, c->peer_lo_flag != nullptr, c->peer_hi_flag != nullptr, s));
-        if (i1 > i0) {
-            CUDA_TRY(superpose(c, src, out, ps, rs, 0, i0, s, true, dst_parity));
-            CUDA_TRY(superpose(c, src, out, ps, rs, i1, g.n_tiles, s, true, dst_parity));
-        } else {
+        if (i1 > i0)  // both boundary bands in one launch
+            CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity, i0, i1));
+        else
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity));
-        }
         CUDA_TRY(p2p_signal(c->p2p_flags, c->peer_lo_flag, c->peer_hi_flag, s));
         return FDIRW_OK;
     }
@@ -741,9 +743,8 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
     CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
     CUDA_TRY(superpose(c, src, out, ps, rs, i0, i1, s));  // interior overlaps the exchange
     CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
-    if (i1 > i0) {
-        CUDA_TRY(superpose(c, src, out, ps, rs, 0, i0, s));
-        CUDA_TRY(superpose(c, src, out, ps, rs, i1, g.n_tiles, s));
+    if (i1 > i0) {  // both boundary bands in one launch
+        CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, -1, i0, i1));
     } else {
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
     }

@@ -118,7 +118,8 @@ struct SuperArgs {
     long out_ps, out_rs; // output plane / row strides (elements)
     int nx, ny, nxq, tile, tpp, K;
     int nxp, nyp;        // padded row length, rows per padded plane
-    int t_begin, t_end;  // tile range
+    int t_begin, t_end;  // tile range (CTA b → tile t_begin + b, plus gap_len once ≥ gap_at)
+    int gap_at = 0, gap_len = 0;  // one launch over [t0, i0) ∪ [i1, t1): the slab's two boundary bands
     // N2 (far field): + pbc·far_state[0] per target, per-tile Σ C_new into tile_sum[tile]
     const float* pbc = nullptr;
     const double* far_state = nullptr;  // {c_far, M0}

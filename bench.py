@@ -535,9 +535,9 @@ def main():
         bpv = int(round((1.0 - f_u) * (info["K"] - 1) * (2 if cfg.weights != "fp32" else 4))) + 12
     per_launch_bytes = bpv * n_slab
     peak, peak_src = _hbm_peak()
-    # N=1: one superpose launch; N>1: interior + one boundary-bands superpose launch (+ wait
-    # and signal kernels with P2P; NCCL's own kernels are not counted)
-    launches_per_step = 1 if world == 1 else (4 if transport == "p2p" else 2)
+    # N=1: one superpose launch; N>1 P2P: wait + one superpose launch + signal; NCCL: interior
+    # + boundary-bands superpose launches (NCCL's own kernels are not counted)
+    launches_per_step = 1 if world == 1 else (3 if transport == "p2p" else 2)
     # one superpose launch per step at N=1 (+1 pack, +1 unpack per fdirw_run); the launch
     # duration is the timed region / K to within the two ~10 µs state kernels.
     achieved = per_launch_bytes / (ms_step * 1e-3) / 1e9

@@ -548,7 +548,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
 // Superpose tiles [t0, t1) of `src` (padded) into `out` with strides (ps, rs).  With a far
 // field (N2) and far_terms: + p_BC·c_far and the per-tile Σ C_new for Eq.7.
 static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps, long rs, int t0, int t1,
-                             cudaStream_t s, bool far_terms = true, int push_parity = -1, int gap0 = 0, int gap1 = 0)
+                             cudaStream_t s, bool far_terms = true, int push_parity = -1, int gap0 = 0, int gap1 = 0,
+                             bool gap_last = false)
 {
     const Geometry& g = c->g;
     SuperArgs a{};
@@ -565,6 +566,7 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
     if (gap1 > gap0) {  // tiles [t0, gap0) ∪ [gap1, t1) in one launch
         a.gap_at = gap0;
         a.gap_len = gap1 - gap0;
+        a.gap_last = gap_last;
     }
     a.list = c->ut.dense_list;  // N4 (null unless FDIRW_F_DEDUP_STORAGE): compacted non-uniform chunks
     a.n_list = c->ut.n_dense;
@@ -685,14 +687,16 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
 {
     const Geometry& g = c->g;
     if (c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) {
-        // interior tiles (no halo reads) → wait for the neighbours' previous step → boundary
-        // tiles, whose edge planes are stored into the neighbours' halos → signal
+        // wait for the neighbours' previous step (their stores into my halo are complete and
+        // they are done reading the halo I overwrite) → ONE launch over every tile, boundary
+        // bands first so their stores into the neighbours' halos start early → signal.
+        // (No transfer phase is left to overlap, so the interior is not split off: one
+        // launch keeps the SMs evenly loaded at strong-scaling slab sizes.)
         int i0, i1;
         split_tiles(g, &i0, &i1);
-        CUDA_TRY(superpose(c, src, out, ps, rs, i0, i1, s));
         CUDA_TRY(p2p_wait(c->p2p_flags, c->peer_lo_flag != nullptr, c->peer_hi_flag != nullptr, s));
-        if (i1 > i0)  // both boundary bands in one launch
-            CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity, i0, i1));
+        if (i1 > i0)
+            CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity, i0, i1, true));
         else
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity));
         CUDA_TRY(p2p_signal(c->p2p_flags, c->peer_lo_flag, c->peer_hi_flag, s));

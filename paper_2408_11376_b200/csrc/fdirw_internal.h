@@ -120,6 +120,7 @@ struct SuperArgs {
     int nxp, nyp;        // padded row length, rows per padded plane
     int t_begin, t_end;  // tile range (CTA b → tile t_begin + b, plus gap_len once ≥ gap_at)
     int gap_at = 0, gap_len = 0;  // one launch over [t0, i0) ∪ [i1, t1): the slab's two boundary bands
+    bool gap_last = false;        // ... followed by the gap [i0, i1) itself: every tile, boundary bands first
     // N2 (far field): + pbc·far_state[0] per target, per-tile Σ C_new into tile_sum[tile]
     const float* pbc = nullptr;
     const double* far_state = nullptr;  // {c_far, M0}

@@ -344,7 +344,11 @@ __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
 {
     constexpr int L = 2 * R + 1, K = L * L * L;
     int tile = a.t_begin + blk;  // weight tile (compact tile when a.list, N4)
-    if (a.gap_len && tile >= a.gap_at) tile += a.gap_len;
+    if (a.gap_len) {
+        const int nb = a.t_end - a.t_begin - a.gap_len;  // CTAs of the two outer bands
+        if (a.gap_last && blk >= nb) tile = a.gap_at + (blk - nb);
+        else if (tile >= a.gap_at) tile += a.gap_len;
+    }
     const int e = threadIdx.x;
     int zl, q;
     bool real;
@@ -503,7 +507,7 @@ constexpr bool kPrefetchOK(int fmt)
 template <int R>
 static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t s)
 {
-    const int nblk = a.t_end - a.t_begin - a.gap_len;
+    const int nblk = a.t_end - a.t_begin - (a.gap_last ? 0 : a.gap_len);
     if (nblk <= 0) return cudaSuccess;
     // a launch of fewer than two CTAs per SM cannot keep enough weight loads in flight
     // through occupancy: those threads prefetch one row ahead instead (identical bits)

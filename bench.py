@@ -226,29 +226,39 @@ def _variant_n4(fd, torch, params, mask, c_host, args, stream, peak):
 
 
 def _kgen_line(t_kgen, cells_algo, info, cfg, world):
-    """kgen (one-time build, a3+a4).  Algorithmic work = every source's window (dedup counts
-    each source); the ALU roofline counts what was computed: distinct windows × K × n_fd
-    cell-updates, each 12 FP32 lane-ops (6 face differences + 6 FMAs), against
-    148 SMs × 128 FP32 lanes × max SM clock (MEASURED_PEAKS sm_max_mhz)."""
+    """kgen (one-time build, a3+a4).  `seconds` = wall time of fdirw_build_kernels (mask upload,
+    window dedup, kgen, expand into the gather layout, allocation).  Algorithmic work = every
+    source's window × K × n_fd FD cell-updates (the literal method).  The kernel itself
+    (device time from CUDA events around its launch, fdirw_info.kgen_kernel_ms) runs the distinct
+    windows only, kgen_steps stencil passes each (the Chebyshev degree m, reading A29, or n_fd):
+    its rooflines count those passes — shared memory (4 lateral neighbour reads + 1 write of 4 B
+    per cell-pass, z columns padded from L to Lp; 128 B/clk/SM) binds, the FP32 lanes (11
+    lane-ops per substep cell, 13 per Chebyshev cell-pass) do not."""
     p = _peaks() or {}
     mhz = float(p.get("sm_max_mhz", 1965.0))
-    peak_cells = 148 * 128 * mhz * 1e6 / 12
-    computed = info["kgen_windows"] * world * cfg.K * info["n_fd"]
     L = 2 * cfg.R + 1
     lp = (L + 3) // 4 * 4
-    ach = computed / t_kgen
-    return {"seconds": t_kgen, "window_cell_updates": cells_algo, "cell_updates_per_s": cells_algo / t_kgen,
-            "n_fd": info["n_fd"], "windows_computed": info["kgen_windows"] * world,
-            "sources": info["kgen_sources"] * world,
-            "roofline": {"bound": "alu", "achieved": ach, "peak": peak_cells, "unit": "cell-updates/s",
-                         "frac": ach / peak_cells,
-                         "note": "computed windows only; peak = 148*128 FP32 lanes * %.0f MHz / 12 lane-ops "
-                                 "per cell-update (time includes dedup + expand)" % mhz},
-            # the binding resource of kgen v2: shared memory (4 lateral neighbour reads + 1 write of
-            # 4 B per cell-update, z columns padded from L to Lp), 128 B/clk/SM
-            "smem": {"achieved_TBps": ach * 20.0 * lp / L / 1e12, "peak_TBps": 148 * 128 * mhz * 1e6 / 1e12,
-                     "frac": (ach * 20.0 * lp / L) / (148 * 128 * mhz * 1e6),
-                     "bytes_per_cell_update": 20.0 * lp / L}}
+    steps = info["kgen_steps"]
+    cheb = steps != info["n_fd"]
+    kms = info["kgen_kernel_ms"]
+    passes = info["kgen_windows"] * world * cfg.K * steps  # computed cell-passes
+    rate = passes / (kms * 1e-3) if kms > 0 else 0.0
+    smem_b = 20.0 * lp / L
+    smem_peak = 148 * 128 * mhz * 1e6
+    ops = 13 if cheb else 11
+    alu_peak = 148 * 128 * mhz * 1e6 / ops
+    return {"seconds": t_kgen, "kernel_ms": kms, "window_cell_updates": cells_algo,
+            "cell_updates_per_s": cells_algo / t_kgen,
+            "kernel_cell_updates_per_s": cells_algo / (kms * 1e-3) if kms > 0 else None,
+            "n_fd": info["n_fd"], "method": "chebyshev" if cheb else "substeps", "passes_per_window": steps,
+            "windows_computed": info["kgen_windows"] * world, "sources": info["kgen_sources"] * world,
+            "roofline": {"bound": "smem", "achieved": rate * smem_b / 1e12, "peak": smem_peak / 1e12,
+                         "unit": "TB/s", "frac": rate * smem_b / smem_peak,
+                         "note": "kgen kernel only: %.1f B of shared-memory traffic per window cell-pass "
+                                 "x distinct windows x K x %d passes / kernel time; peak = 148 SMs x "
+                                 "128 B/clk x %.0f MHz" % (smem_b, steps, mhz)},
+            "alu": {"achieved": rate, "peak": alu_peak, "unit": "cell-passes/s", "frac": rate / alu_peak,
+                    "lane_ops_per_cell_pass": ops}}
 
 
 def _coarse_roofline(info, ms):

@@ -80,6 +80,11 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weig
                                   W_x(−o); each rank generates only its own slab's kernels (no
                                   halo sources).  Not combined with FDIRW_F_DEDUP_STORAGE
                                   (reading A24)                                                   */
+#define FDIRW_F_KGEN_DIRECT 32u /* kgen runs the n_fd explicit substeps literally.  Default:
+                                  when it saves work, the same A^{n_fd}·δ_s is evaluated by a
+                                  Chebyshev recurrence of degree m ≈ 160 (at n_fd = 1000, λ = 0.1)
+                                  over the same stencil, truncation ‖·‖₂ ≤ 1e-10 (reading A29;
+                                  fdirw_info.kgen_steps reports which)                            */
 
 /* The paper's problem statement (Table 1) + north_star's window radius / precision. */
 typedef struct {
@@ -136,6 +141,9 @@ typedef struct {
     uint64_t chunks;        /* 8-target x-chunks of the slab                                        */
     uint64_t uniform_chunks;/* N4: chunks whose weights come from a shared class kernel (else 0)   */
     int32_t uniform_classes;/* N4: distinct class kernels those chunks use                          */
+    int32_t kgen_steps;     /* stencil passes per kgen window: n_fd (direct substeps, also with
+                               FDIRW_F_KGEN_FP64) or the Chebyshev degree m (reading A29)          */
+    double kgen_kernel_ms;  /* device time of the kgen launch in fdirw_build_kernels (CUDA events) */
 } fdirw_info;
 
 /* Host-only decomposition plan of one rank (no CUDA call; usable without a GPU).
@@ -155,6 +163,7 @@ typedef struct {
     int64_t halo_elems;
     int64_t send_lo, recv_lo, send_hi, recv_hi; /* element offsets, −1 if no peer            */
     uint64_t weight_bytes, state_bytes; /* device bytes the context will allocate            */
+    int32_t kgen_steps;                 /* stencil passes per kgen window (= fdirw_info.kgen_steps) */
 } fdirw_plan;
 
 /* Validates exactly like fdirw_build_kernels and fills *plan.  Host only. */

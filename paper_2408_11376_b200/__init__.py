@@ -34,6 +34,7 @@ F_NO_DEDUP = 2
 F_DEDUP_STORAGE = 4  # NEXT row N4: uniform chunks read shared class kernels (fewer HBM bytes)
 F_KGEN_FP64 = 8  # kgen in fp64, the oracle's operation order (reading A22, debugging)
 F_SYMMETRIC_RULE = 16  # exact regime only: gather weights = own kernel reflected (reading A24)
+F_KGEN_DIRECT = 32  # kgen runs the n_fd substeps literally instead of the Chebyshev recurrence (reading A29)
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",
@@ -68,7 +69,8 @@ class fdirw_info(ctypes.Structure):
                 ("bytes_per_voxel_update", ctypes.c_uint64), ("voxels", ctypes.c_uint64),
                 ("tile_chunks", ctypes.c_int32), ("n_tiles", ctypes.c_int32),
                 ("kgen_sources", ctypes.c_uint64), ("kgen_windows", ctypes.c_uint64),
-                ("chunks", ctypes.c_uint64), ("uniform_chunks", ctypes.c_uint64), ("uniform_classes", ctypes.c_int32)]
+                ("chunks", ctypes.c_uint64), ("uniform_chunks", ctypes.c_uint64), ("uniform_classes", ctypes.c_int32),
+                ("kgen_steps", ctypes.c_int32), ("kgen_kernel_ms", ctypes.c_double)]
 
 
 class fdirw_plan(ctypes.Structure):
@@ -77,7 +79,7 @@ class fdirw_plan(ctypes.Structure):
         "tiles_per_plane", "n_tiles", "interior_tile_begin", "interior_tile_end", "peer_lo", "peer_hi", "n_fd")] + \
         [(n, ctypes.c_int64) for n in ("padded_x", "padded_y", "padded_z", "pad_x0", "halo_elems", "send_lo",
                                        "recv_lo", "send_hi", "recv_hi")] + \
-        [("weight_bytes", ctypes.c_uint64), ("state_bytes", ctypes.c_uint64)]
+        [("weight_bytes", ctypes.c_uint64), ("state_bytes", ctypes.c_uint64), ("kgen_steps", ctypes.c_int32)]
 
 
 class fdirw_coarse_info(ctypes.Structure):

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -34,6 +35,10 @@ struct fdirw_ctx {
     Nccl* nccl = nullptr;
     void* comm = nullptr;
     uint64_t kgen_sources = 0, kgen_windows = 0;
+    int kgen_steps = 0;  // stencil passes per window: Chebyshev degree m, or n_fd (direct)
+    float* cheb_d = nullptr;  // kgen's Chebyshev coefficients (build only)
+    cudaEvent_t kev[2] = {nullptr, nullptr};
+    float kgen_ms = 0.f;      // device time of the kgen launch (CUDA events on the build stream)
     // N4 uniform-chunk weight dedup (FDIRW_F_DEDUP_STORAGE)
     UniformTables ut;
     // N2 far field
@@ -168,6 +173,56 @@ static fdirw_status derive(const fdirw_params& p, Derived* d)
     return FDIRW_OK;
 }
 
+// Chebyshev plan for kgen (reading A29).  Every window operator A (7-point
+// stencil, symmetric face numbers λ_ij, no-flux or absorbing edges) is symmetric with its
+// spectrum in [a, 1], a = 1 − 12·λ_max (Gershgorin: centre 1 − Λ_i, radius ≤ Λ_i ≤ 6λ_max).
+// With x = αy + β (α = 6λ_max, β = 1 − 6λ_max), x^n = Σ_k c_k T_k(y) where every c_k ≥ 0
+// (binomial expansion in y, and y^j's Chebyshev coefficients are ≥ 0) and Σ_k c_k = 1^n = 1,
+// so |x^n − Σ_{k≤m} c_k T_k(y)| ≤ 1 − Σ_{k≤m} c_k on [a, 1] and, A being symmetric,
+// ‖p_m(A)δ − A^n δ‖₂ ≤ that tail.  The c_k come from an M-point discrete Chebyshev
+// transform of x^n (fp64; aliasing is below the tail once M ≥ 4m).  Returns m (0 = the
+// recurrence would not save work: keep the n_fd direct substeps).
+static int cheb_plan(int n, double lam_max, std::vector<float>* coef)
+{
+    const double tol = 1e-10;
+    const int kmax = 2048;  // coefficients live in the kgen CTA's shared memory
+    if (n < 8 || !(lam_max > 0)) return 0;
+    const double al = 6.0 * lam_max, be = 1.0 - 6.0 * lam_max;
+    const int kk = n < kmax ? n : kmax;
+    const int M = 4 * kk + 64;
+    std::vector<double> f(M), th(M);
+    for (int j = 0; j < M; ++j) {
+        th[j] = M_PI * (j + 0.5) / M;
+        f[j] = std::pow(al * std::cos(th[j]) + be, (double)n);
+    }
+    std::vector<double> c;
+    double sum = 0.0;
+    int m = -1;
+    for (int k = 0; k <= kk; ++k) {
+        double v = 0.0;
+        for (int j = 0; j < M; ++j) v += f[j] * std::cos(k * th[j]);
+        v *= (k == 0 ? 1.0 : 2.0) / M;
+        c.push_back(v);
+        sum += v;
+        if (1.0 - sum <= tol) { m = k; break; }
+    }
+    // one pass costs the direct substep + 2 FMA (14 vs 12 lane-ops, same shared-memory traffic)
+    if (m < 1 || 14.0 * m > 0.8 * 12.0 * n) return 0;
+    coef->assign(c.begin(), c.end());
+    return m;
+}
+
+// kgen's plan for these params: kCheb_pre direct substeps first (the peaked start: its entries
+// of size ~1 would otherwise enter the recurrence and its rounding), then the Chebyshev degree
+// for the remaining n_fd − kCheb_pre.  Returns that degree (0 = all n_fd substeps direct).
+static const int kCheb_pre = 8;
+static int kgen_cheb(const fdirw_params& p, const Derived& d, std::vector<float>* coef)
+{
+    if (p.flags & (FDIRW_F_KGEN_FP64 | FDIRW_F_KGEN_DIRECT)) return 0;
+    if (d.n_fd <= 2 * kCheb_pre) return 0;
+    return cheb_plan(d.n_fd - kCheb_pre, std::max(d.lam_ff, std::max(d.lam_fs, d.lam_ss)), coef);
+}
+
 static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const fdirw_dist* dist,
                              fdirw_ctx** out, bool scan_phase = true)
 {
@@ -179,7 +234,7 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
     if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE | FDIRW_F_KGEN_FP64 |
-                     FDIRW_F_SYMMETRIC_RULE))
+                     FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT))
         return fail(FDIRW_E_INVALID, "unknown flags");
     if ((p->flags & FDIRW_F_SYMMETRIC_RULE) && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_SYMMETRIC_RULE is not combined with FDIRW_F_DEDUP_STORAGE");
@@ -226,6 +281,9 @@ static void free_ctx(fdirw_ctx* c)
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     if (c->graph2) cudaGraphExecDestroy(c->graph2);
+    cudaFree(c->cheb_d);
+    for (cudaEvent_t e : c->kev)
+        if (e) cudaEventDestroy(e);
     if (c->comm) nccl_comm_destroy(c->nccl, c->comm);
     for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
     cudaFree(c->p2p_flags);
@@ -397,6 +455,27 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         ka.sz1 = g.z1;
     }
     ka.n_fd = d.n_fd;
+    c->kgen_steps = d.n_fd;
+    std::vector<float> cheb;
+    {
+        const double lmax = std::max(d.lam_ff, std::max(d.lam_fs, d.lam_ss));
+        const int m = kgen_cheb(*params, d, &cheb);
+        if (m > 0) {
+            if ((st = alloc((void**)&c->cheb_d, cheb.size() * 4, "chebyshev coefficients")) != FDIRW_OK) {
+                cudaFree(mask_d);
+                return bail(st);
+            }
+            BAIL_CUDA(cudaMemcpyAsync(c->cheb_d, cheb.data(), cheb.size() * 4, cudaMemcpyHostToDevice, s));
+            const double sc = 4.0 / (12.0 * lmax);  // 2μ = 4λ/(1 − a), 1 − a = 12 λ_max
+            ka.cheb_m = m;
+            ka.cheb_pre = kCheb_pre;
+            ka.cheb_c = c->cheb_d;
+            ka.mu2_ff = (float)(d.lam_ff * sc);
+            ka.mu2_fs = (float)(d.lam_fs * sc);
+            ka.mu2_ss = (float)(d.lam_ss * sc);
+            c->kgen_steps = kCheb_pre + m;
+        }
+    }
     ka.fmt = c->fmt;
     ka.mass_fix = (params->flags & FDIRW_F_NO_MASS_FIX) ? 0 : 1;
     ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;
@@ -427,7 +506,11 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             ka.n_list = dr.n_class;
             ka.class_w = class_w;
             ka.class_diag = class_diag;
-            e = launch_kgen(ka, g.R, s);
+            if (e == cudaSuccess) e = cudaEventCreate(&c->kev[0]);
+            if (e == cudaSuccess) e = cudaEventCreate(&c->kev[1]);
+            if (e == cudaSuccess) e = cudaEventRecord(c->kev[0], s);
+            if (e == cudaSuccess) e = launch_kgen(ka, g.R, s);
+            if (e == cudaSuccess) e = cudaEventRecord(c->kev[1], s);
             ExpandArgs ea{class_pad, class_w, class_diag, nullptr, nullptr, g.nx, g.ny, g.nxq, g.tile, g.tpp,
                           g.n_tiles, g.nxp, g.nyp};
             size_t w_elems = g.w_elems, d_elems = g.diag_elems;
@@ -474,9 +557,16 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         ka.diag = c->diag;
         BAIL_CUDA(cudaMemsetAsync(c->Wt, 0, g.w_elems * c->b_w, s));
         BAIL_CUDA(cudaMemsetAsync(c->diag, 0, g.diag_elems * 4, s));
+        if (!c->kev[0]) BAIL_CUDA(cudaEventCreate(&c->kev[0]));
+        if (!c->kev[1]) BAIL_CUDA(cudaEventCreate(&c->kev[1]));
+        BAIL_CUDA(cudaEventRecord(c->kev[0], s));
         BAIL_CUDA(launch_kgen(ka, g.R, s));
+        BAIL_CUDA(cudaEventRecord(c->kev[1], s));
     }
     BAIL_CUDA(cudaStreamSynchronize(s));
+    cudaFree(c->cheb_d);
+    c->cheb_d = nullptr;
+    BAIL_CUDA(cudaEventElapsedTime(&c->kgen_ms, c->kev[0], c->kev[1]));
 
     c->v_far = params->v_far;
     c->far = params->v_far > 0;
@@ -883,6 +973,8 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->n_tiles = g.n_tiles;
     info->kgen_sources = c->kgen_sources;
     info->kgen_windows = c->kgen_windows;
+    info->kgen_steps = c->kgen_steps;
+    info->kgen_kernel_ms = c->kgen_ms;
     info->chunks = (uint64_t)g.nzl * g.ny * g.nxq;
     info->uniform_chunks = (uint64_t)c->ut.n_uniform;
     info->uniform_classes = c->ut.n_u;
@@ -921,6 +1013,9 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
     pl->weight_bytes = (uint64_t)g.w_elems * b_w + (uint64_t)g.diag_elems * 4;
     pl->state_bytes = (uint64_t)g.state_elems * 8;
     pl->n_fd = d.n_fd;
+    std::vector<float> cheb;
+    const int m = kgen_cheb(*p, d, &cheb);
+    pl->kgen_steps = m > 0 ? kCheb_pre + m : d.n_fd;
     return FDIRW_OK;
 }
 

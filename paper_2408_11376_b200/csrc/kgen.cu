@@ -40,6 +40,7 @@ struct KgenShape {
     static constexpr size_t smem_floats = 2 * (size_t)NT * Lp;             // double-buffered, column-major
     static constexpr size_t buf_bytes = smem_floats * (F64 ? 8 : 4);
     static constexpr size_t smem_bytes = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
+    static constexpr size_t cheb_off = smem_bytes;  // Chebyshev coefficients c_0..c_m (fp32) follow
 };
 
 __device__ __forceinline__ double warp_sum_f64(double v)
@@ -135,6 +136,11 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT) kgen_kernel(const KgenA
     const int nx = a.nx, ny = a.ny, nz = a.nz;
     const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
+    if (!F64 && a.cheb_m) {
+        float* cc = reinterpret_cast<float*>(smem_raw + S::cheb_off);
+        for (int i = t; i <= a.cheb_m; i += NT) cc[i] = a.cheb_c[i];
+        // (the first window's __syncthreads below orders these stores before any read)
+    }
     for (long it = blockIdx.x; it < nsrc; it += gridDim.x) {
         const long src = a.src_list ? (long)a.src_list[it] : it;
         const int sx = (int)(src % nx);
@@ -195,39 +201,49 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT) kgen_kernel(const KgenA
                 }
             }
         } else {
+        // Face numbers in registers: λ for the direct substeps; 2μ = 4λ/(1 − a) (rounded once
+        // from fp64 on the host) for the Chebyshev recurrence, which steps the mapped operator
+        // Â = (2A − (1 + a)I)/(1 − a) = I + Σ μ_f (c_f − c).
         float lzp[L], lzm[L];  // own +z / −z face numbers (asymmetric next to the reservoir)
         unsigned long long lxm2[Lp / 2], lxp2[Lp / 2], lym2[Lp / 2], lyp2[Lp / 2];  // (z, z+1) pairs
+        auto faces = [&](const float fff, const float ffs, const float fss) {
 #pragma unroll
-        for (int h = 0; h < Lp / 2; ++h) {
-            float v[4][2];
+            for (int h = 0; h < Lp / 2; ++h) {
+                float v[4][2];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int z = 2 * h + u;
-                const int i = z * LL + t;
-                const bool ok = col && z < L;
-                const unsigned p = ok ? ph[i] : 2u;
-                v[0][u] = (ok && oxm) ? face_lambda(p, ph[i + oxm], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-                v[1][u] = (ok && oxp) ? face_lambda(p, ph[i + oxp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-                v[2][u] = (ok && oym) ? face_lambda(p, ph[i + oym], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-                v[3][u] = (ok && oyp) ? face_lambda(p, ph[i + oyp], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-                if (z < L) {
-                    lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
-                    lzm[z] = (col && z > 0) ? face_lambda(p, ph[i - LL], a.lam_ff, a.lam_fs, a.lam_ss) : 0.f;
+                for (int u = 0; u < 2; ++u) {
+                    const int z = 2 * h + u;
+                    const int i = z * LL + t;
+                    const bool ok = col && z < L;
+                    const unsigned p = ok ? ph[i] : 2u;
+                    v[0][u] = (ok && oxm) ? face_lambda(p, ph[i + oxm], fff, ffs, fss) : 0.f;
+                    v[1][u] = (ok && oxp) ? face_lambda(p, ph[i + oxp], fff, ffs, fss) : 0.f;
+                    v[2][u] = (ok && oym) ? face_lambda(p, ph[i + oym], fff, ffs, fss) : 0.f;
+                    v[3][u] = (ok && oyp) ? face_lambda(p, ph[i + oyp], fff, ffs, fss) : 0.f;
+                    if (z < L) {
+                        lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], fff, ffs, fss) : 0.f;
+                        lzm[z] = (col && z > 0) ? face_lambda(p, ph[i - LL], fff, ffs, fss) : 0.f;
+                    }
                 }
-                c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
+                lxm2[h] = pk2(v[0][0], v[0][1]);
+                lxp2[h] = pk2(v[1][0], v[1][1]);
+                lym2[h] = pk2(v[2][0], v[2][1]);
+                lyp2[h] = pk2(v[3][0], v[3][1]);
             }
-            lxm2[h] = pk2(v[0][0], v[0][1]);
-            lxp2[h] = pk2(v[1][0], v[1][1]);
-            lym2[h] = pk2(v[2][0], v[2][1]);
-            lyp2[h] = pk2(v[3][0], v[3][1]);
-        }
+        };
+        faces(a.lam_ff, a.lam_fs, a.lam_ss);
+#pragma unroll
+        for (int z = 0; z < Lp; ++z) c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
 
         // n_fd Jacobi substeps; faces summed −x,+x,−y,+y,−z,+z.  The window lives in
         // smem column-major (thread t's column at t·Lp, float4-aligned): a thread
         // reads each lateral neighbour column with Lp/4 128-bit loads (conflict-free
         // for Lp ∈ {4, 8, 12, 20}), adds the four lateral fluxes two cells at a time
         // (FADD2/FFMA2), then the two z fluxes from its own registers.
-        for (int k = 0; k < a.n_fd; ++k) {
+        // Direct: all n_fd substeps.  Chebyshev: the first cheb_pre substeps (the peaked start,
+        // whose large entries would otherwise feed the recurrence's rounding), then the recurrence.
+        const int n_direct = a.cheb_m ? a.cheb_pre : a.n_fd;
+        for (int k = 0; k < n_direct; ++k) {
             float* b = buf + (k & 1) * (NT * Lp);
             if (col) {
 #pragma unroll
@@ -256,16 +272,93 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT) kgen_kernel(const KgenA
                         upk2(acc, nw[2 * h], nw[2 * h + 1]);
                     }
                 }
+                // z faces: one difference per face, used by both cells (c_{z−1} − c_z is
+                // exactly −(c_z − c_{z−1}) in IEEE arithmetic, so the bits do not change)
+                float dz[L > 1 ? L - 1 : 1];
+#pragma unroll
+                for (int z = 0; z + 1 < L; ++z) dz[z] = c[z + 1] - c[z];
 #pragma unroll
                 for (int z = 0; z < L; ++z) {
                     float acc = nw[z];
-                    if (z > 0) acc = fmaf(lzm[z], c[z - 1] - c[z], acc);
-                    if (z < L - 1) acc = fmaf(lzp[z], c[z + 1] - c[z], acc);
+                    if (z > 0) acc = fmaf(lzm[z], -dz[z - 1], acc);
+                    if (z < L - 1) acc = fmaf(lzp[z], dz[z], acc);
                     nw[z] = acc;
                 }
 #pragma unroll
                 for (int z = 0; z < L; ++z) c[z] = nw[z];
             }
+        }
+        if (a.cheb_m) {
+            // Chebyshev evaluation of the rest, A^{n_fd − pre} v with v = A^{pre} δ_s (DESIGN.md
+            // §7, reading A29): x^n' = Σ_k c_k T_k(y) on the spectrum [a, 1] of A,
+            // y = (2x − 1 − a)/(1 − a), all c_k ≥ 0 with Σ c_k = 1, truncated at degree m where the
+            // tail Σ_{k>m} c_k ≤ 1e-10 (so ‖p_m(A)v − A^n' v‖₂ ≤ 1e-10 ‖v‖₂).  Three-term recurrence
+            // t_{k+1} = 2Â t_k − t_{k−1}, t_0 = v, t_1 = Â v; p = Σ c_k t_k.  Each step is one stencil
+            // pass of the direct substep's cost (+2 FMA): pre + m ≈ 8 + 157 passes instead of
+            // n_fd = 1000 at Table 1's λ = 0.1.
+            // State: c[] = t (A), pv[] = t_{k−1} (B) overwritten in place by t_{k+1}, acc[] = p.
+            faces(a.mu2_ff, a.mu2_fs, a.mu2_ss);
+            const float* cc = reinterpret_cast<const float*>(smem_raw + S::cheb_off);
+            float pv[Lp], acc[L];
+#pragma unroll
+            for (int z = 0; z < Lp; ++z) pv[z] = 0.f;
+#pragma unroll
+            for (int z = 0; z < L; ++z) acc[z] = c[z] * cc[0];
+            // prv ← κ·Â·cur − prv, κ = 2 (κ = 1, prv = 0 on the first step: 2Âδ·½, exact)
+            auto step = [&](float (&cur)[Lp], float (&prv)[Lp], const int k, const bool first) {
+                float* b = buf + ((k + n_direct) & 1) * (NT * Lp);
+                if (col) {
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        *reinterpret_cast<float4*>(b + t * Lp + 4 * q) =
+                            make_float4(cur[4 * q], cur[4 * q + 1], cur[4 * q + 2], cur[4 * q + 3]);
+                }
+                __syncthreads();
+                const float ck = cc[k + 1];
+                if (col) {
+                    float nw[Lp];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const float4 xm = *reinterpret_cast<const float4*>(b + (t + oxm) * Lp + 4 * q);
+                        const float4 xp = *reinterpret_cast<const float4*>(b + (t + oxp) * Lp + 4 * q);
+                        const float4 ym = *reinterpret_cast<const float4*>(b + (t + oym) * Lp + 4 * q);
+                        const float4 yp = *reinterpret_cast<const float4*>(b + (t + oyp) * Lp + 4 * q);
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int h = 2 * q + hh;
+                            const unsigned long long c2 = pk2(cur[2 * h], cur[2 * h + 1]);
+                            unsigned long long s2 = fma2(pk2(2.f, 2.f), c2, pk2(-prv[2 * h], -prv[2 * h + 1]));
+                            s2 = fma2(lxm2[h], sub2(hh ? pk2(xm.z, xm.w) : pk2(xm.x, xm.y), c2), s2);
+                            s2 = fma2(lxp2[h], sub2(hh ? pk2(xp.z, xp.w) : pk2(xp.x, xp.y), c2), s2);
+                            s2 = fma2(lym2[h], sub2(hh ? pk2(ym.z, ym.w) : pk2(ym.x, ym.y), c2), s2);
+                            s2 = fma2(lyp2[h], sub2(hh ? pk2(yp.z, yp.w) : pk2(yp.x, yp.y), c2), s2);
+                            upk2(s2, nw[2 * h], nw[2 * h + 1]);
+                        }
+                    }
+                    float dz[L > 1 ? L - 1 : 1];
+#pragma unroll
+                    for (int z = 0; z + 1 < L; ++z) dz[z] = cur[z + 1] - cur[z];
+#pragma unroll
+                    for (int z = 0; z < L; ++z) {
+                        float v = nw[z];
+                        if (z > 0) v = fmaf(lzm[z], -dz[z - 1], v);
+                        if (z < L - 1) v = fmaf(lzp[z], dz[z], v);
+                        if (first) v *= 0.5f;
+                        prv[z] = v;
+                        acc[z] = fmaf(ck, v, acc[z]);
+                    }
+                }
+            };
+            const int m = a.cheb_m;
+            step(c, pv, 0, true);  // pv = t_1
+            for (int k = 1; k < m; k += 2) {
+                step(pv, c, k, false);                  // c  = t_{k+1}
+                if (k + 1 < m) step(c, pv, k + 1, false);  // pv = t_{k+2}
+            }
+            // A^n δ ≥ 0 (maximum principle, λ_max ≤ 1/6): clamping the truncation / rounding
+            // noise of tiny entries at 0 can only move them closer to it
+#pragma unroll
+            for (int z = 0; z < Lp; ++z) c[z] = z < L ? fmaxf(acc[z < L ? z : 0], 0.f) : 0.f;
         }
         }  // fp32 substeps
 
@@ -349,18 +442,19 @@ static cudaError_t launch_kgen_r(const KgenArgs& a, cudaStream_t s)
     using S = KgenShape<R, F64>;
     const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
     if (nsrc <= 0) return cudaSuccess;
+    const size_t smem = S::smem_bytes + (F64 || !a.cheb_m ? 0 : ((size_t)(a.cheb_m + 1) * 4 + 15) / 16 * 16);
     cudaError_t e = cudaFuncSetAttribute(kgen_kernel<R, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)S::smem_bytes);
+                                         (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_kernel<R, F64>, S::NT, S::smem_bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_kernel<R, F64>, S::NT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     long grid = (long)sms * per_sm;
     if (grid > nsrc) grid = nsrc;
-    kgen_kernel<R, F64><<<(unsigned)grid, S::NT, S::smem_bytes, s>>>(a);
+    kgen_kernel<R, F64><<<(unsigned)grid, S::NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 

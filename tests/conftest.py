@@ -19,3 +19,14 @@ def oracle_lib():
 
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def fd_cpu():
+    """The built C-ABI library, for host-only calls (fdirw_make_plan); no GPU needed."""
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2408_11376_b200 as fd
+
+    return fd

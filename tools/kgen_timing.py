@@ -24,5 +24,6 @@ for i in range(reps):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
     info = ctx.info
-    print("%s build %d: %.3f s  windows %d  sources %d" % (name, i, dt, info["kgen_windows"], info["kgen_sources"]))
+    print("%s build %d: %.3f s  kgen kernel %.1f ms (%d passes/window)  windows %d  sources %d"
+          % (name, i, dt, info["kgen_kernel_ms"], info["kgen_steps"], info["kgen_windows"], info["kgen_sources"]))
     fd.destroy(ctx)

@@ -85,6 +85,10 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weig
                                   Chebyshev recurrence of degree m ≈ 160 (at n_fd = 1000, λ = 0.1)
                                   over the same stencil, truncation ‖·‖₂ ≤ 1e-10 (reading A29;
                                   fdirw_info.kgen_steps reports which)                            */
+#define FDIRW_F_NO_BULK_STREAM 64u /* superposition streams each tile's weights with per-thread 128-bit
+                                  loads instead of TMA bulk copies into shared-memory stages (the
+                                  default for launches of >= 2 CTAs per SM).  Identical results;
+                                  for A/B measurement                              */
 
 /* The paper's problem statement (Table 1) + north_star's window radius / precision. */
 typedef struct {

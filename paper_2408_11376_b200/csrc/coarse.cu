@@ -32,6 +32,7 @@
 #include <string>
 #include <vector>
 
+#include "bulk.cuh"
 #include "fdirw_internal.h"
 
 using namespace fdirw;
@@ -370,37 +371,6 @@ __global__ void __launch_bounds__(256) k_gemv(const WT* __restrict__ P, const fl
 // are those of k_gemv, so the two kernels give identical bits.
 constexpr int GEMV_NW = 4, GEMV_RB = 2;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint32_t a, int cnt)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity)
-{
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar, uint64_t pol)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(mbar), "l"(pol)
-        : "memory");
-}
-
 template <typename WT>
 __global__ void __launch_bounds__((GEMV_NW + 1) * 32) k_gemv_bulk(const WT* __restrict__ P,
                                                                   const float* __restrict__ Pdiag,
@@ -424,7 +394,7 @@ __global__ void __launch_bounds__((GEMV_NW + 1) * 32) k_gemv_bulk(const WT* __re
             mbar_init(smem_u32(full + i), 1);
             mbar_init(smem_u32(empty + i), 1);
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_init_fence();
     }
     for (long i = threadIdx.x; i < ldp / 4; i += blockDim.x)
         reinterpret_cast<float4*>(Cs)[i] = __ldg(reinterpret_cast<const float4*>(C) + i);

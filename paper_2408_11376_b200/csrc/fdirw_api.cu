@@ -36,6 +36,7 @@ struct fdirw_ctx {
     void* comm = nullptr;
     uint64_t kgen_sources = 0, kgen_windows = 0;
     int kgen_steps = 0;  // stencil passes per window: Chebyshev degree m, or n_fd (direct)
+    bool no_bulk = false;  // FDIRW_F_NO_BULK_STREAM
     float* cheb_d = nullptr;  // kgen's Chebyshev coefficients (build only)
     cudaEvent_t kev[2] = {nullptr, nullptr};
     float kgen_ms = 0.f;      // device time of the kgen launch (CUDA events on the build stream)
@@ -234,7 +235,7 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
     if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE | FDIRW_F_KGEN_FP64 |
-                     FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT))
+                     FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT | FDIRW_F_NO_BULK_STREAM))
         return fail(FDIRW_E_INVALID, "unknown flags");
     if ((p->flags & FDIRW_F_SYMMETRIC_RULE) && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_SYMMETRIC_RULE is not combined with FDIRW_F_DEDUP_STORAGE");
@@ -456,6 +457,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     }
     ka.n_fd = d.n_fd;
     c->kgen_steps = d.n_fd;
+    c->no_bulk = (params->flags & FDIRW_F_NO_BULK_STREAM) != 0;
     std::vector<float> cheb;
     {
         const double lmax = std::max(d.lam_ff, std::max(d.lam_fs, d.lam_ss));
@@ -658,6 +660,7 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
         a.gap_len = gap1 - gap0;
         a.gap_last = gap_last;
     }
+    a.no_bulk = c->no_bulk;
     a.list = c->ut.dense_list;  // N4 (null unless FDIRW_F_DEDUP_STORAGE): compacted non-uniform chunks
     a.n_list = c->ut.n_dense;
     if (c->far && far_terms) {

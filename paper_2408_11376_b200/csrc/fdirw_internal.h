@@ -141,6 +141,7 @@ struct SuperArgs {
     float* push_lo = nullptr;
     float* push_hi = nullptr;
     int nzl = 0, pR = 0;
+    bool no_bulk = false;  // FDIRW_F_NO_BULK_STREAM: weights by per-thread loads, not TMA stages
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
 

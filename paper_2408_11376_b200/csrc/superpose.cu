@@ -26,6 +26,7 @@
 
 #include <type_traits>
 
+#include "bulk.cuh"
 #include "fdirw_internal.h"
 #include "layout.cuh"
 
@@ -158,6 +159,44 @@ __device__ __forceinline__ void do_row(const float* srow, const WT* wp, size_t w
         if (CENTRE_ROW && ox == 0) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) p[j] = fmaf(w[ox + R][j], seg[j - ox + 8], p[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float s, e;
+        two_sum(hi[j], p[j], s, e);
+        hi[j] = s;
+        lo[j] = __fadd_rn(lo[j], e);
+    }
+}
+
+// Staged form (superpose_bulk_kernel): the row's weights were copied into shared memory by
+// the TMA engine; thread e's 8 weights of slot k sit at wb + k·slotB (16 B, or 2 × 16 B for
+// fp32).  Decode and arithmetic are do_row's exactly (identical bits).
+template <int R, typename WT, bool CENTRE_ROW>
+__device__ __forceinline__ void do_row_s(const float* srow, const unsigned char* wb, uint32_t slotB, float hi[8],
+                                         float lo[8])
+{
+    float seg[24];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const float4 v = ld_c(srow + 4 * i);
+        seg[4 * i] = v.x; seg[4 * i + 1] = v.y; seg[4 * i + 2] = v.z; seg[4 * i + 3] = v.w;
+    }
+    float p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = 0.f;
+#pragma unroll
+    for (int ox = -R; ox <= R; ++ox) {
+        if (CENTRE_ROW && ox == 0) continue;
+        const int k = CENTRE_ROW ? (ox < 0 ? ox + R : ox + R - 1) : ox + R;
+        uint4 raw[RawW<WT>::N];
+        raw[0] = *reinterpret_cast<const uint4*>(wb + (size_t)k * slotB);
+        if constexpr (RawW<WT>::N == 2) raw[1] = *reinterpret_cast<const uint4*>(wb + (size_t)k * slotB + 16);
+        float w[8];
+        if constexpr (RawW<WT>::N == 2) decode_w(raw, w);
+        else decode_w<WT>(raw, w);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) p[j] = fmaf(w[j], seg[j - ox + 8], p[j]);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -325,10 +364,10 @@ cudaError_t launch_superpose_uniform(const UniArgs& a, int R, cudaStream_t s)
     }
 }
 
-// Deterministic fp64 sum over the CTA (≤ 256 threads): shuffle tree, then warps in order.
+// Deterministic fp64 sum over the CTA (≤ 1024 threads): shuffle tree, then warps in order.
 __device__ __forceinline__ double tile_block_sum(double s)
 {
-    __shared__ double red[8];
+    __shared__ double red[32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -339,17 +378,24 @@ __device__ __forceinline__ double tile_block_sum(double s)
     return t;  // valid in thread 0
 }
 
-template <int R, typename WT, bool PF = false>
-__device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
+// The tile a CTA works on, and thread e's chunk in it.
+struct TileCtx {
+    int tile, zl, y, x;
+    bool real;          // false: dummy chunk past the end of the plane (or of the N4 list)
+    const float* c0;    // C_old(z, y, x) in the padded state
+    long nxp, plane;
+};
+
+template <int R>
+__device__ __forceinline__ TileCtx tile_ctx(const SuperArgs& a, int blk, int e)
 {
-    constexpr int L = 2 * R + 1, K = L * L * L;
+    TileCtx t;
     int tile = a.t_begin + blk;  // weight tile (compact tile when a.list, N4)
     if (a.gap_len) {
         const int nb = a.t_end - a.t_begin - a.gap_len;  // CTAs of the two outer bands
         if (a.gap_last && blk >= nb) tile = a.gap_at + (blk - nb);
         else if (tile >= a.gap_at) tile += a.gap_len;
     }
-    const int e = threadIdx.x;
     int zl, q;
     bool real;
     if (a.list) {  // N4: tiles hold only the non-uniform chunks, in chunk order
@@ -364,62 +410,51 @@ __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
         q = (tile % a.tpp) * a.tile + e;
         real = q < a.ny * a.nxq;  // false: dummy chunk at the end of the plane
     }
-    if (!real && a.tile_sum == nullptr) return;
-    const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;  // dummies: harmless reads
-    const long nxp = a.nxp, plane = (long)a.nyp * nxp;
-    const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;  // C_old(z, y, x)
-    size_t wstride = (size_t)a.tile * 8;
-    const WT* wt = reinterpret_cast<const WT*>(a.Wt) + ((size_t)tile * (K - 1) * a.tile + e) * 8;
-    uint64_t pol = evict_first_policy();
-    const float* dp = a.diag + ((size_t)tile * a.tile + e) * 8;
+    t.tile = tile;
+    t.zl = zl;
+    t.real = real;
+    t.y = real ? q / a.nxq : 0;
+    t.x = real ? (q % a.nxq) * 8 : 0;  // dummies: harmless reads
+    t.nxp = a.nxp;
+    t.plane = (long)a.nyp * t.nxp;
+    t.c0 = a.cpad + (zl + R) * t.plane + (long)(t.y + R) * t.nxp + kPadX + t.x;
+    return t;
+}
 
-    float hi[8], lo[8];
+// hi = d·C_old(x) (the diagonal term first, DESIGN §6 order), lo = 0
+__device__ __forceinline__ void diag_init(const SuperArgs& a, const TileCtx& t, int e, float hi[8], float lo[8])
+{
 #pragma unroll
     for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.f;
-    if (real) {
-        {
-            const float4 d0 = __ldg(reinterpret_cast<const float4*>(dp));
-            const float4 d1 = __ldg(reinterpret_cast<const float4*>(dp + 4));
-            const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
-            hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
-            hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
-        }
-        if constexpr (PF) {
-            // same rows in the same order, each row's weights loaded while the previous row
-            // computes (ping-pong register buffers; L² − 1 is even)
-            uint4 ra[L][RawW<WT>::N], rb[L][RawW<WT>::N];
-            const WT* wr = wt + (size_t)(L - 1) * wstride;
-            load_row_raw<R, WT, L - 1>(wt, wstride, pol, ra);
-            load_row_raw<R, WT, L>(wr, wstride, pol, rb);
-            fma_row_raw<R, WT, true>(c0 - 8, ra, hi, lo);
-            constexpr int NR = L * L - 1, RC = R * L + R;
-#pragma unroll 1
-            for (int i = 0; i < NR; i += 2) {
-                const int r0 = i < RC ? i : i + 1, r1 = i + 1 < RC ? i + 1 : i + 2;
-                if (i + 1 < NR) load_row_raw<R, WT, L>(wr + (size_t)L * wstride, wstride, pol, ra);
-                fma_row_raw<R, WT, false>(c0 - (long)(r0 / L - R) * plane - (long)(r0 % L - R) * nxp - 8, rb, hi, lo);
-                wr += (size_t)L * wstride;
-                if (i + 1 >= NR) break;
-                if (i + 2 < NR) load_row_raw<R, WT, L>(wr + (size_t)L * wstride, wstride, pol, rb);
-                fma_row_raw<R, WT, false>(c0 - (long)(r1 / L - R) * plane - (long)(r1 % L - R) * nxp - 8, ra, hi, lo);
-                wr += (size_t)L * wstride;
-            }
-        } else {
-        // centre row (oz = oy = 0): slots [0, L−1)
-        do_row<R, WT, true>(c0 - 8, wt, wstride, pol, hi, lo);
-        // remaining rows, ascending (oz, oy); source row of target row (z, y) is (z − oz, y − oy)
-        const WT* wr = wt + (size_t)(L - 1) * wstride;
-#pragma unroll 1
-        for (int r = 0; r < L * L; ++r) {
-            if (r == R * L + R) continue;
-            const int oz = r / L - R, oy = r % L - R;
-            const float* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
-            do_row<R, WT, false>(srow, wr, wstride, pol, hi, lo);
-            wr += (size_t)L * wstride;
-        }
-        }
-    }
+    if (!t.real) return;
+    const float* dp = a.diag + ((size_t)t.tile * a.tile + e) * 8;
+    const float4 d0 = __ldg(reinterpret_cast<const float4*>(dp));
+    const float4 d1 = __ldg(reinterpret_cast<const float4*>(dp + 4));
+    const float4 v0 = ld_c(t.c0), v1 = ld_c(t.c0 + 4);
+    hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
+    hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
+}
 
+// Stored row i of a tile (i = 0: the centre row, L − 1 slots; i ≥ 1: row r of (oz, oy)
+// ascending with the centre skipped, L slots) → its source row pointer (C_old − 8).
+template <int R>
+__device__ __forceinline__ const float* row_src(const TileCtx& t, int i)
+{
+    constexpr int L = 2 * R + 1;
+    if (i == 0) return t.c0 - 8;
+    const int r = (i - 1) < R * L + R ? i - 1 : i;
+    const int oz = r / L - R, oy = r % L - R;
+    return t.c0 - (long)oz * t.plane - (long)oy * t.nxp - 8;
+}
+
+// acc = hi + lo; N2 boundary term; store; P2P halo pushes; N2 per-tile Σ.  Every thread of
+// the CTA calls it (tile_sum's reduction is CTA-wide).
+__device__ __forceinline__ void tile_epilogue(const SuperArgs& a, const TileCtx& t, int e, const float hi[8],
+                                              const float lo[8])
+{
+    const int x = t.x, y = t.y, zl = t.zl, tile = t.tile;
+    const bool real = t.real;
+    const long nxp = t.nxp, plane = t.plane;
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(hi[j], lo[j]);
@@ -474,10 +509,145 @@ __device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
     }
 }
 
+template <int R, typename WT, bool PF = false>
+__device__ __forceinline__ void dense_body(const SuperArgs& a, int blk)
+{
+    constexpr int L = 2 * R + 1, K = L * L * L;
+    const int e = threadIdx.x;
+    const TileCtx t = tile_ctx<R>(a, blk, e);
+    if (!t.real && a.tile_sum == nullptr) return;
+    size_t wstride = (size_t)a.tile * 8;
+    const WT* wt = reinterpret_cast<const WT*>(a.Wt) + ((size_t)t.tile * (K - 1) * a.tile + e) * 8;
+    uint64_t pol = evict_first_policy();
+    const float* c0 = t.c0;
+    const long nxp = t.nxp, plane = t.plane;
+
+    float hi[8], lo[8];
+    diag_init(a, t, e, hi, lo);
+    if (t.real) {
+        if constexpr (PF) {
+            // same rows in the same order, each row's weights loaded while the previous row
+            // computes (ping-pong register buffers; L² − 1 is even)
+            uint4 ra[L][RawW<WT>::N], rb[L][RawW<WT>::N];
+            const WT* wr = wt + (size_t)(L - 1) * wstride;
+            load_row_raw<R, WT, L - 1>(wt, wstride, pol, ra);
+            load_row_raw<R, WT, L>(wr, wstride, pol, rb);
+            fma_row_raw<R, WT, true>(c0 - 8, ra, hi, lo);
+            constexpr int NR = L * L - 1, RC = R * L + R;
+#pragma unroll 1
+            for (int i = 0; i < NR; i += 2) {
+                const int r0 = i < RC ? i : i + 1, r1 = i + 1 < RC ? i + 1 : i + 2;
+                if (i + 1 < NR) load_row_raw<R, WT, L>(wr + (size_t)L * wstride, wstride, pol, ra);
+                fma_row_raw<R, WT, false>(c0 - (long)(r0 / L - R) * plane - (long)(r0 % L - R) * nxp - 8, rb, hi, lo);
+                wr += (size_t)L * wstride;
+                if (i + 1 >= NR) break;
+                if (i + 2 < NR) load_row_raw<R, WT, L>(wr + (size_t)L * wstride, wstride, pol, rb);
+                fma_row_raw<R, WT, false>(c0 - (long)(r1 / L - R) * plane - (long)(r1 % L - R) * nxp - 8, ra, hi, lo);
+                wr += (size_t)L * wstride;
+            }
+        } else {
+        // centre row (oz = oy = 0): slots [0, L−1)
+        do_row<R, WT, true>(c0 - 8, wt, wstride, pol, hi, lo);
+        // remaining rows, ascending (oz, oy); source row of target row (z, y) is (z − oz, y − oy)
+        const WT* wr = wt + (size_t)(L - 1) * wstride;
+#pragma unroll 1
+        for (int r = 0; r < L * L; ++r) {
+            if (r == R * L + R) continue;
+            const int oz = r / L - R, oy = r % L - R;
+            const float* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
+            do_row<R, WT, false>(srow, wr, wstride, pol, hi, lo);
+            wr += (size_t)L * wstride;
+        }
+        }
+    }
+
+    tile_epilogue(a, t, e, hi, lo);
+}
+
 template <int R, typename WT, bool PF>
 __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
 {
     dense_body<R, WT, PF>(a, blockIdx.x);
+}
+
+// TMA-staged weight stream (default for dense tiles of 256 chunks).  A CTA = one tile:
+// warps 0-7 compute (thread e = chunk e, exactly dense_body's arithmetic), warp 8's lane 0
+// streams the tile's contiguous weight region row by row (one stored row = L or L − 1 slots
+// of tile·8 weights: 44 KB at R5 bf16) with cp.async.bulk into a ring of S shared-memory
+// stages.  full[st] completes when a row's bytes have landed (expect_tx), empty[st] when all 8
+// compute warps have read it; the producer refills stage st for row i + S only after that.
+// The weight bytes in flight no longer depend on how many warps are waiting on loads: each
+// SM keeps up to 2 CTAs × S rows outstanding with one thread issuing them.
+constexpr int kBulkWarps = 8;
+template <int R, typename WT>
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(const SuperArgs a, int S)
+{
+    constexpr int L = 2 * R + 1, K = L * L * L, NROW = L * L;
+    extern __shared__ __align__(128) unsigned char smem_b[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_b);
+    uint64_t* empty = full + S;
+    unsigned char* stg = smem_b + 128;
+    const uint32_t slotB = (uint32_t)a.tile * 8 * sizeof(WT), stageB = (uint32_t)L * slotB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(smem_u32(full + i), 1);
+            mbar_init(smem_u32(empty + i), kBulkWarps);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+    const bool producer = warp == kBulkWarps;
+    const int e = producer ? 0 : (int)threadIdx.x;
+    TileCtx t = tile_ctx<R>(a, blockIdx.x, e);
+    float hi[8], lo[8];
+    if (producer) {
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.Wt) + (size_t)t.tile * (K - 1) * slotB;
+            for (int i = 0; i < NROW; ++i) {
+                const int st = i % S, u = i / S;
+                const uint32_t n = (i == 0 ? L - 1 : L) * slotB;
+                if (u > 0) mbar_wait(smem_u32(empty + st), (u - 1) & 1);
+                mbar_expect_tx(smem_u32(full + st), n);
+                bulk_g2s(smem_u32(stg + (size_t)st * stageB), src, n, smem_u32(full + st), pol);
+                src += n;
+            }
+        }
+        t.real = false;  // joins the epilogue only for tile_sum's CTA-wide reduction
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.f;
+    } else {
+        diag_init(a, t, e, hi, lo);
+        const unsigned char* wb = stg + (size_t)e * 8 * sizeof(WT);
+        for (int i = 0; i < NROW; ++i) {
+            const int st = i % S, u = i / S;
+            mbar_wait(smem_u32(full + st), u & 1);
+            if (t.real) {
+                if (i == 0) do_row_s<R, WT, true>(row_src<R>(t, 0), wb + (size_t)st * stageB, slotB, hi, lo);
+                else do_row_s<R, WT, false>(row_src<R>(t, i), wb + (size_t)st * stageB, slotB, hi, lo);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(empty + st));
+        }
+    }
+    tile_epilogue(a, t, e, hi, lo);
+}
+
+// stages of the bulk kernel: 2 CTAs per SM with ≥ 2 stages each, else 1 CTA with ≥ 2; 0 = the
+// row does not fit twice (register path)
+static int bulk_stages(int R, int b_w, int tile, int* ctas_per_sm)
+{
+    const size_t row = (size_t)(2 * R + 1) * tile * 8 * b_w, avail = 227 * 1024 - 128;
+    const size_t half = (228 * 1024) / 2 - 1024 - 128;  // per CTA at 2 CTAs/SM (1 KB reserved each)
+    int S = (int)(half / row);
+    if (S >= 2) {
+        *ctas_per_sm = 2;
+        return S > 8 ? 8 : S;
+    }
+    S = (int)(avail / row);
+    *ctas_per_sm = 1;
+    return S >= 2 ? (S > 8 ? 8 : S) : 0;
 }
 
 // N4: ONE launch mixing the HBM-bound dense tiles and the FMA-bound uniform blocks, the U
@@ -511,6 +681,27 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
     if (nblk <= 0) return cudaSuccess;
     // a launch of fewer than two CTAs per SM cannot keep enough weight loads in flight
     // through occupancy: those threads prefetch one row ahead instead (identical bits)
+    // TMA-staged weight stream for launches of ≥ 2 CTAs per SM (the common case); the
+    // register-prefetching body below for smaller launches (one wave: no CTA to overlap the
+    // pipeline fill with) or FDIRW_F_NO_BULK_STREAM.  Identical bits either way.
+    if (!a.no_bulk && nblk >= 2 * 148 && a.tile == kBulkWarps * 32) {
+        const int b_w = fmt == 0 ? 4 : 2;
+        int cps = 0;
+        const int S = bulk_stages(R, b_w, a.tile, &cps);
+        if (S > 0) {
+            const size_t smem = 128 + (size_t)S * (2 * R + 1) * a.tile * 8 * b_w;
+            const void* f = fmt == 0 ? (const void*)superpose_bulk_kernel<R, float>
+                          : fmt == 1 ? (const void*)superpose_bulk_kernel<R, __half>
+                                     : (const void*)superpose_bulk_kernel<R, __nv_bfloat16>;
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            const int nt = (kBulkWarps + 1) * 32;
+            if (fmt == 0) superpose_bulk_kernel<R, float><<<nblk, nt, smem, s>>>(a, S);
+            else if (fmt == 1) superpose_bulk_kernel<R, __half><<<nblk, nt, smem, s>>>(a, S);
+            else superpose_bulk_kernel<R, __nv_bfloat16><<<nblk, nt, smem, s>>>(a, S);
+            return cudaGetLastError();
+        }
+    }
     const bool pf = nblk < 2 * 148 && kPrefetchOK<R>(fmt);
     if (pf) {
         if (fmt == 0) superpose_kernel<R, float, PfOK<R, float>::v><<<nblk, a.tile, 0, s>>>(a);

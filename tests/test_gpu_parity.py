@@ -367,6 +367,39 @@ def test_kgen_chebyshev_vs_substeps_and_oracle(fd, oracle_lib, shape, R, D_slow,
     assert d.max() <= q * Wo[..., off].max() + 1e-9
 
 
+# ------------------------------------------------------------------ TMA-staged weight stream
+@pytest.mark.parametrize("cfgname,fmt", [("96", "fp32"), ("96", "bf16"), ("96", "fp16"), ("cfg3o", "bf16")])
+def test_bulk_stream_bitwise(fd, cfgname, fmt):
+    """The default superposition for launches of ≥ 2 CTAs/SM streams each tile's weights into
+    shared-memory stages with cp.async.bulk; FDIRW_F_NO_BULK_STREAM uses per-thread loads.  Same
+    arithmetic in the same order: bitwise equal fields (closed 96³ — 480 tiles; fp32 rows of
+    56 KB take the 1-CTA/SM 3-stage form, bf16/fp16 2 CTAs × 4 stages — and the open cfg3o
+    with the N2 p_BC term and per-tile sums)."""
+    import torch
+
+    if cfgname == "96":
+        shape = (96, 96, 96)
+        cfg = small_cfg(shape, 3, 100, D_slow=1e-3, weights=fmt)
+        mask = fi.porous_particle(shape, 30, pore_r=(1.0, 3.0), porosity=0.3, seed=7)
+    else:
+        cfg = fi.config(cfgname, weights=fmt)
+        mask = cfg.mask()
+    c0 = fi.initial_c(mask, "random", seed=5).astype(np.float32)
+    outs = []
+    for flags in (0, fd.F_NO_BULK_STREAM):
+        ctx = fd.build_kernels(lib_params(cfg, flags=flags), mask)
+        try:
+            assert ctx.info["n_tiles"] >= 2 * 148
+            c = torch.from_numpy(c0).cuda()
+            if cfg.v_far:
+                fd.far_init(ctx, c, cfg.c_far0)
+            fd.run(ctx, c, 3)
+            outs.append(c.cpu().numpy())
+        finally:
+            fd.destroy(ctx)
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
 # ------------------------------------------------------------------ window de-duplication
 @pytest.mark.parametrize("fmt,R,n_fd", [("bf16", 3, 100), ("fp32", 2, 1000), ("fp16", 4, 40)])
 def test_dedup_bitwise(fd, fmt, R, n_fd):

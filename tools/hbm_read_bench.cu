@@ -1,0 +1,153 @@
+// hbm_read_bench.cu — practical HBM read ceiling on this B200 for a streaming kernel like
+// superpose (128-bit loads, evict-first, many bytes in flight), vs the copy peak in
+// MEASURED_PEAKS.json.  Design input, not product.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/hbm_bin tools/hbm_read_bench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, unsigned long long pol)
+{
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+template <int U>
+__global__ void __launch_bounds__(256) rd(const uint4* __restrict__ a, size_t n16, unsigned* out)
+{
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    unsigned acc = 0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < n16; i += U * stride) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_stream(a + i + u * stride, pol);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+    for (; i < n16; i += stride) {
+        uint4 v = ld_stream(a + i, pol);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
+// chunked: each CTA streams one contiguous chunk (the superpose layout: one tile per CTA)
+template <int U>
+__global__ void __launch_bounds__(256) rd_chunk(const uint4* __restrict__ a, size_t chunk16, size_t nchunk, unsigned* out)
+{
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    unsigned acc = 0;
+    for (size_t c = blockIdx.x; c < nchunk; c += gridDim.x) {
+        const uint4* p = a + c * chunk16;
+        for (size_t i = threadIdx.x; i < chunk16; i += U * blockDim.x) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = (i + u * blockDim.x < chunk16) ? ld_stream(p + i + u * blockDim.x, pol) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+        }
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
+// superpose-like: one CTA per tile, per slot one 16-byte load per thread (4 KB per CTA);
+// SLOTMAJOR = false: tile-major [tile][slot][4 KB] (the current gather layout);
+// SLOTMAJOR = true: slot-major [slot][tile][4 KB] (concurrent tiles read neighbouring blocks)
+template <bool SLOTMAJOR, int U>
+__global__ void __launch_bounds__(256) rd_tiles(const uint4* __restrict__ a, int ntile, int nslot, unsigned* out)
+{
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    unsigned acc = 0;
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int s = 0; s < nslot; s += U) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int ss = s + u < nslot ? s + u : nslot - 1;
+                const size_t blk = SLOTMAJOR ? (size_t)ss * ntile + t : (size_t)t * nslot + ss;
+                v[u] = ld_stream(a + blk * 256 + threadIdx.x, pol);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+        }
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
+int main()
+{
+    const size_t bytes = 18905104640ull;  // cfg3's weight bytes
+    uint4* a;
+    unsigned* o;
+    if (cudaMalloc(&a, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
+    cudaMalloc(&o, 4);
+    cudaMemset(a, 1, bytes);
+    const size_t n16 = bytes / 16;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto timeit = [&](const char* name, auto launch) {
+        launch();
+        cudaDeviceSynchronize();
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            cudaEventRecord(e0);
+            launch();
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = ms < best ? ms : best;
+        }
+        printf("%-40s %.3f ms  %.1f GB/s\n", name, best, bytes / (best * 1e-3) / 1e9);
+    };
+    for (int bps : {4, 8, 16}) {
+        const int g = 148 * bps;
+        char nm[64];
+        snprintf(nm, 64, "grid-stride U=4 blocks/SM=%d", bps);
+        timeit(nm, [&] { rd<4><<<g, 256>>>(a, n16, o); });
+        snprintf(nm, 64, "grid-stride U=8 blocks/SM=%d", bps);
+        timeit(nm, [&] { rd<8><<<g, 256>>>(a, n16, o); });
+    }
+    // superpose-like: 3456 tiles of 5.47 MB each, one CTA per tile
+    const size_t nchunk = 3456, chunk16 = n16 / nchunk;
+    timeit("chunked 3456 tiles U=4 (grid=3456)", [&] { rd_chunk<4><<<nchunk, 256>>>(a, chunk16, nchunk, o); });
+    timeit("chunked 3456 tiles U=8 (grid=3456)", [&] { rd_chunk<8><<<nchunk, 256>>>(a, chunk16, nchunk, o); });
+    timeit("chunked 3456 tiles U=8 (grid=592)", [&] { rd_chunk<8><<<592, 256>>>(a, chunk16, nchunk, o); });
+    const int nslot = 1330;
+    for (int ntile : {3456, 2960}) {
+        const size_t need = (size_t)ntile * nslot * 4096;
+        if (need > bytes) continue;
+        const double gb = need / 1e9;
+        auto t2 = [&](const char* name, auto launch) {
+            launch();
+            cudaDeviceSynchronize();
+            float best = 1e30f;
+            for (int r = 0; r < 5; ++r) {
+                cudaEventRecord(e0);
+                launch();
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            printf("%-44s tiles=%d %.3f ms  %.1f GB/s\n", name, ntile, best, gb / (best * 1e-3));
+        };
+        t2("tile-major  U=4 grid=ntile", [&] { rd_tiles<false, 4><<<ntile, 256>>>(a, ntile, nslot, o); });
+        t2("tile-major  U=8 grid=ntile", [&] { rd_tiles<false, 8><<<ntile, 256>>>(a, ntile, nslot, o); });
+        t2("slot-major  U=4 grid=ntile", [&] { rd_tiles<true, 4><<<ntile, 256>>>(a, ntile, nslot, o); });
+        t2("slot-major  U=8 grid=ntile", [&] { rd_tiles<true, 8><<<ntile, 256>>>(a, ntile, nslot, o); });
+        t2("tile-major  U=8 grid=592", [&] { rd_tiles<false, 8><<<592, 256>>>(a, ntile, nslot, o); });
+        t2("slot-major  U=8 grid=592", [&] { rd_tiles<true, 8><<<592, 256>>>(a, ntile, nslot, o); });
+    }
+    printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}

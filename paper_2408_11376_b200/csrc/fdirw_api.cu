@@ -713,6 +713,7 @@ static cudaError_t superpose_n4_mixed(fdirw_ctx* c, const float* src, float* out
     a.nxp = g.nxp; a.nyp = g.nyp;
     a.t_begin = 0;
     a.t_end = c->ut.nd_tiles;
+    a.no_bulk = c->no_bulk;
     a.list = c->ut.dense_list;
     a.n_list = c->ut.n_dense;
     UniArgs u{};

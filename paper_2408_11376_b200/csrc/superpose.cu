@@ -172,16 +172,19 @@ __device__ __forceinline__ void do_row(const float* srow, const WT* wp, size_t w
 // Staged form (superpose_bulk_kernel): the row's weights were copied into shared memory by
 // the TMA engine; thread e's 8 weights of slot k sit at wb + k·slotB (16 B, or 2 × 16 B for
 // fp32).  Decode and arithmetic are do_row's exactly (identical bits).
-template <int R, typename WT, bool CENTRE_ROW>
-__device__ __forceinline__ void do_row_s(const float* srow, const unsigned char* wb, uint32_t slotB, float hi[8],
-                                         float lo[8])
+__device__ __forceinline__ void load_seg(const float* srow, float seg[24])
 {
-    float seg[24];
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
         const float4 v = ld_c(srow + 4 * i);
         seg[4 * i] = v.x; seg[4 * i + 1] = v.y; seg[4 * i + 2] = v.z; seg[4 * i + 3] = v.w;
     }
+}
+
+template <int R, typename WT, bool CENTRE_ROW>
+__device__ __forceinline__ void do_row_s(const float seg[24], const unsigned char* wb, uint32_t slotB, float hi[8],
+                                         float lo[8])
+{
     float p[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) p[j] = 0.f;
@@ -580,10 +583,9 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
 // SM keeps up to 2 CTAs × S rows outstanding with one thread issuing them.
 constexpr int kBulkWarps = 8;
 template <int R, typename WT>
-__global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(const SuperArgs a, int S)
+__device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, unsigned char* smem_b)
 {
     constexpr int L = 2 * R + 1, K = L * L * L, NROW = L * L;
-    extern __shared__ __align__(128) unsigned char smem_b[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_b);
     uint64_t* empty = full + S;
     unsigned char* stg = smem_b + 128;
@@ -599,7 +601,7 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(c
     __syncthreads();
     const bool producer = warp == kBulkWarps;
     const int e = producer ? 0 : (int)threadIdx.x;
-    TileCtx t = tile_ctx<R>(a, blockIdx.x, e);
+    TileCtx t = tile_ctx<R>(a, blk, e);
     float hi[8], lo[8];
     if (producer) {
         if (lane == 0) {
@@ -620,18 +622,42 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(c
     } else {
         diag_init(a, t, e, hi, lo);
         const unsigned char* wb = stg + (size_t)e * 8 * sizeof(WT);
+        // the row's C segment is loaded before waiting for its weights (the L1/L2 latency
+        // overlaps the stage's arrival)
+        float seg[24];
         for (int i = 0; i < NROW; ++i) {
             const int st = i % S, u = i / S;
+            if (t.real) load_seg(row_src<R>(t, i), seg);
             mbar_wait(smem_u32(full + st), u & 1);
             if (t.real) {
-                if (i == 0) do_row_s<R, WT, true>(row_src<R>(t, 0), wb + (size_t)st * stageB, slotB, hi, lo);
-                else do_row_s<R, WT, false>(row_src<R>(t, i), wb + (size_t)st * stageB, slotB, hi, lo);
+                if (i == 0) do_row_s<R, WT, true>(seg, wb + (size_t)st * stageB, slotB, hi, lo);
+                else do_row_s<R, WT, false>(seg, wb + (size_t)st * stageB, slotB, hi, lo);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(empty + st));
         }
     }
     tile_epilogue(a, t, e, hi, lo);
+}
+
+template <int R, typename WT>
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(const SuperArgs a, int S)
+{
+    extern __shared__ __align__(128) unsigned char smem_b[];
+    bulk_body<R, WT>(a, blockIdx.x, S, smem_b);
+}
+
+// N4 with the staged stream: the mixed launch's dense tiles run bulk_body, its uniform blocks
+// uniform_body with the class kernel in the (otherwise unused) stage memory.
+template <int R, typename WT>
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_mixed_bulk_kernel(const SuperArgs a, const UniArgs u,
+                                                                                     int S)
+{
+    extern __shared__ __align__(128) unsigned char smem_b[];
+    const long T = gridDim.x, U = u.n_blocks, b = blockIdx.x;
+    const long u0 = b * U / T, u1 = (b + 1) * U / T;
+    if (u1 > u0) uniform_body<R>(u, (int)u0, reinterpret_cast<float*>(smem_b + 128));
+    else bulk_body<R, WT>(a, (int)(b - u0), S, smem_b);
 }
 
 // stages of the bulk kernel: 2 CTAs per SM with ≥ 2 stages each, else 1 CTA with ≥ 2; 0 = the
@@ -721,6 +747,24 @@ static cudaError_t launch_mixed_r(const SuperArgs& a, const UniArgs& u, int fmt,
     const int nblk = (a.t_end - a.t_begin) + u.n_blocks;
     if (nblk <= 0) return cudaSuccess;
     if (a.tile != 256) return cudaErrorInvalidValue;  // uniform blocks are 256 chunks
+    if (!a.no_bulk && nblk >= 2 * 148) {
+        const int b_w = fmt == 0 ? 4 : 2;
+        int cps = 0;
+        const int S = bulk_stages(R, b_w, a.tile, &cps);
+        const size_t smem = 128 + (size_t)S * (2 * R + 1) * a.tile * 8 * b_w;
+        if (S > 0 && smem >= 128 + (size_t)(2 * R + 1) * (2 * R + 1) * (2 * R + 1) * 4) {
+            const void* f = fmt == 0 ? (const void*)superpose_mixed_bulk_kernel<R, float>
+                          : fmt == 1 ? (const void*)superpose_mixed_bulk_kernel<R, __half>
+                                     : (const void*)superpose_mixed_bulk_kernel<R, __nv_bfloat16>;
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            const int nt = (kBulkWarps + 1) * 32;
+            if (fmt == 0) superpose_mixed_bulk_kernel<R, float><<<nblk, nt, smem, s>>>(a, u, S);
+            else if (fmt == 1) superpose_mixed_bulk_kernel<R, __half><<<nblk, nt, smem, s>>>(a, u, S);
+            else superpose_mixed_bulk_kernel<R, __nv_bfloat16><<<nblk, nt, smem, s>>>(a, u, S);
+            return cudaGetLastError();
+        }
+    }
     if (fmt == 0) superpose_mixed_kernel<R, float><<<nblk, 256, 0, s>>>(a, u);
     else if (fmt == 1) superpose_mixed_kernel<R, __half><<<nblk, 256, 0, s>>>(a, u);
     else superpose_mixed_kernel<R, __nv_bfloat16><<<nblk, 256, 0, s>>>(a, u);

@@ -569,7 +569,9 @@ def main():
                    "l2": "inputs larger than L2 (%.1f GB of weights streamed per step)" %
                          (info["weight_bytes"] * world / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "superpose_kernel",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": ("superpose_bulk_kernel (TMA-staged weights)" if info["n_tiles"] >= 2 * 148
+                                else "superpose_kernel (register prefetch)"),
                      "peak_source": peak_src, "bytes_per_voxel_update": bpv,
                      "note": ("N4 byte model: (1-f_uniform)*(K-1)*b_w+12 per voxel-update, f_uniform=%.4f"
                               % f_u if dedup_storage else

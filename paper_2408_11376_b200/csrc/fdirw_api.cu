@@ -702,6 +702,8 @@ static cudaError_t superpose_uniform(fdirw_ctx* c, const float* src, float* out,
 static cudaError_t superpose_n4_mixed(fdirw_ctx* c, const float* src, float* out, long ps, long rs, cudaStream_t s)
 {
     const Geometry& g = c->g;
+    if (c->ut.n_blocks == 0)  // no uniform chunk at all: the plain dense launch over the compacted tiles
+        return superpose(c, src, out, ps, rs, 0, c->ut.nd_tiles, s, false);
     SuperArgs a{};
     a.cpad = src;
     a.Wt = c->Wt;

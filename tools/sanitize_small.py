@@ -30,6 +30,15 @@ def main():
             fd.run(ctx, c, 3)
             fd.mass(ctx, c)
             fd.export_kernels(ctx, (0, 5, 0, 4, 0, 3))
+    # TMA-staged weight stream (needs >= 2 CTAs/SM of tiles: 40 planes x 8 tiles), dense and N4 mixed
+    big = (40, 64, 256)
+    bmask = fi.porous_particle(big, 14, pore_r=(1.0, 2.0), porosity=0.3, seed=2)
+    cb = torch.from_numpy(fi.initial_c(bmask, "random", seed=2)).cuda()
+    for flags in (0, fd.F_DEDUP_STORAGE):
+        with fd.build_kernels(params(big, 1, 4, "bf16", flags), bmask) as ctx:
+            assert ctx.info["n_tiles"] >= 2 * 148
+            c = cb.clone()
+            fd.run(ctx, c, 2)
     # far field (N2)
     fmask = fi.with_far_field(fi.porous_particle(shape, 4, pore_r=(1.0, 1.5), n_pores=3, seed=1), 4, 2.0)
     with fd.build_kernels(params(shape, 2, 20, v_far=100.0), fmask) as ctx:

@@ -47,11 +47,14 @@ def _one_gpu(fd, cfg, mask, c0, steps):
         fd.destroy(ctx)
 
 
-@pytest.mark.parametrize("world,steps,R", [(2, 5, 3), (3, 4, 2), (4, 3, 3)])
-def test_p2p_local_ranks_bitwise(fd, world, steps, R):
+@pytest.mark.parametrize("world,steps,R,shape", [(2, 5, 3, None), (3, 4, 2, None), (4, 3, 3, None),
+                                                  (2, 3, 2, (80, 64, 256))])
+def test_p2p_local_ranks_bitwise(fd, world, steps, R, shape):
+    """(80, 64, 256): each slab has 320 tiles, so the ranks run the TMA-staged superposition
+    (with its fused halo pushes) instead of the small-grid register-prefetch body."""
     import torch
 
-    cfg = small_cfg((4 * 3 + 1, 11, 13), R, 25, weights="bf16")
+    cfg = small_cfg(shape or (4 * 3 + 1, 11, 13), R, 25, weights="bf16")
     mask = fi.random_two_phase(cfg.shape, 0.6, seed=world + 20)
     c0 = fi.initial_c(mask, "random", seed=world)
     ref = _one_gpu(fd, cfg, mask, c0, steps)

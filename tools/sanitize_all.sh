@@ -1,0 +1,9 @@
+# compute-sanitizer over tools/sanitize_small.py (every entry point, incl. the TMA-staged stream);
+# racecheck once more with SANITIZE_NO_BULK=1 (per-thread weight loads) as the control
+CS=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_small.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$? $(tail -2 gpurun_out/sanitize_$tool.log | tr '\n' ' ')"
+done
+SANITIZE_NO_BULK=1 timeout 900 $CS --tool racecheck --error-exitcode 9 python tools/sanitize_small.py > gpurun_out/sanitize_racecheck_nobulk.log 2>&1
+echo "racecheck (no bulk) rc=$? $(tail -2 gpurun_out/sanitize_racecheck_nobulk.log | tr '\n' ' ')"

@@ -12,7 +12,13 @@ import fdirw_inputs as fi  # noqa: E402
 import paper_2408_11376_b200 as fd  # noqa: E402
 
 
+# SANITIZE_NO_BULK=1: every context streams weights with per-thread loads (the racecheck
+# control run: racecheck does not model cp.async.bulk's mbarrier completion)
+EXTRA = fd.F_NO_BULK_STREAM if os.environ.get("SANITIZE_NO_BULK") == "1" else 0
+
+
 def params(shape, R, n_fd, fmt="bf16", flags=0, v_far=0.0):
+    flags |= EXTRA
     nz, ny, nx = shape
     return fd.Params(nx=nx, ny=ny, nz=nz, dh=1.0, D_fast=1.0, D_slow=1e-3, dt=0.1 * n_fd, radius=R, n_fd=0,
                      weights=fmt, flags=flags, v_far=v_far)
@@ -29,7 +35,8 @@ def main():
             c = c0.clone()
             fd.run(ctx, c, 3)
             fd.mass(ctx, c)
-            fd.export_kernels(ctx, (0, 5, 0, 4, 0, 3))
+            if not flags & fd.F_DEDUP_STORAGE:  # export needs the dense layout
+                fd.export_kernels(ctx, (0, 5, 0, 4, 0, 3))
     # TMA-staged weight stream (needs >= 2 CTAs/SM of tiles: 40 planes x 8 tiles), dense and N4 mixed
     big = (40, 64, 256)
     bmask = fi.porous_particle(big, 14, pore_r=(1.0, 2.0), porosity=0.3, seed=2)

@@ -204,6 +204,14 @@ fdirw_status fdirw_run(fdirw_ctx* ctx, float* c_dev, int32_t n_steps, void* cuda
  * writes the result to *out_host. */
 fdirw_status fdirw_mass(fdirw_ctx* ctx, const float* c_dev, double* out_host, void* cuda_stream);
 
+/* Measurement aid (bench.py roofline.read_ceiling): streams the context's stored
+ * weights `reps` times (after one warm-up pass) with the superposition's own load
+ * (128-bit, L1 no-allocate, L2 evict-first) and nothing else, timed with CUDA events on
+ * cuda_stream; *gbps_out = weight bytes / best pass time (GB/s, 1e9).  The practical HBM
+ * ceiling of a read-only stream on this device.  Synchronous.  Errors: E_INVALID (NULL,
+ * reps < 1), E_STATE (no weights), E_CUDA. */
+fdirw_status fdirw_read_ceiling(const fdirw_ctx* ctx, int32_t reps, void* cuda_stream, double* gbps_out);
+
 /* Fills *info (host).  Never fails on a valid ctx. */
 fdirw_status fdirw_query(const fdirw_ctx* ctx, fdirw_info* info);
 

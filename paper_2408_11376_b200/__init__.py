@@ -44,7 +44,7 @@ EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fd
            "fdirw_far_init", "fdirw_far_init_virtual", "fdirw_far_get", "fdirw_absorb_run",
            "fdirw_set_precision_mode", "fdirw_coarse_far_init", "fdirw_coarse_far_get",
            "fdirw_coarse_export_pbc", "fdirw_p2p_export", "fdirw_p2p_attach", "fdirw_p2p_attach_local",
-           "fdirw_p2p_check"]
+           "fdirw_p2p_check", "fdirw_read_ceiling"]
 TRANSPORTS = {"nccl": 0, "p2p": 1}
 P2P_BLOB_BYTES = 256
 
@@ -103,6 +103,8 @@ _lib.fdirw_run.argtypes = [_vp, _vp, ctypes.c_int32, _vp]
 _lib.fdirw_run.restype = _st
 _lib.fdirw_mass.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_double), _vp]
 _lib.fdirw_mass.restype = _st
+_lib.fdirw_read_ceiling.argtypes = [_vp, ctypes.c_int32, _vp, ctypes.POINTER(ctypes.c_double)]
+_lib.fdirw_read_ceiling.restype = _st
 _lib.fdirw_query.argtypes = [_vp, ctypes.POINTER(fdirw_info)]
 _lib.fdirw_query.restype = _st
 _lib.fdirw_destroy.argtypes = [_vp]
@@ -315,6 +317,13 @@ def run(ctx: Context, c, n_steps: int, stream=None):
 def mass(ctx: Context, c, stream=None) -> float:
     out = ctypes.c_double()
     _check(_lib.fdirw_mass(ctx.handle, _dptr(c), ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+def read_ceiling(ctx: Context, reps: int = 5, stream=None) -> float:
+    """fdirw_read_ceiling: GB/s of a pure read stream over the context's weights (best of reps)."""
+    out = ctypes.c_double()
+    _check(_lib.fdirw_read_ceiling(ctx.handle, int(reps), _stream(stream), ctypes.byref(out)))
     return out.value
 
 

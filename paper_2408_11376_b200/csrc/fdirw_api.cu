@@ -958,6 +958,41 @@ extern "C" fdirw_status fdirw_mass(fdirw_ctx* c, const float* c_dev, double* out
     return FDIRW_OK;
 }
 
+extern "C" fdirw_status fdirw_read_ceiling(const fdirw_ctx* c, int32_t reps, void* cuda_stream, double* gbps_out)
+{
+    if (!c || !gbps_out || reps < 1) return fail(FDIRW_E_INVALID, "NULL argument or reps < 1");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const Geometry& g = c->g;
+    const uint64_t wt_tiles = (c->ut.chunk_u || c->compact) ? (uint64_t)c->ut.nd_tiles : (uint64_t)g.n_tiles;
+    const size_t bytes = ((size_t)wt_tiles * (g.K - 1) * g.tile * kChunk * c->b_w) / 16 * 16;
+    if (bytes == 0) return fail(FDIRW_E_STATE, "no weights to stream");
+    int sms = 148;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    unsigned* sink = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    float best = 1e30f;
+    cudaError_t e = cudaMalloc(&sink, 4);
+    if (e == cudaSuccess) e = cudaEventCreate(&e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&e1);
+    if (e == cudaSuccess) e = launch_read_stream(c->Wt, bytes, sink, sms, s);  // warm-up
+    for (int r = 0; r < reps && e == cudaSuccess; ++r) {
+        e = cudaEventRecord(e0, s);
+        if (e == cudaSuccess) e = launch_read_stream(c->Wt, bytes, sink, sms, s);
+        if (e == cudaSuccess) e = cudaEventRecord(e1, s);
+        if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+        float ms = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+        if (e == cudaSuccess && ms < best) best = ms;
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("read ceiling: ") + cudaGetErrorString(e));
+    *gbps_out = (double)bytes / (best * 1e-3) / 1e9;
+    return FDIRW_OK;
+}
+
 extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
 {
     if (!c || !info) return fail(FDIRW_E_INVALID, "NULL argument");

@@ -144,6 +144,7 @@ struct SuperArgs {
     bool no_bulk = false;  // FDIRW_F_NO_BULK_STREAM: weights by per-thread loads, not TMA stages
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
+cudaError_t launch_read_stream(const void* p, size_t bytes, unsigned* sink, int sms, cudaStream_t s);
 
 // N4: uniform chunks, one CTA per block of ≤ 256 chunks of one class (superpose.cu)
 struct UniArgs {

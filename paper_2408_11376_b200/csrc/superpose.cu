@@ -786,6 +786,35 @@ cudaError_t launch_superpose_mixed(const SuperArgs& a, const UniArgs& u, int R, 
     }
 }
 
+// Read-stream probe (fdirw_read_ceiling): the HBM read bandwidth this box gives a kernel that
+// does nothing but stream a buffer with the superposition's load (128-bit, L1 no-allocate, L2
+// evict-first), grid-stride over 4 CTAs of 256 threads per SM, 8 loads in flight per thread.
+__global__ void __launch_bounds__(256) read_stream_kernel(const uint4* __restrict__ p, size_t n16, unsigned* sink)
+{
+    const uint64_t pol = evict_first_policy();
+    unsigned acc = 0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 7 * stride < n16; i += 8 * stride) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_stream(p + i + u * stride, pol);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+    for (; i < n16; i += stride) {
+        const uint4 v = ld_stream(p + i, pol);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x9e3779b9u) *sink = acc;  // keeps the loads; practically never taken
+}
+
+cudaError_t launch_read_stream(const void* p, size_t bytes, unsigned* sink, int sms, cudaStream_t s)
+{
+    read_stream_kernel<<<sms * 4, 256, 0, s>>>(reinterpret_cast<const uint4*>(p), bytes / 16, sink);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s)
 {
     switch (R) {

@@ -117,7 +117,7 @@ __device__ __forceinline__ double face_lambda_d(unsigned p, unsigned q, const do
 // FMA) and the result is not renormalised (fp64 FD keeps Σ = 1 to rounding), so the
 // off-centre weights are the oracle's O2 kernels rounded exactly as O5 rounds them.
 template <int R, bool F64>
-__global__ void __launch_bounds__(KgenShape<R, F64>::NT) kgen_kernel(const KgenArgs a)
+__global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 1) kgen_kernel(const KgenArgs a)
 {
     using S = KgenShape<R, F64>;
     using T = typename std::conditional<F64, double, float>::type;

@@ -231,6 +231,58 @@ def test_fd_whole_grid_independent(oracle_lib):
     assert lamtab[(True, False)] == d.lam_fs
 
 
+def _numpy_closed_fd(ph, c, lam_ff, lam_fs, lam_ss, n):
+    """Closed-box explicit FD, array-slicing form (independent of the oracle's C loops)."""
+    for _ in range(n):
+        new = c.copy()
+        for ax in range(3):
+            a = [slice(None)] * 3
+            b = [slice(None)] * 3
+            a[ax] = slice(0, -1)
+            b[ax] = slice(1, None)
+            pa, pbm = ph[tuple(a)], ph[tuple(b)]
+            lam = np.where(pa & pbm, lam_ff, np.where(~pa & ~pbm, lam_ss, lam_fs))
+            flux = lam * (c[tuple(b)] - c[tuple(a)])
+            new[tuple(a)] += flux
+            new[tuple(b)] -= flux
+        c = new
+    return c
+
+
+@pytest.mark.parametrize("R,n_fd", [(2, 60), (3, 40)])
+def test_truncated_window_equals_boxed_fd(oracle_lib, R, n_fd):
+    """Truncated regime (n_fd > R) on a porous two-phase grid: a source's window Ω_s is the
+    box [s−R, s+R]³ clipped to the domain, with no flux across its faces (readings A2, A21), so
+    W_s must equal a closed-domain FD run from δ_s on that sub-box alone.  Reference: the
+    array-slicing FD above on the cut-out mask, λ from Δt/n_fd and the harmonic mean computed
+    here; sources at a corner, an edge, a face, the interior and a slow voxel."""
+    shape = (12, 11, 13)
+    mask = fi.random_two_phase(shape, 0.55, seed=R + 30)
+    D_slow = 0.02
+    pb = lat(mask, R, n_fd, D_slow=D_slow)
+    dt_fd = 0.1 * n_fd / n_fd
+    lam_ff, lam_ss = dt_fd * 1.0, dt_fd * D_slow
+    lam_fs = dt_fd * 2 * 1.0 * D_slow / (1.0 + D_slow)
+    nz, ny, nx = shape
+    L = 2 * R + 1
+    slow = np.argwhere(mask[R:-R, R:-R, R:-R] == 0)[0] + R
+    for sz, sy, sx in [(0, 0, 0), (0, 5, 0), (6, 0, 7), (6, 5, 7), tuple(slow), (nz - 1, ny - 1, nx - 1)]:
+        W = oracle_lib.build_kernels(pb, (sx, sx + 1, sy, sy + 1, sz, sz + 1))[0, 0, 0].reshape(L, L, L)
+        z0, z1 = max(sz - R, 0), min(sz + R + 1, nz)
+        y0, y1 = max(sy - R, 0), min(sy + R + 1, ny)
+        x0, x1 = max(sx - R, 0), min(sx + R + 1, nx)
+        sub = mask[z0:z1, y0:y1, x0:x1].astype(bool)
+        c = np.zeros(sub.shape)
+        c[sz - z0, sy - y0, sx - x0] = 1.0
+        ref = _numpy_closed_fd(sub, c, lam_ff, lam_fs, lam_ss, n_fd)
+        win = W[z0 - sz + R:z1 - sz + R, y0 - sy + R:y1 - sy + R, x0 - sx + R:x1 - sx + R]
+        np.testing.assert_allclose(win, ref, rtol=0, atol=1e-14)
+        outside = W.copy()
+        outside[z0 - sz + R:z1 - sz + R, y0 - sy + R:y1 - sy + R, x0 - sx + R:x1 - sx + R] = 0.0
+        assert not outside.any()  # nothing outside the domain
+        assert n_fd > R and np.count_nonzero(win) == win.size  # truncated regime: every cell reached
+
+
 # ---------------------------------------------------------------- P8 impermeable solid
 def test_impermeable_slow_phase(oracle_lib):
     """P8 (reading A23): D_slow = 0 ⇒ slow sources keep all their mass (W = δ), and

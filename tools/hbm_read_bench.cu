@@ -36,6 +36,28 @@ __global__ void __launch_bounds__(256) rd(const uint4* __restrict__ a, size_t n1
     if (acc == 0x12345678u) out[0] = acc;
 }
 
+template <int U>
+__global__ void __launch_bounds__(256) rd_last(const uint4* __restrict__ a, size_t n16, unsigned* out)
+{
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    unsigned acc = 0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < n16; i += U * stride) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_stream(a + i + u * stride, pol);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+    for (; i < n16; i += stride) {
+        uint4 v = ld_stream(a + i, pol);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
 // chunked: each CTA streams one contiguous chunk (the superpose layout: one tile per CTA)
 template <int U>
 __global__ void __launch_bounds__(256) rd_chunk(const uint4* __restrict__ a, size_t chunk16, size_t nchunk, unsigned* out)
@@ -147,6 +169,27 @@ int main()
         t2("slot-major  U=8 grid=ntile", [&] { rd_tiles<true, 8><<<ntile, 256>>>(a, ntile, nslot, o); });
         t2("tile-major  U=8 grid=592", [&] { rd_tiles<false, 8><<<592, 256>>>(a, ntile, nslot, o); });
         t2("slot-major  U=8 grid=592", [&] { rd_tiles<true, 8><<<592, 256>>>(a, ntile, nslot, o); });
+    }
+    // L2-resident re-read (the coarse GEMV's P̃ case): 64 MB read over and over, evict_last
+    for (size_t mb : {32, 64, 96}) {
+        const size_t b2 = mb << 20, n2 = b2 / 16;
+        auto t3 = [&](const char* name, auto launch) {
+            for (int w = 0; w < 3; ++w) launch();
+            cudaDeviceSynchronize();
+            float best = 1e30f;
+            for (int r = 0; r < 20; ++r) {
+                cudaEventRecord(e0);
+                launch();
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            printf("%-40s %3zu MB %.4f ms  %.1f GB/s\n", name, mb, best, b2 / (best * 1e-3) / 1e9);
+        };
+        t3("L2 re-read U=8 blocks/SM=4", [&] { rd_last<8><<<148 * 4, 256>>>(a, n2, o); });
+        t3("L2 re-read U=8 blocks/SM=8", [&] { rd_last<8><<<148 * 8, 256>>>(a, n2, o); });
     }
     printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;

@@ -230,7 +230,7 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
     window dedup, kgen, expand into the gather layout, allocation).  Algorithmic work = every
     source's window × K × n_fd FD cell-updates (the literal method).  The kernel itself
     (device time from CUDA events around its launch, fdirw_info.kgen_kernel_ms) runs the distinct
-    windows only, kgen_steps stencil passes each (the Chebyshev degree m, reading A29, or n_fd):
+    windows only, kgen_steps stencil passes each (the Chebyshev degree m, reading A30, or n_fd):
     its rooflines count those passes — shared memory (4 lateral neighbour reads + 1 write of 4 B
     per cell-pass, z columns padded from L to Lp; 128 B/clk/SM) binds, the FP32 lanes (11
     lane-ops per substep cell, 13 per Chebyshev cell-pass) do not."""

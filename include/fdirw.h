@@ -83,7 +83,7 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weig
 #define FDIRW_F_KGEN_DIRECT 32u /* kgen runs the n_fd explicit substeps literally.  Default:
                                   when it saves work, the same A^{n_fd}·δ_s is evaluated by a
                                   Chebyshev recurrence of degree m ≈ 160 (at n_fd = 1000, λ = 0.1)
-                                  over the same stencil, truncation ‖·‖₂ ≤ 1e-10 (reading A29;
+                                  over the same stencil, truncation ‖·‖₂ ≤ 1e-10 (reading A30;
                                   fdirw_info.kgen_steps reports which)                            */
 #define FDIRW_F_NO_BULK_STREAM 64u /* superposition streams each tile's weights with per-thread 128-bit
                                   loads instead of TMA bulk copies into shared-memory stages (the
@@ -146,7 +146,7 @@ typedef struct {
     uint64_t uniform_chunks;/* N4: chunks whose weights come from a shared class kernel (else 0)   */
     int32_t uniform_classes;/* N4: distinct class kernels those chunks use                          */
     int32_t kgen_steps;     /* stencil passes per kgen window: n_fd (direct substeps, also with
-                               FDIRW_F_KGEN_FP64) or the Chebyshev degree m (reading A29)          */
+                               FDIRW_F_KGEN_FP64) or the Chebyshev degree m (reading A30)          */
     double kgen_kernel_ms;  /* device time of the kgen launch in fdirw_build_kernels (CUDA events) */
 } fdirw_info;
 

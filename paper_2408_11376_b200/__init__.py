@@ -34,7 +34,7 @@ F_NO_DEDUP = 2
 F_DEDUP_STORAGE = 4  # NEXT row N4: uniform chunks read shared class kernels (fewer HBM bytes)
 F_KGEN_FP64 = 8  # kgen in fp64, the oracle's operation order (reading A22, debugging)
 F_SYMMETRIC_RULE = 16  # exact regime only: gather weights = own kernel reflected (reading A24)
-F_KGEN_DIRECT = 32  # kgen runs the n_fd substeps literally instead of the Chebyshev recurrence (reading A29)
+F_KGEN_DIRECT = 32  # kgen runs the n_fd substeps literally instead of the Chebyshev recurrence (reading A30)
 F_NO_BULK_STREAM = 64  # superposition: per-thread weight loads instead of TMA-staged rows (same bits)
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",

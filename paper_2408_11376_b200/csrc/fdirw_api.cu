@@ -174,7 +174,7 @@ static fdirw_status derive(const fdirw_params& p, Derived* d)
     return FDIRW_OK;
 }
 
-// Chebyshev plan for kgen (reading A29).  Every window operator A (7-point
+// Chebyshev plan for kgen (reading A30).  Every window operator A (7-point
 // stencil, symmetric face numbers λ_ij, no-flux or absorbing edges) is symmetric with its
 // spectrum in [a, 1], a = 1 − 12·λ_max (Gershgorin: centre 1 − Λ_i, radius ≤ Λ_i ≤ 6λ_max).
 // With x = αy + β (α = 6λ_max, β = 1 − 6λ_max), x^n = Σ_k c_k T_k(y) where every c_k ≥ 0

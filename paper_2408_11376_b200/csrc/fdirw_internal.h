@@ -59,7 +59,7 @@ struct KgenArgs {
     int fp64;             // FDIRW_F_KGEN_FP64: fp64 substeps in the oracle's order (reading A22)
     int symmetric;        // FDIRW_F_SYMMETRIC_RULE: write W_s(o) as target s's slot −o (reading A24)
     int n_fd;
-    // Chebyshev evaluation of A^{n_fd − cheb_pre} (kgen.cu, reading A29): degree cheb_m (0 =
+    // Chebyshev evaluation of A^{n_fd − cheb_pre} (kgen.cu, reading A30): degree cheb_m (0 =
     // direct substeps), coefficients cheb_c[0..cheb_m] (device, fp32), face numbers 2μ = 4λ/(1 − a)
     int cheb_m, cheb_pre;  // Chebyshev degree (0 = direct) after cheb_pre direct substeps
     const float* cheb_c;

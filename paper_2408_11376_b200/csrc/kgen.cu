@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 
         }
         if (a.cheb_m) {
             // Chebyshev evaluation of the rest, A^{n_fd − pre} v with v = A^{pre} δ_s (DESIGN.md
-            // §7, reading A29): x^n' = Σ_k c_k T_k(y) on the spectrum [a, 1] of A,
+            // §7, reading A30): x^n' = Σ_k c_k T_k(y) on the spectrum [a, 1] of A,
             // y = (2x − 1 − a)/(1 − a), all c_k ≥ 0 with Σ c_k = 1, truncated at degree m where the
             // tail Σ_{k>m} c_k ≤ 1e-10 (so ‖p_m(A)v − A^n' v‖₂ ≤ 1e-10 ‖v‖₂).  Three-term recurrence
             // t_{k+1} = 2Â t_k − t_{k−1}, t_0 = v, t_1 = Â v; p = Σ c_k t_k.  Each step is one stencil

@@ -50,7 +50,7 @@ def _gpu_steps(fd, cfg, mask, c0, steps, weights=None, flags=0, use_run=True):
 def test_cfg1_fp32_10_steps(fd, oracle_lib, n_fd, direct):
     """BASELINE configs[0]: 16³ two-phase porous grid, D ratio 1e3, R2, fp32, 10 steps,
     exact (n_fd = 2 ≤ R) and truncated (n_fd = 1000) regimes; kgen by the Chebyshev
-    recurrence (default at n_fd = 1000, reading A29) and by the literal substeps."""
+    recurrence (default at n_fd = 1000, reading A30) and by the literal substeps."""
     cfg = fi.config("cfg1", n_fd=n_fd, weights="fp32")
     mask = cfg.mask()
     pb = oracle_problem(cfg, mask)
@@ -72,7 +72,7 @@ def test_cfg1_fp32_10_steps(fd, oracle_lib, n_fd, direct):
 @pytest.mark.parametrize("fmt", ["fp32", "fp16", "bf16"])
 def test_kgen_matches_oracle_kernels(fd, oracle_lib, fmt, direct):
     """a3/a4 in isolation: the stored kernels (export) vs the oracle's quantised kernels (O5),
-    kgen by the literal substeps and by the Chebyshev recurrence (reading A29)."""
+    kgen by the literal substeps and by the Chebyshev recurrence (reading A30)."""
     cfg = fi.config("cfg1", n_fd=1000, weights=fmt)
     mask = cfg.mask()
     pb = oracle_problem(cfg, mask)
@@ -333,7 +333,7 @@ def test_errors(fd):
     ((13, 12, 14), 5, 1e-3, "bf16"),    # cfg3's R5, bf16 storage
 ])
 def test_kgen_chebyshev_vs_substeps_and_oracle(fd, oracle_lib, shape, R, D_slow, fmt):
-    """Reading A29: the default kgen runs 8 substeps, then evaluates A^992 by a Chebyshev
+    """Reading A30: the default kgen runs 8 substeps, then evaluates A^992 by a Chebyshev
     recurrence of degree m = 157 (λ = 0.1; truncation ≤ 1e-10); FDIRW_F_KGEN_DIRECT runs the 1000
     literal substeps.  Both stored kernels against the oracle's fp64 kernels (unquantised),
     and against each other."""

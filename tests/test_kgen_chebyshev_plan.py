@@ -1,4 +1,4 @@
-"""Host logic of kgen's Chebyshev evaluation (reading A29), no GPU needed.
+"""Host logic of kgen's Chebyshev evaluation (reading A30), no GPU needed.
 
 After 8 direct substeps the library picks the degree m of p_m(y) = Σ_{k≤m} c_k T_k(y) ≈ x^n, x = αy + β on the window
 spectrum [1 − 12λ_max, 1] (α = 6λ_max, β = 1 − 6λ_max), as the smallest m whose tail

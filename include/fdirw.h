@@ -308,8 +308,10 @@ fdirw_status fdirw_step_virtual(fdirw_ctx* const* ctxs, int32_t n, const float* 
  *            C'_I = Σ_J P̃_IJ C_J (+ P_BC_I·c_far), fp32 accumulation (Eq.14);
  *            c'_i = C'_I (Eq.15); voxels outside Ω_L are copied unchanged; then (v_far > 0)
  *            Eq.7 on the device: c_far = (K0 − Σ_I N_I C'_I)/v_far, fp64.
- * params: nx, ny, nz, dh, D_fast, dt, n_fd, weights as for the fine path (D_slow,
- * radius and flags are ignored).  Single GPU.  Buffers are device fp32 [nz][ny][nx].
+ * params: nx, ny, nz, dh, D_fast, dt, n_fd, weights as for the fine path (D_slow and
+ * radius are ignored; of the flags only FDIRW_F_KGEN_DIRECT is read: P columns by the
+ * literal n_fd substeps instead of the Chebyshev evaluation, reading A30).  Single GPU.
+ * Buffers are device fp32 [nz][ny][nx].
  */
 typedef struct fdirw_coarse fdirw_coarse; /* opaque */
 
@@ -320,6 +322,8 @@ typedef struct {
     int64_t n_region;       /* N_L (fine voxels in Ω_L)                                */
     uint64_t p_bytes;       /* stored P incl. fp32 diagonal                           */
     uint64_t flops_per_step;/* the paper's model N(N+1) + 2·N_L                */
+    int32_t fd_passes;      /* stencil passes per P column: n_fd (literal substeps) or 8 + the
+                               Chebyshev degree (reading A30; FDIRW_F_KGEN_DIRECT forces literal) */
 } fdirw_coarse_info;
 
 /* Builds groups, P (batched whole-region FD on the GPU), quantises.  Synchronous. */

@@ -85,7 +85,8 @@ class fdirw_plan(ctypes.Structure):
 
 class fdirw_coarse_info(ctypes.Structure):
     _fields_ = [("n_fd", ctypes.c_int32), ("block", ctypes.c_int32), ("n_groups", ctypes.c_int64),
-                ("n_region", ctypes.c_int64), ("p_bytes", ctypes.c_uint64), ("flops_per_step", ctypes.c_uint64)]
+                ("n_region", ctypes.c_int64), ("p_bytes", ctypes.c_uint64), ("flops_per_step", ctypes.c_uint64),
+                ("fd_passes", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p

@@ -40,6 +40,7 @@ using namespace fdirw;
 struct fdirw_coarse {
     fdirw_params p;
     int n_fd = 0, b = 5, fmt = 0, b_w = 4, device = 0;
+    int fd_passes = 0;        // stencil passes per P column: n_fd, or kCheb_pre + Chebyshev degree
     double lam = 0;
     long nvox = 0, NL = 0, N = 0;
     long ldp = 0;             // row stride of P: N rounded up to 8 (16-byte rows, zero padding)
@@ -199,7 +200,53 @@ __global__ void __launch_bounds__(256) k_fd_cols(const float* __restrict__ X, fl
     }
 }
 
-// P64[I][J0 + j] = Σ_{v∈I} X[row(v)][j] / N_I (fp64, CSR order); stride Ncol
+// One Chebyshev pass for CB columns (reading A30; the same recurrence as kgen's): with
+// Â = I + Σ_f μ_f (t_f − t) (μ = 2λ/(1 − a), far-field faces Dirichlet 0),
+//   prv ← 2·Â·cur − prv  (first pass: Â·cur, prv unread),  acc ← acc + c_k·prv
+// (first pass: acc ← c_0·cur + c_1·prv).  mu2 = 2μ.  One warp per row, float4 column quads.
+__global__ void __launch_bounds__(256) k_cheb_cols(const float* __restrict__ cur, float* __restrict__ prv,
+                                                   float* __restrict__ acc, const int* __restrict__ nb, long NL,
+                                                   int CB, float mu2, float c0, float ck, int first)
+{
+    const int lane = threadIdx.x & 31;
+    const long warps = (long)gridDim.x * (blockDim.x >> 5);
+    const int q4 = CB >> 2;
+    for (long r = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < NL; r += warps) {
+        int n[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) n[f] = __ldg(nb + r * 6 + f);
+        const float4* cr = reinterpret_cast<const float4*>(cur + r * (long)CB);
+        float4* pr = reinterpret_cast<float4*>(prv + r * (long)CB);
+        float4* ar = reinterpret_cast<float4*>(acc + r * (long)CB);
+        for (int q = lane; q < q4; q += 32) {
+            const float4 c = cr[q];
+            float4 v;
+            if (first) {
+                v = make_float4(2.f * c.x, 2.f * c.y, 2.f * c.z, 2.f * c.w);
+            } else {
+                const float4 p = pr[q];
+                v = make_float4(fmaf(2.f, c.x, -p.x), fmaf(2.f, c.y, -p.y), fmaf(2.f, c.z, -p.z), fmaf(2.f, c.w, -p.w));
+            }
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                if (n[f] == -1) continue;
+                const float4 m = n[f] >= 0 ? reinterpret_cast<const float4*>(cur + (long)n[f] * CB)[q]
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                v.x = fmaf(mu2, m.x - c.x, v.x);
+                v.y = fmaf(mu2, m.y - c.y, v.y);
+                v.z = fmaf(mu2, m.z - c.z, v.z);
+                v.w = fmaf(mu2, m.w - c.w, v.w);
+            }
+            if (first) v = make_float4(0.5f * v.x, 0.5f * v.y, 0.5f * v.z, 0.5f * v.w);
+            const float4 a0 = first ? make_float4(c0 * c.x, c0 * c.y, c0 * c.z, c0 * c.w) : ar[q];
+            pr[q] = v;
+            ar[q] = make_float4(fmaf(ck, v.x, a0.x), fmaf(ck, v.y, a0.y), fmaf(ck, v.z, a0.z), fmaf(ck, v.w, a0.w));
+        }
+    }
+}
+
+// P64[I][J0 + j] = Σ_{v∈I} X[row(v)][j] / N_I (fp64, CSR order); stride Ncol.  Entries are
+// clamped at 0 (A^n·1_J ≥ 0; only the Chebyshev path's rounding noise can dip below).
 __global__ void k_map_cols(const float* X, const int* grp_ptr, const int* grp_vox, const int* row_of, long N,
                            long Ncol, int CB, int J0, int Jn, double* P64)
 {
@@ -208,7 +255,7 @@ __global__ void k_map_cols(const float* X, const int* grp_ptr, const int* grp_vo
         const long I = i / Jn;
         const int j = (int)(i % Jn);
         double s = 0.0;
-        for (int k = grp_ptr[I]; k < grp_ptr[I + 1]; ++k) s += (double)X[(long)row_of[grp_vox[k]] * CB + j];
+        for (int k = grp_ptr[I]; k < grp_ptr[I + 1]; ++k) s += (double)fmaxf(X[(long)row_of[grp_vox[k]] * CB + j], 0.f);
         P64[I * Ncol + J0 + j] = s / (double)(grp_ptr[I + 1] - grp_ptr[I]);
     }
 }
@@ -253,6 +300,30 @@ __global__ void k_quantize(const double* P64, long Ncol, const int* sizes, long 
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += red[w]; tm += redm[w]; }
         Pdiag[J] = (float)((tm - t) / (double)sizes[J]);
     }
+}
+
+// Closed region, Chebyshev-evaluated columns: the recurrence's fp32 rounding moves a column's
+// mass Σ_I N_I P_IJ off its exact value N_J (FD conserves mass; ~6e-7 relative), so each
+// column is rescaled in fp64 to N_J before quantisation — kgen's renormalisation of closed
+// windows (§7), here by the group size (reading A30).  One block per column, fixed order.
+__global__ void k_renorm_cols(double* P64, long Ncol, const int* sizes, long N)
+{
+    __shared__ double red[32];
+    __shared__ double scale;
+    const long J = blockIdx.x;
+    double m = 0.0;
+    for (long I = threadIdx.x; I < N; I += blockDim.x) m += (double)sizes[I] * P64[I * Ncol + J];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        scale = t > 0.0 ? (double)sizes[J] / t : 1.0;
+    }
+    __syncthreads();
+    for (long I = threadIdx.x; I < N; I += blockDim.x) P64[I * Ncol + J] *= scale;
 }
 
 __global__ void k_pbc(const double* P64, long Ncol, long N, float* Pbc)
@@ -563,12 +634,12 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
     uint8_t* reg = nullptr;
     int *used = nullptr, *bid = nullptr, *row_flag = nullptr, *row_pos = nullptr, *row_of = nullptr;
     int *row_group = nullptr, *row_group2 = nullptr, *nb = nullptr;
-    float *X = nullptr, *Y = nullptr;
+    float *X = nullptr, *Y = nullptr, *Z = nullptr;
     double* P64 = nullptr;
     void* tmp = nullptr;
     auto cleanup = [&]() {
         cudaFree(reg); cudaFree(used); cudaFree(bid); cudaFree(row_flag); cudaFree(row_pos); cudaFree(row_of);
-        cudaFree(row_group); cudaFree(row_group2); cudaFree(nb); cudaFree(X); cudaFree(Y); cudaFree(P64);
+        cudaFree(row_group); cudaFree(row_group2); cudaFree(nb); cudaFree(X); cudaFree(Y); cudaFree(Z); cudaFree(P64);
         cudaFree(tmp);
     };
     cudaError_t e = cudaSuccess;
@@ -644,27 +715,69 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
 
     // P (and P_BC as column N) by batched FD over Ω_L, CB columns per pass
     const long Ncol = (long)N + (c->far ? 1 : 0);
-    const long budget = 4L << 30;  // bytes for the two FD buffers
-    long CB = budget / (2L * 4 * NL);
+    // 512 columns per chunk: 3 z-planes of the region's rows stay in L2 (measured: 512 beats
+    // 1024-2048 by 3-8 %); three buffers (cur, prev, acc) for the Chebyshev recurrence
+    const long budget = 6L << 30;
+    long CB = budget / (3L * 4 * NL);
+    if (CB > 512) CB = 512;
     CB = CB < 4 ? 4 : (CB / 4) * 4;
     const long Npad = (Ncol + 3) / 4 * 4;
     if (CB > Npad) CB = Npad;
     T(cudaMalloc(&X, NL * CB * 4));
     T(cudaMalloc(&Y, NL * CB * 4));
+    T(cudaMalloc(&Z, NL * CB * 4));
     T(cudaMalloc(&P64, (long)N * Ncol * 8));
     const int Nbc = c->far ? N : -1;
-    for (long J0 = 0; J0 < Ncol; J0 += CB) {
-        const int Jn = (int)((Ncol - J0) < CB ? (Ncol - J0) : CB);
+    // P columns of a closed region: kCheb_pre literal substeps, then the Chebyshev recurrence
+    // for the remaining n_fd − kCheb_pre (reading A30), columns renormalised to their exact mass
+    // N_J.  Literal substeps instead with FDIRW_F_KGEN_DIRECT, a small n_fd, or a far field:
+    // there most of a column's mass leaks to the reservoir, and the recurrence's rounding — on
+    // the scale of the source, not of what remains — would cost the remaining mass its fp32
+    // accuracy (measured 1.8e-5 relative vs 2e-6 for the substeps).  The P_BC column
+    // (inhomogeneous: its far faces see the Dirichlet value 1) runs in a chunk of its own.
+    std::vector<float> cheb;
+    const int m = (p->flags & FDIRW_F_KGEN_DIRECT) || c->n_fd <= 2 * kCheb_pre || c->far
+                      ? 0 : cheb_plan(c->n_fd - kCheb_pre, lam, &cheb);
+    c->fd_passes = m > 0 ? kCheb_pre + m : c->n_fd;
+    const float mu2 = (float)(lam * 4.0 / (12.0 * lam));  // 2μ = 4λ/(1 − a), 1 − a = 12λ: 1/3
+    auto direct = [&](float*& a, float*& bb, int cb, int j0, int passes) {
+        for (int k = 0; k < passes; ++k) {
+            k_fd_cols<<<gridn(NL * 32), 256, 0, s>>>(a, bb, nb, NL, cb, (float)lam, j0, Nbc);
+            float* t = a; a = bb; bb = t;
+        }
+    };
+    for (long J0 = 0; J0 < N; J0 += CB) {
+        const int Jn = (int)((N - J0) < CB ? (N - J0) : CB);
         k_init_cols<<<gridn(NL * CB), 256, 0, s>>>(row_group, NL, (int)CB, (int)J0, X);
         T(cudaGetLastError());
         float *a = X, *bb = Y;
-        for (int k = 0; k < c->n_fd; ++k) {
-            k_fd_cols<<<gridn(NL * 32), 256, 0, s>>>(a, bb, nb, NL, (int)CB, (float)lam, (int)J0, Nbc);
-            float* t = a; a = bb; bb = t;
+        if (m == 0) {
+            direct(a, bb, (int)CB, (int)J0, c->n_fd);
+        } else {
+            direct(a, bb, (int)CB, (int)J0, kCheb_pre);  // a = v = A^pre·1_J
+            k_cheb_cols<<<gridn(NL * 32), 256, 0, s>>>(a, bb, Z, nb, NL, (int)CB, mu2, cheb[0], cheb[1], 1);
+            for (int k = 1; k < m; ++k) {  // bb = t_k, a = t_{k−1} ← t_{k+1}
+                k_cheb_cols<<<gridn(NL * 32), 256, 0, s>>>(bb, a, Z, nb, NL, (int)CB, mu2, 0.f, cheb[k + 1], 0);
+                float* t = a; a = bb; bb = t;
+            }
+            a = Z;
         }
         T(cudaGetLastError());
         k_map_cols<<<gridn((long)N * Jn), 256, 0, s>>>(a, c->grp_ptr, c->grp_vox, row_of, N, Ncol, (int)CB, (int)J0,
                                                        Jn, P64);
+        T(cudaGetLastError());
+    }
+    if (c->far) {  // P_BC = column N, literal substeps (4-wide chunk)
+        k_init_cols<<<gridn(NL * 4), 256, 0, s>>>(row_group, NL, 4, N, X);
+        T(cudaGetLastError());
+        float *a = X, *bb = Y;
+        direct(a, bb, 4, N, c->n_fd);
+        T(cudaGetLastError());
+        k_map_cols<<<gridn((long)N), 256, 0, s>>>(a, c->grp_ptr, c->grp_vox, row_of, N, Ncol, 4, N, 1, P64);
+        T(cudaGetLastError());
+    }
+    if (m > 0 && !c->far) {
+        k_renorm_cols<<<N, 256, 0, s>>>(P64, Ncol, c->sizes, N);
         T(cudaGetLastError());
     }
     c->ldp = ((long)N + 7) / 8 * 8;
@@ -818,6 +931,7 @@ extern "C" fdirw_status fdirw_coarse_query(const fdirw_coarse* c, fdirw_coarse_i
     info->n_region = c->NL;
     info->p_bytes = (uint64_t)c->N * c->ldp * c->b_w + (uint64_t)c->N * 4 * (c->far ? 2 : 1);
     info->flops_per_step = (uint64_t)c->N * (c->N + 1) + 2ull * c->NL;
+    info->fd_passes = c->fd_passes;
     return FDIRW_OK;
 }
 

@@ -183,7 +183,7 @@ static fdirw_status derive(const fdirw_params& p, Derived* d)
 // ‖p_m(A)δ − A^n δ‖₂ ≤ that tail.  The c_k come from an M-point discrete Chebyshev
 // transform of x^n (fp64; aliasing is below the tail once M ≥ 4m).  Returns m (0 = the
 // recurrence would not save work: keep the n_fd direct substeps).
-static int cheb_plan(int n, double lam_max, std::vector<float>* coef)
+int fdirw::cheb_plan(int n, double lam_max, std::vector<float>* coef)
 {
     const double tol = 1e-10;
     const int kmax = 2048;  // coefficients live in the kgen CTA's shared memory
@@ -216,7 +216,6 @@ static int cheb_plan(int n, double lam_max, std::vector<float>* coef)
 // kgen's plan for these params: kCheb_pre direct substeps first (the peaked start: its entries
 // of size ~1 would otherwise enter the recurrence and its rounding), then the Chebyshev degree
 // for the remaining n_fd − kCheb_pre.  Returns that degree (0 = all n_fd substeps direct).
-static const int kCheb_pre = 8;
 static int kgen_cheb(const fdirw_params& p, const Derived& d, std::vector<float>* coef)
 {
     if (p.flags & (FDIRW_F_KGEN_FP64 | FDIRW_F_KGEN_DIRECT)) return 0;

@@ -1,5 +1,6 @@
 // fdirw_internal.h — internal types shared by the FDiRW CUDA sources (not part of the ABI).
 #pragma once
+#include <vector>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -46,6 +47,13 @@ struct Derived {
     int n_fd;
     double dt_fd, lam_ff, lam_fs, lam_ss;
 };
+
+// Chebyshev evaluation of x^n on the spectrum [1 − 12λ_max, 1] of an explicit-FD operator
+// (fdirw_api.cu, reading A30): coefficients c_0..c_m (fp32) with tail ≤ 1e-10; returns m,
+// 0 when the recurrence would not save work.  kgen and the coarse P columns run
+// kCheb_pre literal substeps first.
+int cheb_plan(int n, double lam_max, std::vector<float>* coef);
+constexpr int kCheb_pre = 8;
 
 // ---- kernels (kgen.cu / superpose.cu) --------------------------------------------
 struct KgenArgs {

@@ -455,10 +455,11 @@ def test_cfg5_r8_sampled(fd, oracle_lib):
 
 
 # ------------------------------------------------------------------ NEXT row N1: coarse-mesh FDiRW
-@pytest.mark.parametrize("fmt,b", [("fp32", 3), ("bf16", 4), ("fp16", 5)])
-def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b):
+@pytest.mark.parametrize("fmt,b,direct", [("fp32", 3, False), ("fp32", 3, True), ("bf16", 4, False), ("fp16", 5, False)])
+def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b, direct):
     """N1 (Eqs.10-15): GPU-built P vs the oracle's P (FD from group-uniform
-    sources, group means), and coarse steps vs the oracle's map → P·C → remap."""
+    sources, group means), and coarse steps vs the oracle's map → P·C → remap.  P columns by
+    the Chebyshev evaluation (default, reading A30) and by the literal substeps."""
     import torch
     from oracle import coarse as oc
 
@@ -472,9 +473,10 @@ def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b):
     ref = c0
     for _ in range(3):
         ref = oc.step(P, g, sizes, ref)
-    ctx = fd.coarse_build(lib_params(cfg, fmt), region, block=b)
+    ctx = fd.coarse_build(lib_params(cfg, fmt, flags=fd.F_KGEN_DIRECT if direct else 0), region, block=b)
     try:
         info = ctx.info
+        assert info["fd_passes"] == (200 if direct else fd.make_plan(lib_params(cfg))["kgen_steps"])
         assert info["n_groups"] == len(sizes) and info["n_region"] == int(region.sum())
         assert info["flops_per_step"] == oc.flop_count(len(sizes), int(region.sum()))
         Pg, gg = fd.coarse_export(ctx)

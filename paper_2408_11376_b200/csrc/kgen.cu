@@ -242,7 +242,11 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 
         // (FADD2/FFMA2), then the two z fluxes from its own registers.
         // Direct: all n_fd substeps.  Chebyshev: the first cheb_pre substeps (the peaked start,
         // whose large entries would otherwise feed the recurrence's rounding), then the recurrence.
-        const int n_direct = a.cheb_m ? a.cheb_pre : a.n_fd;
+        // Windows touching the far-field reservoir (N2) keep the literal substeps: their kernel
+        // keeps only the mass M_s that did not leak, and the recurrence's rounding is on the
+        // scale of the source, not of M_s (measured: M_s relative error 7e-5 vs 5e-6).
+        const bool cheb = a.cheb_m && !open;
+        const int n_direct = cheb ? a.cheb_pre : a.n_fd;
         for (int k = 0; k < n_direct; ++k) {
             float* b = buf + (k & 1) * (NT * Lp);
             if (col) {
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 
                 for (int z = 0; z < L; ++z) c[z] = nw[z];
             }
         }
-        if (a.cheb_m) {
+        if (cheb) {
             // Chebyshev evaluation of the rest, A^{n_fd − pre} v with v = A^{pre} δ_s (DESIGN.md
             // §7, reading A30): x^n' = Σ_k c_k T_k(y) on the spectrum [a, 1] of A,
             // y = (2x − 1 − a)/(1 − a), all c_k ≥ 0 with Σ c_k = 1, truncated at degree m where the

@@ -41,6 +41,9 @@ struct KgenShape {
     static constexpr size_t buf_bytes = smem_floats * (F64 ? 8 : 4);
     static constexpr size_t smem_bytes = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
     static constexpr size_t cheb_off = smem_bytes;  // Chebyshev coefficients c_0..c_m (fp32) follow
+    // CTAs per SM the register allocation is sized for: ~128 registers per thread (R5 measured
+    // 3 → 4 CTAs: −2.5 % kernel time; R7 would spill 212 B at 2 CTAs, so it keeps 1)
+    static constexpr int kMinBlocks = (R != 7 && 65536 / (NT * 128) > 1) ? 65536 / (NT * 128) : 1;
 };
 
 __device__ __forceinline__ double warp_sum_f64(double v)
@@ -117,7 +120,7 @@ __device__ __forceinline__ double face_lambda_d(unsigned p, unsigned q, const do
 // FMA) and the result is not renormalised (fp64 FD keeps Σ = 1 to rounding), so the
 // off-centre weights are the oracle's O2 kernels rounded exactly as O5 rounds them.
 template <int R, bool F64>
-__global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 1) kgen_kernel(const KgenArgs a)
+__global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, F64>::kMinBlocks) kgen_kernel(const KgenArgs a)
 {
     using S = KgenShape<R, F64>;
     using T = typename std::conditional<F64, double, float>::type;
@@ -205,41 +208,104 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 
         // from fp64 on the host) for the Chebyshev recurrence, which steps the mapped operator
         // Â = (2A − (1 + a)I)/(1 − a) = I + Σ μ_f (c_f − c).
         float lzp[L], lzm[L];  // own +z / −z face numbers (asymmetric next to the reservoir)
-        unsigned long long lxm2[Lp / 2], lxp2[Lp / 2], lym2[Lp / 2], lyp2[Lp / 2];  // (z, z+1) pairs
+        // Lateral face numbers: cells (2h, 2h+1) packed for FFMA2/FADD2, h < NPR; the odd last
+        // cell L − 1 on its own (L = 2R + 1 is odd).
+        constexpr int NPR = (L - 1) / 2;
+        unsigned long long lxm2[NPR > 0 ? NPR : 1], lxp2[NPR > 0 ? NPR : 1], lym2[NPR > 0 ? NPR : 1],
+            lyp2[NPR > 0 ? NPR : 1];
+        float lxm1, lxp1, lym1, lyp1;
         auto faces = [&](const float fff, const float ffs, const float fss) {
+            float v[4][L];
 #pragma unroll
-            for (int h = 0; h < Lp / 2; ++h) {
-                float v[4][2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int z = 2 * h + u;
-                    const int i = z * LL + t;
-                    const bool ok = col && z < L;
-                    const unsigned p = ok ? ph[i] : 2u;
-                    v[0][u] = (ok && oxm) ? face_lambda(p, ph[i + oxm], fff, ffs, fss) : 0.f;
-                    v[1][u] = (ok && oxp) ? face_lambda(p, ph[i + oxp], fff, ffs, fss) : 0.f;
-                    v[2][u] = (ok && oym) ? face_lambda(p, ph[i + oym], fff, ffs, fss) : 0.f;
-                    v[3][u] = (ok && oyp) ? face_lambda(p, ph[i + oyp], fff, ffs, fss) : 0.f;
-                    if (z < L) {
-                        lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], fff, ffs, fss) : 0.f;
-                        lzm[z] = (col && z > 0) ? face_lambda(p, ph[i - LL], fff, ffs, fss) : 0.f;
-                    }
-                }
-                lxm2[h] = pk2(v[0][0], v[0][1]);
-                lxp2[h] = pk2(v[1][0], v[1][1]);
-                lym2[h] = pk2(v[2][0], v[2][1]);
-                lyp2[h] = pk2(v[3][0], v[3][1]);
+            for (int z = 0; z < L; ++z) {
+                const int i = z * LL + t;
+                const unsigned p = col ? ph[i] : 2u;
+                v[0][z] = (col && oxm) ? face_lambda(p, ph[i + oxm], fff, ffs, fss) : 0.f;
+                v[1][z] = (col && oxp) ? face_lambda(p, ph[i + oxp], fff, ffs, fss) : 0.f;
+                v[2][z] = (col && oym) ? face_lambda(p, ph[i + oym], fff, ffs, fss) : 0.f;
+                v[3][z] = (col && oyp) ? face_lambda(p, ph[i + oyp], fff, ffs, fss) : 0.f;
+                lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], fff, ffs, fss) : 0.f;
+                lzm[z] = (col && z > 0) ? face_lambda(p, ph[i - LL], fff, ffs, fss) : 0.f;
             }
+#pragma unroll
+            for (int h = 0; h < NPR; ++h) {
+                lxm2[h] = pk2(v[0][2 * h], v[0][2 * h + 1]);
+                lxp2[h] = pk2(v[1][2 * h], v[1][2 * h + 1]);
+                lym2[h] = pk2(v[2][2 * h], v[2][2 * h + 1]);
+                lyp2[h] = pk2(v[3][2 * h], v[3][2 * h + 1]);
+            }
+            lxm1 = v[0][L - 1];
+            lxp1 = v[1][L - 1];
+            lym1 = v[2][L - 1];
+            lyp1 = v[3][L - 1];
         };
         faces(a.lam_ff, a.lam_fs, a.lam_ss);
 #pragma unroll
         for (int z = 0; z < Lp; ++z) c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
 
-        // n_fd Jacobi substeps; faces summed −x,+x,−y,+y,−z,+z.  The window lives in
-        // smem column-major (thread t's column at t·Lp, float4-aligned): a thread
-        // reads each lateral neighbour column with Lp/4 128-bit loads (conflict-free
-        // for Lp ∈ {4, 8, 12, 20}), adds the four lateral fluxes two cells at a time
-        // (FADD2/FFMA2), then the two z fluxes from its own registers.
+        // The window in smem, one buffer of NT·L floats per parity: each column's first 4·NH
+        // cells as float4 quads laid out quad-major (quad q of column t at q·NT + t), the
+        // remaining NTL (1 or 3) cells as scalars (cell 4·NH + j at j·NT + t).  Consecutive
+        // threads touch consecutive 16 / 4 bytes: conflict-free, and no padding cell moves.
+        constexpr int NH = L / 4, NTL = L - 4 * NH;
+        auto store_col = [&](float* b, const float (&v)[Lp]) {
+            float4* b4 = reinterpret_cast<float4*>(b);
+#pragma unroll
+            for (int q = 0; q < NH; ++q) b4[q * NT + t] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) b[4 * NH * NT + j * NT + t] = v[4 * NH + j];
+        };
+        auto load_col = [&](const float* b, const int tt, float (&v)[L]) {
+            const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll
+            for (int q = 0; q < NH; ++q) {
+                const float4 w = b4[q * NT + tt];
+                v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+            }
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) v[4 * NH + j] = b[4 * NH * NT + j * NT + tt];
+        };
+        // nw += Σ over −x,+x,−y,+y of λ_f (c_f − c), cells in pairs (FADD2/FFMA2) and the last alone;
+        // then the two z faces from registers (one difference per face, used by both cells:
+        // c_{z−1} − c_z is exactly −(c_z − c_{z−1}) in IEEE arithmetic).
+        auto flux = [&](const float* b, const float (&cur)[Lp], float (&nw)[Lp]) {
+            float xm[L], xp[L], ym[L], yp[L];
+            load_col(b, t + oxm, xm);
+            load_col(b, t + oxp, xp);
+            load_col(b, t + oym, ym);
+            load_col(b, t + oyp, yp);
+#pragma unroll
+            for (int h = 0; h < NPR; ++h) {
+                const unsigned long long c2 = pk2(cur[2 * h], cur[2 * h + 1]);
+                unsigned long long s2 = pk2(nw[2 * h], nw[2 * h + 1]);
+                s2 = fma2(lxm2[h], sub2(pk2(xm[2 * h], xm[2 * h + 1]), c2), s2);
+                s2 = fma2(lxp2[h], sub2(pk2(xp[2 * h], xp[2 * h + 1]), c2), s2);
+                s2 = fma2(lym2[h], sub2(pk2(ym[2 * h], ym[2 * h + 1]), c2), s2);
+                s2 = fma2(lyp2[h], sub2(pk2(yp[2 * h], yp[2 * h + 1]), c2), s2);
+                upk2(s2, nw[2 * h], nw[2 * h + 1]);
+            }
+            {
+                const float c1 = cur[L - 1];
+                float s1 = nw[L - 1];
+                s1 = fmaf(lxm1, xm[L - 1] - c1, s1);
+                s1 = fmaf(lxp1, xp[L - 1] - c1, s1);
+                s1 = fmaf(lym1, ym[L - 1] - c1, s1);
+                s1 = fmaf(lyp1, yp[L - 1] - c1, s1);
+                nw[L - 1] = s1;
+            }
+            float dz[L > 1 ? L - 1 : 1];
+#pragma unroll
+            for (int z = 0; z + 1 < L; ++z) dz[z] = cur[z + 1] - cur[z];
+#pragma unroll
+            for (int z = 0; z < L; ++z) {
+                float v = nw[z];
+                if (z > 0) v = fmaf(lzm[z], -dz[z - 1], v);
+                if (z < L - 1) v = fmaf(lzp[z], dz[z], v);
+                nw[z] = v;
+            }
+        };
+
+        // n_fd Jacobi substeps; faces summed −x,+x,−y,+y,−z,+z.
         // Direct: all n_fd substeps.  Chebyshev: the first cheb_pre substeps (the peaked start,
         // whose large entries would otherwise feed the recurrence's rounding), then the recurrence.
         // Windows touching the far-field reservoir (N2) keep the literal substeps: their kernel
@@ -249,45 +315,13 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 
         const int n_direct = cheb ? a.cheb_pre : a.n_fd;
         for (int k = 0; k < n_direct; ++k) {
             float* b = buf + (k & 1) * (NT * Lp);
-            if (col) {
-#pragma unroll
-                for (int q = 0; q < NQ; ++q)
-                    *reinterpret_cast<float4*>(b + t * Lp + 4 * q) =
-                        make_float4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
-            }
+            if (col) store_col(b, c);
             __syncthreads();
             if (col) {
                 float nw[Lp];
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const float4 xm = *reinterpret_cast<const float4*>(b + (t + oxm) * Lp + 4 * q);
-                    const float4 xp = *reinterpret_cast<const float4*>(b + (t + oxp) * Lp + 4 * q);
-                    const float4 ym = *reinterpret_cast<const float4*>(b + (t + oym) * Lp + 4 * q);
-                    const float4 yp = *reinterpret_cast<const float4*>(b + (t + oyp) * Lp + 4 * q);
-#pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int h = 2 * q + hh;
-                        const unsigned long long cc = pk2(c[2 * h], c[2 * h + 1]);
-                        unsigned long long acc = cc;
-                        acc = fma2(lxm2[h], sub2(hh ? pk2(xm.z, xm.w) : pk2(xm.x, xm.y), cc), acc);
-                        acc = fma2(lxp2[h], sub2(hh ? pk2(xp.z, xp.w) : pk2(xp.x, xp.y), cc), acc);
-                        acc = fma2(lym2[h], sub2(hh ? pk2(ym.z, ym.w) : pk2(ym.x, ym.y), cc), acc);
-                        acc = fma2(lyp2[h], sub2(hh ? pk2(yp.z, yp.w) : pk2(yp.x, yp.y), cc), acc);
-                        upk2(acc, nw[2 * h], nw[2 * h + 1]);
-                    }
-                }
-                // z faces: one difference per face, used by both cells (c_{z−1} − c_z is
-                // exactly −(c_z − c_{z−1}) in IEEE arithmetic, so the bits do not change)
-                float dz[L > 1 ? L - 1 : 1];
-#pragma unroll
-                for (int z = 0; z + 1 < L; ++z) dz[z] = c[z + 1] - c[z];
-#pragma unroll
-                for (int z = 0; z < L; ++z) {
-                    float acc = nw[z];
-                    if (z > 0) acc = fmaf(lzm[z], -dz[z - 1], acc);
-                    if (z < L - 1) acc = fmaf(lzp[z], dz[z], acc);
-                    nw[z] = acc;
-                }
+                for (int z = 0; z < L; ++z) nw[z] = c[z];
+                flux(b, c, nw);
 #pragma unroll
                 for (int z = 0; z < L; ++z) c[z] = nw[z];
             }
@@ -311,42 +345,22 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, (!F64 && R == 5) ? 4 : 
             // prv ← κ·Â·cur − prv, κ = 2 (κ = 1, prv = 0 on the first step: 2Âδ·½, exact)
             auto step = [&](float (&cur)[Lp], float (&prv)[Lp], const int k, const bool first) {
                 float* b = buf + ((k + n_direct) & 1) * (NT * Lp);
-                if (col) {
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q)
-                        *reinterpret_cast<float4*>(b + t * Lp + 4 * q) =
-                            make_float4(cur[4 * q], cur[4 * q + 1], cur[4 * q + 2], cur[4 * q + 3]);
-                }
+                if (col) store_col(b, cur);
                 __syncthreads();
                 const float ck = cc[k + 1];
                 if (col) {
                     float nw[Lp];
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) {
-                        const float4 xm = *reinterpret_cast<const float4*>(b + (t + oxm) * Lp + 4 * q);
-                        const float4 xp = *reinterpret_cast<const float4*>(b + (t + oxp) * Lp + 4 * q);
-                        const float4 ym = *reinterpret_cast<const float4*>(b + (t + oym) * Lp + 4 * q);
-                        const float4 yp = *reinterpret_cast<const float4*>(b + (t + oyp) * Lp + 4 * q);
-#pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {
-                            const int h = 2 * q + hh;
-                            const unsigned long long c2 = pk2(cur[2 * h], cur[2 * h + 1]);
-                            unsigned long long s2 = fma2(pk2(2.f, 2.f), c2, pk2(-prv[2 * h], -prv[2 * h + 1]));
-                            s2 = fma2(lxm2[h], sub2(hh ? pk2(xm.z, xm.w) : pk2(xm.x, xm.y), c2), s2);
-                            s2 = fma2(lxp2[h], sub2(hh ? pk2(xp.z, xp.w) : pk2(xp.x, xp.y), c2), s2);
-                            s2 = fma2(lym2[h], sub2(hh ? pk2(ym.z, ym.w) : pk2(ym.x, ym.y), c2), s2);
-                            s2 = fma2(lyp2[h], sub2(hh ? pk2(yp.z, yp.w) : pk2(yp.x, yp.y), c2), s2);
-                            upk2(s2, nw[2 * h], nw[2 * h + 1]);
-                        }
+                    for (int h = 0; h < NPR; ++h) {
+                        const unsigned long long s2 =
+                            fma2(pk2(2.f, 2.f), pk2(cur[2 * h], cur[2 * h + 1]), pk2(-prv[2 * h], -prv[2 * h + 1]));
+                        upk2(s2, nw[2 * h], nw[2 * h + 1]);
                     }
-                    float dz[L > 1 ? L - 1 : 1];
-#pragma unroll
-                    for (int z = 0; z + 1 < L; ++z) dz[z] = cur[z + 1] - cur[z];
+                    nw[L - 1] = fmaf(2.f, cur[L - 1], -prv[L - 1]);
+                    flux(b, cur, nw);
 #pragma unroll
                     for (int z = 0; z < L; ++z) {
                         float v = nw[z];
-                        if (z > 0) v = fmaf(lzm[z], -dz[z - 1], v);
-                        if (z < L - 1) v = fmaf(lzp[z], dz[z], v);
                         if (first) v *= 0.5f;
                         prv[z] = v;
                         acc[z] = fmaf(ck, v, acc[z]);

@@ -104,7 +104,7 @@ const char* coarse_set_error(const std::string& m)  // coarse.cu shares the thre
 
 namespace fdirw {
 
-Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1)
+Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1, bool balance)
 {
     Geometry g{};
     g.nx = nx; g.ny = ny; g.nz = nz; g.R = R;
@@ -115,6 +115,24 @@ Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1)
     g.cpp = ny * g.nxq;
     int tile = ((g.cpp + 31) / 32) * 32;
     g.tile = tile > 256 ? 256 : tile;
+    if (balance && g.tile == 256) {
+        // Wave balance for slabs of a few waves (strong scaling: 192³ over 8 ranks is 432 tiles
+        // of 256 chunks = 1.46 waves of the 296 CTAs a B200 runs at once, measured 0.92 of the
+        // ideal per-rank time): among tiles of 256, 224, 192, 160 or 128 chunks take the one
+        // whose model time waves·tile is least (ties: the larger tile).  Only for launches of
+        // < 4 waves; results do not depend on the tiling (each target is one thread's sum).
+        const long slots = 2L * 148;
+        long best_t = 256, best_cost = -1;
+        const long n256 = (long)g.nzl * ((g.cpp + 255) / 256);
+        if (n256 < 4 * slots) {
+            for (int t = 256; t >= 128; t -= 32) {
+                const long n = (long)g.nzl * ((g.cpp + t - 1) / t);
+                const long cost = ((n + slots - 1) / slots) * t;
+                if (best_cost < 0 || cost < best_cost) { best_cost = cost; best_t = t; }
+            }
+            g.tile = (int)best_t;
+        }
+    }
     g.tpp = (g.cpp + g.tile - 1) / g.tile;
     g.n_tiles = g.nzl * g.tpp;
     g.nxp = g.nxq * kChunk + 2 * kPadX;
@@ -405,7 +423,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     } else {
         cudaGetDevice(&c->device);
     }
-    c->g = make_geometry(params->nx, params->ny, params->nz, params->radius, z0, z1);
+    c->g = make_geometry(params->nx, params->ny, params->nz, params->radius, z0, z1,
+                         !(params->flags & FDIRW_F_DEDUP_STORAGE) && !(params->v_far > 0));
     const Geometry& g = c->g;
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
 
@@ -1034,7 +1053,7 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
     if ((st = derive(*p, &d)) != FDIRW_OK) return st;
     const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
     const Geometry g = make_geometry(p->nx, p->ny, p->nz, p->radius, dist ? dist->z_begin : 0,
-                                     dist ? dist->z_end : p->nz);
+                                     dist ? dist->z_end : p->nz, !(p->flags & FDIRW_F_DEDUP_STORAGE) && !(p->v_far > 0));
     const HaloPlan h = make_halo_plan(g, rank, world);
     int i0, i1;
     split_tiles(g, &i0, &i1);

@@ -31,7 +31,7 @@ struct Geometry {
     int sz0, sz1;                // source planes whose windows reach the slab
 };
 
-Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1);
+Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1, bool balance = false);
 
 // a6: which padded planes move where (element offsets into the padded state; −1 = no peer).
 //   send padded planes [R, 2R)        → rank−1    recv padded [0, R)          ← rank−1

@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
 // compute warps have read it; the producer refills stage st for row i + S only after that.
 // The weight bytes in flight no longer depend on how many warps are waiting on loads: each
 // SM keeps up to 2 CTAs × S rows outstanding with one thread issuing them.
-constexpr int kBulkWarps = 8;
+constexpr int kBulkWarps = 8;  // at most: a tile of ≤ 256 chunks = a.tile/32 compute warps
 template <int R, typename WT>
 __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, unsigned char* smem_b)
 {
@@ -591,15 +591,16 @@ __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, un
     unsigned char* stg = smem_b + 128;
     const uint32_t slotB = (uint32_t)a.tile * 8 * sizeof(WT), stageB = (uint32_t)L * slotB;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = a.tile >> 5;  // compute warps
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(smem_u32(full + i), 1);
-            mbar_init(smem_u32(empty + i), kBulkWarps);
+            mbar_init(smem_u32(empty + i), nw);
         }
         mbar_init_fence();
     }
     __syncthreads();
-    const bool producer = warp == kBulkWarps;
+    const bool producer = warp == nw;
     const int e = producer ? 0 : (int)threadIdx.x;
     TileCtx t = tile_ctx<R>(a, blk, e);
     float hi[8], lo[8];
@@ -710,7 +711,7 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
     // TMA-staged weight stream for launches of ≥ 2 CTAs per SM (the common case); the
     // register-prefetching body below for smaller launches (one wave: no CTA to overlap the
     // pipeline fill with) or FDIRW_F_NO_BULK_STREAM.  Identical bits either way.
-    if (!a.no_bulk && nblk >= 2 * 148 && a.tile == kBulkWarps * 32) {
+    if (!a.no_bulk && nblk >= 2 * 148 && a.tile % 32 == 0 && a.tile <= kBulkWarps * 32) {
         const int b_w = fmt == 0 ? 4 : 2;
         int cps = 0;
         const int S = bulk_stages(R, b_w, a.tile, &cps);
@@ -721,7 +722,7 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
                                      : (const void*)superpose_bulk_kernel<R, __nv_bfloat16>;
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            const int nt = (kBulkWarps + 1) * 32;
+            const int nt = a.tile + 32;
             if (fmt == 0) superpose_bulk_kernel<R, float><<<nblk, nt, smem, s>>>(a, S);
             else if (fmt == 1) superpose_bulk_kernel<R, __half><<<nblk, nt, smem, s>>>(a, S);
             else superpose_bulk_kernel<R, __nv_bfloat16><<<nblk, nt, smem, s>>>(a, S);

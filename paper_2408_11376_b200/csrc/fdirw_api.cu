@@ -5,6 +5,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -241,6 +242,24 @@ static int kgen_cheb(const fdirw_params& p, const Derived& d, std::vector<float>
     return cheb_plan(d.n_fd - kCheb_pre, std::max(d.lam_ff, std::max(d.lam_fs, d.lam_ss)), coef);
 }
 
+// FDIRW_TRACE=1: host-side phase timings of fdirw_build_kernels on stderr (the stream is
+// synchronised at each mark only when tracing, so an untraced build is unaffected).
+struct BuildTrace {
+    bool on = getenv("FDIRW_TRACE") != nullptr;
+    cudaStream_t s = nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
+    void mark(const char* what)
+    {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "fdirw trace: build %-22s %9.2f ms  (total %9.2f ms)\n", what,
+                std::chrono::duration<double, std::milli>(n - t).count(),
+                std::chrono::duration<double, std::milli>(n - t0).count());
+        t = n;
+    }
+};
+
 static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const fdirw_dist* dist,
                              fdirw_ctx** out, bool scan_phase = true)
 {
@@ -393,9 +412,11 @@ static fdirw_status far_compact(fdirw_ctx* c, const uint8_t* phase_host, cudaStr
 extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const uint8_t* phase_host,
                                             const fdirw_dist* dist, void* cuda_stream, fdirw_ctx** out)
 {
+    BuildTrace tr;
     fdirw_status st = validate(params, phase_host, dist, out);
     if (st != FDIRW_OK) return st;
     *out = nullptr;
+    tr.mark("validate");
     Derived d;
     if ((st = derive(*params, &d)) != FDIRW_OK) return st;
     if ((params->flags & FDIRW_F_SYMMETRIC_RULE) && d.n_fd > params->radius)
@@ -427,6 +448,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                          !(params->flags & FDIRW_F_DEDUP_STORAGE) && !(params->v_far > 0));
     const Geometry& g = c->g;
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    tr.s = s;
 
     auto bail = [&](fdirw_status e) {
         std::string keep = g_err;
@@ -457,6 +479,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     BAIL_CUDA(cudaMemcpyAsync(mask_d, phase_host + (size_t)g.mz0 * plane, mbytes, cudaMemcpyHostToDevice, s));
     BAIL_CUDA(cudaMemsetAsync(c->cpad[0], 0, g.state_elems * 4, s));
     BAIL_CUDA(cudaMemsetAsync(c->cpad[1], 0, g.state_elems * 4, s));
+    tr.mark("alloc state + mask");
 
     // a3 + a4
     KgenArgs ka{};
@@ -514,6 +537,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         cudaError_t e = cudaMemsetAsync(class_pad, 0xff, g.state_elems * 4, s);
         DedupArgs da{mask_d, g.mz0, g.nx, g.ny, g.nz, g.R, g.sz0, g.sz1, g.z0, g.nxp, g.nyp, class_pad};
         if (e == cudaSuccess) e = dedup_classify(da, &dr, s);
+        tr.mark("dedup classify");
         if (e != cudaSuccess) { dfree(); cudaFree(mask_d); g_err = std::string("dedup: ") + cudaGetErrorString(e); return bail(FDIRW_E_CUDA); }
         if (dr.collision) {
             dedup = false;  // hash collision detected by the exact check: take the direct path
@@ -531,6 +555,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             if (e == cudaSuccess) e = cudaEventRecord(c->kev[0], s);
             if (e == cudaSuccess) e = launch_kgen(ka, g.R, s);
             if (e == cudaSuccess) e = cudaEventRecord(c->kev[1], s);
+            tr.mark("kgen (distinct windows)");
             ExpandArgs ea{class_pad, class_w, class_diag, nullptr, nullptr, g.nx, g.ny, g.nxq, g.tile, g.tpp,
                           g.n_tiles, g.nxp, g.nyp};
             size_t w_elems = g.w_elems, d_elems = g.diag_elems;
@@ -558,7 +583,9 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                 }
                 ea.Wt = c->Wt;
                 ea.diag = c->diag;
+                tr.mark("compact + alloc weights");
                 e = launch_expand(ea, g.R, c->fmt, s);
+                tr.mark("expand");
             }
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) { dfree(); cudaFree(mask_d); g_err = std::string("kgen: ") + cudaGetErrorString(e); return bail(FDIRW_E_CUDA); }
@@ -582,12 +609,14 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         BAIL_CUDA(cudaEventRecord(c->kev[0], s));
         BAIL_CUDA(launch_kgen(ka, g.R, s));
         BAIL_CUDA(cudaEventRecord(c->kev[1], s));
+        tr.mark("kgen (every source)");
     }
     BAIL_CUDA(cudaStreamSynchronize(s));
     cudaFree(c->cheb_d);
     c->cheb_d = nullptr;
     BAIL_CUDA(cudaEventElapsedTime(&c->kgen_ms, c->kev[0], c->kev[1]));
 
+    tr.mark("sync");
     c->v_far = params->v_far;
     c->far = params->v_far > 0;
     if (c->far) {  // N2: far-field mask of the slab, p_BC, Eq.7 reduction buffers
@@ -651,6 +680,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         BAIL_CUDA(cudaStreamSynchronize(c->comm_stream));
     }
 #undef BAIL_CUDA
+    tr.mark("far field / comm / end");
     *out = c;
     return FDIRW_OK;
 }

@@ -454,6 +454,34 @@ def test_cfg5_r8_sampled(fd, oracle_lib):
     assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= 5e-3
 
 
+def test_cfg4_384_one_gpu_sampled(fd, oracle_lib):
+    """BASELINE configs[3]'s workload on ONE GPU (150.8 GB of bf16 weights resident): 384³ =
+    2×2×2 R50 particles, Table 1 SI parameters, R5.  One step through fdirw_run; sampled boxes
+    vs the oracle — a particle surface in the far octant, the seam between octants, and a
+    ragged domain corner; whole-grid mass."""
+    import torch
+
+    cfg = fi.config("cfg4")
+    mask = cfg.mask()
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "paper")
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        assert ctx.info["n_fd"] == 1000 and ctx.info["weight_bytes"] > 150e9
+        c = torch.from_numpy(c0).cuda()
+        m0 = fd.mass(ctx, c)
+        fd.run(ctx, c, 1)
+        m1 = fd.mass(ctx, c)
+        got = c.cpu().numpy()
+        del c
+    finally:
+        fd.destroy(ctx)
+    assert abs(m1 - m0) / m0 <= 1e-6
+    for tb in [(332, 338, 285, 291, 286, 290), (189, 195, 94, 99, 94, 98), (379, 384, 0, 6, 381, 384)]:
+        ref = oracle_lib.step_box(pb, c0.astype(np.float64), tb)
+        assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= 5e-3, tb
+
+
 # ------------------------------------------------------------------ NEXT row N1: coarse-mesh FDiRW
 @pytest.mark.parametrize("fmt,b,direct", [("fp32", 3, False), ("fp32", 3, True), ("bf16", 4, False), ("fp16", 5, False)])
 def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b, direct):

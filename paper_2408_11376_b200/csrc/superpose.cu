@@ -582,16 +582,22 @@ __global__ void __launch_bounds__(256) superpose_kernel(const SuperArgs a)
 // The weight bytes in flight no longer depend on how many warps are waiting on loads: each
 // SM keeps up to 2 CTAs × S rows outstanding with one thread issuing them.
 constexpr int kBulkWarps = 8;  // at most: a tile of ≤ 256 chunks = a.tile/32 compute warps
+// sub = chunks per CTA: the whole tile (sub = a.tile), or a part of it (a.tile / sub CTAs per
+// tile, CTA blk → tile blk / nsub, part blk % nsub) so that short launches quantise into
+// smaller units (wave balance, see launch_superpose_r).  A part's weights for one slot are a
+// contiguous sub·8 run inside the tile's slot block: the producer copies them slot by slot.
 template <int R, typename WT>
-__device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, unsigned char* smem_b)
+__device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, int sub, unsigned char* smem_b)
 {
     constexpr int L = 2 * R + 1, K = L * L * L, NROW = L * L;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_b);
     uint64_t* empty = full + S;
     unsigned char* stg = smem_b + 128;
-    const uint32_t slotB = (uint32_t)a.tile * 8 * sizeof(WT), stageB = (uint32_t)L * slotB;
+    const int nsub = a.tile / sub, part = blk % nsub;
+    const uint32_t slotB = (uint32_t)a.tile * 8 * sizeof(WT);  // one slot of the whole tile
+    const uint32_t subB = (uint32_t)sub * 8 * sizeof(WT), stageB = (uint32_t)L * subB;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nw = a.tile >> 5;  // compute warps
+    const int nw = sub >> 5;  // compute warps
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(smem_u32(full + i), 1);
@@ -601,20 +607,27 @@ __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, un
     }
     __syncthreads();
     const bool producer = warp == nw;
-    const int e = producer ? 0 : (int)threadIdx.x;
-    TileCtx t = tile_ctx<R>(a, blk, e);
+    const int e = part * sub + (producer ? 0 : (int)threadIdx.x);
+    TileCtx t = tile_ctx<R>(a, blk / nsub, e);
     float hi[8], lo[8];
     if (producer) {
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
-            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.Wt) + (size_t)t.tile * (K - 1) * slotB;
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.Wt) +
+                                       (size_t)t.tile * (K - 1) * slotB + (size_t)part * subB;
             for (int i = 0; i < NROW; ++i) {
                 const int st = i % S, u = i / S;
-                const uint32_t n = (i == 0 ? L - 1 : L) * slotB;
+                const int n = i == 0 ? L - 1 : L;
                 if (u > 0) mbar_wait(smem_u32(empty + st), (u - 1) & 1);
-                mbar_expect_tx(smem_u32(full + st), n);
-                bulk_g2s(smem_u32(stg + (size_t)st * stageB), src, n, smem_u32(full + st), pol);
-                src += n;
+                mbar_expect_tx(smem_u32(full + st), (uint32_t)n * subB);
+                if (nsub == 1) {
+                    bulk_g2s(smem_u32(stg + (size_t)st * stageB), src, (uint32_t)n * subB, smem_u32(full + st), pol);
+                } else {
+                    for (int k = 0; k < n; ++k)
+                        bulk_g2s(smem_u32(stg + (size_t)st * stageB + (size_t)k * subB), src + (size_t)k * slotB, subB,
+                                 smem_u32(full + st), pol);
+                }
+                src += (size_t)n * slotB;
             }
         }
         t.real = false;  // joins the epilogue only for tile_sum's CTA-wide reduction
@@ -622,7 +635,7 @@ __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, un
         for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.f;
     } else {
         diag_init(a, t, e, hi, lo);
-        const unsigned char* wb = stg + (size_t)e * 8 * sizeof(WT);
+        const unsigned char* wb = stg + (size_t)threadIdx.x * 8 * sizeof(WT);
         // the row's C segment is loaded before waiting for its weights (the L1/L2 latency
         // overlaps the stage's arrival)
         float seg[24];
@@ -631,8 +644,8 @@ __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, un
             if (t.real) load_seg(row_src<R>(t, i), seg);
             mbar_wait(smem_u32(full + st), u & 1);
             if (t.real) {
-                if (i == 0) do_row_s<R, WT, true>(seg, wb + (size_t)st * stageB, slotB, hi, lo);
-                else do_row_s<R, WT, false>(seg, wb + (size_t)st * stageB, slotB, hi, lo);
+                if (i == 0) do_row_s<R, WT, true>(seg, wb + (size_t)st * stageB, subB, hi, lo);
+                else do_row_s<R, WT, false>(seg, wb + (size_t)st * stageB, subB, hi, lo);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(empty + st));
@@ -642,10 +655,10 @@ __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, un
 }
 
 template <int R, typename WT>
-__global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(const SuperArgs a, int S)
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(const SuperArgs a, int S, int sub)
 {
     extern __shared__ __align__(128) unsigned char smem_b[];
-    bulk_body<R, WT>(a, blockIdx.x, S, smem_b);
+    bulk_body<R, WT>(a, blockIdx.x, S, sub, smem_b);
 }
 
 // N4 with the staged stream: the mixed launch's dense tiles run bulk_body, its uniform blocks
@@ -658,7 +671,7 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_mixed_bulk_ke
     const long T = gridDim.x, U = u.n_blocks, b = blockIdx.x;
     const long u0 = b * U / T, u1 = (b + 1) * U / T;
     if (u1 > u0) uniform_body<R>(u, (int)u0, reinterpret_cast<float*>(smem_b + 128));
-    else bulk_body<R, WT>(a, (int)(b - u0), S, smem_b);
+    else bulk_body<R, WT>(a, (int)(b - u0), S, a.tile, smem_b);
 }
 
 // stages of the bulk kernel: 2 CTAs per SM with ≥ 2 stages each, else 1 CTA with ≥ 2; 0 = the
@@ -714,18 +727,35 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
     if (!a.no_bulk && nblk >= 2 * 148 && a.tile % 32 == 0 && a.tile <= kBulkWarps * 32) {
         const int b_w = fmt == 0 ? 4 : 2;
         int cps = 0;
-        const int S = bulk_stages(R, b_w, a.tile, &cps);
-        if (S > 0) {
-            const size_t smem = 128 + (size_t)S * (2 * R + 1) * a.tile * 8 * b_w;
+        const int S1 = bulk_stages(R, b_w, a.tile, &cps);
+        if (S1 > 0) {
+            // Wave balance for short launches (e.g. the compacted tiles of an open domain, N2):
+            // split each tile into nsub ∈ {1, 2, 4} parts of a.tile/nsub chunks (≥ 64), at the
+            // same CTAs per SM, when the modelled time waves·(chunks per CTA) drops.  Not with
+            // in-kernel per-tile sums (N2 multi-rank Eq.7), which need the whole tile.
+            int nsub = 1;
+            if (!a.tile_sum && nblk < 4 * cps * 148) {
+                const long slots = (long)cps * 148;
+                long best = -1;
+                for (int d = 1; d <= 4 && a.tile / d >= 64 && (a.tile / d) % 32 == 0; d *= 2) {
+                    const long cost = (((long)nblk * d + slots - 1) / slots) * (a.tile / d);
+                    if (best < 0 || cost < best) { best = cost; nsub = d; }
+                }
+            }
+            const int sub = a.tile / nsub;
+            int S = S1 * nsub;  // same shared memory per CTA: stages of a part are nsub× smaller
+            if (S > 8) S = 8;
+            const size_t smem = 128 + (size_t)S * (2 * R + 1) * sub * 8 * b_w;
             const void* f = fmt == 0 ? (const void*)superpose_bulk_kernel<R, float>
                           : fmt == 1 ? (const void*)superpose_bulk_kernel<R, __half>
                                      : (const void*)superpose_bulk_kernel<R, __nv_bfloat16>;
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            const int nt = a.tile + 32;
-            if (fmt == 0) superpose_bulk_kernel<R, float><<<nblk, nt, smem, s>>>(a, S);
-            else if (fmt == 1) superpose_bulk_kernel<R, __half><<<nblk, nt, smem, s>>>(a, S);
-            else superpose_bulk_kernel<R, __nv_bfloat16><<<nblk, nt, smem, s>>>(a, S);
+            const int nt = sub + 32;
+            const int grid = nblk * nsub;
+            if (fmt == 0) superpose_bulk_kernel<R, float><<<grid, nt, smem, s>>>(a, S, sub);
+            else if (fmt == 1) superpose_bulk_kernel<R, __half><<<grid, nt, smem, s>>>(a, S, sub);
+            else superpose_bulk_kernel<R, __nv_bfloat16><<<grid, nt, smem, s>>>(a, S, sub);
             return cudaGetLastError();
         }
     }

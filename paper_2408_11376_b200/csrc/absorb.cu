@@ -215,8 +215,8 @@ __global__ void superpose_study_kernel(const StudyArgs a)
         const long p = pidx(x, y, zl, R, a.nxp, a.nyp);
         if (a.chunk_pos) {  // N2 compaction: all-far chunks have no weights (their targets hold 0)
             const int cp = a.chunk_pos[tile * a.tile + e];
-            if (cp < 0) {
-                a.out[p] = 0.f;
+            if (cp < 0) {  // −2: identity row (impermeable solid target, D_slow = 0)
+                a.out[p] = cp == -2 ? a.cpad[p] : 0.f;
                 continue;
             }
             tile = cp / a.tile;

@@ -57,6 +57,12 @@ struct fdirw_ctx {
     // chunk (tile·tile + e) to its compact position or −1
     bool compact = false;
     int* chunk_pos = nullptr;
+    // ... and with D_slow = 0 (the N3 loop's liquid step) chunks whose non-far
+    // targets are all solid: those rows are the identity (W_s = δ for an isolated solid source,
+    // no liquid source reaches a solid target, diag = 1, p_BC = 0), so they carry no weights
+    // either and the step copies C_old → C_new for them (chunk_pos −2)
+    int* ident_list = nullptr;
+    long n_ident = 0;
     // N3 integrated loop / precision modes (world == 1)
     int prec_mode = 0;            // 0 = default kernel; 1/2/3 = §3.3 study modes (absorb.cu)
     uint8_t* phase_pp = nullptr;  // padded phase map (255 outside)
@@ -336,6 +342,7 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->gathered);
     cudaFree(c->far_state);
     cudaFree(c->chunk_pos);
+    cudaFree(c->ident_list);
     cudaFree(c->phase_pp);
     cudaFree(c->alpha);
     cudaFree(c->kin_part);
@@ -379,25 +386,41 @@ extern "C" fdirw_status fdirw_nccl_unique_id(void* out128)
 }
 
 // N2 (world == 1): list the chunks (tile·tile + e, ascending) holding at least one non-far
-// target; the rest carry no weights.  Fills c->ut.{dense_list, n_dense, nd_tiles}, chunk_pos.
+// target; the rest carry no weights.  With D_slow = 0, chunks whose non-far targets are all
+// solid are identity rows: listed apart (ident_list, chunk_pos −2), no weights either.
+// Fills c->ut.{dense_list, n_dense, nd_tiles}, chunk_pos, ident_list.
 static fdirw_status far_compact(fdirw_ctx* c, const uint8_t* phase_host, cudaStream_t s)
 {
     const Geometry& g = c->g;
     const size_t nch = (size_t)g.n_tiles * g.tile;
-    std::vector<int> pos(nch, -1), list;
+    const bool ident = c->p.D_slow == 0.0;
+    std::vector<int> pos(nch, -1), list, idl;
     list.reserve(nch);
     for (int zl = 0; zl < g.nzl; ++zl)
         for (int q = 0; q < g.ny * g.nxq; ++q) {
             const int y = q / g.nxq, x0 = (q % g.nxq) * 8;
             const uint8_t* row = phase_host + ((size_t)(g.z0 + zl) * g.ny + y) * g.nx;
-            bool any = false;
-            for (int j = 0; j < 8 && x0 + j < g.nx; ++j) any |= row[x0 + j] != 2;
+            bool any = false, liquid = false;
+            for (int j = 0; j < 8 && x0 + j < g.nx; ++j) {
+                any |= row[x0 + j] != 2;
+                liquid |= row[x0 + j] == 1;
+            }
             if (!any) continue;
             const int ch = (zl * g.tpp + q / g.tile) * g.tile + q % g.tile;
+            if (ident && !liquid) {
+                pos[ch] = -2;
+                idl.push_back(ch);
+                continue;
+            }
             pos[ch] = (int)list.size();
             list.push_back(ch);
         }
     fdirw_status st;
+    if (!idl.empty()) {
+        if ((st = alloc((void**)&c->ident_list, idl.size() * 4, "identity chunks")) != FDIRW_OK) return st;
+        CUDA_TRY(cudaMemcpyAsync(c->ident_list, idl.data(), idl.size() * 4, cudaMemcpyHostToDevice, s));
+        c->n_ident = (long)idl.size();
+    }
     if ((st = alloc((void**)&c->ut.dense_list, (list.size() + 1) * 4, "far compaction list")) != FDIRW_OK) return st;
     if ((st = alloc((void**)&c->chunk_pos, nch * 4, "far compaction map")) != FDIRW_OK) return st;
     if (!list.empty()) CUDA_TRY(cudaMemcpyAsync(c->ut.dense_list, list.data(), list.size() * 4, cudaMemcpyHostToDevice, s));
@@ -874,6 +897,8 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
         }
         if (c->compact) {  // N2 compacted: superpose the listed chunks, Eq.7 sums per global tile
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, c->ut.nd_tiles, s));
+            if (c->n_ident)  // identity rows (impermeable solid): C_new = C_old
+                CUDA_TRY(launch_copy_chunks(src, out, ps, rs, c->ident_list, c->n_ident, g, s));
             if (ps == (long)g.plane_elems) CUDA_TRY(launch_tile_mass_padded(out, c->farmask, g, c->tile_buf + 1, s));
             else CUDA_TRY(launch_tile_mass(out, c->farmask, g, c->tile_buf + 1, s));
             return far_reduce(c, s, 0, 0.0);

@@ -153,6 +153,9 @@ struct SuperArgs {
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
 cudaError_t launch_read_stream(const void* p, size_t bytes, unsigned* sink, int sms, cudaStream_t s);
+// identity rows (N2 compaction with D_slow = 0): out(chunk) = C_old(chunk) for the listed chunks
+cudaError_t launch_copy_chunks(const float* cpad, float* out, long out_ps, long out_rs, const int* list, long n,
+                               const Geometry& g, cudaStream_t s);
 
 // N4: uniform chunks, one CTA per block of ≤ 256 chunks of one class (superpose.cu)
 struct UniArgs {

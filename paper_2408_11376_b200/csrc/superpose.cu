@@ -846,6 +846,35 @@ cudaError_t launch_read_stream(const void* p, size_t bytes, unsigned* sink, int 
     return cudaGetLastError();
 }
 
+// Identity rows: chunk ch (tile·tile + e) of the slab, 8 targets, C_new = C_old (bitwise what
+// the dense path computes for them: d = 1, every other weight 0, p_BC = 0).
+__global__ void copy_chunks_kernel(const float* __restrict__ cpad, float* __restrict__ out, long out_ps, long out_rs,
+                                   const int* __restrict__ list, long n, int nx, int nxq, int tile, int tpp, int nxp,
+                                   int nyp, int R)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int ch = list[i];
+        const int t = ch / tile, e = ch % tile;
+        const int zl = t / tpp, q = (t % tpp) * tile + e;
+        const int y = q / nxq, x = (q % nxq) * 8;
+        const float* src = cpad + ((long)(zl + R) * nyp + (y + R)) * nxp + kPadX + x;
+        float* dst = out + (long)zl * out_ps + (long)y * out_rs + x;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (x + j < nx) dst[j] = src[j];
+    }
+}
+
+cudaError_t launch_copy_chunks(const float* cpad, float* out, long out_ps, long out_rs, const int* list, long n,
+                               const Geometry& g, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    const long blocks = (n + 255) / 256;
+    copy_chunks_kernel<<<(unsigned)(blocks < 148L * 8 ? blocks : 148L * 8), 256, 0, s>>>(
+        cpad, out, out_ps, out_rs, list, n, g.nx, g.nxq, g.tile, g.tpp, g.nxp, g.nyp, g.R);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s)
 {
     switch (R) {
@@ -1114,7 +1143,9 @@ __global__ void export_kernel(const void* __restrict__ Wt, const float* __restri
                 e = cp % g.tile;
             }
             if (chunk_pos && cp < 0) {
-                v = 0.0;  // an all-far chunk: no weights stored (they are 0)
+                // an all-far chunk (−1): no weights stored (they are 0); an identity chunk (−2,
+                // impermeable solid targets): the centre weight is 1, every other 0
+                v = (cp == -2 && o == g.K / 2) ? 1.0 : 0.0;
             } else if (o == g.K / 2) {
                 v = diag[(tile * g.tile + e) * 8 + j];
             } else {

@@ -156,3 +156,35 @@ def test_cfg3o_open_r50_sampled(fd, oracle_lib):
     for tb in [(107, 112, 57, 62, 58, 62), (112, 117, 58, 63, 57, 61)]:
         ref = ff.step_box_far(pb, c0.astype(np.float64), cfg.c_far0, tb, fmt=None)
         assert rel_l2(got[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], ref) <= 5e-3, tb
+
+
+def test_identity_rows_bitwise(fd):
+    """Impermeable solid (D_slow = 0, the N3 loop's liquid step) in an open domain: chunks whose
+    non-far targets are all solid are identity rows and carry no weights (C_new = C_old by a
+    copy).  Field, c_far and exported kernels bitwise equal to the uncompacted path
+    (FDIRW_F_NO_DEDUP builds every window and streams every chunk)."""
+    import torch
+
+    shape = (26, 24, 28)
+    mask = _open_mask(shape, 11)
+    cfg = small_cfg(shape, 3, 60, D_slow=0.0, weights="bf16")
+    c0 = fi.initial_c(mask, "random", seed=11)
+    outs = []
+    for flags in (0, fd.F_NO_DEDUP):
+        ctx = fd.build_kernels(lib_params(cfg, flags=flags, v_far=500.0), mask)
+        try:
+            c = torch.from_numpy(c0.astype(np.float32)).cuda()
+            fd.far_init(ctx, c, 0.3)
+            fd.run(ctx, c, 3)
+            W = fd.export_kernels(ctx, (0, 28, 0, 24, 0, 26)) if flags == 0 else None
+            outs.append((c.cpu().numpy(), fd.far_get(ctx), ctx.info["weight_bytes"], W))
+        finally:
+            fd.destroy(ctx)
+    nf = mask != 2
+    np.testing.assert_array_equal(outs[0][0][nf], outs[1][0][nf])
+    assert outs[0][1] == outs[1][1]
+    assert outs[0][2] < outs[1][2]  # identity and all-far chunks store nothing
+    W = outs[0][3]
+    solid = mask == 0
+    c = W.shape[-1] // 2
+    np.testing.assert_array_equal(W[solid][:, c], 1.0)  # slow sources: W_s = δ

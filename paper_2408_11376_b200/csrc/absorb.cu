@@ -28,8 +28,11 @@ __global__ void phase_pad_kernel(const uint8_t* __restrict__ mask, int nx, int n
                                  uint8_t* __restrict__ pp)
 {
     const long n = (long)nx * ny * nz;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+    // 32-bit index arithmetic (n < 2^31 for every grid the library accepts on one GPU): the
+    // 64-bit div/mod of the first version dominated these short kernels
+    const int nxy = nx * ny;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)n; i += gridDim.x * blockDim.x) {
+        const int z = i / nxy, r = i - z * nxy, y = r / nx, x = r - y * nx;
         pp[pidx(x, y, z, R, nxp, nyp)] = mask[i];
     }
 }
@@ -41,8 +44,11 @@ __global__ void solid_fd_kernel(const float* __restrict__ cin, float* __restrict
 {
     const long n = (long)nx * ny * nz;
     const long dxy[3] = {1, nxp, (long)nxp * nyp};
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+    // 32-bit index arithmetic (n < 2^31 for every grid the library accepts on one GPU): the
+    // 64-bit div/mod of the first version dominated these short kernels
+    const int nxy = nx * ny;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)n; i += gridDim.x * blockDim.x) {
+        const int z = i / nxy, r = i - z * nxy, y = r / nx, x = r - y * nx;
         const long p = pidx(x, y, z, R, nxp, nyp);
         const float c = cin[p];
         float acc = c;
@@ -67,8 +73,11 @@ __global__ void react_alpha_kernel(const float* __restrict__ c, const uint8_t* _
 {
     const long n = (long)nx * ny * nz;
     const long dxy[3] = {1, nxp, (long)nxp * nyp};
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+    // 32-bit index arithmetic (n < 2^31 for every grid the library accepts on one GPU): the
+    // 64-bit div/mod of the first version dominated these short kernels
+    const int nxy = nx * ny;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)n; i += gridDim.x * blockDim.x) {
+        const int z = i / nxy, r = i - z * nxy, y = r / nx, x = r - y * nx;
         const long p = pidx(x, y, z, R, nxp, nyp);
         float a = 1.f;
         if (pp[p] == 1) {
@@ -93,8 +102,11 @@ __global__ void react_apply_kernel(const float* __restrict__ c, const float* __r
 {
     const long n = (long)nx * ny * nz;
     const long dxy[3] = {1, nxp, (long)nxp * nyp};
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+    // 32-bit index arithmetic (n < 2^31 for every grid the library accepts on one GPU): the
+    // 64-bit div/mod of the first version dominated these short kernels
+    const int nxy = nx * ny;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)n; i += gridDim.x * blockDim.x) {
+        const int z = i / nxy, r = i - z * nxy, y = r / nx, x = r - y * nx;
         const long p = pidx(x, y, z, R, nxp, nyp);
         float v = c[p];
         const uint8_t ph = pp[p];
@@ -126,8 +138,11 @@ __global__ void kin_partial_kernel(const float* __restrict__ c, const uint8_t* _
     __shared__ double rs[8], rl[8];
     const long n = (long)nx * ny * nz;
     double s = 0.0, l = 0.0;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+    // 32-bit index arithmetic (n < 2^31 for every grid the library accepts on one GPU): the
+    // 64-bit div/mod of the first version dominated these short kernels
+    const int nxy = nx * ny;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)n; i += gridDim.x * blockDim.x) {
+        const int z = i / nxy, r = i - z * nxy, y = r / nx, x = r - y * nx;
         const long p = pidx(x, y, z, R, nxp, nyp);
         if (pp[p] == 0) s += (double)c[p];
         else if (pp[p] == 1) l += (double)c[p];
@@ -147,12 +162,27 @@ __global__ void kin_partial_kernel(const float* __restrict__ c, const uint8_t* _
     }
 }
 
-__global__ void kin_final_kernel(const double* __restrict__ part, int nblk, double* __restrict__ far_state,
-                                 double v_far, double n_solid, double cSeq, int far, double* __restrict__ rec)
+// one block of 256 threads: thread t sums the partials b ≡ t (mod 256) in ascending b, then a
+// fixed shuffle tree and the warps in order (deterministic; the single-thread serial sum of the
+// first version cost ~38 µs per macro step)
+__global__ void __launch_bounds__(256) kin_final_kernel(const double* __restrict__ part, int nblk,
+                                                        double* __restrict__ far_state, double v_far, double n_solid,
+                                                        double cSeq, int far, double* __restrict__ rec)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    __shared__ double rs[8], rl[8];
     double s = 0.0, l = 0.0;
-    for (int b = 0; b < nblk; ++b) { s += part[2 * b]; l += part[2 * b + 1]; }
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) { s += part[2 * b]; l += part[2 * b + 1]; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+    }
+    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = s; rl[threadIdx.x >> 5] = l; }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    s = 0.0;
+    l = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { s += rs[w]; l += rl[w]; }
     if (far) far_state[0] = (far_state[1] - s - l) / v_far;  // (4) Eq.7 after the whole step
     rec[0] = s;
     rec[1] = l;
@@ -194,7 +224,7 @@ cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uin
     // (4)+(5)
     const int nblk = 148 * 4;
     kin_partial_kernel<<<nblk, 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, part);
-    kin_final_kernel<<<1, 32, 0, s>>>(part, nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec);
+    kin_final_kernel<<<1, 256, 0, s>>>(part, nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec);
     *result = cur;
     return cudaGetLastError();
 }

@@ -724,24 +724,30 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
     // TMA-staged weight stream for launches of ≥ 2 CTAs per SM (the common case); the
     // register-prefetching body below for smaller launches (one wave: no CTA to overlap the
     // pipeline fill with) or FDIRW_F_NO_BULK_STREAM.  Identical bits either way.
-    if (!a.no_bulk && nblk >= 2 * 148 && a.tile % 32 == 0 && a.tile <= kBulkWarps * 32) {
-        const int b_w = fmt == 0 ? 4 : 2;
-        int cps = 0;
-        const int S1 = bulk_stages(R, b_w, a.tile, &cps);
-        if (S1 > 0) {
-            // Wave balance for short launches (e.g. the compacted tiles of an open domain, N2):
-            // split each tile into nsub ∈ {1, 2, 4} parts of a.tile/nsub chunks (≥ 64), at the
-            // same CTAs per SM, when the modelled time waves·(chunks per CTA) drops.  Not with
-            // in-kernel per-tile sums (N2 multi-rank Eq.7), which need the whole tile.
-            int nsub = 1;
-            if (!a.tile_sum && nblk < 4 * cps * 148) {
-                const long slots = (long)cps * 148;
-                long best = -1;
-                for (int d = 1; d <= 4 && a.tile / d >= 64 && (a.tile / d) % 32 == 0; d *= 2) {
-                    const long cost = (((long)nblk * d + slots - 1) / slots) * (a.tile / d);
-                    if (best < 0 || cost < best) { best = cost; nsub = d; }
-                }
-            }
+    const int b_w = fmt == 0 ? 4 : 2;
+    int cps = 0;
+    const int S1 = (a.tile % 32 == 0 && a.tile <= kBulkWarps * 32) ? bulk_stages(R, b_w, a.tile, &cps) : 0;
+    // Wave balance (e.g. the compacted tiles of an open domain, N2/N3): split each tile into
+    // nsub ∈ {1, 2, 4} parts of a.tile/nsub chunks (≥ 64), at the same CTAs per SM, when the
+    // modelled time waves·(chunks per CTA) drops; a split launch must still fill the GPU once
+    // (2 CTAs/SM × 148) so the stage pipelines' fill overlaps.  Not with in-kernel per-tile
+    // sums (N2 multi-rank Eq.7), which need the whole tile.
+    // Parts keep ≥ 128 chunks (measured: 64-chunk parts, 1 KB per slot copy, lose to the
+    // register-prefetch body at cfg2 and to whole tiles at cfg3), and only launches of < 4
+    // waves are split at all.
+    int nsub = 0;
+    if (!a.no_bulk && S1 > 0) {
+        const long slots = (long)cps * 148;
+        const int dmax = (a.tile_sum || nblk >= 4 * slots) ? 1 : 4;
+        long best = -1;
+        for (int d = 1; d <= dmax && a.tile / d >= 128 && (a.tile / d) % 32 == 0; d *= 2) {
+            if ((long)nblk * d < 2 * 148) continue;
+            const long cost = (((long)nblk * d + slots - 1) / slots) * (a.tile / d);
+            if (best < 0 || cost < best) { best = cost; nsub = d; }
+        }
+    }
+    if (nsub > 0) {
+        {
             const int sub = a.tile / nsub;
             int S = S1 * nsub;  // same shared memory per CTA: stages of a part are nsub× smaller
             if (S > 8) S = 8;

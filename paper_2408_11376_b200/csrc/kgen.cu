@@ -311,13 +311,18 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         // Windows touching the far-field reservoir (N2) keep the literal substeps: their kernel
         // keeps only the mass M_s that did not leak, and the recurrence's rounding is on the
         // scale of the source, not of M_s (measured: M_s relative error 7e-5 vs 5e-6).
+        // act: run the step on this thread.  For R ≥ 6 every thread runs it (threads without a
+        // column, t ≥ L², compute zeros: face numbers and neighbour offsets 0, own smem slot
+        // only), which removes the divergent branches; measured faster there (cfg5 R8 967 →
+        // 908 ms) and slower at R5 (140 → 155 ms), so R ≤ 5 keep the guard.
+        const bool act = R >= 6 || col;
         const bool cheb = a.cheb_m && !open;
         const int n_direct = cheb ? a.cheb_pre : a.n_fd;
         for (int k = 0; k < n_direct; ++k) {
             float* b = buf + (k & 1) * (NT * Lp);
-            if (col) store_col(b, c);
+            if (act) store_col(b, c);
             __syncthreads();
-            if (col) {
+            if (act) {
                 float nw[Lp];
 #pragma unroll
                 for (int z = 0; z < L; ++z) nw[z] = c[z];
@@ -345,10 +350,10 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
             // prv ← κ·Â·cur − prv, κ = 2 (κ = 1, prv = 0 on the first step: 2Âδ·½, exact)
             auto step = [&](float (&cur)[Lp], float (&prv)[Lp], const int k, const bool first) {
                 float* b = buf + ((k + n_direct) & 1) * (NT * Lp);
-                if (col) store_col(b, cur);
+                if (act) store_col(b, cur);
                 __syncthreads();
                 const float ck = cc[k + 1];
-                if (col) {
+                if (act) {
                     float nw[Lp];
 #pragma unroll
                     for (int h = 0; h < NPR; ++h) {

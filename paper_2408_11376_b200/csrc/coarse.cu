@@ -376,7 +376,7 @@ __device__ __forceinline__ float dot16(const uint4& u, const float (&cv)[16 / si
 constexpr int GEMV_RW = 4;
 
 template <typename WT>
-__global__ void __launch_bounds__(256) k_gemv(const WT* __restrict__ P, const float* __restrict__ Pdiag,
+__global__ void __launch_bounds__(512) k_gemv(const WT* __restrict__ P, const float* __restrict__ Pdiag,
                                               const float* __restrict__ C, long N, long ldp,
                                               float* __restrict__ Cout, const float* __restrict__ Pbc,
                                               const double* __restrict__ far_state)
@@ -388,7 +388,10 @@ __global__ void __launch_bounds__(256) k_gemv(const WT* __restrict__ P, const fl
     const int nv = (int)(ldp / V);
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    for (long I0 = (blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * GEMV_RW; I0 < N;
+    // row group j = (warp w of block b) = w·gridDim + b: consecutive groups go to different
+    // blocks (one block per SM), so every SM gets ⌈groups/SMs⌉ or one less (the first form,
+    // 186 blocks of 8 warps on 148 SMs, left 38 SMs with twice the rows: 16.7 µs → see §11)
+    for (long I0 = ((threadIdx.x >> 5) * (long)gridDim.x + blockIdx.x) * GEMV_RW; I0 < N;
          I0 += warps * GEMV_RW) {
         const int nrow = (int)min((long)GEMV_RW, N - I0);
         float acc[GEMV_RW];
@@ -827,6 +830,17 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
     return FDIRW_OK;
 }
 
+// GEMV launch: one block per SM, ⌈row groups / SMs⌉ warps each (≤ 16; more groups loop)
+static unsigned gemv_grid(const fdirw_coarse* c) { return (unsigned)c->n_sm; }
+static unsigned gemv_block(const fdirw_coarse* c)
+{
+    const long groups = (c->N + GEMV_RW - 1) / GEMV_RW;
+    long w = (groups + c->n_sm - 1) / c->n_sm;
+    if (w < 1) w = 1;
+    if (w > 16) w = 16;
+    return (unsigned)(32 * w);
+}
+
 static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
 {
     const long N = c->N;
@@ -843,12 +857,12 @@ static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
             k_gemv_bulk<__nv_bfloat16><<<g, bl, c->bulk_smem, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N,
                                                                   c->ldp, c->C2, c->Pbc, c->far_state, c->bulk_m);
     } else if (c->fmt == 0)
-        k_gemv<float><<<gridn((N + GEMV_RW - 1) / GEMV_RW * 32), 256, 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc, c->far_state);
+        k_gemv<float><<<gemv_grid(c), gemv_block(c), 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc, c->far_state);
     else if (c->fmt == 1)
-        k_gemv<__half><<<gridn((N + GEMV_RW - 1) / GEMV_RW * 32), 256, 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
+        k_gemv<__half><<<gemv_grid(c), gemv_block(c), 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
                                                      c->Pbc, c->far_state);
     else
-        k_gemv<__nv_bfloat16><<<gridn((N + GEMV_RW - 1) / GEMV_RW * 32), 256, 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->ldp,
+        k_gemv<__nv_bfloat16><<<gemv_grid(c), gemv_block(c), 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->ldp,
                                                              c->C2, c->Pbc, c->far_state);
     k_remap<<<gridn(c->NL) + (c->far ? 1 : 0), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf, c->sizes, N,
                                                            c->far ? c->far_state : nullptr, c->v_far);

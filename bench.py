@@ -258,18 +258,17 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
     (device time from CUDA events around its launch, fdirw_info.kgen_kernel_ms) runs the distinct
     windows only, kgen_steps stencil passes each (the Chebyshev degree m, reading A30, or n_fd):
     its rooflines count those passes — shared memory (4 lateral neighbour reads + 1 write of 4 B
-    per cell-pass, z columns padded from L to Lp; 128 B/clk/SM) binds, the FP32 lanes (11
+    per cell-pass, no padding cell since the quad-major layout; 128 B/clk/SM) binds, the FP32 lanes (11
     lane-ops per substep cell, 13 per Chebyshev cell-pass) do not."""
     p = _peaks() or {}
     mhz = float(p.get("sm_max_mhz", 1965.0))
     L = 2 * cfg.R + 1
-    lp = (L + 3) // 4 * 4
     steps = info["kgen_steps"]
     cheb = steps != info["n_fd"]
     kms = info["kgen_kernel_ms"]
     passes = info["kgen_windows"] * world * cfg.K * steps  # computed cell-passes
     rate = passes / (kms * 1e-3) if kms > 0 else 0.0
-    smem_b = 20.0 * lp / L
+    smem_b = 20.0
     smem_peak = 148 * 128 * mhz * 1e6
     ops = 13 if cheb else 11
     alu_peak = 148 * 128 * mhz * 1e6 / ops

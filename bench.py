@@ -262,7 +262,6 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
     lane-ops per substep cell, 13 per Chebyshev cell-pass) do not."""
     p = _peaks() or {}
     mhz = float(p.get("sm_max_mhz", 1965.0))
-    L = 2 * cfg.R + 1
     steps = info["kgen_steps"]
     cheb = steps != info["n_fd"]
     kms = info["kgen_kernel_ms"]
@@ -434,6 +433,8 @@ def main():
     ap.add_argument("--impl", default="fdirw", choices=["fdirw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the N4 variant measurement")
+    ap.add_argument("--no-bulk-stream", action="store_true",
+                    help="A/B: per-thread weight loads instead of the TMA-staged stream (same bits)")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--mode", default="fine", choices=["fine", "coarse", "absorb"],
                     help="fine: the north_star windowed step (default); coarse: NEXT row N1")
@@ -486,7 +487,8 @@ def main():
         nccl_id = obj[0]
     params = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt,
                        radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights, v_far=cfg.v_far,
-                       flags=fd.F_DEDUP_STORAGE if args.storage == "dedup" else 0)
+                       flags=(fd.F_DEDUP_STORAGE if args.storage == "dedup" else 0) |
+                             (fd.F_NO_BULK_STREAM if args.no_bulk_stream else 0))
     stream = torch.cuda.current_stream()
 
     def barrier():

@@ -275,6 +275,7 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
             "cell_updates_per_s": cells_algo / t_kgen,
             "kernel_cell_updates_per_s": cells_algo / (kms * 1e-3) if kms > 0 else None,
             "n_fd": info["n_fd"], "method": "chebyshev" if cheb else "substeps", "passes_per_window": steps,
+            "builds_timed": 3 if info.get("_median3") else 1,
             "windows_computed": info["kgen_windows"] * world, "sources": info["kgen_sources"] * world,
             "roofline": {"bound": "smem", "achieved": rate * smem_b / 1e12, "peak": smem_peak / 1e12,
                          "unit": "TB/s", "frac": rate * smem_b / smem_peak,
@@ -433,6 +434,7 @@ def main():
     ap.add_argument("--impl", default="fdirw", choices=["fdirw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the N4 variant measurement")
+    ap.add_argument("--no-kgen-median", action="store_true", help="time one build instead of the median of 3")
     ap.add_argument("--no-bulk-stream", action="store_true",
                     help="A/B: per-thread weight loads instead of the TMA-staged stream (same bits)")
     ap.add_argument("--e2e-steps", type=int, default=50)
@@ -539,6 +541,16 @@ def main():
     warm = fd.Params(nx=16, ny=16, nz=16, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=cfg.D_slow, dt=cfg.dt,
                      radius=cfg.R, n_fd=cfg.n_fd, weights=cfg.weights, v_far=0.0)
     fd.destroy(fd.build_kernels(warm, fi.config("cfg1").mask(), device=local, stream=stream))
+    # kgen is reported as the median of 3 builds: two extra full builds on one GPU
+    # (each destroyed before the next), then the measured build that the steps use
+    extra_builds = []
+    if world == 1 and not args.no_kgen_median:
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            cx = fd.build_kernels(params, mask, device=local, stream=stream)
+            extra_builds.append((time.perf_counter() - t, cx.info["kgen_kernel_ms"]))
+            fd.destroy(cx)
     torch.cuda.synchronize()
     t = time.perf_counter()
     ctx = build(transport)
@@ -548,6 +560,11 @@ def main():
         ctx = build(transport)
     t_kgen = time.perf_counter() - t
     info = ctx.info
+    if extra_builds:
+        walls = sorted([w for w, _ in extra_builds] + [t_kgen])
+        kms = sorted([k for _, k in extra_builds] + [info["kgen_kernel_ms"]])
+        t_kgen = walls[1]
+        info = dict(info, kgen_kernel_ms=kms[1], _median3=True)
 
     def gmass(cc):  # with P2P fdirw_mass is slab-local
         m = fd.mass(ctx, cc)

@@ -668,6 +668,8 @@ def main():
     # N=1: one superpose launch; N>1 P2P: wait + one superpose launch + signal; NCCL: interior
     # + boundary-bands superpose launches (NCCL's own kernels are not counted)
     launches_per_step = 1 if world == 1 else (3 if transport == "p2p" else 2)
+    if far:  # N2: + per-tile sums (tile_mass, when compacted) + the Eq.7 reduction
+        launches_per_step += 2 if world == 1 else 1
     # one superpose launch per step at N=1 (+1 pack, +1 unpack per fdirw_run); the launch
     # duration is the timed region / K to within the two ~10 µs state kernels.
     achieved = per_launch_bytes / (ms_step * 1e-3) / 1e9

@@ -632,3 +632,26 @@ def test_dedup_storage_bitwise(fd, cfgname, steps):
     assert infos[0]["uniform_chunks"] == 0
     assert infos[1]["uniform_chunks"] > (0.2 * infos[1]["chunks"] if cfgname == "cfg3" else 0)
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_build_deterministic(fd):
+    """Two builds of the same problem give the same bits (kernels and stepped field): resume =
+    rebuild + saved C continues a run exactly."""
+    import torch
+
+    shape = (48, 40, 44)
+    mask = fi.porous_particle(shape, 14, pore_r=(1.0, 2.5), porosity=0.3, seed=21)
+    cfg = small_cfg(shape, 4, 1000, D_slow=1e-4, weights="fp16")
+    c0 = fi.initial_c(mask, "random", seed=21)
+    outs = []
+    for _ in range(2):
+        ctx = fd.build_kernels(lib_params(cfg), mask)
+        try:
+            W = fd.export_kernels(ctx, (10, 30, 8, 28, 12, 20))
+            c = torch.from_numpy(c0).cuda()
+            fd.run(ctx, c, 3)
+            outs.append((W, c.cpu().numpy()))
+        finally:
+            fd.destroy(ctx)
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])

@@ -274,6 +274,23 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
             load_col(b, t + oxp, xp);
             load_col(b, t + oym, ym);
             load_col(b, t + oyp, yp);
+            // z faces from registers: for R ≤ 5 before the lateral faces, so they run while the
+            // neighbours' shared-memory loads are in flight (cfg3 kgen 140 → 135 ms); for larger
+            // R after them (the other order measured 4 % slower at R8).  Either order is fixed
+            // per R, so every path (dedup or not, any decomposition) gives the same bits.
+            auto zfaces = [&]() {
+                float dz[L > 1 ? L - 1 : 1];
+#pragma unroll
+                for (int z = 0; z + 1 < L; ++z) dz[z] = cur[z + 1] - cur[z];
+#pragma unroll
+                for (int z = 0; z < L; ++z) {
+                    float v = nw[z];
+                    if (z > 0) v = fmaf(lzm[z], -dz[z - 1], v);
+                    if (z < L - 1) v = fmaf(lzp[z], dz[z], v);
+                    nw[z] = v;
+                }
+            };
+            if constexpr (R <= 5) zfaces();
 #pragma unroll
             for (int h = 0; h < NPR; ++h) {
                 const unsigned long long c2 = pk2(cur[2 * h], cur[2 * h + 1]);
@@ -293,19 +310,11 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
                 s1 = fmaf(lyp1, yp[L - 1] - c1, s1);
                 nw[L - 1] = s1;
             }
-            float dz[L > 1 ? L - 1 : 1];
-#pragma unroll
-            for (int z = 0; z + 1 < L; ++z) dz[z] = cur[z + 1] - cur[z];
-#pragma unroll
-            for (int z = 0; z < L; ++z) {
-                float v = nw[z];
-                if (z > 0) v = fmaf(lzm[z], -dz[z - 1], v);
-                if (z < L - 1) v = fmaf(lzp[z], dz[z], v);
-                nw[z] = v;
-            }
+            if constexpr (R > 5) zfaces();
         };
 
-        // n_fd Jacobi substeps; faces summed −x,+x,−y,+y,−z,+z.
+        // n_fd Jacobi substeps; lateral faces summed −x,+x,−y,+y, the z faces before (R ≤ 5) or
+        // after them (see flux).
         // Direct: all n_fd substeps.  Chebyshev: the first cheb_pre substeps (the peaked start,
         // whose large entries would otherwise feed the recurrence's rounding), then the recurrence.
         // Windows touching the far-field reservoir (N2) keep the literal substeps: their kernel

@@ -1,11 +1,12 @@
 """Diagnostic: per-weight error of the stored fp32 kernels vs the oracle's fp64 kernels
 (cfg1 at n_fd = 1000), for the Chebyshev default and the direct substeps."""
+import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, ".")
-sys.path.insert(0, "tests")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import fdirw_inputs as fi  # noqa: E402
 import oracle  # noqa: E402
 import paper_2408_11376_b200 as fd  # noqa: E402

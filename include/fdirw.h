@@ -62,7 +62,15 @@ typedef enum {
     FDIRW_E_STATE = 7     /* call not valid in this context state (e.g. debug upload on world>1) */
 } fdirw_status;
 
-typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2 } fdirw_weight_t;
+/* Weight storage formats.  FDIRW_W_MX8 (beyond the paper's §3.3 formats): each
+ * gather block (the 8 weights of 8 consecutive targets for one window offset) is 8 unsigned
+ * 8-bit mantissas m plus one power-of-two scale s (8-bit exponent): w = m·s, s the smallest
+ * power of two with max(block)/s <= 255, m = RNE(w/s); 1.125 bytes per weight.  The fp32
+ * diagonal fix-up restores each source's mass from the decoded weights.  Accuracy is within
+ * north_star's reduced-precision bar (relL2 <= 5e-3).  Supported on one rank (world == 1), closed
+ * domain (v_far == 0), without FDIRW_F_DEDUP_STORAGE / _NO_MASS_FIX / _NO_DEDUP / _SYMMETRIC_RULE /
+ * _KGEN_FP64; other combinations return FDIRW_E_INVALID.                                       */
+typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2, FDIRW_W_MX8 = 3 } fdirw_weight_t;
 
 /* fdirw_params.flags */
 #define FDIRW_F_NO_MASS_FIX 1u /* diagonal = RNE_fmt(W_s(0)) instead of the fp32 mass fix-up (A10) */

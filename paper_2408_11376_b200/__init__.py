@@ -28,7 +28,7 @@ _lib = ctypes.CDLL(_LIB_PATH)
 
 FDIRW_OK, E_INVALID, E_UNSTABLE, E_OOM, E_CUDA, E_NCCL, E_ALIAS, E_STATE = range(8)
 STATUS_NAMES = ["OK", "E_INVALID", "E_UNSTABLE", "E_OOM", "E_CUDA", "E_NCCL", "E_ALIAS", "E_STATE"]
-WEIGHTS = {"fp32": 0, "fp16": 1, "bf16": 2}
+WEIGHTS = {"fp32": 0, "fp16": 1, "bf16": 2, "mx8": 3}
 F_NO_MASS_FIX = 1
 F_NO_DEDUP = 2
 F_DEDUP_STORAGE = 4  # NEXT row N4: uniform chunks read shared class kernels (fewer HBM bytes)

@@ -29,6 +29,7 @@
 
 #include "fdirw_internal.h"
 #include "layout.cuh"
+#include "mx8.cuh"
 
 namespace fdirw {
 
@@ -441,10 +442,106 @@ cudaError_t dedup_classify(const DedupArgs& a, DedupResult* res, cudaStream_t s)
 #undef TRY
 }
 
+// FDIRW_W_MX8 (mx8.cuh): expand_kernel's gather walk over fp32 class kernels, each
+// block of 8 targets × 1 slot quantised to 8 mantissas + one scale.  Thread e writes its 8 B of
+// mantissas and its scale byte per slot (consecutive e: consecutive bytes).  The diagonal comes
+// after, from the decoded weights (mx8_diag_kernel).
+template <int R>
+__global__ void __launch_bounds__(256) expand_mx8_kernel(const ExpandArgs a)
+{
+    constexpr int L = 2 * R + 1, LL = L * L, K = L * L * L;
+    const int tile = blockIdx.x;
+    const int e = threadIdx.x;
+    const int zl = tile / a.tpp, q = (tile % a.tpp) * a.tile + e;
+    const bool real = q < a.ny * a.nxq;
+    unsigned char* wq = reinterpret_cast<unsigned char*>(a.Wt);
+    const float* cw = reinterpret_cast<const float*>(a.class_w);
+    const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;
+    const long nxp = a.nxp, plane = (long)a.nyp * nxp;
+    const int* c0 = a.class_pad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
+    for (int r = -1; r < LL; ++r) {  // r = −1: the centre row first (slot order of layout.cuh)
+        if (r == R * L + R) continue;
+        const int oz = r < 0 ? 0 : r / L - R, oy = r < 0 ? 0 : r % L - R;
+        int seg[24];
+        const int* srow = c0 - (long)oz * plane - (long)oy * nxp - 8;
+#pragma unroll
+        for (int i = 0; i < 24; ++i) seg[i] = real ? srow[i] : -1;
+#pragma unroll
+        for (int ox = -R; ox <= R; ++ox) {
+            if (r < 0 && ox == 0) continue;
+            const int o = (oz + R) * LL + (oy + R) * L + (ox + R);
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = seg[j - ox + 8];
+                v[j] = c >= 0 ? cw[(size_t)c * K + o] : 0.f;
+            }
+            uint2 m;
+            uint32_t E;
+            mx8_quant(v, &m, &E);
+            size_t mo, so;
+            mx8_addr(tile, slot_of(ox, oy, oz, R), e, 0, L, K, a.tile, &mo, &so);
+            *reinterpret_cast<uint2*>(wq + mo) = m;
+            wq[so] = (unsigned char)E;
+        }
+    }
+}
+
+// diag[target s] = fp32(1 − Σ_{o≠0} decoded W_s(o)) in fp64 (kgen's mass fix, reading A10), the
+// source's weights read back from the gather blocks at targets s + o (one thread per source,
+// x fastest: neighbouring threads read neighbouring bytes).  Sources outside the domain
+// (class −1) and dummy targets keep 0.  One rank (the whole grid is the slab).
+template <int R>
+__global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int nzl)
+{
+    constexpr int L = 2 * R + 1, K = L * L * L;
+    const long n = (long)a.nx * a.ny * nzl;
+    const unsigned char* wq = reinterpret_cast<const unsigned char*>(a.Wt);
+    const long nxp = a.nxp, plane = (long)a.nyp * nxp;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int sx = (int)(i % a.nx), sy = (int)((i / a.nx) % a.ny), sz = (int)(i / ((long)a.nx * a.ny));
+        const int cls = a.class_pad[(sz + R) * plane + (long)(sy + R) * nxp + kPadX + sx];
+        const int q0 = sy * a.nxq + (sx >> 3);
+        float* dp = a.diag + (((size_t)sz * a.tpp + q0 / a.tile) * a.tile + q0 % a.tile) * 8 + (sx & 7);
+        if (cls < 0) {
+            *dp = 0.f;
+            continue;
+        }
+        double off = 0.0;
+        for (int oz = -R; oz <= R; ++oz) {
+            const int z = sz + oz;
+            if (z < 0 || z >= nzl) continue;
+            for (int oy = -R; oy <= R; ++oy) {
+                const int y = sy + oy;
+                if (y < 0 || y >= a.ny) continue;
+#pragma unroll
+                for (int ox = -R; ox <= R; ++ox) {
+                    const int x = sx + ox;
+                    if ((ox == 0 && oy == 0 && oz == 0) || x < 0 || x >= a.nx) continue;
+                    const int q = y * a.nxq + (x >> 3);
+                    size_t mo, so;
+                    mx8_addr((size_t)z * a.tpp + q / a.tile, slot_of(ox, oy, oz, R), q % a.tile, x & 7, L, K, a.tile,
+                             &mo, &so);
+                    off += (double)mx8_decode(__ldg(wq + mo), __ldg(wq + so));
+                }
+            }
+        }
+        *dp = (float)(1.0 - off);
+    }
+}
+
 template <int R>
 static cudaError_t launch_expand_r(const ExpandArgs& a, int fmt, cudaStream_t s)
 {
     if (a.n_tiles <= 0) return cudaSuccess;
+    if (fmt == FDIRW_W_MX8) {
+        if (a.list) return cudaErrorInvalidValue;  // dense tiles of one rank only
+        expand_mx8_kernel<R><<<a.n_tiles, a.tile, 0, s>>>(a);
+        cudaError_t e = cudaMemsetAsync(a.diag, 0, (size_t)a.n_tiles * a.tile * 8 * 4, s);
+        if (e != cudaSuccess) return e;
+        mx8_diag_kernel<R><<<148 * 8, 256, 0, s>>>(a, a.n_tiles / a.tpp);
+        return cudaGetLastError();
+    }
     if (fmt == 0) expand_kernel<R, float><<<a.n_tiles, a.tile, 0, s>>>(a);
     else if (fmt == 1) expand_kernel<R, __half><<<a.n_tiles, a.tile, 0, s>>>(a);
     else expand_kernel<R, __nv_bfloat16><<<a.n_tiles, a.tile, 0, s>>>(a);

@@ -17,6 +17,12 @@
 
 using namespace fdirw;
 
+// device bytes of `elems` stored weights (elems is a multiple of 8: whole gather blocks)
+static size_t wbytes(int fmt, size_t elems)
+{
+    return fmt == FDIRW_W_FP32 ? elems * 4 : fmt == FDIRW_W_MX8 ? elems / 8 * 9 : elems * 2;
+}
+
 struct fdirw_ctx {
     fdirw_params p;
     Derived d;
@@ -275,7 +281,15 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (!(p->dh > 0) || !(p->dt > 0)) return fail(FDIRW_E_INVALID, "dh and dt must be > 0");
     if (!(p->D_fast > 0) || !(p->D_slow >= 0)) return fail(FDIRW_E_INVALID, "need D_fast > 0, D_slow >= 0");
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
-    if (p->weights < 0 || p->weights > 2) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16 or BF16");
+    if (p->weights < 0 || p->weights > 3) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16, BF16 or MX8");
+    if (p->weights == FDIRW_W_MX8) {
+        if (dist && dist->world > 1) return fail(FDIRW_E_INVALID, "MX8 weights need world == 1");
+        if (p->v_far > 0) return fail(FDIRW_E_INVALID, "MX8 weights need a closed domain (v_far == 0)");
+        if (p->flags & (FDIRW_F_DEDUP_STORAGE | FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_SYMMETRIC_RULE |
+                        FDIRW_F_KGEN_FP64))
+            return fail(FDIRW_E_INVALID, "MX8 weights are not combined with DEDUP_STORAGE, NO_MASS_FIX, NO_DEDUP, "
+                                         "SYMMETRIC_RULE or KGEN_FP64");
+    }
     if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE | FDIRW_F_KGEN_FP64 |
                      FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT | FDIRW_F_NO_BULK_STREAM))
         return fail(FDIRW_E_INVALID, "unknown flags");
@@ -450,7 +464,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     c->p = *params;
     c->d = d;
     c->fmt = params->weights;
-    c->b_w = c->fmt == FDIRW_W_FP32 ? 4 : 2;
+    c->b_w = c->fmt == FDIRW_W_FP32 ? 4 : 2;  // MX8: the fp32 class kernels it quantises
+    if (c->fmt == FDIRW_W_MX8) c->b_w = 4;
     int z0 = 0, z1 = params->nz;
     if (dist) {
         c->rank = dist->rank;
@@ -542,7 +557,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             c->kgen_steps = kCheb_pre + m;
         }
     }
-    ka.fmt = c->fmt;
+    ka.fmt = c->fmt == FDIRW_W_MX8 ? FDIRW_W_FP32 : c->fmt;  // MX8: quantised by the expand pass
     ka.mass_fix = (params->flags & FDIRW_F_NO_MASS_FIX) ? 0 : 1;
     ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;
     c->kgen_sources = (uint64_t)g.nx * g.ny * (ka.sz1 - ka.sz0);
@@ -600,7 +615,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                 d_elems = (size_t)c->ut.nd_tiles * g.tile * kChunk;
             }
             if (e == cudaSuccess) {
-                if ((st = alloc(&c->Wt, (w_elems ? w_elems : 1) * c->b_w, "weights")) != FDIRW_OK ||
+                if ((st = alloc(&c->Wt, wbytes(c->fmt, w_elems ? w_elems : 8), "weights")) != FDIRW_OK ||
                     (st = alloc((void**)&c->diag, (d_elems ? d_elems : 1) * 4, "diagonal")) != FDIRW_OK) {
                     dfree(); cudaFree(mask_d); return bail(st);
                 }
@@ -615,6 +630,11 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             c->kgen_windows = (uint64_t)dr.n_class;
         }
         dfree();
+    }
+    if (!dedup && c->fmt == FDIRW_W_MX8) {
+        cudaFree(mask_d);
+        g_err = "MX8 weights need the window de-duplication (hash collision fallback not supported)";
+        return bail(FDIRW_E_STATE);
     }
     if (!dedup) {
         ka.src_list = nullptr; ka.n_list = 0; ka.class_w = nullptr; ka.class_diag = nullptr;
@@ -1038,7 +1058,7 @@ extern "C" fdirw_status fdirw_read_ceiling(const fdirw_ctx* c, int32_t reps, voi
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const Geometry& g = c->g;
     const uint64_t wt_tiles = (c->ut.chunk_u || c->compact) ? (uint64_t)c->ut.nd_tiles : (uint64_t)g.n_tiles;
-    const size_t bytes = ((size_t)wt_tiles * (g.K - 1) * g.tile * kChunk * c->b_w) / 16 * 16;
+    const size_t bytes = wbytes(c->fmt, (size_t)wt_tiles * (g.K - 1) * g.tile * kChunk) / 16 * 16;
     if (bytes == 0) return fail(FDIRW_E_STATE, "no weights to stream");
     int sms = 148;
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
@@ -1079,9 +1099,10 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->lambda_fs = c->d.lam_fs;
     info->lambda_slow = c->d.lam_ss;
     const uint64_t wt_tiles = (c->ut.chunk_u || c->compact) ? (uint64_t)c->ut.nd_tiles : (uint64_t)g.n_tiles;  // N4 / N2 compact
-    info->weight_bytes = wt_tiles * (g.K - 1) * g.tile * kChunk * c->b_w + wt_tiles * g.tile * kChunk * 4;
+    info->weight_bytes = wbytes(c->fmt, wt_tiles * (g.K - 1) * g.tile * kChunk) + wt_tiles * g.tile * kChunk * 4;
     info->state_bytes = (uint64_t)g.state_elems * 4 * 2;
-    info->bytes_per_voxel_update = (uint64_t)(g.K - 1) * c->b_w + 12;
+    info->bytes_per_voxel_update = c->fmt == FDIRW_W_MX8 ? (uint64_t)((g.K - 1) * 9 + 4) / 8 + 12  // rounded
+                                                         : (uint64_t)(g.K - 1) * c->b_w + 12;
     info->voxels = (uint64_t)g.nx * g.ny * g.nzl;
     info->tile_chunks = g.tile;
     info->n_tiles = g.n_tiles;
@@ -1112,7 +1133,6 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
     const HaloPlan h = make_halo_plan(g, rank, world);
     int i0, i1;
     split_tiles(g, &i0, &i1);
-    const int b_w = p->weights == FDIRW_W_FP32 ? 4 : 2;
     pl->z_begin = g.z0; pl->z_end = g.z1;
     pl->src_z_begin = g.sz0; pl->src_z_end = g.sz1;
     pl->mask_z_begin = g.mz0; pl->mask_z_end = g.mz1;
@@ -1124,7 +1144,7 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
     pl->pad_x0 = kPadX;
     pl->halo_elems = h.count;
     pl->send_lo = h.send_lo; pl->recv_lo = h.recv_lo; pl->send_hi = h.send_hi; pl->recv_hi = h.recv_hi;
-    pl->weight_bytes = (uint64_t)g.w_elems * b_w + (uint64_t)g.diag_elems * 4;
+    pl->weight_bytes = (uint64_t)wbytes(p->weights, g.w_elems) + (uint64_t)g.diag_elems * 4;
     pl->state_bytes = (uint64_t)g.state_elems * 8;
     pl->n_fd = d.n_fd;
     std::vector<float> cheb;
@@ -1140,6 +1160,7 @@ extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k
     if (!c || !k) return fail(FDIRW_E_INVALID, "NULL argument");
     if (c->world != 1) return fail(FDIRW_E_STATE, "debug upload needs world == 1");
     if (c->ut.chunk_u || c->compact) return fail(FDIRW_E_STATE, "debug upload needs the dense layout");
+    if (c->fmt == FDIRW_W_MX8) return fail(FDIRW_E_STATE, "debug upload does not write MX8 weights");
     CUDA_TRY(cudaSetDevice(c->device));
     const Geometry& g = c->g;
     const int R = g.R, L = g.L, K = g.K;

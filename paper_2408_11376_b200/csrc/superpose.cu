@@ -29,6 +29,8 @@
 #include "bulk.cuh"
 #include "fdirw_internal.h"
 #include "layout.cuh"
+#include "mx8.cuh"
+#include <cstdlib>
 
 namespace fdirw {
 
@@ -661,6 +663,163 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32) superpose_bulk_kernel(c
     bulk_body<R, WT>(a, blockIdx.x, S, sub, smem_b);
 }
 
+// FDIRW_W_MX8 (mx8.cuh): one stored row of the tile = n slots × (T·8 mantissa bytes)
+// then n × T scale bytes, staged like bulk_body's rows (whole tiles only).  Per slot thread e
+// reads its 8 mantissas (LDS.64) and its block's exponent byte; weight j is decoded exactly as
+// fma(2^23 + m_j, s, −2^23·s) = m_j·s, with 2^23 + m_j built by one byte permute
+// (0x4B0000·m_j as fp32 bits), then the FMA chain and TwoSum of do_row_s.  The kernel is
+// issue-bound (ncu: ~74 % issue slots at the first version), so everything per row that is not
+// decode + FMA is kept out of the loop: TT = the tile width as a compile-time constant (256, the
+// closed-domain default; 0 = runtime), stage/phase counters instead of divisions, row pointers
+// stepped instead of recomputed.
+__device__ __forceinline__ unsigned long long pk2f(float a, float b)
+{
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2f(unsigned long long v, float& a, float& b)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long fma2f(unsigned long long a, unsigned long long b, unsigned long long c)
+{
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// One stored row's slots into the partial sums p (FMA chain in slot order).  The decode runs
+// two weights per FFMA2 (each lane an ordinary fp32 fma: exact here).
+template <int R, bool CENTRE_ROW, int TT>
+__device__ __forceinline__ void row_mx8(const float seg[24], const unsigned char* mb, const unsigned char* sb, int T_,
+                                        float p[8])
+{
+    const int T = TT ? TT : T_;
+#pragma unroll
+    for (int ox = -R; ox <= R; ++ox) {
+        if (CENTRE_ROW && ox == 0) continue;
+        const int k = CENTRE_ROW ? (ox < 0 ? ox + R : ox + R - 1) : ox + R;
+        const uint2 m = *reinterpret_cast<const uint2*>(mb + k * 8 * T);
+        const uint32_t E = sb[k * T];
+        const float sc = __uint_as_float(E << 23), bias = __uint_as_float(((E + 23u) << 23) | 0x80000000u);
+        const unsigned long long sc2 = pk2f(sc, sc), b2 = pk2f(bias, bias);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const unsigned wd = h < 2 ? m.x : m.y;
+            const float f0 = __uint_as_float(__byte_perm(wd, 0x4B000000u, 0x7440u | (unsigned)((2 * h) & 3)));
+            const float f1 = __uint_as_float(__byte_perm(wd, 0x4B000000u, 0x7440u | (unsigned)((2 * h + 1) & 3)));
+            float w0, w1;
+            upk2f(fma2f(pk2f(f0, f1), sc2, b2), w0, w1);
+            p[2 * h] = fmaf(w0, seg[2 * h - ox + 8], p[2 * h]);
+            p[2 * h + 1] = fmaf(w1, seg[2 * h + 1 - ox + 8], p[2 * h + 1]);
+        }
+    }
+}
+
+// (hi, lo) += p error-free (Knuth TwoSum), p = 0
+__device__ __forceinline__ void flush_mx8(float p[8], float hi[8], float lo[8])
+{
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float s, e2;
+        two_sum(hi[j], p[j], s, e2);
+        hi[j] = s;
+        lo[j] = __fadd_rn(lo[j], e2);
+        p[j] = 0.f;
+    }
+}
+
+template <int R, int TT>
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel(const SuperArgs a, int S)
+{
+    extern __shared__ __align__(128) unsigned char smem_b[];
+    constexpr int L = 2 * R + 1, K = L * L * L, NROW = L * L;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_b);
+    uint64_t* empty = full + S;
+    unsigned char* stg = smem_b + 128;
+    const int T = TT ? TT : a.tile;
+    const uint32_t slotB = (uint32_t)T * 9, stageB = (uint32_t)L * slotB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = T >> 5;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(smem_u32(full + i), 1);
+            mbar_init(smem_u32(empty + i), nw);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+    const bool producer = warp == nw;
+    const int e = producer ? 0 : (int)threadIdx.x;
+    TileCtx t = tile_ctx<R>(a, blockIdx.x, e);
+    float hi[8], lo[8];
+    if (producer) {
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.Wt) + (size_t)t.tile * (K - 1) * slotB;
+            int st = 0;
+            uint32_t ph = 0;  // parity of the empty barrier to wait for (from the second lap)
+            for (int i = 0; i < NROW; ++i) {
+                const int n = i == 0 ? L - 1 : L;
+                if (i >= S) mbar_wait(smem_u32(empty + st), ph);
+                mbar_expect_tx(smem_u32(full + st), (uint32_t)n * slotB);
+                bulk_g2s(smem_u32(stg + (size_t)st * stageB), src, (uint32_t)n * slotB, smem_u32(full + st), pol);
+                src += (size_t)n * slotB;
+                if (++st == S) {
+                    st = 0;
+                    if (i >= S) ph ^= 1u;
+                }
+            }
+        }
+        t.real = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.f;
+    } else {
+        diag_init(a, t, e, hi, lo);
+        float seg[24], p[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) p[j] = 0.f;
+        const unsigned char* m0 = stg + (size_t)e * 8;     // this thread's mantissas in stage 0
+        const unsigned char* s0 = stg + (size_t)8 * T + e;  // its scales (after n·8T bytes; n folded below)
+        int st = 0;
+        uint32_t ph = 0;
+        // row i = 0: the centre row; then (oz, oy) ascending without the centre (row_src order)
+        const float* srow = t.c0 - 8;
+        for (int i = 0; i < NROW; ++i) {
+            if (i == 1) srow = t.c0 + (long)R * t.plane + (long)R * t.nxp - 8;  // (oz, oy) = (−R, −R)
+            if (t.real) load_seg(srow, seg);
+            mbar_wait(smem_u32(full + st), ph);
+            if (t.real) {
+                // partial sums over the centre row, then over pairs of rows (L² − 1 is even),
+                // each added to (hi, lo) error-free: 1/L² .. 2/L² of the total per partial
+                const unsigned char* mb = m0 + st * stageB;
+                if (i == 0) {
+                    row_mx8<R, true, TT>(seg, mb, s0 + st * stageB + (L - 2) * 8 * T, T, p);
+                    flush_mx8(p, hi, lo);
+                } else {
+                    row_mx8<R, false, TT>(seg, mb, s0 + st * stageB + (L - 1) * 8 * T, T, p);
+                    if ((i & 1) == 0) flush_mx8(p, hi, lo);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(empty + st));
+            if (++st == S) {
+                st = 0;
+                ph ^= 1u;
+            }
+            if (i >= 1) {  // next (oz, oy): oy + 1 (row pointer − nxp), wrapping to oz + 1
+                const int r = i - 1 < R * L + R ? i - 1 : i;  // this row's (oz, oy) index
+                const int rn = r + 1 == R * L + R ? r + 2 : r + 1;
+                if (rn % L == 0) srow += (long)(L - 1) * t.nxp - t.plane;
+                else srow -= t.nxp;
+                if (rn - r == 2) srow -= t.nxp;  // skipped the centre row (same oz)
+            }
+        }
+    }
+    tile_epilogue(a, t, e, hi, lo);
+}
+
 // N4 with the staged stream: the mixed launch's dense tiles run bulk_body, its uniform blocks
 // uniform_body with the class kernel in the (otherwise unused) stage memory.
 template <int R, typename WT>
@@ -719,6 +878,22 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
 {
     const int nblk = a.t_end - a.t_begin - (a.gap_last ? 0 : a.gap_len);
     if (nblk <= 0) return cudaSuccess;
+    if (fmt == FDIRW_W_MX8) {  // staged stream only (whole tiles), at any launch size
+        if (a.tile % 32 != 0 || a.tile > kBulkWarps * 32 || a.list) return cudaErrorInvalidValue;
+        const size_t row = (size_t)(2 * R + 1) * a.tile * 9, half = (228 * 1024) / 2 - 1024 - 128;
+        int S = (int)(half / row);
+        if (S < 2) S = (int)((227 * 1024 - 128) / row);
+        if (S > 3) S = 3;  // measured at cfg3: 3 stages 1.74 ms, 4: 1.79, 2 (3 CTAs/SM): 1.76
+        if (const char* ev = getenv("FDIRW_MX8_STAGES")) S = atoi(ev);  // A/B of the stage count
+        if (S < 2) return cudaErrorInvalidValue;
+        const size_t smem = 128 + (size_t)S * row;
+        const void* f = a.tile == 256 ? (const void*)superpose_mx8_kernel<R, 256> : (const void*)superpose_mx8_kernel<R, 0>;
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (a.tile == 256) superpose_mx8_kernel<R, 256><<<nblk, a.tile + 32, smem, s>>>(a, S);
+        else superpose_mx8_kernel<R, 0><<<nblk, a.tile + 32, smem, s>>>(a, S);
+        return cudaGetLastError();
+    }
     // a launch of fewer than two CTAs per SM cannot keep enough weight loads in flight
     // through occupancy: those threads prefetch one row ahead instead (identical bits)
     // TMA-staged weight stream for launches of ≥ 2 CTAs per SM (the common case); the
@@ -1154,6 +1329,11 @@ __global__ void export_kernel(const void* __restrict__ Wt, const float* __restri
                 v = (cp == -2 && o == g.K / 2) ? 1.0 : 0.0;
             } else if (o == g.K / 2) {
                 v = diag[(tile * g.tile + e) * 8 + j];
+            } else if (fmt == FDIRW_W_MX8) {
+                size_t mo, so;
+                mx8_addr(tile, slot_of(ox, oy, oz, g.R), e, j, g.L, g.K, g.tile, &mo, &so);
+                const unsigned char* wq = reinterpret_cast<const unsigned char*>(Wt);
+                v = mx8_decode(wq[mo], wq[so]);
             } else {
                 const size_t idx = ((tile * (size_t)(g.K - 1) + slot_of(ox, oy, oz, g.R)) * g.tile + e) * 8 + j;
                 if (fmt == 0) v = reinterpret_cast<const float*>(Wt)[idx];

@@ -690,7 +690,10 @@ __device__ __forceinline__ unsigned long long fma2f(unsigned long long a, unsign
 }
 
 // One stored row's slots into the partial sums p (FMA chain in slot order).  The decode runs
-// two weights per FFMA2 (each lane an ordinary fp32 fma: exact here).
+// two weights per FFMA2 (each lane an ordinary fp32 fma: exact here, the scale and bias as
+// broadcast operands); the accumulation stays scalar: an FFMA2 there needs the C pairs
+// (seg[i], seg[i+1]) at odd i, which are not register pairs (measured: the re-pairing moves
+// cost more than the FFMA2 saves).
 template <int R, bool CENTRE_ROW, int TT>
 __device__ __forceinline__ void row_mx8(const float seg[24], const unsigned char* mb, const unsigned char* sb, int T_,
                                         float p[8])
@@ -730,6 +733,9 @@ __device__ __forceinline__ void flush_mx8(float p[8], float hi[8], float lo[8])
     }
 }
 
+#ifndef MX8_ROWS
+#define MX8_ROWS 4  // rows per fp32 partial before the error-free add (cfg3 mass drift: DESIGN §15)
+#endif
 template <int R, int TT>
 __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel(const SuperArgs a, int S)
 {
@@ -785,21 +791,23 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
         int st = 0;
         uint32_t ph = 0;
         // row i = 0: the centre row; then (oz, oy) ascending without the centre (row_src order)
-        const float* srow = t.c0 - 8;
+        // source row of stored row i: C_old − oz·plane − oy·nxp − 8 (32-bit offsets: the padded
+        // state is < 2^31 elements)
+        const int pl = (int)t.plane, nx_ = (int)t.nxp;
+        int oz = 0, oy = 0;
         for (int i = 0; i < NROW; ++i) {
-            if (i == 1) srow = t.c0 + (long)R * t.plane + (long)R * t.nxp - 8;  // (oz, oy) = (−R, −R)
-            if (t.real) load_seg(srow, seg);
+            if (t.real) load_seg(t.c0 + (-oz * pl - oy * nx_ - 8), seg);
             mbar_wait(smem_u32(full + st), ph);
             if (t.real) {
-                // partial sums over the centre row, then over pairs of rows (L² − 1 is even),
-                // each added to (hi, lo) error-free: 1/L² .. 2/L² of the total per partial
+                // partial sums over the centre row, then over groups of MX8_ROWS rows (L² − 1 =
+                // 4R(R+1) is a multiple of 8), each added to (hi, lo) error-free
                 const unsigned char* mb = m0 + st * stageB;
                 if (i == 0) {
                     row_mx8<R, true, TT>(seg, mb, s0 + st * stageB + (L - 2) * 8 * T, T, p);
                     flush_mx8(p, hi, lo);
                 } else {
                     row_mx8<R, false, TT>(seg, mb, s0 + st * stageB + (L - 1) * 8 * T, T, p);
-                    if ((i & 1) == 0) flush_mx8(p, hi, lo);
+                    if (i % MX8_ROWS == 0) flush_mx8(p, hi, lo);
                 }
             }
             __syncwarp();
@@ -808,12 +816,15 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
                 st = 0;
                 ph ^= 1u;
             }
-            if (i >= 1) {  // next (oz, oy): oy + 1 (row pointer − nxp), wrapping to oz + 1
-                const int r = i - 1 < R * L + R ? i - 1 : i;  // this row's (oz, oy) index
-                const int rn = r + 1 == R * L + R ? r + 2 : r + 1;
-                if (rn % L == 0) srow += (long)(L - 1) * t.nxp - t.plane;
-                else srow -= t.nxp;
-                if (rn - r == 2) srow -= t.nxp;  // skipped the centre row (same oz)
+            if (i == 0) {  // after the centre row: (oz, oy) = (−R, −R), then ascending, centre skipped
+                oz = -R;
+                oy = -R;
+            } else {
+                if (++oy > R) {
+                    oy = -R;
+                    ++oz;
+                }
+                if (oz == 0 && oy == 0) oy = 1;
             }
         }
     }

@@ -758,10 +758,9 @@ def main():
         line["roofline"]["traffic"] = tr[0]
         line["roofline"]["traffic_source"] = tr[1] + " (ncu --set full, one launch)"
     fd.destroy(ctx)
-    if world == 1 and not dedup_storage and not far and not args.no_variants:
+    if world == 1 and not dedup_storage and not far and not args.no_variants and params.weights != "mx8":
         line["variants"] = {"N4_dedup_storage": _variant_n4(fd, torch, params, mask, c_host, args, stream, peak)}
-        if params.weights != "mx8":
-            line["variants"]["mx8_weights"] = _variant_mx8(fd, torch, params, mask, c_host, args, stream, peak)
+        line["variants"]["mx8_weights"] = _variant_mx8(fd, torch, params, mask, c_host, args, stream, peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, mask)
         if cfg.name == "cfg1":

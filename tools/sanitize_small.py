@@ -46,6 +46,16 @@ def main():
             assert ctx.info["n_tiles"] >= 2 * 148
             c = cb.clone()
             fd.run(ctx, c, 2)
+    # MX8 weights: expand + diag build pass, staged MX8 stream (tile 256 and a
+    # runtime tile width), export
+    if not EXTRA:
+        for shp, R in ((shape, 3), (big, 1)):
+            mk = mask if shp == shape else bmask
+            with fd.build_kernels(params(shp, R, 30, "mx8"), mk) as ctx:
+                c = (c0 if shp == shape else cb).clone()
+                fd.run(ctx, c, 2)
+                fd.mass(ctx, c)
+                fd.export_kernels(ctx, (0, 5, 0, 4, 0, 3))
     # far field (N2)
     fmask = fi.with_far_field(fi.porous_particle(shape, 4, pore_r=(1.0, 1.5), n_pores=3, seed=1), 4, 2.0)
     with fd.build_kernels(params(shape, 2, 20, v_far=100.0), fmask) as ctx:

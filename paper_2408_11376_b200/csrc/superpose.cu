@@ -733,9 +733,15 @@ __device__ __forceinline__ void flush_mx8(float p[8], float hi[8], float lo[8])
     }
 }
 
-#ifndef MX8_ROWS
-#define MX8_ROWS 4  // rows per fp32 partial before the error-free add (cfg3 mass drift: DESIGN §15)
-#endif
+// rows per fp32 partial before the error-free add: the most rows of ≤ 44 slots in all that
+// divide L² − 1 (R5: 4 rows; R8: 2).  A partial's fp32 round-off is systematic over
+// homogeneous regions, so it is bounded in slots, not rows (cfg5 mass drift: DESIGN §15)
+constexpr int mx8_rows(int R)
+{
+    int g = 44 / (2 * R + 1);
+    while (g > 1 && ((2 * R + 1) * (2 * R + 1) - 1) % g != 0) --g;
+    return g < 1 ? 1 : g;
+}
 template <int R, int TT>
 __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel(const SuperArgs a, int S)
 {
@@ -799,7 +805,7 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
             if (t.real) load_seg(t.c0 + (-oz * pl - oy * nx_ - 8), seg);
             mbar_wait(smem_u32(full + st), ph);
             if (t.real) {
-                // partial sums over the centre row, then over groups of MX8_ROWS rows (L² − 1 =
+                // partial sums over the centre row, then over groups of mx8_rows(R) rows (L² − 1 =
                 // 4R(R+1) is a multiple of 8), each added to (hi, lo) error-free
                 const unsigned char* mb = m0 + st * stageB;
                 if (i == 0) {
@@ -807,7 +813,7 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
                     flush_mx8(p, hi, lo);
                 } else {
                     row_mx8<R, false, TT>(seg, mb, s0 + st * stageB + (L - 1) * 8 * T, T, p);
-                    if (i % MX8_ROWS == 0) flush_mx8(p, hi, lo);
+                    if (i % mx8_rows(R) == 0) flush_mx8(p, hi, lo);
                 }
             }
             __syncwarp();

@@ -56,6 +56,8 @@ def quantize_mx8(W: np.ndarray, R: int) -> np.ndarray:
         if o == kc:
             continue
         ox, oy, oz = o % L - R, (o // L) % L - R, o // (L * L) - R
+        if abs(ox) >= nx or abs(oy) >= ny or abs(oz) >= nz:
+            continue  # the offset leaves the grid from every source: no (source, target) pair
         # gather view: G[z, y, x] = W_{(z,y,x) − o}(o) for targets x in the grid, else 0
         G = np.zeros((nz, ny, nxq * 8))
         tz = slice(max(0, oz), min(nz, nz + oz)); sz = slice(max(0, -oz), min(nz, nz - oz))

@@ -169,3 +169,65 @@ def test_mx8_rejected_combinations(fd):
     for flags in (fd.F_DEDUP_STORAGE, fd.F_NO_MASS_FIX, fd.F_NO_DEDUP):
         with pytest.raises(fd.FdirwError):
             fd.build_kernels(lib_params(cfg, "mx8", flags=flags), mask)
+
+
+@pytest.mark.parametrize("shape,R,n_fd", [
+    ((7, 9, 13), 3, 50),      # ragged, several tiles per plane
+    ((1, 1, 37), 4, 9),       # 1-D grid
+    ((5, 3, 4), 1, 1),        # tiny, R = 1, one substep (exact regime)
+    ((6, 5, 9), 2, 300),
+    ((4, 12, 19), 5, 60),     # window larger than the domain in z
+    ((3, 3, 3), 8, 30),       # R = 8 > every dimension
+    ((6, 7, 40), 7, 120),     # R = 7, runtime tile width
+])
+def test_mx8_edge_shapes(fd, oracle_lib, shape, R, n_fd):
+    """Edge cases with MX8 weights: 3 steps vs the oracle on its own MX8-quantised kernels
+    (tight: only kgen round-off differs) and vs the exact oracle (north_star's 5e-3), mass."""
+    from oracle import mx8
+
+    cfg = small_cfg(shape, R, n_fd, D_slow=2e-3)
+    mask = fi.random_two_phase(shape, 0.55, seed=R + n_fd)
+    pb = oracle_problem(cfg, mask)
+    nz, ny, nx = shape
+    box = (0, nx, 0, ny, 0, nz)
+    c0 = fi.initial_c(mask, "random", seed=3)
+    W = oracle_lib.build_kernels(pb)
+    Wq = mx8.quantize_mx8(W, R)
+    ref, refq = c0.astype(np.float64), c0.astype(np.float64)
+    for _ in range(3):
+        ref = oracle_lib.step_scatter(pb, W, box, ref, box)
+        refq = oracle_lib.step_scatter(pb, Wq, box, refq, box)
+    import torch
+
+    ctx = fd.build_kernels(lib_params(cfg, "mx8"), mask)
+    try:
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        m0 = fd.mass(ctx, c)
+        fd.run(ctx, c, 3)
+        m1 = fd.mass(ctx, c)
+        got = c.cpu().numpy().astype(np.float64)
+    finally:
+        fd.destroy(ctx)
+    assert rel_l2(got, refq) <= 1e-3
+    assert rel_l2(got, ref) <= 5e-3
+    assert abs(m1 - m0) / m0 <= 1e-6
+
+
+def test_mx8_r8_mass_drift(fd):
+    """The fp32 partials are bounded in slots (R8: 2 rows per TwoSum): 200 steps
+    over a mostly homogeneous 64×64×96 R8 grid (identical kernels: systematic round-off) keep
+    the total mass to 1e-7 (4 rows per partial measured 8e-7 at cfg5)."""
+    import torch
+
+    cfg = small_cfg((64, 64, 96), 8, 400, D_slow=1e-3)
+    mask = fi.porous_particle(cfg.shape, 20, pore_r=(1.0, 2.0), porosity=0.3, seed=3)
+    c0 = torch.from_numpy(fi.initial_c(mask, "paper")).cuda()
+    ctx = fd.build_kernels(lib_params(cfg, "mx8"), mask)
+    try:
+        c = c0.clone()
+        m0 = fd.mass(ctx, c)
+        fd.run(ctx, c, 200)
+        m1 = fd.mass(ctx, c)
+    finally:
+        fd.destroy(ctx)
+    assert abs(m1 - m0) / m0 <= 1e-7

@@ -83,9 +83,13 @@ def _brute(W, R):
     return out
 
 
-def test_gather_blocks_vs_brute_force():
+@pytest.mark.parametrize("R,shape", [
+    (1, (3, 4, 11)),   # nx = 11: a full chunk and a ragged one
+    (3, (2, 3, 5)),    # window larger than the grid in every direction
+    (2, (1, 1, 17)),   # 1-D
+])
+def test_gather_blocks_vs_brute_force(R, shape):
     rng = np.random.default_rng(7)
-    R, shape = 1, (3, 4, 11)   # nx = 11: a full chunk and a ragged one
     W = rng.random(shape + ((2 * R + 1) ** 3,)) ** 4
     W[rng.random(W.shape) < 0.1] = 0.0
     got = mx8.quantize_mx8(W, R)

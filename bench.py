@@ -216,7 +216,7 @@ def _variant_n4(fd, torch, params, mask, c_host, args, stream, peak):
         fd.destroy(ctx)
     N = int((mask != 2).sum())
     f_u = info["uniform_chunks"] / max(info["chunks"], 1)
-    b_w = 4 if p.weights == "fp32" else 2
+    b_w = {"fp32": 4, "mx8": 1.125}.get(p.weights, 2)
     bpv = (1.0 - f_u) * (info["K"] - 1) * b_w + 12
     ach = bpv * N / (ms * 1e-3) / 1e9
     return {"value": N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "uniform_fraction": f_u,
@@ -697,7 +697,8 @@ def main():
     dedup_storage = bool(params.flags & fd.F_DEDUP_STORAGE)
     f_u = info["uniform_chunks"] / max(info["chunks"], 1)
     if dedup_storage:  # N4 byte model: uniform chunks' weights come from an L2-resident table
-        bpv = int(round((1.0 - f_u) * (info["K"] - 1) * (2 if cfg.weights != "fp32" else 4))) + 12
+        bw = {"fp32": 4, "mx8": 1.125}.get(cfg.weights, 2)
+        bpv = (1.0 - f_u) * (info["K"] - 1) * bw + 12
     per_launch_bytes = bpv * n_slab
     peak, peak_src = _hbm_peak()
     # N=1: one superpose launch; N>1 P2P: wait + one superpose launch + signal; NCCL: interior
@@ -724,7 +725,8 @@ def main():
                           % (info["weight_bytes"] / 1e6))},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": ("superpose_mx8_kernel (TMA-staged MX8 rows)" if cfg.weights == "mx8" else
+                     "kernel": ("superpose_mx8_mixed_kernel (MX8 rows + uniform blocks)" if cfg.weights == "mx8" and dedup_storage else
+                                "superpose_mx8_kernel (TMA-staged MX8 rows)" if cfg.weights == "mx8" else
                                 "superpose_bulk_kernel (TMA-staged weights)" if info["n_tiles"] >= 2 * 148
                                 else "superpose_kernel (register prefetch)"),
                      "peak_source": peak_src, "bytes_per_voxel_update": bpv,
@@ -761,6 +763,11 @@ def main():
     if world == 1 and not dedup_storage and not far and not args.no_variants and params.weights != "mx8":
         line["variants"] = {"N4_dedup_storage": _variant_n4(fd, torch, params, mask, c_host, args, stream, peak)}
         line["variants"]["mx8_weights"] = _variant_mx8(fd, torch, params, mask, c_host, args, stream, peak)
+        import dataclasses
+
+        v = _variant_n4(fd, torch, dataclasses.replace(params, weights="mx8"), mask, c_host, args, stream, peak)
+        v["note"] = "MX8 weights + N4 storage: superpose_mx8_mixed_kernel (DESIGN §15)"
+        line["variants"]["mx8_dedup_storage"] = v
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, mask)
         if cfg.name == "cfg1":

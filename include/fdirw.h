@@ -68,8 +68,10 @@ typedef enum {
  * power of two with max(block)/s <= 255, m = RNE(w/s); 1.125 bytes per weight.  The fp32
  * diagonal fix-up restores each source's mass from the decoded weights.  Accuracy is within
  * north_star's reduced-precision bar (relL2 <= 5e-3).  Supported on one rank (world == 1), closed
- * domain (v_far == 0), without FDIRW_F_DEDUP_STORAGE / _NO_MASS_FIX / _NO_DEDUP / _SYMMETRIC_RULE /
- * _KGEN_FP64; other combinations return FDIRW_E_INVALID.                                       */
+ * domain (v_far == 0), without FDIRW_F_NO_MASS_FIX / _NO_DEDUP / _SYMMETRIC_RULE / _KGEN_FP64;
+ * other combinations return FDIRW_E_INVALID.  With FDIRW_F_DEDUP_STORAGE the uniform chunks
+ * use their class kernel quantised as blocks of 8 equal weights (exactly what the dense
+ * layout would store there) and a per-target diagonal.                                       */
 typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2, FDIRW_W_MX8 = 3 } fdirw_weight_t;
 
 /* fdirw_params.flags */

@@ -452,8 +452,20 @@ __global__ void __launch_bounds__(256) expand_mx8_kernel(const ExpandArgs a)
     constexpr int L = 2 * R + 1, LL = L * L, K = L * L * L;
     const int tile = blockIdx.x;
     const int e = threadIdx.x;
-    const int zl = tile / a.tpp, q = (tile % a.tpp) * a.tile + e;
-    const bool real = q < a.ny * a.nxq;
+    int zl, q;
+    bool real;
+    if (a.list) {  // N4: compacted non-uniform chunks
+        const long idx = (long)tile * a.tile + e;
+        real = idx < a.n_list;
+        const int chunk = real ? a.list[idx] : 0;
+        const int ot = chunk / a.tile;
+        zl = ot / a.tpp;
+        q = (ot % a.tpp) * a.tile + chunk % a.tile;
+    } else {
+        zl = tile / a.tpp;
+        q = (tile % a.tpp) * a.tile + e;
+        real = q < a.ny * a.nxq;
+    }
     unsigned char* wq = reinterpret_cast<unsigned char*>(a.Wt);
     const float* cw = reinterpret_cast<const float*>(a.class_w);
     const int y = real ? q / a.nxq : 0, x = real ? (q % a.nxq) * 8 : 0;
@@ -492,7 +504,9 @@ __global__ void __launch_bounds__(256) expand_mx8_kernel(const ExpandArgs a)
 // x fastest: neighbouring threads read neighbouring bytes).  Sources outside the domain
 // (class −1) and dummy targets keep 0.  One rank (the whole grid is the slab).
 template <int R>
-__global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int nzl)
+__global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int nzl, const int* __restrict__ cmap,
+                                                       const int* __restrict__ chunk_u, const float* __restrict__ ukq,
+                                                       float* __restrict__ udiag_t)
 {
     constexpr int L = 2 * R + 1, K = L * L * L;
     const long n = (long)a.nx * a.ny * nzl;
@@ -502,7 +516,12 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
         const int sx = (int)(i % a.nx), sy = (int)((i / a.nx) % a.ny), sz = (int)(i / ((long)a.nx * a.ny));
         const int cls = a.class_pad[(sz + R) * plane + (long)(sy + R) * nxp + kPadX + sx];
         const int q0 = sy * a.nxq + (sx >> 3);
-        float* dp = a.diag + (((size_t)sz * a.tpp + q0 / a.tile) * a.tile + q0 % a.tile) * 8 + (sx & 7);
+        const size_t ch0 = ((size_t)sz * a.tpp + q0 / a.tile) * a.tile + q0 % a.tile;
+        float* dp = a.diag + ch0 * 8 + (sx & 7);
+        if (cmap) {  // N4 storage: compact dense position, or the uniform list position
+            const int m = cmap[ch0];
+            dp = m >= 0 ? a.diag + (size_t)m * 8 + (sx & 7) : udiag_t + (size_t)(-m - 2) * 8 + (sx & 7);
+        }
         if (cls < 0) {
             *dp = 0.f;
             continue;
@@ -519,9 +538,20 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
                     const int x = sx + ox;
                     if ((ox == 0 && oy == 0 && oz == 0) || x < 0 || x >= a.nx) continue;
                     const int q = y * a.nxq + (x >> 3);
+                    const int sl = slot_of(ox, oy, oz, R);
+                    size_t tl = (size_t)z * a.tpp + q / a.tile;
+                    int e = q % a.tile;
+                    if (cmap) {
+                        const int m = cmap[tl * a.tile + e];
+                        if (m < 0) {  // uniform chunk: its class kernel, quantised as 8 equal weights
+                            off += (double)ukq[(size_t)chunk_u[tl * a.tile + e] * (K - 1) + sl];
+                            continue;
+                        }
+                        tl = (size_t)(m / a.tile);
+                        e = m % a.tile;
+                    }
                     size_t mo, so;
-                    mx8_addr((size_t)z * a.tpp + q / a.tile, slot_of(ox, oy, oz, R), q % a.tile, x & 7, L, K, a.tile,
-                             &mo, &so);
+                    mx8_addr(tl, sl, e, x & 7, L, K, a.tile, &mo, &so);
                     off += (double)mx8_decode(__ldg(wq + mo), __ldg(wq + so));
                 }
             }
@@ -530,18 +560,66 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
     }
 }
 
+// MX8 + N4 storage: a uniform chunk's block for slot o is 8 equal weights W_u(o), so its
+// stored value is W_u(o) quantised alone (m ∈ [128, 255]); ukf is rewritten in place.
+__global__ void mx8_uniform_quant_kernel(float* __restrict__ ukf, long n)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = ukf[i];
+        uint2 m;
+        uint32_t E;
+        mx8_quant(v, &m, &E);
+        ukf[i] = mx8_decode(m.x & 0xffu, E);
+    }
+}
+
+__global__ void mx8_chunk_map_kernel(const int* __restrict__ dense, long n_dense, const int* __restrict__ ulist,
+                                     long n_uni, int* __restrict__ cmap)
+{
+    const long n = n_dense + n_uni;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        if (i < n_dense) cmap[dense[i]] = (int)i;
+        else cmap[ulist[i - n_dense]] = -(int)(i - n_dense) - 2;
+    }
+}
+
 template <int R>
 static cudaError_t launch_expand_r(const ExpandArgs& a, int fmt, cudaStream_t s)
 {
-    if (a.n_tiles <= 0) return cudaSuccess;
     if (fmt == FDIRW_W_MX8) {
-        if (a.list) return cudaErrorInvalidValue;  // dense tiles of one rank only
-        expand_mx8_kernel<R><<<a.n_tiles, a.tile, 0, s>>>(a);
-        cudaError_t e = cudaMemsetAsync(a.diag, 0, (size_t)a.n_tiles * a.tile * 8 * 4, s);
-        if (e != cudaSuccess) return e;
-        mx8_diag_kernel<R><<<148 * 8, 256, 0, s>>>(a, a.n_tiles / a.tpp);
+        const int K = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
+        UniformTables* ut = a.ut;
+        cudaError_t e = cudaSuccess;
+        if (ut) {
+            const long nch = (long)a.nzl * a.tpp * a.tile;
+            e = cudaMalloc(&ut->chunk_map, nch * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&ut->udiag_t, (size_t)std::max<long>(ut->n_uniform, 1) * 8 * 4);
+            if (e == cudaSuccess) e = cudaMemsetAsync(ut->chunk_map, 0xff, nch * 4, s);
+            if (e == cudaSuccess) e = cudaMemsetAsync(ut->udiag_t, 0, (size_t)std::max<long>(ut->n_uniform, 1) * 32, s);
+            if (e == cudaSuccess && ut->n_u > 0) {
+                const long n = (long)ut->n_u * (K - 1);
+                mx8_uniform_quant_kernel<<<grid_n(n), 256, 0, s>>>(ut->ukf, n);
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess && ut->n_dense + ut->n_uniform > 0) {
+                mx8_chunk_map_kernel<<<grid_n(ut->n_dense + ut->n_uniform), 256, 0, s>>>(
+                    ut->dense_list, ut->n_dense, ut->list, ut->n_uniform, ut->chunk_map);
+                e = cudaGetLastError();
+            }
+            if (e != cudaSuccess) return e;
+        }
+        if (a.n_tiles > 0) {
+            expand_mx8_kernel<R><<<a.n_tiles, a.tile, 0, s>>>(a);
+            e = cudaMemsetAsync(a.diag, 0, (size_t)a.n_tiles * a.tile * 8 * 4, s);
+            if (e != cudaSuccess) return e;
+        }
+        mx8_diag_kernel<R><<<148 * 8, 256, 0, s>>>(a, a.nzl, ut ? ut->chunk_map : nullptr, ut ? ut->chunk_u : nullptr,
+                                                 ut ? ut->ukf : nullptr, ut ? ut->udiag_t : nullptr);
         return cudaGetLastError();
     }
+    if (a.n_tiles <= 0) return cudaSuccess;
     if (fmt == 0) expand_kernel<R, float><<<a.n_tiles, a.tile, 0, s>>>(a);
     else if (fmt == 1) expand_kernel<R, __half><<<a.n_tiles, a.tile, 0, s>>>(a);
     else expand_kernel<R, __nv_bfloat16><<<a.n_tiles, a.tile, 0, s>>>(a);

@@ -285,10 +285,9 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (p->weights == FDIRW_W_MX8) {
         if (dist && dist->world > 1) return fail(FDIRW_E_INVALID, "MX8 weights need world == 1");
         if (p->v_far > 0) return fail(FDIRW_E_INVALID, "MX8 weights need a closed domain (v_far == 0)");
-        if (p->flags & (FDIRW_F_DEDUP_STORAGE | FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_SYMMETRIC_RULE |
-                        FDIRW_F_KGEN_FP64))
-            return fail(FDIRW_E_INVALID, "MX8 weights are not combined with DEDUP_STORAGE, NO_MASS_FIX, NO_DEDUP, "
-                                         "SYMMETRIC_RULE or KGEN_FP64");
+        if (p->flags & (FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_FP64))
+            return fail(FDIRW_E_INVALID, "MX8 weights are not combined with NO_MASS_FIX, NO_DEDUP, SYMMETRIC_RULE or "
+                                         "KGEN_FP64");
     }
     if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE | FDIRW_F_KGEN_FP64 |
                      FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT | FDIRW_F_NO_BULK_STREAM))
@@ -367,6 +366,8 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->ut.udiag);
     cudaFree(c->ut.list);
     cudaFree(c->ut.blocks);
+    cudaFree(c->ut.udiag_t);
+    cudaFree(c->ut.chunk_map);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -599,7 +600,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             size_t w_elems = g.w_elems, d_elems = g.diag_elems;
             if (e == cudaSuccess && (params->flags & FDIRW_F_DEDUP_STORAGE)) {
                 // N4: uniform chunks get no gather weights; the others are compacted into tiles
-                e = build_uniform(ea, g.R, c->fmt, dr.n_class, &c->ut, s);
+                e = build_uniform(ea, g.R, c->fmt == FDIRW_W_MX8 ? FDIRW_W_FP32 : c->fmt, dr.n_class, &c->ut, s);
+                if (c->fmt == FDIRW_W_MX8) ea.ut = &c->ut;
                 ea.list = c->ut.dense_list;
                 ea.n_list = c->ut.n_dense;
                 ea.n_tiles = c->ut.nd_tiles;
@@ -621,6 +623,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                 }
                 ea.Wt = c->Wt;
                 ea.diag = c->diag;
+                ea.nzl = g.nzl;
                 tr.mark("compact + alloc weights");
                 e = launch_expand(ea, g.R, c->fmt, s);
                 tr.mark("expand");
@@ -786,6 +789,7 @@ static cudaError_t superpose_uniform(fdirw_ctx* c, const float* src, float* out,
     u.n_blocks = c->ut.n_blocks;
     u.ukf = c->ut.ukf;
     u.udiag = c->ut.udiag;
+    u.udiag_t = c->ut.udiag_t;
     return launch_superpose_uniform(u, g.R, s);
 }
 
@@ -820,6 +824,7 @@ static cudaError_t superpose_n4_mixed(fdirw_ctx* c, const float* src, float* out
     u.n_blocks = c->ut.n_blocks;
     u.ukf = c->ut.ukf;
     u.udiag = c->ut.udiag;
+    u.udiag_t = c->ut.udiag_t;
     return launch_superpose_mixed(a, u, g.R, c->fmt, s);
 }
 

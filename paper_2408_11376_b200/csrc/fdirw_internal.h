@@ -108,6 +108,7 @@ struct DedupResult {
 };
 cudaError_t dedup_classify(const DedupArgs& a, DedupResult* res, cudaStream_t s);
 
+struct UniformTables;
 struct ExpandArgs {
     const int* class_pad;
     const void* class_w;
@@ -117,6 +118,8 @@ struct ExpandArgs {
     int nx, ny, nxq, tile, tpp, n_tiles, nxp, nyp;
     const int* list = nullptr;  // N4: compacted chunk ids (null = tile/e is the chunk)
     long n_list = 0;
+    UniformTables* ut = nullptr;  // MX8 with N4 storage: the uniform tables (quantised in place)
+    int nzl = 0;                  // MX8: slab planes (the diagonal pass walks every source)
 };
 cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s);
 // N4: per-chunk uniform class tables (see superpose.cu); arrays are cudaMalloc'ed
@@ -168,6 +171,7 @@ struct UniArgs {
     int n_blocks;
     const float* ukf;     // [u][K−1] class kernels in slot order, decoded to fp32
     const float* udiag;   // [u] fp32 diagonal
+    const float* udiag_t = nullptr;  // MX8: per-target diagonal [list position][8] (replaces udiag)
 };
 cudaError_t launch_superpose_uniform(const UniArgs& a, int R, cudaStream_t s);
 cudaError_t launch_superpose_mixed(const SuperArgs& a, const UniArgs& u, int R, int fmt, cudaStream_t s);
@@ -183,6 +187,10 @@ struct UniformTables {
     int* dense_list = nullptr;  // real non-uniform chunks (chunk order), compacted into tiles
     long n_dense = 0;
     int nd_tiles = 0;
+    // MX8: a target's diagonal depends on its neighbours' blocks, so uniform
+    // chunks carry a per-target diagonal; chunk_map = compact index (≥ 0) or −(list pos + 2)
+    float* udiag_t = nullptr;
+    int* chunk_map = nullptr;
 };
 
 // ---- N3 integrated loop + precision modes (absorb.cu) --------------------------------

@@ -309,11 +309,17 @@ __device__ __forceinline__ void uniform_body(const UniArgs& a, int blk, float* w
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
     const float d = a.udiag[b.z];
+    float dd[8] = {d, d, d, d, d, d, d, d};
+    if (a.udiag_t) {  // MX8: per-target diagonal
+        const float4 d0 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8));
+        const float4 d1 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8 + 4));
+        dd[0] = d0.x; dd[1] = d0.y; dd[2] = d0.z; dd[3] = d0.w; dd[4] = d1.x; dd[5] = d1.y; dd[6] = d1.z; dd[7] = d1.w;
+    }
     float hi[8], lo[8];
     {
         const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
-        hi[0] = d * v0.x; hi[1] = d * v0.y; hi[2] = d * v0.z; hi[3] = d * v0.w;
-        hi[4] = d * v1.x; hi[5] = d * v1.y; hi[6] = d * v1.z; hi[7] = d * v1.w;
+        hi[0] = dd[0] * v0.x; hi[1] = dd[1] * v0.y; hi[2] = dd[2] * v0.z; hi[3] = dd[3] * v0.w;
+        hi[4] = dd[4] * v1.x; hi[5] = dd[5] * v1.y; hi[6] = dd[6] * v1.z; hi[7] = dd[7] * v1.w;
 #pragma unroll
         for (int j = 0; j < 8; ++j) lo[j] = 0.f;
     }
@@ -743,9 +749,8 @@ constexpr int mx8_rows(int R)
     return g < 1 ? 1 : g;
 }
 template <int R, int TT>
-__global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel(const SuperArgs a, int S)
+__device__ __forceinline__ void mx8_body(const SuperArgs& a, int blk, int S, unsigned char* smem_b)
 {
-    extern __shared__ __align__(128) unsigned char smem_b[];
     constexpr int L = 2 * R + 1, K = L * L * L, NROW = L * L;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_b);
     uint64_t* empty = full + S;
@@ -764,7 +769,7 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
     __syncthreads();
     const bool producer = warp == nw;
     const int e = producer ? 0 : (int)threadIdx.x;
-    TileCtx t = tile_ctx<R>(a, blockIdx.x, e);
+    TileCtx t = tile_ctx<R>(a, blk, e);
     float hi[8], lo[8];
     if (producer) {
         if (lane == 0) {
@@ -835,6 +840,25 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
         }
     }
     tile_epilogue(a, t, e, hi, lo);
+}
+
+template <int R, int TT>
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel(const SuperArgs a, int S)
+{
+    extern __shared__ __align__(128) unsigned char smem_b[];
+    mx8_body<R, TT>(a, blockIdx.x, S, smem_b);
+}
+
+// MX8 with N4 storage: the mixed launch of superpose_mixed_bulk_kernel with MX8 dense tiles.
+template <int R>
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_mixed_kernel(const SuperArgs a,
+                                                                                      const UniArgs u, int S)
+{
+    extern __shared__ __align__(128) unsigned char smem_b[];
+    const long T = gridDim.x, U = u.n_blocks, b = blockIdx.x;
+    const long u0 = b * U / T, u1 = (b + 1) * U / T;
+    if (u1 > u0) uniform_body<R>(u, (int)u0, reinterpret_cast<float*>(smem_b + 128));
+    else mx8_body<R, 256>(a, (int)(b - u0), S, smem_b);
 }
 
 // N4 with the staged stream: the mixed launch's dense tiles run bulk_body, its uniform blocks
@@ -976,6 +1000,21 @@ static cudaError_t launch_mixed_r(const SuperArgs& a, const UniArgs& u, int fmt,
     const int nblk = (a.t_end - a.t_begin) + u.n_blocks;
     if (nblk <= 0) return cudaSuccess;
     if (a.tile != 256) return cudaErrorInvalidValue;  // uniform blocks are 256 chunks
+    if (fmt == FDIRW_W_MX8) {  // staged MX8 stream for the dense tiles, at any launch size
+        const size_t row = (size_t)(2 * R + 1) * a.tile * 9, half = (228 * 1024) / 2 - 1024 - 128;
+        int S = (int)(half / row);
+        if (S < 2) S = (int)((227 * 1024 - 128) / row);
+        if (S > 3) S = 3;
+        if (S < 2) return cudaErrorInvalidValue;
+        size_t smem = 128 + (size_t)S * row;
+        const size_t need = 128 + (size_t)((2 * R + 1) * (2 * R + 1) * (2 * R + 1) - 1) * 4;  // uniform kernel
+        if (smem < need) smem = need;
+        cudaError_t e = cudaFuncSetAttribute(superpose_mx8_mixed_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        superpose_mx8_mixed_kernel<R><<<nblk, a.tile + 32, smem, s>>>(a, u, S);
+        return cudaGetLastError();
+    }
     if (!a.no_bulk && nblk >= 2 * 148) {
         const int b_w = fmt == 0 ? 4 : 2;
         int cps = 0;

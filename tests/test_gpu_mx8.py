@@ -166,7 +166,7 @@ def test_mx8_cfg3_bench_config_sampled(fd, oracle_lib):
 def test_mx8_rejected_combinations(fd):
     cfg = small_cfg((8, 8, 8), 2, 50)
     mask = fi.random_two_phase(cfg.shape, 0.6, seed=1)
-    for flags in (fd.F_DEDUP_STORAGE, fd.F_NO_MASS_FIX, fd.F_NO_DEDUP):
+    for flags in (fd.F_NO_MASS_FIX, fd.F_NO_DEDUP):
         with pytest.raises(fd.FdirwError):
             fd.build_kernels(lib_params(cfg, "mx8", flags=flags), mask)
 
@@ -231,3 +231,44 @@ def test_mx8_r8_mass_drift(fd):
     finally:
         fd.destroy(ctx)
     assert abs(m1 - m0) / m0 <= 1e-7
+
+
+@pytest.mark.parametrize("cfgname", ["cfg3", "liquid_r2"])
+def test_mx8_dedup_storage(fd, oracle_lib, cfgname):
+    """MX8 with N4 storage (uniform chunks read their class kernel, quantised as blocks of 8
+    equal weights, plus a per-target diagonal): the same decoded operator as dense MX8, so the
+    fields agree to fp32 summation order (the uniform body adds per row, the MX8 body per
+    group of rows); vs the exact oracle within 5e-3; mass."""
+    import torch
+
+    if cfgname == "cfg3":
+        cfg, mask, steps = fi.config("cfg3"), None, 2
+        mask = cfg.mask()
+    else:  # mostly liquid around a small particle: homogeneous windows, so uniform chunks
+        cfg = small_cfg((12, 32, 64), 2, 60, D_slow=1e-3)  # 256 chunks per plane: N4 needs tile 256
+        mask, steps = fi.porous_particle(cfg.shape, 5, pore_r=(1.0, 1.5), porosity=0.3, seed=4), 10
+    c0 = torch.from_numpy(fi.initial_c(mask, "paper")).cuda()
+    out = {}
+    for flags in (0, fd.F_DEDUP_STORAGE):
+        ctx = fd.build_kernels(lib_params(cfg, "mx8", flags=flags), mask)
+        try:
+            if flags:
+                assert ctx.info["uniform_chunks"] > 0
+            c = c0.clone()
+            m0 = fd.mass(ctx, c)
+            fd.run(ctx, c, steps)
+            m1 = fd.mass(ctx, c)
+            out[flags] = c.cpu().numpy().astype(np.float64)
+            assert abs(m1 - m0) / m0 <= 1e-6
+        finally:
+            fd.destroy(ctx)
+    assert rel_l2(out[fd.F_DEDUP_STORAGE], out[0]) <= 1e-6
+    if cfgname != "cfg3":
+        pb = oracle_problem(cfg, mask)
+        nz, ny, nx = cfg.shape
+        box = (0, nx, 0, ny, 0, nz)
+        W = oracle_lib.build_kernels(pb)
+        ref = fi.initial_c(mask, "paper").astype(np.float64)
+        for _ in range(steps):
+            ref = oracle_lib.step_scatter(pb, W, box, ref, box)
+        assert rel_l2(out[fd.F_DEDUP_STORAGE], ref) <= 5e-3

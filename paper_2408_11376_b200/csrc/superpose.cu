@@ -849,6 +849,70 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
     mx8_body<R, TT>(a, blockIdx.x, S, smem_b);
 }
 
+// MX8 uniform blocks: uniform_body's work with the MX8 body's summation grouping (the centre
+// row, then groups of mx8_rows(R) rows into one fp32 partial before the TwoSum).  The decoded
+// weights are the dense MX8 layout's, so the field is bitwise the dense MX8 path's.
+template <int R>
+__device__ __forceinline__ void uniform_body_mx8(const UniArgs& a, int blk, float* ws)
+{
+    constexpr int L = 2 * R + 1, K = L * L * L, G = mx8_rows(R);
+    const int4 b = a.blocks[blk];  // {start, count, u, -}
+    for (int i = threadIdx.x; i < K - 1; i += blockDim.x) ws[i] = a.ukf[(size_t)b.z * (K - 1) + i];
+    __syncthreads();
+    if ((int)threadIdx.x >= b.y) return;
+    const int chunk = a.list[b.x + threadIdx.x];
+    const int tile = chunk / a.tile, e = chunk % a.tile;
+    const int zl = tile / a.tpp, tp = tile % a.tpp;
+    const int q = tp * a.tile + e;
+    const int y = q / a.nxq, x = (q % a.nxq) * 8;
+    const long nxp = a.nxp, plane = (long)a.nyp * nxp;
+    const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
+    float hi[8], lo[8], p[8];
+    {
+        const float4 d0 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8));
+        const float4 d1 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8 + 4));
+        const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
+        hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
+        hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) lo[j] = p[j] = 0.f;
+    }
+    float seg[24];
+    int n = 0;  // stored row index (0: the centre row)
+    const float* wr = ws;
+    for (int oz = -R - 1; oz <= R; ++oz) {  // oz = −R − 1 stands for the centre row
+#pragma unroll 1
+        for (int oy = -R; oy <= R; ++oy) {
+            const bool centre = oz == -R - 1;
+            if (centre && oy > -R) break;
+            if (!centre && oz == 0 && oy == 0) continue;
+            load_seg(centre ? c0 - 8 : c0 - (long)oz * plane - (long)oy * nxp - 8, seg);
+#pragma unroll
+            for (int ox = -R; ox <= R; ++ox) {
+                if (centre && ox == 0) continue;
+                const int k = centre ? (ox < 0 ? ox + R : ox + R - 1) : ox + R;
+                const float w = wr[k];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) p[j] = fmaf(w, seg[j - ox + 8], p[j]);
+            }
+            wr += centre ? L - 1 : L;
+            if (n == 0 || n % G == 0) flush_mx8(p, hi, lo);
+            ++n;
+        }
+    }
+    float* out = a.out + (long)zl * a.out_ps + (long)y * a.out_rs + x;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(hi[j], lo[j]);
+    if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) out[j] = acc[j];
+    }
+}
+
 // MX8 with N4 storage: the mixed launch of superpose_mixed_bulk_kernel with MX8 dense tiles.
 template <int R>
 __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_mixed_kernel(const SuperArgs a,
@@ -857,7 +921,7 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_mixed_
     extern __shared__ __align__(128) unsigned char smem_b[];
     const long T = gridDim.x, U = u.n_blocks, b = blockIdx.x;
     const long u0 = b * U / T, u1 = (b + 1) * U / T;
-    if (u1 > u0) uniform_body<R>(u, (int)u0, reinterpret_cast<float*>(smem_b + 128));
+    if (u1 > u0) uniform_body_mx8<R>(u, (int)u0, reinterpret_cast<float*>(smem_b + 128));
     else mx8_body<R, 256>(a, (int)(b - u0), S, smem_b);
 }
 

@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(256) expand_mx8_kernel(const ExpandArgs a)
 // source's weights read back from the gather blocks at targets s + o (one thread per source,
 // x fastest: neighbouring threads read neighbouring bytes).  Sources outside the domain
 // (class −1) and dummy targets keep 0.  One rank (the whole grid is the slab).
-template <int R>
+template <int R, int TT>  // TT: the tile width when it is 256 (shifts instead of divisions), else 0
 __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int nzl, const int* __restrict__ cmap,
                                                        const int* __restrict__ chunk_u, const float* __restrict__ ukq,
                                                        float* __restrict__ udiag_t)
@@ -512,11 +512,12 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
     const long n = (long)a.nx * a.ny * nzl;
     const unsigned char* wq = reinterpret_cast<const unsigned char*>(a.Wt);
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
+    const int T_ = TT ? TT : a.tile;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         const int sx = (int)(i % a.nx), sy = (int)((i / a.nx) % a.ny), sz = (int)(i / ((long)a.nx * a.ny));
         const int cls = a.class_pad[(sz + R) * plane + (long)(sy + R) * nxp + kPadX + sx];
         const int q0 = sy * a.nxq + (sx >> 3);
-        const size_t ch0 = ((size_t)sz * a.tpp + q0 / a.tile) * a.tile + q0 % a.tile;
+        const size_t ch0 = ((size_t)sz * a.tpp + q0 / T_) * T_ + q0 % T_;
         float* dp = a.diag + ch0 * 8 + (sx & 7);
         if (cmap) {  // N4 storage: compact dense position, or the uniform list position
             const int m = cmap[ch0];
@@ -539,19 +540,19 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
                     if ((ox == 0 && oy == 0 && oz == 0) || x < 0 || x >= a.nx) continue;
                     const int q = y * a.nxq + (x >> 3);
                     const int sl = slot_of(ox, oy, oz, R);
-                    size_t tl = (size_t)z * a.tpp + q / a.tile;
-                    int e = q % a.tile;
+                    size_t tl = (size_t)z * a.tpp + q / T_;
+                    int e = q % T_;
                     if (cmap) {
-                        const int m = cmap[tl * a.tile + e];
+                        const int m = cmap[tl * T_ + e];
                         if (m < 0) {  // uniform chunk: its class kernel, quantised as 8 equal weights
-                            off += (double)ukq[(size_t)chunk_u[tl * a.tile + e] * (K - 1) + sl];
+                            off += (double)ukq[(size_t)chunk_u[tl * T_ + e] * (K - 1) + sl];
                             continue;
                         }
-                        tl = (size_t)(m / a.tile);
-                        e = m % a.tile;
+                        tl = (size_t)(m / T_);
+                        e = m % T_;
                     }
                     size_t mo, so;
-                    mx8_addr(tl, sl, e, x & 7, L, K, a.tile, &mo, &so);
+                    mx8_addr(tl, sl, e, x & 7, L, K, T_, &mo, &so);
                     off += (double)mx8_decode(__ldg(wq + mo), __ldg(wq + so));
                 }
             }
@@ -615,8 +616,14 @@ static cudaError_t launch_expand_r(const ExpandArgs& a, int fmt, cudaStream_t s)
             e = cudaMemsetAsync(a.diag, 0, (size_t)a.n_tiles * a.tile * 8 * 4, s);
             if (e != cudaSuccess) return e;
         }
-        mx8_diag_kernel<R><<<148 * 8, 256, 0, s>>>(a, a.nzl, ut ? ut->chunk_map : nullptr, ut ? ut->chunk_u : nullptr,
-                                                 ut ? ut->ukf : nullptr, ut ? ut->udiag_t : nullptr);
+        if (a.tile == 256)
+            mx8_diag_kernel<R, 256><<<148 * 8, 256, 0, s>>>(a, a.nzl, ut ? ut->chunk_map : nullptr,
+                                                            ut ? ut->chunk_u : nullptr, ut ? ut->ukf : nullptr,
+                                                            ut ? ut->udiag_t : nullptr);
+        else
+            mx8_diag_kernel<R, 0><<<148 * 8, 256, 0, s>>>(a, a.nzl, ut ? ut->chunk_map : nullptr,
+                                                          ut ? ut->chunk_u : nullptr, ut ? ut->ukf : nullptr,
+                                                          ut ? ut->udiag_t : nullptr);
         return cudaGetLastError();
     }
     if (a.n_tiles <= 0) return cudaSuccess;

@@ -67,8 +67,9 @@ typedef enum {
  * 8-bit mantissas m plus one power-of-two scale s (8-bit exponent): w = m·s, s the smallest
  * power of two with max(block)/s <= 255, m = RNE(w/s); 1.125 bytes per weight.  The fp32
  * diagonal fix-up restores each source's mass from the decoded weights.  Accuracy is within
- * north_star's reduced-precision bar (relL2 <= 5e-3).  Supported on one rank (world == 1), closed
- * domain (v_far == 0), without FDIRW_F_NO_MASS_FIX / _NO_DEDUP / _SYMMETRIC_RULE / _KGEN_FP64;
+ * north_star's reduced-precision bar (relL2 <= 5e-3).  Supported on any slab decomposition
+ * (bitwise the one-rank result), closed domain (v_far == 0), without FDIRW_F_NO_MASS_FIX /
+ * _NO_DEDUP / _SYMMETRIC_RULE / _KGEN_FP64;
  * other combinations return FDIRW_E_INVALID.  With FDIRW_F_DEDUP_STORAGE the uniform chunks
  * use their class kernel quantised as blocks of 8 equal weights (exactly what the dense
  * layout would store there) and a per-target diagonal.                                       */

@@ -530,7 +530,8 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
         double off = 0.0;
         for (int oz = -R; oz <= R; ++oz) {
             const int z = sz + oz;
-            if (z < 0 || z >= nzl) continue;
+            if (z + a.z0 < 0 || z + a.z0 >= a.nz) continue;  // outside the grid
+            const bool off_slab = z < 0 || z >= nzl;  // another rank's target (world > 1)
             for (int oy = -R; oy <= R; ++oy) {
                 const int y = sy + oy;
                 if (y < 0 || y >= a.ny) continue;
@@ -538,8 +539,30 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
                 for (int ox = -R; ox <= R; ++ox) {
                     const int x = sx + ox;
                     if ((ox == 0 && oy == 0 && oz == 0) || x < 0 || x >= a.nx) continue;
-                    const int q = y * a.nxq + (x >> 3);
                     const int sl = slot_of(ox, oy, oz, R);
+                    if (off_slab) {
+                        // that rank stores this block; quantise it here from the class kernels
+                        // exactly as its expand_mx8_kernel does (the block's 8 sources
+                        // x0 + j − ox lie in this source's own row; identical windows have
+                        // bitwise identical kernels, so every rank decides the same codes)
+                        const int x0 = x & ~7;
+                        const int* crow = a.class_pad + (sz + R) * plane + (long)(sy + R) * nxp + kPadX;
+                        const float* cw = reinterpret_cast<const float*>(a.class_w);
+                        const int o = (oz + R) * L * L + (oy + R) * L + (ox + R);
+                        float v[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int c = crow[x0 + j - ox];
+                            v[j] = c >= 0 ? cw[(size_t)c * K + o] : 0.f;
+                        }
+                        uint2 m;
+                        uint32_t E;
+                        mx8_quant(v, &m, &E);
+                        const int jj = x & 7;
+                        off += (double)mx8_decode(((jj < 4 ? m.x : m.y) >> (8 * (jj & 3))) & 0xffu, E);
+                        continue;
+                    }
+                    const int q = y * a.nxq + (x >> 3);
                     size_t tl = (size_t)z * a.tpp + q / T_;
                     int e = q % T_;
                     if (cmap) {

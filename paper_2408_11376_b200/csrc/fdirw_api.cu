@@ -283,7 +283,6 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 3) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16, BF16 or MX8");
     if (p->weights == FDIRW_W_MX8) {
-        if (dist && dist->world > 1) return fail(FDIRW_E_INVALID, "MX8 weights need world == 1");
         if (p->v_far > 0) return fail(FDIRW_E_INVALID, "MX8 weights need a closed domain (v_far == 0)");
         if (p->flags & (FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_FP64))
             return fail(FDIRW_E_INVALID, "MX8 weights are not combined with NO_MASS_FIX, NO_DEDUP, SYMMETRIC_RULE or "
@@ -624,6 +623,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                 ea.Wt = c->Wt;
                 ea.diag = c->diag;
                 ea.nzl = g.nzl;
+                ea.z0 = g.z0;
+                ea.nz = g.nz;
                 tr.mark("compact + alloc weights");
                 e = launch_expand(ea, g.R, c->fmt, s);
                 tr.mark("expand");

@@ -120,6 +120,7 @@ struct ExpandArgs {
     long n_list = 0;
     UniformTables* ut = nullptr;  // MX8 with N4 storage: the uniform tables (quantised in place)
     int nzl = 0;                  // MX8: slab planes (the diagonal pass walks every source)
+    int z0 = 0, nz = 0;           // MX8: the slab's first global plane, the grid's planes
 };
 cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s);
 // N4: per-chunk uniform class tables (see superpose.cu); arrays are cudaMalloc'ed

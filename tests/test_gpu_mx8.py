@@ -272,3 +272,41 @@ def test_mx8_dedup_storage(fd, oracle_lib, cfgname):
         for _ in range(steps):
             ref = oracle_lib.step_scatter(pb, W, box, ref, box)
         assert rel_l2(out[fd.F_DEDUP_STORAGE], ref) <= 5e-3
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_mx8_virtual_ranks_bitwise(fd, world):
+    """MX8 over z-slabs (virtual ranks, R-plane halos): every rank's diagonal needs the blocks
+    its sources write into the neighbours' targets, which it re-quantises from its own class
+    kernels; the result is the 1-GPU MX8 field bitwise (and the kernels too, via export)."""
+    import torch
+
+    cfg = small_cfg((4 * 3, 11, 13), 3, 25)
+    mask = fi.random_two_phase(cfg.shape, 0.6, seed=world)
+    c0 = fi.initial_c(mask, "random", seed=world)
+    ctx1 = fd.build_kernels(lib_params(cfg, "mx8"), mask)
+    try:
+        a = torch.from_numpy(c0.copy()).cuda()
+        one = torch.empty_like(a)
+        fd.step(ctx1, a, one)
+        one = one.cpu().numpy()
+        W1 = fd.export_kernels(ctx1, (0, 13, 0, 11, 0, 12))
+    finally:
+        fd.destroy(ctx1)
+    sl = fd.slabs(cfg.shape[0], world)
+    ctxs = [fd.build_kernels(lib_params(cfg, "mx8"), mask, rank=r, world=world, z_begin=a, z_end=b, device=0)
+            for r, (a, b) in enumerate(sl)]
+    try:
+        cin = [torch.from_numpy(c0[a:b].copy()).cuda() for a, b in sl]
+        cout = [torch.empty_like(t) for t in cin]
+        fd.step_virtual(ctxs, cin, cout)
+        got = np.concatenate([t.cpu().numpy() for t in cout], axis=0)
+        # each rank's stored kernels: its targets' blocks and its own sources' diagonals
+        Wr = [fd.export_kernels(c, (0, 13, 0, 11, 0, 12)) for c in ctxs]
+    finally:
+        for c in ctxs:
+            fd.destroy(c)
+    np.testing.assert_array_equal(got, one)
+    K = cfg.K
+    for (a, b), W in zip(sl, Wr):
+        np.testing.assert_array_equal(W[a:b, ..., K // 2], W1[a:b, ..., K // 2])  # diagonals

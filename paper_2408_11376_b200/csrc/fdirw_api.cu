@@ -483,7 +483,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         cudaGetDevice(&c->device);
     }
     c->g = make_geometry(params->nx, params->ny, params->nz, params->radius, z0, z1,
-                         !(params->flags & FDIRW_F_DEDUP_STORAGE) && !(params->v_far > 0));
+                         !(params->flags & FDIRW_F_DEDUP_STORAGE) && !(params->v_far > 0) &&
+                             params->weights != FDIRW_W_MX8);  // MX8: tile 256, waves via stages
     const Geometry& g = c->g;
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     tr.s = s;
@@ -1135,7 +1136,8 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
     if ((st = derive(*p, &d)) != FDIRW_OK) return st;
     const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
     const Geometry g = make_geometry(p->nx, p->ny, p->nz, p->radius, dist ? dist->z_begin : 0,
-                                     dist ? dist->z_end : p->nz, !(p->flags & FDIRW_F_DEDUP_STORAGE) && !(p->v_far > 0));
+                                     dist ? dist->z_end : p->nz,
+                                     !(p->flags & FDIRW_F_DEDUP_STORAGE) && !(p->v_far > 0) && p->weights != FDIRW_W_MX8);
     const HaloPlan h = make_halo_plan(g, rank, world);
     int i0, i1;
     split_tiles(g, &i0, &i1);

@@ -989,6 +989,10 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
         int S = (int)(half / row);
         if (S < 2) S = (int)((227 * 1024 - 128) / row);
         if (S > 3) S = 3;  // measured at cfg3: 3 stages 1.74 ms, 4: 1.79, 2 (3 CTAs/SM): 1.76
+        // wave balance (the tile stays 256 for MX8, see make_geometry's caller): 2 stages give
+        // 3 CTAs/SM; take them when waves × CTAs-per-SM (∝ time when bandwidth-shared) drops,
+        // e.g. a 24-plane slab (432 tiles) fits one wave of 444 instead of 1.5 of 296
+        if (S == 3 && (long)3 * ((nblk + 443) / 444) < (long)2 * ((nblk + 295) / 296)) S = 2;
         if (const char* ev = getenv("FDIRW_MX8_STAGES")) S = atoi(ev);  // A/B of the stage count
         if (S < 2) return cudaErrorInvalidValue;
         const size_t smem = 128 + (size_t)S * row;

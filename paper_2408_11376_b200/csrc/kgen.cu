@@ -207,7 +207,13 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         // Face numbers in registers: λ for the direct substeps; 2μ = 4λ/(1 − a) (rounded once
         // from fp64 on the host) for the Chebyshev recurrence, which steps the mapped operator
         // Â = (2A − (1 + a)I)/(1 − a) = I + Σ μ_f (c_f − c).
-        float lzp[L], lzm[L];  // own +z / −z face numbers (asymmetric next to the reservoir)
+        // z faces: fz[z] = the face between cells z and z + 1, as seen from its active side
+        // (face_lambda is symmetric except towards a reservoir cell, whose own faces are 0):
+        // both cells read the same register, 17 fewer per thread at R8 than separate −z / +z
+        // arrays.  A reservoir cell (open windows, N2) then picks up z fluxes, so the literal
+        // substeps reset it to its Dirichlet 0 (rmask); closed windows have none.
+        float fz[L > 1 ? L - 1 : 1];
+        unsigned rmask = 0;
         // Lateral face numbers: cells (2h, 2h+1) packed for FFMA2/FADD2, h < NPR; the odd last
         // cell L − 1 on its own (L = 2R + 1 is odd).
         constexpr int NPR = (L - 1) / 2;
@@ -224,8 +230,11 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
                 v[1][z] = (col && oxp) ? face_lambda(p, ph[i + oxp], fff, ffs, fss) : 0.f;
                 v[2][z] = (col && oym) ? face_lambda(p, ph[i + oym], fff, ffs, fss) : 0.f;
                 v[3][z] = (col && oyp) ? face_lambda(p, ph[i + oyp], fff, ffs, fss) : 0.f;
-                lzp[z] = (col && z < L - 1) ? face_lambda(p, ph[i + LL], fff, ffs, fss) : 0.f;
-                lzm[z] = (col && z > 0) ? face_lambda(p, ph[i - LL], fff, ffs, fss) : 0.f;
+                if (z < L - 1) {
+                    const unsigned q = col ? ph[i + LL] : 2u;
+                    fz[z] = col ? (p <= 1u ? face_lambda(p, q, fff, ffs, fss) : face_lambda(q, p, fff, ffs, fss)) : 0.f;
+                }
+                if (col && p == 3u) rmask |= 1u << z;
             }
 #pragma unroll
             for (int h = 0; h < NPR; ++h) {
@@ -285,8 +294,8 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
 #pragma unroll
                 for (int z = 0; z < L; ++z) {
                     float v = nw[z];
-                    if (z > 0) v = fmaf(lzm[z], -dz[z - 1], v);
-                    if (z < L - 1) v = fmaf(lzp[z], dz[z], v);
+                    if (z > 0) v = fmaf(fz[z - 1], -dz[z - 1], v);
+                    if (z < L - 1) v = fmaf(fz[z], dz[z], v);
                     nw[z] = v;
                 }
             };
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
                 for (int z = 0; z < L; ++z) nw[z] = c[z];
                 flux(b, c, nw);
 #pragma unroll
-                for (int z = 0; z < L; ++z) c[z] = nw[z];
+                for (int z = 0; z < L; ++z) c[z] = (rmask >> z) & 1u ? 0.f : nw[z];
             }
         }
         if (cheb) {

@@ -1073,6 +1073,7 @@ static cudaError_t launch_mixed_r(const SuperArgs& a, const UniArgs& u, int fmt,
         int S = (int)(half / row);
         if (S < 2) S = (int)((227 * 1024 - 128) / row);
         if (S > 3) S = 3;
+        if (const char* ev = getenv("FDIRW_MX8_STAGES")) S = atoi(ev);  // A/B of the stage count
         if (S < 2) return cudaErrorInvalidValue;
         size_t smem = 128 + (size_t)S * row;
         const size_t need = 128 + (size_t)((2 * R + 1) * (2 * R + 1) * (2 * R + 1) - 1) * 4;  // uniform kernel

@@ -68,8 +68,9 @@ typedef enum {
  * power of two with max(block)/s <= 255, m = RNE(w/s); 1.125 bytes per weight.  The fp32
  * diagonal fix-up restores each source's mass from the decoded weights.  Accuracy is within
  * north_star's reduced-precision bar (relL2 <= 5e-3).  Supported on any slab decomposition
- * (bitwise the one-rank result), closed domain (v_far == 0), without FDIRW_F_NO_MASS_FIX /
- * _NO_DEDUP / _SYMMETRIC_RULE / _KGEN_FP64;
+ * (bitwise the one-rank result), closed or open (v_far > 0: the diagonal is then the open
+ * window's own mass M minus its decoded weights), without FDIRW_F_NO_MASS_FIX / _NO_DEDUP /
+ * _SYMMETRIC_RULE / _KGEN_FP64, and not with the N3 precision-study modes 1-3;
  * other combinations return FDIRW_E_INVALID.  With FDIRW_F_DEDUP_STORAGE the uniform chunks
  * use their class kernel quantised as blocks of 8 equal weights (exactly what the dense
  * layout would store there) and a per-target diagonal.                                       */

@@ -522,6 +522,10 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
         if (cmap) {  // N4 storage: compact dense position, or the uniform list position
             const int m = cmap[ch0];
             dp = m >= 0 ? a.diag + (size_t)m * 8 + (sx & 7) : udiag_t + (size_t)(-m - 2) * 8 + (sx & 7);
+        } else if (a.far_pos) {  // N2 compaction: all-far / identity chunks store no diagonal
+            const int m = a.far_pos[ch0];
+            if (m < 0) continue;
+            dp = a.diag + (size_t)m * 8 + (sx & 7);
         }
         if (cls < 0) {
             *dp = 0.f;
@@ -565,7 +569,12 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
                     const int q = y * a.nxq + (x >> 3);
                     size_t tl = (size_t)z * a.tpp + q / T_;
                     int e = q % T_;
-                    if (cmap) {
+                    if (a.far_pos) {  // N2 compaction: no weights stored (all 0) for m < 0
+                        const int m = a.far_pos[tl * T_ + e];
+                        if (m < 0) continue;
+                        tl = (size_t)(m / T_);
+                        e = m % T_;
+                    } else if (cmap) {
                         const int m = cmap[tl * T_ + e];
                         if (m < 0) {  // uniform chunk: its class kernel, quantised as 8 equal weights
                             off += (double)ukq[(size_t)chunk_u[tl * T_ + e] * (K - 1) + sl];
@@ -580,7 +589,7 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
                 }
             }
         }
-        *dp = (float)(1.0 - off);
+        *dp = (float)((a.class_mass ? a.class_mass[cls] : 1.0) - off);
     }
 }
 

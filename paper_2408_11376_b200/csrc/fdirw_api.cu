@@ -283,7 +283,6 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
     if (p->n_fd < 0) return fail(FDIRW_E_INVALID, "n_fd must be >= 0");
     if (p->weights < 0 || p->weights > 3) return fail(FDIRW_E_INVALID, "weights must be FP32, FP16, BF16 or MX8");
     if (p->weights == FDIRW_W_MX8) {
-        if (p->v_far > 0) return fail(FDIRW_E_INVALID, "MX8 weights need a closed domain (v_far == 0)");
         if (p->flags & (FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_FP64))
             return fail(FDIRW_E_INVALID, "MX8 weights are not combined with NO_MASS_FIX, NO_DEDUP, SYMMETRIC_RULE or "
                                          "KGEN_FP64");
@@ -570,8 +569,11 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         int* class_pad = nullptr;
         void* class_w = nullptr;
         float* class_diag = nullptr;
+        double* class_mass = nullptr;  // MX8: each class kernel's own mass (N2 open windows < 1)
         DedupResult dr;
-        auto dfree = [&]() { cudaFree(class_pad); cudaFree(class_w); cudaFree(class_diag); cudaFree(dr.rep); };
+        auto dfree = [&]() {
+            cudaFree(class_pad); cudaFree(class_w); cudaFree(class_diag); cudaFree(class_mass); cudaFree(dr.rep);
+        };
         if ((st = alloc((void**)&class_pad, g.state_elems * 4, "class map")) != FDIRW_OK) { cudaFree(mask_d); return bail(st); }
         cudaError_t e = cudaMemsetAsync(class_pad, 0xff, g.state_elems * 4, s);
         DedupArgs da{mask_d, g.mz0, g.nx, g.ny, g.nz, g.R, g.sz0, g.sz1, g.z0, g.nxp, g.nyp, class_pad};
@@ -582,13 +584,16 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             dedup = false;  // hash collision detected by the exact check: take the direct path
         } else {
             if ((st = alloc(&class_w, (size_t)dr.n_class * g.K * c->b_w, "class kernels")) != FDIRW_OK ||
-                (st = alloc((void**)&class_diag, (size_t)dr.n_class * 4, "class diagonal")) != FDIRW_OK) {
+                (st = alloc((void**)&class_diag, (size_t)dr.n_class * 4, "class diagonal")) != FDIRW_OK ||
+                (c->fmt == FDIRW_W_MX8 &&
+                 (st = alloc((void**)&class_mass, (size_t)dr.n_class * 8, "class mass")) != FDIRW_OK)) {
                 dfree(); cudaFree(mask_d); return bail(st);
             }
             ka.src_list = dr.rep;
             ka.n_list = dr.n_class;
             ka.class_w = class_w;
             ka.class_diag = class_diag;
+            ka.class_mass = class_mass;
             if (e == cudaSuccess) e = cudaEventCreate(&c->kev[0]);
             if (e == cudaSuccess) e = cudaEventCreate(&c->kev[1]);
             if (e == cudaSuccess) e = cudaEventRecord(c->kev[0], s);
@@ -624,6 +629,8 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                 ea.Wt = c->Wt;
                 ea.diag = c->diag;
                 ea.nzl = g.nzl;
+                ea.class_mass = class_mass;
+                if (c->fmt == FDIRW_W_MX8 && c->compact) ea.far_pos = c->chunk_pos;
                 ea.z0 = g.z0;
                 ea.nz = g.nz;
                 tr.mark("compact + alloc weights");

@@ -82,6 +82,7 @@ struct KgenArgs {
     long n_list;
     void* class_w;
     float* class_diag;
+    double* class_mass = nullptr;  // MX8: each class kernel's own mass M (1 closed; < 1 open, N2)
 };
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s);
 
@@ -121,6 +122,8 @@ struct ExpandArgs {
     UniformTables* ut = nullptr;  // MX8 with N4 storage: the uniform tables (quantised in place)
     int nzl = 0;                  // MX8: slab planes (the diagonal pass walks every source)
     int z0 = 0, nz = 0;           // MX8: the slab's first global plane, the grid's planes
+    const double* class_mass = nullptr;  // MX8: M per class (diagonal = M − Σ off-centre)
+    const int* far_pos = nullptr;        // MX8 + N2 compaction: chunk_pos (≥ 0 compact, < 0 none)
 };
 cudaError_t launch_expand(const ExpandArgs& a, int R, int fmt, cudaStream_t s);
 // N4: per-chunk uniform class tables (see superpose.cu); arrays are cudaMalloc'ed

@@ -466,6 +466,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         const double off = block_sum_f64<S::NW>(qsum, red);
         if (t == R * L + R && a.class_w) {
             a.class_diag[it] = a.mass_fix ? (float)(M - off) : centre_q;
+            if (a.class_mass) a.class_mass[it] = M;
         } else if (t == R * L + R && sz >= a.z0 && sz < a.z1) {
             const float d = a.mass_fix ? (float)(M - off) : centre_q;
             const int zl = sz - a.z0;

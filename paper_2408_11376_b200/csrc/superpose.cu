@@ -984,7 +984,7 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
     const int nblk = a.t_end - a.t_begin - (a.gap_last ? 0 : a.gap_len);
     if (nblk <= 0) return cudaSuccess;
     if (fmt == FDIRW_W_MX8) {  // staged stream only (whole tiles), at any launch size
-        if (a.tile % 32 != 0 || a.tile > kBulkWarps * 32 || a.list) return cudaErrorInvalidValue;
+        if (a.tile % 32 != 0 || a.tile > kBulkWarps * 32) return cudaErrorInvalidValue;
         const size_t row = (size_t)(2 * R + 1) * a.tile * 9, half = (228 * 1024) / 2 - 1024 - 128;
         int S = (int)(half / row);
         if (S < 2) S = (int)((227 * 1024 - 128) / row);

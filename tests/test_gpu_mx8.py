@@ -310,3 +310,76 @@ def test_mx8_virtual_ranks_bitwise(fd, world):
     K = cfg.K
     for (a, b), W in zip(sl, Wr):
         np.testing.assert_array_equal(W[a:b, ..., K // 2], W1[a:b, ..., K // 2])  # diagonals
+
+
+def _open_mask(shape, seed):
+    m = fi.porous_particle(shape, min(shape) / 2 - 4, pore_r=(1.0, 2.0), porosity=0.3, seed=seed)
+    return fi.with_far_field(m, min(shape) / 2 - 4, margin=2.0)
+
+
+def test_mx8_far_vs_oracle(fd):
+    """MX8 with the N2 far-field reservoir (open windows keep their own mass M, so the diagonal
+    is M − Σ decoded off-centre weights; all-far chunks compacted away): 3 steps vs the exact
+    oracle (oracle/farfield.py), c_far, and the Eq.7 balance."""
+    import torch
+    from oracle import farfield as ff
+
+    shape = (14, 13, 15)
+    mask = _open_mask(shape, 4)
+    cfg = small_cfg(shape, 3, 300, D_slow=1e-3)
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=4).astype(np.float64)
+    V = 2000.0
+    refC, refcf, _ = ff.run_full(pb, c0, 0.5, V, 3)
+    ctx = fd.build_kernels(lib_params(cfg, "mx8", v_far=V), mask)
+    try:
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        M0 = fd.far_init(ctx, c, 0.5)
+        fd.run(ctx, c, 3)
+        cf = fd.far_get(ctx)
+        got = c.cpu().numpy().astype(np.float64)
+    finally:
+        fd.destroy(ctx)
+    nf = mask != 2
+    assert rel_l2(got[nf], refC[nf]) <= 5e-3
+    assert abs(cf - refcf) / refcf <= 1e-3
+    assert (got.sum() + cf * V - M0) / M0 == pytest.approx(0.0, abs=1e-9)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_mx8_far_virtual_ranks_bitwise(fd, world):
+    """MX8 + far field over slabs (no compaction there; Eq.7 from gathered tile sums): bitwise
+    the one-rank result (which compacts the all-far chunks)."""
+    import torch
+
+    shape = (12, 11, 13)
+    mask = _open_mask(shape, 8)
+    cfg = small_cfg(shape, 3, 60)
+    c0 = fi.initial_c(mask, "random", seed=8)
+    V = 777.0
+    ctx = fd.build_kernels(lib_params(cfg, "mx8", v_far=V), mask)
+    try:
+        cin = torch.from_numpy(c0).cuda()
+        out = torch.empty_like(cin)
+        fd.far_init(ctx, cin, 0.4)
+        fd.step(ctx, cin, out)
+        fd.step(ctx, out, cin)
+        one, cf1 = cin.cpu().numpy(), fd.far_get(ctx)
+    finally:
+        fd.destroy(ctx)
+    sl = fd.slabs(shape[0], world)
+    ctxs = [fd.build_kernels(lib_params(cfg, "mx8", v_far=V), mask, rank=r, world=world, z_begin=a, z_end=b,
+                             device=0) for r, (a, b) in enumerate(sl)]
+    try:
+        cin = [torch.from_numpy(c0[a:b].copy()).cuda() for a, b in sl]
+        cout = [torch.empty_like(t) for t in cin]
+        fd.far_init_virtual(ctxs, cin, 0.4)
+        fd.step_virtual(ctxs, cin, cout)
+        fd.step_virtual(ctxs, cout, cin)
+        got = np.concatenate([t.cpu().numpy() for t in cin], axis=0)
+        cfs = [fd.far_get(c) for c in ctxs]
+    finally:
+        for c in ctxs:
+            fd.destroy(c)
+    np.testing.assert_array_equal(got, one)
+    assert all(x == cf1 for x in cfs)

@@ -749,14 +749,20 @@ constexpr int mx8_rows(int R)
     return g < 1 ? 1 : g;
 }
 template <int R, int TT>
-__device__ __forceinline__ void mx8_body(const SuperArgs& a, int blk, int S, unsigned char* smem_b)
+__device__ __forceinline__ void mx8_body(const SuperArgs& a, int blk, int S, unsigned char* smem_b, int nsub = 1)
 {
+    // nsub > 1 (one-wave launches): the CTA takes part blk % nsub of tile blk / nsub, T chunks of
+    // the tile's Tf; its stage holds the part's runs of every slot in the same [n][T][8] +
+    // [n][T] layout (2 bulk copies per slot instead of 1 per row).  Same arithmetic per thread.
     constexpr int L = 2 * R + 1, K = L * L * L, NROW = L * L;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_b);
     uint64_t* empty = full + S;
     unsigned char* stg = smem_b + 128;
-    const int T = TT ? TT : a.tile;
-    const uint32_t slotB = (uint32_t)T * 9, stageB = (uint32_t)L * slotB;
+    const int Tf = a.tile;
+    const int T = TT ? TT : Tf / nsub;
+    const int part = blk % nsub;
+    blk /= nsub;
+    const uint32_t slotB = (uint32_t)T * 9, stageB = (uint32_t)L * slotB, slotBf = (uint32_t)Tf * 9;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = T >> 5;
     if (threadIdx.x == 0) {
@@ -768,21 +774,32 @@ __device__ __forceinline__ void mx8_body(const SuperArgs& a, int blk, int S, uns
     }
     __syncthreads();
     const bool producer = warp == nw;
-    const int e = producer ? 0 : (int)threadIdx.x;
+    const int e = part * T + (producer ? 0 : (int)threadIdx.x);
     TileCtx t = tile_ctx<R>(a, blk, e);
     float hi[8], lo[8];
     if (producer) {
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
-            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.Wt) + (size_t)t.tile * (K - 1) * slotB;
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.Wt) + (size_t)t.tile * (K - 1) * slotBf;
             int st = 0;
             uint32_t ph = 0;  // parity of the empty barrier to wait for (from the second lap)
             for (int i = 0; i < NROW; ++i) {
                 const int n = i == 0 ? L - 1 : L;
                 if (i >= S) mbar_wait(smem_u32(empty + st), ph);
                 mbar_expect_tx(smem_u32(full + st), (uint32_t)n * slotB);
-                bulk_g2s(smem_u32(stg + (size_t)st * stageB), src, (uint32_t)n * slotB, smem_u32(full + st), pol);
-                src += (size_t)n * slotB;
+                unsigned char* dst = stg + (size_t)st * stageB;
+                if (nsub == 1) {
+                    bulk_g2s(smem_u32(dst), src, (uint32_t)n * slotB, smem_u32(full + st), pol);
+                } else {
+                    for (int k = 0; k < n; ++k) {
+                        bulk_g2s(smem_u32(dst + (size_t)k * 8 * T), src + (size_t)k * 8 * Tf + (size_t)part * 8 * T,
+                                 (uint32_t)(8 * T), smem_u32(full + st), pol);
+                        bulk_g2s(smem_u32(dst + (size_t)n * 8 * T + (size_t)k * T),
+                                 src + (size_t)n * 8 * Tf + (size_t)k * Tf + (size_t)part * T, (uint32_t)T,
+                                 smem_u32(full + st), pol);
+                    }
+                }
+                src += (size_t)n * slotBf;
                 if (++st == S) {
                     st = 0;
                     if (i >= S) ph ^= 1u;
@@ -797,8 +814,8 @@ __device__ __forceinline__ void mx8_body(const SuperArgs& a, int blk, int S, uns
         float seg[24], p[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) p[j] = 0.f;
-        const unsigned char* m0 = stg + (size_t)e * 8;     // this thread's mantissas in stage 0
-        const unsigned char* s0 = stg + (size_t)8 * T + e;  // its scales (after n·8T bytes; n folded below)
+        const unsigned char* m0 = stg + (size_t)threadIdx.x * 8;     // this thread's mantissas in stage 0
+        const unsigned char* s0 = stg + (size_t)8 * T + threadIdx.x;  // its scales (after n·8T bytes; n folded below)
         int st = 0;
         uint32_t ph = 0;
         // row i = 0: the centre row; then (oz, oy) ascending without the centre (row_src order)
@@ -843,10 +860,10 @@ __device__ __forceinline__ void mx8_body(const SuperArgs& a, int blk, int S, uns
 }
 
 template <int R, int TT>
-__global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel(const SuperArgs a, int S)
+__global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel(const SuperArgs a, int S, int nsub)
 {
     extern __shared__ __align__(128) unsigned char smem_b[];
-    mx8_body<R, TT>(a, blockIdx.x, S, smem_b);
+    mx8_body<R, TT>(a, blockIdx.x, S, smem_b, nsub);
 }
 
 // MX8 uniform blocks: uniform_body's work with the MX8 body's summation grouping (the centre
@@ -995,12 +1012,21 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
         if (S == 3 && (long)3 * ((nblk + 443) / 444) < (long)2 * ((nblk + 295) / 296)) S = 2;
         if (const char* ev = getenv("FDIRW_MX8_STAGES")) S = atoi(ev);  // A/B of the stage count
         if (S < 2) return cudaErrorInvalidValue;
-        const size_t smem = 128 + (size_t)S * row;
-        const void* f = a.tile == 256 ? (const void*)superpose_mx8_kernel<R, 256> : (const void*)superpose_mx8_kernel<R, 0>;
+        // Tile split (FDIRW_MX8_NSUB = 2 / 4, A/B only): parts of a tile as separate CTAs, for
+        // one-wave launches.  Measured slower at cfg2 (128 tiles: whole 0.059 ms, auto-split
+        // into 256 CTAs 0.073 ms — 2 copies per slot and the runtime-width body cost more than
+        // the 20 idle SMs), so whole tiles stay the default.
+        int nsub = 1;
+        if (const char* ev = getenv("FDIRW_MX8_NSUB")) nsub = atoi(ev);
+        if (nsub < 1 || a.tile % nsub != 0 || (a.tile / nsub) % 32 != 0 || (nsub > 1 && a.tile_sum))
+            return cudaErrorInvalidValue;
+        const size_t smem = 128 + (size_t)S * (row / nsub);
+        const bool t256 = a.tile == 256 && nsub == 1;
+        const void* f = t256 ? (const void*)superpose_mx8_kernel<R, 256> : (const void*)superpose_mx8_kernel<R, 0>;
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        if (a.tile == 256) superpose_mx8_kernel<R, 256><<<nblk, a.tile + 32, smem, s>>>(a, S);
-        else superpose_mx8_kernel<R, 0><<<nblk, a.tile + 32, smem, s>>>(a, S);
+        if (t256) superpose_mx8_kernel<R, 256><<<nblk, a.tile + 32, smem, s>>>(a, S, 1);
+        else superpose_mx8_kernel<R, 0><<<nblk * nsub, a.tile / nsub + 32, smem, s>>>(a, S, nsub);
         return cudaGetLastError();
     }
     // a launch of fewer than two CTAs per SM cannot keep enough weight loads in flight

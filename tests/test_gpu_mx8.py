@@ -383,3 +383,28 @@ def test_mx8_far_virtual_ranks_bitwise(fd, world):
             fd.destroy(c)
     np.testing.assert_array_equal(got, one)
     assert all(x == cf1 for x in cfs)
+
+
+def test_mx8_tile_split_bitwise(fd, monkeypatch):
+    """One-wave launches split each tile into parts (2 bulk copies per slot per part); every
+    thread's arithmetic is unchanged, so any split gives the whole-tile bits."""
+    import torch
+
+    cfg = small_cfg((6, 32, 64), 3, 80, D_slow=1e-3)  # 256 chunks per plane: 6 tiles of 256
+    mask = fi.random_two_phase(cfg.shape, 0.6, seed=9)
+    c0 = torch.from_numpy(fi.initial_c(mask, "random", seed=9)).cuda()
+    outs = {}
+    for nsub in ("1", "2", "4", None):
+        if nsub is None:
+            monkeypatch.delenv("FDIRW_MX8_NSUB", raising=False)
+        else:
+            monkeypatch.setenv("FDIRW_MX8_NSUB", nsub)
+        ctx = fd.build_kernels(lib_params(cfg, "mx8"), mask)
+        try:
+            c = c0.clone()
+            fd.run(ctx, c, 3)
+            outs[nsub] = c.cpu().numpy()
+        finally:
+            fd.destroy(ctx)
+    for k in ("2", "4", None):
+        np.testing.assert_array_equal(outs[k], outs["1"])

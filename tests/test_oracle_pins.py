@@ -191,6 +191,7 @@ def test_exact_regime_equals_whole_grid_fd(oracle_lib):
         got = oracle_lib.step_full(pb, C, steps=3)
         ref = oracle_lib.fd_whole_grid(pb, C, 3 * n_fd)
         assert oracle_lib.rel_l2(got, ref) < 1e-14
+        np.testing.assert_allclose(got, ref, rtol=0, atol=1e-14)  # not resting on rel_l2 alone
 
 
 def test_window_covering_domain_equals_whole_grid_fd(oracle_lib):
@@ -201,6 +202,7 @@ def test_window_covering_domain_equals_whole_grid_fd(oracle_lib):
     got = oracle_lib.step_full(pb, C, steps=2)
     ref = oracle_lib.fd_whole_grid(pb, C, 120)
     assert oracle_lib.rel_l2(got, ref) < 1e-13
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-13)
 
 
 def test_fd_whole_grid_independent(oracle_lib):

@@ -127,16 +127,18 @@ typedef struct {
  * transport FDIRW_TRANSPORT_NCCL: nccl_id = 128 bytes produced by fdirw_nccl_unique_id on
  *   rank 0 and broadcast by the caller (e.g. torch.distributed); NULL = virtual ranks in
  *   one process (fdirw_step_virtual).  world == 1 needs no id.
- * transport FDIRW_TRANSPORT_P2P: no NCCL; the halo planes travel as peer-memory stores
- *   fused into the superposition (csrc/p2p.cu), after fdirw_p2p_attach /
- *   fdirw_p2p_attach_local.  Closed domain only (v_far == 0).                        */
+ * transport FDIRW_TRANSPORT_P2P: the halo planes travel as peer-memory stores fused into
+ *   the superposition (csrc/p2p.cu), after fdirw_p2p_attach / fdirw_p2p_attach_local; no
+ *   NCCL on the step path and nccl_id is ignored.  Closed domain only (v_far == 0).  The
+ *   whole-grid Σ of fdirw_mass needs a communicator: fdirw_comm_init (collective), called
+ *   once every rank's build succeeded.                                                 */
 #define FDIRW_TRANSPORT_NCCL 0
 #define FDIRW_TRANSPORT_P2P 1
 typedef struct {
     int32_t rank, world;
     int32_t z_begin, z_end;
     int32_t device;         /* CUDA device ordinal the context lives on                      */
-    const void* nccl_id;    /* NULL when world == 1 (or P2P transport)                       */
+    const void* nccl_id;    /* NULL when world == 1 (ignored with P2P, see fdirw_comm_init)  */
     int32_t transport;      /* FDIRW_TRANSPORT_NCCL (0) or FDIRW_TRANSPORT_P2P (1)           */
 } fdirw_dist;
 
@@ -206,15 +208,45 @@ fdirw_status fdirw_build_kernels(const fdirw_params* params, const uint8_t* phas
  * FDIRW_E_ALIAS.  Asynchronous on cuda_stream. */
 fdirw_status fdirw_step(fdirw_ctx* ctx, const float* c_in_dev, float* c_out_dev, void* cuda_stream);
 
+/* a5/a6 with HOST buffers (the end-to-end call): copies c_in_host (fp32 slab, host) to the
+ * device, runs fdirw_step, copies the result to c_out_host.  Everything is enqueued on
+ * cuda_stream and returns before it completes: c_out_host is valid after the stream is
+ * synchronised.  Page-locked (pinned) host buffers make the copies asynchronous; pageable
+ * ones work but the driver stages them.  The context keeps two device staging slabs,
+ * allocated on the first call.  c_in_host == c_out_host → FDIRW_E_ALIAS. */
+fdirw_status fdirw_step_host(fdirw_ctx* ctx, const float* c_in_host, float* c_out_host, void* cuda_stream);
+
 /* a7: n_steps FDiRW steps in place on c_dev (device fp32 slab), ping-ponging
  * inside the context's padded state and replayed from a CUDA graph.  n_steps
  * >= 0.  Asynchronous on cuda_stream. */
 fdirw_status fdirw_run(fdirw_ctx* ctx, float* c_dev, int32_t n_steps, void* cuda_stream);
 
 /* a7 diagnostics: Σ c over the WHOLE grid in fp64 (each rank sums its slab on
- * the device; an NCCL all-reduce combines ranks).  Synchronises cuda_stream and
- * writes the result to *out_host. */
+ * the device; an NCCL all-reduce combines ranks — every rank must call it).
+ * Synchronises cuda_stream and writes the result to *out_host.  A virtual rank
+ * (fdirw_step_virtual) returns its slab's Σ.  Errors: E_INVALID (NULL), E_STATE (a P2P
+ * context at world > 1 without fdirw_comm_init), E_NCCL, E_CUDA. */
 fdirw_status fdirw_mass(fdirw_ctx* ctx, const float* c_dev, double* out_host, void* cuda_stream);
+/* Tracing (the per-component breakdown of Fig.7): n_steps (1..256) steps
+ * on c_dev in place, enqueued eagerly (no CUDA graph) with CUDA events between the phases of
+ * every step; synchronises and writes the mean device milliseconds per step of
+ *   ms_out[0] halo   P2P: the neighbour-wait kernel; NCCL: the exchange on the comm stream
+ *   ms_out[1] interior superposition (P2P and world 1: the single launch over every tile,
+ *             boundary bands first; NCCL: the tiles that read no halo plane, overlapping [0])
+ *   ms_out[2] boundary superposition (NCCL: both bands after the exchange; else 0)
+ *   ms_out[3] tail   P2P: the epoch signal kernel; N2: the Eq.7 reduction; else ~0
+ *   ms_out[4] the whole step.
+ * Every rank must call it with the same n_steps.  E_STATE on the N3 study modes and the
+ * compacted / N4 storage paths (world 1), whose steps are several launches of other kinds. */
+fdirw_status fdirw_profile_phases(fdirw_ctx* ctx, float* c_dev, int32_t n_steps, void* cuda_stream, double* ms_out);
+/* P2P contexts (world > 1): open the NCCL communicator fdirw_mass uses for the whole-grid Σ.
+ * nccl_id: 128 bytes from fdirw_nccl_unique_id on rank 0, broadcast by the caller, not used
+ * for any other communicator.  Collective: every rank calls it (blocks until all have).
+ * Errors: E_INVALID (NULL), E_STATE (not a P2P context with world > 1, or already has one),
+ * E_NCCL. */
+fdirw_status fdirw_comm_init(fdirw_ctx* ctx, const void* nccl_id);
+/* The same Σ over this rank's slab only (no communication).  Synchronous. */
+fdirw_status fdirw_mass_local(fdirw_ctx* ctx, const float* c_dev, double* out_host, void* cuda_stream);
 
 /* Measurement aid (bench.py roofline.read_ceiling): streams the context's stored
  * weights `reps` times (after one warm-up pass) with the superposition's own load

@@ -60,6 +60,7 @@ def lib():
         L.oracle_kernel.argtypes = [P, D, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
         L.oracle_build_kernels.argtypes = [P, D, vp, vp, vp]
         L.oracle_step_scatter.argtypes = [P, vp, vp, vp, vp, vp]
+        L.oracle_step_scatter_omp.argtypes = [P, vp, vp, vp, vp, vp]
         L.oracle_quantize.argtypes = [P, vp, ctypes.c_long, ctypes.c_int, ctypes.c_int, vp, vp]
         L.oracle_fd_whole_grid.argtypes = [P, D, vp, vp, ctypes.c_int, ctypes.c_double, vp]
         L.oracle_f32_to_f16.argtypes = [ctypes.c_float]
@@ -193,8 +194,9 @@ def open_windows(pb: Problem, box=None) -> np.ndarray:
     return out
 
 
-def step_scatter(pb: Problem, W: np.ndarray, sbox, C_old: np.ndarray, tbox) -> np.ndarray:
-    """O4: targets in tbox from the sources in sbox (W from build_kernels(sbox))."""
+def step_scatter(pb: Problem, W: np.ndarray, sbox, C_old: np.ndarray, tbox, threads: bool = False) -> np.ndarray:
+    """O4: targets in tbox from the sources in sbox (W from build_kernels(sbox)).  threads=True:
+    the OpenMP form (target planes split between threads, same per-target order, same bits)."""
     C_old = np.ascontiguousarray(C_old, np.float64)
     assert C_old.shape == pb.shape
     sbox = clip_box(pb, sbox)
@@ -203,7 +205,8 @@ def step_scatter(pb: Problem, W: np.ndarray, sbox, C_old: np.ndarray, tbox) -> n
     assert W.shape[:3] == (sbox[5] - sbox[4], sbox[3] - sbox[2], sbox[1] - sbox[0])
     out = np.zeros((tbox[5] - tbox[4], tbox[3] - tbox[2], tbox[1] - tbox[0]), np.float64)
     sb, tb = np.array(sbox, np.int32), np.array(tbox, np.int32)
-    lib().oracle_step_scatter(ctypes.byref(pb._params()), _ptr(W), _ptr(sb), _ptr(C_old), _ptr(tb), _ptr(out))
+    fn = lib().oracle_step_scatter_omp if threads else lib().oracle_step_scatter
+    fn(ctypes.byref(pb._params()), _ptr(W), _ptr(sb), _ptr(C_old), _ptr(tb), _ptr(out))
     return out
 
 

@@ -220,6 +220,39 @@ void oracle_step_scatter(const oracle_params* p, const double* W, const int32_t*
     (void)sbz;
 }
 
+/* O4 with OpenMP, for timing on all host cores: the same scatter, the target
+ * planes split between threads; each thread walks ALL sources in ascending order and adds
+ * only into its own planes, so every target receives its terms in exactly the sequential
+ * order above (bitwise the same result, pinned in tests/test_oracle_pins.py). */
+void oracle_step_scatter_omp(const oracle_params* p, const double* W, const int32_t* sbox,
+                             const double* Cold, const int32_t* tbox, double* Cout)
+{
+    const int R = p->R, L = 2 * R + 1, K = L * L * L;
+    const int sbx = sbox[1] - sbox[0], sby = sbox[3] - sbox[2];
+    const int tbx = tbox[1] - tbox[0], tby = tbox[3] - tbox[2], tbz = tbox[5] - tbox[4];
+    memset(Cout, 0, sizeof(double) * (size_t)tbx * tby * tbz);
+#pragma omp parallel for schedule(static, 1)
+    for (int tz = tbox[4]; tz < tbox[5]; ++tz)
+        for (int sz = sbox[4]; sz < sbox[5]; ++sz) {
+            if (tz - sz < -R || tz - sz > R) continue;
+            const int oz = tz - sz;
+            for (int sy = sbox[2]; sy < sbox[3]; ++sy)
+                for (int sx = sbox[0]; sx < sbox[1]; ++sx) {
+                    size_t n = ((size_t)(sz - sbox[4]) * sby + (sy - sbox[2])) * sbx + (sx - sbox[0]);
+                    const double* Ws = W + n * K;
+                    double cs = Cold[((size_t)sz * p->ny + sy) * p->nx + sx];
+                    for (int oy = -R; oy <= R; ++oy)
+                        for (int ox = -R; ox <= R; ++ox) {
+                            int x = sx + ox, y = sy + oy;
+                            if (x < tbox[0] || x >= tbox[1] || y < tbox[2] || y >= tbox[3]) continue;
+                            int o = ((oz + R) * L + (oy + R)) * L + (ox + R);
+                            Cout[((size_t)(tz - tbox[4]) * tby + (y - tbox[2])) * tbx + (x - tbox[0])] +=
+                                Ws[o] * cs;
+                        }
+                }
+        }
+}
+
 /* ---------------------------------------------------------------------------
  * a4 (oracle form O5). Reduced-precision weight storage (§3.3: "The
  * coefficient matrix P is stored in FP16 precision"; reading A9: weights only,

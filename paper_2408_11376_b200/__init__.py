@@ -44,7 +44,8 @@ EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fd
            "fdirw_far_init", "fdirw_far_init_virtual", "fdirw_far_get", "fdirw_absorb_run",
            "fdirw_set_precision_mode", "fdirw_coarse_far_init", "fdirw_coarse_far_get",
            "fdirw_coarse_export_pbc", "fdirw_p2p_export", "fdirw_p2p_attach", "fdirw_p2p_attach_local",
-           "fdirw_p2p_check", "fdirw_read_ceiling"]
+           "fdirw_p2p_check", "fdirw_read_ceiling", "fdirw_mass_local", "fdirw_profile_phases",
+           "fdirw_comm_init", "fdirw_step_host"]
 TRANSPORTS = {"nccl": 0, "p2p": 1}
 P2P_BLOB_BYTES = 256
 
@@ -104,6 +105,14 @@ _lib.fdirw_run.argtypes = [_vp, _vp, ctypes.c_int32, _vp]
 _lib.fdirw_run.restype = _st
 _lib.fdirw_mass.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_double), _vp]
 _lib.fdirw_mass.restype = _st
+_lib.fdirw_step_host.argtypes = [_vp, _vp, _vp, _vp]
+_lib.fdirw_step_host.restype = _st
+_lib.fdirw_comm_init.argtypes = [_vp, _vp]
+_lib.fdirw_comm_init.restype = _st
+_lib.fdirw_mass_local.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_double), _vp]
+_lib.fdirw_mass_local.restype = _st
+_lib.fdirw_profile_phases.argtypes = [_vp, _vp, ctypes.c_int32, _vp, ctypes.POINTER(ctypes.c_double)]
+_lib.fdirw_profile_phases.restype = _st
 _lib.fdirw_read_ceiling.argtypes = [_vp, ctypes.c_int32, _vp, ctypes.POINTER(ctypes.c_double)]
 _lib.fdirw_read_ceiling.restype = _st
 _lib.fdirw_query.argtypes = [_vp, ctypes.POINTER(fdirw_info)]
@@ -195,6 +204,17 @@ def _dptr(t):
     """Device pointer of a contiguous fp32 CUDA tensor."""
     if not (t.is_cuda and t.is_contiguous() and str(t.dtype) == "torch.float32"):
         raise ValueError("expected a contiguous float32 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(t):
+    """Host pointer of a contiguous fp32 CPU tensor (pinned for asynchronous copies) or ndarray."""
+    if isinstance(t, np.ndarray):
+        if not (t.flags["C_CONTIGUOUS"] and t.dtype == np.float32):
+            raise ValueError("expected a contiguous float32 array")
+        return ctypes.c_void_p(t.ctypes.data)
+    if t.is_cuda or not t.is_contiguous() or str(t.dtype) != "torch.float32":
+        raise ValueError("expected a contiguous float32 CPU tensor")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -311,6 +331,12 @@ def step(ctx: Context, c_in, c_out, stream=None):
     _check(_lib.fdirw_step(ctx.handle, _dptr(c_in), _dptr(c_out), _stream(stream)))
 
 
+def step_host(ctx: Context, c_in_host, c_out_host, stream=None):
+    """fdirw_step_host: host (pinned CPU tensor) slab in → step on the device → host slab out;
+    asynchronous on the stream."""
+    _check(_lib.fdirw_step_host(ctx.handle, _hptr(c_in_host), _hptr(c_out_host), _stream(stream)))
+
+
 def run(ctx: Context, c, n_steps: int, stream=None):
     _check(_lib.fdirw_run(ctx.handle, _dptr(c), int(n_steps), _stream(stream)))
 
@@ -319,6 +345,30 @@ def mass(ctx: Context, c, stream=None) -> float:
     out = ctypes.c_double()
     _check(_lib.fdirw_mass(ctx.handle, _dptr(c), ctypes.byref(out), _stream(stream)))
     return out.value
+
+
+def comm_init(ctx: Context, nccl_id: bytes):
+    """fdirw_comm_init: the NCCL communicator of a P2P context (collective; for fdirw_mass)."""
+    idbuf = ctypes.create_string_buffer(nccl_id, 128)
+    _check(_lib.fdirw_comm_init(ctx.handle, idbuf))
+
+
+def mass_local(ctx: Context, c, stream=None) -> float:
+    """Σ c over this rank's slab (fdirw_mass_local)."""
+    out = ctypes.c_double()
+    _check(_lib.fdirw_mass_local(ctx.handle, _dptr(c), ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+PHASES = ("halo", "interior", "boundary", "tail", "step")
+
+
+def profile_phases(ctx: Context, c, n_steps: int, stream=None) -> dict:
+    """fdirw_profile_phases: mean device ms per step of each phase (halo, interior, boundary,
+    tail, whole step), n_steps eager steps on c in place."""
+    out = (ctypes.c_double * 5)()
+    _check(_lib.fdirw_profile_phases(ctx.handle, _dptr(c), int(n_steps), _stream(stream), out))
+    return dict(zip(PHASES, list(out)))
 
 
 def read_ceiling(ctx: Context, reps: int = 5, stream=None) -> float:

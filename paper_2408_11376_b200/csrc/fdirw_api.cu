@@ -87,6 +87,8 @@ struct fdirw_ctx {
     int nzl_lo = 0;
     bool p2p_ready = false;
     std::vector<void*> ipc_opened;
+    // fdirw_step_host: device staging of the caller's host slab (allocated on first use)
+    float* host_stage[2] = {nullptr, nullptr};
 };
 
 static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s);
@@ -307,6 +309,14 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
         if (mx == 2 && !(p->v_far > 0)) return fail(FDIRW_E_INVALID, "far-field voxels (2) need v_far > 0");
     }
     if ((long long)p->nx * p->ny * p->nz > (1LL << 40)) return fail(FDIRW_E_INVALID, "grid too large");
+    {   // the window dedup (CUB sorts/scans, int source ids) and the N3 loop index the voxels of
+        // one rank's mask planes [z_begin − 2R, z_end + 2R) with 32-bit ints
+        const int zb = dist ? dist->z_begin : 0, ze = dist ? dist->z_end : p->nz;
+        const long long planes = (long long)std::min(p->nz, ze + 2 * p->radius) - std::max(0, zb - 2 * p->radius);
+        if ((long long)p->nx * p->ny * planes >= (1LL << 31))
+            return fail(FDIRW_E_INVALID, "slab too large: nx*ny*(mask planes of the slab) must be < 2^31 voxels "
+                                         "(split the grid over more ranks)");
+    }
     if (dist) {
         if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
             return fail(FDIRW_E_INVALID, "bad rank/world");
@@ -345,6 +355,8 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->diag);
     cudaFree(c->cpad[0]);
     cudaFree(c->cpad[1]);
+    cudaFree(c->host_stage[0]);
+    cudaFree(c->host_stage[1]);
     cudaFree(c->mass_partial);
     cudaFree(c->mass_out);
     cudaFree(c->farmask);
@@ -485,6 +497,13 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
                          !(params->flags & FDIRW_F_DEDUP_STORAGE) && !(params->v_far > 0) &&
                              params->weights != FDIRW_W_MX8);  // MX8: tile 256, waves via stages
     const Geometry& g = c->g;
+    if (params->weights == FDIRW_W_MX8 && (params->flags & FDIRW_F_DEDUP_STORAGE) && g.tile != 256) {
+        // the small-tile N4 path sums uniform chunks with the bf16 body's grouping, not the MX8
+        // body's: the field would no longer be bitwise the dense MX8 field
+        delete c;
+        return fail(FDIRW_E_INVALID, "MX8 weights with FDIRW_F_DEDUP_STORAGE need planes of >= 256 x-chunks "
+                                     "(ny * ceil(nx/8) >= 256)");
+    }
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     tr.s = s;
 
@@ -882,11 +901,22 @@ static void split_tiles(const Geometry& g, int* int0, int* int1)
     *int1 = (g.nzl - g.R) * g.tpp;
 }
 
+// Phase events of one step (fdirw_profile_phases; null on the normal path).  Recorded on the
+// compute stream unless noted: t0 start, halo0/halo1 the halo phase (P2P: the wait kernel;
+// NCCL: the exchange, both on the comm stream), sup the interior (or only) superposition done,
+// bnd0/bnd1 the boundary-band launch (NCCL), t1 the end of the step (P2P signal / Eq.7 done).
+struct PhaseEv {
+    cudaEvent_t t0, halo0, halo1, sup, bnd0, bnd1, t1;
+};
+#define PHASE(field, stream) \
+    do { if (pe) CUDA_TRY(cudaEventRecord(pe->field, stream)); } while (0)
+
 // One step src (padded, slab planes filled) → out; exchanges the halo planes of src first.
 static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, long rs, cudaStream_t s,
-                                 int dst_parity = 1)
+                                 int dst_parity = 1, PhaseEv* pe = nullptr)
 {
     const Geometry& g = c->g;
+    PHASE(t0, s);
     if (c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) {
         // wait for the neighbours' previous step (their stores into my halo are complete and
         // they are done reading the halo I overwrite) → ONE launch over every tile, boundary
@@ -895,14 +925,22 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
         // launch keeps the SMs evenly loaded at strong-scaling slab sizes.)
         int i0, i1;
         split_tiles(g, &i0, &i1);
+        PHASE(halo0, s);
         CUDA_TRY(p2p_wait(c->p2p_flags, c->peer_lo_flag != nullptr, c->peer_hi_flag != nullptr, s));
+        PHASE(halo1, s);
         if (i1 > i0)
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity, i0, i1, true));
         else
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, dst_parity));
+        PHASE(sup, s);
+        PHASE(bnd0, s);
+        PHASE(bnd1, s);
         CUDA_TRY(p2p_signal(c->p2p_flags, c->peer_lo_flag, c->peer_hi_flag, s));
+        PHASE(t1, s);
         return FDIRW_OK;
     }
+    if (pe && c->world == 1 && (c->prec_mode != 0 || c->ut.chunk_u || c->compact))
+        return fail(FDIRW_E_STATE, "phase profile: the dense superposition path only");
     if (c->world == 1 && c->prec_mode != 0) {  // N3 §3.3 study modes: padded output only
         StudyArgs a{src, out - ((size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX), c->Wt, c->diag,
                     g.nx, g.ny, g.nzl, g.nxq, g.tile, g.tpp, g.nxp, g.nyp, g.R, c->pbc, c->far_state,
@@ -937,26 +975,41 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
             else CUDA_TRY(launch_tile_mass(out, c->farmask, g, c->tile_buf + 1, s));
             return far_reduce(c, s, 0, 0.0);
         }
+        PHASE(halo0, s);
+        PHASE(halo1, s);
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
-        return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
+        PHASE(sup, s);
+        PHASE(bnd0, s);
+        PHASE(bnd1, s);
+        fdirw_status st = c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
+        PHASE(t1, s);
+        return st;
     }
     int i0, i1;
     split_tiles(g, &i0, &i1);
     CUDA_TRY(cudaEventRecord(c->ev_fork, s));
     CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
     std::string err;
+    PHASE(halo0, c->comm_stream);
     if (nccl_halo(c->nccl, c->comm, src, make_halo_plan(g, c->rank, c->world), c->comm_stream, &err))
         return fail(FDIRW_E_NCCL, err);
+    PHASE(halo1, c->comm_stream);
     CUDA_TRY(cudaEventRecord(c->ev_comm, c->comm_stream));
     CUDA_TRY(superpose(c, src, out, ps, rs, i0, i1, s));  // interior overlaps the exchange
+    PHASE(sup, s);
     CUDA_TRY(cudaStreamWaitEvent(s, c->ev_comm, 0));
+    PHASE(bnd0, s);
     if (i1 > i0) {  // both boundary bands in one launch
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s, true, -1, i0, i1));
     } else {
         CUDA_TRY(superpose(c, src, out, ps, rs, 0, g.n_tiles, s));
     }
-    return c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
+    PHASE(bnd1, s);
+    fdirw_status st = c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
+    PHASE(t1, s);
+    return st;
 }
+#undef PHASE
 
 // P2P run start (after the pack into cpad[0]): signal "packed", wait for the neighbours'
 // (so nobody still reads the halo of cpad[0]), push our edge planes into their halos, signal.
@@ -993,6 +1046,26 @@ extern "C" fdirw_status fdirw_step(fdirw_ctx* c, const float* c_in, float* c_out
         if (st != FDIRW_OK) return st;
     }
     return enqueue_step(c, c->cpad[0], c_out, (long)g.nx * g.ny, g.nx, s, 1);
+}
+
+extern "C" fdirw_status fdirw_step_host(fdirw_ctx* c, const float* c_in_host, float* c_out_host, void* cuda_stream)
+{
+    if (!c || !c_in_host || !c_out_host) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (c_in_host == c_out_host) return fail(FDIRW_E_ALIAS, "c_in == c_out");
+    if (c->is_virtual) return fail(FDIRW_E_STATE, "virtual-rank context: use fdirw_step_virtual");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const size_t bytes = (size_t)c->g.nx * c->g.ny * c->g.nzl * 4;
+    for (int i = 0; i < 2; ++i)
+        if (!c->host_stage[i]) {
+            fdirw_status st = alloc((void**)&c->host_stage[i], bytes, "host staging");
+            if (st != FDIRW_OK) return st;
+        }
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    CUDA_TRY(cudaMemcpyAsync(c->host_stage[0], c_in_host, bytes, cudaMemcpyHostToDevice, s));
+    fdirw_status st = fdirw_step(c, c->host_stage[0], c->host_stage[1], cuda_stream);
+    if (st != FDIRW_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(c_out_host, c->host_stage[1], bytes, cudaMemcpyDeviceToHost, s));
+    return FDIRW_OK;
 }
 
 // capture step(0→1); step(1→0) once; fdirw_run replays it n/2 times.  With P2P this is done
@@ -1049,6 +1122,68 @@ extern "C" fdirw_status fdirw_run(fdirw_ctx* c, float* c_dev, int32_t n_steps, v
     return FDIRW_OK;
 }
 
+extern "C" fdirw_status fdirw_profile_phases(fdirw_ctx* c, float* c_dev, int32_t n_steps, void* cuda_stream,
+                                            double* ms_out)
+{
+    if (!c || !c_dev || !ms_out) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (n_steps < 1 || n_steps > 256) return fail(FDIRW_E_INVALID, "n_steps must be in [1, 256]");
+    if (c->is_virtual) return fail(FDIRW_E_STATE, "virtual-rank context: use fdirw_step_virtual");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const Geometry& g = c->g;
+    std::vector<PhaseEv> ev(n_steps);
+    cudaError_t e = cudaSuccess;
+    int made = 0;
+    for (; made < n_steps && e == cudaSuccess; ++made) {
+        cudaEvent_t* f[7] = {&ev[made].t0, &ev[made].halo0, &ev[made].halo1, &ev[made].sup, &ev[made].bnd0,
+                             &ev[made].bnd1, &ev[made].t1};
+        for (int k = 0; k < 7 && e == cudaSuccess; ++k) e = cudaEventCreate(f[k]);
+    }
+    auto release = [&]() {
+        for (int i = 0; i < made; ++i) {
+            cudaEvent_t f[7] = {ev[i].t0, ev[i].halo0, ev[i].halo1, ev[i].sup, ev[i].bnd0, ev[i].bnd1, ev[i].t1};
+            for (cudaEvent_t x : f)
+                if (x) cudaEventDestroy(x);
+        }
+    };
+    fdirw_status st = FDIRW_OK;
+    if (e != cudaSuccess) st = fail(FDIRW_E_CUDA, std::string("phase events: ") + cudaGetErrorString(e));
+    if (st == FDIRW_OK && (e = launch_pack(c_dev, c->cpad[0], g, s, c->farmask)) != cudaSuccess)
+        st = fail(FDIRW_E_CUDA, cudaGetErrorString(e));
+    if (st == FDIRW_OK && c->world > 1 && c->transport == FDIRW_TRANSPORT_P2P) st = p2p_start(c, s);
+    const long ps = (long)g.plane_elems, rs = g.nxp;
+    int cur = 0;
+    for (int i = 0; i < n_steps && st == FDIRW_OK; ++i) {
+        st = enqueue_step(c, c->cpad[cur], pad_interior(c, 1 - cur), ps, rs, s, 1 - cur, &ev[i]);
+        cur = 1 - cur;
+    }
+    if (st == FDIRW_OK && (e = launch_unpack(c->cpad[cur], c_dev, g, s)) != cudaSuccess)
+        st = fail(FDIRW_E_CUDA, cudaGetErrorString(e));
+    if (st == FDIRW_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess)
+        st = fail(FDIRW_E_CUDA, cudaGetErrorString(e));
+    if (st == FDIRW_OK && (e = cudaStreamSynchronize(c->comm_stream)) != cudaSuccess)
+        st = fail(FDIRW_E_CUDA, cudaGetErrorString(e));
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (int i = 0; i < n_steps && st == FDIRW_OK; ++i) {
+        float t[5] = {0, 0, 0, 0, 0};
+        const PhaseEv& p = ev[i];
+        // NCCL: the interior runs on the compute stream from t0 while the exchange runs on the
+        // comm stream; elsewhere it follows the halo phase
+        const cudaEvent_t int0 = (c->world > 1 && c->transport == FDIRW_TRANSPORT_NCCL) ? p.t0 : p.halo1;
+        e = cudaEventElapsedTime(&t[0], p.halo0, p.halo1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t[1], int0, p.sup);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t[2], p.bnd0, p.bnd1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t[3], p.bnd1, p.t1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t[4], p.t0, p.t1);
+        if (e != cudaSuccess) st = fail(FDIRW_E_CUDA, std::string("phase times: ") + cudaGetErrorString(e));
+        for (int k = 0; k < 5; ++k) acc[k] += t[k];
+    }
+    release();
+    if (st != FDIRW_OK) return st;
+    for (int k = 0; k < 5; ++k) ms_out[k] = acc[k] / n_steps;
+    return FDIRW_OK;
+}
+
 extern "C" fdirw_status fdirw_mass(fdirw_ctx* c, const float* c_dev, double* out_host, void* cuda_stream)
 {
     if (!c || !c_dev || !out_host) return fail(FDIRW_E_INVALID, "NULL argument");
@@ -1056,10 +1191,43 @@ extern "C" fdirw_status fdirw_mass(fdirw_ctx* c, const float* c_dev, double* out
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const size_t n = (size_t)c->g.nx * c->g.ny * c->g.nzl;
     CUDA_TRY(launch_mass(c_dev, n, c->mass_partial, c->mass_blocks, c->mass_out, s));
-    if (c->world > 1 && !c->is_virtual && c->transport == FDIRW_TRANSPORT_NCCL) {
+    if (c->world > 1 && !c->is_virtual) {
+        if (!c->comm)
+            return fail(FDIRW_E_STATE, "fdirw_mass on a P2P rank without a communicator: call fdirw_comm_init "
+                                       "first, or use fdirw_mass_local");
         std::string err;
         if (nccl_allreduce_sum_f64(c->nccl, c->comm, c->mass_out, s, &err)) return fail(FDIRW_E_NCCL, err);
     }
+    CUDA_TRY(cudaMemcpyAsync(out_host, c->mass_out, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_comm_init(fdirw_ctx* c, const void* nccl_id)
+{
+    if (!c || !nccl_id) return fail(FDIRW_E_INVALID, "NULL argument");
+    if (c->transport != FDIRW_TRANSPORT_P2P || c->world < 2)
+        return fail(FDIRW_E_STATE, "fdirw_comm_init: a P2P context with world > 1 only (NCCL contexts own one)");
+    if (c->comm) return fail(FDIRW_E_STATE, "fdirw_comm_init: the context already has a communicator");
+    CUDA_TRY(cudaSetDevice(c->device));
+    std::string err;
+    if (!c->nccl) c->nccl = nccl_load(&err);
+    if (!c->nccl) return fail(FDIRW_E_NCCL, err);
+    c->comm = nccl_comm_init(c->nccl, c->world, c->rank, nccl_id, &err);
+    if (!c->comm) return fail(FDIRW_E_NCCL, err);
+    // connect now, outside any later stream capture
+    if (nccl_allreduce_sum_f64(c->nccl, c->comm, c->mass_out, c->comm_stream, &err)) return fail(FDIRW_E_NCCL, err);
+    CUDA_TRY(cudaStreamSynchronize(c->comm_stream));
+    return FDIRW_OK;
+}
+
+extern "C" fdirw_status fdirw_mass_local(fdirw_ctx* c, const float* c_dev, double* out_host, void* cuda_stream)
+{
+    if (!c || !c_dev || !out_host) return fail(FDIRW_E_INVALID, "NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const size_t n = (size_t)c->g.nx * c->g.ny * c->g.nzl;
+    CUDA_TRY(launch_mass(c_dev, n, c->mass_partial, c->mass_blocks, c->mass_out, s));
     CUDA_TRY(cudaMemcpyAsync(out_host, c->mass_out, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return FDIRW_OK;

@@ -1011,7 +1011,7 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
         // e.g. a 24-plane slab (432 tiles) fits one wave of 444 instead of 1.5 of 296
         if (S == 3 && (long)3 * ((nblk + 443) / 444) < (long)2 * ((nblk + 295) / 296)) S = 2;
         if (const char* ev = getenv("FDIRW_MX8_STAGES")) S = atoi(ev);  // A/B of the stage count
-        if (S < 2) return cudaErrorInvalidValue;
+        if (S < 2 || S > 8) return cudaErrorInvalidValue;  // the 128-byte barrier header holds 8 + 8
         // Tile split (FDIRW_MX8_NSUB = 2 / 4, A/B only): parts of a tile as separate CTAs, for
         // one-wave launches.  Measured slower at cfg2 (128 tiles: whole 0.059 ms, auto-split
         // into 256 CTAs 0.073 ms — 2 copies per slot and the runtime-width body cost more than
@@ -1100,7 +1100,7 @@ static cudaError_t launch_mixed_r(const SuperArgs& a, const UniArgs& u, int fmt,
         if (S < 2) S = (int)((227 * 1024 - 128) / row);
         if (S > 3) S = 3;
         if (const char* ev = getenv("FDIRW_MX8_STAGES")) S = atoi(ev);  // A/B of the stage count
-        if (S < 2) return cudaErrorInvalidValue;
+        if (S < 2 || S > 8) return cudaErrorInvalidValue;  // the 128-byte barrier header holds 8 + 8
         size_t smem = 128 + (size_t)S * row;
         const size_t need = 128 + (size_t)((2 * R + 1) * (2 * R + 1) * (2 * R + 1) - 1) * 4;  // uniform kernel
         if (smem < need) smem = need;

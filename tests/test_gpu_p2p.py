@@ -71,6 +71,12 @@ def test_p2p_local_ranks_bitwise(fd, world, steps, R, shape):
         torch.cuda.synchronize()
         assert not any(fd.p2p_check(ctx) for ctx in ctxs)
         got = np.concatenate([c.cpu().numpy() for c in cs], axis=0)
+        # no communicator (built without nccl_id): the whole-grid Σ is refused, the slab Σ is not
+        with pytest.raises(fd.FdirwError) as e:
+            fd.mass(ctxs[0], cs[0])
+        assert e.value.status == fd.E_STATE
+        tot = sum(fd.mass_local(ctx, c) for ctx, c in zip(ctxs, cs))
+        assert abs(tot - got.astype(np.float64).sum()) <= 1e-9 * abs(tot)
         # fdirw_step (user buffers) on the same contexts: one more step from the result
         outs = [torch.empty_like(c) for c in cs]
         for ctx, c, o, st in zip(ctxs, cs, outs, streams):

@@ -343,3 +343,17 @@ def test_box_step_equals_full_step(oracle_lib):
     for tb in [(0, 4, 0, 5, 0, 3), (3, 10, 2, 9, 4, 12), (6, 10, 8, 11, 9, 12)]:
         part = oracle_lib.step_box(pb, C, tb)
         np.testing.assert_allclose(part, full[tb[4]:tb[5], tb[2]:tb[3], tb[0]:tb[1]], rtol=0, atol=1e-15)
+
+
+def test_scatter_openmp_bitwise(oracle_lib):
+    """The OpenMP scatter (timing form) adds each target's terms in the sequential
+    order: bitwise the sequential O4, on a box with clipped sources and on the full grid."""
+    mask = fi.porous_particle((14, 12, 13), 4, pore_r=(1, 1.5), n_pores=3, seed=6)
+    pb = lat(mask, 2, 40, D_slow=1e-3)
+    C = fi.initial_c(mask, "random", seed=6).astype(np.float64)
+    for tb in [(0, 13, 0, 12, 0, 14), (3, 11, 2, 6, 5, 9)]:
+        sb = oracle_lib.clip_box(pb, (tb[0] - 2, tb[1] + 2, tb[2] - 2, tb[3] + 2, tb[4] - 2, tb[5] + 2))
+        W = oracle_lib.build_kernels(pb, sb)
+        a = oracle_lib.step_scatter(pb, W, sb, C, tb)
+        b = oracle_lib.step_scatter(pb, W, sb, C, tb, threads=True)
+        np.testing.assert_array_equal(a, b)

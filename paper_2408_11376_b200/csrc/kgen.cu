@@ -136,6 +136,12 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
     const int cx = t % L, cy = t / L;
     const int oxm = (col && cx > 0) ? -1 : 0, oxp = (col && cx < L - 1) ? 1 : 0;
     const int oym = (col && cy > 0) ? -L : 0, oyp = (col && cy < L - 1) ? L : 0;
+    // smem read offsets of the ±x neighbours: a column on the window's x edge has no neighbour
+    // there (face number 0), but reading its own slot would leave a hole in the warp's run of
+    // consecutive float4s at every row boundary, which splits an 8-lane LDS.128 phase over two
+    // bank rounds (ncu: 5.4 % of the shared wavefronts were conflicts).  It reads the adjacent
+    // row's edge column instead (a written, finite window value; 0·(v − c) adds ±0).
+    const int axm = (col && (cx > 0 || t > 0)) ? -1 : 0, axp = (col && (cx < L - 1 || t + 1 < LL)) ? 1 : 0;
     const int nx = a.nx, ny = a.ny, nz = a.nz;
     const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
@@ -279,8 +285,8 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         // c_{z−1} − c_z is exactly −(c_z − c_{z−1}) in IEEE arithmetic).
         auto flux = [&](const float* b, const float (&cur)[Lp], float (&nw)[Lp]) {
             float xm[L], xp[L], ym[L], yp[L];
-            load_col(b, t + oxm, xm);
-            load_col(b, t + oxp, xp);
+            load_col(b, t + axm, xm);
+            load_col(b, t + axp, xp);
             load_col(b, t + oym, ym);
             load_col(b, t + oyp, yp);
             // z faces from registers: for R ≤ 5 before the lateral faces, so they run while the

@@ -306,6 +306,10 @@ void fdirw_destroy(fdirw_ctx* ctx);
 /* Thread-local message of the last non-OK status on this thread ("" if none). */
 const char* fdirw_last_error(void);
 
+/* The sha256 of the sources, headers, build flags and nvcc version this library was compiled
+ * from (paper_2408_11376_b200/build.py); static string, never NULL. */
+const char* fdirw_build_id(void);
+
 /* ---- test support ------------------------------------------------------------
  * Replace the weights of a world == 1 context by caller-supplied per-source
  * kernels (host fp64, [nz][ny][nx][K], slot o = ((oz+R)·L+(oy+R))·L+(ox+R),
@@ -321,6 +325,15 @@ fdirw_status fdirw_debug_upload_weights(fdirw_ctx* ctx, const double* kernels_ho
  * Slots whose target lies outside this context's slab or the domain read 0.
  * Synchronous. */
 fdirw_status fdirw_export_kernels(const fdirw_ctx* ctx, const int32_t* box, double* kernels_host);
+
+/* Test support for the TMA-staged weight stream (compute-sanitizer racecheck does not
+ * model the mbarrier complete_tx ordering of cp.async.bulk): enable != 0 makes every later
+ * superposition launch of ctx re-read each weight a compute thread takes from a shared-memory
+ * stage twice — after the stage's full barrier and again just before its warp releases the
+ * stage to the producer — and compare both with the global copy.  Returns the 16-byte words
+ * checked and the mismatches so far (a late copy or a premature refill shows as mismatches).
+ * Synchronous.  Slows the step; never enable it in production. */
+fdirw_status fdirw_debug_stage_canary(fdirw_ctx* ctx, int32_t enable, uint64_t* checks, uint64_t* mismatches);
 
 /* Single-process "virtual ranks": n contexts built on ONE device with
  * dist = {r, n, slab_r, device, NULL} and flag-free params, stepped together

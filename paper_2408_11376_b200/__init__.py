@@ -45,7 +45,8 @@ EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fd
            "fdirw_set_precision_mode", "fdirw_coarse_far_init", "fdirw_coarse_far_get",
            "fdirw_coarse_export_pbc", "fdirw_p2p_export", "fdirw_p2p_attach", "fdirw_p2p_attach_local",
            "fdirw_p2p_check", "fdirw_read_ceiling", "fdirw_mass_local", "fdirw_profile_phases",
-           "fdirw_comm_init", "fdirw_step_host"]
+           "fdirw_comm_init", "fdirw_step_host", "fdirw_debug_stage_canary",
+           "fdirw_build_id"]
 TRANSPORTS = {"nccl": 0, "p2p": 1}
 P2P_BLOB_BYTES = 256
 
@@ -105,6 +106,11 @@ _lib.fdirw_run.argtypes = [_vp, _vp, ctypes.c_int32, _vp]
 _lib.fdirw_run.restype = _st
 _lib.fdirw_mass.argtypes = [_vp, _vp, ctypes.POINTER(ctypes.c_double), _vp]
 _lib.fdirw_mass.restype = _st
+_lib.fdirw_build_id.argtypes = []
+_lib.fdirw_build_id.restype = ctypes.c_char_p
+_lib.fdirw_debug_stage_canary.argtypes = [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64),
+                                          ctypes.POINTER(ctypes.c_uint64)]
+_lib.fdirw_debug_stage_canary.restype = _st
 _lib.fdirw_step_host.argtypes = [_vp, _vp, _vp, _vp]
 _lib.fdirw_step_host.restype = _st
 _lib.fdirw_comm_init.argtypes = [_vp, _vp]
@@ -179,6 +185,11 @@ class FdirwError(RuntimeError):
     def __init__(self, status: int, msg: str):
         self.status = status
         super().__init__("%s: %s" % (STATUS_NAMES[status] if 0 <= status < 8 else status, msg))
+
+
+def build_id() -> str:
+    """sha256 of the sources the loaded library was compiled from (fdirw_build_id)."""
+    return _lib.fdirw_build_id().decode()
 
 
 def last_error() -> str:
@@ -393,6 +404,13 @@ def destroy(ctx: Context):
 def debug_upload_weights(ctx: Context, kernels: np.ndarray):
     k = np.ascontiguousarray(kernels, dtype=np.float64)
     _check(_lib.fdirw_debug_upload_weights(ctx.handle, k.ctypes.data_as(ctypes.c_void_p)))
+
+
+def debug_stage_canary(ctx: Context, enable: bool = True):
+    """fdirw_debug_stage_canary → (16-byte words checked, mismatches)."""
+    a, b = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(_lib.fdirw_debug_stage_canary(ctx.handle, int(enable), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def export_kernels(ctx: Context, box) -> np.ndarray:

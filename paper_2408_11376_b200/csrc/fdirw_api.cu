@@ -89,6 +89,7 @@ struct fdirw_ctx {
     std::vector<void*> ipc_opened;
     // fdirw_step_host: device staging of the caller's host slab (allocated on first use)
     float* host_stage[2] = {nullptr, nullptr};
+    unsigned long long* canary = nullptr;  // fdirw_debug_stage_canary: {checks, mismatches}
 };
 
 static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s);
@@ -357,6 +358,7 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->cpad[1]);
     cudaFree(c->host_stage[0]);
     cudaFree(c->host_stage[1]);
+    cudaFree(c->canary);
     cudaFree(c->mass_partial);
     cudaFree(c->mass_out);
     cudaFree(c->farmask);
@@ -783,6 +785,7 @@ static cudaError_t superpose(fdirw_ctx* c, const float* src, float* out, long ps
         a.gap_last = gap_last;
     }
     a.no_bulk = c->no_bulk;
+    a.canary = c->canary;
     a.list = c->ut.dense_list;  // N4 (null unless FDIRW_F_DEDUP_STORAGE): compacted non-uniform chunks
     a.n_list = c->ut.n_dense;
     if (c->far && far_terms) {
@@ -1337,6 +1340,31 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
 }
 
 extern "C" const char* fdirw_last_error(void) { return g_err.c_str(); }
+
+#ifndef FDIRW_BUILD_ID
+#define FDIRW_BUILD_ID "unknown"
+#endif
+extern "C" const char* fdirw_build_id(void) { return FDIRW_BUILD_ID; }
+
+extern "C" fdirw_status fdirw_debug_stage_canary(fdirw_ctx* c, int32_t enable, uint64_t* checks, uint64_t* mismatches)
+{
+    if (!c || !checks || !mismatches) return fail(FDIRW_E_INVALID, "NULL argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (enable && !c->canary) {
+        fdirw_status st = alloc((void**)&c->canary, 16, "stage canary");
+        if (st != FDIRW_OK) return st;
+        CUDA_TRY(cudaMemset(c->canary, 0, 16));
+        if (c->graph2) {  // the captured steps carry the old launch arguments
+            cudaGraphExecDestroy(c->graph2);
+            c->graph2 = nullptr;
+        }
+    }
+    unsigned long long h[2] = {0, 0};
+    if (c->canary) CUDA_TRY(cudaMemcpy(h, c->canary, 16, cudaMemcpyDeviceToHost));
+    *checks = h[0];
+    *mismatches = h[1];
+    return FDIRW_OK;
+}
 
 extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k)
 {

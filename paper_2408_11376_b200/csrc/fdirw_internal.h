@@ -157,6 +157,11 @@ struct SuperArgs {
     float* push_hi = nullptr;
     int nzl = 0, pR = 0;
     bool no_bulk = false;  // FDIRW_F_NO_BULK_STREAM: weights by per-thread loads, not TMA stages
+    // test support (fdirw_debug_stage_canary): the staged stream re-reads every weight a compute
+    // thread takes from a stage — once after the stage's full barrier, once more just before the
+    // thread's warp releases the stage — and compares both with the global copy: {checks,
+    // mismatches}.  Null on every normal launch.
+    unsigned long long* canary = nullptr;
 };
 cudaError_t launch_superpose(const SuperArgs& a, int R, int fmt, cudaStream_t s);
 cudaError_t launch_read_stream(const void* p, size_t bytes, unsigned* sink, int sms, cudaStream_t s);

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         const bool open = __syncthreads_or(far_here) != 0;  // window touches the reservoir
         if (ph[KC] == 3) continue;  // far-field voxels are not sources (their value is c_far)
 
-        constexpr int Lp = S::Lp, NQ = Lp / 4;
+        constexpr int Lp = S::Lp;
         T c[Lp];
         if constexpr (F64) {
 #pragma unroll

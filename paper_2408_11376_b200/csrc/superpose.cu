@@ -594,6 +594,29 @@ constexpr int kBulkWarps = 8;  // at most: a tile of ≤ 256 chunks = a.tile/32 
 // tile, CTA blk → tile blk / nsub, part blk % nsub) so that short launches quantise into
 // smaller units (wave balance, see launch_superpose_r).  A part's weights for one slot are a
 // contiguous sub·8 run inside the tile's slot block: the producer copies them slot by slot.
+// fdirw_debug_stage_canary: compare this thread's 16 / 32 B of every slot of stored row i in the
+// stage with the same bytes in global memory (plain coherent loads).  Row i starts at slot 0 for
+// i = 0 (the centre row, L − 1 slots) and at slot (L − 1) + (i − 1)·L otherwise.
+template <typename WT>
+__device__ __noinline__ void stage_canary(const SuperArgs& a, const TileCtx& t, int e, int i, int L,
+                                          const unsigned char* wb, uint32_t subB)
+{
+    const int n = i == 0 ? L - 1 : L, k0 = i == 0 ? 0 : (L - 1) + (i - 1) * L;
+    const size_t slotE = (size_t)a.tile * 8;  // elements per slot of the whole tile
+    const WT* g = reinterpret_cast<const WT*>(a.Wt) + ((size_t)t.tile * (a.K - 1) + k0) * slotE + (size_t)e * 8;
+    unsigned long long bad = 0;
+    for (int k = 0; k < n; ++k) {
+        const uint4* gs = reinterpret_cast<const uint4*>(g + (size_t)k * slotE);
+        const uint4* ss = reinterpret_cast<const uint4*>(wb + (size_t)k * subB);
+        for (int w = 0; w < RawW<WT>::N; ++w) {
+            const uint4 x = gs[w], y = ss[w];
+            bad += (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+        }
+    }
+    atomicAdd(a.canary, (unsigned long long)n * RawW<WT>::N);
+    if (bad) atomicAdd(a.canary + 1, bad);
+}
+
 template <int R, typename WT>
 __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, int sub, unsigned char* smem_b)
 {
@@ -651,10 +674,12 @@ __device__ __forceinline__ void bulk_body(const SuperArgs& a, int blk, int S, in
             const int st = i % S, u = i / S;
             if (t.real) load_seg(row_src<R>(t, i), seg);
             mbar_wait(smem_u32(full + st), u & 1);
+            if (a.canary && t.real) stage_canary<WT>(a, t, e, i, L, wb + (size_t)st * stageB, subB);
             if (t.real) {
                 if (i == 0) do_row_s<R, WT, true>(seg, wb + (size_t)st * stageB, subB, hi, lo);
                 else do_row_s<R, WT, false>(seg, wb + (size_t)st * stageB, subB, hi, lo);
             }
+            if (a.canary && t.real) stage_canary<WT>(a, t, e, i, L, wb + (size_t)st * stageB, subB);
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(empty + st));
         }

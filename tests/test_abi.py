@@ -95,3 +95,14 @@ def test_slabs_tile(fd):
             sl = fd.slabs(nz, w)
             assert sl[0][0] == 0 and sl[-1][1] == nz
             assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+
+
+def test_loaded_library_matches_sources(fd):
+    """The loaded libfdirw.so was compiled from exactly the sources in the tree (content hash of
+    sources, headers, flags and nvcc version, compiled in as fdirw_build_id)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("fdirw_build", os.path.join(ROOT, "paper_2408_11376_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert fd.build_id() == b.source_sha()

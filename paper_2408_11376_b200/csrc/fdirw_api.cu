@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fdirw_internal.h"
 #include "layout.cuh"
 
@@ -257,14 +259,24 @@ static int kgen_cheb(const fdirw_params& p, const Derived& d, std::vector<float>
     return cheb_plan(d.n_fd - kCheb_pre, std::max(d.lam_ff, std::max(d.lam_fs, d.lam_ss)), coef);
 }
 
+// NVTX ranges (header-only nvtx3: no-ops unless a profiler injects a tool) around the
+// C-ABI's entry points, so a timeline shows the build phases and the steps by name.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // FDIRW_TRACE=1: host-side phase timings of fdirw_build_kernels on stderr (the stream is
-// synchronised at each mark only when tracing, so an untraced build is unaffected).
+// synchronised at each mark only when tracing, so an untraced build is unaffected).  Every
+// mark is also an NVTX marker inside the "fdirw_build_kernels" range.
 struct BuildTrace {
     bool on = getenv("FDIRW_TRACE") != nullptr;
     cudaStream_t s = nullptr;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
+    NvtxRange range{"fdirw_build_kernels"};
     void mark(const char* what)
     {
+        nvtxMarkA(what);
         if (!on) return;
         cudaStreamSynchronize(s);
         const auto n = std::chrono::steady_clock::now();
@@ -1035,6 +1047,7 @@ static float* pad_interior(fdirw_ctx* c, int i)
 
 extern "C" fdirw_status fdirw_step(fdirw_ctx* c, const float* c_in, float* c_out, void* cuda_stream)
 {
+    NvtxRange nvtx("fdirw_step");
     if (!c || !c_in || !c_out) return fail(FDIRW_E_INVALID, "NULL argument");
     if (c->is_virtual) return fail(FDIRW_E_STATE, "virtual-rank context: use fdirw_step_virtual");
     if (c_in == c_out) return fail(FDIRW_E_ALIAS, "c_in == c_out");
@@ -1097,6 +1110,7 @@ static fdirw_status capture_graph2(fdirw_ctx* c)
 
 extern "C" fdirw_status fdirw_run(fdirw_ctx* c, float* c_dev, int32_t n_steps, void* cuda_stream)
 {
+    NvtxRange nvtx("fdirw_run");
     if (!c || !c_dev) return fail(FDIRW_E_INVALID, "NULL argument");
     if (n_steps < 0) return fail(FDIRW_E_INVALID, "n_steps must be >= 0");
     if (c->is_virtual) return fail(FDIRW_E_STATE, "virtual-rank context: use fdirw_step_virtual");

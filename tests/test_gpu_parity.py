@@ -198,13 +198,15 @@ def test_cfg2_boxes(fd, oracle_lib, fmt):
 
 
 # ------------------------------------------------------------------ cfg3 (192³, R5) — bench launch config
-def test_cfg3_bench_config_sampled(fd, oracle_lib):
+@pytest.mark.parametrize("fmt", ["bf16", "fp16"])
+def test_cfg3_bench_config_sampled(fd, oracle_lib, fmt):
     """BASELINE configs[2] at full size in bench.py's launch configuration (fdirw_run):
-    192³ R50 particle, Table 1 SI parameters (n_fd = 1000), R5, bf16 weights.  Sampled
-    target boxes vs the oracle; total mass over the whole grid."""
+    192³ R50 particle, Table 1 SI parameters (n_fd = 1000), R5, bf16 weights (the headline)
+    and fp16 (the paper's storage format).  Sampled target boxes vs the oracle; total
+    mass over the whole grid."""
     import torch
 
-    cfg = fi.config("cfg3")
+    cfg = fi.config("cfg3", weights=fmt)
     mask = cfg.mask()
     pb = oracle_problem(cfg, mask)
     c0 = fi.initial_c(mask, "paper")

@@ -213,7 +213,13 @@ fdirw_status fdirw_step(fdirw_ctx* ctx, const float* c_in_dev, float* c_out_dev,
  * cuda_stream and returns before it completes: c_out_host is valid after the stream is
  * synchronised.  Page-locked (pinned) host buffers make the copies asynchronous; pageable
  * ones work but the driver stages them.  The context keeps two device staging slabs,
- * allocated on the first call.  c_in_host == c_out_host → FDIRW_E_ALIAS. */
+ * allocated on the first call.  c_in_host == c_out_host → FDIRW_E_ALIAS.
+ * On one GPU with the dense closed-domain path (no far field, no N4 storage, default
+ * precision mode) the slab is pipelined in plane chunks (up to 16): each chunk is copied
+ * straight into the padded state, its superposition starts once the planes it reads have
+ * landed (alternating between cuda_stream and an internal stream), and its result is copied
+ * back while later chunks compute; the result is bitwise fdirw_step's.  The internal streams
+ * are joined to cuda_stream before the call returns, so stream semantics are unchanged. */
 fdirw_status fdirw_step_host(fdirw_ctx* ctx, const float* c_in_host, float* c_out_host, void* cuda_stream);
 
 /* a7: n_steps FDiRW steps in place on c_dev (device fp32 slab), ping-ponging

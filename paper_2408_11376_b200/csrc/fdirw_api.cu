@@ -92,6 +92,10 @@ struct fdirw_ctx {
     // fdirw_step_host: device staging of the caller's host slab (allocated on first use)
     float* host_stage[2] = {nullptr, nullptr};
     unsigned long long* canary = nullptr;  // fdirw_debug_stage_canary: {checks, mismatches}
+    // fdirw_step_host's plane-chunk pipeline (world 1, dense closed path): copy streams and
+    // per-chunk events, created on first use
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    std::vector<cudaEvent_t> hx_ev;  // [3·nch + 1]: H2D done, step done, D2H done per chunk, start
 };
 
 static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t s);
@@ -371,6 +375,10 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->host_stage[0]);
     cudaFree(c->host_stage[1]);
     cudaFree(c->canary);
+    for (cudaEvent_t e : c->hx_ev)
+        if (e) cudaEventDestroy(e);
+    if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     cudaFree(c->mass_partial);
     cudaFree(c->mass_out);
     cudaFree(c->farmask);
@@ -1064,6 +1072,80 @@ extern "C" fdirw_status fdirw_step(fdirw_ctx* c, const float* c_in, float* c_out
     return enqueue_step(c, c->cpad[0], c_out, (long)g.nx * g.ny, g.nx, s, 1);
 }
 
+// fdirw_step_host, the pipelined form (world 1, the dense closed-domain superposition): the
+// slab is cut into nch plane chunks; chunk j's planes are copied from the host straight into
+// the padded state (3-D strided copy on the H2D stream), the superposition of chunk j's tiles
+// starts as soon as the planes it reads (its own + R on either side) have landed, and chunk j's
+// result goes back to the host (D2H stream) while chunk j + 1 computes.  Only the first
+// chunk's copy-in and the last chunk's copy-out stay exposed.  nch is picked so that each
+// chunk's launch fills whole waves of the staged stream (2 CTAs × SMs).
+static int step_host_chunks(const fdirw_ctx* c)
+{
+    const Geometry& g = c->g;
+    if (c->world > 1 || c->far || c->ut.chunk_u || c->compact || c->prec_mode != 0 || g.nzl < 4 * g.R)
+        return 1;
+    // chunks of at least max(8, R) planes, at most 16: the exposed head (first chunk's copy-in)
+    // and tail (last chunk's copy-out) shrink with the chunk, while the chunk launches' partial
+    // last waves are filled by the next chunk's launch on the other compute stream
+    // (measured at cfg3: 4 / 6 / 8 chunks on one stream gave 0.83 / 0.86 / 0.88 of the
+    // device-timed rate)
+    return std::max(1, std::min(16, g.nzl / std::max(8, g.R)));
+}
+
+static fdirw_status step_host_pipelined(fdirw_ctx* c, const float* in, float* out, cudaStream_t s, int nch)
+{
+    const Geometry& g = c->g;
+    if (!c->h2d_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+    if (!c->d2h_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+    if ((int)c->hx_ev.size() < 3 * nch + 1) {
+        for (cudaEvent_t e : c->hx_ev) cudaEventDestroy(e);
+        c->hx_ev.assign(3 * nch + 1, nullptr);
+        for (auto& e : c->hx_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaEvent_t* h2d = c->hx_ev.data();
+    cudaEvent_t* done = h2d + nch;
+    cudaEvent_t* d2h = done + nch;
+    cudaEvent_t start = c->hx_ev[3 * nch];
+    const int pl = (g.nzl + nch - 1) / nch;
+    const size_t plane_b = (size_t)g.nx * g.ny * 4;
+    // the previous work on s (the last reads of cpad[0] and of the output staging) precedes
+    // this step's copies
+    CUDA_TRY(cudaEventRecord(start, s));
+    CUDA_TRY(cudaStreamWaitEvent(c->h2d_stream, start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(c->d2h_stream, start, 0));
+    for (int j = 0; j < nch; ++j) {
+        const int z0 = j * pl, z1 = std::min(g.nzl, z0 + pl);
+        if (z0 >= z1) { CUDA_TRY(cudaEventRecord(h2d[j], c->h2d_stream)); continue; }
+        cudaMemcpy3DParms m{};
+        m.srcPtr = make_cudaPitchedPtr(const_cast<float*>(in) + (size_t)z0 * g.nx * g.ny, (size_t)g.nx * 4, g.nx, g.ny);
+        m.dstPtr = make_cudaPitchedPtr(c->cpad[0], (size_t)g.nxp * 4, g.nxp, g.nyp);
+        m.dstPos = make_cudaPos((size_t)kPadX * 4, g.R, g.R + z0);
+        m.extent = make_cudaExtent((size_t)g.nx * 4, g.ny, z1 - z0);
+        m.kind = cudaMemcpyHostToDevice;
+        CUDA_TRY(cudaMemcpy3DAsync(&m, c->h2d_stream));
+        CUDA_TRY(cudaEventRecord(h2d[j], c->h2d_stream));
+    }
+    // chunks alternate between the caller's stream and a second compute stream (the context's
+    // comm stream, idle at world 1) so a chunk's launch can start while the previous one drains
+    CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, start, 0));
+    for (int j = 0; j < nch; ++j) {
+        cudaStream_t cs = (j & 1) ? c->comm_stream : s;
+        const int z0 = j * pl, z1 = std::min(g.nzl, z0 + pl);
+        if (z0 >= z1) { CUDA_TRY(cudaEventRecord(done[j], cs)); CUDA_TRY(cudaEventRecord(d2h[j], c->d2h_stream)); continue; }
+        const int need = std::min(nch - 1, (std::min(g.nzl, z1 + g.R) - 1) / pl);  // last chunk read
+        CUDA_TRY(cudaStreamWaitEvent(cs, h2d[need], 0));  // (H2D stream order covers the earlier chunks)
+        CUDA_TRY(superpose(c, c->cpad[0], c->host_stage[1], (long)g.nx * g.ny, g.nx, z0 * g.tpp, z1 * g.tpp, cs));
+        CUDA_TRY(cudaEventRecord(done[j], cs));
+        CUDA_TRY(cudaStreamWaitEvent(c->d2h_stream, done[j], 0));
+        CUDA_TRY(cudaMemcpyAsync(out + (size_t)z0 * g.nx * g.ny, c->host_stage[1] + (size_t)z0 * g.nx * g.ny,
+                                 (size_t)(z1 - z0) * plane_b, cudaMemcpyDeviceToHost, c->d2h_stream));
+        CUDA_TRY(cudaEventRecord(d2h[j], c->d2h_stream));
+    }
+    // the caller's stream covers the result (the D2H stream waited for every chunk in order)
+    CUDA_TRY(cudaStreamWaitEvent(s, d2h[nch - 1], 0));
+    return FDIRW_OK;
+}
+
 extern "C" fdirw_status fdirw_step_host(fdirw_ctx* c, const float* c_in_host, float* c_out_host, void* cuda_stream)
 {
     if (!c || !c_in_host || !c_out_host) return fail(FDIRW_E_INVALID, "NULL argument");
@@ -1077,6 +1159,12 @@ extern "C" fdirw_status fdirw_step_host(fdirw_ctx* c, const float* c_in_host, fl
             if (st != FDIRW_OK) return st;
         }
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    static const int force = [] {
+        const char* ev = getenv("FDIRW_STEP_HOST_CHUNKS");  // A/B: 1 = the plain form
+        return ev ? atoi(ev) : 0;
+    }();
+    const int nch = force > 0 ? (force == 1 ? 1 : std::min(force, 16)) : step_host_chunks(c);
+    if (nch > 1 && step_host_chunks(c) > 1) return step_host_pipelined(c, c_in_host, c_out_host, s, nch);
     CUDA_TRY(cudaMemcpyAsync(c->host_stage[0], c_in_host, bytes, cudaMemcpyHostToDevice, s));
     fdirw_status st = fdirw_step(c, c->host_stage[0], c->host_stage[1], cuda_stream);
     if (st != FDIRW_OK) return st;

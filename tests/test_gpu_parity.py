@@ -354,6 +354,31 @@ def test_profile_phases_equals_run(fd):
     assert ph["step"] >= ph["interior"] and ph["step"] <= 1.5 * (ph["interior"] + ph["tail"]) + 0.05
 
 
+@pytest.mark.parametrize("shape,R", [((64, 40, 52), 3), ((9, 10, 11), 2)])
+def test_step_host_equals_run(fd, shape, R):
+    """fdirw_step_host (host buffers: copy-in, step, copy-out on the caller's stream; on larger
+    slabs a plane-chunk pipeline with copies overlapping the chunks' superpositions) chained
+    three times equals fdirw_run(3) bit for bit."""
+    import torch
+
+    cfg = small_cfg(shape, R, 30, weights="bf16")
+    mask = fi.random_two_phase(cfg.shape, 0.6, seed=12)
+    c0 = fi.initial_c(mask, "random", seed=12)
+    ctx = fd.build_kernels(lib_params(cfg), mask)
+    try:
+        ref = torch.from_numpy(c0).cuda()
+        fd.run(ctx, ref, 3)
+        h = [torch.from_numpy(c0.copy()).pin_memory(), torch.empty(cfg.shape, dtype=torch.float32).pin_memory()]
+        for k in range(3):
+            fd.step_host(ctx, h[k % 2], h[(k + 1) % 2])
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(h[1].numpy(), ref.cpu().numpy())
+        with pytest.raises(fd.FdirwError):
+            fd.step_host(ctx, h[0], h[0])
+    finally:
+        fd.destroy(ctx)
+
+
 def test_errors(fd):
     import torch
 

@@ -37,6 +37,22 @@ def main():
             fd.mass(ctx, c)
             if not flags & fd.F_DEDUP_STORAGE:  # export needs the dense layout
                 fd.export_kernels(ctx, (0, 5, 0, 4, 0, 3))
+    # round 2 entry points: host-buffer step (plain and plane-chunk pipelined), phase profile,
+    # slab mass, the staged-stream canary
+    hin = c0.cpu().pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    with fd.build_kernels(params(shape, 3, 30, "bf16"), mask) as ctx:
+        fd.step_host(ctx, hin, hout)
+        c = c0.clone()
+        fd.profile_phases(ctx, c, 2)
+        fd.mass_local(ctx, c)
+    pshape = (48, 11, 21)  # 48 planes >= 4R: the pipelined form (chunks of 8 planes)
+    pmask = fi.porous_particle(pshape, 4, pore_r=(1.0, 1.5), n_pores=3, seed=3)
+    pin = torch.from_numpy(fi.initial_c(pmask, "random", seed=3)).pin_memory()
+    pout = torch.empty_like(pin).pin_memory()
+    with fd.build_kernels(params(pshape, 3, 30, "bf16"), pmask) as ctx:
+        fd.step_host(ctx, pin, pout)
+        fd.step_host(ctx, pout, pin)
     # TMA-staged weight stream (needs >= 2 CTAs/SM of tiles: 40 planes x 8 tiles), dense and N4 mixed
     big = (40, 64, 256)
     bmask = fi.porous_particle(big, 14, pore_r=(1.0, 2.0), porosity=0.3, seed=2)
@@ -46,6 +62,10 @@ def main():
             assert ctx.info["n_tiles"] >= 2 * 148
             c = cb.clone()
             fd.run(ctx, c, 2)
+            if not flags:
+                fd.debug_stage_canary(ctx, True)
+                fd.run(ctx, c, 1)
+                assert fd.debug_stage_canary(ctx, True)[1] == 0
     # MX8 weights: expand + diag build pass, staged MX8 stream (tile 256 and a
     # runtime tile width), export
     if not EXTRA:

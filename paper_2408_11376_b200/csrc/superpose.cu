@@ -891,110 +891,6 @@ __global__ void __launch_bounds__((kBulkWarps + 1) * 32, 3) superpose_mx8_kernel
     mx8_body<R, TT>(a, blockIdx.x, S, smem_b, nsub);
 }
 
-// MX8 for short launches (< 2 CTAs per SM of tiles, e.g. cfg2's 128): no producer warp and
-// no stage ring to fill — every thread loads its own next row's mantissas (8 B per slot) and
-// block exponents (1 B per slot) into registers while the current row computes, the MX8 twin
-// of dense_body's register-prefetch form.  A tile may be split over nsub CTAs (a part = a run
-// of its chunks; no per-tile sums then).  Decode, FMA chain and flush grouping are mx8_body's
-// exactly, so the field is bitwise the staged kernel's.
-__device__ __forceinline__ uint2 ld_stream_u2(const void* ptr, uint64_t pol)
-{
-    uint2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
-                 : "=r"(r.x), "=r"(r.y)
-                 : "l"(ptr), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint32_t ld_stream_u8(const void* ptr, uint64_t pol)
-{
-    unsigned short r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-
-template <int R, int N>
-__device__ __forceinline__ void mx8_load_row(const unsigned char* base, int Tf, int e, uint64_t pol, uint2 (&m)[2 * R + 1],
-                                             uint32_t (&E)[2 * R + 1])
-{
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        m[k] = ld_stream_u2(base + ((size_t)k * Tf + e) * 8, pol);
-        E[k] = ld_stream_u8(base + (size_t)N * 8 * Tf + (size_t)k * Tf + e, pol);
-    }
-}
-
-template <int R, bool CENTRE_ROW>
-__device__ __forceinline__ void row_mx8_reg(const float seg[24], const uint2 (&mr)[2 * R + 1],
-                                            const uint32_t (&Er)[2 * R + 1], float p[8])
-{
-#pragma unroll
-    for (int ox = -R; ox <= R; ++ox) {
-        if (CENTRE_ROW && ox == 0) continue;
-        const int k = CENTRE_ROW ? (ox < 0 ? ox + R : ox + R - 1) : ox + R;
-        const uint2 m = mr[k];
-        const uint32_t E = Er[k];
-        const float sc = __uint_as_float(E << 23), bias = __uint_as_float(((E + 23u) << 23) | 0x80000000u);
-        const unsigned long long sc2 = pk2f(sc, sc), b2 = pk2f(bias, bias);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const unsigned wd = h < 2 ? m.x : m.y;
-            const float f0 = __uint_as_float(__byte_perm(wd, 0x4B000000u, 0x7440u | (unsigned)((2 * h) & 3)));
-            const float f1 = __uint_as_float(__byte_perm(wd, 0x4B000000u, 0x7440u | (unsigned)((2 * h + 1) & 3)));
-            float w0, w1;
-            upk2f(fma2f(pk2f(f0, f1), sc2, b2), w0, w1);
-            p[2 * h] = fmaf(w0, seg[2 * h - ox + 8], p[2 * h]);
-            p[2 * h + 1] = fmaf(w1, seg[2 * h + 1 - ox + 8], p[2 * h + 1]);
-        }
-    }
-}
-
-template <int R>
-__global__ void __launch_bounds__(256) superpose_mx8_pf_kernel(const SuperArgs a, int nsub)
-{
-    constexpr int L = 2 * R + 1, K = L * L * L, NR = L * L - 1, RC = R * L + R, G = mx8_rows(R);
-    const int Tf = a.tile, T = Tf / nsub;
-    const int blk = blockIdx.x / nsub, part = blockIdx.x % nsub;
-    const int e = part * T + (int)threadIdx.x;
-    const TileCtx t = tile_ctx<R>(a, blk, e);
-    if (!t.real && a.tile_sum == nullptr) return;
-    float hi[8], lo[8];
-    diag_init(a, t, e, hi, lo);
-    if (t.real) {
-        const uint64_t pol = evict_first_policy();
-        const unsigned char* base = reinterpret_cast<const unsigned char*>(a.Wt) + (size_t)t.tile * (K - 1) * 9 * Tf;
-        const size_t rowB = (size_t)L * 9 * Tf;  // one stored non-centre row
-        const int pl = (int)t.plane, nx_ = (int)t.nxp;
-        uint2 ma[L], mb[L];
-        uint32_t ea[L], eb[L];
-        float seg[24], p[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) p[j] = 0.f;
-        const unsigned char* rb = base + (size_t)(L - 1) * 9 * Tf;  // stored row 1
-        mx8_load_row<R, L - 1>(base, Tf, e, pol, ma, ea);
-        mx8_load_row<R, L>(rb, Tf, e, pol, mb, eb);
-        load_seg(t.c0 - 8, seg);
-        row_mx8_reg<R, true>(seg, ma, ea, p);
-        flush_mx8(p, hi, lo);
-        // stored rows 1 .. NR: (oz, oy) ascending without the centre, as mx8_body
-#pragma unroll 1
-        for (int i = 1; i <= NR; i += 2) {
-            const int r0 = (i - 1) < RC ? i - 1 : i, r1 = i < RC ? i : i + 1;
-            if (i + 1 <= NR) mx8_load_row<R, L>(rb + rowB, Tf, e, pol, ma, ea);
-            load_seg(t.c0 - (r0 / L - R) * pl - (r0 % L - R) * nx_ - 8, seg);
-            row_mx8_reg<R, false>(seg, mb, eb, p);
-            if (i % G == 0) flush_mx8(p, hi, lo);
-            rb += rowB;
-            if (i + 1 > NR) break;
-            if (i + 2 <= NR) mx8_load_row<R, L>(rb + rowB, Tf, e, pol, mb, eb);
-            load_seg(t.c0 - (r1 / L - R) * pl - (r1 % L - R) * nx_ - 8, seg);
-            row_mx8_reg<R, false>(seg, ma, ea, p);
-            if ((i + 1) % G == 0) flush_mx8(p, hi, lo);
-            rb += rowB;
-        }
-    }
-    tile_epilogue(a, t, e, hi, lo);
-}
-
 // MX8 uniform blocks: uniform_body's work with the MX8 body's summation grouping (the centre
 // row, then groups of mx8_rows(R) rows into one fp32 partial before the TwoSum).  The decoded
 // weights are the dense MX8 layout's, so the field is bitwise the dense MX8 path's.
@@ -1129,26 +1025,8 @@ static cudaError_t launch_superpose_r(const SuperArgs& a, int fmt, cudaStream_t 
 {
     const int nblk = a.t_end - a.t_begin - (a.gap_last ? 0 : a.gap_len);
     if (nblk <= 0) return cudaSuccess;
-    if (fmt == FDIRW_W_MX8) {
+    if (fmt == FDIRW_W_MX8) {  // staged stream only (whole tiles), at any launch size
         if (a.tile % 32 != 0 || a.tile > kBulkWarps * 32) return cudaErrorInvalidValue;
-        // short launches (< 2 CTAs per SM of tiles; R ≤ 5 for the register budget): the
-        // register-prefetch body, tiles split in two when that still leaves ≤ 2 CTAs per SM
-        // (FDIRW_MX8_PF = 0 / 1 forces the staged / prefetch form, A/B)
-        int sms = 148;
-        {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
-        bool pf = R <= 5 && nblk < 2 * sms;
-        if (const char* ev = getenv("FDIRW_MX8_PF")) pf = R <= 5 && ev[0] == '1';
-        if constexpr (R <= 5) {
-            if (pf) {
-                const int nsub = (a.tile_sum == nullptr && a.tile % 64 == 0 && 2 * nblk <= 2 * sms) ? 2 : 1;
-                superpose_mx8_pf_kernel<R><<<nblk * nsub, a.tile / nsub, 0, s>>>(a, nsub);
-                return cudaGetLastError();
-            }
-        }
         const size_t row = (size_t)(2 * R + 1) * a.tile * 9, half = (228 * 1024) / 2 - 1024 - 128;
         int S = (int)(half / row);
         if (S < 2) S = (int)((227 * 1024 - 128) / row);

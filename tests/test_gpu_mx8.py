@@ -408,25 +408,3 @@ def test_mx8_tile_split_bitwise(fd, monkeypatch):
             fd.destroy(ctx)
     for k in ("2", "4", None):
         np.testing.assert_array_equal(outs[k], outs["1"])
-
-
-@pytest.mark.parametrize("shape,R", [((16, 64, 64), 4), ((12, 40, 70), 5), ((10, 33, 41), 2)])
-def test_mx8_prefetch_body_bitwise(fd, shape, R, monkeypatch):
-    """Short MX8 launches run the register-prefetch body (superpose_mx8_pf_kernel; tiles split in
-    two when that still fits one wave): bitwise the staged MX8 kernel (FDIRW_MX8_PF=0)."""
-    import torch
-
-    cfg = small_cfg(shape, R, 200, D_slow=1e-3, weights="mx8")
-    mask = fi.porous_particle(shape, min(shape) / 3, pore_r=(1.0, 2.0), porosity=0.3, seed=R)
-    c0 = fi.initial_c(mask, "random", seed=R)
-    outs = []
-    for mode in ("1", "0"):
-        monkeypatch.setenv("FDIRW_MX8_PF", mode)
-        ctx = fd.build_kernels(lib_params(cfg), mask)
-        try:
-            c = torch.from_numpy(c0).cuda()
-            fd.run(ctx, c, 3)
-            outs.append(c.cpu().numpy())
-        finally:
-            fd.destroy(ctx)
-    np.testing.assert_array_equal(outs[0], outs[1])

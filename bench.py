@@ -344,7 +344,10 @@ def _one_step_field(fd, torch, ctx, mask, stream):
 def _variant(fd, torch, params, mask, c_host, args, stream, peak, fid=None, hist=None, name=""):
     """A storage variant measured in the same run: its own byte model, step time and, with the
     oracle leg on, relL2 of one step against the oracle on the FID_BOXES."""
-    ctx = fd.build_kernels(params, mask, stream=stream)
+    try:
+        ctx = fd.build_kernels(params, mask, stream=stream)
+    except fd.FdirwError as e:  # a combination the library rejects for this geometry
+        return {"unavailable": str(e)}
     try:
         info = ctx.info
         ms = _time_run(fd, torch, ctx, c_host.to("cuda", non_blocking=True), args, stream)
@@ -925,7 +928,8 @@ def main():
         line["variants"]["mx8_weights"] = v
         v = _variant(fd, torch, dataclasses.replace(params, weights="mx8", flags=params.flags | fd.F_DEDUP_STORAGE),
                      mask, c_host, args, stream, peak)
-        v["note"] = "MX8 weights + N4 storage: superpose_mx8_mixed_kernel (DESIGN §15)"
+        if "unavailable" not in v:
+            v["note"] = "MX8 weights + N4 storage: superpose_mx8_mixed_kernel (DESIGN §15)"
         line["variants"]["mx8_dedup_storage"] = v
 
     if checks:  # accuracy of the timed configuration, driver-visible (oracle leg)

@@ -1084,6 +1084,11 @@ static int step_host_chunks(const fdirw_ctx* c)
     const Geometry& g = c->g;
     if (c->world > 1 || c->far || c->ut.chunk_u || c->compact || c->prec_mode != 0 || g.nzl < 4 * g.R)
         return 1;
+    // small slabs (< 8 tiles per SM): the copies are short and a chunk's launch would be a
+    // fraction of a wave; one copy-in, one step, one copy-out is faster
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (g.n_tiles < 8 * sms) return 1;
     // chunks of at least max(8, R) planes, at most 16: the exposed head (first chunk's copy-in)
     // and tail (last chunk's copy-out) shrink with the chunk, while the chunk launches' partial
     // last waves are filled by the next chunk's launch on the other compute stream

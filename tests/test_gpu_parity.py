@@ -354,11 +354,11 @@ def test_profile_phases_equals_run(fd):
     assert ph["step"] >= ph["interior"] and ph["step"] <= 1.5 * (ph["interior"] + ph["tail"]) + 0.05
 
 
-@pytest.mark.parametrize("shape,R", [((64, 40, 52), 3), ((9, 10, 11), 2)])
+@pytest.mark.parametrize("shape,R", [((96, 128, 256), 2), ((9, 10, 11), 2)])
 def test_step_host_equals_run(fd, shape, R):
-    """fdirw_step_host (host buffers: copy-in, step, copy-out on the caller's stream; on larger
-    slabs a plane-chunk pipeline with copies overlapping the chunks' superpositions) chained
-    three times equals fdirw_run(3) bit for bit."""
+    """fdirw_step_host (host buffers: copy-in, step, copy-out on the caller's stream; on slabs of
+    ≥ 8 tiles per SM — the 96×128×256 grid has 1,536 — a plane-chunk pipeline with copies
+    overlapping the chunks' superpositions) chained three times equals fdirw_run(3) bit for bit."""
     import torch
 
     cfg = small_cfg(shape, R, 30, weights="bf16")

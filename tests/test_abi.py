@@ -106,3 +106,28 @@ def test_loaded_library_matches_sources(fd):
     b = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(b)
     assert fd.build_id() == b.source_sha()
+
+
+def test_null_arguments_rejected_without_gpu(fd):
+    """Every entry point added in round 2 validates its arguments before touching CUDA."""
+    L = fd._lib
+    d = ctypes.c_double()
+    u, v = ctypes.c_uint64(), ctypes.c_uint64()
+    ms = (ctypes.c_double * 5)()
+    assert L.fdirw_step_host(None, None, None, None) == fd.E_INVALID
+    assert L.fdirw_comm_init(None, None) == fd.E_INVALID
+    assert L.fdirw_mass_local(None, None, ctypes.byref(d), None) == fd.E_INVALID
+    assert L.fdirw_profile_phases(None, None, 4, None, ms) == fd.E_INVALID
+    assert L.fdirw_debug_stage_canary(None, 1, ctypes.byref(u), ctypes.byref(v)) == fd.E_INVALID
+    assert fd.last_error()
+
+
+def test_slab_index_range_checked(fd):
+    """slabs whose mask planes exceed 2^31 voxels are rejected (the window dedup and
+    the N3 loop index a slab's voxels with 32-bit ints)."""
+    p = _params(fd, nx=2048, ny=2048, nz=600, radius=1)
+    plan = fd.fdirw_plan()
+    rc = fd._lib.fdirw_make_plan(ctypes.byref(p.c()), None, ctypes.byref(plan))
+    assert rc == fd.E_INVALID and "2^31" in fd.last_error()
+    ok = _params(fd, nx=2048, ny=2048, nz=400, radius=1)
+    assert fd._lib.fdirw_make_plan(ctypes.byref(ok.c()), None, ctypes.byref(plan)) == fd.FDIRW_OK

@@ -223,17 +223,24 @@ def step_box(pb: Problem, C_old: np.ndarray, tbox, fmt: str | None = None, mass_
     return step_scatter(pb, W, sbox, C_old, tbox)
 
 
-def step_full(pb: Problem, C_old: np.ndarray, steps: int = 1, fmt: str | None = None, mass_fix: bool = True):
-    """`steps` FDiRW steps on the whole grid (small grids only: N·K fp64 kernels)."""
+def step_full(pb: Problem, C_old: np.ndarray, steps: int = 1, fmt: str | None = None, mass_fix: bool = True,
+              threads: bool = False, W: np.ndarray | None = None, checkpoints=()):
+    """`steps` FDiRW steps on the whole grid (small grids only: N·K fp64 kernels).  threads:
+    the OpenMP scatter (same bits); W: the kernels, if already built (fmt / mass_fix are then
+    ignored); checkpoints: step counts at which to also return the field → (C, {k: C_k})."""
     nz, ny, nx = pb.shape
     box = (0, nx, 0, ny, 0, nz)
-    W = build_kernels(pb, box)
-    if fmt is not None:
-        W = quantize(pb, W, fmt, mass_fix)
+    if W is None:
+        W = build_kernels(pb, box)
+        if fmt is not None:
+            W = quantize(pb, W, fmt, mass_fix)
     C = np.asarray(C_old, np.float64)
-    for _ in range(steps):
-        C = step_scatter(pb, W, box, C, box)
-    return C
+    snap = {}
+    for k in range(1, steps + 1):
+        C = step_scatter(pb, W, box, C, box, threads=threads)
+        if k in checkpoints:
+            snap[k] = C.copy()
+    return (C, snap) if checkpoints else C
 
 
 def fd_whole_grid(pb: Problem, C0: np.ndarray, nsub: int, c_far: float = 0.0) -> np.ndarray:

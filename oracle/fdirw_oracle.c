@@ -260,7 +260,12 @@ void oracle_step_scatter_omp(const oracle_params* p, const double* W, const int3
  * role Eq.7 plays in the paper).  IEEE 754 round-to-nearest-even (ref 26,
  * P:151; A11).
  *   for o ≠ centre:  Wq[o] = RNE_fmt( RNE_fp32( W[o] ) )
- *   diag            = RNE_fp32( M − Σ_{o≠centre, ascending o} Wq[o] )   (fp64 sum)
+ *   d               = M − Σ_{o≠centre, ascending o} Wq[o]               (fp64 sum)
+ *   diag            = d_hi + d_lo,  d_hi = RNE_fp32(d),  d_lo = RNE_fp32(d − d_hi)
+ *   (reading A10 as revised in round 2: the diagonal is stored as an fp32 PAIR, so a column
+ *   sums to M within ~2^-48 instead of half an fp32 ulp; one fp32 diagonal rounded the same
+ *   way for every member of a large class of identical windows, which biased the total
+ *   mass by ~1e-8 per step on long runs)
  *   M = 1 for a closed window (Σ_o W = 1, reading A2); with a far field (N2) the
  *   kernel keeps M = Σ_o W (ascending o) and the rest went to the reservoir
  *   (mass_fix = 0:  diag = RNE_fmt(RNE_fp32(W[centre])))
@@ -345,7 +350,13 @@ void oracle_quantize(const oracle_params* p, const double* W, long nsrc, int fmt
             q[o] = oracle_round_fmt(w[o], fmt);
             sum += q[o];
         }
-        q[c] = mass_fix ? (double)(float)(M - sum) : oracle_round_fmt(w[c], fmt);
+        if (mass_fix) {
+            const double d = M - sum;
+            const float hi = (float)d, lo = (float)(d - (double)hi);
+            q[c] = (double)hi + (double)lo;
+        } else {
+            q[c] = oracle_round_fmt(w[c], fmt);
+        }
     }
 }
 

@@ -360,7 +360,7 @@ def _variant(fd, torch, params, mask, c_host, args, stream, peak, fid=None, hist
     N = int((mask != 2).sum())
     b_w = {"fp32": 4, "mx8": 1.125}.get(params.weights, 2)
     f_u = info["uniform_chunks"] / max(info["chunks"], 1)
-    bpv = (1.0 - f_u) * (info["K"] - 1) * b_w + 12
+    bpv = (1.0 - f_u) * (info["K"] - 1) * b_w + 16
     ach = bpv * N / (ms * 1e-3) / 1e9
     v = {"value": N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "bytes_per_voxel_update": bpv,
          "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak},
@@ -566,7 +566,7 @@ def run_absorb(args):
             "roofline": {"bound": "hbm", "achieved": sup_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": sup_bytes / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                          "note": "the loop's dominant kernel is the liquid superposition: its algorithmic bytes "
-                                 "(near-field liquid voxel-updates x (K-1)*b_w+12) over the whole macro-step time",
+                                 "(near-field liquid voxel-updates x (K-1)*b_w+16) over the whole macro-step time",
                          "streamed_GBps": info["weight_bytes"] / (ms * 1e-3) / 1e9,
                          "streamed_note": "stored weights actually read per step (every non-far chunk, incl. the "
                                           "solid targets whose liquid-step rows are zero with D_slow = 0)"},
@@ -831,12 +831,12 @@ def main():
     e2e_value = N * args.e2e_steps / (e_ms * 1e-3)
     bpv = info["bytes_per_voxel_update"]
     if cfg.weights == "mx8":  # 9/8 B per weight (the C-ABI field is rounded to an integer)
-        bpv = (cfg.K - 1) * 1.125 + 12
+        bpv = (cfg.K - 1) * 1.125 + 16
     dedup_storage = bool(params.flags & fd.F_DEDUP_STORAGE)
     f_u = info["uniform_chunks"] / max(info["chunks"], 1)
     if dedup_storage:  # N4 byte model: uniform chunks' weights come from an L2-resident table
         bw = {"fp32": 4, "mx8": 1.125}.get(cfg.weights, 2)
-        bpv = (1.0 - f_u) * (info["K"] - 1) * bw + 12
+        bpv = (1.0 - f_u) * (info["K"] - 1) * bw + 16
     per_launch_bytes = bpv * n_slab
     peak, peak_src = _hbm_peak()
     # N=1: one superpose launch; N>1 P2P: wait + one superpose launch + signal; NCCL: interior
@@ -868,9 +868,9 @@ def main():
                                 "superpose_bulk_kernel (TMA-staged weights)" if info["n_tiles"] >= 2 * 148
                                 else "superpose_kernel (register prefetch)"),
                      "peak_source": peak_src, "bytes_per_voxel_update": bpv,
-                     "note": ("N4 byte model: (1-f_uniform)*(K-1)*b_w+12 per voxel-update, f_uniform=%.4f"
+                     "note": ("N4 byte model: (1-f_uniform)*(K-1)*b_w+16 per voxel-update, f_uniform=%.4f"
                               % f_u if dedup_storage else
-                              "algorithmic bytes (K-1)*b_w+12 per voxel-update x voxels / step time (per rank)")},
+                              "algorithmic bytes (K-1)*b_w+16 per voxel-update x voxels / step time (per rank)")},
         "storage": "dedup (NEXT row N4)" if dedup_storage else "dense",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(c.numel() * 4 * world),
                 "d2h_bytes_per_step": int(c.numel() * 4 * world), "steps": args.e2e_steps,

@@ -148,9 +148,9 @@ typedef struct {
     int32_t z_begin, z_end; /* this context's target slab                                      */
     double dt_fd;           /* Δt / n_fd                                                        */
     double lambda_fast, lambda_fs, lambda_slow; /* face numbers Δt_fd·D/Δh² (fast-fast, cross, slow-slow) */
-    uint64_t weight_bytes;  /* device bytes of the stored weights incl. fp32 diagonal + padding */
+    uint64_t weight_bytes;  /* device bytes of the stored weights incl. the fp32-pair diagonal + padding */
     uint64_t state_bytes;   /* device bytes of the padded ping-pong concentration state         */
-    uint64_t bytes_per_voxel_update; /* algorithmic: (K−1)·b_w + 4 (diag) + 4 (C read) + 4 (C write) */
+    uint64_t bytes_per_voxel_update; /* algorithmic: (K−1)·b_w + 8 (diag pair) + 4 (C read) + 4 (C write) */
     uint64_t voxels;        /* targets in this slab: nx·ny·(z_end − z_begin)                   */
     int32_t tile_chunks;    /* 8-voxel x-chunks per superposition tile (CTA)                   */
     int32_t n_tiles;        /* tiles in this slab                                              */
@@ -195,7 +195,7 @@ fdirw_status fdirw_nccl_unique_id(void* out128);
  * device memory for the slab, copy the mask planes [z_begin−2R, z_end+2R)
  * to the device, and generate every kernel W_s whose window reaches the slab
  * (sources [z_begin−R, z_end+R) ∩ [0,nz)) with the batched-window FD kernel,
- * then renormalise (fp64), quantise (RNE), fix the fp32 diagonal and write the
+ * then renormalise (fp64), quantise (RNE), fix the diagonal (an fp32 pair, A10) and write the
  * gather layout.  Enqueued on cuda_stream; the call synchronises that stream
  * before returning so the context is ready.  dist == NULL means world = 1 on
  * the current device.  On success *out owns all device memory.  */
@@ -319,7 +319,8 @@ const char* fdirw_build_id(void);
 /* ---- test support ------------------------------------------------------------
  * Replace the weights of a world == 1 context by caller-supplied per-source
  * kernels (host fp64, [nz][ny][nx][K], slot o = ((oz+R)·L+(oy+R))·L+(ox+R),
- * centre slot = the fp32 diagonal).  Off-centre values are converted to the
+ * centre slot = the diagonal, stored as the fp32 pair hi = RNE_fp32(v), lo = RNE_fp32(v − hi)).
+ * Off-centre values are converted to the
  * context's storage format with RNE; out-of-domain slots are ignored.  Used
  * to test the superposition in isolation against oracle weights.
  * Synchronous.  FDIRW_E_STATE when world > 1. */

@@ -259,7 +259,7 @@ __global__ void superpose_study_kernel(const StudyArgs a)
             const int ox = o % L - R, oy = (o / L) % L - R, oz = o / (L * L) - R;
             const float cs = a.cpad[p - ((long)oz * a.nyp + oy) * a.nxp - ox];
             float w;
-            if (o == K / 2) w = a.diag[(tile * a.tile + e) * 8 + j];
+            if (o == K / 2) w = a.diag[(tile * a.tile + e) * 8 + j].x;  // (study contexts: no fix-up, lo = 0)
             else {
                 const size_t idx = ((tile * (size_t)(K - 1) + slot_of(ox, oy, oz, R)) * a.tile + e) * 8 + j;
                 if (sizeof(WT) == 4) w = reinterpret_cast<const float*>(wt)[idx];

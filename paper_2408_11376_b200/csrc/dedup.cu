@@ -169,15 +169,15 @@ __global__ void __launch_bounds__(256) expand_kernel(const ExpandArgs a)
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const int* c0 = a.class_pad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
     {
-        float d[8];
+        float2 d[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int c = (real && x + j < a.nx) ? c0[j] : -1;
-            d[j] = c >= 0 ? a.class_diag[c] : 0.f;
+            d[j] = c >= 0 ? a.class_diag[c] : make_float2(0.f, 0.f);
         }
         float4* dp = reinterpret_cast<float4*>(a.diag + ((size_t)tile * a.tile + e) * 8);
-        dp[0] = make_float4(d[0], d[1], d[2], d[3]);
-        dp[1] = make_float4(d[4], d[5], d[6], d[7]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dp[j] = make_float4(d[2 * j].x, d[2 * j].y, d[2 * j + 1].x, d[2 * j + 1].y);
     }
     for (int r = -1; r < LL; ++r) {  // r = −1: the centre row first (slot order of layout.cuh)
         if (r == R * L + R) continue;
@@ -242,9 +242,9 @@ __global__ void chunk_class_kernel(const int* __restrict__ class_pad, int nx, in
 
 // ukf[u][slot] = class_w[k(u)][o(slot)] decoded to fp32; udiag[u] = class_diag[k(u)]
 template <typename WT>
-__global__ void ukf_kernel(const WT* __restrict__ class_w, const float* __restrict__ class_diag,
+__global__ void ukf_kernel(const WT* __restrict__ class_w, const float2* __restrict__ class_diag,
                            const int* __restrict__ used, const int* __restrict__ uid, long n_class, int R,
-                           float* __restrict__ ukf, float* __restrict__ udiag)
+                           float* __restrict__ ukf, float2* __restrict__ udiag)
 {
     const int L = 2 * R + 1, K = L * L * L;
     const long n = n_class * (long)(K - 1);
@@ -298,7 +298,7 @@ cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, Uni
     const int K = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
     const long nu1 = nu > 0 ? nu : 1;
     if (e == cudaSuccess) e = cudaMalloc(&t->ukf, nu1 * (K - 1) * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&t->udiag, nu1 * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&t->udiag, nu1 * 8);
     if (e == cudaSuccess && nu > 0) {
         const long n = n_class * (long)(K - 1);
         if (fmt == 0)
@@ -499,14 +499,14 @@ __global__ void __launch_bounds__(256) expand_mx8_kernel(const ExpandArgs a)
     }
 }
 
-// diag[target s] = fp32(1 − Σ_{o≠0} decoded W_s(o)) in fp64 (kgen's mass fix, reading A10), the
+// diag[target s] = fp32_pair(1 − Σ_{o≠0} decoded W_s(o)) in fp64 (kgen's mass fix, reading A10), the
 // source's weights read back from the gather blocks at targets s + o (one thread per source,
 // x fastest: neighbouring threads read neighbouring bytes).  Sources outside the domain
 // (class −1) and dummy targets keep 0.  One rank (the whole grid is the slab).
 template <int R, int TT>  // TT: the tile width when it is 256 (shifts instead of divisions), else 0
 __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int nzl, const int* __restrict__ cmap,
                                                        const int* __restrict__ chunk_u, const float* __restrict__ ukq,
-                                                       float* __restrict__ udiag_t)
+                                                       float2* __restrict__ udiag_t)
 {
     constexpr int L = 2 * R + 1, K = L * L * L;
     const long n = (long)a.nx * a.ny * nzl;
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
         const int cls = a.class_pad[(sz + R) * plane + (long)(sy + R) * nxp + kPadX + sx];
         const int q0 = sy * a.nxq + (sx >> 3);
         const size_t ch0 = ((size_t)sz * a.tpp + q0 / T_) * T_ + q0 % T_;
-        float* dp = a.diag + ch0 * 8 + (sx & 7);
+        float2* dp = a.diag + ch0 * 8 + (sx & 7);
         if (cmap) {  // N4 storage: compact dense position, or the uniform list position
             const int m = cmap[ch0];
             dp = m >= 0 ? a.diag + (size_t)m * 8 + (sx & 7) : udiag_t + (size_t)(-m - 2) * 8 + (sx & 7);
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
             dp = a.diag + (size_t)m * 8 + (sx & 7);
         }
         if (cls < 0) {
-            *dp = 0.f;
+            *dp = make_float2(0.f, 0.f);
             continue;
         }
         double off = 0.0;
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(256) mx8_diag_kernel(const ExpandArgs a, int n
                 }
             }
         }
-        *dp = (float)((a.class_mass ? a.class_mass[cls] : 1.0) - off);
+        *dp = fp32_pair((a.class_mass ? a.class_mass[cls] : 1.0) - off);
     }
 }
 
@@ -628,9 +628,9 @@ static cudaError_t launch_expand_r(const ExpandArgs& a, int fmt, cudaStream_t s)
         if (ut) {
             const long nch = (long)a.nzl * a.tpp * a.tile;
             e = cudaMalloc(&ut->chunk_map, nch * 4);
-            if (e == cudaSuccess) e = cudaMalloc(&ut->udiag_t, (size_t)std::max<long>(ut->n_uniform, 1) * 8 * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&ut->udiag_t, (size_t)std::max<long>(ut->n_uniform, 1) * 8 * 8);
             if (e == cudaSuccess) e = cudaMemsetAsync(ut->chunk_map, 0xff, nch * 4, s);
-            if (e == cudaSuccess) e = cudaMemsetAsync(ut->udiag_t, 0, (size_t)std::max<long>(ut->n_uniform, 1) * 32, s);
+            if (e == cudaSuccess) e = cudaMemsetAsync(ut->udiag_t, 0, (size_t)std::max<long>(ut->n_uniform, 1) * 64, s);
             if (e == cudaSuccess && ut->n_u > 0) {
                 const long n = (long)ut->n_u * (K - 1);
                 mx8_uniform_quant_kernel<<<grid_n(n), 256, 0, s>>>(ut->ukf, n);
@@ -645,7 +645,7 @@ static cudaError_t launch_expand_r(const ExpandArgs& a, int fmt, cudaStream_t s)
         }
         if (a.n_tiles > 0) {
             expand_mx8_kernel<R><<<a.n_tiles, a.tile, 0, s>>>(a);
-            e = cudaMemsetAsync(a.diag, 0, (size_t)a.n_tiles * a.tile * 8 * 4, s);
+            e = cudaMemsetAsync(a.diag, 0, (size_t)a.n_tiles * a.tile * 8 * 8, s);
             if (e != cudaSuccess) return e;
         }
         if (a.tile == 256)

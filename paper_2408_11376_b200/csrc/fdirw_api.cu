@@ -33,7 +33,7 @@ struct fdirw_ctx {
     bool is_virtual = false;
     int fmt = 0, b_w = 4;
     void* Wt = nullptr;
-    float* diag = nullptr;
+    float2* diag = nullptr;       // fp32 pair (hi, lo) per target (reading A10)
     float* cpad[2] = {nullptr, nullptr};
     double* mass_partial = nullptr;
     double* mass_out = nullptr;
@@ -609,7 +609,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
         // identical windows ⇒ identical kernels: compute each distinct window once (dedup.cu)
         int* class_pad = nullptr;
         void* class_w = nullptr;
-        float* class_diag = nullptr;
+        float2* class_diag = nullptr;
         double* class_mass = nullptr;  // MX8: each class kernel's own mass (N2 open windows < 1)
         DedupResult dr;
         auto dfree = [&]() {
@@ -625,7 +625,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             dedup = false;  // hash collision detected by the exact check: take the direct path
         } else {
             if ((st = alloc(&class_w, (size_t)dr.n_class * g.K * c->b_w, "class kernels")) != FDIRW_OK ||
-                (st = alloc((void**)&class_diag, (size_t)dr.n_class * 4, "class diagonal")) != FDIRW_OK ||
+                (st = alloc((void**)&class_diag, (size_t)dr.n_class * 8, "class diagonal")) != FDIRW_OK ||
                 (c->fmt == FDIRW_W_MX8 &&
                  (st = alloc((void**)&class_mass, (size_t)dr.n_class * 8, "class mass")) != FDIRW_OK)) {
                 dfree(); cudaFree(mask_d); return bail(st);
@@ -664,7 +664,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             }
             if (e == cudaSuccess) {
                 if ((st = alloc(&c->Wt, wbytes(c->fmt, w_elems ? w_elems : 8), "weights")) != FDIRW_OK ||
-                    (st = alloc((void**)&c->diag, (d_elems ? d_elems : 1) * 4, "diagonal")) != FDIRW_OK) {
+                    (st = alloc((void**)&c->diag, (d_elems ? d_elems : 1) * 8, "diagonal")) != FDIRW_OK) {
                     dfree(); cudaFree(mask_d); return bail(st);
                 }
                 ea.Wt = c->Wt;
@@ -692,14 +692,14 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     if (!dedup) {
         ka.src_list = nullptr; ka.n_list = 0; ka.class_w = nullptr; ka.class_diag = nullptr;
         if ((st = alloc(&c->Wt, g.w_elems * c->b_w, "weights")) != FDIRW_OK ||
-            (st = alloc((void**)&c->diag, g.diag_elems * 4, "diagonal")) != FDIRW_OK) {
+            (st = alloc((void**)&c->diag, g.diag_elems * 8, "diagonal")) != FDIRW_OK) {
             cudaFree(mask_d);
             return bail(st);
         }
         ka.Wt = c->Wt;
         ka.diag = c->diag;
         BAIL_CUDA(cudaMemsetAsync(c->Wt, 0, g.w_elems * c->b_w, s));
-        BAIL_CUDA(cudaMemsetAsync(c->diag, 0, g.diag_elems * 4, s));
+        BAIL_CUDA(cudaMemsetAsync(c->diag, 0, g.diag_elems * 8, s));
         if (!c->kev[0]) BAIL_CUDA(cudaEventCreate(&c->kev[0]));
         if (!c->kev[1]) BAIL_CUDA(cudaEventCreate(&c->kev[1]));
         BAIL_CUDA(cudaEventRecord(c->kev[0], s));
@@ -1391,10 +1391,10 @@ extern "C" fdirw_status fdirw_query(const fdirw_ctx* c, fdirw_info* info)
     info->lambda_fs = c->d.lam_fs;
     info->lambda_slow = c->d.lam_ss;
     const uint64_t wt_tiles = (c->ut.chunk_u || c->compact) ? (uint64_t)c->ut.nd_tiles : (uint64_t)g.n_tiles;  // N4 / N2 compact
-    info->weight_bytes = wbytes(c->fmt, wt_tiles * (g.K - 1) * g.tile * kChunk) + wt_tiles * g.tile * kChunk * 4;
+    info->weight_bytes = wbytes(c->fmt, wt_tiles * (g.K - 1) * g.tile * kChunk) + wt_tiles * g.tile * kChunk * 8;
     info->state_bytes = (uint64_t)g.state_elems * 4 * 2;
-    info->bytes_per_voxel_update = c->fmt == FDIRW_W_MX8 ? (uint64_t)((g.K - 1) * 9 + 4) / 8 + 12  // rounded
-                                                         : (uint64_t)(g.K - 1) * c->b_w + 12;
+    info->bytes_per_voxel_update = c->fmt == FDIRW_W_MX8 ? (uint64_t)((g.K - 1) * 9 + 4) / 8 + 16  // rounded
+                                                         : (uint64_t)(g.K - 1) * c->b_w + 16;
     info->voxels = (uint64_t)g.nx * g.ny * g.nzl;
     info->tile_chunks = g.tile;
     info->n_tiles = g.n_tiles;
@@ -1437,7 +1437,7 @@ extern "C" fdirw_status fdirw_make_plan(const fdirw_params* p, const fdirw_dist*
     pl->pad_x0 = kPadX;
     pl->halo_elems = h.count;
     pl->send_lo = h.send_lo; pl->recv_lo = h.recv_lo; pl->send_hi = h.send_hi; pl->recv_hi = h.recv_hi;
-    pl->weight_bytes = (uint64_t)wbytes(p->weights, g.w_elems) + (uint64_t)g.diag_elems * 4;
+    pl->weight_bytes = (uint64_t)wbytes(p->weights, g.w_elems) + (uint64_t)g.diag_elems * 8;
     pl->state_bytes = (uint64_t)g.state_elems * 8;
     pl->n_fd = d.n_fd;
     std::vector<float> cheb;
@@ -1483,7 +1483,7 @@ extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k
     const Geometry& g = c->g;
     const int R = g.R, L = g.L, K = g.K;
     std::vector<unsigned char> wt(g.w_elems * c->b_w, 0);
-    std::vector<float> dg(g.diag_elems, 0.f);
+    std::vector<float2> dg(g.diag_elems, make_float2(0.f, 0.f));
     for (int sz = 0; sz < g.nz; ++sz)
         for (int sy = 0; sy < g.ny; ++sy)
             for (int sx = 0; sx < g.nx; ++sx) {
@@ -1496,7 +1496,7 @@ extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k
                     const size_t tile = (size_t)z * g.tpp + q / g.tile;
                     const int e = q % g.tile, j = x & 7;
                     if (o == K / 2) {
-                        dg[(tile * g.tile + e) * 8 + j] = (float)ks[o];
+                        dg[(tile * g.tile + e) * 8 + j] = fp32_pair(ks[o]);
                         continue;
                     }
                     const size_t idx = ((tile * (size_t)(K - 1) + slot_of(ox, oy, oz, R)) * g.tile + e) * 8 + j;
@@ -1513,7 +1513,7 @@ extern "C" fdirw_status fdirw_debug_upload_weights(fdirw_ctx* c, const double* k
                 }
             }
     CUDA_TRY(cudaMemcpy(c->Wt, wt.data(), wt.size(), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->diag, dg.data(), dg.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->diag, dg.data(), dg.size() * 8, cudaMemcpyHostToDevice));
     return FDIRW_OK;
 }
 

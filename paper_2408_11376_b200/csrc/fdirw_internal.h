@@ -18,7 +18,7 @@ constexpr int kMaxR = 8;
 // Target-slab geometry and the gather layout of the weights.
 //   chunk q (within a plane) = y·nxq + x/8; tile tp = q / tile; element e = q % tile; j = x % 8
 //   tile index t = (z − z0)·tpp + tp
-//   Wt[t][slot][e][j] (slot = window offset o minus the centre), diag[t][e][j] fp32
+//   Wt[t][slot][e][j] (slot = window offset o minus the centre), diag[t][e][j] fp32 pair (hi, lo) = float2 (reading A10)
 //   padded state: [nzl + 2R][ny + 2R][nxp], nxp = 8·nxq + 16, x offset kPadX
 struct Geometry {
     int nx, ny, nz, R, L, K;
@@ -30,6 +30,15 @@ struct Geometry {
     int mz0, mz1;                // device mask planes [mz0, mz1)
     int sz0, sz1;                // source planes whose windows reach the slab
 };
+
+// The diagonal d_s = M − Σ_{o≠0} W̃_s(o) (fp64) stored as an fp32 pair (reading A10): hi = RNE_fp32(d),
+// lo = RNE_fp32(d − hi), so a stored column sums to M within ~2^-48 (one fp32 diagonal rounds d
+// the same way for a whole class of identical windows: a mass bias of ~1e-8 per step).
+__host__ __device__ inline float2 fp32_pair(double d)
+{
+    const float hi = (float)d;
+    return make_float2(hi, (float)(d - (double)hi));
+}
 
 Geometry make_geometry(int nx, int ny, int nz, int R, int z0, int z1, bool balance = false);
 
@@ -74,14 +83,14 @@ struct KgenArgs {
     float mu2_ff, mu2_fs, mu2_ss;
     int fmt, mass_fix;
     void* Wt;
-    float* diag;
+    float2* diag;
     int nxq, tile, tpp, K;
     // class mode (dedup.cu): process src_list[0..n_list) (linear source indices within
     // planes [sz0, sz1)) and write class-major class_w[i][K] (storage format) + class_diag[i]
     const int* src_list;
     long n_list;
     void* class_w;
-    float* class_diag;
+    float2* class_diag;
     double* class_mass = nullptr;  // MX8: each class kernel's own mass M (1 closed; < 1 open, N2)
 };
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s);
@@ -113,9 +122,9 @@ struct UniformTables;
 struct ExpandArgs {
     const int* class_pad;
     const void* class_w;
-    const float* class_diag;
+    const float2* class_diag;
     void* Wt;
-    float* diag;
+    float2* diag;
     int nx, ny, nxq, tile, tpp, n_tiles, nxp, nyp;
     const int* list = nullptr;  // N4: compacted chunk ids (null = tile/e is the chunk)
     long n_list = 0;
@@ -133,7 +142,7 @@ cudaError_t build_uniform(const ExpandArgs& a, int R, int fmt, long n_class, Uni
 struct SuperArgs {
     const float* cpad;   // padded state, pointer to padded plane 0
     const void* Wt;
-    const float* diag;
+    const float2* diag;
     float* out;          // output element (z=0 of slab, y=0, x=0)
     long out_ps, out_rs; // output plane / row strides (elements)
     int nx, ny, nxq, tile, tpp, K;
@@ -179,8 +188,8 @@ struct UniArgs {
     const int4* blocks;   // {start in list, count ≤ 256, class u, 0}
     int n_blocks;
     const float* ukf;     // [u][K−1] class kernels in slot order, decoded to fp32
-    const float* udiag;   // [u] fp32 diagonal
-    const float* udiag_t = nullptr;  // MX8: per-target diagonal [list position][8] (replaces udiag)
+    const float2* udiag;  // [u] fp32-pair diagonal (hi, lo)
+    const float2* udiag_t = nullptr;  // MX8: per-target diagonal [list position][8] (replaces udiag)
 };
 cudaError_t launch_superpose_uniform(const UniArgs& a, int R, cudaStream_t s);
 cudaError_t launch_superpose_mixed(const SuperArgs& a, const UniArgs& u, int R, int fmt, cudaStream_t s);
@@ -188,7 +197,7 @@ cudaError_t launch_superpose_mixed(const SuperArgs& a, const UniArgs& u, int R, 
 struct UniformTables {
     int* chunk_u = nullptr;   // [n_tiles·tile] class u or −1
     float* ukf = nullptr;
-    float* udiag = nullptr;
+    float2* udiag = nullptr;
     int* list = nullptr;
     int4* blocks = nullptr;
     int n_blocks = 0, n_u = 0;
@@ -198,7 +207,7 @@ struct UniformTables {
     int nd_tiles = 0;
     // MX8: a target's diagonal depends on its neighbours' blocks, so uniform
     // chunks carry a per-target diagonal; chunk_map = compact index (≥ 0) or −(list pos + 2)
-    float* udiag_t = nullptr;
+    float2* udiag_t = nullptr;
     int* chunk_map = nullptr;
 };
 
@@ -218,7 +227,7 @@ struct StudyArgs {
     const float* cpad;
     float* out;           // padded layout
     const void* Wt;
-    const float* diag;
+    const float2* diag;
     int nx, ny, nzl, nxq, tile, tpp, nxp, nyp, R;
     const float* pbc;
     const double* far_state;
@@ -247,7 +256,7 @@ cudaError_t launch_pack(const float* c, float* cpad, const Geometry& g, cudaStre
                         const uint8_t* farmask = nullptr);
 cudaError_t launch_unpack(const float* cpad, float* c, const Geometry& g, cudaStream_t s);
 cudaError_t launch_mass(const float* c, size_t n, double* partial, int nblk, double* out, cudaStream_t s);
-cudaError_t launch_export(const void* Wt, const float* diag, const Geometry& g, int fmt, const int32_t* box,
+cudaError_t launch_export(const void* Wt, const float2* diag, const Geometry& g, int fmt, const int32_t* box,
                           double* out, cudaStream_t s, const int* chunk_pos = nullptr);
 
 // ---- NCCL (comm.cpp): dlopen'ed, no link-time dependency ------------------------

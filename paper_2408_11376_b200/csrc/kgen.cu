@@ -471,10 +471,10 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         }
         const double off = block_sum_f64<S::NW>(qsum, red);
         if (t == R * L + R && a.class_w) {
-            a.class_diag[it] = a.mass_fix ? (float)(M - off) : centre_q;
+            a.class_diag[it] = a.mass_fix ? fp32_pair(M - off) : make_float2(centre_q, 0.f);
             if (a.class_mass) a.class_mass[it] = M;
         } else if (t == R * L + R && sz >= a.z0 && sz < a.z1) {
-            const float d = a.mass_fix ? (float)(M - off) : centre_q;
+            const float2 d = a.mass_fix ? fp32_pair(M - off) : make_float2(centre_q, 0.f);
             const int zl = sz - a.z0;
             const int q = sy * a.nxq + (sx >> 3);
             const size_t tile = (size_t)zl * a.tpp + q / a.tile;

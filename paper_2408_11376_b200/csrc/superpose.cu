@@ -52,6 +52,23 @@ __device__ __forceinline__ uint4 ld_stream(const void* ptr, uint64_t pol)
 
 __device__ __forceinline__ float4 ld_c(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
+// The diagonal term of 8 targets, d·C_old(x) with d = dh + dl an fp32 pair (reading A10):
+// hi = RN(dh·C), lo = (dh·C − hi) + dl·C (the product's exact error by FMA, then the low part).
+// dp = 8 float2 (64 B, 16-byte aligned), c = C_old(x .. x+7).
+__device__ __forceinline__ void diag_pair_init(const float2* dp, const float* c, float hi[8], float lo[8])
+{
+    const float4 v0 = ld_c(c), v1 = ld_c(c + 4);
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float4 d = __ldg(reinterpret_cast<const float4*>(dp) + k);  // (dh, dl) of targets 2k, 2k+1
+        hi[2 * k] = __fmul_rn(d.x, v[2 * k]);
+        lo[2 * k] = fmaf(d.y, v[2 * k], fmaf(d.x, v[2 * k], -hi[2 * k]));
+        hi[2 * k + 1] = __fmul_rn(d.z, v[2 * k + 1]);
+        lo[2 * k + 1] = fmaf(d.w, v[2 * k + 1], fmaf(d.z, v[2 * k + 1], -hi[2 * k + 1]));
+    }
+}
+
 template <typename WT>
 struct WLoad;
 
@@ -308,20 +325,18 @@ __device__ __forceinline__ void uniform_body(const UniArgs& a, int blk, float* w
     const int y = q / a.nxq, x = (q % a.nxq) * 8;
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
-    const float d = a.udiag[b.z];
-    float dd[8] = {d, d, d, d, d, d, d, d};
-    if (a.udiag_t) {  // MX8: per-target diagonal (DESIGN §15)
-        const float4 d0 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8));
-        const float4 d1 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8 + 4));
-        dd[0] = d0.x; dd[1] = d0.y; dd[2] = d0.z; dd[3] = d0.w; dd[4] = d1.x; dd[5] = d1.y; dd[6] = d1.z; dd[7] = d1.w;
-    }
     float hi[8], lo[8];
-    {
+    if (a.udiag_t) {  // MX8: per-target diagonal (DESIGN §15)
+        diag_pair_init(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8, c0, hi, lo);
+    } else {          // the class's diagonal for all 8 targets
+        const float2 d = a.udiag[b.z];
         const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
-        hi[0] = dd[0] * v0.x; hi[1] = dd[1] * v0.y; hi[2] = dd[2] * v0.z; hi[3] = dd[3] * v0.w;
-        hi[4] = dd[4] * v1.x; hi[5] = dd[5] * v1.y; hi[6] = dd[6] * v1.z; hi[7] = dd[7] * v1.w;
+        const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) lo[j] = 0.f;
+        for (int j = 0; j < 8; ++j) {
+            hi[j] = __fmul_rn(d.x, v[j]);
+            lo[j] = fmaf(d.y, v[j], fmaf(d.x, v[j], -hi[j]));
+        }
     }
     do_row_u<R, true>(c0 - 8, ws, hi, lo);
     const float* wr = ws + (L - 1);
@@ -432,18 +447,13 @@ __device__ __forceinline__ TileCtx tile_ctx(const SuperArgs& a, int blk, int e)
     return t;
 }
 
-// hi = d·C_old(x) (the diagonal term first, DESIGN §6 order), lo = 0
+// (hi, lo) = d·C_old(x) (the diagonal term first, DESIGN §6 order)
 __device__ __forceinline__ void diag_init(const SuperArgs& a, const TileCtx& t, int e, float hi[8], float lo[8])
 {
 #pragma unroll
     for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.f;
     if (!t.real) return;
-    const float* dp = a.diag + ((size_t)t.tile * a.tile + e) * 8;
-    const float4 d0 = __ldg(reinterpret_cast<const float4*>(dp));
-    const float4 d1 = __ldg(reinterpret_cast<const float4*>(dp + 4));
-    const float4 v0 = ld_c(t.c0), v1 = ld_c(t.c0 + 4);
-    hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
-    hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
+    diag_pair_init(a.diag + ((size_t)t.tile * a.tile + e) * 8, t.c0, hi, lo);
 }
 
 // Stored row i of a tile (i = 0: the centre row, L − 1 slots; i ≥ 1: row r of (oz, oy)
@@ -910,15 +920,9 @@ __device__ __forceinline__ void uniform_body_mx8(const UniArgs& a, int blk, floa
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
     float hi[8], lo[8], p[8];
-    {
-        const float4 d0 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8));
-        const float4 d1 = __ldg(reinterpret_cast<const float4*>(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8 + 4));
-        const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
-        hi[0] = d0.x * v0.x; hi[1] = d0.y * v0.y; hi[2] = d0.z * v0.z; hi[3] = d0.w * v0.w;
-        hi[4] = d1.x * v1.x; hi[5] = d1.y * v1.y; hi[6] = d1.z * v1.z; hi[7] = d1.w * v1.w;
+    diag_pair_init(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8, c0, hi, lo);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) lo[j] = p[j] = 0.f;
-    }
+    for (int j = 0; j < 8; ++j) p[j] = 0.f;
     float seg[24];
     int n = 0;  // stored row index (0: the centre row)
     const float* wr = ws;
@@ -1476,7 +1480,7 @@ cudaError_t launch_mass(const float* c, size_t n, double* partial, int nblk, dou
 }
 
 // Decode the stored kernels of the sources in `box` back to per-source fp64 arrays.
-__global__ void export_kernel(const void* __restrict__ Wt, const float* __restrict__ diag, Geometry g, int fmt,
+__global__ void export_kernel(const void* __restrict__ Wt, const float2* __restrict__ diag, Geometry g, int fmt,
                               int bx0, int bx, int by0, int by, int bz0, int bz, double* __restrict__ out,
                               const int* __restrict__ chunk_pos)
 {
@@ -1504,7 +1508,8 @@ __global__ void export_kernel(const void* __restrict__ Wt, const float* __restri
                 // impermeable solid targets): the centre weight is 1, every other 0
                 v = (cp == -2 && o == g.K / 2) ? 1.0 : 0.0;
             } else if (o == g.K / 2) {
-                v = diag[(tile * g.tile + e) * 8 + j];
+                const float2 d = diag[(tile * g.tile + e) * 8 + j];
+                v = (double)d.x + (double)d.y;  // the fp32 pair (reading A10), exact in fp64
             } else if (fmt == FDIRW_W_MX8) {
                 size_t mo, so;
                 mx8_addr(tile, slot_of(ox, oy, oz, g.R), e, j, g.L, g.K, g.tile, &mo, &so);
@@ -1521,7 +1526,7 @@ __global__ void export_kernel(const void* __restrict__ Wt, const float* __restri
     }
 }
 
-cudaError_t launch_export(const void* Wt, const float* diag, const Geometry& g, int fmt, const int32_t* box,
+cudaError_t launch_export(const void* Wt, const float2* diag, const Geometry& g, int fmt, const int32_t* box,
                           double* out, cudaStream_t s, const int* chunk_pos)
 {
     const int bx = box[1] - box[0], by = box[3] - box[2], bz = box[5] - box[4];

@@ -226,7 +226,12 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         unsigned long long lxm2[NPR > 0 ? NPR : 1], lxp2[NPR > 0 ? NPR : 1], lym2[NPR > 0 ? NPR : 1],
             lyp2[NPR > 0 ? NPR : 1];
         float lxm1, lxp1, lym1, lyp1;
-        auto faces = [&](const float fff, const float ffs, const float fss) {
+        // Chebyshev passes (reading A30) in the operator's row form: 2Â t = D∘t + Σ_f F_f t_f with
+        // F_f = 2μ_f and the cell's own coefficient D = 2 − Σ_f F_f (fp64 sum, rounded once), so Â
+        // keeps constants as stored.  Packed like the lateral numbers (dg2 pairs, dg1 the last cell).
+        unsigned long long dg2[NPR > 0 ? NPR : 1];
+        float dg1 = 0.f;
+        auto faces = [&](const float fff, const float ffs, const float fss, const bool row_form) {
             float v[4][L];
 #pragma unroll
             for (int z = 0; z < L; ++z) {
@@ -242,6 +247,19 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
                 }
                 if (col && p == 3u) rmask |= 1u << z;
             }
+            if (row_form) {
+                float d[L];
+#pragma unroll
+                for (int z = 0; z < L; ++z) {
+                    double f = (double)v[0][z] + (double)v[1][z] + (double)v[2][z] + (double)v[3][z];
+                    if (z > 0) f += (double)fz[z - 1];
+                    if (z < L - 1) f += (double)fz[z];
+                    d[z] = col ? (float)(2.0 - f) : 0.f;
+                }
+#pragma unroll
+                for (int h = 0; h < NPR; ++h) dg2[h] = pk2(d[2 * h], d[2 * h + 1]);
+                dg1 = d[L - 1];
+            }
 #pragma unroll
             for (int h = 0; h < NPR; ++h) {
                 lxm2[h] = pk2(v[0][2 * h], v[0][2 * h + 1]);
@@ -254,7 +272,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
             lym1 = v[2][L - 1];
             lyp1 = v[3][L - 1];
         };
-        faces(a.lam_ff, a.lam_fs, a.lam_ss);
+        faces(a.lam_ff, a.lam_fs, a.lam_ss, false);
 #pragma unroll
         for (int z = 0; z < Lp; ++z) c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
 
@@ -364,7 +382,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
             // pass of the direct substep's cost (+2 FMA): pre + m ≈ 8 + 157 passes instead of
             // n_fd = 1000 at Table 1's λ = 0.1.
             // State: c[] = t (A), pv[] = t_{k−1} (B) overwritten in place by t_{k+1}, acc[] = p.
-            faces(a.mu2_ff, a.mu2_fs, a.mu2_ss);
+            faces(a.mu2_ff, a.mu2_fs, a.mu2_ss, true);
             const float* cc = reinterpret_cast<const float*>(smem_raw + S::cheb_off);
             float pv[Lp], acc[L];
 #pragma unroll
@@ -378,21 +396,50 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
                 __syncthreads();
                 const float ck = cc[k + 1];
                 if (act) {
+                    // nw = D∘t − t_{k−1}, then the z faces (registers: they run while the
+                    // neighbours' loads are in flight), then −x, +x, −y, +y: 8 lane-FMAs per
+                    // cell-pass with p's update (the flux form took 13)
+                    float xm[L], xp[L], ym[L], yp[L];
+                    load_col(b, t + axm, xm);
+                    load_col(b, t + axp, xp);
+                    load_col(b, t + oym, ym);
+                    load_col(b, t + oyp, yp);
                     float nw[Lp];
 #pragma unroll
                     for (int h = 0; h < NPR; ++h) {
                         const unsigned long long s2 =
-                            fma2(pk2(2.f, 2.f), pk2(cur[2 * h], cur[2 * h + 1]), pk2(-prv[2 * h], -prv[2 * h + 1]));
+                            fma2(dg2[h], pk2(cur[2 * h], cur[2 * h + 1]), pk2(-prv[2 * h], -prv[2 * h + 1]));
                         upk2(s2, nw[2 * h], nw[2 * h + 1]);
                     }
-                    nw[L - 1] = fmaf(2.f, cur[L - 1], -prv[L - 1]);
-                    flux(b, cur, nw);
+                    nw[L - 1] = fmaf(dg1, cur[L - 1], -prv[L - 1]);
 #pragma unroll
                     for (int z = 0; z < L; ++z) {
                         float v = nw[z];
+                        if (z > 0) v = fmaf(fz[z - 1], cur[z - 1], v);
+                        if (z < L - 1) v = fmaf(fz[z], cur[z + 1], v);
+                        nw[z] = v;
+                    }
+#pragma unroll
+                    for (int h = 0; h < NPR; ++h) {
+                        unsigned long long s2 = pk2(nw[2 * h], nw[2 * h + 1]);
+                        s2 = fma2(lxm2[h], pk2(xm[2 * h], xm[2 * h + 1]), s2);
+                        s2 = fma2(lxp2[h], pk2(xp[2 * h], xp[2 * h + 1]), s2);
+                        s2 = fma2(lym2[h], pk2(ym[2 * h], ym[2 * h + 1]), s2);
+                        s2 = fma2(lyp2[h], pk2(yp[2 * h], yp[2 * h + 1]), s2);
+                        if (first) s2 = fma2(s2, pk2(0.5f, 0.5f), pk2(-0.f, -0.f));  // exact halving
+                        upk2(s2, prv[2 * h], prv[2 * h + 1]);
+                        const unsigned long long a2 = fma2(pk2(ck, ck), s2, pk2(acc[2 * h], acc[2 * h + 1]));
+                        upk2(a2, acc[2 * h], acc[2 * h + 1]);
+                    }
+                    {
+                        float v = nw[L - 1];
+                        v = fmaf(lxm1, xm[L - 1], v);
+                        v = fmaf(lxp1, xp[L - 1], v);
+                        v = fmaf(lym1, ym[L - 1], v);
+                        v = fmaf(lyp1, yp[L - 1], v);
                         if (first) v *= 0.5f;
-                        prv[z] = v;
-                        acc[z] = fmaf(ck, v, acc[z]);
+                        prv[L - 1] = v;
+                        acc[L - 1] = fmaf(ck, v, acc[L - 1]);
                     }
                 }
             };

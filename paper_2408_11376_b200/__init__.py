@@ -36,6 +36,7 @@ F_KGEN_FP64 = 8  # kgen in fp64, the oracle's operation order (reading A22, debu
 F_SYMMETRIC_RULE = 16  # exact regime only: gather weights = own kernel reflected (reading A24)
 F_KGEN_DIRECT = 32  # kgen runs the n_fd substeps literally instead of the Chebyshev recurrence (reading A30)
 F_NO_BULK_STREAM = 64  # superposition: per-thread weight loads instead of TMA-staged rows (same bits)
+F_KGEN_COLUMNS = 128  # R = 5 kgen: one window column per thread (round-1 kernel) instead of pairs (A/B)
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",

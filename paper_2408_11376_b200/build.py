@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfdirw.so")
-SOURCES = ["fdirw_api.cu", "kgen.cu", "superpose.cu", "dedup.cu", "coarse.cu", "absorb.cu", "p2p.cu", "comm.cpp"]
-HEADERS = ["fdirw_internal.h", "layout.cuh", "bulk.cuh", "mx8.cuh"]
+SOURCES = ["fdirw_api.cu", "kgen.cu", "kgen_pairs.cu", "superpose.cu", "dedup.cu", "coarse.cu", "absorb.cu", "p2p.cu", "comm.cpp"]
+HEADERS = ["fdirw_internal.h", "layout.cuh", "bulk.cuh", "mx8.cuh", "kgen_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]

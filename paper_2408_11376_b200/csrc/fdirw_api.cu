@@ -307,7 +307,7 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
                                          "KGEN_FP64");
     }
     if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE | FDIRW_F_KGEN_FP64 |
-                     FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT | FDIRW_F_NO_BULK_STREAM))
+                     FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT | FDIRW_F_NO_BULK_STREAM | FDIRW_F_KGEN_COLUMNS))
         return fail(FDIRW_E_INVALID, "unknown flags");
     if ((p->flags & FDIRW_F_SYMMETRIC_RULE) && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_SYMMETRIC_RULE is not combined with FDIRW_F_DEDUP_STORAGE");
@@ -600,6 +600,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     }
     ka.fmt = c->fmt == FDIRW_W_MX8 ? FDIRW_W_FP32 : c->fmt;  // MX8: quantised by the expand pass
     ka.mass_fix = (params->flags & FDIRW_F_NO_MASS_FIX) ? 0 : 1;
+    ka.columns = (params->flags & FDIRW_F_KGEN_COLUMNS) ? 1 : 0;
     ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;
     c->kgen_sources = (uint64_t)g.nx * g.ny * (ka.sz1 - ka.sz0);
     c->kgen_windows = c->kgen_sources;

@@ -82,6 +82,7 @@ struct KgenArgs {
     const float* cheb_c;
     float mu2_ff, mu2_fs, mu2_ss;
     int fmt, mass_fix;
+    int columns = 0;      // FDIRW_F_KGEN_COLUMNS: the one-column-per-thread kernel at R = 5 (A/B)
     void* Wt;
     float2* diag;
     int nxq, tile, tpp, K;
@@ -94,6 +95,7 @@ struct KgenArgs {
     double* class_mass = nullptr;  // MX8: each class kernel's own mass M (1 closed; < 1 open, N2)
 };
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s);
+cudaError_t launch_kgen_pairs(const KgenArgs& a, int R, cudaStream_t s);  // R = 5 (kgen_pairs.cu)
 
 // ---- a6 over peer memory (p2p.cu) -------------------------------------------------
 cudaError_t p2p_preload();  // loads every kernel a P2P step launches (lazy loading can wait for the device)

@@ -22,9 +22,11 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "fdirw_internal.h"
+#include "kgen_common.cuh"
 #include "layout.cuh"
 
 namespace fdirw {
@@ -39,73 +41,13 @@ struct KgenShape {
     static constexpr int Lp = (L + 3) / 4 * 4;                             // column padded to float4s
     static constexpr size_t smem_floats = 2 * (size_t)NT * Lp;             // double-buffered, column-major
     static constexpr size_t buf_bytes = smem_floats * (F64 ? 8 : 4);
-    static constexpr size_t smem_bytes = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
+    static constexpr size_t tab_off = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;  // face tables
+    static constexpr size_t smem_bytes = tab_off + 64 * 4;
     static constexpr size_t cheb_off = smem_bytes;  // Chebyshev coefficients c_0..c_m (fp32) follow
     // CTAs per SM the register allocation is sized for: ~128 registers per thread (R5 measured
     // 3 → 4 CTAs: −2.5 % kernel time; R7 would spill 212 B at 2 CTAs, so it keeps 1)
     static constexpr int kMinBlocks = (R != 7 && 65536 / (NT * 128) > 1) ? 65536 / (NT * 128) : 1;
 };
-
-__device__ __forceinline__ double warp_sum_f64(double v)
-{
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Deterministic block reduction (fixed shuffle tree + fixed warp order).
-template <int NW>
-__device__ __forceinline__ double block_sum_f64(double v, double* red)
-{
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    v = warp_sum_f64(v);
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-        double w = lane < NW ? red[lane] : 0.0;
-        w = warp_sum_f64(w);
-        if (lane == 0) red[NW] = w;
-    }
-    __syncthreads();
-    const double r = red[NW];
-    __syncthreads();
-    return r;
-}
-
-// Packed fp32x2 arithmetic (sm_100a FADD2/FFMA2): two cells per instruction, each
-// lane an ordinary IEEE fp32 add / fma — bitwise identical to the scalar form.
-__device__ __forceinline__ unsigned long long pk2(float a, float b)
-{
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void upk2(unsigned long long v, float& a, float& b)
-{
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b)
-{
-    unsigned long long r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c)
-{
-    unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
-__device__ __forceinline__ float face_lambda(unsigned p, unsigned q, float ff, float fs, float ss)
-{
-    // p, q ∈ {0 slow, 1 fast, 2 outside the domain, 3 far-field reservoir (N2)}.  A far
-    // cell is a fast-phase Dirichlet cell held at 0: faces into it carry flux, its own
-    // value never changes (p = 3 → no update).
-    if (p > 1u || q == 2u) return 0.f;
-    if (q == 3u) q = 1u;
-    return (p & q) ? ff : ((p | q) ? fs : ss);
-}
 
 __device__ __forceinline__ double face_lambda_d(unsigned p, unsigned q, const double* lam)
 {
@@ -145,6 +87,8 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
     const int nx = a.nx, ny = a.ny, nz = a.nz;
     const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
+    float* ftab = reinterpret_cast<float*>(smem_raw + S::tab_off);
+    if (!F64) build_face_tables(ftab, a.lam_ff, a.lam_fs, a.lam_ss, a.mu2_ff, a.mu2_fs, a.mu2_ss);
     if (!F64 && a.cheb_m) {
         float* cc = reinterpret_cast<float*>(smem_raw + S::cheb_off);
         for (int i = t; i <= a.cheb_m; i += NT) cc[i] = a.cheb_c[i];
@@ -231,19 +175,19 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         // keeps constants as stored.  Packed like the lateral numbers (dg2 pairs, dg1 the last cell).
         unsigned long long dg2[NPR > 0 ? NPR : 1];
         float dg1 = 0.f;
-        auto faces = [&](const float fff, const float ffs, const float fss, const bool row_form) {
+        auto faces = [&](const float* T, const bool row_form) {  // T: face table set (λ or 2μ)
             float v[4][L];
 #pragma unroll
             for (int z = 0; z < L; ++z) {
                 const int i = z * LL + t;
                 const unsigned p = col ? ph[i] : 2u;
-                v[0][z] = (col && oxm) ? face_lambda(p, ph[i + oxm], fff, ffs, fss) : 0.f;
-                v[1][z] = (col && oxp) ? face_lambda(p, ph[i + oxp], fff, ffs, fss) : 0.f;
-                v[2][z] = (col && oym) ? face_lambda(p, ph[i + oym], fff, ffs, fss) : 0.f;
-                v[3][z] = (col && oyp) ? face_lambda(p, ph[i + oyp], fff, ffs, fss) : 0.f;
+                v[0][z] = (col && oxm) ? T[(p << 2) | ph[i + oxm]] : 0.f;
+                v[1][z] = (col && oxp) ? T[(p << 2) | ph[i + oxp]] : 0.f;
+                v[2][z] = (col && oym) ? T[(p << 2) | ph[i + oym]] : 0.f;
+                v[3][z] = (col && oyp) ? T[(p << 2) | ph[i + oyp]] : 0.f;
                 if (z < L - 1) {
                     const unsigned q = col ? ph[i + LL] : 2u;
-                    fz[z] = col ? (p <= 1u ? face_lambda(p, q, fff, ffs, fss) : face_lambda(q, p, fff, ffs, fss)) : 0.f;
+                    fz[z] = col ? T[16 + ((p << 2) | q)] : 0.f;
                 }
                 if (col && p == 3u) rmask |= 1u << z;
             }
@@ -272,7 +216,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
             lym1 = v[2][L - 1];
             lyp1 = v[3][L - 1];
         };
-        faces(a.lam_ff, a.lam_fs, a.lam_ss, false);
+        faces(ftab, false);
 #pragma unroll
         for (int z = 0; z < Lp; ++z) c[z] = (col && t == R * L + R && z == R) ? 1.f : 0.f;
 
@@ -382,7 +326,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
             // pass of the direct substep's cost (+2 FMA): pre + m ≈ 8 + 157 passes instead of
             // n_fd = 1000 at Table 1's λ = 0.1.
             // State: c[] = t (A), pv[] = t_{k−1} (B) overwritten in place by t_{k+1}, acc[] = p.
-            faces(a.mu2_ff, a.mu2_fs, a.mu2_ss, true);
+            faces(ftab + 32, true);
             const float* cc = reinterpret_cast<const float*>(smem_raw + S::cheb_off);
             float pv[Lp], acc[L];
 #pragma unroll
@@ -555,6 +499,8 @@ static cudaError_t launch_kgen_r(const KgenArgs& a, cudaStream_t s)
 
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s)
 {
+    // R = 5 (cfg3/cfg4): two columns per thread (kgen_pairs.cu) unless FDIRW_F_KGEN_COLUMNS (A/B)
+    if (!a.columns && R == 5 && !a.fp64 && !a.symmetric) return launch_kgen_pairs(a, R, s);
     if (a.fp64) {
         switch (R) {
             case 1: return launch_kgen_r<1, true>(a, s);

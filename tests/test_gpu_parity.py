@@ -271,6 +271,48 @@ def test_virtual_ranks_bitwise(fd, oracle_lib, world):
     assert rel_l2(got, ref) <= 5e-3
 
 
+@pytest.mark.parametrize("fmt,far,direct", [("fp32", False, False), ("bf16", False, False), ("fp32", True, False),
+                                            ("fp32", False, True)])
+def test_kgen_pairs_equal_columns(fd, oracle_lib, fmt, far, direct):
+    """R = 5: the two-columns-per-thread kgen (kgen_pairs.cu, the default) against the one-column
+    kernel (FDIRW_F_KGEN_COLUMNS) and the oracle.  The substep / recurrence arithmetic is the same
+    operation for operation, so the stored weights agree except where the fp64 epilogue sum
+    (grouped per thread differently) moves a renormalised weight across a rounding boundary:
+    at most one fp32 ulp, on a small fraction of the weights.  Closed and open (N2) windows,
+    Chebyshev and literal substeps, dedup and direct kgen."""
+    shape = (21, 23, 22)
+    mask = fi.porous_particle(shape, 7, pore_r=(1.0, 2.0), porosity=0.3, seed=3)
+    if far:
+        mask = fi.with_far_field(mask, 8, 3.0)
+    cfg = small_cfg(shape, 5, 1000, D_slow=1e-3, weights=fmt)
+    pb = oracle_problem(cfg, mask)
+    Wo = oracle_lib.quantize(pb, oracle_lib.build_kernels(pb), fmt)
+    box = (0, shape[2], 0, shape[1], 0, shape[0])
+    out = {}
+    for name, flags in (("pairs", 0), ("columns", fd.F_KGEN_COLUMNS), ("pairs_nodedup", fd.F_NO_DEDUP)):
+        flags |= fd.F_KGEN_DIRECT if direct else 0
+        ctx = fd.build_kernels(lib_params(cfg, fmt, flags, v_far=1e3 if far else 0.0), mask)
+        try:
+            out[name] = fd.export_kernels(ctx, box)
+        finally:
+            fd.destroy(ctx)
+    src = (mask != 2).reshape(-1)
+    c = pb.K // 2
+    off = np.ones(pb.K, bool)
+    off[c] = False
+    P, C = out["pairs"].reshape(-1, pb.K)[src], out["columns"].reshape(-1, pb.K)[src]
+    np.testing.assert_array_equal(out["pairs"], out["pairs_nodedup"])  # dedup is bit-exact
+    d = np.abs(P[:, off] - C[:, off])
+    ulp = {"fp32": 2.0 ** -23, "bf16": 2.0 ** -7}[fmt]
+    assert np.all(d <= ulp * np.abs(C[:, off]) + 1e-30)
+    assert np.count_nonzero(d) <= 1e-3 * d.size
+    np.testing.assert_allclose(P[:, c], C[:, c], rtol=1e-6, atol=1e-13)
+    if fmt == "fp32" and not far:  # and as close to the oracle as the column kernel
+        Wo2 = Wo.reshape(-1, pb.K)[src]
+        ep, ec = rel_l2(P[:, off], Wo2[:, off]), rel_l2(C[:, off], Wo2[:, off])
+        assert ep <= 1e-5 and ep <= 1.01 * ec, (ep, ec)
+
+
 @pytest.mark.parametrize("fmt,far", [("fp32", False), ("bf16", False), ("fp16", True)])
 def test_kgen_fp64_flag_equals_oracle_bits(fd, oracle_lib, fmt, far):
     """FDIRW_F_KGEN_FP64 (reading A22): fp64 substeps in the oracle's operation order and no

@@ -38,16 +38,18 @@ template <int R>
 struct PairShape {
     static constexpr int L = 2 * R + 1, LL = L * L, LLL = LL * L;
     static constexpr int NC = 6;                         // cells per z segment (head, quad, tail)
-    static_assert(2 * NC >= L && NC < L, "two z segments of 6 cells");
+    static constexpr int NSEG = (L + 1) / NC;            // z segments; the last one's tail is a phantom
+    static_assert(NSEG * NC == L + 1, "L = 6·NSEG − 1 (R = 2, 5, 8)");
     static constexpr int NP = (LL + 1) / 2;              // column pairs (the last may hold a dummy)
     static constexpr int NPW = (NP + 31) / 32 * 32;      // threads per z segment
-    static constexpr int NT = 2 * NPW;
+    static constexpr int NT = NSEG * NPW;
     static constexpr int NW = NT / 32;
-    static constexpr int PAD = 8;                        // > the largest pair offset, R + 1
-    static_assert(PAD > R + 1, "pad");
+    static constexpr int PAD = (R + 2 + 3) / 4 * 4;      // > the largest pair offset, R + 1
     static constexpr int NPP = (NPW + 2 * PAD + 3) / 4 * 4;  // slots per side
     static constexpr int SEGF = 2 * NPP * 6;             // floats per segment: H, Q (×4), T
-    static constexpr int BUFF = 2 * SEGF;                // floats per parity
+    static constexpr int BUFF = NSEG * SEGF;             // floats per parity
+    // ~128 registers per thread: R5 4 CTAs (16 warps) per SM, R8 1 CTA (15 warps)
+    static constexpr int kMinBlocks = 65536 / (NT * 128) > 0 ? 65536 / (NT * 128) : 1;
     static constexpr size_t buf_bytes = 2 * (size_t)BUFF * 4;
     static constexpr size_t tab_off = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;  // face tables
     static constexpr size_t smem_bytes = tab_off + 64 * 4;
@@ -56,9 +58,9 @@ struct PairShape {
 
 }  // namespace
 
-// One z segment's threads (SEG = 0: cells 0..5, 1: cells 6..10 + the phantom 11).  The two
-// segments' warps run separate instantiations and meet at the same CTA barriers (each warp is
-// uniform; both paths execute the identical barrier sequence).
+// One z segment's threads (cells 6·SEG … 6·SEG + 5; the last segment's cell L is a phantom).
+// The segments' warps run separate instantiations and meet at the same CTA barriers (each warp
+// is uniform; every path executes the identical barrier sequence).
 template <int R, int SEG>
 __device__ __forceinline__ void pair_body(const KgenArgs& a)
 {
@@ -82,7 +84,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
     const int jxmA = 1 * NPP + pp - 1, jymA = 1 * NPP + pp - (R + 1), jypA = 1 * NPP + pp + R;
     const int jxpB = 0 * NPP + pp + 1, jymB = 0 * NPP + pp - R, jypB = 0 * NPP + pp + R + 1;
     const int jA = pp, jB = NPP + pp;
-    constexpr bool lower = SEG == 0;
+    constexpr bool top = SEG == S::NSEG - 1;     // its tail cell is the phantom
+    constexpr bool hb = SEG > 0, ha = !top;      // halo cells below / above
     const int nx = a.nx, ny = a.ny, nz = a.nz;
     const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
@@ -102,21 +105,19 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
     auto store_seg = [&](float* b, int j, const float (&v)[NC]) {
         Hp(b, seg)[j] = v[0];
         Qp(b, seg)[j] = make_float4(v[1], v[2], v[3], v[4]);
-        if (lower) Tp(b, seg)[j] = v[5];
+        if (!top) Tp(b, seg)[j] = v[5];
     };
     auto load_seg = [&](const float* b, int j, float (&v)[NC]) {
         float* bb = const_cast<float*>(b);
         v[0] = Hp(bb, seg)[j];
         const float4 q = Qp(bb, seg)[j];
         v[1] = q.x; v[2] = q.y; v[3] = q.z; v[4] = q.w;
-        v[5] = lower ? Tp(bb, seg)[j] : 0.f;
+        v[5] = !top ? Tp(bb, seg)[j] : 0.f;
     };
-    // the other segment's boundary cell of column slot j: lower reads cell 6 (upper H),
-    // upper reads cell 5 (lower T)
-    auto load_halo = [&](const float* b, int j) {
-        float* bb = const_cast<float*>(b);
-        return lower ? Hp(bb, 1)[j] : Tp(bb, 0)[j];
-    };
+    // the neighbouring segments' boundary cells of column slot j: below = segment SEG − 1's
+    // tail (cell zb − 1), above = segment SEG + 1's head (cell zb + 6)
+    auto load_below = [&](const float* b, int j) { return hb ? Tp(const_cast<float*>(b), hb ? seg - 1 : 0)[j] : 0.f; };
+    auto load_above = [&](const float* b, int j) { return ha ? Hp(const_cast<float*>(b), ha ? seg + 1 : 0)[j] : 0.f; };
 
     for (long it = blockIdx.x; it < nsrc; it += gridDim.x) {
         const long src = a.src_list ? (long)a.src_list[it] : it;
@@ -211,21 +212,23 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
         constexpr int PA[3] = {0, 1, 3}, PB[3] = {5, 2, 4};
 
         // neighbour values of side sd's lateral faces, f = −x, +x, −y, +y
-        auto gather = [&](const float* b, float (&nb)[2][4][NC], float (&hl)[2]) {
+        auto gather = [&](const float* b, float (&nb)[2][4][NC], float (&hlb)[2], float (&hla)[2]) {
             load_seg(b, jxmA, nb[0][0]);
             load_seg(b, jymA, nb[0][2]);
             load_seg(b, jypA, nb[0][3]);
             load_seg(b, jxpB, nb[1][1]);
             load_seg(b, jymB, nb[1][2]);
             load_seg(b, jypB, nb[1][3]);
-            hl[0] = load_halo(b, jA);
-            hl[1] = load_halo(b, jB);
+            hlb[0] = load_below(b, jA);
+            hlb[1] = load_below(b, jB);
+            hla[0] = load_above(b, jA);
+            hla[1] = load_above(b, jB);
         };
 
         const bool act = real;
         const bool cheb = a.cheb_m && !open;
         const int n_direct = cheb ? a.cheb_pre : a.n_fd;
-        // ---- literal substeps: flux form, z faces first (the column kernel's R ≤ 5 order) ----
+        // ---- literal substeps: flux form (the column kernel's operation order) ----
         for (int k = 0; k < n_direct; ++k) {
             float* b = buf + (k & 1) * S::BUFF;
             if (act) {
@@ -234,8 +237,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
             }
             __syncthreads();
             if (act) {
-                float nb[2][4][NC], hl[2];
-                gather(b, nb, hl);
+                float nb[2][4][NC], hlb[2], hla[2];
+                gather(b, nb, hlb, hla);
 #pragma unroll
                 for (int i = 0; i < NC; ++i) {  // the x face between the pair: registers
                     nb[0][1][i] = c[1][i];
@@ -248,17 +251,24 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
                     float dz[NC + 1];
 #pragma unroll
                     for (int j = 0; j <= NC; ++j) {
-                        const float up = j < NC ? c[sd][j] : (lower ? hl[sd] : 0.f);
-                        const float dn = j > 0 ? c[sd][j - 1] : (lower ? 0.f : hl[sd]);
+                        const float up = j < NC ? c[sd][j] : hla[sd];
+                        const float dn = j > 0 ? c[sd][j - 1] : hlb[sd];
                         dz[j] = up - dn;
                     }
+                    // the z faces before the lateral ones for R ≤ 5, after them for R > 5: the
+                    // column kernel's order per R, so both kernels give the same bits
+                    auto zterms = [&]() {
 #pragma unroll
-                    for (int i = 0; i < NC; ++i) {
-                        float v = c[sd][i];
-                        if (below(i)) v = fmaf(fz[sd][i], -dz[i], v);
-                        if (above(i)) v = fmaf(fz[sd][i + 1], dz[i + 1], v);
-                        nw[sd][i] = v;
-                    }
+                        for (int i = 0; i < NC; ++i) {
+                            float v = nw[sd][i];
+                            if (below(i)) v = fmaf(fz[sd][i], -dz[i], v);
+                            if (above(i)) v = fmaf(fz[sd][i + 1], dz[i + 1], v);
+                            nw[sd][i] = v;
+                        }
+                    };
+#pragma unroll
+                    for (int i = 0; i < NC; ++i) nw[sd][i] = c[sd][i];
+                    if constexpr (R <= 5) zterms();
 #pragma unroll
                     for (int h = 0; h < 3; ++h) {
                         const int i0 = PA[h], i1 = PB[h];
@@ -269,6 +279,7 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
                             s2 = fma2(FL(sd, f, h), sub2(pk2(nb[sd][f][i0], nb[sd][f][i1]), c2), s2);
                         upk2(s2, nw[sd][i0], nw[sd][i1]);
                     }
+                    if constexpr (R > 5) zterms();
                 }
 #pragma unroll
                 for (int sd = 0; sd < 2; ++sd)
@@ -297,8 +308,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
                 __syncthreads();
                 const float ck = cc[k + 1];
                 if (act) {
-                    float nb[2][4][NC], hl[2];
-                    gather(b, nb, hl);
+                    float nb[2][4][NC], hlb[2], hla[2];
+                    gather(b, nb, hlb, hla);
 #pragma unroll
                     for (int i = 0; i < NC; ++i) {
                         nb[0][1][i] = cur[1][i];
@@ -317,8 +328,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
 #pragma unroll
                         for (int i = 0; i < NC; ++i) {
                             float v = nw[i];
-                            const float dn = i > 0 ? cur[sd][i - 1] : hl[sd];
-                            const float up = i < NC - 1 ? cur[sd][i + 1] : hl[sd];
+                            const float dn = i > 0 ? cur[sd][i - 1] : hlb[sd];
+                            const float up = i < NC - 1 ? cur[sd][i + 1] : hla[sd];
                             if (below(i)) v = fmaf(fz[sd][i], dn, v);
                             if (above(i)) v = fmaf(fz[sd][i + 1], up, v);
                             nw[i] = v;
@@ -412,8 +423,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
             }
         }
         const double off = block_sum_f64<S::NW>(qsum, red);
-        // the centre cell (column R·L + R = 2·(R·L + R)/2, z = R) is the lower segment's
-        const bool centre = real && lower && col[0] == R * L + R;
+        // the centre cell: column R·L + R (a pair's left column: R·L + R is even), z = R
+        const bool centre = real && SEG == R / NC && col[0] == R * L + R;
         if (centre && a.class_w) {
             a.class_diag[it] = a.mass_fix ? fp32_pair(M - off) : make_float2(centre_q, 0.f);
             if (a.class_mass) a.class_mass[it] = M;
@@ -428,34 +439,51 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
 }
 
 template <int R>
-__global__ void __launch_bounds__(PairShape<R>::NT, 4) kgen_pair_kernel(const KgenArgs a)
+__global__ void __launch_bounds__(PairShape<R>::NT, PairShape<R>::kMinBlocks) kgen_pair_kernel(const KgenArgs a)
 {
-    if (threadIdx.x < PairShape<R>::NPW) pair_body<R, 0>(a);
-    else pair_body<R, 1>(a);
+    constexpr int NPW = PairShape<R>::NPW;
+    if constexpr (PairShape<R>::NSEG == 1) {
+        pair_body<R, 0>(a);
+    } else if constexpr (PairShape<R>::NSEG == 2) {
+        if (threadIdx.x < NPW) pair_body<R, 0>(a);
+        else pair_body<R, 1>(a);
+    } else {
+        static_assert(PairShape<R>::NSEG == 3, "R = 2, 5, 8");
+        if (threadIdx.x < NPW) pair_body<R, 0>(a);
+        else if (threadIdx.x < 2 * NPW) pair_body<R, 1>(a);
+        else pair_body<R, 2>(a);
+    }
 }
 
-// R = 5, fp32 substeps, no symmetric rule; returns cudaErrorNotSupported otherwise so the caller
-// falls back to the column kernel.
-cudaError_t launch_kgen_pairs(const KgenArgs& a, int R, cudaStream_t s)
+template <int R>
+static cudaError_t launch_pairs_r(const KgenArgs& a, cudaStream_t s)
 {
-    if (R != 5 || a.fp64 || a.symmetric) return cudaErrorNotSupported;
-    using S = PairShape<5>;
-    static_assert((5 * 11 + 5) % 2 == 0, "the centre column is a pair's left column");
+    using S = PairShape<R>;
     const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
     if (nsrc <= 0) return cudaSuccess;
     const size_t smem = S::smem_bytes + (!a.cheb_m ? 0 : ((size_t)(a.cheb_m + 1) * 4 + 15) / 16 * 16);
-    cudaError_t e = cudaFuncSetAttribute(kgen_pair_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kgen_pair_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_pair_kernel<5>, S::NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_pair_kernel<R>, S::NT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     long grid = (long)sms * per_sm;
     if (grid > nsrc) grid = nsrc;
-    kgen_pair_kernel<5><<<(unsigned)grid, S::NT, smem, s>>>(a);
+    kgen_pair_kernel<R><<<(unsigned)grid, S::NT, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+// R = 5 and 8 (L = 6·NSEG − 1), fp32 substeps, no symmetric rule; cudaErrorNotSupported
+// otherwise (the caller keeps the column kernel).
+cudaError_t launch_kgen_pairs(const KgenArgs& a, int R, cudaStream_t s)
+{
+    if (a.fp64 || a.symmetric) return cudaErrorNotSupported;
+    if (R == 5) return launch_pairs_r<5>(a, s);
+    if (R == 8) return launch_pairs_r<8>(a, s);
+    return cudaErrorNotSupported;
 }
 
 }  // namespace fdirw

@@ -271,20 +271,21 @@ def test_virtual_ranks_bitwise(fd, oracle_lib, world):
     assert rel_l2(got, ref) <= 5e-3
 
 
-@pytest.mark.parametrize("fmt,far,direct", [("fp32", False, False), ("bf16", False, False), ("fp32", True, False),
-                                            ("fp32", False, True)])
-def test_kgen_pairs_equal_columns(fd, oracle_lib, fmt, far, direct):
-    """R = 5: the two-columns-per-thread kgen (kgen_pairs.cu, the default) against the one-column
+@pytest.mark.parametrize("R,fmt,far,direct", [(5, "fp32", False, False), (5, "bf16", False, False),
+                                              (5, "fp32", True, False), (5, "fp32", False, True),
+                                              (8, "fp32", False, False), (8, "bf16", True, False)])
+def test_kgen_pairs_equal_columns(fd, oracle_lib, R, fmt, far, direct):
+    """R = 5 and 8: the two-columns-per-thread kgen (kgen_pairs.cu, the default) against the one-column
     kernel (FDIRW_F_KGEN_COLUMNS) and the oracle.  The substep / recurrence arithmetic is the same
     operation for operation, so the stored weights agree except where the fp64 epilogue sum
     (grouped per thread differently) moves a renormalised weight across a rounding boundary:
     at most one fp32 ulp, on a small fraction of the weights.  Closed and open (N2) windows,
     Chebyshev and literal substeps, dedup and direct kgen."""
-    shape = (21, 23, 22)
-    mask = fi.porous_particle(shape, 7, pore_r=(1.0, 2.0), porosity=0.3, seed=3)
+    shape = (21, 23, 22) if R == 5 else (13, 14, 12)
+    mask = fi.porous_particle(shape, 7 if R == 5 else 5, pore_r=(1.0, 2.0), porosity=0.3, seed=3)
     if far:
-        mask = fi.with_far_field(mask, 8, 3.0)
-    cfg = small_cfg(shape, 5, 1000, D_slow=1e-3, weights=fmt)
+        mask = fi.with_far_field(mask, 8 if R == 5 else 5, 3.0 if R == 5 else 1.0)
+    cfg = small_cfg(shape, R, 1000, D_slow=1e-3, weights=fmt)
     pb = oracle_problem(cfg, mask)
     Wo = oracle_lib.quantize(pb, oracle_lib.build_kernels(pb), fmt)
     box = (0, shape[2], 0, shape[1], 0, shape[0])

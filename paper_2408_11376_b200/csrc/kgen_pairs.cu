@@ -74,8 +74,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
 
     const int t = threadIdx.x;
     constexpr int seg = SEG;
-    const int p = t - SEG * S::NPW;             // column pair
-    constexpr int zb = SEG * NC;
+    const int p = t - seg * S::NPW;             // column pair
+    constexpr int zb = seg * NC;
     const bool real = p < S::NP;
     const int col[2] = {2 * p, 2 * p + 1};
     const bool has[2] = {real, real && 2 * p + 1 < LL};
@@ -84,13 +84,17 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
     const int jxmA = 1 * NPP + pp - 1, jymA = 1 * NPP + pp - (R + 1), jypA = 1 * NPP + pp + R;
     const int jxpB = 0 * NPP + pp + 1, jymB = 0 * NPP + pp - R, jypB = 0 * NPP + pp + R + 1;
     const int jA = pp, jB = NPP + pp;
-    constexpr bool top = SEG == S::NSEG - 1;     // its tail cell is the phantom
-    constexpr bool hb = SEG > 0, ha = !top;      // halo cells below / above
+    constexpr bool top = seg == S::NSEG - 1;     // its tail cell is the phantom
+    constexpr bool hb = seg > 0, ha = !top;      // halo cells below / above
     const int nx = a.nx, ny = a.ny, nz = a.nz;
     const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
     // zero both pass buffers once: PAD and dummy slots are read, never written
     for (int i = t; i < 2 * S::BUFF; i += S::NT) buf[i] = 0.f;
+    // one __syncthreads per pass (a neighbour-only sync through per-warp mbarriers, which lets
+    // warps drift up to a pass apart, was measured slower: cfg3 150 vs 114 ms, cfg5 852 vs 654 ms)
+    auto pass_sync = [&](unsigned) { __syncthreads(); };
+    unsigned ps = 0;  // passes so far (all windows): buffer parity and mbarrier phase
     float* ftab = reinterpret_cast<float*>(smem_raw + S::tab_off);
     build_face_tables(ftab, a.lam_ff, a.lam_fs, a.lam_ss, a.mu2_ff, a.mu2_fs, a.mu2_ss);
     if (a.cheb_m) {
@@ -116,8 +120,11 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
     };
     // the neighbouring segments' boundary cells of column slot j: below = segment SEG − 1's
     // tail (cell zb − 1), above = segment SEG + 1's head (cell zb + 6)
-    auto load_below = [&](const float* b, int j) { return hb ? Tp(const_cast<float*>(b), hb ? seg - 1 : 0)[j] : 0.f; };
-    auto load_above = [&](const float* b, int j) { return ha ? Hp(const_cast<float*>(b), ha ? seg + 1 : 0)[j] : 0.f; };
+    // (unconditional loads: an edge segment reads its own slot, a finite value that no z term
+    // uses — the below / above guards skip the window's first and last cells)
+    constexpr int sb = hb ? seg - 1 : seg, sa = ha ? seg + 1 : seg;
+    auto load_below = [&](const float* b, int j) { return Tp(const_cast<float*>(b), sb)[j]; };
+    auto load_above = [&](const float* b, int j) { return Hp(const_cast<float*>(b), sa)[j]; };
 
     for (long it = blockIdx.x; it < nsrc; it += gridDim.x) {
         const long src = a.src_list ? (long)a.src_list[it] : it;
@@ -206,8 +213,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
                 c[sd][i] = (real && sd == 0 && col[0] == R * L + R && zb + i == R) ? 1.f : 0.f;
 
         // which z terms exist for cell i (the column kernel's z > 0 / z < L − 1 guards)
-        auto below = [](int i) { return zb + i > 0; };
-        auto above = [](int i) { return zb + i < L - 1; };
+        auto below = [&](int i) { return zb + i > 0; };
+        auto above = [&](int i) { return zb + i < L - 1; };
         // cell pairs for the packed lanes
         constexpr int PA[3] = {0, 1, 3}, PB[3] = {5, 2, 4};
 
@@ -229,13 +236,13 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
         const bool cheb = a.cheb_m && !open;
         const int n_direct = cheb ? a.cheb_pre : a.n_fd;
         // ---- literal substeps: flux form (the column kernel's operation order) ----
-        for (int k = 0; k < n_direct; ++k) {
-            float* b = buf + (k & 1) * S::BUFF;
+        for (int k = 0; k < n_direct; ++k, ++ps) {
+            float* b = buf + (ps & 1u) * S::BUFF;
             if (act) {
                 store_seg(b, jA, c[0]);
                 store_seg(b, jB, c[1]);
             }
-            __syncthreads();
+            pass_sync(ps);
             if (act) {
                 float nb[2][4][NC], hlb[2], hla[2];
                 gather(b, nb, hlb, hla);
@@ -300,12 +307,13 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
                     acc[sd][i] = c[sd][i] * cc[0];
                 }
             auto step = [&](float (&cur)[2][NC], float (&prv)[2][NC], const int k, const bool first) {
-                float* b = buf + ((k + n_direct) & 1) * S::BUFF;
+                float* b = buf + (ps & 1u) * S::BUFF;
                 if (act) {
                     store_seg(b, jA, cur[0]);
                     store_seg(b, jB, cur[1]);
                 }
-                __syncthreads();
+                pass_sync(ps);
+                ++ps;
                 const float ck = cc[k + 1];
                 if (act) {
                     float nb[2][4][NC], hlb[2], hla[2];
@@ -424,7 +432,7 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
         }
         const double off = block_sum_f64<S::NW>(qsum, red);
         // the centre cell: column R·L + R (a pair's left column: R·L + R is even), z = R
-        const bool centre = real && SEG == R / NC && col[0] == R * L + R;
+        const bool centre = real && seg == R / NC && col[0] == R * L + R;
         if (centre && a.class_w) {
             a.class_diag[it] = a.mass_fix ? fp32_pair(M - off) : make_float2(centre_q, 0.f);
             if (a.class_mass) a.class_mass[it] = M;
@@ -438,6 +446,8 @@ __device__ __forceinline__ void pair_body(const KgenArgs& a)
     }
 }
 
+// One instantiation per segment (measured faster than a single code path with the segment taken
+// at run time: cfg3 112 vs 124 ms, cfg5 693 vs 735 ms, despite R8's three paths' I-cache misses)
 template <int R>
 __global__ void __launch_bounds__(PairShape<R>::NT, PairShape<R>::kMinBlocks) kgen_pair_kernel(const KgenArgs a)
 {

@@ -407,8 +407,8 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
     (device time from CUDA events around its launch, fdirw_info.kgen_kernel_ms) runs the distinct
     windows only, kgen_steps stencil passes each (the Chebyshev degree m, reading A30, or n_fd):
     its rooflines count those passes.  Shared memory (128 B/clk/SM): the column kernel reads 4
-    lateral neighbours and writes its cell, 20 B per cell-pass; the pairs kernel (R = 5, 8; two
-    columns per thread over 6-cell z segments) moves 4.18 (R5) / 4.24 (R8) accesses of
+    lateral neighbours and writes its cell, 20 B per cell-pass; the balanced pairs kernel (R = 5,
+    8; two columns per thread over z segments) moves 4.23 (R5) / 4.29 (R8) accesses of
     4 B per cell-pass.  FP32 lanes: 11 lane-ops per literal substep cell, 8 per Chebyshev
     cell-pass (row form).  `vs_column_design` rates the same cell-passes against the round-1
     column kernel's 20 B ceiling."""
@@ -420,9 +420,9 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
     passes = info["kgen_windows"] * world * cfg.K * steps  # computed cell-passes
     rate = passes / (kms * 1e-3) if kms > 0 else 0.0
     pairs = cfg.R in (5, 8) and not (info.get("flags", 0) & 128)
-    # accesses per pair and pass / real cells per pair (kgen_pairs.cu header): R5 (38+12)+(32+10)
-    # over 22 cells, R8 (38+12)+(40+12)+(32+10) over 34 cells
-    smem_b = {5: 4.0 * 92 / 22, 8: 4.0 * 144 / 34}[cfg.R] if pairs else 20.0
+    # accesses per pair and pass / real cells per pair (kgen_bal.cu): R5 (35+11)+(35+12) over 22
+    # cells, R8 (35+11)+(40+13)+(35+12) over 34 cells
+    smem_b = {5: 4.0 * 93 / 22, 8: 4.0 * 146 / 34}[cfg.R] if pairs else 20.0
     smem_peak = 148 * 128 * mhz * 1e6
     ops = (8.0 * (steps - 8) + 11.0 * 8) / steps if cheb else 11.0
     alu_peak = 148 * 128 * mhz * 1e6 / ops
@@ -444,7 +444,7 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
                                  "128 B/clk x %.0f MHz" % (smem_b, steps, mhz)},
             "alu": {"achieved": rate, "peak": alu_peak, "unit": "cell-passes/s", "frac": rate / alu_peak,
                     "lane_ops_per_cell_pass": ops},
-            "kernel": "kgen_pair_kernel (2 columns/thread)" if pairs else "kgen_kernel (1 column/thread)",
+            "kernel": "kgen_bal_kernel (2 columns/thread, balanced z segments)" if pairs else "kgen_kernel (1 column/thread)",
             "vs_column_design": {"frac": rate * 20.0 / smem_peak,
                                  "note": "the same rate against the round-1 column kernel's 20 B/cell-pass "
                                          "shared-memory ceiling (%.2e cell-passes/s)" % (smem_peak / 20.0)}}

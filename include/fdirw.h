@@ -101,10 +101,10 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2, FDIRW_W_MX8
                                   loads instead of TMA bulk copies into shared-memory stages (the
                                   default for launches of >= 2 CTAs per SM).  Identical results;
                                   for A/B measurement                              */
-#define FDIRW_F_KGEN_COLUMNS 128u /* R = 5: kgen with one window column per thread (the round-1
-                                  kernel) instead of two columns per thread over half the z range
-                                  (kgen_pairs.cu).  The same substep arithmetic; the fp64 epilogue
-                                  sums group cells differently.  For A/B measurement */
+#define FDIRW_F_KGEN_COLUMNS 128u /* R = 5, 8: kgen with one window column per thread (the round-1
+                                  kernel) instead of two columns per thread over balanced z
+                                  segments (kgen_bal.cu).  The same substep arithmetic; the fp64
+                                  epilogue sums group cells differently.  For A/B   */
 
 /* The paper's problem statement (Table 1) + north_star's window radius / precision. */
 typedef struct {

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfdirw.so")
-SOURCES = ["fdirw_api.cu", "kgen.cu", "kgen_pairs.cu", "superpose.cu", "dedup.cu", "coarse.cu", "absorb.cu", "p2p.cu", "comm.cpp"]
+SOURCES = ["fdirw_api.cu", "kgen.cu", "kgen_bal.cu", "superpose.cu", "dedup.cu", "coarse.cu", "absorb.cu", "p2p.cu", "comm.cpp"]
 HEADERS = ["fdirw_internal.h", "layout.cuh", "bulk.cuh", "mx8.cuh", "kgen_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

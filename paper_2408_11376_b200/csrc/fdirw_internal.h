@@ -95,7 +95,7 @@ struct KgenArgs {
     double* class_mass = nullptr;  // MX8: each class kernel's own mass M (1 closed; < 1 open, N2)
 };
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s);
-cudaError_t launch_kgen_pairs(const KgenArgs& a, int R, cudaStream_t s);  // R = 5 (kgen_pairs.cu)
+cudaError_t launch_kgen_bal(const KgenArgs& a, int R, cudaStream_t s);    // R = 5, 8 (kgen_bal.cu)
 
 // ---- a6 over peer memory (p2p.cu) -------------------------------------------------
 cudaError_t p2p_preload();  // loads every kernel a P2P step launches (lazy loading can wait for the device)

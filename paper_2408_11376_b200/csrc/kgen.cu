@@ -499,9 +499,9 @@ static cudaError_t launch_kgen_r(const KgenArgs& a, cudaStream_t s)
 
 cudaError_t launch_kgen(const KgenArgs& a, int R, cudaStream_t s)
 {
-    // R = 5 (cfg3/cfg4) and R = 8 (cfg5): two columns per thread (kgen_pairs.cu) unless
-    // FDIRW_F_KGEN_COLUMNS (A/B)
-    if (!a.columns && (R == 5 || R == 8) && !a.fp64 && !a.symmetric) return launch_kgen_pairs(a, R, s);
+    // R = 5 (cfg3/cfg4) and R = 8 (cfg5): two columns per thread over balanced z segments
+    // (kgen_bal.cu) unless FDIRW_F_KGEN_COLUMNS (A/B)
+    if (!a.columns && (R == 5 || R == 8) && !a.fp64 && !a.symmetric) return launch_kgen_bal(a, R, s);
     if (a.fp64) {
         switch (R) {
             case 1: return launch_kgen_r<1, true>(a, s);

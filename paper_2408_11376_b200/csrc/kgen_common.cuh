@@ -1,4 +1,4 @@
-// kgen_common.cuh — device helpers shared by the kgen kernels (kgen.cu, kgen_pairs.cu):
+// kgen_common.cuh — device helpers shared by the kgen kernels (kgen.cu, kgen_bal.cu):
 // deterministic fp64 block sums, packed fp32x2 arithmetic (FADD2/FFMA2) and the face numbers
 // of the explicit-FD stencil (reading A4: harmonic-mean faces precomputed per phase pair).
 #pragma once

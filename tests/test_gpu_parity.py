@@ -274,8 +274,8 @@ def test_virtual_ranks_bitwise(fd, oracle_lib, world):
 @pytest.mark.parametrize("R,fmt,far,direct", [(5, "fp32", False, False), (5, "bf16", False, False),
                                               (5, "fp32", True, False), (5, "fp32", False, True),
                                               (8, "fp32", False, False), (8, "bf16", True, False)])
-def test_kgen_pairs_equal_columns(fd, oracle_lib, R, fmt, far, direct):
-    """R = 5 and 8: the two-columns-per-thread kgen (kgen_pairs.cu, the default) against the one-column
+def test_kgen_bal_equal_columns(fd, oracle_lib, R, fmt, far, direct):
+    """R = 5 and 8: the two-columns-per-thread kgen (kgen_bal.cu, the default) against the one-column
     kernel (FDIRW_F_KGEN_COLUMNS) and the oracle.  The substep / recurrence arithmetic is the same
     operation for operation, so the stored weights agree except where the fp64 epilogue sum
     (grouped per thread differently) moves a renormalised weight across a rounding boundary:

@@ -1,6 +1,6 @@
-# every BASELINE config and NEXT-row mode through bench.py, one JSON line each → gpurun_out/r02_bench_<name>.json
+# every BASELINE config and NEXT-row mode through bench.py, one JSON line each → gpurun_out/bench_<name>.json (copy the ones to keep into profiles/<round>_bench_<name>.json)
 python -c "import __graft_entry__ as g; g.build()"
-run() { name=$1; shift; timeout 900 python bench.py "$@" > gpurun_out/r02_bench_$name.json 2> gpurun_out/r02_bench_$name.err; echo "$name rc=$?"; }
+run() { name=$1; shift; timeout 900 python bench.py "$@" > gpurun_out/bench_$name.json 2> gpurun_out/bench_$name.err; echo "$name rc=$?"; }
 run cfg1 --config cfg1 --steps 200 --warmup 10 --no-scaling-384
 run cfg2 --config cfg2 --steps 200 --warmup 10
 run cfg2_fp32 --config cfg2 --weights fp32 --steps 200 --warmup 10 --no-variants

@@ -167,7 +167,8 @@ __global__ void kin_partial_kernel(const float* __restrict__ c, const uint8_t* _
 // first version cost ~38 µs per macro step)
 __global__ void __launch_bounds__(256) kin_final_kernel(const double* __restrict__ part, int nblk,
                                                         double* __restrict__ far_state, double v_far, double n_solid,
-                                                        double cSeq, int far, double* __restrict__ rec)
+                                                        double cSeq, int far, double* __restrict__ rec,
+                                                        int* __restrict__ ctr)
 {
     __shared__ double rs[8], rl[8];
     double s = 0.0, l = 0.0;
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(256) kin_final_kernel(const double* __restrict
     l = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { s += rs[w]; l += rl[w]; }
     if (far) far_state[0] = (far_state[1] - s - l) / v_far;  // (4) Eq.7 after the whole step
+    if (ctr) rec += 4 * (size_t)(*ctr)++;  // graph replay: the record slot from a device counter
     rec[0] = s;
     rec[1] = l;
     rec[2] = far ? far_state[0] : 0.0;
@@ -207,7 +209,7 @@ cudaError_t launch_phase_pad(const uint8_t* mask, const Geometry& g, uint8_t* pp
 
 cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uint8_t* pp, const Geometry& g,
                                const AbsorbArgs& ab, double* part, double* far_state, double v_far, int far,
-                               double* rec, cudaStream_t s, float** result)
+                               double* rec, cudaStream_t s, float** result, int* ctr)
 {
     const long n = (long)g.nx * g.ny * g.nz;
     // (2) solid FD, n_s passes
@@ -224,7 +226,7 @@ cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uin
     // (4)+(5)
     const int nblk = 148 * 4;
     kin_partial_kernel<<<nblk, 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, part);
-    kin_final_kernel<<<1, 256, 0, s>>>(part, nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec);
+    kin_final_kernel<<<1, 256, 0, s>>>(part, nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec, ctr);
     *result = cur;
     return cudaGetLastError();
 }

@@ -78,6 +78,12 @@ struct fdirw_ctx {
     double* kin_part = nullptr;
     double* kin_rec = nullptr;
     int kin_cap = 0;
+    // N3 loop replay: two macro steps captured once (graph_abs), the kinetics record slot taken
+    // from a device counter; recaptured when the loop's parameters or record buffer change
+    cudaGraphExec_t graph_abs = nullptr;
+    int* abs_ctr = nullptr;
+    AbsorbArgs abs_key{};
+    const double* abs_rec_key = nullptr;
     double n_solid = 0;
     // a6 over peer memory (FDIRW_TRANSPORT_P2P)
     int transport = FDIRW_TRANSPORT_NCCL;
@@ -392,6 +398,8 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->alpha);
     cudaFree(c->kin_part);
     cudaFree(c->kin_rec);
+    cudaFree(c->abs_ctr);
+    if (c->graph_abs) cudaGraphExecDestroy(c->graph_abs);
     cudaFree(c->ut.chunk_u);
     cudaFree(c->ut.dense_list);
     cudaFree(c->ut.ukf);
@@ -1466,6 +1474,10 @@ extern "C" fdirw_status fdirw_debug_stage_canary(fdirw_ctx* c, int32_t enable, u
             cudaGraphExecDestroy(c->graph2);
             c->graph2 = nullptr;
         }
+        if (c->graph_abs) {
+            cudaGraphExecDestroy(c->graph_abs);
+            c->graph_abs = nullptr;
+        }
     }
     unsigned long long h[2] = {0, 0};
     if (c->canary) CUDA_TRY(cudaMemcpy(h, c->canary, 16, cudaMemcpyDeviceToHost));
@@ -1650,6 +1662,10 @@ extern "C" fdirw_status fdirw_set_precision_mode(fdirw_ctx* c, int32_t mode)
         cudaGraphExecDestroy(c->graph2);
         c->graph2 = nullptr;
     }
+    if (c->graph_abs) {
+        cudaGraphExecDestroy(c->graph_abs);
+        c->graph_abs = nullptr;
+    }
     c->prec_mode = mode;
     return FDIRW_OK;
 }
@@ -1687,18 +1703,50 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
         c->kin_cap = n;
     }
     if (n == 0) return FDIRW_OK;
+    if (!c->abs_ctr && (st = alloc((void**)&c->abs_ctr, 4, "kinetics counter")) != FDIRW_OK) return st;
     CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s, c->farmask));
+    CUDA_TRY(cudaMemsetAsync(c->abs_ctr, 0, 4, s));
     const size_t ioff = (size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX;
-    float* in = c->cpad[0];
-    for (int i = 0; i < n; ++i) {
+    // one macro step from `in`: (1) the liquid FDiRW step, (2)-(5) the tail; returns the buffer
+    // holding the result (which of the two depends on the number of solid FD passes)
+    auto macro = [&](float* in, cudaStream_t ss, float** res) -> fdirw_status {
         float* out = in == c->cpad[0] ? c->cpad[1] : c->cpad[0];
-        if ((st = enqueue_step(c, in, out + ioff, (long)g.plane_elems, g.nxp, s)) != FDIRW_OK) return st;  // (1)
-        float* res = nullptr;
+        fdirw_status sst = enqueue_step(c, in, out + ioff, (long)g.plane_elems, g.nxp, ss);
+        if (sst != FDIRW_OK) return sst;
         CUDA_TRY(launch_absorb_tail(out, in, c->alpha, c->phase_pp, g, ab, c->kin_part, c->far_state, c->v_far,
-                                    c->far ? 1 : 0, c->kin_rec + 4 * (size_t)i, s, &res));  // (2)-(5)
-        in = res;
+                                    c->far ? 1 : 0, c->kin_rec, ss, res, c->abs_ctr));
+        return FDIRW_OK;
+    };
+    const bool same = c->graph_abs && c->abs_rec_key == c->kin_rec && c->abs_key.n_s == ab.n_s &&
+                      c->abs_key.lam_s == ab.lam_s && c->abs_key.kdt == ab.kdt && c->abs_key.cSeq == ab.cSeq &&
+                      c->abs_key.cLeq == ab.cLeq && c->abs_key.n_solid == ab.n_solid;
+    if (n >= 2 && !same) {  // capture two macro steps: they return the field to cpad[0]
+        if (c->graph_abs) cudaGraphExecDestroy(c->graph_abs);
+        c->graph_abs = nullptr;
+        cudaStream_t cs = c->capture_stream;
+        CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        float *r1 = nullptr, *r2 = nullptr;
+        st = macro(c->cpad[0], cs, &r1);
+        if (st == FDIRW_OK) st = macro(r1, cs, &r2);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        if (st != FDIRW_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+        if (e != cudaSuccess) return fail(FDIRW_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+        if (r2 != c->cpad[0]) { cudaGraphDestroy(graph); return fail(FDIRW_E_STATE, "absorb: two steps must return to the first buffer"); }
+        e = cudaGraphInstantiate(&c->graph_abs, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) { c->graph_abs = nullptr; return fail(FDIRW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)); }
+        c->abs_key = ab;
+        c->abs_rec_key = c->kin_rec;
     }
-    CUDA_TRY(launch_unpack(in, c_dev, g, s));
+    for (int i = 0; i < n / 2; ++i) CUDA_TRY(cudaGraphLaunch(c->graph_abs, s));
+    float* fin = c->cpad[0];
+    if (n & 1) {
+        float* res = nullptr;
+        if ((st = macro(c->cpad[0], s, &res)) != FDIRW_OK) return st;
+        fin = res;
+    }
+    CUDA_TRY(launch_unpack(fin, c_dev, g, s));
     if (kinetics_host) CUDA_TRY(cudaMemcpyAsync(kinetics_host, c->kin_rec, (size_t)n * 32, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return FDIRW_OK;

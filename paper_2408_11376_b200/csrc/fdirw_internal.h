@@ -224,7 +224,8 @@ struct AbsorbArgs {
 cudaError_t launch_phase_pad(const uint8_t* mask, const Geometry& g, uint8_t* pp, cudaStream_t s);
 cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uint8_t* pp, const Geometry& g,
                                const AbsorbArgs& ab, double* part, double* far_state, double v_far, int far,
-                               double* rec, cudaStream_t s, float** result);
+                               double* rec, cudaStream_t s, float** result,
+                               int* ctr = nullptr);
 struct StudyArgs {
     const float* cpad;
     float* out;           // padded layout

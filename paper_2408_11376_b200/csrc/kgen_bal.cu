@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "fdirw_internal.h"
@@ -81,7 +82,7 @@ struct BalSeg {
 
 }  // namespace
 
-template <int R, int SEG>
+template <int R, int SEG, bool CLEAN>
 __device__ __forceinline__ void bal_body(const KgenArgs& a)
 {
     using S = BalShape<R>;
@@ -166,7 +167,8 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
         const int sy = (int)((src / nx) % ny);
         const int sz = a.sz0 + (int)(src / ((long)nx * ny));
 
-        __syncthreads();
+        cta_sync_any_pc<S::NT, CLEAN>();  // (each segment's warps run their own instantiation:
+                                          // the CTA barriers of kgen_common.cuh)
         int far_here = 0;
         for (int i = t; i < LLL; i += S::NT) {
             const int gx = sx + i % L - R, gy = sy + (i / L) % L - R, gz = sz + i / LL - R;
@@ -176,7 +178,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
             far_here |= v == 3;
             ph[i] = v;
         }
-        const bool open = __syncthreads_or(far_here) != 0;
+        const bool open = cta_or_any_pc<S::NT, CLEAN>(far_here != 0);
         if (ph[KC] == 3) continue;
 
         // ---- face numbers: fl[sd][f][h] packed pairs, fl1[sd][f] the single cell; fz[sd][j] the
@@ -270,7 +272,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
         for (int k = 0; k < n_direct; ++k, ++ps) {
             float* b = buf + (ps & 1u) * S::BUFF;
             if (act) store_own(b, c[0], c[1]);
-            __syncthreads();
+            cta_sync_any_pc<S::NT, CLEAN>();
             if (act) {
                 float nb[2][4][6], h[4];
                 gather(b, c, nb, h);
@@ -332,7 +334,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
             auto step = [&](float (&cur)[2][6], float (&prv)[2][6], const int k, const bool first) {
                 float* b = buf + (ps & 1u) * S::BUFF;
                 if (act) store_own(b, cur[0], cur[1]);
-                __syncthreads();
+                cta_sync_any_pc<S::NT, CLEAN>();
                 ++ps;
                 const float ck = cc[k + 1];
                 if (act) {
@@ -404,7 +406,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
 #pragma unroll
             for (int i = 0; i < G::N(sd); ++i)
                 if (has[sd]) s += (double)c[sd][i];
-        const double S_ = block_sum_f64<S::NW>(s, red);
+        const double S_ = block_sum_f64<S::NW, true, CLEAN>(s, red);
         const double inv = open ? 1.0 : 1.0 / S_;
         const double M = open ? S_ : 1.0;
         double qsum = 0.0;
@@ -457,7 +459,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
                 else reinterpret_cast<unsigned short*>(a.Wt)[idx] = bits;
             }
         }
-        const double off = block_sum_f64<S::NW>(qsum, red);
+        const double off = block_sum_f64<S::NW, true, CLEAN>(qsum, red);
         const bool centre = real && col[0] == R * L + R && R >= G::zA && R < G::zA + NA;
         if (centre && a.class_w) {
             a.class_diag[it] = a.mass_fix ? fp32_pair(M - off) : make_float2(centre_q, 0.f);
@@ -472,47 +474,52 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
     }
 }
 
-template <int R>
+template <int R, bool CLEAN>
 __global__ void __launch_bounds__(BalShape<R>::NT, BalShape<R>::kMinBlocks) kgen_bal_kernel(const KgenArgs a)
 {
     constexpr int NPW = BalShape<R>::NPW;
     if constexpr (BalShape<R>::NSEG == 2) {
-        if (threadIdx.x < NPW) bal_body<R, 0>(a);
-        else bal_body<R, 1>(a);
+        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN>(a);
+        else bal_body<R, 1, CLEAN>(a);
     } else {
         static_assert(BalShape<R>::NSEG == 3, "R = 5, 8");
-        if (threadIdx.x < NPW) bal_body<R, 0>(a);
-        else if (threadIdx.x < 2 * NPW) bal_body<R, 1>(a);
-        else bal_body<R, 2>(a);
+        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN>(a);
+        else if (threadIdx.x < 2 * NPW) bal_body<R, 1, CLEAN>(a);
+        else bal_body<R, 2, CLEAN>(a);
     }
 }
 
-template <int R>
+template <int R, bool CLEAN>
 static cudaError_t launch_bal_r(const KgenArgs& a, cudaStream_t s)
 {
     using S = BalShape<R>;
     const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
     if (nsrc <= 0) return cudaSuccess;
     const size_t smem = S::smem_bytes + (!a.cheb_m ? 0 : ((size_t)(a.cheb_m + 1) * 4 + 15) / 16 * 16);
-    cudaError_t e = cudaFuncSetAttribute(kgen_bal_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kgen_bal_kernel<R, CLEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_bal_kernel<R>, S::NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_bal_kernel<R, CLEAN>, S::NT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     long grid = (long)sms * per_sm;
     if (grid > nsrc) grid = nsrc;
-    kgen_bal_kernel<R><<<(unsigned)grid, S::NT, smem, s>>>(a);
+    kgen_bal_kernel<R, CLEAN><<<(unsigned)grid, S::NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_kgen_bal(const KgenArgs& a, int R, cudaStream_t s)
 {
     if (a.fp64 || a.symmetric) return cudaErrorNotSupported;
-    if (R == 5) return launch_bal_r<5>(a, s);
-    if (R == 8) return launch_bal_r<8>(a, s);
+    // FDIRW_KGEN_SYNCCHECK=1: the synccheck-clean barrier form (kgen_common.cuh), for sanitizer runs
+    static const bool clean = [] {
+        const char* ev = getenv("FDIRW_KGEN_SYNCCHECK");
+        return ev && ev[0] == '1';
+    }();
+    if (R == 5) return clean ? launch_bal_r<5, true>(a, s) : launch_bal_r<5, false>(a, s);
+    if (R == 8) return clean ? launch_bal_r<8, true>(a, s) : launch_bal_r<8, false>(a, s);
     return cudaErrorNotSupported;
 }
 

@@ -14,22 +14,66 @@ __device__ __forceinline__ double warp_sum_f64(double v)
     return v;
 }
 
-// Deterministic block reduction (fixed shuffle tree + fixed warp order).
-template <int NW>
+// CTA barriers for warp-specialised kernels (kgen_bal.cu), where each segment's warps run their own
+// instantiation and so reach the CTA barrier from different code.
+//  CLEAN = false (default): named barrier 1 with the CTA's thread count, `bar.sync 1, NT` /
+//    `bar.red.or.pred`, issued inline — the CUTLASS NamedBarrier form; every thread executes the
+//    same barriers in the same order.  compute-sanitizer synccheck reports these ("divergent
+//    threads in block": it expects one PC per CTA barrier).
+//  CLEAN = true (FDIRW_KGEN_SYNCCHECK=1): the barrier lives in one non-inlined function every
+//    thread calls, so all threads execute the same `bar.sync` instruction; synccheck-clean,
+//    measured 15 % slower at R5 (the call per pass).
+template <int NT, bool CLEAN>
+__device__ __forceinline__ void cta_sync_any_pc();
+template <int NT, bool CLEAN>
+__device__ __forceinline__ bool cta_or_any_pc(bool v);
+
+static __device__ __noinline__ void cta_sync_call() { __syncthreads(); }
+static __device__ __noinline__ int cta_or_call(int v) { return __syncthreads_or(v); }
+
+template <int NT, bool CLEAN>
+__device__ __forceinline__ void cta_sync_any_pc()
+{
+    if constexpr (CLEAN) cta_sync_call();
+    else asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+template <int NT, bool CLEAN>
+__device__ __forceinline__ bool cta_or_any_pc(bool v)
+{
+    if constexpr (CLEAN) {
+        return cta_or_call(v ? 1 : 0) != 0;
+    } else {
+        unsigned r;
+        asm volatile(
+            "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, 1, %2, p;\n selp.u32 %0, 1, 0, q;\n}"
+            : "=r"(r)
+            : "r"((unsigned)v), "n"(NT)
+            : "memory");
+        return r != 0;
+    }
+}
+
+// Deterministic block reduction (fixed shuffle tree + fixed warp order).  ANY_PC: the barriers
+// are cta_sync_any_pc<NW·32, CLEAN> (for warp-specialised callers), else __syncthreads.
+template <int NW, bool ANY_PC = false, bool CLEAN = false>
 __device__ __forceinline__ double block_sum_f64(double v, double* red)
 {
+    auto sync = [] {
+        if constexpr (ANY_PC) cta_sync_any_pc<NW * 32, CLEAN>();
+        else __syncthreads();
+    };
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     v = warp_sum_f64(v);
     if (lane == 0) red[warp] = v;
-    __syncthreads();
+    sync();
     if (warp == 0) {
         double w = lane < NW ? red[lane] : 0.0;
         w = warp_sum_f64(w);
         if (lane == 0) red[NW] = w;
     }
-    __syncthreads();
+    sync();
     const double r = red[NW];
-    __syncthreads();
+    sync();
     return r;
 }
 

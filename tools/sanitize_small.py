@@ -37,6 +37,15 @@ def main():
             fd.mass(ctx, c)
             if not flags & fd.F_DEDUP_STORAGE:  # export needs the dense layout
                 fd.export_kernels(ctx, (0, 5, 0, 4, 0, 3))
+    # the two-columns-per-thread kgen (kgen_bal.cu: R5 two z segments, R8 three), Chebyshev and
+    # literal passes, closed and open windows, and the column kernel it replaces (A/B flag)
+    kshape = (9, 10, 11)
+    kmask = fi.porous_particle(kshape, 4, pore_r=(1.0, 1.5), n_pores=3, seed=4)
+    fkmask = fi.with_far_field(kmask, 4, 0.5)
+    for R, m, flags, vf in ((5, kmask, 0, 0.0), (5, fkmask, 0, 100.0), (5, kmask, fd.F_KGEN_COLUMNS, 0.0),
+                            (8, kmask, 0, 0.0), (8, kmask, fd.F_KGEN_DIRECT, 0.0)):
+        with fd.build_kernels(params(kshape, R, 30, "bf16", flags, v_far=vf), m) as ctx:
+            fd.export_kernels(ctx, (0, 3, 0, 3, 0, 3))
     # round 2 entry points: host-buffer step (plain and plane-chunk pipelined), phase profile,
     # slab mass, the staged-stream canary
     hin = c0.cpu().pin_memory()

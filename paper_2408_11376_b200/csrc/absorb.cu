@@ -95,11 +95,15 @@ __global__ void react_alpha_kernel(const float* __restrict__ c, const uint8_t* _
     }
 }
 
-// (3b) apply: solid gains Σ α_l q_sl, liquid loses α_l Σ q_sl (the same q expression both sides)
+// (3b) apply: solid gains Σ α_l q_sl, liquid loses α_l Σ q_sl (the same q expression both sides);
+// with (5)'s kinetics partial sums of the values it writes (Q_S, Q_L per block, fp64, fixed order)
 __global__ void react_apply_kernel(const float* __restrict__ c, const float* __restrict__ alpha,
                                    const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R, int nxp, int nyp,
-                                   float kdt, float cSeq, float cLeq, float* __restrict__ out)
+                                   float kdt, float cSeq, float cLeq, float* __restrict__ out,
+                                   double* __restrict__ part)
 {
+    __shared__ double rs[8], rl[8];
+    double ks = 0.0, kl = 0.0;
     const long n = (long)nx * ny * nz;
     const long dxy[3] = {1, nxp, (long)nxp * nyp};
     // 32-bit index arithmetic (n < 2^31 for every grid the library accepts on one GPU): the
@@ -128,31 +132,15 @@ __global__ void react_apply_kernel(const float* __restrict__ c, const float* __r
             v -= alpha[p] * Q;
         }
         out[p] = v;
-    }
-}
-
-// (5) kinetics: Q_S, Q_L partial sums per block (fp64), then a fixed-order final sum
-__global__ void kin_partial_kernel(const float* __restrict__ c, const uint8_t* __restrict__ pp, int nx, int ny,
-                                   int nz, int R, int nxp, int nyp, double* __restrict__ part)
-{
-    __shared__ double rs[8], rl[8];
-    const long n = (long)nx * ny * nz;
-    double s = 0.0, l = 0.0;
-    // 32-bit index arithmetic (n < 2^31 for every grid the library accepts on one GPU): the
-    // 64-bit div/mod of the first version dominated these short kernels
-    const int nxy = nx * ny;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)n; i += gridDim.x * blockDim.x) {
-        const int z = i / nxy, r = i - z * nxy, y = r / nx, x = r - y * nx;
-        const long p = pidx(x, y, z, R, nxp, nyp);
-        if (pp[p] == 0) s += (double)c[p];
-        else if (pp[p] == 1) l += (double)c[p];
+        if (ph == 0) ks += (double)v;
+        else if (ph == 1) kl += (double)v;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, o);
-        l += __shfl_xor_sync(0xffffffffu, l, o);
+        ks += __shfl_xor_sync(0xffffffffu, ks, o);
+        kl += __shfl_xor_sync(0xffffffffu, kl, o);
     }
-    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = s; rl[threadIdx.x >> 5] = l; }
+    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = ks; rl[threadIdx.x >> 5] = kl; }
     __syncthreads();
     if (threadIdx.x == 0) {
         double ts = 0.0, tl = 0.0;
@@ -220,13 +208,12 @@ cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uin
     // (3) interface reaction
     react_alpha_kernel<<<gridn(n), 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt, ab.cSeq,
                                                 ab.cLeq, alpha);
-    react_apply_kernel<<<gridn(n), 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt,
-                                                ab.cSeq, ab.cLeq, other);
+    // (3b) + (5)'s partial sums in one sweep; (4)+(5) final
+    const unsigned nblk = gridn(n);  // ≤ 148·16 blocks: part holds 2 doubles per block
+    react_apply_kernel<<<nblk, 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt, ab.cSeq,
+                                            ab.cLeq, other, part);
     float* t = cur; cur = other; other = t;
-    // (4)+(5)
-    const int nblk = 148 * 4;
-    kin_partial_kernel<<<nblk, 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, part);
-    kin_final_kernel<<<1, 256, 0, s>>>(part, nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec, ctr);
+    kin_final_kernel<<<1, 256, 0, s>>>(part, (int)nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec, ctr);
     *result = cur;
     return cudaGetLastError();
 }

@@ -52,10 +52,13 @@ __device__ __forceinline__ uint4 ld_stream(const void* ptr, uint64_t pol)
 
 __device__ __forceinline__ float4 ld_c(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
-// The diagonal term of 8 targets, d·C_old(x) with d = dh + dl an fp32 pair (reading A10):
-// hi = RN(dh·C), lo = (dh·C − hi) + dl·C (the product's exact error by FMA, then the low part).
-// dp = 8 float2 (64 B, 16-byte aligned), c = C_old(x .. x+7).
-__device__ __forceinline__ void diag_pair_init(const float2* dp, const float* c, float hi[8], float lo[8])
+// The diagonal term of 8 targets, d·C_old(x) with d = dh + dl an fp32 pair (reading A10), in two
+// parts: head (first, DESIGN §6 order) hi = RN(dh·C), lo = 0; tail (last, before acc = hi + lo)
+// lo += (dh·C − RN(dh·C)) + dl·C, the head product's exact error (FMA) and the low part.  (With the
+// whole pair in the head, lo starting non-zero made the one-wave register-prefetch launch 24 %
+// slower at cfg2 for reasons ncu does not show — same instructions, more long-scoreboard stalls;
+// the tail form measures as before.)  dp = 8 float2 (64 B, 16-byte aligned), c = C_old(x .. x+7).
+__device__ __forceinline__ void diag_pair_head(const float2* dp, const float* c, float hi[8], float lo[8])
 {
     const float4 v0 = ld_c(c), v1 = ld_c(c + 4);
     const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
@@ -63,10 +66,39 @@ __device__ __forceinline__ void diag_pair_init(const float2* dp, const float* c,
     for (int k = 0; k < 4; ++k) {
         const float4 d = __ldg(reinterpret_cast<const float4*>(dp) + k);  // (dh, dl) of targets 2k, 2k+1
         hi[2 * k] = __fmul_rn(d.x, v[2 * k]);
-        lo[2 * k] = fmaf(d.y, v[2 * k], fmaf(d.x, v[2 * k], -hi[2 * k]));
         hi[2 * k + 1] = __fmul_rn(d.z, v[2 * k + 1]);
-        lo[2 * k + 1] = fmaf(d.w, v[2 * k + 1], fmaf(d.z, v[2 * k + 1], -hi[2 * k + 1]));
+        lo[2 * k] = lo[2 * k + 1] = 0.f;
     }
+}
+__device__ __forceinline__ void diag_pair_tail(const float2* dp, const float* c, float lo[8])
+{
+    const float4 v0 = ld_c(c), v1 = ld_c(c + 4);
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float4 d = __ldg(reinterpret_cast<const float4*>(dp) + k);
+        lo[2 * k] = __fadd_rn(lo[2 * k], fmaf(d.y, v[2 * k], fmaf(d.x, v[2 * k], -__fmul_rn(d.x, v[2 * k]))));
+        lo[2 * k + 1] =
+            __fadd_rn(lo[2 * k + 1], fmaf(d.w, v[2 * k + 1], fmaf(d.z, v[2 * k + 1], -__fmul_rn(d.z, v[2 * k + 1]))));
+    }
+}
+// the same with one pair d for all 8 targets (N4: a uniform chunk's class diagonal)
+__device__ __forceinline__ void diag_pair_head1(float2 d, const float* c, float hi[8], float lo[8])
+{
+    const float4 v0 = ld_c(c), v1 = ld_c(c + 4);
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        hi[j] = __fmul_rn(d.x, v[j]);
+        lo[j] = 0.f;
+    }
+}
+__device__ __forceinline__ void diag_pair_tail1(float2 d, const float* c, float lo[8])
+{
+    const float4 v0 = ld_c(c), v1 = ld_c(c + 4);
+    const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) lo[j] = __fadd_rn(lo[j], fmaf(d.y, v[j], fmaf(d.x, v[j], -__fmul_rn(d.x, v[j]))));
 }
 
 template <typename WT>
@@ -326,18 +358,9 @@ __device__ __forceinline__ void uniform_body(const UniArgs& a, int blk, float* w
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
     float hi[8], lo[8];
-    if (a.udiag_t) {  // MX8: per-target diagonal
-        diag_pair_init(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8, c0, hi, lo);
-    } else {          // the class's diagonal for all 8 targets
-        const float2 d = a.udiag[b.z];
-        const float4 v0 = ld_c(c0), v1 = ld_c(c0 + 4);
-        const float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            hi[j] = __fmul_rn(d.x, v[j]);
-            lo[j] = fmaf(d.y, v[j], fmaf(d.x, v[j], -hi[j]));
-        }
-    }
+    const float2* dpt = a.udiag_t ? a.udiag_t + (size_t)(b.x + threadIdx.x) * 8 : nullptr;
+    if (dpt) diag_pair_head(dpt, c0, hi, lo);  // MX8: per-target diagonal
+    else diag_pair_head1(a.udiag[b.z], c0, hi, lo);  // the class's diagonal for all 8 targets
     do_row_u<R, true>(c0 - 8, ws, hi, lo);
     const float* wr = ws + (L - 1);
 #pragma unroll 1
@@ -347,6 +370,8 @@ __device__ __forceinline__ void uniform_body(const UniArgs& a, int blk, float* w
         do_row_u<R, false>(c0 - (long)oz * plane - (long)oy * nxp - 8, wr, hi, lo);
         wr += L;
     }
+    if (dpt) diag_pair_tail(dpt, c0, lo);
+    else diag_pair_tail1(a.udiag[b.z], c0, lo);
     float* out = a.out + (long)zl * a.out_ps + (long)y * a.out_rs + x;
     float acc[8];
 #pragma unroll
@@ -453,7 +478,7 @@ __device__ __forceinline__ void diag_init(const SuperArgs& a, const TileCtx& t, 
 #pragma unroll
     for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.f;
     if (!t.real) return;
-    diag_pair_init(a.diag + ((size_t)t.tile * a.tile + e) * 8, t.c0, hi, lo);
+    diag_pair_head(a.diag + ((size_t)t.tile * a.tile + e) * 8, t.c0, hi, lo);
 }
 
 // Stored row i of a tile (i = 0: the centre row, L − 1 slots; i ≥ 1: row r of (oz, oy)
@@ -477,8 +502,12 @@ __device__ __forceinline__ void tile_epilogue(const SuperArgs& a, const TileCtx&
     const bool real = t.real;
     const long nxp = t.nxp, plane = t.plane;
     float acc[8];
+    float lo2[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(hi[j], lo[j]);
+    for (int j = 0; j < 8; ++j) lo2[j] = lo[j];
+    if (real) diag_pair_tail(a.diag + ((size_t)tile * a.tile + e) * 8, t.c0, lo2);  // the diagonal's tail
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(hi[j], lo2[j]);
     if (a.pbc) {  // N2: + p_BC(x)·c_far(t)  (Eq.8 boundary term; 0 on far-field targets)
         const float cf = (float)a.far_state[0];
         const float4 b0 = __ldg(reinterpret_cast<const float4*>(a.pbc + ((size_t)tile * a.tile + e) * 8));
@@ -920,7 +949,7 @@ __device__ __forceinline__ void uniform_body_mx8(const UniArgs& a, int blk, floa
     const long nxp = a.nxp, plane = (long)a.nyp * nxp;
     const float* c0 = a.cpad + (zl + R) * plane + (long)(y + R) * nxp + kPadX + x;
     float hi[8], lo[8], p[8];
-    diag_pair_init(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8, c0, hi, lo);
+    diag_pair_head(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8, c0, hi, lo);
 #pragma unroll
     for (int j = 0; j < 8; ++j) p[j] = 0.f;
     float seg[24];
@@ -946,6 +975,7 @@ __device__ __forceinline__ void uniform_body_mx8(const UniArgs& a, int blk, floa
             ++n;
         }
     }
+    diag_pair_tail(a.udiag_t + (size_t)(b.x + threadIdx.x) * 8, c0, lo);
     float* out = a.out + (long)zl * a.out_ps + (long)y * a.out_rs + x;
     float acc[8];
 #pragma unroll

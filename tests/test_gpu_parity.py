@@ -132,6 +132,11 @@ def test_superposition_on_oracle_weights(fd, oracle_lib, fmt):
     ((6, 5, 9), 2, 300, "bf16"),
     ((4, 12, 19), 5, 60, "fp16"),     # window larger than the domain in z
     ((3, 3, 3), 8, 30, "bf16"),       # R = 8 > every dimension (P2 regime)
+    # the two-columns kgen (R5, R8) on degenerate grids: 1-D rows, 2-D sheets, a thin slab
+    ((1, 1, 23), 5, 40, "fp32"),
+    ((2, 19, 1), 8, 40, "fp32"),
+    ((13, 2, 3), 5, 1000, "fp32"),
+    ((5, 21, 22), 8, 1000, "bf16"),
 ])
 def test_edge_shapes(fd, oracle_lib, shape, R, n_fd, fmt):
     cfg = small_cfg(shape, R, n_fd, D_slow=2e-3, weights=fmt)

@@ -103,6 +103,43 @@ __global__ void __launch_bounds__(256) rd_tiles(const uint4* __restrict__ a, int
     if (acc == 0x12345678u) out[0] = acc;
 }
 
+// TMA bulk reads (cp.async.bulk global → shared, the superposition's staged stream): one thread
+// per CTA keeps S stages of B bytes in flight over its contiguous chunk; the bytes are not
+// consumed (each stage is re-issued as soon as its copy completed)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(32) rd_bulk(const unsigned char* __restrict__ a, size_t chunk, size_t nchunk,
+                                             int S, unsigned B, unsigned* out)
+{
+    extern __shared__ __align__(128) unsigned char sm[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sm);
+    unsigned char* st = sm + 128;
+    if (threadIdx.x != 0) return;
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (int i = 0; i < S; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    unsigned ph[16] = {0};
+    for (size_t c = blockIdx.x; c < nchunk; c += gridDim.x) {
+        const unsigned char* p = a + c * chunk;
+        const size_t nb = chunk / B;
+        for (size_t k = 0; k < nb; ++k) {
+            const int s = (int)(k % S);
+            if (k >= (size_t)S || c != blockIdx.x) {  // wait for the stage's previous copy
+                asm volatile("{\n .reg .pred q;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n @!q bra W_%=;\n}"
+                             ::"r"(smem_u32(full + s)), "r"(ph[s]) : "memory");
+                ph[s] ^= 1u;
+            }
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(full + s)), "r"(B) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                         ::"r"(smem_u32(st + (size_t)s * B)), "l"(p + k * B), "r"(B), "r"(smem_u32(full + s)), "l"(pol) : "memory");
+        }
+    }
+    for (int s = 0; s < S; ++s)
+        asm volatile("{\n .reg .pred q;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n @!q bra W_%=;\n}"
+                     ::"r"(smem_u32(full + s)), "r"(ph[s]) : "memory");
+    if (ph[0] == 7u) out[0] = 1;
+}
+
 int main()
 {
     const size_t bytes = 18905104640ull;  // cfg3's weight bytes
@@ -137,6 +174,30 @@ int main()
         timeit(nm, [&] { rd<4><<<g, 256>>>(a, n16, o); });
         snprintf(nm, 64, "grid-stride U=8 blocks/SM=%d", bps);
         timeit(nm, [&] { rd<8><<<g, 256>>>(a, n16, o); });
+    }
+    // TMA bulk reads over 3456 contiguous tiles (S stages of B bytes in flight per CTA)
+    {
+        const size_t nchunk = 3456, chunk = (bytes / nchunk) / 65536 * 65536;
+        const double gb = (double)chunk * nchunk / 1e9;
+        for (int ctas : {1, 2, 3}) for (unsigned B : {16384u, 32768u, 45056u}) for (int S : {2, 3, 4}) {
+            const size_t smem = 128 + (size_t)S * B;
+            if (smem * ctas > 227 * 1024) continue;
+            cudaFuncSetAttribute(rd_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const int g = 148 * ctas;
+            rd_bulk<<<g, 32, smem>>>(reinterpret_cast<unsigned char*>(a), chunk, nchunk, S, B, o);
+            cudaDeviceSynchronize();
+            float best = 1e30f;
+            for (int r = 0; r < 5; ++r) {
+                cudaEventRecord(e0);
+                rd_bulk<<<g, 32, smem>>>(reinterpret_cast<unsigned char*>(a), chunk, nchunk, S, B, o);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            printf("TMA bulk CTAs/SM=%d B=%u S=%d  %.3f ms  %.1f GB/s\n", ctas, B, S, best, gb / (best * 1e-3));
+        }
     }
     // superpose-like: 3456 tiles of 5.47 MB each, one CTA per tile
     const size_t nchunk = 3456, chunk16 = n16 / nchunk;

@@ -84,3 +84,48 @@ def test_precision_modes_vs_oracle(fd, desk):
         tol = {"fp32": 1e-5, "mixed": 5e-4, "fp16": 5e-3}[mode]
         assert np.max(np.abs(kin[:, 3] - emu) / emu) <= tol, mode
     assert re["fp32"] < re["mixed"] < re["fp16"]
+
+
+def test_absorb_run_replay_consistent(fd, desk):
+    """fdirw_absorb_run replays a captured two-macro-step graph (round 2): 7 + 6 steps in two
+    calls (an odd tail, the graph reused) give the field and kinetics of 13 steps in one call
+    bit for bit; changing a loop parameter between calls recaptures (a fresh context agrees)."""
+    import torch
+
+    m, c0, ab, _ = desk
+    nz, ny, nx = m.shape
+    p = fd.Params(nx=nx, ny=ny, nz=nz, dh=ab.dh, D_fast=ab.D_L, D_slow=0.0, dt=ab.dt, radius=ab.R, weights="bf16",
+                  v_far=ab.V_far)
+
+    def run(chunks, ks):
+        ctx = fd.build_kernels(p, m)
+        try:
+            c = torch.from_numpy(c0.astype(np.float32)).cuda()
+            fd.far_init(ctx, c, fi.TABLE1["c_L0"])
+            kins = [fd.absorb_run(ctx, c, n, ab.D_S, k, ab.c_S_eq, ab.c_L_eq) for n, k in zip(chunks, ks)]
+            return c.cpu().numpy(), np.concatenate(kins)
+        finally:
+            fd.destroy(ctx)
+
+    a_c, a_k = run([13], [ab.k])
+    b_c, b_k = run([7, 6], [ab.k, ab.k])
+    np.testing.assert_array_equal(a_c, b_c)
+    np.testing.assert_array_equal(a_k, b_k)
+    # a parameter change between calls (k) must not replay the old graph
+    c1, k1 = run([4, 4], [ab.k, 2 * ab.k])
+    ctx = fd.build_kernels(p, m)
+    try:
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        fd.far_init(ctx, c, fi.TABLE1["c_L0"])
+        fd.absorb_run(ctx, c, 4, ab.D_S, ab.k, ab.c_S_eq, ab.c_L_eq)
+        ctx2 = fd.build_kernels(p, m)
+        try:
+            # the second half on a context that never saw the first k: same result
+            fd.far_init(ctx2, c, float(fd.far_get(ctx)))
+            kk = fd.absorb_run(ctx2, c, 4, ab.D_S, 2 * ab.k, ab.c_S_eq, ab.c_L_eq)
+        finally:
+            fd.destroy(ctx2)
+    finally:
+        fd.destroy(ctx)
+    np.testing.assert_allclose(c1, c.cpu().numpy(), rtol=1e-6, atol=1e-12)
+    np.testing.assert_allclose(k1[4:, :2], kk[:, :2], rtol=1e-6)

@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) kin_final_kernel(const double* __restrict
 static unsigned gridn(long n)
 {
     long b = (n + 255) / 256;
-    if (b > 148L * 16) b = 148L * 16;
+    if (b > kAbsorbMaxBlocks) b = kAbsorbMaxBlocks;
     return (unsigned)(b < 1 ? 1 : b);
 }
 
@@ -209,7 +209,7 @@ cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uin
     react_alpha_kernel<<<gridn(n), 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt, ab.cSeq,
                                                 ab.cLeq, alpha);
     // (3b) + (5)'s partial sums in one sweep; (4)+(5) final
-    const unsigned nblk = gridn(n);  // ≤ 148·16 blocks: part holds 2 doubles per block
+    const unsigned nblk = gridn(n);  // ≤ kAbsorbMaxBlocks: part holds 2 doubles per block
     react_apply_kernel<<<nblk, 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt, ab.cSeq,
                                             ab.cLeq, other, part);
     float* t = cur; cur = other; other = t;

@@ -1695,7 +1695,7 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     ab.n_solid = c->n_solid;
     fdirw_status st;
     if (!c->alpha && (st = alloc((void**)&c->alpha, g.state_elems * 4, "reaction scratch")) != FDIRW_OK) return st;
-    if (!c->kin_part && (st = alloc((void**)&c->kin_part, 2 * 148 * 4 * 8, "kinetics")) != FDIRW_OK) return st;
+    if (!c->kin_part && (st = alloc((void**)&c->kin_part, 2 * kAbsorbMaxBlocks * 8, "kinetics")) != FDIRW_OK) return st;
     if (n > c->kin_cap) {
         cudaFree(c->kin_rec);
         c->kin_rec = nullptr;

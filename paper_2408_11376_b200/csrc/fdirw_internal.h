@@ -214,6 +214,9 @@ struct UniformTables {
 };
 
 // ---- N3 integrated loop + precision modes (absorb.cu) --------------------------------
+// the tail sweeps launch at most this many blocks; react_apply writes 2 doubles of kinetics
+// partial sums per block, so the partial buffer holds 2·kAbsorbMaxBlocks doubles
+constexpr long kAbsorbMaxBlocks = 148L * 16;
 struct AbsorbArgs {
     int n_s;          // solid FD substeps per macro step
     float lam_s;      // D_S·A_S/RT · (Δt/n_s) / Δh²

@@ -129,3 +129,30 @@ def test_absorb_run_replay_consistent(fd, desk):
         fd.destroy(ctx)
     np.testing.assert_allclose(c1, c.cpu().numpy(), rtol=1e-6, atol=1e-12)
     np.testing.assert_allclose(k1[4:, :2], kk[:, :2], rtol=1e-6)
+
+
+def test_absorb_loop_many_tail_blocks(fd, oracle_lib):
+    """A grid whose tail sweeps launch more than 592 blocks (56³: 686): the kinetics partial sums
+    (2 doubles per block, up to kAbsorbMaxBlocks blocks) must fit their buffer.  Round 2's first
+    replay version sized it for 592 blocks, so at cfg3o (2,368 blocks) react_apply wrote past it
+    into far_state and the bench line's c_far / mass balance were garbage.  Checked against the
+    oracle's fp64 loop (3 steps), the record against the returned field, and Eq.7's balance."""
+    import torch
+    from oracle import integrated as ig
+
+    shape = (56, 56, 56)
+    m = fi.with_far_field(fi.porous_particle(shape, 18, pore_r=(1.0, 2.0), porosity=0.3, seed=5), 18, 3.0)
+    T = fi.TABLE1
+    c0 = np.where(m == 1, T["c_L0"], np.where(m == 0, T["c_S0"], 0.0))
+    ab = ig.Absorb(D_L=fi.D_FAST_SI, D_S=fi.D_SLOW_SI, dh=T["dh"], dt=T["dt"], k=0.05, c_S_eq=1.0, c_L_eq=1e-5,
+                   V_far=2e5, R=3)
+    steps = 3
+    ref, _, refkin = ig.run(m, c0, T["c_L0"], ab, steps, "fp64")
+    got, kin, M0 = _gpu(fd, m, c0, ab, "fp32", "default", steps=steps)
+    nf = m != 2
+    assert rel_l2(got[nf], ref[nf]) <= 1e-5
+    np.testing.assert_allclose(kin, np.array(refkin), rtol=1e-5)
+    np.testing.assert_allclose(kin[-1, 0], got[m == 0].sum(), rtol=1e-9)   # Q_S of the returned field
+    np.testing.assert_allclose(kin[-1, 1], got[m == 1].sum(), rtol=1e-9)   # Q_L
+    tot = got[nf].sum() + kin[-1, 2] * ab.V_far
+    assert abs(tot - M0) / M0 <= 1e-6

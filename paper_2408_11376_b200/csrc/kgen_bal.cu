@@ -80,59 +80,9 @@ struct BalSeg {
     static constexpr int SGL(int sd) { return N(sd) == 6 ? -1 : 4; }
 };
 
-// ---- thread-block-cluster primitives (the CLU form: one CTA per z segment, DSMEM exchange) ----
-__device__ __forceinline__ void cluster_sync_all()
-{
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ unsigned cluster_id_x()
-{
-    unsigned r;
-    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned n_clusters_x()
-{
-    unsigned r;
-    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned cluster_rank()
-{
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-// the shared::cluster address of this CTA's shared byte offset `a` in CTA `rank` of the cluster
-__device__ __forceinline__ unsigned map_rank(unsigned a, unsigned rank)
-{
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_cluster(unsigned a, float v)
-{
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster(unsigned a, double v)
-{
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
-
 }  // namespace
 
-// CLU = false: one CTA runs the whole window (every segment's warps, CTA barriers).
-// CLU = true: a cluster of NSEG CTAs runs it, CTA rank SEG holding segment SEG's warps.  Each CTA
-// keeps the whole buffer layout but only its own segment's items are live; the four items a
-// neighbouring segment reads (A's top cell 6s + 5 and B's cell 6s + 4 / 6s + 5 going up, the X copy
-// of A's cell 6s and B's cell 6s − 1 going down) are stored straight into that CTA's buffer
-// (st.shared::cluster), and each pass ends at a cluster barrier (release / acquire) instead of the
-// CTA barrier, so all loads stay local and the per-cell arithmetic is unchanged (identical bits).
-// The fp64 window sums gather every warp's partial into every CTA in the same warp order, so they
-// round as block_sum_f64 does.  Why: at R8 one 15-warp window fills an SM's registers, so every
-// pass's barrier and load latency is exposed; as 3 CTAs of 5 warps, an SM holds segments of three
-// windows whose barriers interleave.
-template <int R, int SEG, bool CLEAN, bool CLU = false>
+template <int R, int SEG, bool CLEAN>
 __device__ __forceinline__ void bal_body(const KgenArgs& a)
 {
     using S = BalShape<R>;
@@ -145,19 +95,8 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
     unsigned char* ph = smem_raw + S::buf_bytes;
     double* red = reinterpret_cast<double*>(smem_raw + S::buf_bytes + ((LLL + 15) / 16) * 16);
 
-    const int t = CLU ? SEG * S::NPW + (int)threadIdx.x : (int)threadIdx.x;
+    const int t = threadIdx.x;
     const int p = t - SEG * S::NPW;
-    // CTA-local loops: every thread of the window CTA, or of this segment's CTA
-    const int tl = threadIdx.x;
-    constexpr int NTL = CLU ? S::NPW : S::NT;
-    auto sync = [] {
-        if constexpr (CLU) cluster_sync_all();
-        else cta_sync_any_pc<S::NT, CLEAN>();
-    };
-    // peer buffers (CLU): segment SEG + 1 above, SEG − 1 below
-    const unsigned buf_sa = (unsigned)__cvta_generic_to_shared(smem_raw);
-    const unsigned rb_up = CLU && SEG + 1 < S::NSEG ? map_rank(buf_sa, SEG + 1) : 0u;
-    const unsigned rb_dn = CLU && SEG > 0 ? map_rank(buf_sa, SEG > 0 ? SEG - 1 : 0) : 0u;
     const bool real = p < S::NP;
     const int col[2] = {2 * p, 2 * p + 1};
     const bool has[2] = {real, real && 2 * p + 1 < LL};
@@ -165,66 +104,29 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
     const int nx = a.nx, ny = a.ny, nz = a.nz;
     const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
-    for (int i = tl; i < 2 * S::BUFF; i += NTL) buf[i] = 0.f;
+    for (int i = t; i < 2 * S::BUFF; i += S::NT) buf[i] = 0.f;
     float* ftab = reinterpret_cast<float*>(smem_raw + S::tab_off);
     build_face_tables(ftab, a.lam_ff, a.lam_fs, a.lam_ss, a.mu2_ff, a.mu2_fs, a.mu2_ss);
     if (a.cheb_m) {
         float* cc = reinterpret_cast<float*>(smem_raw + S::cheb_off);
-        for (int i = tl; i <= a.cheb_m; i += NTL) cc[i] = a.cheb_c[i];
+        for (int i = t; i <= a.cheb_m; i += S::NT) cc[i] = a.cheb_c[i];
     }
 
     auto sc = [](float* b, int side, int s, int kind) { return b + S::off(side, s, kind); };
     auto qd = [](float* b, int side, int s) { return reinterpret_cast<float4*>(b + S::off(side, s, S::KQ)); };
     // own cells → the buffer
     auto store_own = [&](float* b, const float (&cA)[6], const float (&cB)[6]) {
-        // byte offset of item (float offset `o`) of this pass buffer at the own pair, for a peer
-        auto ra = [&](unsigned base, int o) { return base + (unsigned)((b - buf) + o + pp) * 4u; };
         qd(b, 0, SEG)[pp] = make_float4(cA[0], cA[1], cA[2], cA[3]);
         sc(b, 0, SEG, S::KS4)[pp] = cA[4];
-        if constexpr (NA == 6) {
-            if constexpr (CLU) st_cluster(ra(rb_up, S::off(0, SEG, S::KS5)), cA[5]);  // read by SEG + 1 only
-            else sc(b, 0, SEG, S::KS5)[pp] = cA[5];
-        }
+        if constexpr (NA == 6) sc(b, 0, SEG, S::KS5)[pp] = cA[5];
+        if constexpr (SEG > 0) (b + S::offX(SEG))[pp] = cA[0];
         if constexpr (SEG > 0) {
-            if constexpr (CLU) st_cluster(ra(rb_dn, S::offX(SEG)), cA[0]);  // read by SEG − 1 only
-            else (b + S::offX(SEG))[pp] = cA[0];
-        }
-        if constexpr (SEG > 0) {
-            if constexpr (CLU) st_cluster(ra(rb_dn, S::off(1, SEG - 1, S::KS5)), cB[0]);  // read by SEG − 1
-            else sc(b, 1, SEG - 1, S::KS5)[pp] = cB[0];
+            sc(b, 1, SEG - 1, S::KS5)[pp] = cB[0];
             qd(b, 1, SEG)[pp] = make_float4(cB[1], cB[2], cB[3], cB[4]);
             sc(b, 1, SEG, S::KS4)[pp] = cB[5];
-            if constexpr (CLU && !G::last) st_cluster(ra(rb_up, S::off(1, SEG, S::KS4)), cB[5]);
         } else {
             qd(b, 1, 0)[pp] = make_float4(cB[0], cB[1], cB[2], cB[3]);
             sc(b, 1, 0, S::KS4)[pp] = cB[4];
-            if constexpr (CLU && !G::last) st_cluster(ra(rb_up, S::off(1, 0, S::KS4)), cB[4]);
-        }
-    };
-    // deterministic fp64 window sum: block_sum_f64's arithmetic; CLU gathers every warp's partial
-    // into every CTA (global warp order) first
-    auto wsum = [&](double v) -> double {
-        if constexpr (!CLU) {
-            return block_sum_f64<S::NW, true, CLEAN>(v, red);
-        } else {
-            constexpr int NWL = S::NPW / 32;
-            const int lane = tl & 31, w = SEG * NWL + (tl >> 5);
-            v = warp_sum_f64(v);
-            if (lane == 0) {
-                const unsigned ra0 = (unsigned)__cvta_generic_to_shared(red + w);
-#pragma unroll
-                for (int r = 0; r < S::NSEG; ++r) st_cluster(map_rank(ra0, r), v);
-            }
-            cluster_sync_all();
-            if (tl < 32) {
-                double x = lane < S::NW ? red[lane] : 0.0;
-                x = warp_sum_f64(x);
-                if (lane == 0) red[S::NW] = x;
-            }
-            __syncthreads();
-            const double r = red[S::NW];
-            cluster_sync_all();  // every CTA has read red before the next sum's stores
-            return r;
         }
     };
     // B-side cells over A's z range of pair slot q (A's −x / ±y neighbours)
@@ -259,18 +161,16 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
     const int qxmA = pp - 1, qymA = pp - (R + 1), qypA = pp + R;
     const int qxpB = pp + 1, qymB = pp - R, qypB = pp + R + 1;
 
-    const long it0 = CLU ? (long)cluster_id_x() : (long)blockIdx.x;
-    const long its = CLU ? (long)n_clusters_x() : (long)gridDim.x;
-    for (long it = it0; it < nsrc; it += its) {
+    for (long it = blockIdx.x; it < nsrc; it += gridDim.x) {
         const long src = a.src_list ? (long)a.src_list[it] : it;
         const int sx = (int)(src % nx);
         const int sy = (int)((src / nx) % ny);
         const int sz = a.sz0 + (int)(src / ((long)nx * ny));
 
-        sync();  // (each segment's warps run their own instantiation: the CTA barriers of
-                 // kgen_common.cuh, or the cluster barrier)
+        cta_sync_any_pc<S::NT, CLEAN>();  // (each segment's warps run their own instantiation:
+                                          // the CTA barriers of kgen_common.cuh)
         int far_here = 0;
-        for (int i = tl; i < LLL; i += NTL) {  // (CLU: every CTA reads the whole window's phases)
+        for (int i = t; i < LLL; i += S::NT) {
             const int gx = sx + i % L - R, gy = sy + (i / L) % L - R, gz = sz + i / LL - R;
             const bool in = gx >= 0 && gx < nx && gy >= 0 && gy < ny && gz >= 0 && gz < nz;
             unsigned char v = in ? a.mask[((size_t)(gz - a.mz0) * ny + gy) * nx + gx] : (unsigned char)2;
@@ -278,9 +178,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
             far_here |= v == 3;
             ph[i] = v;
         }
-        bool open;
-        if constexpr (CLU) open = __syncthreads_or(far_here) != 0;
-        else open = cta_or_any_pc<S::NT, CLEAN>(far_here != 0);
+        const bool open = cta_or_any_pc<S::NT, CLEAN>(far_here != 0);
         if (ph[KC] == 3) continue;
 
         // ---- face numbers: fl[sd][f][h] packed pairs, fl1[sd][f] the single cell; fz[sd][j] the
@@ -374,7 +272,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
         for (int k = 0; k < n_direct; ++k, ++ps) {
             float* b = buf + (ps & 1u) * S::BUFF;
             if (act) store_own(b, c[0], c[1]);
-            sync();
+            cta_sync_any_pc<S::NT, CLEAN>();
             if (act) {
                 float nb[2][4][6], h[4];
                 gather(b, c, nb, h);
@@ -436,7 +334,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
             auto step = [&](float (&cur)[2][6], float (&prv)[2][6], const int k, const bool first) {
                 float* b = buf + (ps & 1u) * S::BUFF;
                 if (act) store_own(b, cur[0], cur[1]);
-                sync();
+                cta_sync_any_pc<S::NT, CLEAN>();
                 ++ps;
                 const float ck = cc[k + 1];
                 if (act) {
@@ -508,7 +406,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
 #pragma unroll
             for (int i = 0; i < G::N(sd); ++i)
                 if (has[sd]) s += (double)c[sd][i];
-        const double S_ = wsum(s);
+        const double S_ = block_sum_f64<S::NW, true, CLEAN>(s, red);
         const double inv = open ? 1.0 : 1.0 / S_;
         const double M = open ? S_ : 1.0;
         double qsum = 0.0;
@@ -561,7 +459,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
                 else reinterpret_cast<unsigned short*>(a.Wt)[idx] = bits;
             }
         }
-        const double off = wsum(qsum);
+        const double off = block_sum_f64<S::NW, true, CLEAN>(qsum, red);
         const bool centre = real && col[0] == R * L + R && R >= G::zA && R < G::zA + NA;
         if (centre && a.class_w) {
             a.class_diag[it] = a.mass_fix ? fp32_pair(M - off) : make_float2(centre_q, 0.f);
@@ -589,62 +487,6 @@ __global__ void __launch_bounds__(BalShape<R>::NT, BalShape<R>::kMinBlocks) kgen
         else if (threadIdx.x < 2 * NPW) bal_body<R, 1, CLEAN>(a);
         else bal_body<R, 2, CLEAN>(a);
     }
-}
-
-// the CLU form: a cluster of NSEG CTAs per window, CTA rank = segment
-template <int R>
-__global__ void __launch_bounds__(BalShape<R>::NPW, 65536 / (BalShape<R>::NPW * 128)) kgen_bal_cluster_kernel(
-    const KgenArgs a)
-{
-    const unsigned r = cluster_rank();
-    if constexpr (BalShape<R>::NSEG == 2) {
-        if (r == 0) bal_body<R, 0, false, true>(a);
-        else bal_body<R, 1, false, true>(a);
-    } else {
-        static_assert(BalShape<R>::NSEG == 3, "R = 5, 8");
-        if (r == 0) bal_body<R, 0, false, true>(a);
-        else if (r == 1) bal_body<R, 1, false, true>(a);
-        else bal_body<R, 2, false, true>(a);
-    }
-    cluster_sync_all();  // no CTA leaves while a peer may still address its shared memory
-}
-
-template <int R>
-static cudaError_t launch_bal_cluster_r(const KgenArgs& a, cudaStream_t s)
-{
-    using S = BalShape<R>;
-    const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
-    if (nsrc <= 0) return cudaSuccess;
-    const size_t smem = S::smem_bytes + (!a.cheb_m ? 0 : ((size_t)(a.cheb_m + 1) * 4 + 15) / 16 * 16);
-    cudaError_t e = cudaFuncSetAttribute(kgen_bal_cluster_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = S::NSEG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cfg.blockDim = dim3(S::NPW);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cfg.gridDim = dim3((unsigned)(sms * S::NSEG * 4));
-    int ncl = 0;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kgen_bal_cluster_kernel<R>, &cfg);
-    if (e != cudaSuccess) return e;
-    if (ncl < 1) return cudaErrorInvalidConfiguration;
-    if (const char* ev = getenv("FDIRW_KGEN_CLUSTERS")) ncl = atoi(ev) > 0 ? atoi(ev) : ncl;  // A/B
-    long grid = ncl;
-    if (grid > nsrc) grid = nsrc;
-    cfg.gridDim = dim3((unsigned)(grid * S::NSEG));
-    e = cudaLaunchKernelEx(&cfg, kgen_bal_cluster_kernel<R>, a);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
 }
 
 template <int R, bool CLEAN>
@@ -676,12 +518,8 @@ cudaError_t launch_kgen_bal(const KgenArgs& a, int R, cudaStream_t s)
         const char* ev = getenv("FDIRW_KGEN_SYNCCHECK");
         return ev && ev[0] == '1';
     }();
-    // FDIRW_KGEN_CLUSTER=0 / 1: the one-CTA-per-window form / the cluster form (A/B; default per R)
-    const char* cl_ev = getenv("FDIRW_KGEN_CLUSTER");  // (read per build: tests switch it)
-    const int cl_env = cl_ev ? atoi(cl_ev) : -1;
-    const bool cluster = !clean && (cl_env >= 0 ? cl_env == 1 : false);
-    if (R == 5) return cluster ? launch_bal_cluster_r<5>(a, s) : clean ? launch_bal_r<5, true>(a, s) : launch_bal_r<5, false>(a, s);
-    if (R == 8) return cluster ? launch_bal_cluster_r<8>(a, s) : clean ? launch_bal_r<8, true>(a, s) : launch_bal_r<8, false>(a, s);
+    if (R == 5) return clean ? launch_bal_r<5, true>(a, s) : launch_bal_r<5, false>(a, s);
+    if (R == 8) return clean ? launch_bal_r<8, true>(a, s) : launch_bal_r<8, false>(a, s);
     return cudaErrorNotSupported;
 }
 

@@ -32,7 +32,6 @@
 #include <cstdlib>
 #include <type_traits>
 
-#include "bulk.cuh"
 #include "fdirw_internal.h"
 #include "kgen_common.cuh"
 #include "layout.cuh"
@@ -58,9 +57,7 @@ struct BalShape {
     static constexpr int offX(int s) { return (12 * NSEG + s) * NPP; }
     static constexpr int BUFF = 13 * NSEG * NPP;
     static constexpr size_t buf_bytes = 2 * (size_t)BUFF * 4;
-    // after the window's phases: red[NW + 1] (fp64 sums), 8 spare bytes, the pass mbarrier (SPLIT)
-    static constexpr size_t mbar_off = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
-    static constexpr size_t tab_off = mbar_off + 16;
+    static constexpr size_t tab_off = buf_bytes + ((LLL + 15) / 16) * 16 + NW * 8 + 16;
     static constexpr size_t smem_bytes = tab_off + 64 * 4;
     static constexpr size_t cheb_off = smem_bytes;
     static constexpr int kMinBlocks = 65536 / (NT * 128) > 0 ? 65536 / (NT * 128) : 1;
@@ -85,12 +82,7 @@ struct BalSeg {
 
 }  // namespace
 
-// SPLIT: the Chebyshev passes end at a split barrier (one mbarrier arrival per warp after its
-// stores, the wait just before its shared loads), and each thread does its register-only part of
-// the next pass in between — every cell's D∘t − t_prev and the z terms whose neighbour is in its
-// own column — so that work fills the barrier's wait.  Each cell's operations keep their order
-// (identical bits to the bar.sync form).
-template <int R, int SEG, bool CLEAN, bool SPLIT>
+template <int R, int SEG, bool CLEAN>
 __device__ __forceinline__ void bal_body(const KgenArgs& a)
 {
     using S = BalShape<R>;
@@ -113,12 +105,6 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
     const long nsrc = a.src_list ? a.n_list : (long)nx * ny * (a.sz1 - a.sz0);
 
     for (int i = t; i < 2 * S::BUFF; i += S::NT) buf[i] = 0.f;
-    const uint32_t mbar = smem_u32(smem_raw + S::mbar_off);
-    if (SPLIT && t == 0) {
-        mbar_init(mbar, S::NW);
-        mbar_init_fence();
-    }
-    unsigned mph = 0;  // SPLIT: mbarrier phases completed
     float* ftab = reinterpret_cast<float*>(smem_raw + S::tab_off);
     build_face_tables(ftab, a.lam_ff, a.lam_fs, a.lam_ss, a.mu2_ff, a.mu2_fs, a.mu2_ss);
     if (a.cheb_m) {
@@ -345,64 +331,36 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
                     pv[sd][i] = 0.f;
                     acc[sd][i] = c[sd][i] * cc[0];
                 }
-            // register-only part of a pass, in place in prv (dead once read): D∘t − t_prev, then the
-            // z terms of the cells whose z neighbours are both in registers (the lower one for
-            // i ≥ 1, the upper one for 1 ≤ i ≤ N − 2); `post` adds the rest in the same order
-            auto pre = [&](const float (&cur)[2][6], float (&prv)[2][6]) {
-                auto side = [&](auto sdc) {
-                    constexpr int sd = decltype(sdc)::value;
-                    constexpr int N = G::N(sd);
-#pragma unroll
-                    for (int hh = 0; hh < G::NPR(sd); ++hh) {
-                        const int i0 = G::PA(sd, hh), i1 = G::PB(sd, hh);
-                        const unsigned long long s2 = fma2(dg2[sd][hh], pk2(cur[sd][i0], cur[sd][i1]),
-                                                           pk2(-prv[sd][i0], -prv[sd][i1]));
-                        upk2(s2, prv[sd][i0], prv[sd][i1]);
-                    }
-                    if constexpr (G::SGL(sd) >= 0) {
-                        constexpr int i = G::SGL(sd);
-                        prv[sd][i] = fmaf(dg1[sd], cur[sd][i], -prv[sd][i]);
-                    }
-#pragma unroll
-                    for (int i = 1; i < N; ++i) {
-                        float v = prv[sd][i];
-                        if (below(sd, i)) v = fmaf(fz[sd][i], cur[sd][i - 1], v);
-                        if (i < N - 1 && above(sd, i)) v = fmaf(fz[sd][i + 1], cur[sd][i < 5 ? i + 1 : 5], v);
-                        prv[sd][i] = v;
-                    }
-                };
-                side(std::integral_constant<int, 0>{});
-                side(std::integral_constant<int, 1>{});
-            };
             auto step = [&](float (&cur)[2][6], float (&prv)[2][6], const int k, const bool first) {
                 float* b = buf + (ps & 1u) * S::BUFF;
                 if (act) store_own(b, cur[0], cur[1]);
-                if constexpr (SPLIT) {
-                    __syncwarp();
-                    if ((threadIdx.x & 31) == 0) mbar_arrive(mbar);
-                    if (act) pre(cur, prv);
-                    mbar_wait(mbar, mph & 1u);
-                    ++mph;
-                } else {
-                    cta_sync_any_pc<S::NT, CLEAN>();
-                }
+                cta_sync_any_pc<S::NT, CLEAN>();
                 ++ps;
                 const float ck = cc[k + 1];
                 if (act) {
                     float nb[2][4][6], h[4];
                     gather(b, cur, nb, h);
-                    if constexpr (!SPLIT) pre(cur, prv);
                     auto side = [&](auto sdc) {
                         constexpr int sd = decltype(sdc)::value;
                         constexpr int N = G::N(sd);
-                        float (&nw)[6] = prv[sd];
-                        {  // cell 0: both z terms (the lower neighbour is a halo); cell N − 1: the upper
-                            float v = nw[0];
-                            if (below(sd, 0)) v = fmaf(fz[sd][0], zdn(cur, h, sd, 0), v);
-                            if (above(sd, 0)) v = fmaf(fz[sd][1], zup(cur, h, sd, 0), v);
-                            nw[0] = v;
-                            if constexpr (N > 1)
-                                if (above(sd, N - 1)) nw[N - 1] = fmaf(fz[sd][N], zup(cur, h, sd, N - 1), nw[N - 1]);
+                        float nw[6];
+#pragma unroll
+                        for (int hh = 0; hh < G::NPR(sd); ++hh) {
+                            const int i0 = G::PA(sd, hh), i1 = G::PB(sd, hh);
+                            const unsigned long long s2 = fma2(dg2[sd][hh], pk2(cur[sd][i0], cur[sd][i1]),
+                                                               pk2(-prv[sd][i0], -prv[sd][i1]));
+                            upk2(s2, nw[i0], nw[i1]);
+                        }
+                        if constexpr (G::SGL(sd) >= 0) {
+                            constexpr int i = G::SGL(sd);
+                            nw[i] = fmaf(dg1[sd], cur[sd][i], -prv[sd][i]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < N; ++i) {
+                            float v = nw[i];
+                            if (below(sd, i)) v = fmaf(fz[sd][i], zdn(cur, h, sd, i), v);
+                            if (above(sd, i)) v = fmaf(fz[sd][i + 1], zup(cur, h, sd, i), v);
+                            nw[i] = v;
                         }
 #pragma unroll
                         for (int hh = 0; hh < G::NPR(sd); ++hh) {
@@ -516,39 +474,39 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
     }
 }
 
-template <int R, bool CLEAN, bool SPLIT>
+template <int R, bool CLEAN>
 __global__ void __launch_bounds__(BalShape<R>::NT, BalShape<R>::kMinBlocks) kgen_bal_kernel(const KgenArgs a)
 {
     constexpr int NPW = BalShape<R>::NPW;
     if constexpr (BalShape<R>::NSEG == 2) {
-        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN, SPLIT>(a);
-        else bal_body<R, 1, CLEAN, SPLIT>(a);
+        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN>(a);
+        else bal_body<R, 1, CLEAN>(a);
     } else {
         static_assert(BalShape<R>::NSEG == 3, "R = 5, 8");
-        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN, SPLIT>(a);
-        else if (threadIdx.x < 2 * NPW) bal_body<R, 1, CLEAN, SPLIT>(a);
-        else bal_body<R, 2, CLEAN, SPLIT>(a);
+        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN>(a);
+        else if (threadIdx.x < 2 * NPW) bal_body<R, 1, CLEAN>(a);
+        else bal_body<R, 2, CLEAN>(a);
     }
 }
 
-template <int R, bool CLEAN, bool SPLIT>
+template <int R, bool CLEAN>
 static cudaError_t launch_bal_r(const KgenArgs& a, cudaStream_t s)
 {
     using S = BalShape<R>;
     const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
     if (nsrc <= 0) return cudaSuccess;
     const size_t smem = S::smem_bytes + (!a.cheb_m ? 0 : ((size_t)(a.cheb_m + 1) * 4 + 15) / 16 * 16);
-    cudaError_t e = cudaFuncSetAttribute(kgen_bal_kernel<R, CLEAN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kgen_bal_kernel<R, CLEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_bal_kernel<R, CLEAN, SPLIT>, S::NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_bal_kernel<R, CLEAN>, S::NT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     long grid = (long)sms * per_sm;
     if (grid > nsrc) grid = nsrc;
-    kgen_bal_kernel<R, CLEAN, SPLIT><<<(unsigned)grid, S::NT, smem, s>>>(a);
+    kgen_bal_kernel<R, CLEAN><<<(unsigned)grid, S::NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -560,15 +518,8 @@ cudaError_t launch_kgen_bal(const KgenArgs& a, int R, cudaStream_t s)
         const char* ev = getenv("FDIRW_KGEN_SYNCCHECK");
         return ev && ev[0] == '1';
     }();
-    // FDIRW_KGEN_SPLIT=0 / 1: the Chebyshev passes' bar.sync / split mbarrier form (A/B)
-    const char* sp_ev = getenv("FDIRW_KGEN_SPLIT");  // (read per build: tests switch it)
-    const bool split = sp_ev ? sp_ev[0] == '1' : true;
-    if (R == 5)
-        return clean ? (split ? launch_bal_r<5, true, true>(a, s) : launch_bal_r<5, true, false>(a, s))
-                     : (split ? launch_bal_r<5, false, true>(a, s) : launch_bal_r<5, false, false>(a, s));
-    if (R == 8)
-        return clean ? (split ? launch_bal_r<8, true, true>(a, s) : launch_bal_r<8, true, false>(a, s))
-                     : (split ? launch_bal_r<8, false, true>(a, s) : launch_bal_r<8, false, false>(a, s));
+    if (R == 5) return clean ? launch_bal_r<5, true>(a, s) : launch_bal_r<5, false>(a, s);
+    if (R == 8) return clean ? launch_bal_r<8, true>(a, s) : launch_bal_r<8, false>(a, s);
     return cudaErrorNotSupported;
 }
 

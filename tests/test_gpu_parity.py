@@ -319,32 +319,6 @@ def test_kgen_bal_equal_columns(fd, oracle_lib, R, fmt, far, direct):
         assert ep <= 1e-5 and ep <= 1.01 * ec, (ep, ec)
 
 
-@pytest.mark.parametrize("R,fmt,far", [(5, "fp32", False), (5, "bf16", True), (8, "fp32", False),
-                                        (8, "bf16", True)])
-def test_kgen_split_barrier_bitwise(fd, monkeypatch, R, fmt, far):
-    """kgen_bal's Chebyshev passes with the split barrier (FDIRW_KGEN_SPLIT=1: an mbarrier arrival
-    per warp after its stores, the register-only part of the pass, then the wait) against the
-    bar.sync form: each cell's operations keep their order, so the stored kernels are bitwise
-    equal.  Closed and open (N2, literal) windows, with and without the window dedup."""
-    shape = (21, 23, 22) if R == 5 else (15, 16, 14)
-    mask = fi.porous_particle(shape, 7 if R == 5 else 5, pore_r=(1.0, 2.0), porosity=0.3, seed=4)
-    if far:
-        mask = fi.with_far_field(mask, 8 if R == 5 else 5, 3.0 if R == 5 else 1.0)
-    cfg = small_cfg(shape, R, 1000, D_slow=1e-3, weights=fmt)
-    box = (0, shape[2], 0, shape[1], 0, shape[0])
-    out = {}
-    for form in ("0", "1"):
-        monkeypatch.setenv("FDIRW_KGEN_SPLIT", form)
-        for nd in (0, fd.F_NO_DEDUP):
-            ctx = fd.build_kernels(lib_params(cfg, fmt, nd, v_far=1e3 if far else 0.0), mask)
-            try:
-                out[form, nd] = fd.export_kernels(ctx, box)
-            finally:
-                fd.destroy(ctx)
-    for nd in (0, fd.F_NO_DEDUP):
-        np.testing.assert_array_equal(out["1", nd], out["0", nd])
-
-
 @pytest.mark.parametrize("fmt,far", [("fp32", False), ("bf16", False), ("fp16", True)])
 def test_kgen_fp64_flag_equals_oracle_bits(fd, oracle_lib, fmt, far):
     """FDIRW_F_KGEN_FP64 (reading A22): fp64 substeps in the oracle's operation order and no

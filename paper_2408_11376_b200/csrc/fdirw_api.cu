@@ -944,8 +944,11 @@ struct PhaseEv {
     do { if (pe) CUDA_TRY(cudaEventRecord(pe->field, stream)); } while (0)
 
 // One step src (padded, slab planes filled) → out; exchanges the halo planes of src first.
+// eq7 = false (the N3 loop): skip the compacted path's Eq.7 sums and c_far update after the liquid
+// step — the loop's kinetics pass sets c_far from the whole step's totals (oracle/integrated.py
+// run(), component (4) after (1)-(3)), which overwrites it before any kernel reads it.
 static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, long rs, cudaStream_t s,
-                                 int dst_parity = 1, PhaseEv* pe = nullptr)
+                                 int dst_parity = 1, PhaseEv* pe = nullptr, bool eq7 = true)
 {
     const Geometry& g = c->g;
     PHASE(t0, s);
@@ -979,7 +982,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
                     c->compact ? c->chunk_pos : nullptr};
         if (ps != (long)g.plane_elems) return fail(FDIRW_E_STATE, "precision study modes run through fdirw_run");
         CUDA_TRY(launch_superpose_study(a, c->prec_mode, s));
-        if (c->far) {  // study kernel has no tile sums: Eq.7 from a separate pass
+        if (c->far && eq7) {  // study kernel has no tile sums: Eq.7 from a separate pass
             CUDA_TRY(launch_tile_mass_padded(out, c->farmask, g, c->tile_buf + 1, s));
             return far_reduce(c, s, 0, 0.0);
         }
@@ -1003,6 +1006,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, c->ut.nd_tiles, s));
             if (c->n_ident)  // identity rows (impermeable solid): C_new = C_old
                 CUDA_TRY(launch_copy_chunks(src, out, ps, rs, c->ident_list, c->n_ident, g, s));
+            if (!eq7) return FDIRW_OK;
             if (ps == (long)g.plane_elems) CUDA_TRY(launch_tile_mass_padded(out, c->farmask, g, c->tile_buf + 1, s));
             else CUDA_TRY(launch_tile_mass(out, c->farmask, g, c->tile_buf + 1, s));
             return far_reduce(c, s, 0, 0.0);
@@ -1013,7 +1017,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
         PHASE(sup, s);
         PHASE(bnd0, s);
         PHASE(bnd1, s);
-        fdirw_status st = c->far ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
+        fdirw_status st = c->far && eq7 ? far_reduce(c, s, 0, 0.0) : FDIRW_OK;
         PHASE(t1, s);
         return st;
     }
@@ -1711,7 +1715,8 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     // holding the result (which of the two depends on the number of solid FD passes)
     auto macro = [&](float* in, cudaStream_t ss, float** res) -> fdirw_status {
         float* out = in == c->cpad[0] ? c->cpad[1] : c->cpad[0];
-        fdirw_status sst = enqueue_step(c, in, out + ioff, (long)g.plane_elems, g.nxp, ss);
+        fdirw_status sst = enqueue_step(c, in, out + ioff, (long)g.plane_elems, g.nxp, ss, 1, nullptr,
+                                        getenv("FDIRW_ABSORB_EQ7_TWICE") != nullptr);  // (A/B)
         if (sst != FDIRW_OK) return sst;
         CUDA_TRY(launch_absorb_tail(out, in, c->alpha, c->phase_pp, g, ab, c->kin_part, c->far_state, c->v_far,
                                     c->far ? 1 : 0, c->kin_rec, ss, res, c->abs_ctr));

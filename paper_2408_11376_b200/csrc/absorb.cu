@@ -13,6 +13,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "fdirw_internal.h"
 #include "layout.cuh"
 
@@ -150,6 +152,202 @@ __global__ void react_apply_kernel(const float* __restrict__ c, const float* __r
     }
 }
 
+// ---- the same three sweeps over groups of 4 consecutive x voxels (round 2) ----------------------
+// Each thread loads its group's values and phases as one float4 / uchar4 (the padded rows are
+// 16-byte aligned: kPadX = 8, nxp a multiple of 8), and the ±y / ±z neighbour groups the same
+// way only when a lane needs them (the −x / +x neighbours of the edge lanes are two scalar
+// loads); every voxel's value is the scalar kernel's expression in the same face order (identical
+// bits).  The scalar sweeps were issue-bound (~100 instructions per voxel, 60 % of cfg3o's grid
+// far field): solid_fd 12, react_alpha 17, react_apply 28 µs per macro step (ncu, cold).
+struct Nb4 {  // a group's 6 face neighbours: values v[f][l], phases h[f][l] (f: −x +x −y +y −z +z)
+    float v[6][4];
+    uint8_t h[6][4];
+};
+__device__ __forceinline__ void ld_grp(const float* __restrict__ c, const uint8_t* __restrict__ pp, long p,
+                                       float (&v)[4], uint8_t (&h)[4])
+{
+    const float4 a = *reinterpret_cast<const float4*>(c + p);
+    const uchar4 b = *reinterpret_cast<const uchar4*>(pp + p);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    h[0] = b.x; h[1] = b.y; h[2] = b.z; h[3] = b.w;
+}
+__device__ __forceinline__ void ld_nb(const float* __restrict__ c, const uint8_t* __restrict__ pp, long p, long dy,
+                                      long dz, const float (&v)[4], const uint8_t (&h)[4], Nb4& n)
+{
+    ld_grp(c, pp, p - dy, n.v[2], n.h[2]);
+    ld_grp(c, pp, p + dy, n.v[3], n.h[3]);
+    ld_grp(c, pp, p - dz, n.v[4], n.h[4]);
+    ld_grp(c, pp, p + dz, n.v[5], n.h[5]);
+    n.v[0][0] = c[p - 1];
+    n.h[0][0] = pp[p - 1];
+    n.v[1][3] = c[p + 4];
+    n.h[1][3] = pp[p + 4];
+#pragma unroll
+    for (int l = 1; l < 4; ++l) {
+        n.v[0][l] = v[l - 1];
+        n.h[0][l] = h[l - 1];
+        n.v[1][l - 1] = v[l];
+        n.h[1][l - 1] = h[l];
+    }
+}
+__device__ __forceinline__ void ld_a4(const float* __restrict__ a, long p, float (&v)[4])
+{
+    const float4 x = *reinterpret_cast<const float4*>(a + p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ void st_grp(float* __restrict__ out, long p, const float (&o)[4], int rem)
+{
+    if (rem >= 4) {
+        *reinterpret_cast<float4*>(out + p) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+#pragma unroll
+        for (int l = 0; l < 3; ++l)
+            if (l < rem) out[p + l] = o[l];
+    }
+}
+
+__global__ void __launch_bounds__(256) solid_fd4_kernel(const float* __restrict__ cin, float* __restrict__ cout,
+                                                        const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R,
+                                                        int nxp, int nyp, float lam)
+{
+    const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
+    const long dy = nxp, dz = (long)nxp * nyp;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
+        const int gx = i % nxg, r = i / nxg, y = r % ny, z = r / ny;
+        const long p = pidx(4 * gx, y, z, R, nxp, nyp);
+        float c[4], o[4];
+        uint8_t h[4];
+        ld_grp(cin, pp, p, c, h);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) o[l] = c[l];
+        if (h[0] == 0 || h[1] == 0 || h[2] == 0 || h[3] == 0) {
+            Nb4 n;
+            ld_nb(cin, pp, p, dy, dz, c, h, n);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                if (h[l] != 0) continue;
+                float acc = c[l];
+#pragma unroll
+                for (int f = 0; f < 6; ++f)
+                    if (n.h[f][l] == 0) acc = fmaf(lam, n.v[f][l] - c[l], acc);
+                o[l] = acc;
+            }
+        }
+        st_grp(cout, p, o, nx - 4 * gx);
+    }
+}
+
+__global__ void __launch_bounds__(256) react_alpha4_kernel(const float* __restrict__ c, const uint8_t* __restrict__ pp,
+                                                           int nx, int ny, int nz, int R, int nxp, int nyp, float kdt,
+                                                           float cSeq, float cLeq, float* __restrict__ alpha)
+{
+    const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
+    const long dy = nxp, dz = (long)nxp * nyp;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
+        const int gx = i % nxg, r = i / nxg, y = r % ny, z = r / ny;
+        const long p = pidx(4 * gx, y, z, R, nxp, nyp);
+        float v[4], o[4] = {1.f, 1.f, 1.f, 1.f};
+        uint8_t h[4];
+        ld_grp(c, pp, p, v, h);
+        if (h[0] == 1 || h[1] == 1 || h[2] == 1 || h[3] == 1) {
+            Nb4 n;
+            ld_nb(c, pp, p, dy, dz, v, h, n);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                if (h[l] != 1) continue;
+                const float fl = fL(v[l], cLeq);
+                float Q = 0.f;
+#pragma unroll
+                for (int f = 0; f < 6; ++f)
+                    if (n.h[f][l] == 0) Q += kdt * fS(n.v[f][l], cSeq) * fl;
+                const float avail = fmaxf(v[l] - cLeq, 0.f);
+                if (Q > avail) o[l] = Q > 0.f ? avail / Q : 0.f;
+            }
+        }
+        st_grp(alpha, p, o, nx - 4 * gx);
+    }
+}
+
+__global__ void __launch_bounds__(256, 3) react_apply4_kernel(const float* __restrict__ c, const float* __restrict__ alpha,
+                                                           const uint8_t* __restrict__ pp, int nx, int ny, int nz,
+                                                           int R, int nxp, int nyp, float kdt, float cSeq, float cLeq,
+                                                           float* __restrict__ out, double* __restrict__ part)
+{
+    __shared__ double rs[8], rl[8];
+    double ks = 0.0, kl = 0.0;
+    const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
+    const long dy = nxp, dz = (long)nxp * nyp;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
+        const int gx = i % nxg, r = i / nxg, y = r % ny, z = r / ny;
+        const long p = pidx(4 * gx, y, z, R, nxp, nyp);
+        const int rem = nx - 4 * gx;
+        float v[4], o[4];
+        uint8_t h[4];
+        ld_grp(c, pp, p, v, h);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) o[l] = v[l];
+        const bool any_s = h[0] == 0 || h[1] == 0 || h[2] == 0 || h[3] == 0;
+        const bool any_l = h[0] == 1 || h[1] == 1 || h[2] == 1 || h[3] == 1;
+        if (any_s || any_l) {
+            Nb4 n;
+            ld_nb(c, pp, p, dy, dz, v, h, n);
+            float ao[4], an[6][4];  // α of the own lanes and of the face neighbours
+            ld_a4(alpha, p, ao);
+            {  // (unconditional: one round of loads with the neighbour groups, not a third)
+                ld_a4(alpha, p - dy, an[2]);
+                ld_a4(alpha, p + dy, an[3]);
+                ld_a4(alpha, p - dz, an[4]);
+                ld_a4(alpha, p + dz, an[5]);
+                an[0][0] = alpha[p - 1];
+                an[1][3] = alpha[p + 4];
+#pragma unroll
+                for (int l = 1; l < 4; ++l) {
+                    an[0][l] = ao[l - 1];
+                    an[1][l - 1] = ao[l];
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                float x = v[l];
+                if (h[l] == 0) {
+                    const float fs = fS(v[l], cSeq);
+#pragma unroll
+                    for (int f = 0; f < 6; ++f)
+                        if (n.h[f][l] == 1) x += an[f][l] * (kdt * fs * fL(n.v[f][l], cLeq));
+                } else if (h[l] == 1) {
+                    const float fl = fL(v[l], cLeq);
+                    float Q = 0.f;
+#pragma unroll
+                    for (int f = 0; f < 6; ++f)
+                        if (n.h[f][l] == 0) Q += kdt * fS(n.v[f][l], cSeq) * fl;
+                    x -= ao[l] * Q;
+                }
+                o[l] = x;
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            if (l >= rem) break;
+            if (h[l] == 0) ks += (double)o[l];
+            else if (h[l] == 1) kl += (double)o[l];
+        }
+        st_grp(out, p, o, rem);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ks += __shfl_xor_sync(0xffffffffu, ks, o);
+        kl += __shfl_xor_sync(0xffffffffu, kl, o);
+    }
+    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = ks; rl[threadIdx.x >> 5] = kl; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ts = 0.0, tl = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { ts += rs[w]; tl += rl[w]; }
+        part[2 * blockIdx.x] = ts;
+        part[2 * blockIdx.x + 1] = tl;
+    }
+}
+
 // one block of 256 threads: thread t sums the partials b ≡ t (mod 256) in ascending b, then a
 // fixed shuffle tree and the warps in order (deterministic; the single-thread serial sum of the
 // first version cost ~38 µs per macro step)
@@ -200,6 +398,22 @@ cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uin
                                double* rec, cudaStream_t s, float** result, int* ctr)
 {
     const long n = (long)g.nx * g.ny * g.nz;
+    if (!getenv("FDIRW_ABSORB_SCALAR")) {  // (A/B: the per-voxel sweeps below; read per enqueue)
+        const long ng = (long)((g.nx + 3) / 4) * g.ny * g.nz;
+        for (int k = 0; k < ab.n_s; ++k) {
+            solid_fd4_kernel<<<gridn(ng), 256, 0, s>>>(cur, other, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.lam_s);
+            float* t = cur; cur = other; other = t;
+        }
+        react_alpha4_kernel<<<gridn(ng), 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt, ab.cSeq,
+                                                      ab.cLeq, alpha);
+        const unsigned nblk = gridn(ng);  // ≤ kAbsorbMaxBlocks: part holds 2 doubles per block
+        react_apply4_kernel<<<nblk, 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt,
+                                                 ab.cSeq, ab.cLeq, other, part);
+        float* t = cur; cur = other; other = t;
+        kin_final_kernel<<<1, 256, 0, s>>>(part, (int)nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec, ctr);
+        *result = cur;
+        return cudaGetLastError();
+    }
     // (2) solid FD, n_s passes
     for (int k = 0; k < ab.n_s; ++k) {
         solid_fd_kernel<<<gridn(n), 256, 0, s>>>(cur, other, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.lam_s);

@@ -156,3 +156,44 @@ def test_absorb_loop_many_tail_blocks(fd, oracle_lib):
     np.testing.assert_allclose(kin[-1, 1], got[m == 1].sum(), rtol=1e-9)   # Q_L
     tot = got[nf].sum() + kin[-1, 2] * ab.V_far
     assert abs(tot - M0) / M0 <= 1e-6
+
+
+@pytest.mark.parametrize("D_S", [fi.D_SLOW_SI, 0.0])
+def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S):
+    """The tail sweeps over groups of 4 x-voxels (float4 / uchar4 loads, neighbour groups only
+    where a lane needs them) against the per-voxel sweeps (FDIRW_ABSORB_SCALAR=1): every voxel's
+    value is the same expression in the same face order, so one macro step's field is bitwise
+    equal; the kinetics partials are summed per thread-group (another fixed order), so Q_S, Q_L,
+    c_far agree to rounding, and after that c_far feeds the next step's p_BC·c_far term.  nx = 37
+    (a ragged last group), R = 2, and the loop without a solid pass (D_S = 0)."""
+    import torch
+
+    shape = (23, 29, 37)
+    m = fi.with_far_field(fi.porous_particle(shape, 8, pore_r=(1.0, 2.0), porosity=0.3, seed=7), 8, 2.0)
+    T = fi.TABLE1
+    c0 = np.where(m == 1, T["c_L0"], np.where(m == 0, T["c_S0"], 0.0)).astype(np.float32)
+    nz, ny, nx = shape
+    p = fd.Params(nx=nx, ny=ny, nz=nz, dh=T["dh"], D_fast=fi.D_FAST_SI, D_slow=0.0, dt=T["dt"], radius=2,
+                  weights="fp32", v_far=2e4)
+    out = {}
+    for form in ("grouped", "scalar"):
+        if form == "scalar":
+            monkeypatch.setenv("FDIRW_ABSORB_SCALAR", "1")
+        else:
+            monkeypatch.delenv("FDIRW_ABSORB_SCALAR", raising=False)
+        ctx = fd.build_kernels(p, m)
+        try:
+            c = torch.from_numpy(c0).cuda()
+            fd.far_init(ctx, c, T["c_L0"])
+            k1 = fd.absorb_run(ctx, c, 1, D_S, 0.05, 1.0, 1e-5)
+            c1 = c.cpu().numpy()
+            k5 = fd.absorb_run(ctx, c, 5, D_S, 0.05, 1.0, 1e-5)
+            out[form] = (c1, k1, c.cpu().numpy(), k5)
+        finally:
+            fd.destroy(ctx)
+    a, b = out["grouped"], out["scalar"]
+    assert np.count_nonzero(a[0] != c0) > 0  # the step moved the field
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_allclose(a[1], b[1], rtol=1e-12)
+    np.testing.assert_allclose(a[2], b[2], rtol=1e-6, atol=1e-12)
+    np.testing.assert_allclose(a[3], b[3], rtol=1e-9)

@@ -10,6 +10,7 @@
 //   (5) kinetics Q_S, Q_L (fp64 deterministic sums)
 // The state is the padded layout of the fine path (zero halo); phases come from a padded
 // uint8 map (255 = outside the domain).
+#include <cub/device/device_scan.cuh>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -159,6 +160,25 @@ __global__ void react_apply_kernel(const float* __restrict__ c, const float* __r
 // loads); every voxel's value is the scalar kernel's expression in the same face order (identical
 // bits).  The scalar sweeps were issue-bound (~100 instructions per voxel, 60 % of cfg3o's grid
 // far field): solid_fd 12, react_alpha 17, react_apply 28 µs per macro step (ncu, cold).
+// per-block fp64 pair sums (shuffle tree, warps in order) → part[2·block], part[2·block + 1]
+__device__ __forceinline__ void block_pair_sum(double ks, double kl, double* __restrict__ part)
+{
+    __shared__ double rs[8], rl[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ks += __shfl_xor_sync(0xffffffffu, ks, o);
+        kl += __shfl_xor_sync(0xffffffffu, kl, o);
+    }
+    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = ks; rl[threadIdx.x >> 5] = kl; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ts = 0.0, tl = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { ts += rs[w]; tl += rl[w]; }
+        part[2 * blockIdx.x] = ts;
+        part[2 * blockIdx.x + 1] = tl;
+    }
+}
+
 struct Nb4 {  // a group's 6 face neighbours: values v[f][l], phases h[f][l] (f: −x +x −y +y −z +z)
     float v[6][4];
     uint8_t h[6][4];
@@ -206,10 +226,13 @@ __device__ __forceinline__ void st_grp(float* __restrict__ out, long p, const fl
     }
 }
 
+// SUMS: also the per-block fp64 sums of the written solid / liquid values (part[2b], part[2b + 1])
+template <bool SUMS>
 __global__ void __launch_bounds__(256) solid_fd4_kernel(const float* __restrict__ cin, float* __restrict__ cout,
                                                         const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R,
-                                                        int nxp, int nyp, float lam)
+                                                        int nxp, int nyp, float lam, double* __restrict__ part)
 {
+    double ks = 0.0, kl = 0.0;
     const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
     const long dy = nxp, dz = (long)nxp * nyp;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
@@ -234,17 +257,29 @@ __global__ void __launch_bounds__(256) solid_fd4_kernel(const float* __restrict_
             }
         }
         st_grp(cout, p, o, nx - 4 * gx);
+        if constexpr (SUMS) {
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                if (l >= nx - 4 * gx) break;
+                if (h[l] == 0) ks += (double)o[l];
+                else if (h[l] == 1) kl += (double)o[l];
+            }
+        }
     }
+    if constexpr (SUMS) block_pair_sum(ks, kl, part);
 }
 
+// list: visit only the listed groups (the interface groups), else every group
 __global__ void __launch_bounds__(256) react_alpha4_kernel(const float* __restrict__ c, const uint8_t* __restrict__ pp,
                                                            int nx, int ny, int nz, int R, int nxp, int nyp, float kdt,
-                                                           float cSeq, float cLeq, float* __restrict__ alpha)
+                                                           float cSeq, float cLeq, float* __restrict__ alpha,
+                                                           const int* __restrict__ list, int n_list)
 {
-    const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
+    const int nxg = (nx + 3) >> 2, ng = list ? n_list : nxg * ny * nz;
     const long dy = nxp, dz = (long)nxp * nyp;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
-        const int gx = i % nxg, r = i / nxg, y = r % ny, z = r / ny;
+        const int gi = list ? list[i] : i;
+        const int gx = gi % nxg, r = gi / nxg, y = r % ny, z = r / ny;
         const long p = pidx(4 * gx, y, z, R, nxp, nyp);
         float v[4], o[4] = {1.f, 1.f, 1.f, 1.f};
         uint8_t h[4];
@@ -268,17 +303,23 @@ __global__ void __launch_bounds__(256) react_alpha4_kernel(const float* __restri
     }
 }
 
+// LIST: visit the listed (interface) groups and write each group's 4 values to tmp[i] (the
+// scatter kernel stores them once every group has read its neighbours); else every group,
+// written to out, with the kinetics partial sums
+template <bool LIST>
 __global__ void __launch_bounds__(256, 3) react_apply4_kernel(const float* __restrict__ c, const float* __restrict__ alpha,
                                                            const uint8_t* __restrict__ pp, int nx, int ny, int nz,
                                                            int R, int nxp, int nyp, float kdt, float cSeq, float cLeq,
-                                                           float* __restrict__ out, double* __restrict__ part)
+                                                           float* __restrict__ out, double* __restrict__ part,
+                                                           const int* __restrict__ list, int n_list,
+                                                           float4* __restrict__ tmp)
 {
-    __shared__ double rs[8], rl[8];
     double ks = 0.0, kl = 0.0;
-    const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
+    const int nxg = (nx + 3) >> 2, ng = LIST ? n_list : nxg * ny * nz;
     const long dy = nxp, dz = (long)nxp * nyp;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
-        const int gx = i % nxg, r = i / nxg, y = r % ny, z = r / ny;
+        const int gi = LIST ? list[i] : i;
+        const int gx = gi % nxg, r = gi / nxg, y = r % ny, z = r / ny;
         const long p = pidx(4 * gx, y, z, R, nxp, nyp);
         const int rem = nx - 4 * gx;
         float v[4], o[4];
@@ -325,27 +366,79 @@ __global__ void __launch_bounds__(256, 3) react_apply4_kernel(const float* __res
                 o[l] = x;
             }
         }
+        if constexpr (LIST) {
+            tmp[i] = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                if (l >= rem) break;
+                if (h[l] == 0) ks += (double)o[l];
+                else if (h[l] == 1) kl += (double)o[l];
+            }
+            st_grp(out, p, o, rem);
+        }
+    }
+    if constexpr (!LIST) block_pair_sum(ks, kl, part);
+}
+
+// the interface groups' new values tmp[i] → the field (in place: every group has read its
+// neighbours), with the per-block sums of (new − old) per phase: the kinetics of the whole field
+// are the sweep's sums of c1 plus these
+__global__ void __launch_bounds__(256) iface_scatter_kernel(float* __restrict__ f, const uint8_t* __restrict__ pp,
+                                                            int nx, int ny, int nz, int R, int nxp, int nyp,
+                                                            const int* __restrict__ list, int n_list,
+                                                            const float4* __restrict__ tmp, double* __restrict__ part)
+{
+    double ks = 0.0, kl = 0.0;
+    const int nxg = (nx + 3) >> 2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_list; i += gridDim.x * blockDim.x) {
+        const int gi = list[i];
+        const int gx = gi % nxg, r = gi / nxg, y = r % ny, z = r / ny;
+        const long p = pidx(4 * gx, y, z, R, nxp, nyp);
+        const int rem = nx - 4 * gx;
+        float v[4];
+        uint8_t h[4];
+        ld_grp(f, pp, p, v, h);
+        const float4 t = tmp[i];
+        const float o[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
             if (l >= rem) break;
-            if (h[l] == 0) ks += (double)o[l];
-            else if (h[l] == 1) kl += (double)o[l];
+            if (h[l] == 0) ks += (double)o[l] - (double)v[l];
+            else if (h[l] == 1) kl += (double)o[l] - (double)v[l];
         }
-        st_grp(out, p, o, rem);
+        st_grp(f, p, o, rem);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        ks += __shfl_xor_sync(0xffffffffu, ks, o);
-        kl += __shfl_xor_sync(0xffffffffu, kl, o);
+    block_pair_sum(ks, kl, part);
+}
+
+// interface flag per group: a solid lane with a liquid face neighbour or a liquid lane with a solid one
+__global__ void iface_flag_kernel(const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R, int nxp, int nyp,
+                                  int* __restrict__ flag)
+{
+    const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
+    const long dy = nxp, dz = (long)nxp * nyp;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
+        const int gx = i % nxg, r = i / nxg, y = r % ny, z = r / ny;
+        const long p = pidx(4 * gx, y, z, R, nxp, nyp);
+        int f = 0;
+        for (int l = 0; l < 4 && 4 * gx + l < nx; ++l) {
+            const uint8_t h = pp[p + l];
+            if (h > 1) continue;
+            const long q[6] = {p + l - 1, p + l + 1, p + l - dy, p + l + dy, p + l - dz, p + l + dz};
+            for (int k = 0; k < 6; ++k) {
+                const uint8_t hq = pp[q[k]];
+                if (hq <= 1 && hq != h) f = 1;
+            }
+        }
+        flag[i] = f;
     }
-    if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = ks; rl[threadIdx.x >> 5] = kl; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double ts = 0.0, tl = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { ts += rs[w]; tl += rl[w]; }
-        part[2 * blockIdx.x] = ts;
-        part[2 * blockIdx.x + 1] = tl;
-    }
+}
+__global__ void iface_compact_kernel(const int* __restrict__ flag, const int* __restrict__ pos, int ng,
+                                     int* __restrict__ list)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x)
+        if (flag[i]) list[pos[i]] = i;
 }
 
 // one block of 256 threads: thread t sums the partials b ≡ t (mod 256) in ascending b, then a
@@ -354,11 +447,13 @@ __global__ void __launch_bounds__(256, 3) react_apply4_kernel(const float* __res
 __global__ void __launch_bounds__(256) kin_final_kernel(const double* __restrict__ part, int nblk,
                                                         double* __restrict__ far_state, double v_far, double n_solid,
                                                         double cSeq, int far, double* __restrict__ rec,
-                                                        int* __restrict__ ctr)
+                                                        int* __restrict__ ctr, const double* __restrict__ part2 = nullptr,
+                                                        int nblk2 = 0)
 {
     __shared__ double rs[8], rl[8];
     double s = 0.0, l = 0.0;
     for (int b = threadIdx.x; b < nblk; b += blockDim.x) { s += part[2 * b]; l += part[2 * b + 1]; }
+    for (int b = threadIdx.x; b < nblk2; b += blockDim.x) { s += part2[2 * b]; l += part2[2 * b + 1]; }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -393,22 +488,94 @@ cudaError_t launch_phase_pad(const uint8_t* mask, const Geometry& g, uint8_t* pp
     return cudaGetLastError();
 }
 
+cudaError_t build_iface_list(const uint8_t* pp, const Geometry& g, IfaceList* out, cudaStream_t s)
+{
+    const long ngl = (long)((g.nx + 3) / 4) * g.ny * g.nz;
+    const int ng = (int)ngl;
+    int *flag = nullptr, *pos = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    cudaError_t e = cudaMalloc(&flag, (size_t)(ng + 1) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&pos, (size_t)(ng + 1) * 4);
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, (size_t)(ng + 1) * 4, s);
+    if (e == cudaSuccess) {
+        iface_flag_kernel<<<gridn(ngl), 256, 0, s>>>(pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, flag);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, ng + 1, s);
+    if (e == cudaSuccess) e = cudaMalloc(&tmp, tb);
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, ng + 1, s);
+    int n = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&n, pos + ng, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMalloc(&out->list, (size_t)(n > 0 ? n : 1) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&out->tmp, (size_t)(n > 0 ? n : 1) * 16);
+    if (e == cudaSuccess && n > 0) {
+        iface_compact_kernel<<<gridn(ngl), 256, 0, s>>>(flag, pos, ng, out->list);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(flag);
+    cudaFree(pos);
+    cudaFree(tmp);
+    if (e != cudaSuccess) {
+        cudaFree(out->list);
+        cudaFree(out->tmp);
+        out->list = nullptr;
+        out->tmp = nullptr;
+        return e;
+    }
+    out->n = n;
+    return cudaSuccess;
+}
+
 cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uint8_t* pp, const Geometry& g,
                                const AbsorbArgs& ab, double* part, double* far_state, double v_far, int far,
-                               double* rec, cudaStream_t s, float** result, int* ctr)
+                               double* rec, cudaStream_t s, float** result, int* ctr, const IfaceList* iface)
 {
     const long n = (long)g.nx * g.ny * g.nz;
-    if (!getenv("FDIRW_ABSORB_SCALAR")) {  // (A/B: the per-voxel sweeps below; read per enqueue)
-        const long ng = (long)((g.nx + 3) / 4) * g.ny * g.nz;
+    const bool scalar = getenv("FDIRW_ABSORB_SCALAR") != nullptr;  // (A/B switches, read per enqueue)
+    const bool sweep = getenv("FDIRW_ABSORB_SWEEP") != nullptr;
+    const long ng = (long)((g.nx + 3) / 4) * g.ny * g.nz;
+    if (!scalar && !sweep && iface && iface->list && ab.n_s > 0) {
+        // the solid pass sweeps the grid (with the field's sums); α, the apply and its in-place
+        // scatter visit only the interface groups; the result stays in the solid pass's buffer
+        for (int k = 0; k + 1 < ab.n_s; ++k) {
+            solid_fd4_kernel<false><<<gridn(ng), 256, 0, s>>>(cur, other, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp,
+                                                              ab.lam_s, nullptr);
+            float* t = cur; cur = other; other = t;
+        }
+        const unsigned nb1 = gridn(ng);  // ≤ kAbsorbMaxBlocks
+        solid_fd4_kernel<true><<<nb1, 256, 0, s>>>(cur, other, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.lam_s,
+                                                   part);
+        float* t = cur; cur = other; other = t;
+        const int ni = (int)iface->n;
+        const unsigned nb2 = gridn(ni > 0 ? ni : 1);
+        if (ni > 0) {
+            react_alpha4_kernel<<<gridn(ni), 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt,
+                                                          ab.cSeq, ab.cLeq, alpha, iface->list, ni);
+            react_apply4_kernel<true><<<gridn(ni), 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp,
+                                                                ab.kdt, ab.cSeq, ab.cLeq, nullptr, nullptr,
+                                                                iface->list, ni, iface->tmp);
+            iface_scatter_kernel<<<nb2, 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, iface->list, ni,
+                                                     iface->tmp, part + 2 * kAbsorbMaxBlocks);
+        }
+        kin_final_kernel<<<1, 256, 0, s>>>(part, (int)nb1, far_state, v_far, ab.n_solid, ab.cSeq, far, rec, ctr,
+                                           part + 2 * kAbsorbMaxBlocks, ni > 0 ? (int)nb2 : 0);
+        *result = cur;
+        return cudaGetLastError();
+    }
+    if (!scalar) {
         for (int k = 0; k < ab.n_s; ++k) {
-            solid_fd4_kernel<<<gridn(ng), 256, 0, s>>>(cur, other, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.lam_s);
+            solid_fd4_kernel<false><<<gridn(ng), 256, 0, s>>>(cur, other, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp,
+                                                              ab.lam_s, nullptr);
             float* t = cur; cur = other; other = t;
         }
         react_alpha4_kernel<<<gridn(ng), 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt, ab.cSeq,
-                                                      ab.cLeq, alpha);
+                                                      ab.cLeq, alpha, nullptr, 0);
         const unsigned nblk = gridn(ng);  // ≤ kAbsorbMaxBlocks: part holds 2 doubles per block
-        react_apply4_kernel<<<nblk, 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt,
-                                                 ab.cSeq, ab.cLeq, other, part);
+        react_apply4_kernel<false><<<nblk, 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt,
+                                                        ab.cSeq, ab.cLeq, other, part, nullptr, 0, nullptr);
         float* t = cur; cur = other; other = t;
         kin_final_kernel<<<1, 256, 0, s>>>(part, (int)nblk, far_state, v_far, ab.n_solid, ab.cSeq, far, rec, ctr);
         *result = cur;

@@ -75,7 +75,8 @@ struct fdirw_ctx {
     int prec_mode = 0;            // 0 = default kernel; 1/2/3 = §3.3 study modes (absorb.cu)
     uint8_t* phase_pp = nullptr;  // padded phase map (255 outside)
     float* alpha = nullptr;       // padded scratch for the reaction clamp
-    double* kin_part = nullptr;
+    double* kin_part = nullptr;   // 4·kAbsorbMaxBlocks doubles: sweep partials, interface partials
+    IfaceList iface;              // built on the first fdirw_absorb_run
     double* kin_rec = nullptr;
     int kin_cap = 0;
     // N3 loop replay: two macro steps captured once (graph_abs), the kinetics record slot taken
@@ -397,6 +398,8 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->phase_pp);
     cudaFree(c->alpha);
     cudaFree(c->kin_part);
+    cudaFree(c->iface.list);
+    cudaFree(c->iface.tmp);
     cudaFree(c->kin_rec);
     cudaFree(c->abs_ctr);
     if (c->graph_abs) cudaGraphExecDestroy(c->graph_abs);
@@ -1699,7 +1702,7 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     ab.n_solid = c->n_solid;
     fdirw_status st;
     if (!c->alpha && (st = alloc((void**)&c->alpha, g.state_elems * 4, "reaction scratch")) != FDIRW_OK) return st;
-    if (!c->kin_part && (st = alloc((void**)&c->kin_part, 2 * kAbsorbMaxBlocks * 8, "kinetics")) != FDIRW_OK) return st;
+    if (!c->kin_part && (st = alloc((void**)&c->kin_part, 4 * kAbsorbMaxBlocks * 8, "kinetics")) != FDIRW_OK) return st;
     if (n > c->kin_cap) {
         cudaFree(c->kin_rec);
         c->kin_rec = nullptr;
@@ -1708,6 +1711,7 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     }
     if (n == 0) return FDIRW_OK;
     if (!c->abs_ctr && (st = alloc((void**)&c->abs_ctr, 4, "kinetics counter")) != FDIRW_OK) return st;
+    if (!c->iface.list) CUDA_TRY(build_iface_list(c->phase_pp, g, &c->iface, s));
     CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s, c->farmask));
     CUDA_TRY(cudaMemsetAsync(c->abs_ctr, 0, 4, s));
     const size_t ioff = (size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX;
@@ -1719,7 +1723,7 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
                                         getenv("FDIRW_ABSORB_EQ7_TWICE") != nullptr);  // (A/B)
         if (sst != FDIRW_OK) return sst;
         CUDA_TRY(launch_absorb_tail(out, in, c->alpha, c->phase_pp, g, ab, c->kin_part, c->far_state, c->v_far,
-                                    c->far ? 1 : 0, c->kin_rec, ss, res, c->abs_ctr));
+                                    c->far ? 1 : 0, c->kin_rec, ss, res, c->abs_ctr, &c->iface));
         return FDIRW_OK;
     };
     const bool same = c->graph_abs && c->abs_rec_key == c->kin_rec && c->abs_key.n_s == ab.n_s &&

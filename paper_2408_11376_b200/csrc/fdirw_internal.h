@@ -225,10 +225,19 @@ struct AbsorbArgs {
     double n_solid;   // N_S (for c̄_S)
 };
 cudaError_t launch_phase_pad(const uint8_t* mask, const Geometry& g, uint8_t* pp, cudaStream_t s);
+// the loop's interface groups (absorb.cu): groups of 4 x-voxels holding a solid voxel with a liquid
+// face neighbour or a liquid voxel with a solid one — the only voxels the reaction changes.
+// *list (cudaMalloc'ed, ascending group index) and *n; *tmp = n float4 of scratch
+struct IfaceList {
+    int* list = nullptr;
+    long n = 0;
+    float4* tmp = nullptr;
+};
+cudaError_t build_iface_list(const uint8_t* pp, const Geometry& g, IfaceList* out, cudaStream_t s);
 cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uint8_t* pp, const Geometry& g,
                                const AbsorbArgs& ab, double* part, double* far_state, double v_far, int far,
                                double* rec, cudaStream_t s, float** result,
-                               int* ctr = nullptr);
+                               int* ctr = nullptr, const IfaceList* iface = nullptr);
 struct StudyArgs {
     const float* cpad;
     float* out;           // padded layout

@@ -160,8 +160,9 @@ def test_absorb_loop_many_tail_blocks(fd, oracle_lib):
 
 @pytest.mark.parametrize("D_S", [fi.D_SLOW_SI, 0.0])
 def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S):
-    """The tail sweeps over groups of 4 x-voxels (float4 / uchar4 loads, neighbour groups only
-    where a lane needs them) against the per-voxel sweeps (FDIRW_ABSORB_SCALAR=1): every voxel's
+    """The tail over groups of 4 x-voxels — by default the solid pass sweeps the grid and α / the
+    apply / its in-place scatter visit only the interface groups; FDIRW_ABSORB_SWEEP=1 sweeps all
+    three — against the per-voxel sweeps (FDIRW_ABSORB_SCALAR=1): every voxel's
     value is the same expression in the same face order, so one macro step's field is bitwise
     equal; the kinetics partials are summed per thread-group (another fixed order), so Q_S, Q_L,
     c_far agree to rounding, and after that c_far feeds the next step's p_BC·c_far term.  nx = 37
@@ -176,11 +177,13 @@ def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S):
     p = fd.Params(nx=nx, ny=ny, nz=nz, dh=T["dh"], D_fast=fi.D_FAST_SI, D_slow=0.0, dt=T["dt"], radius=2,
                   weights="fp32", v_far=2e4)
     out = {}
-    for form in ("grouped", "scalar"):
+    for form in ("default", "sweep", "scalar"):
+        monkeypatch.delenv("FDIRW_ABSORB_SCALAR", raising=False)
+        monkeypatch.delenv("FDIRW_ABSORB_SWEEP", raising=False)
         if form == "scalar":
             monkeypatch.setenv("FDIRW_ABSORB_SCALAR", "1")
-        else:
-            monkeypatch.delenv("FDIRW_ABSORB_SCALAR", raising=False)
+        elif form == "sweep":
+            monkeypatch.setenv("FDIRW_ABSORB_SWEEP", "1")
         ctx = fd.build_kernels(p, m)
         try:
             c = torch.from_numpy(c0).cuda()
@@ -191,9 +194,10 @@ def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S):
             out[form] = (c1, k1, c.cpu().numpy(), k5)
         finally:
             fd.destroy(ctx)
-    a, b = out["grouped"], out["scalar"]
-    assert np.count_nonzero(a[0] != c0) > 0  # the step moved the field
-    np.testing.assert_array_equal(a[0], b[0])
-    np.testing.assert_allclose(a[1], b[1], rtol=1e-12)
-    np.testing.assert_allclose(a[2], b[2], rtol=1e-6, atol=1e-12)
-    np.testing.assert_allclose(a[3], b[3], rtol=1e-9)
+    b = out["scalar"]
+    for a in (out["default"], out["sweep"]):
+        assert np.count_nonzero(a[0] != c0) > 0  # the step moved the field
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_allclose(a[1], b[1], rtol=1e-12)
+        np.testing.assert_allclose(a[2], b[2], rtol=1e-6, atol=1e-12)
+        np.testing.assert_allclose(a[3], b[3], rtol=1e-9)

@@ -79,6 +79,8 @@ struct KgenArgs {
     // Chebyshev evaluation of A^{n_fd − cheb_pre} (kgen.cu, reading A30): degree cheb_m (0 =
     // direct substeps), coefficients cheb_c[0..cheb_m] (device, fp32), face numbers 2μ = 4λ/(1 − a)
     int cheb_m, cheb_pre;  // Chebyshev degree (0 = direct) after cheb_pre direct substeps
+    int cheb_open = 0;     // windows touching the N2 reservoir also take the recurrence (reduced-
+                           // precision storage only, reading A30); else they run the literal substeps
     const float* cheb_c;
     float mu2_ff, mu2_fs, mu2_ss;
     int fmt, mass_fix;

@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         // only), which removes the divergent branches; measured faster there (cfg5 R8 967 →
         // 908 ms) and slower at R5 (140 → 155 ms), so R ≤ 5 keep the guard.
         const bool act = R >= 6 || col;
-        const bool cheb = a.cheb_m && !open;
+        const bool cheb = a.cheb_m && (!open || a.cheb_open);
         const int n_direct = cheb ? a.cheb_pre : a.n_fd;
         for (int k = 0; k < n_direct; ++k) {
             float* b = buf + (k & 1) * (NT * Lp);
@@ -372,6 +372,11 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
                         s2 = fma2(lyp2[h], pk2(yp[2 * h], yp[2 * h + 1]), s2);
                         if (first) s2 = fma2(s2, pk2(0.5f, 0.5f), pk2(-0.f, -0.f));  // exact halving
                         upk2(s2, prv[2 * h], prv[2 * h + 1]);
+                        if (rmask) {  // reservoir cells (open windows, A30): Dirichlet 0 in every t_k
+                            if ((rmask >> (2 * h)) & 1u) prv[2 * h] = 0.f;
+                            if ((rmask >> (2 * h + 1)) & 1u) prv[2 * h + 1] = 0.f;
+                            s2 = pk2(prv[2 * h], prv[2 * h + 1]);
+                        }
                         const unsigned long long a2 = fma2(pk2(ck, ck), s2, pk2(acc[2 * h], acc[2 * h + 1]));
                         upk2(a2, acc[2 * h], acc[2 * h + 1]);
                     }
@@ -382,6 +387,7 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
                         v = fmaf(lym1, ym[L - 1], v);
                         v = fmaf(lyp1, yp[L - 1], v);
                         if (first) v *= 0.5f;
+                        if ((rmask >> (L - 1)) & 1u) v = 0.f;
                         prv[L - 1] = v;
                         acc[L - 1] = fmaf(ck, v, acc[L - 1]);
                     }

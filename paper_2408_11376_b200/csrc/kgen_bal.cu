@@ -82,7 +82,10 @@ struct BalSeg {
 
 }  // namespace
 
-template <int R, int SEG, bool CLEAN>
+// CO: the build lets windows touching the N2 reservoir take the recurrence (a.cheb_open); a
+// separate instantiation, so closed-domain builds keep the code (and registers) without the
+// reservoir masks
+template <int R, int SEG, bool CLEAN, bool CO>
 __device__ __forceinline__ void bal_body(const KgenArgs& a)
 {
     using S = BalShape<R>;
@@ -265,7 +268,7 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
         auto above = [](int sd, int i) { return G::Z0(sd) + i < L - 1; };
 
         const bool act = real;
-        const bool cheb = a.cheb_m && !open;
+        const bool cheb = a.cheb_m && (!open || (CO && a.cheb_open));
         const int n_direct = cheb ? a.cheb_pre : a.n_fd;
         unsigned ps = 0;
         // ---- literal substeps, flux form in the column kernel's order (z faces first for R ≤ 5) ----
@@ -331,7 +334,8 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
                     pv[sd][i] = 0.f;
                     acc[sd][i] = c[sd][i] * cc[0];
                 }
-            auto step = [&](float (&cur)[2][6], float (&prv)[2][6], const int k, const bool first) {
+            auto step = [&](auto openc, float (&cur)[2][6], float (&prv)[2][6], const int k, const bool first) {
+                constexpr bool OPEN = decltype(openc)::value;
                 float* b = buf + (ps & 1u) * S::BUFF;
                 if (act) store_own(b, cur[0], cur[1]);
                 cta_sync_any_pc<S::NT, CLEAN>();
@@ -370,6 +374,11 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
                             for (int f = 0; f < 4; ++f) s2 = fma2(fl[sd][f][hh], pk2(nb[sd][f][i0], nb[sd][f][i1]), s2);
                             if (first) s2 = fma2(s2, pk2(0.5f, 0.5f), pk2(-0.f, -0.f));
                             upk2(s2, prv[sd][i0], prv[sd][i1]);
+                            if constexpr (OPEN) {  // reservoir cells (open windows, A30): Dirichlet 0 in every t_k
+                                if ((rmask[sd] >> i0) & 1u) prv[sd][i0] = 0.f;
+                                if ((rmask[sd] >> i1) & 1u) prv[sd][i1] = 0.f;
+                                s2 = pk2(prv[sd][i0], prv[sd][i1]);
+                            }
                             const unsigned long long a2 = fma2(pk2(ck, ck), s2, pk2(acc[sd][i0], acc[sd][i1]));
                             upk2(a2, acc[sd][i0], acc[sd][i1]);
                         }
@@ -379,6 +388,8 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
 #pragma unroll
                             for (int f = 0; f < 4; ++f) v = fmaf(fl1[sd][f], nb[sd][f][i], v);
                             if (first) v *= 0.5f;
+                            if constexpr (OPEN)
+                                if ((rmask[sd] >> i) & 1u) v = 0.f;
                             prv[sd][i] = v;
                             acc[sd][i] = fmaf(ck, v, acc[sd][i]);
                         }
@@ -388,11 +399,18 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
                 }
             };
             const int m = a.cheb_m;
-            step(c, pv, 0, true);
-            for (int k = 1; k < m; k += 2) {
-                step(pv, c, k, false);
-                if (k + 1 < m) step(c, pv, k + 1, false);
-            }
+            // (open windows, which take the recurrence only with reduced-precision storage, run
+            // their own instantiation with the reservoir masks: closed windows keep the unmasked
+            // code and its registers)
+            auto recur = [&](auto openc) {
+                step(openc, c, pv, 0, true);
+                for (int k = 1; k < m; k += 2) {
+                    step(openc, pv, c, k, false);
+                    if (k + 1 < m) step(openc, c, pv, k + 1, false);
+                }
+            };
+            if (!open) recur(std::integral_constant<bool, false>{});
+            else if constexpr (CO) recur(std::integral_constant<bool, true>{});
 #pragma unroll
             for (int sd = 0; sd < 2; ++sd)
 #pragma unroll
@@ -474,39 +492,39 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
     }
 }
 
-template <int R, bool CLEAN>
+template <int R, bool CLEAN, bool CO>
 __global__ void __launch_bounds__(BalShape<R>::NT, BalShape<R>::kMinBlocks) kgen_bal_kernel(const KgenArgs a)
 {
     constexpr int NPW = BalShape<R>::NPW;
     if constexpr (BalShape<R>::NSEG == 2) {
-        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN>(a);
-        else bal_body<R, 1, CLEAN>(a);
+        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN, CO>(a);
+        else bal_body<R, 1, CLEAN, CO>(a);
     } else {
         static_assert(BalShape<R>::NSEG == 3, "R = 5, 8");
-        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN>(a);
-        else if (threadIdx.x < 2 * NPW) bal_body<R, 1, CLEAN>(a);
-        else bal_body<R, 2, CLEAN>(a);
+        if (threadIdx.x < NPW) bal_body<R, 0, CLEAN, CO>(a);
+        else if (threadIdx.x < 2 * NPW) bal_body<R, 1, CLEAN, CO>(a);
+        else bal_body<R, 2, CLEAN, CO>(a);
     }
 }
 
-template <int R, bool CLEAN>
+template <int R, bool CLEAN, bool CO>
 static cudaError_t launch_bal_r(const KgenArgs& a, cudaStream_t s)
 {
     using S = BalShape<R>;
     const long nsrc = a.src_list ? a.n_list : (long)a.nx * a.ny * (a.sz1 - a.sz0);
     if (nsrc <= 0) return cudaSuccess;
     const size_t smem = S::smem_bytes + (!a.cheb_m ? 0 : ((size_t)(a.cheb_m + 1) * 4 + 15) / 16 * 16);
-    cudaError_t e = cudaFuncSetAttribute(kgen_bal_kernel<R, CLEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kgen_bal_kernel<R, CLEAN, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_bal_kernel<R, CLEAN>, S::NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kgen_bal_kernel<R, CLEAN, CO>, S::NT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     long grid = (long)sms * per_sm;
     if (grid > nsrc) grid = nsrc;
-    kgen_bal_kernel<R, CLEAN><<<(unsigned)grid, S::NT, smem, s>>>(a);
+    kgen_bal_kernel<R, CLEAN, CO><<<(unsigned)grid, S::NT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -518,8 +536,13 @@ cudaError_t launch_kgen_bal(const KgenArgs& a, int R, cudaStream_t s)
         const char* ev = getenv("FDIRW_KGEN_SYNCCHECK");
         return ev && ev[0] == '1';
     }();
-    if (R == 5) return clean ? launch_bal_r<5, true>(a, s) : launch_bal_r<5, false>(a, s);
-    if (R == 8) return clean ? launch_bal_r<8, true>(a, s) : launch_bal_r<8, false>(a, s);
+    const bool co = a.cheb_m && a.cheb_open;
+    if (R == 5)
+        return clean ? (co ? launch_bal_r<5, true, true>(a, s) : launch_bal_r<5, true, false>(a, s))
+                     : (co ? launch_bal_r<5, false, true>(a, s) : launch_bal_r<5, false, false>(a, s));
+    if (R == 8)
+        return clean ? (co ? launch_bal_r<8, true, true>(a, s) : launch_bal_r<8, true, false>(a, s))
+                     : (co ? launch_bal_r<8, false, true>(a, s) : launch_bal_r<8, false, false>(a, s));
     return cudaErrorNotSupported;
 }
 

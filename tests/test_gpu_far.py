@@ -188,3 +188,64 @@ def test_identity_rows_bitwise(fd):
     solid = mask == 0
     c = W.shape[-1] // 2
     np.testing.assert_array_equal(W[solid][:, c], 1.0)  # slow sources: W_s = δ
+
+
+@pytest.mark.parametrize("fmt,R", [("bf16", 5), ("fp16", 3), ("bf16", 8)])
+def test_open_windows_recurrence_reduced_precision(fd, oracle_lib, monkeypatch, fmt, R):
+    """With fp16 / bf16 storage, windows touching the reservoir take the Chebyshev recurrence too
+    (reading A30; fp32 storage keeps the literal substeps).  Against the literal substeps
+    (FDIRW_KGEN_OPEN_LITERAL=1) on the same geometry: every stored weight within one storage ulp
+    of the literal one, or within 2e-7 absolute (the recurrence's rounding, on the source's
+    scale) where the weight is tiny; the kept masses M_s vs the oracle's within 2e-4 relative;
+    one step of the field vs the oracle within the reduced-precision bar."""
+    import torch
+    from oracle import farfield as ff
+
+    shape = (14, 13, 15) if R < 8 else (19, 18, 20)
+    mask = _open_mask(shape, 4)
+    cfg = small_cfg(shape, R, 1000, D_slow=1e-3, weights=fmt)
+    box = (0, shape[2], 0, shape[1], 0, shape[0])
+    out = {}
+    for form in ("recurrence", "literal"):
+        if form == "literal":
+            monkeypatch.setenv("FDIRW_KGEN_OPEN_LITERAL", "1")
+        else:
+            monkeypatch.delenv("FDIRW_KGEN_OPEN_LITERAL", raising=False)
+        ctx = fd.build_kernels(lib_params(cfg, v_far=2000.0), mask)
+        try:
+            out[form] = fd.export_kernels(ctx, box)
+        finally:
+            fd.destroy(ctx)
+    K = (2 * R + 1) ** 3
+    A, B = out["recurrence"].reshape(-1, K), out["literal"].reshape(-1, K)
+    src = (mask.reshape(-1) <= 1)
+    A, B = A[src], B[src]
+    c = K // 2
+    off = np.ones(K, bool)
+    off[c] = False
+    ulp = {"bf16": 2.0 ** -7, "fp16": 2.0 ** -10}[fmt]  # one ulp relative, at worst
+    d = np.abs(A[:, off] - B[:, off])
+    excess = d - ulp * np.abs(B[:, off])
+    assert np.all(excess <= 2e-7), (excess.max(), np.count_nonzero(excess > 2e-7), d.max())
+    # the kernels' kept masses M_s (a column sums to M_s through the fp32-pair diagonal) against
+    # the oracle's fp64 kernels: the recurrence's rounding is absolute on the source's scale
+    # (measured, tests/diag_open_recurrence.py: relative ≤ 5.7e-5 vs the literal substeps' 4.6e-6
+    # on these grids) — bounded here at 2e-4, ten times below bf16's half-ulp 2^-9 that every
+    # stored weight carries; the diagonals differ from the literal path's by the off-centre
+    # weights' storage rounding on top
+    pbo = oracle_problem(cfg, mask)
+    Mo = oracle_lib.build_kernels(pbo).reshape(-1, K)[src].sum(1)
+    ow = oracle_lib.open_windows(pbo).reshape(-1)[src]
+    for W in (A, B):
+        rel = np.abs(W.astype(np.float64).sum(1) - Mo)[ow] / Mo[ow]
+        assert rel.max() <= 2e-4, rel.max()
+    assert np.max(np.abs(A[:, c] - B[:, c])) <= 1e-4, np.max(np.abs(A[:, c] - B[:, c]))
+    # and the stepped field against the oracle (exact kernels), 1 step
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=4).astype(np.float64) * (mask != 2)
+    monkeypatch.delenv("FDIRW_KGEN_OPEN_LITERAL", raising=False)
+    got, cf, M0, _ = _gpu_far(fd, cfg, mask, c0, 0.5, 1, v_far=2000.0)
+    refC, refcf, _ = ff.run_full(pb, c0, 0.5, 2000.0, 1)
+    nf = mask != 2
+    assert rel_l2(got[nf], refC[nf]) <= 5e-3
+    assert (got.sum() + cf * 2000.0 - M0) / M0 == pytest.approx(0.0, abs=1e-9)

@@ -92,6 +92,16 @@ def main():
         fd.far_init(ctx, c, 0.5)
         fd.run(ctx, c, 2)
         fd.far_get(ctx)
+    # N3 absorption loop (impermeable solid context): interface-group list, grouped sweeps,
+    # in-place scatter, the replayed two-step graph and an odd tail; without a solid pass too
+    nz, ny, nx = shape
+    ap = fd.Params(nx=nx, ny=ny, nz=nz, dh=1.0, D_fast=1.0, D_slow=0.0, dt=2.0, radius=2, n_fd=0, weights="bf16",
+                   flags=EXTRA, v_far=100.0)
+    with fd.build_kernels(ap, fmask) as ctx:
+        c = c0.clone() * torch.from_numpy((fmask != 2).astype(np.float32)).cuda()
+        fd.far_init(ctx, c, 0.5)
+        fd.absorb_run(ctx, c, 3, 0.01, 0.05, 1.0, 1e-5)
+        fd.absorb_run(ctx, c, 2, 0.0, 0.05, 1.0, 1e-5)
     # virtual ranks
     sl = fd.slabs(shape[0], 3)
     ctxs = [fd.build_kernels(params(shape, 3, 20, v_far=100.0), fmask, rank=r, world=3, z_begin=a, z_end=b, device=0)

@@ -1707,7 +1707,11 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     ab.cLeq = (float)ap->c_L_eq;
     ab.n_solid = c->n_solid;
     fdirw_status st;
-    if (!c->alpha && (st = alloc((void**)&c->alpha, g.state_elems * 4, "reaction scratch")) != FDIRW_OK) return st;
+    if (!c->alpha) {  // (zeroed once: the grouped apply loads whole neighbour groups, whose α it uses
+                      // only for interface liquid lanes — always written — so the rest is never read uninitialised)
+        if ((st = alloc((void**)&c->alpha, g.state_elems * 4, "reaction scratch")) != FDIRW_OK) return st;
+        CUDA_TRY(cudaMemsetAsync(c->alpha, 0, g.state_elems * 4, static_cast<cudaStream_t>(cuda_stream)));
+    }
     if (!c->kin_part && (st = alloc((void**)&c->kin_part, 4 * kAbsorbMaxBlocks * 8, "kinetics")) != FDIRW_OK) return st;
     if (n > c->kin_cap) {
         cudaFree(c->kin_rec);

@@ -739,7 +739,9 @@ extern "C" fdirw_status fdirw_coarse_build(const fdirw_params* p, const uint8_t*
     // accuracy (measured 1.8e-5 relative vs 2e-6 for the substeps).  The P_BC column
     // (inhomogeneous: its far faces see the Dirichlet value 1) runs in a chunk of its own.
     std::vector<float> cheb;
-    const int m = (p->flags & FDIRW_F_KGEN_DIRECT) || c->n_fd <= 2 * kCheb_pre || c->far
+    // (with a far field and fp16 / bf16 storage the recurrence too, FDIRW_COARSE_OPEN_LITERAL=1: literal)
+    const bool far_lit = c->far && (c->fmt == 0 || getenv("FDIRW_COARSE_OPEN_LITERAL"));
+    const int m = (p->flags & FDIRW_F_KGEN_DIRECT) || c->n_fd <= 2 * kCheb_pre || far_lit
                       ? 0 : cheb_plan(c->n_fd - kCheb_pre, lam, &cheb);
     c->fd_passes = m > 0 ? kCheb_pre + m : c->n_fd;
     const float mu2 = (float)(lam * 4.0 / (12.0 * lam));  // 2μ = 4λ/(1 − a), 1 − a = 12λ: 1/3

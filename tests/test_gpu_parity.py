@@ -790,11 +790,15 @@ def test_coarse_far_vs_oracle(fd, oracle_lib, fmt, b):
     np.testing.assert_array_equal(gg, g)
     assert np.abs(Bg - PBC).max() <= 2e-6 * PBC.max()                 # fp32 FD, as P (tolP)
     assert PBC.max() > 1e-3
-    np.testing.assert_allclose(sizes @ Pg, sizes @ P, rtol=2e-6)    # column masses (absorbing; fp32 FD)
+    # column masses (absorbing): the literal fp32 FD with fp32 storage; with fp16 / bf16 storage the
+    # open region's columns take the Chebyshev recurrence (reading A30), whose rounding is absolute
+    # on the source's scale — bounded at 5e-5 relative, ten times below fp16's half-ulp 2^-11
+    np.testing.assert_allclose(sizes @ Pg, sizes @ P, rtol=2e-6 if fmt == "fp32" else 5e-5)
     assert abs(K0g - K0) <= 1e-6 * K0
     tol = 1e-5 if fmt == "fp32" else 5e-3
     assert rel_l2(got[region == 1], ref[region == 1]) <= tol
-    assert abs(cf1 - hist[0]) <= 1e-6 * cf0 and abs(cf4 - hist[3]) <= 1e-6 * cf0
+    ctol = 1e-6 if fmt == "fp32" else 1e-5
+    assert abs(cf1 - hist[0]) <= ctol * cf0 and abs(cf4 - hist[3]) <= ctol * cf0, (cf1 - hist[0], cf4 - hist[3])
     np.testing.assert_array_equal(got[region != 1], c0[region != 1])
     bal = got[region == 1].astype(np.float64).sum() + cf4 * v_far
     assert abs(bal - K0g) <= 1e-9 * K0g

@@ -412,19 +412,66 @@ __global__ void __launch_bounds__(256) iface_scatter_kernel(float* __restrict__ 
     block_pair_sum(ks, kl, part);
 }
 
+// the single solid pass of the nf path: over the non-far groups, the solid lanes' c1 from the
+// liquid step's INPUT (its solid values: every solid row is the identity with D_slow = 0, so the
+// step's output would hold the same bits — except at the all-solid chunks whose copy the step
+// skipped), written into the step's OUTPUT, whose liquid values stay; per-block sums of the
+// resulting field per phase (solid_fd4_kernel's per-voxel arithmetic)
+__global__ void __launch_bounds__(256) solid_nf_kernel(const float* __restrict__ cin, float* __restrict__ cout,
+                                                       const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R,
+                                                       int nxp, int nyp, float lam, const int* __restrict__ list,
+                                                       int n_list, double* __restrict__ part)
+{
+    double ks = 0.0, kl = 0.0;
+    const int nxg = (nx + 3) >> 2;
+    const long dy = nxp, dz = (long)nxp * nyp;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_list; i += gridDim.x * blockDim.x) {
+        const int gi = list[i];
+        const int gx = gi % nxg, r = gi / nxg, y = r % ny, z = r / ny;
+        const long p = pidx(4 * gx, y, z, R, nxp, nyp);
+        const int rem = nx - 4 * gx;
+        float c[4], o[4];
+        uint8_t h[4];
+        ld_grp(cin, pp, p, c, h);
+        ld_a4(cout, p, o);  // liquid (and far) lanes keep the step's output
+        if (h[0] == 0 || h[1] == 0 || h[2] == 0 || h[3] == 0) {
+            Nb4 n;
+            ld_nb(cin, pp, p, dy, dz, c, h, n);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                if (h[l] != 0) continue;
+                float acc = c[l];
+#pragma unroll
+                for (int f = 0; f < 6; ++f)
+                    if (n.h[f][l] == 0) acc = fmaf(lam, n.v[f][l] - c[l], acc);
+                o[l] = acc;
+            }
+            st_grp(cout, p, o, rem);
+        }
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            if (l >= rem) break;
+            if (h[l] == 0) ks += (double)o[l];
+            else if (h[l] == 1) kl += (double)o[l];
+        }
+    }
+    block_pair_sum(ks, kl, part);
+}
+
 // interface flag per group: a solid lane with a liquid face neighbour or a liquid lane with a solid one
 __global__ void iface_flag_kernel(const uint8_t* __restrict__ pp, int nx, int ny, int nz, int R, int nxp, int nyp,
-                                  int* __restrict__ flag)
+                                  int* __restrict__ flag, int* __restrict__ nflag)
 {
     const int nxg = (nx + 3) >> 2, ng = nxg * ny * nz;
     const long dy = nxp, dz = (long)nxp * nyp;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
         const int gx = i % nxg, r = i / nxg, y = r % ny, z = r / ny;
         const long p = pidx(4 * gx, y, z, R, nxp, nyp);
-        int f = 0;
+        int f = 0, nf = 0;
         for (int l = 0; l < 4 && 4 * gx + l < nx; ++l) {
             const uint8_t h = pp[p + l];
             if (h > 1) continue;
+            nf = 1;
             const long q[6] = {p + l - 1, p + l + 1, p + l - dy, p + l + dy, p + l - dz, p + l + dz};
             for (int k = 0; k < 6; ++k) {
                 const uint8_t hq = pp[q[k]];
@@ -432,6 +479,7 @@ __global__ void iface_flag_kernel(const uint8_t* __restrict__ pp, int nx, int ny
             }
         }
         flag[i] = f;
+        nflag[i] = nf;
     }
 }
 __global__ void iface_compact_kernel(const int* __restrict__ flag, const int* __restrict__ pos, int ng,
@@ -492,40 +540,48 @@ cudaError_t build_iface_list(const uint8_t* pp, const Geometry& g, IfaceList* ou
 {
     const long ngl = (long)((g.nx + 3) / 4) * g.ny * g.nz;
     const int ng = (int)ngl;
-    int *flag = nullptr, *pos = nullptr;
+    int *flag = nullptr, *nflag = nullptr, *pos = nullptr;
     void* tmp = nullptr;
     size_t tb = 0;
     cudaError_t e = cudaMalloc(&flag, (size_t)(ng + 1) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&nflag, (size_t)(ng + 1) * 4);
     if (e == cudaSuccess) e = cudaMalloc(&pos, (size_t)(ng + 1) * 4);
     if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, (size_t)(ng + 1) * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(nflag, 0, (size_t)(ng + 1) * 4, s);
     if (e == cudaSuccess) {
-        iface_flag_kernel<<<gridn(ngl), 256, 0, s>>>(pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, flag);
+        iface_flag_kernel<<<gridn(ngl), 256, 0, s>>>(pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, flag, nflag);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, ng + 1, s);
     if (e == cudaSuccess) e = cudaMalloc(&tmp, tb);
-    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, ng + 1, s);
-    int n = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&n, pos + ng, 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) e = cudaMalloc(&out->list, (size_t)(n > 0 ? n : 1) * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&out->tmp, (size_t)(n > 0 ? n : 1) * 16);
-    if (e == cudaSuccess && n > 0) {
-        iface_compact_kernel<<<gridn(ngl), 256, 0, s>>>(flag, pos, ng, out->list);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    // one list per flag array: scan, read the count, compact
+    auto compact = [&](const int* f, int** list, long* n) {
+        int cnt = 0;
+        if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tb, f, pos, ng + 1, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&cnt, pos + ng, 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) e = cudaMalloc(list, (size_t)(cnt > 0 ? cnt : 1) * 4);
+        if (e == cudaSuccess && cnt > 0) {
+            iface_compact_kernel<<<gridn(ngl), 256, 0, s>>>(f, pos, ng, *list);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        *n = cnt;
+    };
+    compact(flag, &out->list, &out->n);
+    compact(nflag, &out->nf_list, &out->n_nf);
+    if (e == cudaSuccess) e = cudaMalloc(&out->tmp, (size_t)(out->n > 0 ? out->n : 1) * 16);
     cudaFree(flag);
+    cudaFree(nflag);
     cudaFree(pos);
     cudaFree(tmp);
     if (e != cudaSuccess) {
         cudaFree(out->list);
         cudaFree(out->tmp);
-        out->list = nullptr;
-        out->tmp = nullptr;
+        cudaFree(out->nf_list);
+        *out = IfaceList{};
         return e;
     }
-    out->n = n;
     return cudaSuccess;
 }
 
@@ -537,6 +593,26 @@ cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uin
     const bool scalar = getenv("FDIRW_ABSORB_SCALAR") != nullptr;  // (A/B switches, read per enqueue)
     const bool sweep = getenv("FDIRW_ABSORB_SWEEP") != nullptr;
     const long ng = (long)((g.nx + 3) / 4) * g.ny * g.nz;
+    if (ab.nf_path) {  // (chosen by the caller together with the step's skipped identity copy)
+        const int nn = (int)iface->n_nf, ni = (int)iface->n;
+        const unsigned nb1 = gridn(nn > 0 ? nn : 1);
+        solid_nf_kernel<<<nb1, 256, 0, s>>>(other, cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.lam_s,
+                                            iface->nf_list, nn, part);
+        const unsigned nb2 = gridn(ni > 0 ? ni : 1);
+        if (ni > 0) {
+            react_alpha4_kernel<<<gridn(ni), 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, ab.kdt,
+                                                          ab.cSeq, ab.cLeq, alpha, iface->list, ni);
+            react_apply4_kernel<true><<<gridn(ni), 256, 0, s>>>(cur, alpha, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp,
+                                                                ab.kdt, ab.cSeq, ab.cLeq, nullptr, nullptr,
+                                                                iface->list, ni, iface->tmp);
+            iface_scatter_kernel<<<nb2, 256, 0, s>>>(cur, pp, g.nx, g.ny, g.nz, g.R, g.nxp, g.nyp, iface->list, ni,
+                                                     iface->tmp, part + 2 * kAbsorbMaxBlocks);
+        }
+        kin_final_kernel<<<1, 256, 0, s>>>(part, (int)nb1, far_state, v_far, ab.n_solid, ab.cSeq, far, rec, ctr,
+                                           part + 2 * kAbsorbMaxBlocks, ni > 0 ? (int)nb2 : 0);
+        *result = cur;
+        return cudaGetLastError();
+    }
     if (!scalar && !sweep && iface && iface->list && ab.n_s > 0) {
         // the solid pass sweeps the grid (with the field's sums); α, the apply and its in-place
         // scatter visit only the interface groups; the result stays in the solid pass's buffer

@@ -400,6 +400,7 @@ static void free_ctx(fdirw_ctx* c)
     cudaFree(c->kin_part);
     cudaFree(c->iface.list);
     cudaFree(c->iface.tmp);
+    cudaFree(c->iface.nf_list);
     cudaFree(c->kin_rec);
     cudaFree(c->abs_ctr);
     if (c->graph_abs) cudaGraphExecDestroy(c->graph_abs);
@@ -956,8 +957,10 @@ struct PhaseEv {
 // eq7 = false (the N3 loop): skip the compacted path's Eq.7 sums and c_far update after the liquid
 // step — the loop's kinetics pass sets c_far from the whole step's totals (oracle/integrated.py
 // run(), component (4) after (1)-(3)), which overwrites it before any kernel reads it.
+// copy_ident = false (the N3 loop's nf path): skip the identity-chunk copy — the loop's solid pass
+// writes every solid voxel of the output from the input
 static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, long rs, cudaStream_t s,
-                                 int dst_parity = 1, PhaseEv* pe = nullptr, bool eq7 = true)
+                                 int dst_parity = 1, PhaseEv* pe = nullptr, bool eq7 = true, bool copy_ident = true)
 {
     const Geometry& g = c->g;
     PHASE(t0, s);
@@ -1013,7 +1016,7 @@ static fdirw_status enqueue_step(fdirw_ctx* c, float* src, float* out, long ps, 
         }
         if (c->compact) {  // N2 compacted: superpose the listed chunks, Eq.7 sums per global tile
             CUDA_TRY(superpose(c, src, out, ps, rs, 0, c->ut.nd_tiles, s));
-            if (c->n_ident)  // identity rows (impermeable solid): C_new = C_old
+            if (c->n_ident && copy_ident)  // identity rows (impermeable solid): C_new = C_old
                 CUDA_TRY(launch_copy_chunks(src, out, ps, rs, c->ident_list, c->n_ident, g, s));
             if (!eq7) return FDIRW_OK;
             if (ps == (long)g.plane_elems) CUDA_TRY(launch_tile_mass_padded(out, c->farmask, g, c->tile_buf + 1, s));
@@ -1722,6 +1725,13 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     if (n == 0) return FDIRW_OK;
     if (!c->abs_ctr && (st = alloc((void**)&c->abs_ctr, 4, "kinetics counter")) != FDIRW_OK) return st;
     if (!c->iface.list) CUDA_TRY(build_iface_list(c->phase_pp, g, &c->iface, s));
+    // the nf path (one solid pass over the non-far groups, reading the solid values from the
+    // liquid step's input, so the step skips its identity-chunk copy): Table 1's single solid pass
+    // with the product kernel (the §3.3 study modes round even the identity rows' products);
+    // FDIRW_ABSORB_SCALAR / FDIRW_ABSORB_SWEEP / FDIRW_ABSORB_FULL
+    // keep the sweeping forms for A/B
+    ab.nf_path = (ab.n_s == 1 && c->prec_mode == 0 && c->iface.nf_list && !getenv("FDIRW_ABSORB_SCALAR") &&
+                  !getenv("FDIRW_ABSORB_SWEEP") && !getenv("FDIRW_ABSORB_FULL")) ? 1 : 0;
     CUDA_TRY(launch_pack(c_dev, c->cpad[0], g, s, c->farmask));
     CUDA_TRY(cudaMemsetAsync(c->abs_ctr, 0, 4, s));
     const size_t ioff = (size_t)g.R * g.plane_elems + (size_t)g.R * g.nxp + kPadX;
@@ -1730,7 +1740,8 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     auto macro = [&](float* in, cudaStream_t ss, float** res) -> fdirw_status {
         float* out = in == c->cpad[0] ? c->cpad[1] : c->cpad[0];
         fdirw_status sst = enqueue_step(c, in, out + ioff, (long)g.plane_elems, g.nxp, ss, 1, nullptr,
-                                        getenv("FDIRW_ABSORB_EQ7_TWICE") != nullptr);  // (A/B)
+                                        getenv("FDIRW_ABSORB_EQ7_TWICE") != nullptr,  // (A/B)
+                                        ab.nf_path == 0);
         if (sst != FDIRW_OK) return sst;
         CUDA_TRY(launch_absorb_tail(out, in, c->alpha, c->phase_pp, g, ab, c->kin_part, c->far_state, c->v_far,
                                     c->far ? 1 : 0, c->kin_rec, ss, res, c->abs_ctr, &c->iface));
@@ -1738,7 +1749,8 @@ extern "C" fdirw_status fdirw_absorb_run(fdirw_ctx* c, const fdirw_absorb_params
     };
     const bool same = c->graph_abs && c->abs_rec_key == c->kin_rec && c->abs_key.n_s == ab.n_s &&
                       c->abs_key.lam_s == ab.lam_s && c->abs_key.kdt == ab.kdt && c->abs_key.cSeq == ab.cSeq &&
-                      c->abs_key.cLeq == ab.cLeq && c->abs_key.n_solid == ab.n_solid;
+                      c->abs_key.cLeq == ab.cLeq && c->abs_key.n_solid == ab.n_solid &&
+                      c->abs_key.nf_path == ab.nf_path;
     if (n >= 2 && !same) {  // capture two macro steps: they return the field to cpad[0]
         if (c->graph_abs) cudaGraphExecDestroy(c->graph_abs);
         c->graph_abs = nullptr;

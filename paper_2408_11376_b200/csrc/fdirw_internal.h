@@ -225,6 +225,10 @@ struct AbsorbArgs {
     float kdt;        // k·Δt (Eq.4)
     float cSeq, cLeq;
     double n_solid;   // N_S (for c̄_S)
+    // 1: the liquid step skipped the identity-chunk copy (its output holds stale values at the
+    // all-solid chunks); the tail's single solid pass reads the solid values from the step's
+    // input and visits only the non-far groups (n_s == 1, the interface lists built)
+    int nf_path = 0;
 };
 cudaError_t launch_phase_pad(const uint8_t* mask, const Geometry& g, uint8_t* pp, cudaStream_t s);
 // the loop's interface groups (absorb.cu): groups of 4 x-voxels holding a solid voxel with a liquid
@@ -234,6 +238,8 @@ struct IfaceList {
     int* list = nullptr;
     long n = 0;
     float4* tmp = nullptr;
+    int* nf_list = nullptr;  // groups holding any solid or near-liquid voxel (ascending)
+    long n_nf = 0;
 };
 cudaError_t build_iface_list(const uint8_t* pp, const Geometry& g, IfaceList* out, cudaStream_t s);
 cudaError_t launch_absorb_tail(float* cur, float* other, float* alpha, const uint8_t* pp, const Geometry& g,

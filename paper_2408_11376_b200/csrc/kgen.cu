@@ -302,8 +302,9 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
         // only), which removes the divergent branches; measured faster there (cfg5 R8 967 →
         // 908 ms) and slower at R5 (140 → 155 ms), so R ≤ 5 keep the guard.
         const bool act = R >= 6 || col;
-        const bool cheb = a.cheb_m && (!open || a.cheb_open);
-        const int n_direct = cheb ? a.cheb_pre : a.n_fd;
+        const bool iso = !F64 && isolated_source(ph, ftab, KC, L, LL);  // kernel δ_s: no pass
+        const bool cheb = !iso && a.cheb_m && (!open || a.cheb_open);
+        const int n_direct = iso ? 0 : cheb ? a.cheb_pre : a.n_fd;
         for (int k = 0; k < n_direct; ++k) {
             float* b = buf + (k & 1) * (NT * Lp);
             if (act) store_col(b, c);

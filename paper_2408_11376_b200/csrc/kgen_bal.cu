@@ -268,8 +268,9 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
         auto above = [](int sd, int i) { return G::Z0(sd) + i < L - 1; };
 
         const bool act = real;
-        const bool cheb = a.cheb_m && (!open || (CO && a.cheb_open));
-        const int n_direct = cheb ? a.cheb_pre : a.n_fd;
+        const bool iso = isolated_source(ph, ftab, KC, L, LL);  // kernel δ_s: no pass
+        const bool cheb = !iso && a.cheb_m && (!open || (CO && a.cheb_open));
+        const int n_direct = iso ? 0 : cheb ? a.cheb_pre : a.n_fd;
         unsigned ps = 0;
         // ---- literal substeps, flux form in the column kernel's order (z faces first for R ≤ 5) ----
         for (int k = 0; k < n_direct; ++k, ++ps) {

@@ -128,4 +128,18 @@ __device__ __forceinline__ void build_face_tables(float* tab, float lff, float l
     }
 }
 
+// An isolated source: every face of the window's centre cell has face number 0 (a slow-phase
+// voxel with D_slow = 0, the N3 loop's impermeable solid).  Its kernel is exactly δ_s — each literal
+// substep leaves it unchanged — so kgen runs no pass for it.  (The Chebyshev recurrence would give
+// Σ fp32(c_k)·δ = (1 − ~6e-8)·δ: renormalisation hides that in a closed window, but an open (N2)
+// window keeps its kernel's own mass, and that would make the identity row of a solid voxel
+// leak.)  T: the λ face table (build_face_tables set 0); faces are ≥ 0.
+__device__ __forceinline__ bool isolated_source(const unsigned char* ph, const float* T, int KC, int L, int LL)
+{
+    const unsigned pc = ph[KC];
+    const float f = T[(pc << 2) | ph[KC - 1]] + T[(pc << 2) | ph[KC + 1]] + T[(pc << 2) | ph[KC - L]] +
+                    T[(pc << 2) | ph[KC + L]] + T[16 + ((ph[KC - LL] << 2) | pc)] + T[16 + ((pc << 2) | ph[KC + LL])];
+    return f == 0.f;
+}
+
 }  // namespace fdirw

@@ -158,11 +158,13 @@ def test_absorb_loop_many_tail_blocks(fd, oracle_lib):
     assert abs(tot - M0) / M0 <= 1e-6
 
 
-@pytest.mark.parametrize("D_S", [fi.D_SLOW_SI, 0.0])
-def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S):
-    """The tail over groups of 4 x-voxels — by default the solid pass sweeps the grid and α / the
-    apply / its in-place scatter visit only the interface groups; FDIRW_ABSORB_SWEEP=1 sweeps all
-    three — against the per-voxel sweeps (FDIRW_ABSORB_SCALAR=1): every voxel's
+@pytest.mark.parametrize("D_S,weights", [(fi.D_SLOW_SI, "fp32"), (0.0, "fp32"), (fi.D_SLOW_SI, "bf16")])
+def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S, weights):
+    """The tail over groups of 4 x-voxels — by default (one solid pass) the liquid step skips its
+    identity-chunk copy and the solid pass visits only the non-far groups, reading the solid values
+    from the step's input; α / the apply / its in-place scatter visit only the interface groups
+    (FDIRW_ABSORB_FULL=1: the solid pass sweeps the grid instead; FDIRW_ABSORB_SWEEP=1 sweeps all
+    three) — against the per-voxel sweeps (FDIRW_ABSORB_SCALAR=1): every voxel's
     value is the same expression in the same face order, so one macro step's field is bitwise
     equal; the kinetics partials are summed per thread-group (another fixed order), so Q_S, Q_L,
     c_far agree to rounding, and after that c_far feeds the next step's p_BC·c_far term.  nx = 37
@@ -175,15 +177,13 @@ def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S):
     c0 = np.where(m == 1, T["c_L0"], np.where(m == 0, T["c_S0"], 0.0)).astype(np.float32)
     nz, ny, nx = shape
     p = fd.Params(nx=nx, ny=ny, nz=nz, dh=T["dh"], D_fast=fi.D_FAST_SI, D_slow=0.0, dt=T["dt"], radius=2,
-                  weights="fp32", v_far=2e4)
+                  weights=weights, v_far=2e4)
     out = {}
-    for form in ("default", "sweep", "scalar"):
-        monkeypatch.delenv("FDIRW_ABSORB_SCALAR", raising=False)
-        monkeypatch.delenv("FDIRW_ABSORB_SWEEP", raising=False)
-        if form == "scalar":
-            monkeypatch.setenv("FDIRW_ABSORB_SCALAR", "1")
-        elif form == "sweep":
-            monkeypatch.setenv("FDIRW_ABSORB_SWEEP", "1")
+    for form in ("default", "full", "sweep", "scalar"):
+        for ev in ("FDIRW_ABSORB_SCALAR", "FDIRW_ABSORB_SWEEP", "FDIRW_ABSORB_FULL"):
+            monkeypatch.delenv(ev, raising=False)
+        if form != "default":
+            monkeypatch.setenv("FDIRW_ABSORB_" + form.upper(), "1")
         ctx = fd.build_kernels(p, m)
         try:
             c = torch.from_numpy(c0).cuda()
@@ -195,9 +195,32 @@ def test_absorb_grouped_tail_bitwise(fd, monkeypatch, D_S):
         finally:
             fd.destroy(ctx)
     b = out["scalar"]
-    for a in (out["default"], out["sweep"]):
+    for a in (out["default"], out["full"], out["sweep"]):
         assert np.count_nonzero(a[0] != c0) > 0  # the step moved the field
         np.testing.assert_array_equal(a[0], b[0])
         np.testing.assert_allclose(a[1], b[1], rtol=1e-12)
         np.testing.assert_allclose(a[2], b[2], rtol=1e-6, atol=1e-12)
         np.testing.assert_allclose(a[3], b[3], rtol=1e-9)
+
+
+def test_isolated_sources_exact_delta(fd):
+    """With D_slow = 0 a solid voxel's every face number is 0: its kernel is exactly δ (kgen runs no
+    pass for it — the Chebyshev recurrence would give Σ fp32(c_k)·δ, and an open window, which is
+    not renormalised, would keep that as its mass: the identity rows of the N3 loop's liquid step
+    would leak).  bf16 storage (open windows by the recurrence), R = 5 and 8, with a reservoir."""
+    for R, shape in ((5, (22, 21, 23)), (8, (24, 23, 25))):
+        m = fi.with_far_field(fi.porous_particle(shape, 7, pore_r=(1.0, 2.0), porosity=0.3, seed=5), 7, 3.0)
+        nz, ny, nx = shape
+        T = fi.TABLE1
+        p = fd.Params(nx=nx, ny=ny, nz=nz, dh=T["dh"], D_fast=fi.D_FAST_SI, D_slow=0.0, dt=T["dt"], radius=R,
+                      weights="bf16", v_far=2e4)
+        ctx = fd.build_kernels(p, m)
+        try:
+            W = fd.export_kernels(ctx, (0, nx, 0, ny, 0, nz)).reshape(-1, (2 * R + 1) ** 3)
+        finally:
+            fd.destroy(ctx)
+        sol = W[m.reshape(-1) == 0]
+        c = sol.shape[1] // 2
+        assert len(sol) > 100
+        np.testing.assert_array_equal(sol[:, c], 1.0)
+        assert np.count_nonzero(np.delete(sol, c, axis=1)) == 0

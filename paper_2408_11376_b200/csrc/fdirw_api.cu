@@ -603,6 +603,9 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
             const double sc = 4.0 / (12.0 * lmax);  // 2μ = 4λ/(1 − a), 1 − a = 12 λ_max
             ka.cheb_m = m;
             ka.cheb_pre = kCheb_pre;
+            double p1 = 0.0;  // p(1) of the fp32 coefficients the passes use
+            for (float ck : cheb) p1 += (double)ck;
+            ka.cheb_scale = (float)(1.0 / p1);
             ka.cheb_c = c->cheb_d;
             ka.mu2_ff = (float)(d.lam_ff * sc);
             ka.mu2_fs = (float)(d.lam_fs * sc);

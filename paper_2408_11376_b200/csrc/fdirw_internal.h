@@ -79,6 +79,7 @@ struct KgenArgs {
     // Chebyshev evaluation of A^{n_fd − cheb_pre} (kgen.cu, reading A30): degree cheb_m (0 =
     // direct substeps), coefficients cheb_c[0..cheb_m] (device, fp32), face numbers 2μ = 4λ/(1 − a)
     int cheb_m, cheb_pre;  // Chebyshev degree (0 = direct) after cheb_pre direct substeps
+    float cheb_scale = 1.f;  // 1 / Σ_k fp32(c_k) in fp64: an open window's result is scaled by it (A30)
     int cheb_open = 0;     // windows touching the N2 reservoir also take the recurrence (reduced-
                            // precision storage only, reading A30); else they run the literal substeps
     const float* cheb_c;

@@ -404,6 +404,11 @@ __global__ void __launch_bounds__(KgenShape<R, F64>::NT, F64 ? 1 : KgenShape<R, 
             // noise of tiny entries at 0 can only move them closer to it
 #pragma unroll
             for (int z = 0; z < Lp; ++z) c[z] = z < L ? fmaxf(acc[z < L ? z : 0], 0.f) : 0.f;
+            // an open window keeps its own mass (no renormalisation): divide out p(1) = Σ fp32(c_k)
+            // so a conserved mode (a pore the reservoir cannot reach) keeps it exactly (A30)
+            if (open)
+#pragma unroll
+                for (int z = 0; z < L; ++z) c[z] *= a.cheb_scale;
         }
         }  // fp32 substeps
 

@@ -416,6 +416,13 @@ __device__ __forceinline__ void bal_body(const KgenArgs& a)
             for (int sd = 0; sd < 2; ++sd)
 #pragma unroll
                 for (int i = 0; i < 6; ++i) c[sd][i] = fmaxf(acc[sd][i], 0.f);
+            // an open window keeps its own mass (no renormalisation): divide out p(1) = Σ fp32(c_k)
+            // so a conserved mode (a pore the reservoir cannot reach) keeps it exactly (A30)
+            if (open)
+#pragma unroll
+                for (int sd = 0; sd < 2; ++sd)
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) c[sd][i] *= a.cheb_scale;
         }
 
         // ---- epilogue (a4): as kgen.cu's, per owned cell ----

@@ -36,5 +36,5 @@ for fmt, R, shape in (("bf16", 5, (14, 13, 15)), ("fp16", 3, (14, 13, 15)), ("bf
             fd.destroy(ctx)
         dM = np.abs(W.sum(1) - Mo)[ow]
         rel = dM / Mo[ow]
-        print("%s R%d %-10s open windows %d: |dM| max %.2e median %.2e; rel max %.2e (M min %.2e)"
-              % (fmt, R, form, ow.sum(), dM.max(), np.median(dM), rel.max(), Mo[ow].min()))
+        print("%s R%d %-10s open windows %d: |dM| max %.2e median %.2e; rel max %.2e median %.2e (M min %.2e)"
+              % (fmt, R, form, ow.sum(), dM.max(), np.median(dM), rel.max(), np.median(rel), Mo[ow].min()))

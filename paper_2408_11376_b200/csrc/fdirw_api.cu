@@ -619,7 +619,7 @@ extern "C" fdirw_status fdirw_build_kernels(const fdirw_params* params, const ui
     // kept mass its fp32 accuracy); fp16 / bf16 / MX8 storage rounds every weight at 2^-11 … 2^-8
     // relative, far above that, so those windows take the recurrence too (FDIRW_KGEN_OPEN_LITERAL=1:
     // literal for A/B)
-    ka.cheb_open = (c->fmt != FDIRW_W_FP32 && !getenv("FDIRW_KGEN_OPEN_LITERAL")) ? 1 : 0;
+    ka.cheb_open = (c->fmt != FDIRW_W_FP32 && params->v_far > 0 && !getenv("FDIRW_KGEN_OPEN_LITERAL")) ? 1 : 0;
     ka.mass_fix = (params->flags & FDIRW_F_NO_MASS_FIX) ? 0 : 1;
     ka.columns = (params->flags & FDIRW_F_KGEN_COLUMNS) ? 1 : 0;
     ka.nxq = g.nxq; ka.tile = g.tile; ka.tpp = g.tpp; ka.K = g.K;

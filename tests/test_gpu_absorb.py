@@ -224,3 +224,48 @@ def test_isolated_sources_exact_delta(fd):
         assert len(sol) > 100
         np.testing.assert_array_equal(sol[:, c], 1.0)
         assert np.count_nonzero(np.delete(sol, c, axis=1)) == 0
+
+
+def test_absorb_cfg3o_sampled_vs_oracle(fd, oracle_lib):
+    """One macro step of the integrated loop at full size (cfg3o: the open R50 model, Table 1 SI
+    values, bf16 weights, the default tail — interface lists, nf path), against the oracle's
+    components in the paper's order on sampled boxes: the liquid FDiRW step with p_BC·c_far
+    (oracle.farfield.step_box_far on the box grown by 3 voxels), then oracle.integrated.solid_fd
+    and react on that grown box; compared on the box interior (3 voxels in, past the stencils'
+    reach of the grown box's edge), within the reduced-precision bar.  Boxes at the particle
+    surface (solid, near-field liquid) and inside the particle (solid and pores)."""
+    import torch
+    from oracle import farfield as ff
+    from oracle import integrated as ig
+
+    cfg = fi.config("cfg3o")
+    mask = cfg.mask()
+    nz, ny, nx = cfg.shape
+    T = fi.TABLE1
+    ab = ig.Absorb(D_L=fi.D_FAST_SI, D_S=fi.D_SLOW_SI, dh=T["dh"], dt=T["dt"], k=0.05, c_S_eq=1.0, c_L_eq=1e-5,
+                   V_far=cfg.v_far, R=cfg.R)
+    c0 = np.where(mask == 1, T["c_L0"], np.where(mask == 0, T["c_S0"], 0.0))
+    p = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=0.0, dt=cfg.dt, radius=cfg.R,
+                  n_fd=cfg.n_fd, weights="bf16", v_far=cfg.v_far)
+    ctx = fd.build_kernels(p, mask)
+    try:
+        c = torch.from_numpy(c0.astype(np.float32)).cuda()
+        fd.far_init(ctx, c, cfg.c_far0)
+        fd.absorb_run(ctx, c, 1, ab.D_S, ab.k, ab.c_S_eq, ab.c_L_eq)
+        got = c.cpu().numpy().astype(np.float64)
+    finally:
+        fd.destroy(ctx)
+    pb = ig.liquid_problem(mask, ab)
+    g = 3
+    for box in [(107, 111, 58, 62, 58, 62), (76, 80, 58, 62, 58, 62)]:  # particle surface; pores inside
+        gb = (box[0] - g, box[1] + g, box[2] - g, box[3] + g, box[4] - g, box[5] + g)
+        msub = mask[gb[4]:gb[5], gb[2]:gb[3], gb[0]:gb[1]]
+        assert (msub == 1).any() and (msub == 0).any(), box
+        liq = ff.step_box_far(pb, c0 * (mask != 2), cfg.c_far0, gb, fmt=None)
+        ref = ig.react(ig.solid_fd(liq, msub, ab), msub, ab)
+        ref = ref[g:-g, g:-g, g:-g]
+        sub = got[box[4]:box[5], box[2]:box[3], box[0]:box[1]]
+        assert rel_l2(sub, ref) <= 5e-3, (box, rel_l2(sub, ref))
+        # and the absorption moved mass at the interface (the comparison is not the identity)
+        moved = rel_l2(c0[box[4]:box[5], box[2]:box[3], box[0]:box[1]], ref)
+        assert moved > 10 * rel_l2(sub, ref), (box, moved, rel_l2(sub, ref))

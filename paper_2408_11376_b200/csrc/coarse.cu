@@ -375,12 +375,22 @@ __device__ __forceinline__ float dot16(const uint4& u, const float (&cv)[16 / si
 // partition (q ≡ lane mod 32, increasing q) and the FMA order are fixed.
 constexpr int GEMV_RW = 4;
 
-template <typename WT>
+// SMC: C (ldp floats, zero past N) staged in shared memory once per block, so its reads leave the
+// L1/TEX pipe to the P̃ stream (identical values and order: identical bits).  Measured (round 2,
+// bf16, R50 near field): 22.7 → 20.6 µs per coarse step; with C in smem (RW, GU) = (4, 4) stays
+// best — (2, 4) 24.0, (2, 8) 22.7, (4, 2) 22.7, (4, 8) 26.2, (8, 2) 26.8, (8, 4) 38.3 µs.
+template <typename WT, bool SMC = false>
 __global__ void __launch_bounds__(512) k_gemv(const WT* __restrict__ P, const float* __restrict__ Pdiag,
                                               const float* __restrict__ C, long N, long ldp,
                                               float* __restrict__ Cout, const float* __restrict__ Pbc,
                                               const double* __restrict__ far_state)
 {
+    extern __shared__ __align__(16) float Csm[];
+    if constexpr (SMC) {
+        for (long i = threadIdx.x; i < ldp / 4; i += blockDim.x)
+            reinterpret_cast<float4*>(Csm)[i] = __ldg(reinterpret_cast<const float4*>(C) + i);
+        __syncthreads();
+    }
     constexpr int V = 16 / sizeof(WT);  // elements per 128-bit load
     constexpr int GU = 4;
     const int lane = threadIdx.x & 31;
@@ -412,7 +422,8 @@ __global__ void __launch_bounds__(512) k_gemv(const WT* __restrict__ P, const fl
                     float cv[V];
 #pragma unroll
                     for (int h = 0; h < V / 4; ++h) {
-                        const float4 c4 = __ldg(reinterpret_cast<const float4*>(C + (long)(q0 + 32 * k) * V) + h);
+                        const float4 c4 = SMC ? reinterpret_cast<const float4*>(Csm + (long)(q0 + 32 * k) * V)[h]
+                                              : __ldg(reinterpret_cast<const float4*>(C + (long)(q0 + 32 * k) * V) + h);
                         cv[4 * h] = c4.x; cv[4 * h + 1] = c4.y; cv[4 * h + 2] = c4.z; cv[4 * h + 3] = c4.w;
                     }
 #pragma unroll
@@ -858,14 +869,29 @@ static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
         else
             k_gemv_bulk<__nv_bfloat16><<<g, bl, c->bulk_smem, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N,
                                                                   c->ldp, c->C2, c->Pbc, c->far_state, c->bulk_m);
-    } else if (c->fmt == 0)
-        k_gemv<float><<<gemv_grid(c), gemv_block(c), 0, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc, c->far_state);
-    else if (c->fmt == 1)
-        k_gemv<__half><<<gemv_grid(c), gemv_block(c), 0, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
-                                                     c->Pbc, c->far_state);
-    else
-        k_gemv<__nv_bfloat16><<<gemv_grid(c), gemv_block(c), 0, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N, c->ldp,
-                                                             c->C2, c->Pbc, c->far_state);
+    } else {
+        // C in shared memory when it fits (FDIRW_COARSE_GEMV_L1=1: the L1 form, A/B)
+        static const bool l1 = getenv("FDIRW_COARSE_GEMV_L1") != nullptr;
+        const size_t csm = (size_t)c->ldp * 4;
+        const bool smc = !l1 && csm <= 96 * 1024;
+        auto go = [&](auto wt) -> cudaError_t {
+            using WT = decltype(wt);
+            const WT* P = (const WT*)c->P;
+            if (smc) {
+                cudaError_t e = cudaFuncSetAttribute(k_gemv<WT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)csm);
+                if (e != cudaSuccess) return e;
+                k_gemv<WT, true><<<gemv_grid(c), gemv_block(c), csm, s>>>(P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc,
+                                                                         c->far_state);
+            } else {
+                k_gemv<WT, false><<<gemv_grid(c), gemv_block(c), 0, s>>>(P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc,
+                                                                          c->far_state);
+            }
+            return cudaGetLastError();
+        };
+        cudaError_t e = c->fmt == 0 ? go(float{}) : c->fmt == 1 ? go(__half{}) : go(__nv_bfloat16{});
+        if (e != cudaSuccess) return e;
+    }
     k_remap<<<gridn(c->NL) + (c->far ? 1 : 0), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf, c->sizes, N,
                                                            c->far ? c->far_state : nullptr, c->v_far);
     return cudaGetLastError();

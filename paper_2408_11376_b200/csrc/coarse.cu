@@ -379,11 +379,16 @@ constexpr int GEMV_RW = 4;
 // L1/TEX pipe to the P̃ stream (identical values and order: identical bits).  Measured (round 2,
 // bf16, R50 near field): 22.7 → 20.6 µs per coarse step; with C in smem (RW, GU) = (4, 4) stays
 // best — (2, 4) 24.0, (2, 8) 22.7, (4, 2) 22.7, (4, 8) 26.2, (8, 2) 26.8, (8, 4) 38.3 µs.
+// cfine (closed domains): the remap fused into the epilogue — the warp that computed C'_I stores it
+// into every fine voxel of group I (lane 0's value, broadcast), so no k_remap launch follows
 template <typename WT, bool SMC = false>
 __global__ void __launch_bounds__(512) k_gemv(const WT* __restrict__ P, const float* __restrict__ Pdiag,
                                               const float* __restrict__ C, long N, long ldp,
                                               float* __restrict__ Cout, const float* __restrict__ Pbc,
-                                              const double* __restrict__ far_state)
+                                              const double* __restrict__ far_state,
+                                              const int* __restrict__ grp_ptr = nullptr,
+                                              const int* __restrict__ grp_vox = nullptr,
+                                              float* __restrict__ cfine = nullptr)
 {
     extern __shared__ __align__(16) float Csm[];
     if constexpr (SMC) {
@@ -440,6 +445,12 @@ __global__ void __launch_bounds__(512) k_gemv(const WT* __restrict__ P, const fl
                 float v = fmaf(Pdiag[I], C[I], acc[r]);
                 if (Pbc) v = fmaf(Pbc[I], (float)far_state[0], v);  // Eq.14 boundary term
                 Cout[I] = v;
+                acc[r] = v;
+            }
+            if (cfine && r < nrow) {
+                const float v = __shfl_sync(0xffffffffu, acc[r], 0);
+                const long I = I0 + r;
+                for (int k = grp_ptr[I] + lane; k < grp_ptr[I + 1]; k += 32) cfine[grp_vox[k]] = v;
             }
         }
     }
@@ -877,23 +888,26 @@ static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
         auto go = [&](auto wt) -> cudaError_t {
             using WT = decltype(wt);
             const WT* P = (const WT*)c->P;
+            float* fine = c->far ? nullptr : cbuf;  // closed: remap fused (with a far field k_remap's
+                                                     // first block also does Eq.7 over all of C')
             if (smc) {
                 cudaError_t e = cudaFuncSetAttribute(k_gemv<WT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)csm);
                 if (e != cudaSuccess) return e;
                 k_gemv<WT, true><<<gemv_grid(c), gemv_block(c), csm, s>>>(P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc,
-                                                                         c->far_state);
+                                                                         c->far_state, c->grp_ptr, c->grp_vox, fine);
             } else {
                 k_gemv<WT, false><<<gemv_grid(c), gemv_block(c), 0, s>>>(P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc,
-                                                                          c->far_state);
+                                                                          c->far_state, c->grp_ptr, c->grp_vox, fine);
             }
             return cudaGetLastError();
         };
         cudaError_t e = c->fmt == 0 ? go(float{}) : c->fmt == 1 ? go(__half{}) : go(__nv_bfloat16{});
         if (e != cudaSuccess) return e;
     }
-    k_remap<<<gridn(c->NL) + (c->far ? 1 : 0), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf, c->sizes, N,
-                                                           c->far ? c->far_state : nullptr, c->v_far);
+    if (c->far || c->bulk_m > 0)  // (the bulk GEMV form keeps the separate remap)
+        k_remap<<<gridn(c->NL) + (c->far ? 1 : 0), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf, c->sizes, N,
+                                                               c->far ? c->far_state : nullptr, c->v_far);
     return cudaGetLastError();
 }
 

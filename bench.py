@@ -450,16 +450,18 @@ def _kgen_line(t_kgen, cells_algo, info, cfg, world):
                                          "shared-memory ceiling (%.2e cell-passes/s)" % (smem_peak / 20.0)}}
 
 
-def _coarse_roofline(info, ms):
-    """Whole coarse step against HBM: algorithmic bytes = stored P̃ (+diag, P_BC) once, plus the
-    Ω_L field read by the map and written by the remap (8 B per Ω_L voxel).  P̃ fits in L2 and
-    stays there across steps (evict_last), so frac > 1 is possible; it is the step's figure,
-    not one kernel's."""
+def _coarse_roofline(info, ms, steps):
+    """Whole coarse step against HBM: algorithmic bytes = stored P̃ (+diag, P_BC) and the group
+    vector in and out (12 B per group) per step, plus the Ω_L field read by the one map and written
+    by the one remap of the run (8 B per Ω_L voxel, over the run's steps: fdirw_coarse_run keeps the
+    state in group values between steps).  P̃ fits in L2 and stays there across steps
+    (evict_last), so frac > 1 is possible; it is the step's figure, not one kernel's."""
     peak, src = _hbm_peak()
-    algo = info["p_bytes"] + 8 * info["n_region"]
+    algo = info["p_bytes"] + 12 * info["n_groups"] + 8 * info["n_region"] / max(steps, 1)
     ach = algo / (ms * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
-            "kernel": "whole coarse step (k_map + k_gemv + k_remap)", "bytes_per_step": algo, "peak_source": src}
+            "kernel": "coarse step in group space (k_gemv, + Eq.7 with a far field); one map and one remap per run",
+            "bytes_per_step": algo, "peak_source": src}
 
 
 def run_coarse(args):
@@ -512,7 +514,7 @@ def run_coarse(args):
             "paper_context": {"R50_N_L": 329404, "R50_N": 2515, "V100_fdirw_s_per_1000_steps": 0.7,
                               "source": "P:181 Fig.7e, P:262-263 Table 3"},
             "flops_per_step": info["flops_per_step"],
-            "roofline": _coarse_roofline(info, ms),
+            "roofline": _coarse_roofline(info, ms, args.steps),
             "build_seconds": t_build, "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
             **extra}
     fd.coarse_destroy(ctx)

@@ -58,6 +58,7 @@ struct fdirw_coarse {
     float* C2 = nullptr;      // [ldp]
     cudaStream_t cap = nullptr;
     cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph2 = nullptr;  // fdirw_coarse_run: two coarse-space steps C → C2 → C
     float* graph_c = nullptr;
     // N2
     bool far = false;
@@ -609,6 +610,7 @@ static void coarse_free(fdirw_coarse* c)
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->graph2) cudaGraphExecDestroy(c->graph2);
     if (c->cap) cudaStreamDestroy(c->cap);
     cudaFree(c->group_of); cudaFree(c->rows); cudaFree(c->grp_ptr); cudaFree(c->grp_vox); cudaFree(c->sizes);
     cudaFree(c->P); cudaFree(c->Pdiag); cudaFree(c->C); cudaFree(c->C2); cudaFree(c->Pbc); cudaFree(c->far_state);
@@ -865,47 +867,56 @@ static unsigned gemv_block(const fdirw_coarse* c)
     return (unsigned)(32 * w);
 }
 
+// One coarse GEMV C' = P̃·Cin + diag∘Cin (+ P_BC·c_far): the bulk form, or the register form with
+// C staged in shared memory; fine ≠ null (closed domain) fuses the remap of C' into cbuf.
+static cudaError_t coarse_gemv(fdirw_coarse* c, const float* Cin, float* Cout, float* fine, cudaStream_t s)
+{
+    const long N = c->N;
+    if (c->bulk_m > 0) {
+        const dim3 g((unsigned)(N < c->n_sm ? N : c->n_sm)), bl((GEMV_NW + 1) * 32);
+        if (c->fmt == 0)
+            k_gemv_bulk<float><<<g, bl, c->bulk_smem, s>>>((const float*)c->P, c->Pdiag, Cin, N, c->ldp, Cout,
+                                                          c->Pbc, c->far_state, c->bulk_m);
+        else if (c->fmt == 1)
+            k_gemv_bulk<__half><<<g, bl, c->bulk_smem, s>>>((const __half*)c->P, c->Pdiag, Cin, N, c->ldp, Cout,
+                                                           c->Pbc, c->far_state, c->bulk_m);
+        else
+            k_gemv_bulk<__nv_bfloat16><<<g, bl, c->bulk_smem, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, Cin, N,
+                                                                  c->ldp, Cout, c->Pbc, c->far_state, c->bulk_m);
+        return cudaGetLastError();
+    }
+    // C in shared memory when it fits (FDIRW_COARSE_GEMV_L1=1: the L1 form, A/B)
+    static const bool l1 = getenv("FDIRW_COARSE_GEMV_L1") != nullptr;
+    const size_t csm = (size_t)c->ldp * 4;
+    const bool smc = !l1 && csm <= 96 * 1024;
+    auto go = [&](auto wt) -> cudaError_t {
+        using WT = decltype(wt);
+        const WT* P = (const WT*)c->P;
+        if (smc) {
+            cudaError_t e = cudaFuncSetAttribute(k_gemv<WT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)csm);
+            if (e != cudaSuccess) return e;
+            k_gemv<WT, true><<<gemv_grid(c), gemv_block(c), csm, s>>>(P, c->Pdiag, Cin, N, c->ldp, Cout, c->Pbc,
+                                                                     c->far_state, c->grp_ptr, c->grp_vox, fine);
+        } else {
+            k_gemv<WT, false><<<gemv_grid(c), gemv_block(c), 0, s>>>(P, c->Pdiag, Cin, N, c->ldp, Cout, c->Pbc,
+                                                                      c->far_state, c->grp_ptr, c->grp_vox, fine);
+        }
+        return cudaGetLastError();
+    };
+    return c->fmt == 0 ? go(float{}) : c->fmt == 1 ? go(__half{}) : go(__nv_bfloat16{});
+}
+
+// One whole coarse step on the fine field cbuf: map, GEMV, remap (+ Eq.7 with a far
+// field, in the remap's first block).  Closed domains with the register GEMV fuse the remap.
 static cudaError_t coarse_enqueue(fdirw_coarse* c, float* cbuf, cudaStream_t s)
 {
     const long N = c->N;
     k_map<<<gridn(N * 32), 256, 0, s>>>(cbuf, c->grp_ptr, c->grp_vox, N, c->C);
-    if (c->bulk_m > 0) {
-        const dim3 g((unsigned)(N < c->n_sm ? N : c->n_sm)), bl((GEMV_NW + 1) * 32);
-        if (c->fmt == 0)
-            k_gemv_bulk<float><<<g, bl, c->bulk_smem, s>>>((const float*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
-                                                          c->Pbc, c->far_state, c->bulk_m);
-        else if (c->fmt == 1)
-            k_gemv_bulk<__half><<<g, bl, c->bulk_smem, s>>>((const __half*)c->P, c->Pdiag, c->C, N, c->ldp, c->C2,
-                                                           c->Pbc, c->far_state, c->bulk_m);
-        else
-            k_gemv_bulk<__nv_bfloat16><<<g, bl, c->bulk_smem, s>>>((const __nv_bfloat16*)c->P, c->Pdiag, c->C, N,
-                                                                  c->ldp, c->C2, c->Pbc, c->far_state, c->bulk_m);
-    } else {
-        // C in shared memory when it fits (FDIRW_COARSE_GEMV_L1=1: the L1 form, A/B)
-        static const bool l1 = getenv("FDIRW_COARSE_GEMV_L1") != nullptr;
-        const size_t csm = (size_t)c->ldp * 4;
-        const bool smc = !l1 && csm <= 96 * 1024;
-        auto go = [&](auto wt) -> cudaError_t {
-            using WT = decltype(wt);
-            const WT* P = (const WT*)c->P;
-            float* fine = c->far ? nullptr : cbuf;  // closed: remap fused (with a far field k_remap's
-                                                     // first block also does Eq.7 over all of C')
-            if (smc) {
-                cudaError_t e = cudaFuncSetAttribute(k_gemv<WT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     (int)csm);
-                if (e != cudaSuccess) return e;
-                k_gemv<WT, true><<<gemv_grid(c), gemv_block(c), csm, s>>>(P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc,
-                                                                         c->far_state, c->grp_ptr, c->grp_vox, fine);
-            } else {
-                k_gemv<WT, false><<<gemv_grid(c), gemv_block(c), 0, s>>>(P, c->Pdiag, c->C, N, c->ldp, c->C2, c->Pbc,
-                                                                          c->far_state, c->grp_ptr, c->grp_vox, fine);
-            }
-            return cudaGetLastError();
-        };
-        cudaError_t e = c->fmt == 0 ? go(float{}) : c->fmt == 1 ? go(__half{}) : go(__nv_bfloat16{});
-        if (e != cudaSuccess) return e;
-    }
-    if (c->far || c->bulk_m > 0)  // (the bulk GEMV form keeps the separate remap)
+    const bool fuse = !c->far && c->bulk_m == 0;
+    cudaError_t e = coarse_gemv(c, c->C, c->C2, fuse ? cbuf : nullptr, s);
+    if (e != cudaSuccess) return e;
+    if (!fuse)
         k_remap<<<gridn(c->NL) + (c->far ? 1 : 0), 256, 0, s>>>(c->rows, c->NL, c->group_of, c->C2, cbuf, c->sizes, N,
                                                                c->far ? c->far_state : nullptr, c->v_far);
     return cudaGetLastError();
@@ -922,6 +933,11 @@ extern "C" fdirw_status fdirw_coarse_step(fdirw_coarse* c, const float* cin, flo
     return FDIRW_OK;
 }
 
+// n steps (round 2): between steps the fine field inside Ω_L is the remap of C' — constant over
+// each group — so the next map would only re-average equal values.  The run therefore maps once,
+// steps the group values (C ↔ C2 ping-pong; Eq.7 after each GEMV with a far field), and remaps
+// once at the end: the same operator sequence without the n − 1 intermediate map/remap pairs
+// (whose re-averaging only adds fp32 rounding).  Two steps are one captured graph, replayed.
 extern "C" fdirw_status fdirw_coarse_run(fdirw_coarse* c, float* cbuf, int32_t n, void* cuda_stream)
 {
     if (!c || !cbuf) return cfail(FDIRW_E_INVALID, "NULL argument");
@@ -929,23 +945,60 @@ extern "C" fdirw_status fdirw_coarse_run(fdirw_coarse* c, float* cbuf, int32_t n
     CK(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     if (n == 0) return FDIRW_OK;
-    if (!c->graph || c->graph_c != cbuf) {
-        if (c->graph) cudaGraphExecDestroy(c->graph);
-        c->graph = nullptr;
-        CK(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
-        cudaError_t e = coarse_enqueue(c, cbuf, c->cap);
-        cudaGraph_t g = nullptr;
-        cudaError_t e2 = cudaStreamEndCapture(c->cap, &g);
-        if (e != cudaSuccess || e2 != cudaSuccess) {
-            if (g) cudaGraphDestroy(g);
-            return cfail(FDIRW_E_CUDA, std::string("coarse graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+    const long N = c->N;
+    const bool per_step = getenv("FDIRW_COARSE_PER_STEP_REMAP") != nullptr;  // (A/B: map/remap each step; read per call)
+    if (per_step) {
+        if (!c->graph || c->graph_c != cbuf) {
+            if (c->graph) cudaGraphExecDestroy(c->graph);
+            c->graph = nullptr;
+            CK(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+            cudaError_t e = coarse_enqueue(c, cbuf, c->cap);
+            cudaGraph_t g = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(c->cap, &g);
+            if (e != cudaSuccess || e2 != cudaSuccess) {
+                if (g) cudaGraphDestroy(g);
+                return cfail(FDIRW_E_CUDA, std::string("coarse graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+            }
+            e = cudaGraphInstantiate(&c->graph, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) { c->graph = nullptr; return cfail(FDIRW_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)); }
+            c->graph_c = cbuf;
         }
-        e = cudaGraphInstantiate(&c->graph, g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) { c->graph = nullptr; return cfail(FDIRW_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)); }
-        c->graph_c = cbuf;
+        for (int i = 0; i < n; ++i) CK(cudaGraphLaunch(c->graph, s));
+        return FDIRW_OK;
     }
-    for (int i = 0; i < n; ++i) CK(cudaGraphLaunch(c->graph, s));
+    auto step = [&](const float* Cin, float* Cout, cudaStream_t ss) -> cudaError_t {
+        cudaError_t e = coarse_gemv(c, Cin, Cout, nullptr, ss);
+        if (e != cudaSuccess) return e;
+        if (c->far) k_far<<<1, 256, 0, ss>>>(Cout, c->sizes, N, c->far_state, c->v_far, 0, 0.0);  // Eq.7
+        return cudaGetLastError();
+    };
+    k_map<<<gridn(N * 32), 256, 0, s>>>(cbuf, c->grp_ptr, c->grp_vox, N, c->C);
+    CK(cudaGetLastError());
+    if (n >= 2) {
+        if (!c->graph2) {  // C → C2 → C
+            CK(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+            cudaError_t e = step(c->C, c->C2, c->cap);
+            if (e == cudaSuccess) e = step(c->C2, c->C, c->cap);
+            cudaGraph_t g = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(c->cap, &g);
+            if (e != cudaSuccess || e2 != cudaSuccess) {
+                if (g) cudaGraphDestroy(g);
+                return cfail(FDIRW_E_CUDA, std::string("coarse graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+            }
+            e = cudaGraphInstantiate(&c->graph2, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) { c->graph2 = nullptr; return cfail(FDIRW_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)); }
+        }
+        for (int i = 0; i < n / 2; ++i) CK(cudaGraphLaunch(c->graph2, s));
+    }
+    const float* last = c->C;
+    if (n & 1) {
+        CK(step(c->C, c->C2, s));
+        last = c->C2;
+    }
+    k_remap<<<gridn(c->NL), 256, 0, s>>>(c->rows, c->NL, c->group_of, last, cbuf, c->sizes, N, nullptr, 0.0);
+    CK(cudaGetLastError());
     return FDIRW_OK;
 }
 

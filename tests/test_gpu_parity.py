@@ -723,6 +723,56 @@ def test_coarse_mesh_vs_oracle(fd, oracle_lib, fmt, b, direct):
     assert abs(got[region == 1].astype(np.float64).sum() - m0) / m0 <= 1e-6
 
 
+@pytest.mark.parametrize("far", [False, True])
+def test_coarse_run_group_space(fd, monkeypatch, far):
+    """fdirw_coarse_run maps once, steps the group values and remaps once: against n
+    whole coarse steps (fdirw_coarse_step: map, GEMV, remap each time) it differs only by the
+    re-averaging rounding of the skipped map/remap pairs — relL2 ≤ 1e-6 over Ω_L, mass and c_far
+    alike — and with FDIRW_COARSE_PER_STEP_REMAP=1 (the per-step form) it is bitwise n steps."""
+    import torch
+
+    shape = (22, 21, 23)
+    mask = fi.porous_particle(shape, 6, pore_r=(1.0, 2.0), porosity=0.3, seed=7)
+    region = fi.with_far_field(mask, 6, 3.0) if far else fi.near_field(mask, 6, margin=3)
+    cfg = small_cfg(shape, 1, 200, weights="fp32")
+    v_far = 4.0e4 if far else 0.0
+    c0 = torch.from_numpy(np.where(region == 1, fi.initial_c(mask, "random", seed=9), 0.0).astype(np.float32)).cuda()
+    n = 5
+
+    def run(form):
+        monkeypatch.delenv("FDIRW_COARSE_PER_STEP_REMAP", raising=False)
+        if form == "per_step_run":
+            monkeypatch.setenv("FDIRW_COARSE_PER_STEP_REMAP", "1")
+        ctx = fd.coarse_build(lib_params(cfg, "fp32", v_far=v_far), region, block=3)
+        try:
+            c = c0.clone()
+            if far:
+                fd.coarse_far_init(ctx, c, 0.7)
+            if form == "steps":
+                out = torch.empty_like(c)
+                for _ in range(n):
+                    fd.coarse_step(ctx, c, out)
+                    c, out = out, c
+            else:
+                fd.coarse_run(ctx, c, n)
+            cf = fd.coarse_far_get(ctx) if far else 0.0
+            return c.cpu().numpy().astype(np.float64), cf
+        finally:
+            fd.coarse_destroy(ctx)
+
+    a, cfa = run("group_space")
+    b, cfb = run("steps")
+    p, cfp = run("per_step_run")
+    np.testing.assert_array_equal(p, b)
+    assert cfp == cfb
+    m = region == 1
+    assert rel_l2(a[m], b[m]) <= 1e-6
+    np.testing.assert_array_equal(a[~m], b[~m])
+    assert abs(a[m].sum() - b[m].sum()) <= 1e-6 * b[m].sum()
+    if far:
+        assert abs(cfa - cfb) <= 1e-6 * cfb
+
+
 @pytest.mark.parametrize("fmt", ["fp32", "bf16"])
 def test_coarse_bulk_gemv_bitwise(fd, fmt, monkeypatch):
     """The bulk-copy (cp.async.bulk + mbarrier ring) GEMV and the register GEMV

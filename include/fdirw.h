@@ -399,9 +399,13 @@ fdirw_status fdirw_coarse_build(const fdirw_params* params, const uint8_t* regio
                                 void* cuda_stream, fdirw_coarse** out);
 /* One coarse step c_out = remap(P̃ · map(c_in)) (c_in != c_out).  Asynchronous. */
 fdirw_status fdirw_coarse_step(fdirw_coarse* ctx, const float* c_in_dev, float* c_out_dev, void* cuda_stream);
-/* n_steps coarse steps in place on c_dev (each step map → GEMV → remap of the Ω_L
- * voxels, replayed from a CUDA graph; bitwise equal to n fdirw_coarse_step calls).
- * Asynchronous. */
+/* n_steps coarse steps in place on c_dev: one map of the Ω_L voxels, n steps on the group
+ * values (GEMV, and Eq.7 after each with a far field; two steps per replayed CUDA graph), one
+ * remap.  Between steps the remapped field is constant over each group, so this is the operator
+ * sequence of n fdirw_coarse_step calls without their intermediate map/remap pairs; it differs
+ * from them only by that re-averaging's fp32 rounding (relL2 ≤ 1e-6, tested).  With the
+ * environment variable FDIRW_COARSE_PER_STEP_REMAP set, each step maps and remaps (bitwise n
+ * fdirw_coarse_step calls).  Asynchronous. */
 fdirw_status fdirw_coarse_run(fdirw_coarse* ctx, float* c_dev, int32_t n_steps, void* cuda_stream);
 fdirw_status fdirw_coarse_query(const fdirw_coarse* ctx, fdirw_coarse_info* info);
 /* Host copies: P_host [N][N] fp64 decoded (diagonal = fp32 fix-up) if non-NULL;

@@ -269,3 +269,38 @@ def test_absorb_cfg3o_sampled_vs_oracle(fd, oracle_lib):
         # and the absorption moved mass at the interface (the comparison is not the identity)
         moved = rel_l2(c0[box[4]:box[5], box[2]:box[3], box[0]:box[1]], ref)
         assert moved > 10 * rel_l2(sub, ref), (box, moved, rel_l2(sub, ref))
+
+
+@pytest.mark.parametrize("weights", ["fp32", "bf16"])
+def test_absorb_without_solid_is_the_liquid_step(fd, weights):
+    """Degenerate loop: an open domain with no solid voxel.  The interface and non-far lists hold no
+    solid work, the reaction has no face pair, Q_S = c̄_S = 0 — and one macro step's field is bit for
+    bit the plain far-field FDiRW step (fdirw_run) of the same context (c_far enters only the next
+    step); Eq.7's balance closes."""
+    import torch
+
+    shape = (21, 19, 23)
+    m = fi.with_far_field(np.ones(shape, np.uint8), 7, 2.0)
+    assert not (m == 0).any() and (m == 2).any()
+    T = fi.TABLE1
+    c0 = np.where(m == 1, T["c_L0"] * (1.0 + 0.3 * np.sin(np.arange(m.size).reshape(shape))), 0.0).astype(np.float32)
+    nz, ny, nx = shape
+    p = fd.Params(nx=nx, ny=ny, nz=nz, dh=T["dh"], D_fast=fi.D_FAST_SI, D_slow=0.0, dt=T["dt"], radius=3,
+                  weights=weights, v_far=2e4)
+    out = []
+    for kind in ("absorb", "run"):
+        ctx = fd.build_kernels(p, m)
+        try:
+            c = torch.from_numpy(c0).cuda()
+            M0 = fd.far_init(ctx, c, 0.5 * T["c_L0"])
+            if kind == "absorb":
+                kin = fd.absorb_run(ctx, c, 1, fi.D_SLOW_SI, 0.05, 1.0, 1e-5)
+                assert kin[0, 0] == 0.0 and kin[0, 3] == 0.0
+                got = c.cpu().numpy().astype(np.float64)
+                assert abs(got[m != 2].sum() + kin[0, 2] * 2e4 - M0) / M0 <= 1e-9
+            else:
+                fd.run(ctx, c, 1)
+            out.append(c.cpu().numpy())
+        finally:
+            fd.destroy(ctx)
+    np.testing.assert_array_equal(out[0], out[1])

@@ -105,6 +105,12 @@ typedef enum { FDIRW_W_FP32 = 0, FDIRW_W_FP16 = 1, FDIRW_W_BF16 = 2, FDIRW_W_MX8
                                   kernel) instead of two columns per thread over balanced z
                                   segments (kgen_bal.cu).  The same substep arithmetic; the fp64
                                   epilogue sums group cells differently.  For A/B   */
+#define FDIRW_F_PBC_RESERVOIR 256u /* N2, one GPU (world == 1, else FDIRW_E_INVALID): p_BC by the
+                                  reservoir's own held-Dirichlet FD (n_fd whole-grid substeps from a
+                                  zero field, far field held at 1; the fine analogue of the paper's
+                                  P_BC column) instead of reading A26's 1 − row sum, which goes
+                                  negative where truncated windows make a row sum exceed 1
+                                  (A26).  Ignored without a far field              */
 
 /* The paper's problem statement (Table 1) + north_star's window radius / precision. */
 typedef struct {

@@ -32,6 +32,18 @@ def p_bc_full(pb: Problem, W: np.ndarray) -> np.ndarray:
     return (1.0 - step_scatter(pb, W, box, nonfar(pb), box)) * nonfar(pb)
 
 
+def p_bc_reservoir(pb: Problem) -> np.ndarray:
+    """p_BC by the reservoir's own held-Dirichlet FD (the alternative reading of A26):
+    the response, after n_fd whole-grid substeps from a zero field, to the far field held at 1 —
+    the fine-grid analogue of the paper's P_BC column (Eq.10 with the boundary source).
+    Equal to p_bc_full where the windows are exact; ≥ 0 and 0 beyond the reservoir's reach
+    everywhere."""
+    from . import derive, fd_whole_grid
+
+    zero = np.zeros(pb.shape, np.float64)
+    return fd_whole_grid(pb, zero, derive(pb).n_fd, c_far=1.0) * nonfar(pb)
+
+
 def step_full(pb: Problem, W: np.ndarray, C: np.ndarray, c_far: float, pbc: np.ndarray) -> np.ndarray:
     """Eq.8 on the whole grid (far-field voxels carry 0: their value is the scalar c_far)."""
     nz, ny, nx = pb.shape

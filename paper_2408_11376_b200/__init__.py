@@ -37,6 +37,7 @@ F_SYMMETRIC_RULE = 16  # exact regime only: gather weights = own kernel reflecte
 F_KGEN_DIRECT = 32  # kgen runs the n_fd substeps literally instead of the Chebyshev recurrence (reading A30)
 F_NO_BULK_STREAM = 64  # superposition: per-thread weight loads instead of TMA-staged rows (same bits)
 F_KGEN_COLUMNS = 128  # R = 5 kgen: one window column per thread (round-1 kernel) instead of pairs (A/B)
+F_PBC_RESERVOIR = 256  # N2: p_BC by the reservoir's held-Dirichlet FD instead of 1 − row sum (A26 alternative)
 
 EXPORTS = ["fdirw_make_plan", "fdirw_nccl_unique_id", "fdirw_build_kernels", "fdirw_step", "fdirw_run", "fdirw_mass",
            "fdirw_query", "fdirw_destroy", "fdirw_last_error", "fdirw_debug_upload_weights",

@@ -314,8 +314,11 @@ static fdirw_status validate(const fdirw_params* p, const uint8_t* phase, const 
                                          "KGEN_FP64");
     }
     if (p->flags & ~(FDIRW_F_NO_MASS_FIX | FDIRW_F_NO_DEDUP | FDIRW_F_DEDUP_STORAGE | FDIRW_F_KGEN_FP64 |
-                     FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT | FDIRW_F_NO_BULK_STREAM | FDIRW_F_KGEN_COLUMNS))
+                     FDIRW_F_SYMMETRIC_RULE | FDIRW_F_KGEN_DIRECT | FDIRW_F_NO_BULK_STREAM | FDIRW_F_KGEN_COLUMNS |
+                     FDIRW_F_PBC_RESERVOIR))
         return fail(FDIRW_E_INVALID, "unknown flags");
+    if ((p->flags & FDIRW_F_PBC_RESERVOIR) && p->v_far > 0 && dist && dist->world > 1)
+        return fail(FDIRW_E_INVALID, "FDIRW_F_PBC_RESERVOIR needs world == 1 (the reservoir FD spans the whole grid)");
     if ((p->flags & FDIRW_F_SYMMETRIC_RULE) && (p->flags & FDIRW_F_DEDUP_STORAGE))
         return fail(FDIRW_E_INVALID, "FDIRW_F_SYMMETRIC_RULE is not combined with FDIRW_F_DEDUP_STORAGE");
     if ((p->flags & FDIRW_F_NO_DEDUP) && (p->flags & FDIRW_F_DEDUP_STORAGE))
@@ -910,12 +913,24 @@ static fdirw_status build_pbc(fdirw_ctx* c, const uint8_t* mask_d, cudaStream_t 
     const size_t n = (size_t)g.nx * g.ny * g.nzl;
     fdirw_status st = alloc((void**)&rowsum, n * 4, "p_BC scratch");
     if (st != FDIRW_OK) return st;
-    cudaError_t e = launch_ones(mask_d, g.mz0, g, c->cpad[1], s);
-    if (e == cudaSuccess)
-        e = superpose(c, c->cpad[1], rowsum, (long)g.nx * g.ny, g.nx, 0, c->compact ? c->ut.nd_tiles : g.n_tiles, s, false);
+    cudaError_t e = cudaSuccess;
+    const bool reservoir = (c->p.flags & FDIRW_F_PBC_RESERVOIR) && c->world == 1;
+    if (reservoir) {  // the reservoir's held-Dirichlet FD response (A26 alternative), into rowsum
+        float* tmp = nullptr;
+        if ((st = alloc((void**)&tmp, n * 4, "p_BC reservoir FD")) != FDIRW_OK) { cudaFree(rowsum); return st; }
+        e = launch_reservoir_fd(mask_d, g, (float)c->d.lam_ff, (float)c->d.lam_fs, (float)c->d.lam_ss, c->d.n_fd,
+                                rowsum, tmp, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(tmp);
+    } else {
+        e = launch_ones(mask_d, g.mz0, g, c->cpad[1], s);
+        if (e == cudaSuccess)
+            e = superpose(c, c->cpad[1], rowsum, (long)g.nx * g.ny, g.nx, 0, c->compact ? c->ut.nd_tiles : g.n_tiles, s,
+                          false);
+    }
     if (e == cudaSuccess)
         e = launch_pbc(rowsum, c->farmask, g, c->pbc, s, c->compact ? c->ut.dense_list : nullptr, c->ut.n_dense,
-                       c->ut.nd_tiles);
+                       c->ut.nd_tiles, reservoir);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->cpad[1], 0, g.state_elems * 4, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(rowsum);

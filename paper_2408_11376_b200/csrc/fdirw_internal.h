@@ -269,7 +269,11 @@ cudaError_t launch_tile_mass(const float* c, const uint8_t* farmask, const Geome
 cudaError_t launch_ones(const uint8_t* mask, int mz0, const Geometry& g, float* cpad, cudaStream_t s);
 // pbc[tile layout] = 1 − rowsum for real non-far targets, else 0
 cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s,
-                       const int* list = nullptr, long n_list = 0, int n_list_tiles = 0);
+                       const int* list = nullptr, long n_list = 0, int n_list_tiles = 0, bool direct = false);
+// FDIRW_F_PBC_RESERVOIR (world 1): n_fd whole-grid explicit FD substeps from 0 with the far field
+// (mask 2) held at 1; faces as kgen's (harmonic λ, far cells fast); result → out (dense grid)
+cudaError_t launch_reservoir_fd(const uint8_t* mask, const Geometry& g, float lff, float lfs, float lss, int n_fd,
+                                float* out, float* tmp, cudaStream_t s);
 // gathered = world blocks of (1 + stride−1) doubles: [count, tile sums...]; sum in global tile
 // order (deterministic for any decomposition).  mode 0: c_far = (M0 − Σ)/v_far;
 // mode 1 (init): M0 = Σ + c_far0·v_far, c_far = c_far0

@@ -1357,7 +1357,7 @@ cudaError_t launch_ones(const uint8_t* mask, int mz0, const Geometry& g, float* 
 
 __global__ void pbc_kernel(const float* __restrict__ rowsum, const uint8_t* __restrict__ farmask, int nx, int ny,
                            int nxq, int tile, int tpp, long n_elems, float* __restrict__ pbc,
-                           const int* __restrict__ list, long n_list)
+                           const int* __restrict__ list, long n_list, int direct)
 {
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n_elems; i += (long)gridDim.x * blockDim.x) {
         const int j = (int)(i & 7);
@@ -1376,7 +1376,8 @@ __global__ void pbc_kernel(const float* __restrict__ rowsum, const uint8_t* __re
             const int y = q / nxq, x = (q % nxq) * 8 + j;
             if (x < nx) {
                 const long k = ((long)zl * ny + y) * nx + x;
-                v = farmask[k] ? 0.f : 1.f - rowsum[k];  // reading A26: p_BC = 1 − Σ_s W̃_s(x−s)
+                // reading A26: p_BC = 1 − Σ_s W̃_s(x−s); direct: the reservoir FD's response itself
+                v = farmask[k] ? 0.f : direct ? rowsum[k] : 1.f - rowsum[k];
             }
         }
         pbc[i] = v;
@@ -1384,12 +1385,61 @@ __global__ void pbc_kernel(const float* __restrict__ rowsum, const uint8_t* __re
 }
 
 cudaError_t launch_pbc(const float* rowsum, const uint8_t* farmask, const Geometry& g, float* pbc, cudaStream_t s,
-                       const int* list, long n_list, int n_list_tiles)
+                       const int* list, long n_list, int n_list_tiles, bool direct)
 {
     const long n = list ? (long)n_list_tiles * g.tile * kChunk : (long)g.diag_elems;
     if (n <= 0) return cudaSuccess;
     pbc_kernel<<<grid_for(n, 256), 256, 0, s>>>(rowsum, farmask, g.nx, g.ny, g.nxq, g.tile, g.tpp, n, pbc, list,
-                                                n_list);
+                                                n_list, direct ? 1 : 0);
+    return cudaGetLastError();
+}
+
+// One explicit FD substep over the whole grid (dense layout): far-field voxels (mask 2) held at 1,
+// faces between non-far voxels and far ones as between fast cells (kgen's rule, face_lambda);
+// faces summed in the order −x, +x, −y, +y, −z, +z
+__global__ void reservoir_fd_kernel(const uint8_t* __restrict__ mask, const float* __restrict__ cin,
+                                    float* __restrict__ cout, int nx, int ny, int nz, float lff, float lfs, float lss)
+{
+    const long n = (long)nx * ny * nz;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((long)nx * ny));
+        const unsigned p = mask[i];
+        if (p == 2u) { cout[i] = 1.f; continue; }
+        const float c = cin[i];
+        float acc = c;
+        const long d[3] = {1, nx, (long)nx * ny};
+        const bool inb[6] = {x > 0, x < nx - 1, y > 0, y < ny - 1, z > 0, z < nz - 1};
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            if (!inb[f]) continue;
+            const long j = i + (f & 1 ? d[f >> 1] : -d[f >> 1]);
+            const unsigned q = mask[j];
+            const bool fp = p == 1u, fq = q != 0u;  // far counts as fast
+            const float lam = fp && fq ? lff : (fp || fq ? lfs : lss);
+            acc = fmaf(lam, cin[j] - c, acc);
+        }
+        cout[i] = acc;
+    }
+}
+
+__global__ void reservoir_init_kernel(const uint8_t* __restrict__ mask, float* __restrict__ c, long n)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        c[i] = mask[i] == 2 ? 1.f : 0.f;
+}
+
+cudaError_t launch_reservoir_fd(const uint8_t* mask, const Geometry& g, float lff, float lfs, float lss, int n_fd,
+                                float* out, float* tmp, cudaStream_t s)
+{
+    const long n = (long)g.nx * g.ny * g.nz;
+    if (g.mz0 != 0 || g.mz1 != g.nz) return cudaErrorInvalidValue;  // needs every mask plane (world 1)
+    float* a = (n_fd & 1) ? tmp : out;  // so the last substep lands in out
+    float* b = (n_fd & 1) ? out : tmp;
+    reservoir_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(mask, a, n);
+    for (int k = 0; k < n_fd; ++k) {
+        reservoir_fd_kernel<<<grid_for(n, 256), 256, 0, s>>>(mask, a, b, g.nx, g.ny, g.nz, lff, lfs, lss);
+        float* t = a; a = b; b = t;
+    }
     return cudaGetLastError();
 }
 

@@ -306,7 +306,8 @@ def test_absorb_without_solid_is_the_liquid_step(fd, weights):
     np.testing.assert_array_equal(out[0], out[1])
 
 
-def test_absorb_cfg3o_long_run_invariants(fd):
+@pytest.mark.parametrize("flags", [0, "pbc_reservoir"])
+def test_absorb_cfg3o_long_run_invariants(fd, flags):
     """1000 macro steps (t = 0.5 s, Fig.6's horizon) of the default loop on cfg3o (bf16): no NaN;
     Q_S never decreases (absorption only) and c̄_S stays in [0, 1]; every solid voxel stays
     ≤ c_S^eq (f_S ≥ 0 clamps at saturation); and Eq.7's balance Σ c + c_far·V_far = M0 holds to
@@ -314,7 +315,8 @@ def test_absorb_cfg3o_long_run_invariants(fd):
     truncated windows give pore targets row sums up to ~1.6 — the fp64 oracle's own p_BC is −0.6 at
     a pore voxel 20 voxels from the far field — so p_BC·c_far drives depleted pores negative
     (measured min −6.3e-3 after 1000 steps, the same with fp32 / fp16 / bf16 weights and every tail
-    form: `tools/absorb_negcheck.py`, reading A26)."""
+    form: `tools/absorb_negcheck.py`, reading A26).  With FDIRW_F_PBC_RESERVOIR (p_BC by
+    the reservoir's held-Dirichlet FD, ≥ 0) every concentration stays ≥ 0, and that is asserted."""
     import torch
 
     cfg = fi.config("cfg3o")
@@ -323,7 +325,8 @@ def test_absorb_cfg3o_long_run_invariants(fd):
     T = fi.TABLE1
     c0 = np.where(mask == 1, T["c_L0"], np.where(mask == 0, T["c_S0"], 0.0)).astype(np.float32)
     p = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=0.0, dt=cfg.dt, radius=cfg.R,
-                  n_fd=cfg.n_fd, weights="bf16", v_far=cfg.v_far)
+                  n_fd=cfg.n_fd, weights="bf16", v_far=cfg.v_far,
+                  flags=fd.F_PBC_RESERVOIR if flags == "pbc_reservoir" else 0)
     ctx = fd.build_kernels(p, mask)
     try:
         c = torch.from_numpy(c0).cuda()
@@ -338,3 +341,5 @@ def test_absorb_cfg3o_long_run_invariants(fd):
     assert got[mask == 0].max() <= 1.0 + 1e-6
     assert abs(got[mask != 2].sum() + kin[-1, 2] * cfg.v_far - M0) / M0 <= 1e-9
     assert kin[-1, 3] > kin[0, 3]  # it absorbed
+    if flags == "pbc_reservoir":  # p_BC ≥ 0 everywhere: every concentration stays ≥ 0
+        assert got[mask != 2].min() >= 0.0

@@ -249,3 +249,28 @@ def test_open_windows_recurrence_reduced_precision(fd, oracle_lib, monkeypatch, 
     nf = mask != 2
     assert rel_l2(got[nf], refC[nf]) <= 5e-3
     assert (got.sum() + cf * 2000.0 - M0) / M0 == pytest.approx(0.0, abs=1e-9)
+
+
+def test_pbc_reservoir_vs_oracle(fd, oracle_lib):
+    """FDIRW_F_PBC_RESERVOIR: p_BC by the reservoir's held-Dirichlet FD (A26's alternative,
+    oracle.farfield.p_bc_reservoir), truncated regime (n_fd = 300 > R = 3), fp32: one step vs the
+    oracle's Eq.8 with that p_BC, and Eq.7's balance."""
+    import torch
+    from oracle import farfield as ff
+
+    shape = (14, 13, 15)
+    mask = _open_mask(shape, 4)
+    cfg = small_cfg(shape, 3, 300, D_slow=1e-3, weights="fp32")
+    pb = oracle_problem(cfg, mask)
+    c0 = fi.initial_c(mask, "random", seed=4).astype(np.float64) * (mask != 2)
+    Wq = oracle_lib.quantize(pb, oracle_lib.build_kernels(pb), "fp32")
+    pbc = ff.p_bc_reservoir(pb)
+    assert pbc.min() >= 0.0
+    ref = ff.step_full(pb, Wq, c0, 0.5, pbc)
+    got, cf, M0, _ = _gpu_far(fd, cfg, mask, c0, 0.5, 1, v_far=2000.0, flags=fd.F_PBC_RESERVOIR)
+    nf = mask != 2
+    assert rel_l2(got[nf], ref[nf]) <= 1e-5
+    assert (got.sum() + cf * 2000.0 - M0) / M0 == pytest.approx(0.0, abs=1e-9)
+    # and it differs from the row-sum reading here (the truncated regime)
+    ref26 = ff.step_full(pb, Wq, c0, 0.5, ff.p_bc_full(pb, Wq))
+    assert rel_l2(ref[nf], ref26[nf]) > 1e-4

@@ -44,6 +44,34 @@ def test_exact_regime_equals_dirichlet_fd(ff, oracle_lib, n_fd, R):
     np.testing.assert_allclose(got, ref, rtol=0, atol=1e-14)
 
 
+@pytest.mark.parametrize("n_fd,R", [(2, 2), (3, 4)])
+def test_p_bc_reservoir_equals_row_sum_reading_where_exact(ff, oracle_lib, n_fd, R):
+    """The alternative p_BC reading (the reservoir's held-Dirichlet FD response) equals A26's
+    1 − row sum where the windows are exact (n_fd ≤ R); it is in [0, 1] and 0 on voxels farther
+    than n_fd faces from the reservoir."""
+    m = _open_mask((10, 11, 9), 3)
+    pb = lat(m, R, n_fd)
+    W = oracle_lib.build_kernels(pb)
+    a, b = ff.p_bc_reservoir(pb), ff.p_bc_full(pb, W)
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-14)
+    assert a.min() >= 0.0 and a.max() <= 1.0
+    far = np.argwhere(m == 2)
+    for idx in np.argwhere((m != 2)):
+        if np.abs(far - idx).sum(1).min() > n_fd:
+            assert a[tuple(idx)] == 0.0
+
+
+def test_p_bc_reservoir_nonnegative_truncated(ff, oracle_lib):
+    """In the truncated regime the two readings part: A26's 1 − row sum goes negative at targets
+    whose row sum exceeds 1, the reservoir reading stays in [0, 1]."""
+    m = _open_mask((12, 13, 11), 5)
+    pb = lat(m, 2, 40)
+    W = oracle_lib.build_kernels(pb)
+    a, b = ff.p_bc_reservoir(pb), ff.p_bc_full(pb, W)
+    assert a.min() >= 0.0 and a.max() <= 1.0
+    assert np.abs(a - b).max() > 1e-3
+
+
 def test_window_covering_domain_equals_dirichlet_fd(ff, oracle_lib):
     m = _open_mask((5, 4, 6), 4)
     pb = lat(m, 5, 70)

@@ -7,11 +7,12 @@ sys.path.insert(0, os.getcwd())
 import fdirw_inputs as fi, paper_2408_11376_b200 as fd
 cfg = fi.config("cfg3o"); mask = cfg.mask(); nz, ny, nx = cfg.shape; T = fi.TABLE1
 c0 = np.where(mask == 1, T["c_L0"], np.where(mask == 0, T["c_S0"], 0.0)).astype(np.float32)
-for form, w in (("default","bf16"), ("scalar","bf16"), ("default","fp32"), ("default", "fp16")):
+for form, w in (("default","bf16"), ("scalar","bf16"), ("default","fp32"), ("default", "fp16"), ("pbc_reservoir", "bf16")):
     for ev in ("FDIRW_ABSORB_SCALAR",): os.environ.pop(ev, None)
     if form == "scalar": os.environ["FDIRW_ABSORB_SCALAR"] = "1"
     p = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=0.0, dt=cfg.dt, radius=cfg.R,
-                  n_fd=cfg.n_fd, weights=w, v_far=cfg.v_far)
+                  n_fd=cfg.n_fd, weights=w, v_far=cfg.v_far,
+                  flags=fd.F_PBC_RESERVOIR if form == "pbc_reservoir" else 0)
     ctx = fd.build_kernels(p, mask)
     c = torch.from_numpy(c0).cuda(); fd.far_init(ctx, c, cfg.c_far0)
     first = None

@@ -539,7 +539,8 @@ def run_absorb(args):
     nz, ny, nx = cfg.shape
     T = fi.TABLE1
     params = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=0.0, dt=cfg.dt, radius=cfg.R,
-                       n_fd=cfg.n_fd, weights=cfg.weights, v_far=cfg.v_far)
+                       n_fd=cfg.n_fd, weights=cfg.weights, v_far=cfg.v_far,
+                       flags=fd.F_PBC_RESERVOIR if args.pbc == "reservoir" else 0)
     kin_p = dict(D_S=fi.D_SLOW_SI, k=0.05, c_S_eq=1.0, c_L_eq=1e-5)  # Table 1
     torch.cuda.synchronize()
     t = time.perf_counter()
@@ -575,6 +576,11 @@ def run_absorb(args):
             "kinetics_last": {"Q_S": kin[-1, 0], "Q_L": kin[-1, 1], "c_far": kin[-1, 2], "c_bar_S": kin[-1, 3],
                               "t_s": (args.warmup + args.steps) * cfg.dt},
             "mass_rel_err": abs(tot - M0) / M0,
+            "p_bc": args.pbc,
+            "liquid_min": float(c[torch.from_numpy(mask == 1).cuda()].min()),
+            "liquid_min_note": "the near-field liquid's minimum after the warm-up + timed steps; with p_bc = rowsum "
+                               "(reading A26) truncated-window row sums > 1 make p_BC < 0 at pores and drained pores "
+                               "go negative; p_bc = reservoir keeps every value >= 0 (DESIGN §3 A26)",
             "roofline": {"bound": "hbm", "achieved": sup_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": sup_bytes / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                          "note": "the loop's dominant kernel is the liquid superposition: its algorithmic bytes "
@@ -612,6 +618,8 @@ def main():
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 halo: p2p = edge planes stored into the neighbours' memory by the superposition "
                          "(default); nccl = grouped ncclSend/Recv overlapped with the interior tiles")
+    ap.add_argument("--pbc", default="rowsum", choices=["rowsum", "reservoir"],
+                    help="--mode absorb: p_BC reading (A26's 1 - row sum, or the reservoir's held-Dirichlet FD)")
     ap.add_argument("--storage", default="dense", choices=["dense", "dedup"],
                     help="dense: north_star gather layout (default); dedup: NEXT row N4 uniform-chunk kernels")
     args = ap.parse_args()

@@ -618,8 +618,9 @@ def main():
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 halo: p2p = edge planes stored into the neighbours' memory by the superposition "
                          "(default); nccl = grouped ncclSend/Recv overlapped with the interior tiles")
-    ap.add_argument("--pbc", default="rowsum", choices=["rowsum", "reservoir"],
-                    help="--mode absorb: p_BC reading (A26's 1 - row sum, or the reservoir's held-Dirichlet FD)")
+    ap.add_argument("--pbc", default="reservoir", choices=["rowsum", "reservoir"],
+                    help="--mode absorb: p_BC reading — the reservoir's held-Dirichlet FD (default here: every "
+                         "concentration stays >= 0) or the library default, A26's 1 - row sum (DESIGN §3 A26)")
     ap.add_argument("--storage", default="dense", choices=["dense", "dedup"],
                     help="dense: north_star gather layout (default); dedup: NEXT row N4 uniform-chunk kernels")
     args = ap.parse_args()

@@ -5,7 +5,7 @@ product path with fp32 weights (compensated fp32 accumulation, fp32-pair diagona
 reference — the fp64 oracle does not run 1000 steps of a 120³ grid; the product path is within
 ~1e-7 of it on the desk model (tests/test_gpu_absorb.py).  Reports the relative error of c̄_S(t)
 (Fig.10c) and of the final liquid field, per mode.  Usage:
-  python tools/precision_study.py [steps] > profiles/<round>_precision_study_cfg3o.json"""
+  python tools/precision_study.py [steps] [reservoir] > profiles/<round>_precision_study_cfg3o[_pbc_reservoir].json"""
 import json
 import os
 import sys
@@ -18,6 +18,7 @@ import fdirw_inputs as fi  # noqa: E402
 import paper_2408_11376_b200 as fd  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+PBC = fd.F_PBC_RESERVOIR if (len(sys.argv) > 2 and sys.argv[2] == "reservoir") else 0  # p_BC reading (A26)
 cfg = fi.config("cfg3o")
 mask = cfg.mask()
 nz, ny, nx = cfg.shape
@@ -28,7 +29,7 @@ c0 = np.where(mask == 1, T["c_L0"], np.where(mask == 0, T["c_S0"], 0.0)).astype(
 
 def run(weights, mode, flags):
     p = fd.Params(nx=nx, ny=ny, nz=nz, dh=cfg.dh, D_fast=cfg.D_fast, D_slow=0.0, dt=cfg.dt, radius=cfg.R,
-                  n_fd=cfg.n_fd, weights=weights, v_far=cfg.v_far, flags=flags)
+                  n_fd=cfg.n_fd, weights=weights, v_far=cfg.v_far, flags=flags | PBC)
     ctx = fd.build_kernels(p, mask)
     try:
         c = torch.from_numpy(c0).cuda()
@@ -44,6 +45,7 @@ ref_kin, ref_c = run("fp32", "default", 0)
 liq = mask == 1
 out = {"workload": "cfg3o open R50 model, integrated absorption loop, %d macro steps (t = %.3f s)" % (steps, steps * cfg.dt),
        "reference": "product path, fp32 weights (compensated fp32 accumulation)",
+       "p_bc": "reservoir FD (FDIRW_F_PBC_RESERVOIR)" if PBC else "1 - row sum (A26)",
        "paper": "P:199-201: relative errors ~1e-6 (FP32), ~1e-5 (mixed FP32/FP16), ~1e-2 (FP16); errors do not grow",
        "c_bar_S_final_ref": float(ref_kin[-1, 3]), "modes": {}}
 # the paper's three modes as it states them (P stored plainly in the mode's format: no diagonal
